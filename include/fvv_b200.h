@@ -1,0 +1,133 @@
+/*
+ * fvv_b200.h -- C ABI of the B200-native dense view-synthesis path.
+ *
+ * This is the drop-in boundary for the reference's interpolation / tiling
+ * path (reference = arxiv/paper_2112_10603, package `fvv`, pure Python).
+ * The reference has no FFI of its own; each entry point below replaces one
+ * Python function of its public API, with the same argument meaning and the
+ * same error classes (mapped back to ValueError / LayoutError by the host
+ * shim paper_2112_10603_b200/_lib.py):
+ *
+ *   fvv_validate_params        <- InterpConfig.__post_init__   interp.py:24-36
+ *   fvv_interpolate_pairs      <- interpolate(left, right, cfg) interp.py:97-148 (batched)
+ *   fvv_dense_views            <- dense_views(left, right, n)   interp.py:151-170
+ *   fvv_rig_views              <- PipelineHandle._interp        server/pipeline.py:254-271
+ *   fvv_downscale              <- downscale(frame, factor)      cluster.py:77-89 (batched)
+ *   fvv_assemble_cluster       <- assemble_cluster_frame        cluster.py:143-191
+ *   fvv_rig_clusters           <- PipelineHandle._stitch        server/pipeline.py:273-292
+ *
+ * Conventions
+ *  - Frames are packed planes in the reference's Frame.raw_planes() order
+ *    (frame.py:99-101): GRAY8 = Y (H,W); YUV420 = Y (H,W), U, V (H/2,W/2);
+ *    RGB8 = interleaved (H,W,3).  Byte size: fvv_frame_bytes().
+ *  - All frame pointers are DEVICE pointers (the caller -- torch -- owns
+ *    every buffer); pointer arrays (`const uint8_t* const*`) are HOST arrays
+ *    of device pointers.  Work is enqueued on the caller's stream; no call
+ *    synchronises the device or allocates memory after fvv_engine_create.
+ *  - Return value: FVV_OK (0) or a negative error class; the message is in
+ *    fvv_last_error() (thread-local).  Entry points are reentrant per engine
+ *    and keep no global mutable state besides that message.
+ */
+#ifndef FVV_B200_H
+#define FVV_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FVV_OK 0
+#define FVV_EINVAL (-1)       /* ValueError in the reference               */
+#define FVV_ELAYOUT (-2)      /* cluster.LayoutError in the reference      */
+#define FVV_ECUDA (-3)        /* CUDA launch / runtime failure             */
+#define FVV_EUNSUPPORTED (-4) /* valid for the reference, outside this path */
+
+enum { FVV_GRAY8 = 0, FVV_YUV420 = 1, FVV_RGB8 = 2 }; /* frame.py:11-14 */
+
+typedef struct {
+    int32_t width;
+    int32_t height;
+    int32_t format; /* FVV_GRAY8 / FVV_YUV420 / FVV_RGB8 */
+} fvv_frame_desc;
+
+/* InterpConfig (interp.py:24-36); `refine` is a host-side hook, not here. */
+typedef struct {
+    int32_t block_size[3];    /* coarse -> fine, default (8, 8, 8)   */
+    int32_t search_radius[3]; /* coarse -> fine, default (12, 4, 2)  */
+    double mask_epsilon;      /* default 1e-3                        */
+} fvv_interp_params;
+
+typedef struct fvv_engine fvv_engine;
+
+const char* fvv_last_error(void);
+const char* fvv_build_info(void);
+
+/* frame.py:22-30 plane_shapes -> total bytes of a packed frame */
+size_t fvv_frame_bytes(const fvv_frame_desc* desc);
+
+/* interp.py:32-36 validation (ValueError) plus this path's limits
+ * (FVV_EUNSUPPORTED): block sizes in {2,4,8}, max_span <= 120. */
+int fvv_validate_params(const fvv_interp_params* params);
+
+/* Engine = geometry + config + a caller-owned device workspace able to run
+ * up to `max_pairs` interpolations per recursion stage. */
+size_t fvv_engine_workspace_size(const fvv_frame_desc* desc, const fvv_interp_params* params,
+                                 int max_pairs);
+int fvv_engine_create(const fvv_frame_desc* desc, const fvv_interp_params* params, int max_pairs,
+                      void* workspace, size_t workspace_bytes, fvv_engine** out);
+void fvv_engine_destroy(fvv_engine* engine);
+int fvv_engine_max_pairs(const fvv_engine* engine);
+
+/* interp.py:97-148, batched: out[i] = interpolate(left[i], right[i]).
+ * npairs <= max_pairs.  Outputs may not alias inputs. */
+int fvv_interpolate_pairs(fvv_engine* engine, const uint8_t* const* left,
+                          const uint8_t* const* right, uint8_t* const* out, int npairs,
+                          void* stream);
+
+/* Optional diagnostics of the most recent fvv_interpolate_pairs call, pair i:
+ * final full-resolution flows (H,W,2) f32 and the blend mask (H,W) f64, as
+ * InterpDiagnostics.scales[-1].flow_lr / flow_rl and .mask (interp.py:49-64).
+ * Device pointers; pass NULL to skip.  Must be enqueued on the same stream. */
+int fvv_interp_diagnostics(fvv_engine* engine, int pair, float* flow_lr, float* flow_rl,
+                           double* mask, void* stream);
+
+/* interp.py:151-170: views = (2^stages - 1) frames, contiguous, left -> right.
+ * Requires max_pairs >= 2^(stages-1). */
+int fvv_dense_views(fvv_engine* engine, const uint8_t* left, const uint8_t* right, int stages,
+                    uint8_t* views, void* stream);
+
+/* server/pipeline.py:254-271: one rig frame.  cams = ncams contiguous frames;
+ * views = (ncams-1)*2^stages + 1 contiguous frames in global view order
+ * (viewmodel.py:23-71: camera c at c*2^stages).  Requires
+ * max_pairs >= (ncams-1)*2^(stages-1). */
+int fvv_rig_views(fvv_engine* engine, const uint8_t* cams, int ncams, int stages, uint8_t* views,
+                  void* stream);
+
+/* cluster.py:77-89, batched over nframes contiguous frames. */
+int fvv_downscale(const fvv_frame_desc* desc, const uint8_t* frames, int nframes, int factor,
+                  uint8_t* out, void* stream);
+
+/* cluster.py:135-140 cluster_geometry: stitched width for nsmall quarter tiles */
+int fvv_cluster_width(int base_width, int nsmall);
+
+/* cluster.py:143-191: anchor (W,H) + nsmall quarter frames (W/4,H/4) ->
+ * stitched frame (fvv_cluster_width(W, nsmall), H); GRAY8 / YUV420 only. */
+int fvv_assemble_cluster(const fvv_frame_desc* anchor_desc, const uint8_t* anchor,
+                         const uint8_t* const* smalls, int nsmall, uint8_t* stitched,
+                         void* stream);
+
+/* server/pipeline.py:273-292 + cluster.py:58-74: every cluster frame of one
+ * rig frame straight from the global views buffer (downscale fused into the
+ * paste).  clusters: ncams stitched frames packed back to back in camera
+ * order; cluster c has fvv_rig_cluster_bytes(..., c) bytes. */
+size_t fvv_rig_cluster_bytes(const fvv_frame_desc* desc, int ncams, int stages,
+                             int views_per_side, int cluster);
+int fvv_rig_clusters(const fvv_frame_desc* desc, int ncams, int stages, int views_per_side,
+                     const uint8_t* views, uint8_t* clusters, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FVV_B200_H */

@@ -1,0 +1,458 @@
+// api.cu -- the C ABI (include/fvv_b200.h): validation with the reference's
+// error classes, workspace planning, recursion-stage scheduling.  No host
+// synchronisation and no allocation after fvv_engine_create.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "fvv_device.cuh"
+
+namespace fvv {
+cudaError_t run_interp_stage(const Geometry& g, const PairTable& pt, uint8_t* ws, const Planes& P,
+                             const int16_t* const* rank_of, const int16_t* const* cand_of_rank,
+                             int npairs, double* mask_out, cudaStream_t st);
+cudaError_t run_diag(const Geometry& g, const PairTable& pt, uint8_t* ws, const Planes& P, int pair,
+                     float* flow_lr, float* flow_rl, double* mask, cudaStream_t st);
+cudaError_t launch_downscale(int W, int H, int fmt, const uint8_t* frames, int n, int f,
+                             uint8_t* out, cudaStream_t st);
+cudaError_t launch_assemble(int W, int H, int fmt, const uint8_t* anchor,
+                            const uint8_t* const* smalls, int nsmall, int sw, uint8_t* out,
+                            cudaStream_t st);
+cudaError_t launch_rig_clusters(int W, int H, int fmt, const ClusterJob* jobs, int njobs,
+                                long max_cluster_bytes, const uint8_t* views, uint8_t* out,
+                                cudaStream_t st);
+}  // namespace fvv
+
+using namespace fvv;
+
+namespace {
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+int cuda_fail(cudaError_t e, const char* where) {
+    return fail(FVV_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+size_t align_up(size_t v, size_t a = 256) { return (v + a - 1) / a * a; }
+
+bool pow2_block(int b) { return b == 2 || b == 4 || b == 8; }
+
+int check_desc(const fvv_frame_desc* d) {
+    if (!d) return fail(FVV_EINVAL, "null frame descriptor");
+    if (d->width <= 0 || d->height <= 0)
+        return fail(FVV_EINVAL, "bad frame size " + std::to_string(d->width) + "x" +
+                                    std::to_string(d->height));
+    if (d->format < FVV_GRAY8 || d->format > FVV_RGB8)
+        return fail(FVV_EINVAL, "unknown pixel format " + std::to_string(d->format));
+    return FVV_OK;
+}
+
+// Tie-rule order of flow.py:57-66: lexsort((dx, dy, |dy|, dx^2+dy^2))
+void candidate_tables(int r, std::vector<int16_t>& rank_of, std::vector<int16_t>& cand_of_rank) {
+    const int side = 2 * r + 1, n = side * side;
+    std::vector<int> idx(n);
+    for (int i = 0; i < n; i++) idx[i] = i;
+    std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) {
+        int ady = a / side - r, adx = a % side - r, bdy = b / side - r, bdx = b % side - r;
+        int da = adx * adx + ady * ady, db = bdx * bdx + bdy * bdy;
+        if (da != db) return da < db;
+        if (std::abs(ady) != std::abs(bdy)) return std::abs(ady) < std::abs(bdy);
+        if (ady != bdy) return ady < bdy;
+        return adx < bdx;
+    });
+    rank_of.assign(n, 0);
+    cand_of_rank.assign(n, 0);
+    for (int k = 0; k < n; k++) {
+        cand_of_rank[k] = (int16_t)idx[k];
+        rank_of[idx[k]] = (int16_t)k;
+    }
+}
+
+void make_geometry(const fvv_frame_desc* d, const fvv_interp_params* p, Geometry* g) {
+    g->W = d->width;
+    g->H = d->height;
+    g->fmt = d->format;
+    g->cw = (d->width + 1) / 2;
+    g->ch = (d->height + 1) / 2;
+    fvv_frame_desc dd = *d;
+    g->frame_bytes = (long)fvv_frame_bytes(&dd);
+    for (int s = 0; s < 3; s++) {
+        const int f = s == 0 ? 4 : (s == 1 ? 2 : 1);
+        Level& L = g->lv[s];
+        L.w = d->width / f;
+        L.h = d->height / f;
+        L.block = p->block_size[s];
+        L.r = p->search_radius[s];
+        L.nbx = (L.w + L.block - 1) / L.block;
+        L.nby = (L.h + L.block - 1) / L.block;
+    }
+    g->eps = p->mask_epsilon;
+    g->eps2 = 2.0 * p->mask_epsilon;
+}
+
+// workspace = [header: candidate tables][pair slot 0][pair slot 1]...
+struct Layout {
+    size_t header;
+    size_t tab_off[3][2];
+    Planes P;
+};
+
+Layout make_layout(const Geometry& g) {
+    Layout lay{};
+    size_t off = 0;
+    for (int s = 0; s < 3; s++) {
+        const int side = 2 * g.lv[s].r + 1;
+        for (int k = 0; k < 2; k++) {
+            lay.tab_off[s][k] = off;
+            off = align_up(off + (size_t)side * side * 2);
+        }
+    }
+    lay.header = off;
+    Planes& P = lay.P;
+    size_t o = 0;
+    auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes); return r; };
+    const size_t W = g.W, H = g.H;
+    const size_t n0 = (size_t)g.lv[0].w * g.lv[0].h, n1 = (size_t)g.lv[1].w * g.lv[1].h;
+    const size_t n2 = W * H;
+    for (int s = 0; s < 2; s++) {
+        P.luma[s] = g.fmt == FVV_RGB8 ? take(n2) : 0;
+        P.s4[s] = take(n1 * 2);
+        P.s16[s] = take(n0 * 2);
+    }
+    for (int d = 0; d < 2; d++) {
+        for (int s = 0; s < 3; s++)
+            P.hit[s][d] = take((size_t)g.lv[s].nbx * g.lv[s].nby * sizeof(BlockHit));
+        P.flow0[d] = take(n0 * 8);
+        P.flow1[d] = take(n1 * 8);
+        P.tq1[d] = take(n1 * 2);
+        P.tq2[d] = take(n2 * 2);
+    }
+    P.sd = take(n2 * 2);
+    P.occ_l = take(n2 * 4);
+    P.occ_r = take(n2 * 4);
+    P.wl = take(n2);
+    P.wr = take(n2);
+    P.wc = g.fmt == FVV_YUV420 ? take((size_t)g.cw * g.ch * 4) : 0;
+    P.wrgb = g.fmt == FVV_RGB8 ? take(n2 * 6) : 0;
+    P.stride = align_up(o, 4096);
+    return lay;
+}
+}  // namespace
+
+struct fvv_engine {
+    Geometry g;
+    Layout lay;
+    Planes P;  // plane offsets relative to the first pair slot
+    uint8_t* ws;
+    uint8_t* slots;
+    int max_pairs;
+    const int16_t* rank_of[3];
+    const int16_t* cand_of_rank[3];
+    PairTable last;  // frame pointers of the most recent batch (diagnostics)
+    int last_npairs;
+};
+
+extern "C" {
+
+const char* fvv_last_error(void) { return g_err.c_str(); }
+
+const char* fvv_build_info(void) {
+    return "fvv_b200: sm_100a, integer SAD (u16x2 VIMNMX), literal-f64 warps, "
+           "scipy running-sum replay";
+}
+
+size_t fvv_frame_bytes(const fvv_frame_desc* d) {
+    if (!d || d->width <= 0 || d->height <= 0) return 0;
+    const size_t w = d->width, h = d->height;
+    if (d->format == FVV_GRAY8) return w * h;
+    if (d->format == FVV_RGB8) return w * h * 3;
+    return w * h + 2 * ((w + 1) / 2) * ((h + 1) / 2);
+}
+
+int fvv_validate_params(const fvv_interp_params* p) {
+    if (!p) return fail(FVV_EINVAL, "null params");
+    int mb = std::min(std::min(p->block_size[0], p->block_size[1]), p->block_size[2]);
+    int mr = std::min(std::min(p->search_radius[0], p->search_radius[1]), p->search_radius[2]);
+    if (mb < 2 || mr < 1) return fail(FVV_EINVAL, "degenerate block size or search radius");
+    for (int s = 0; s < 3; s++)
+        if (!pow2_block(p->block_size[s]))
+            return fail(FVV_EUNSUPPORTED,
+                        "block sizes must be 2, 4 or 8 on the B200 path (bit-exact fixed-point "
+                        "argument, DESIGN.md sec. 3)");
+    const int span = 4 * p->search_radius[0] + 2 * p->search_radius[1] + p->search_radius[2];
+    if (span > 120)
+        return fail(FVV_EUNSUPPORTED, "max_span " + std::to_string(span) +
+                                          " > 120 is outside the B200 path's exactness range");
+    if (!(p->mask_epsilon > 0.0))
+        return fail(FVV_EUNSUPPORTED, "mask_epsilon must be positive on the B200 path");
+    return FVV_OK;
+}
+
+static int check_interp_desc(const fvv_frame_desc* d) {
+    int rc = check_desc(d);
+    if (rc) return rc;
+    if (d->width % 4 || d->height % 4)
+        return fail(FVV_EINVAL, "frame dimensions must be divisible by 4 for the 3-scale pyramid");
+    return FVV_OK;
+}
+
+size_t fvv_engine_workspace_size(const fvv_frame_desc* d, const fvv_interp_params* p,
+                                 int max_pairs) {
+    if (check_interp_desc(d) || fvv_validate_params(p) || max_pairs < 1) return 0;
+    Geometry g;
+    make_geometry(d, p, &g);
+    Layout lay = make_layout(g);
+    return lay.header + lay.P.stride * (size_t)max_pairs;
+}
+
+int fvv_engine_create(const fvv_frame_desc* d, const fvv_interp_params* p, int max_pairs,
+                      void* workspace, size_t workspace_bytes, fvv_engine** out) {
+    int rc;
+    if ((rc = check_interp_desc(d))) return rc;
+    if ((rc = fvv_validate_params(p))) return rc;
+    if (max_pairs < 1) return fail(FVV_EINVAL, "max_pairs must be >= 1");
+    if (!out) return fail(FVV_EINVAL, "null engine out-pointer");
+    const size_t need = fvv_engine_workspace_size(d, p, max_pairs);
+    if (!workspace || workspace_bytes < need)
+        return fail(FVV_EINVAL, "workspace too small: need " + std::to_string(need) + " bytes");
+    fvv_engine* e = new fvv_engine();
+    make_geometry(d, p, &e->g);
+    e->lay = make_layout(e->g);
+    e->P = e->lay.P;
+    e->ws = static_cast<uint8_t*>(workspace);
+    e->slots = e->ws + e->lay.header;
+    e->max_pairs = max_pairs;
+    e->last_npairs = 0;
+    for (int s = 0; s < 3; s++) {
+        std::vector<int16_t> ro, cr;
+        candidate_tables(e->g.lv[s].r, ro, cr);
+        cudaError_t ce = cudaMemcpy(e->ws + e->lay.tab_off[s][0], ro.data(), ro.size() * 2,
+                                    cudaMemcpyHostToDevice);
+        if (ce == cudaSuccess)
+            ce = cudaMemcpy(e->ws + e->lay.tab_off[s][1], cr.data(), cr.size() * 2,
+                            cudaMemcpyHostToDevice);
+        if (ce != cudaSuccess) {
+            delete e;
+            return cuda_fail(ce, "fvv_engine_create: table upload");
+        }
+        e->rank_of[s] = reinterpret_cast<const int16_t*>(e->ws + e->lay.tab_off[s][0]);
+        e->cand_of_rank[s] = reinterpret_cast<const int16_t*>(e->ws + e->lay.tab_off[s][1]);
+    }
+    *out = e;
+    return FVV_OK;
+}
+
+void fvv_engine_destroy(fvv_engine* e) { delete e; }
+
+int fvv_engine_max_pairs(const fvv_engine* e) { return e ? e->max_pairs : 0; }
+
+static int run_pairs(fvv_engine* e, const uint8_t* const* L, const uint8_t* const* R,
+                     uint8_t* const* O, int npairs, cudaStream_t st) {
+    for (int b = 0; b < npairs; b += std::min(e->max_pairs, kMaxPairsPerLaunch)) {
+        const int n = std::min(std::min(e->max_pairs, kMaxPairsPerLaunch), npairs - b);
+        PairTable pt;
+        for (int i = 0; i < n; i++) {
+            pt.left[i] = L[b + i];
+            pt.right[i] = R[b + i];
+            pt.out[i] = O[b + i];
+        }
+        cudaError_t ce = run_interp_stage(e->g, pt, e->slots, e->P, e->rank_of, e->cand_of_rank, n,
+                                          nullptr, st);
+        if (ce != cudaSuccess) return cuda_fail(ce, "interpolate");
+        e->last = pt;
+        e->last_npairs = n;
+    }
+    return FVV_OK;
+}
+
+int fvv_interpolate_pairs(fvv_engine* e, const uint8_t* const* left, const uint8_t* const* right,
+                          uint8_t* const* out, int npairs, void* stream) {
+    if (!e) return fail(FVV_EINVAL, "null engine");
+    if (npairs < 0) return fail(FVV_EINVAL, "npairs < 0");
+    if (npairs == 0) return FVV_OK;
+    if (!left || !right || !out) return fail(FVV_EINVAL, "null pointer table");
+    return run_pairs(e, left, right, out, npairs, static_cast<cudaStream_t>(stream));
+}
+
+int fvv_interp_diagnostics(fvv_engine* e, int pair, float* flow_lr, float* flow_rl, double* mask,
+                           void* stream) {
+    if (!e) return fail(FVV_EINVAL, "null engine");
+    if (pair < 0 || pair >= e->last_npairs)
+        return fail(FVV_EINVAL, "no such pair in the most recent batch");
+    cudaError_t ce = run_diag(e->g, e->last, e->slots, e->P, pair, flow_lr, flow_rl, mask,
+                              static_cast<cudaStream_t>(stream));
+    if (ce != cudaSuccess) return cuda_fail(ce, "diagnostics");
+    return FVV_OK;
+}
+
+// Recursive midpoints over a views array whose slot k holds position k:
+// stage s interpolates between positions a and a+step for every a, writing
+// a+step/2 (interp.py:163-169).  `base` points at slot 0; `nslots` = last+1.
+static int run_recursion(fvv_engine* e, uint8_t* base, long stride, int nslots, int stages,
+                         cudaStream_t st) {
+    std::vector<const uint8_t*> L, R;
+    std::vector<uint8_t*> O;
+    for (int k = 1; k <= stages; k++) {
+        const int step = 1 << (stages - k + 1);
+        L.clear(); R.clear(); O.clear();
+        for (int a = 0; a + step < nslots; a += step) {
+            L.push_back(base + (long)a * stride);
+            R.push_back(base + (long)(a + step) * stride);
+            O.push_back(base + (long)(a + step / 2) * stride);
+        }
+        int rc = run_pairs(e, L.data(), R.data(), O.data(), (int)L.size(), st);
+        if (rc) return rc;
+    }
+    return FVV_OK;
+}
+
+int fvv_dense_views(fvv_engine* e, const uint8_t* left, const uint8_t* right, int stages,
+                    uint8_t* views, void* stream) {
+    if (!e) return fail(FVV_EINVAL, "null engine");
+    if (stages < 1) return fail(FVV_EINVAL, "stages must be >= 1");
+    if (stages > 6) return fail(FVV_EINVAL, "stages > 6 refused: 2**n - 1 views grows too fast");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const long fb = e->g.frame_bytes;
+    const int n = (1 << stages) - 1;
+    // the recursion reads the endpoints from their own buffers: build a
+    // pointer table over [left, views..., right]
+    std::vector<const uint8_t*> slot(n + 2);
+    slot[0] = left;
+    for (int i = 0; i < n; i++) slot[i + 1] = views + (long)i * fb;
+    slot[n + 1] = right;
+    std::vector<const uint8_t*> L, R;
+    std::vector<uint8_t*> O;
+    for (int k = 1; k <= stages; k++) {
+        const int step = 1 << (stages - k + 1);
+        L.clear(); R.clear(); O.clear();
+        for (int a = 0; a + step <= n + 1; a += step) {
+            L.push_back(slot[a]);
+            R.push_back(slot[a + step]);
+            O.push_back(const_cast<uint8_t*>(slot[a + step / 2]));
+        }
+        int rc = run_pairs(e, L.data(), R.data(), O.data(), (int)L.size(), st);
+        if (rc) return rc;
+    }
+    return FVV_OK;
+}
+
+int fvv_rig_views(fvv_engine* e, const uint8_t* cams, int ncams, int stages, uint8_t* views,
+                  void* stream) {
+    if (!e) return fail(FVV_EINVAL, "null engine");
+    if (ncams < 2) return fail(FVV_EINVAL, "need at least 2 cameras");
+    if (stages < 1 || stages > 6) return fail(FVV_EINVAL, "stages must be in 1..6");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const long fb = e->g.frame_bytes;
+    const int step = 1 << stages;
+    for (int c = 0; c < ncams; c++) {
+        cudaError_t ce = cudaMemcpyAsync(views + (long)c * step * fb, cams + (long)c * fb, fb,
+                                         cudaMemcpyDeviceToDevice, st);
+        if (ce != cudaSuccess) return cuda_fail(ce, "rig_views: camera copy");
+    }
+    return run_recursion(e, views, fb, (ncams - 1) * step + 1, stages, st);
+}
+
+int fvv_downscale(const fvv_frame_desc* d, const uint8_t* frames, int nframes, int factor,
+                  uint8_t* out, void* stream) {
+    int rc = check_desc(d);
+    if (rc) return rc;
+    if (factor < 1) return fail(FVV_EINVAL, "factor must be >= 1");
+    if (d->width % factor || d->height % factor)
+        return fail(FVV_EINVAL, std::to_string(d->width) + "x" + std::to_string(d->height) +
+                                    " not divisible by " + std::to_string(factor));
+    if (d->format == FVV_YUV420) {
+        const int cw = (d->width + 1) / 2, ch = (d->height + 1) / 2;
+        if (cw % factor || ch % factor)
+            return fail(FVV_EINVAL, std::to_string(ch) + "x" + std::to_string(cw) +
+                                        " not divisible by " + std::to_string(factor));
+    }
+    cudaError_t ce = launch_downscale(d->width, d->height, d->format, frames, nframes, factor, out,
+                                      static_cast<cudaStream_t>(stream));
+    if (ce != cudaSuccess) return cuda_fail(ce, "downscale");
+    return FVV_OK;
+}
+
+int fvv_cluster_width(int base_width, int nsmall) {
+    const int cols = (nsmall + 3) / 4;
+    return base_width + cols * (base_width / 4);
+}
+
+int fvv_assemble_cluster(const fvv_frame_desc* d, const uint8_t* anchor,
+                         const uint8_t* const* smalls, int nsmall, uint8_t* stitched,
+                         void* stream) {
+    int rc = check_desc(d);
+    if (rc) return rc;
+    if (d->format == FVV_RGB8) return fail(FVV_ELAYOUT, "cluster frames are gray or 4:2:0");
+    if (d->width % 8 || d->height % 8)
+        return fail(FVV_ELAYOUT, "anchor dimensions must be divisible by 8");
+    if (nsmall < 0 || nsmall > 256) return fail(FVV_ELAYOUT, "too many small tiles");
+    cudaError_t ce = launch_assemble(d->width, d->height, d->format, anchor, smalls, nsmall,
+                                     fvv_cluster_width(d->width, nsmall), stitched,
+                                     static_cast<cudaStream_t>(stream));
+    if (ce != cudaSuccess) return cuda_fail(ce, "assemble");
+    return FVV_OK;
+}
+
+// cluster.py:58-74 build_layouts for camera c
+static void layout_of(int ncams, int stages, int vps, int c, int* lo, int* hi) {
+    const int total = (ncams - 1) * (1 << stages) + 1;
+    const int anchor = c << stages;
+    *lo = std::max(0, anchor - vps);
+    *hi = std::min(total - 1, anchor + vps);
+}
+
+size_t fvv_rig_cluster_bytes(const fvv_frame_desc* d, int ncams, int stages, int vps,
+                             int cluster) {
+    if (check_desc(d) || cluster < 0 || cluster >= ncams) return 0;
+    int lo, hi;
+    layout_of(ncams, stages, vps, cluster, &lo, &hi);
+    const int nsmall = hi - lo;  // tiles minus the anchor
+    fvv_frame_desc s = *d;
+    s.width = fvv_cluster_width(d->width, nsmall);
+    return fvv_frame_bytes(&s);
+}
+
+int fvv_rig_clusters(const fvv_frame_desc* d, int ncams, int stages, int vps,
+                     const uint8_t* views, uint8_t* clusters, void* stream) {
+    int rc = check_desc(d);
+    if (rc) return rc;
+    if (ncams < 2) return fail(FVV_EINVAL, "need at least 2 cameras");
+    if (stages < 1 || stages > 6) return fail(FVV_EINVAL, "stages must be in 1..6");
+    if (vps < 1) return fail(FVV_ELAYOUT, "views_per_side must be >= 1");
+    if (vps > (1 << stages))
+        return fail(FVV_ELAYOUT, "views_per_side " + std::to_string(vps) + " exceeds the " +
+                                     std::to_string((1 << stages) - 1) +
+                                     " interpolated views available per gap");
+    if (d->format == FVV_RGB8) return fail(FVV_ELAYOUT, "cluster frames are gray or 4:2:0");
+    if (d->width % 8 || d->height % 8)
+        return fail(FVV_ELAYOUT, "anchor dimensions must be divisible by 8");
+    std::vector<ClusterJob> jobs(ncams);
+    long off = 0, maxb = 0;
+    for (int c = 0; c < ncams; c++) {
+        int lo, hi;
+        layout_of(ncams, stages, vps, c, &lo, &hi);
+        ClusterJob& j = jobs[c];
+        j.anchor_view = c << stages;
+        j.first_small = lo;
+        j.nsmall = hi - lo;
+        j.skip = j.anchor_view;
+        j.sw = fvv_cluster_width(d->width, j.nsmall);
+        j.out_offset = off;
+        const long b = (long)fvv_rig_cluster_bytes(d, ncams, stages, vps, c);
+        off += b;
+        maxb = std::max(maxb, b);
+    }
+    cudaError_t ce = launch_rig_clusters(d->width, d->height, d->format, jobs.data(), ncams, maxb,
+                                         views, clusters, static_cast<cudaStream_t>(stream));
+    if (ce != cudaSuccess) return cuda_fail(ce, "rig_clusters");
+    return FVV_OK;
+}
+
+}  // extern "C"

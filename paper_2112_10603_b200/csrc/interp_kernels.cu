@@ -1,0 +1,789 @@
+// interp_kernels.cu -- the per-stage kernels of interpolate() (interp.py:97-148)
+// for a batch of camera/view pairs.  One launch of each kernel covers every
+// pair of a recursion stage and both flow directions.
+//
+//   k_pyramid    luma + exact 2x2 / 4x4 pyramid sums      interp.py:67-71
+//   k_sad<L>     exhaustive SAD block search + tie rule    flow.py:69-91, _kernels.py:28-49
+//   k_flow<L>    flow = upscale(prev) + block_to_pixel     flow.py:47-54, 94-98, 129
+//   k_warpq<L>   target warped by the base flow, *8, rint  flow.py:123-124, 77-78
+//   k_mask_prod  final flows, mid warps, |wl-wr| column    interp.py:131-136, 78-94
+//                sums, occlusion cue (exact, order-free)   warp.py:27-46
+//   k_rowscan    scipy running-sum replay along rows,      imageops.py:51-52, warp.py:49-88
+//                mask, blend of every plane
+//
+// Numerics: see DESIGN.md sec. 3 -- integer SAD, literal f64 bilinear
+// arithmetic (no FMA), and the row-sequential replay of scipy's running sum
+// where the reference's rounding is order dependent.
+#include <algorithm>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "fvv_device.cuh"
+
+namespace fvv {
+
+// ---------------------------------------------------------------------------
+// k_pyramid: one thread per level-0 pixel (a 4x4 luma block).
+// s4 = 4 x level-1 value, s16 = 16 x level-0 value: box_downsample of the
+// integer luma is exact, so the f32 pyramid of interp.py:67-71 equals
+// s4/4 and s16/16 exactly.
+// ---------------------------------------------------------------------------
+__global__ void k_pyramid(Geometry g, PairTable pt, uint8_t* __restrict__ ws, Planes P) {
+    const int w0 = g.lv[0].w, h0 = g.lv[0].h;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    const int pair = blockIdx.z >> 1, side = blockIdx.z & 1;
+    if (x >= w0 || y >= h0) return;
+    const uint8_t* fr = side ? pt.right[pair] : pt.left[pair];
+    const int W = g.W;
+    int v[4][4];
+    if (g.fmt == FVV_RGB8) {
+        uint8_t* luma = plane<uint8_t>(ws, P, P.luma[side], pair);
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const uint8_t* row = fr + ((size_t)(4 * y + i) * W + 4 * x) * 3;
+            uchar4 o;
+            uint8_t t[4];
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                t[j] = bt601(row[3 * j], row[3 * j + 1], row[3 * j + 2]);
+                v[i][j] = t[j];
+            }
+            o.x = t[0]; o.y = t[1]; o.z = t[2]; o.w = t[3];
+            *reinterpret_cast<uchar4*>(luma + (size_t)(4 * y + i) * W + 4 * x) = o;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            uchar4 q = *reinterpret_cast<const uchar4*>(fr + (size_t)(4 * y + i) * W + 4 * x);
+            v[i][0] = q.x; v[i][1] = q.y; v[i][2] = q.z; v[i][3] = q.w;
+        }
+    }
+    uint16_t* s4 = plane<uint16_t>(ws, P, P.s4[side], pair);
+    const int w1 = g.lv[1].w;
+    int s16 = 0;
+#pragma unroll
+    for (int a = 0; a < 2; a++) {
+        int s0 = (v[2 * a][0] + v[2 * a][1]) + (v[2 * a + 1][0] + v[2 * a + 1][1]);
+        int s1 = (v[2 * a][2] + v[2 * a][3]) + (v[2 * a + 1][2] + v[2 * a + 1][3]);
+        *reinterpret_cast<ushort2*>(s4 + (size_t)(2 * y + a) * w1 + 2 * x) =
+            make_ushort2((uint16_t)s0, (uint16_t)s1);
+        s16 += s0 + s1;
+    }
+    plane<uint16_t>(ws, P, P.s16[side], pair)[(size_t)y * w0 + x] = (uint16_t)s16;
+}
+
+// rint(8 * s16/16) = rint(s16/2), half to even (flow.py:77-78 at level 0)
+__device__ __forceinline__ uint32_t q0_of(uint32_t s) { return (s + ((s >> 1) & 1u)) >> 1; }
+
+// ---------------------------------------------------------------------------
+// Level-specific sample access for the search.  d = direction: the reference
+// block is on side d, the target on side 1-d (flow.py:119).
+// ---------------------------------------------------------------------------
+template <int LEVEL>
+struct SadSrc {
+    const uint16_t* s16_ref;  // level 0
+    const uint16_t* s16_tgt;
+    const uint16_t* s4_ref;   // level 1
+    const uint8_t* y_ref;     // level 2
+    const uint16_t* tq;       // levels 1, 2: quantized warped target
+    __device__ __forceinline__ uint32_t ref(int idx) const {
+        if (LEVEL == 0) return q0_of(s16_ref[idx]);
+        if (LEVEL == 1) return 2u * s4_ref[idx];
+        return 8u * y_ref[idx];
+    }
+    __device__ __forceinline__ uint32_t tgt(int idx) const {
+        if (LEVEL == 0) return q0_of(s16_tgt[idx]);
+        return tq[idx];
+    }
+};
+
+template <int LEVEL>
+__device__ __forceinline__ SadSrc<LEVEL> make_src(const Geometry& g, const PairTable& pt,
+                                                  uint8_t* ws, const Planes& P, int pair, int d) {
+    SadSrc<LEVEL> s;
+    s.s16_ref = cplane<uint16_t>(ws, P, P.s16[d], pair);
+    s.s16_tgt = cplane<uint16_t>(ws, P, P.s16[1 - d], pair);
+    s.s4_ref = cplane<uint16_t>(ws, P, P.s4[d], pair);
+    if (g.fmt == FVV_RGB8) s.y_ref = cplane<uint8_t>(ws, P, P.luma[d], pair);
+    else s.y_ref = d ? pt.right[pair] : pt.left[pair];
+    s.tq = LEVEL == 1 ? cplane<uint16_t>(ws, P, P.tq1[d], pair)
+                      : cplane<uint16_t>(ws, P, P.tq2[d], pair);
+    return s;
+}
+
+struct SadLaunch {
+    int nbx_cta;      // blocks per CTA (horizontal strip)
+    int bx_begin;     // first block column covered by this launch
+    int bx_end;       // one past the last block column
+    int groups;       // dx groups per dy row (G)
+    int pw;           // pair-plane pitch (u32) -- covers every thread's reads
+    const int16_t* rank_of;      // stack index -> tie-rule rank  (flow.py:57-66)
+    const int16_t* cand_of_rank; // tie-rule rank -> stack index
+};
+
+// ---------------------------------------------------------------------------
+// k_sad: exhaustive SAD over the (2r+1)^2 candidates of every block of one
+// block row strip, fused with the reference's tie rule.
+//
+// SAD = sum |a - b| = 2 * sum max(a, b) - sum a - sum b.  Samples are
+// <= 2040 (8 * 255), so two candidates (dx, dx+1) share one 32-bit register
+// as u16 lanes: max via VIMNMX.U16x2, sums accumulated lane-wise in plain
+// 32-bit adds (no carry crosses lanes while a lane holds <= 32 samples) and
+// flushed to 32-bit totals.  Exact integer arithmetic: order free.
+// Winner = min over (sad, tie-rule rank) -> first minimum of
+// np.argmin over the lexsorted candidate stack (flow.py:81-82).
+// ---------------------------------------------------------------------------
+template <int LEVEL, int KP, bool FULL8>
+__global__ void __launch_bounds__(256) k_sad(Geometry g, PairTable pt, uint8_t* __restrict__ ws,
+                                             Planes P, SadLaunch sl) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const Level L = g.lv[LEVEL];
+    const int B = L.block, r = L.r, side = 2 * r + 1;
+    const int pair = blockIdx.z >> 1, d = blockIdx.z & 1;
+    const int by = blockIdx.y;
+    const int bx0 = sl.bx_begin + blockIdx.x * sl.nbx_cta;
+    const int nb = min(sl.nbx_cta, sl.bx_end - bx0);  // blocks in this CTA
+    const int stripW = sl.nbx_cta * B;
+    const int RW = stripW;                 // ref row pitch (u32)
+    const int PW = sl.pw;                  // pair-plane pitch (u32)
+    const int PH = B + 2 * r;
+    uint32_t* Rs = reinterpret_cast<uint32_t*>(smem);                 // B x RW
+    uint32_t* Ps = Rs + B * RW;                                        // PH x PW
+    unsigned long long* best = reinterpret_cast<unsigned long long*>(
+        smem + (((size_t)(B * RW + PH * PW) * 4 + 7) & ~(size_t)7));
+    int* suma = reinterpret_cast<int*>(best + sl.nbx_cta);
+    int16_t* rk = reinterpret_cast<int16_t*>(suma + sl.nbx_cta);      // side*side
+
+    const SadSrc<LEVEL> src = make_src<LEVEL>(g, pt, ws, P, pair, d);
+    const int w = L.w, h = L.h;
+    const int ys = by * B;
+    const int rows = min(B, h - ys);
+    const int nthreads = blockDim.x;
+    const int tid = threadIdx.x;
+
+    // stage the reference strip (duplicated into both u16 lanes) and the
+    // edge-padded target window (np.pad mode="edge", flow.py:78) as pairs
+    for (int i = tid; i < B * RW; i += nthreads) {
+        int yy = i / RW, xx = i % RW;
+        int gx = bx0 * B + xx, gy = ys + yy;
+        uint32_t q = 0;
+        if (gy < h && gx < w && xx < nb * B) q = src.ref(gy * w + gx);
+        Rs[i] = q | (q << 16);
+    }
+    for (int i = tid; i < PH * PW; i += nthreads) {
+        int yy = i / PW, xx = i % PW;
+        int gy = clampi(ys - r + yy, 0, h - 1);
+        int gx0 = clampi(bx0 * B - r + xx, 0, w - 1);
+        int gx1 = clampi(bx0 * B - r + xx + 1, 0, w - 1);
+        Ps[i] = src.tgt(gy * w + gx0) | (src.tgt(gy * w + gx1) << 16);
+    }
+    for (int i = tid; i < side * side; i += nthreads) rk[i] = sl.rank_of[i];
+    for (int i = tid; i < sl.nbx_cta; i += nthreads) best[i] = ~0ull;
+    __syncthreads();
+    // sum of reference samples per block (valid region only)
+    for (int kb = tid; kb < nb; kb += nthreads) {
+        int cols = min(B, w - (bx0 + kb) * B);
+        int s = 0;
+        for (int yy = 0; yy < rows; yy++)
+            for (int xx = 0; xx < cols; xx++) s += (int)(Rs[yy * RW + kb * B + xx] & 0xFFFFu);
+        suma[kb] = s;
+    }
+
+    const int per_block = side * sl.groups;
+    const int kb = tid / per_block;
+    const int rem = tid - kb * per_block;
+    const int iy = rem / sl.groups;             // dy + r
+    const int grp = rem - iy * sl.groups;
+    const int dxo = grp * 2 * KP;               // dx + r of this thread's first candidate
+    const bool active = kb < nb;
+
+    int tot_lo[KP], tot_hi[KP];  // 2*sum(max) - sum(b), per candidate
+#pragma unroll
+    for (int k = 0; k < KP; k++) tot_lo[k] = tot_hi[k] = 0;
+
+    if (active) {
+        const int cols = min(B, w - (bx0 + kb) * B);
+        const uint32_t* Rb = Rs + kb * B;
+        const uint32_t* Pb = Ps + iy * PW + kb * B + dxo;
+        if (FULL8) {
+            // B == 8, full block: 4-row packed accumulation then flush
+#pragma unroll 1
+            for (int y0 = 0; y0 < 8; y0 += 4) {
+                uint32_t am[KP], ab[KP];
+#pragma unroll
+                for (int k = 0; k < KP; k++) am[k] = ab[k] = 0;
+#pragma unroll
+                for (int yy = y0; yy < y0 + 4; yy++) {
+                    if (yy < rows) {
+                        uint32_t pv[2 * KP + 6];
+#pragma unroll
+                        for (int j = 0; j < 2 * KP + 6; j++) pv[j] = Pb[yy * PW + j];
+#pragma unroll
+                        for (int xx = 0; xx < 8; xx++) {
+                            const uint32_t rv = Rb[yy * RW + xx];
+#pragma unroll
+                            for (int k = 0; k < KP; k++) {
+                                const uint32_t p = pv[xx + 2 * k];
+                                am[k] += __vmaxu2(p, rv);
+                                ab[k] += p;
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < KP; k++) {
+                    tot_lo[k] += 2 * (int)(am[k] & 0xFFFFu) - (int)(ab[k] & 0xFFFFu);
+                    tot_hi[k] += 2 * (int)(am[k] >> 16) - (int)(ab[k] >> 16);
+                }
+            }
+        } else {
+            // general block size / ragged block: guarded, flush every row
+            for (int yy = 0; yy < rows; yy++) {
+                uint32_t am[KP], ab[KP];
+#pragma unroll
+                for (int k = 0; k < KP; k++) am[k] = ab[k] = 0;
+                for (int xx = 0; xx < cols; xx++) {
+                    const uint32_t rv = Rb[yy * RW + xx];
+#pragma unroll
+                    for (int k = 0; k < KP; k++) {
+                        const uint32_t p = Pb[yy * PW + xx + 2 * k];
+                        am[k] += __vmaxu2(p, rv);
+                        ab[k] += p;
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < KP; k++) {
+                    tot_lo[k] += 2 * (int)(am[k] & 0xFFFFu) - (int)(ab[k] & 0xFFFFu);
+                    tot_hi[k] += 2 * (int)(am[k] >> 16) - (int)(ab[k] >> 16);
+                }
+            }
+        }
+    }
+    __syncthreads();  // suma ready
+    if (active) {
+        const int sa = suma[kb];
+        unsigned long long mine = ~0ull;
+#pragma unroll
+        for (int k = 0; k < KP; k++) {
+            const int c0 = dxo + 2 * k;
+            if (c0 < side) {
+                unsigned long long key = ((unsigned long long)(uint32_t)(tot_lo[k] - sa) << 32) |
+                                         (uint32_t)rk[iy * side + c0];
+                mine = key < mine ? key : mine;
+            }
+            if (c0 + 1 < side) {
+                unsigned long long key = ((unsigned long long)(uint32_t)(tot_hi[k] - sa) << 32) |
+                                         (uint32_t)rk[iy * side + c0 + 1];
+                mine = key < mine ? key : mine;
+            }
+        }
+        atomicMin(&best[kb], mine);
+    }
+    __syncthreads();
+    for (int k = tid; k < nb; k += nthreads) {
+        const unsigned long long key = best[k];
+        const int idx = sl.cand_of_rank[(int)(key & 0xFFFFFFFFu)];
+        BlockHit hit;
+        hit.dy = (int16_t)(idx / side - r);
+        hit.dx = (int16_t)(idx % side - r);
+        hit.sad = (int32_t)(key >> 32);
+        plane<BlockHit>(ws, P, P.hit[LEVEL][d], pair)[by * L.nbx + bx0 + k] = hit;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_flow<L>: flow_L = base + f32(block_to_pixel(offsets))  (flow.py:122-129)
+// base = 0 at level 0, f32(2 * upscale(flow_{L-1})) otherwise.
+// ---------------------------------------------------------------------------
+template <int LEVEL>
+__global__ void k_flow(Geometry g, uint8_t* __restrict__ ws, Planes P) {
+    const Level L = g.lv[LEVEL];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int pair = blockIdx.z >> 1, d = blockIdx.z & 1;
+    if (i >= L.w * L.h) return;
+    const int y = i / L.w, x = i - (i / L.w) * L.w;
+    const float2 res = block_to_pixel_at(cplane<BlockHit>(ws, P, P.hit[LEVEL][d], pair), L.nby,
+                                         L.nbx, L.block, y, x);
+    float2 base = make_float2(0.0f, 0.0f);
+    if (LEVEL > 0) {
+        const Level Lp = g.lv[LEVEL - 1];
+        base = upscale_at(cplane<float2>(ws, P, P.flow0[d], pair), Lp.h, Lp.w, L.h, L.w, y, x);
+    }
+    float2 f = make_float2(__fadd_rn(base.x, res.x), __fadd_rn(base.y, res.y));
+    plane<float2>(ws, P, LEVEL == 0 ? P.flow0[d] : P.flow1[d], pair)[i] = f;
+}
+
+// ---------------------------------------------------------------------------
+// k_warpq<L> (L = 1, 2): pad_q source = rint(8 * warp_plane(target, base))
+// (flow.py:123-124 then :78); the edge padding is applied by the search.
+// ---------------------------------------------------------------------------
+template <int LEVEL>
+__global__ void k_warpq(Geometry g, PairTable pt, uint8_t* __restrict__ ws, Planes P) {
+    const Level L = g.lv[LEVEL];
+    const Level Lp = g.lv[LEVEL - 1];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int pair = blockIdx.z >> 1, d = blockIdx.z & 1;
+    if (i >= L.w * L.h) return;
+    const int y = i / L.w, x = i - (i / L.w) * L.w;
+    const float2* prev = cplane<float2>(ws, P, LEVEL == 1 ? P.flow0[d] : P.flow1[d], pair);
+    const float2 base = upscale_at(prev, Lp.h, Lp.w, L.h, L.w, y, x);
+    double v;
+    if (LEVEL == 1) {
+        const uint16_t* s4 = cplane<uint16_t>(ws, P, P.s4[1 - d], pair);
+        const int w = L.w;
+        auto src = [&](int yy, int xx) { return __dmul_rn((double)s4[yy * w + xx], 0.25); };
+        v = warp_at(src, L.h, L.w, y, x, base);
+    } else {
+        const uint8_t* yp = g.fmt == FVV_RGB8 ? cplane<uint8_t>(ws, P, P.luma[1 - d], pair)
+                                              : (d ? pt.left[pair] : pt.right[pair]);
+        const int w = L.w;
+        auto src = [&](int yy, int xx) { return (double)yp[yy * w + xx]; };
+        v = warp_at(src, L.h, L.w, y, x, base);
+    }
+    plane<uint16_t>(ws, P, LEVEL == 1 ? P.tq1[d] : P.tq2[d], pair)[i] =
+        (uint16_t)rint_i(__dmul_rn(v, 8.0));
+}
+
+// ---------------------------------------------------------------------------
+// k_mask_prod: per 16x32 output tile, everything of _mask_inputs
+// (interp.py:78-94) that does not depend on scipy's order of summation,
+// plus the mid warps of every plane (warp.py:27-46).
+//
+// Exactness: with power-of-two blocks every flow value is
+// a dyadic rational with <= 24 significant bits, so np.gradient, the f32
+// occlusion cue and BOTH smoothing passes over it are exact sums -- the
+// running sum of uniform_filter1d equals the plain 3-tap sum bitwise and
+// can be evaluated tile by tile.  |wl - wr| is integral, so its column pass
+// is exact too; only its row pass (k_rowscan) must replay scipy in order.
+// ---------------------------------------------------------------------------
+constexpr int kTH = 16, kTW = 32;           // output tile
+constexpr int kRH = kTH + 4, kRW = kTW + 4;  // flow region (+-2)
+constexpr int kOH = kTH + 2, kOW = kTW + 2;  // occlusion region (+-1)
+
+__global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
+                                                   uint8_t* __restrict__ ws, Planes P) {
+    __shared__ float2 fm[2][kRH][kRW];       // mid flows f_ml, f_mr (x -0.5)
+    __shared__ float occ[2][kOH][kOW];       // max(0, -div)
+    __shared__ float o0[2][kTH][kOW];        // column pass
+    __shared__ uint8_t dd[kTH + 2][kTW];     // |wl - wr| rows -1..TH
+    const int W = g.W, H = g.H;
+    const int x0 = blockIdx.x * kTW, y0 = blockIdx.y * kTH;
+    const int pair = blockIdx.z;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const Level L1 = g.lv[1], L2 = g.lv[2];
+    const uint8_t* frL = pt.left[pair];
+    const uint8_t* frR = pt.right[pair];
+
+    // (a) final flows (flow.py:122-129 at level 2) and mid flows (interp.py:131-132)
+    for (int i = tid; i < 2 * kRH * kRW; i += nt) {
+        const int d = i / (kRH * kRW);
+        const int j = i - d * (kRH * kRW);
+        const int ry = j / kRW, rx = j - (j / kRW) * kRW;
+        const int yi = clampi(y0 - 2 + ry, 0, H - 1), xi = clampi(x0 - 2 + rx, 0, W - 1);
+        const float2 base = upscale_at(cplane<float2>(ws, P, P.flow1[d], pair), L1.h, L1.w, H, W,
+                                       yi, xi);
+        const float2 res = block_to_pixel_at(cplane<BlockHit>(ws, P, P.hit[2][d], pair), L2.nby,
+                                             L2.nbx, L2.block, yi, xi);
+        float2 f = make_float2(__fadd_rn(base.x, res.x), __fadd_rn(base.y, res.y));
+        fm[d][ry][rx] = make_float2(__fmul_rn(f.x, -0.5f), __fmul_rn(f.y, -0.5f));
+    }
+    __syncthreads();
+
+    // (b) occlusion cue at clamped image positions (np.gradient, edge order 1)
+    for (int i = tid; i < 2 * kOH * kOW; i += nt) {
+        const int d = i / (kOH * kOW);
+        const int j = i - d * (kOH * kOW);
+        const int qy = j / kOW, qx = j - (j / kOW) * kOW;
+        const int yi = clampi(y0 - 1 + qy, 0, H - 1), xi = clampi(x0 - 1 + qx, 0, W - 1);
+        const int ry = yi - (y0 - 2), rx = xi - (x0 - 2);
+        float gx, gy;
+        if (W < 2) gx = 0.0f;
+        else if (xi == 0) gx = __fsub_rn(fm[d][ry][rx + 1].x, fm[d][ry][rx].x);
+        else if (xi == W - 1) gx = __fsub_rn(fm[d][ry][rx].x, fm[d][ry][rx - 1].x);
+        else gx = __fdiv_rn(__fsub_rn(fm[d][ry][rx + 1].x, fm[d][ry][rx - 1].x), 2.0f);
+        if (H < 2) gy = 0.0f;
+        else if (yi == 0) gy = __fsub_rn(fm[d][ry + 1][rx].y, fm[d][ry][rx].y);
+        else if (yi == H - 1) gy = __fsub_rn(fm[d][ry][rx].y, fm[d][ry - 1][rx].y);
+        else gy = __fdiv_rn(__fsub_rn(fm[d][ry + 1][rx].y, fm[d][ry - 1][rx].y), 2.0f);
+        const float v = -__fadd_rn(gx, gy);
+        occ[d][qy][qx] = v > 0.0f ? v : 0.0f;
+    }
+    __syncthreads();
+    // (c) column pass of smooth3 on occ (exact sums; f32 result of the f64 /3)
+    for (int i = tid; i < 2 * kTH * kOW; i += nt) {
+        const int d = i / (kTH * kOW);
+        const int j = i - d * (kTH * kOW);
+        const int ty = j / kOW, qx = j - (j / kOW) * kOW;
+        const double s = __dadd_rn(__dadd_rn((double)occ[d][ty][qx], (double)occ[d][ty + 1][qx]),
+                                   (double)occ[d][ty + 2][qx]);
+        o0[d][ty][qx] = (float)__ddiv_rn(s, 3.0);
+    }
+    // (e) luma warps for rows -1..TH (clamped), d = |wl - wr|
+    for (int i = tid; i < (kTH + 2) * kTW; i += nt) {
+        const int qy = i / kTW, tx = i - (i / kTW) * kTW;
+        const int yi = clampi(y0 - 1 + qy, 0, H - 1), xi = x0 + tx;
+        if (xi >= W) continue;
+        const int ry = yi - (y0 - 2), rx = xi - (x0 - 2);
+        const float2 fl = fm[0][ry][rx], fr = fm[1][ry][rx];
+        const bool center = qy >= 1 && qy <= kTH && y0 - 1 + qy < H;
+        uint8_t wl, wr;
+        if (g.fmt == FVV_RGB8) {
+            uint8_t cl[3], cr[3];
+#pragma unroll
+            for (int c = 0; c < 3; c++) {
+                auto sl = [&](int yy, int xx) { return (double)frL[((size_t)yy * W + xx) * 3 + c]; };
+                auto sr = [&](int yy, int xx) { return (double)frR[((size_t)yy * W + xx) * 3 + c]; };
+                cl[c] = to_u8(warp_at(sl, H, W, yi, xi, fl));
+                cr[c] = to_u8(warp_at(sr, H, W, yi, xi, fr));
+            }
+            wl = bt601(cl[0], cl[1], cl[2]);
+            wr = bt601(cr[0], cr[1], cr[2]);
+            if (center) {
+                uint8_t* o = plane<uint8_t>(ws, P, P.wrgb, pair) + ((size_t)yi * W + xi) * 6;
+#pragma unroll
+                for (int c = 0; c < 3; c++) { o[c] = cl[c]; o[3 + c] = cr[c]; }
+            }
+        } else {
+            auto sl = [&](int yy, int xx) { return (double)frL[(size_t)yy * W + xx]; };
+            auto sr = [&](int yy, int xx) { return (double)frR[(size_t)yy * W + xx]; };
+            wl = to_u8(warp_at(sl, H, W, yi, xi, fl));
+            wr = to_u8(warp_at(sr, H, W, yi, xi, fr));
+        }
+        dd[qy][tx] = (uint8_t)abs((int)wl - (int)wr);
+        if (center) {
+            plane<uint8_t>(ws, P, P.wl, pair)[(size_t)yi * W + xi] = wl;
+            plane<uint8_t>(ws, P, P.wr, pair)[(size_t)yi * W + xi] = wr;
+        }
+    }
+    // (g) chroma warps with the half-resolution, half-magnitude flow
+    //     (imageops.py:40-48; f32 pairwise mean, exact here)
+    if (g.fmt == FVV_YUV420) {
+        const int cw = g.cw, chh = g.ch;
+        const uint8_t* uL = frL + (size_t)W * H;
+        const uint8_t* uR = frR + (size_t)W * H;
+        const size_t cplane_sz = (size_t)cw * chh;
+        for (int i = tid; i < (kTH / 2) * (kTW / 2); i += nt) {
+            const int cy = y0 / 2 + i / (kTW / 2), cx = x0 / 2 + i % (kTW / 2);
+            if (cy >= chh || cx >= cw) continue;
+            const int ry = 2 * cy - (y0 - 2), rx = 2 * cx - (x0 - 2);
+            float2 cv[2];
+#pragma unroll
+            for (int d = 0; d < 2; d++) {
+                const float2 a = fm[d][ry][rx], b = fm[d][ry][rx + 1];
+                const float2 c = fm[d][ry + 1][rx], e = fm[d][ry + 1][rx + 1];
+                const float sx = __fadd_rn(__fadd_rn(a.x, b.x), __fadd_rn(c.x, e.x));
+                const float sy = __fadd_rn(__fadd_rn(a.y, b.y), __fadd_rn(c.y, e.y));
+                cv[d] = make_float2(__fmul_rn(__fdiv_rn(sx, 4.0f), 0.5f),
+                                    __fmul_rn(__fdiv_rn(sy, 4.0f), 0.5f));
+            }
+            uint8_t o[4];
+#pragma unroll
+            for (int p = 0; p < 2; p++) {
+                const uint8_t* pl = uL + p * cplane_sz;
+                const uint8_t* pr = uR + p * cplane_sz;
+                auto sl = [&](int yy, int xx) { return (double)pl[(size_t)yy * cw + xx]; };
+                auto sr = [&](int yy, int xx) { return (double)pr[(size_t)yy * cw + xx]; };
+                o[2 * p] = to_u8(warp_at(sl, chh, cw, cy, cx, cv[0]));
+                o[2 * p + 1] = to_u8(warp_at(sr, chh, cw, cy, cx, cv[1]));
+            }
+            plane<uchar4>(ws, P, P.wc, pair)[(size_t)cy * cw + cx] = make_uchar4(o[0], o[1], o[2], o[3]);
+        }
+    }
+    __syncthreads();
+    // (d) row pass of smooth3 on occ; (f) column sums of |wl - wr|
+    for (int i = tid; i < kTH * kTW; i += nt) {
+        const int ty = i / kTW, tx = i - (i / kTW) * kTW;
+        const int yi = y0 + ty, xi = x0 + tx;
+        if (yi >= H || xi >= W) continue;
+        const size_t o = (size_t)yi * W + xi;
+#pragma unroll
+        for (int d = 0; d < 2; d++) {
+            const double s = __dadd_rn(__dadd_rn((double)o0[d][ty][tx], (double)o0[d][ty][tx + 1]),
+                                       (double)o0[d][ty][tx + 2]);
+            plane<float>(ws, P, d ? P.occ_r : P.occ_l, pair)[o] = (float)__ddiv_rn(s, 3.0);
+        }
+        plane<uint16_t>(ws, P, P.sd, pair)[o] =
+            (uint16_t)((int)dd[ty][tx] + (int)dd[ty + 1][tx] + (int)dd[ty + 2][tx]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_rowscan: the row pass of smooth3(|wl - wr|) replayed in scipy's order
+// (tmp = (p0+p1)+p2; tmp += p[i+2]-p[i-1]; out = tmp/3, all f64), then the
+// mask (warp.py:49-63) and the blend of every plane (warp.py:66-88).
+// One CTA = 32 rows of one pair; 64-column chunks; one thread per row runs
+// the sequential chain, all threads do the per-pixel work around it.
+// ---------------------------------------------------------------------------
+constexpr int kRB = 32, kCW = 64;
+
+__global__ void __launch_bounds__(128) k_rowscan(Geometry g, PairTable pt,
+                                                 const uint8_t* __restrict__ ws, Planes P,
+                                                 int pair_base, bool write_frame,
+                                                 double* mask_out /* nullable: one pair */) {
+    __shared__ double dtab[766];          // s/3.0 for the integral column sums
+    __shared__ double buf[kRB][kCW + 1];  // deltas, then running sums, then masks
+    __shared__ double tmp_carry[kRB];
+    const int W = g.W, H = g.H;
+    const int pair = blockIdx.y + pair_base;
+    const int y0 = blockIdx.x * kRB;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const uint16_t* sd = cplane<uint16_t>(ws, P, P.sd, pair);
+    const float* ol = cplane<float>(ws, P, P.occ_l, pair);
+    const float* orr = cplane<float>(ws, P, P.occ_r, pair);
+    const uint8_t* wl = cplane<uint8_t>(ws, P, P.wl, pair);
+    const uint8_t* wr = cplane<uint8_t>(ws, P, P.wr, pair);
+    uint8_t* out = pt.out[pair];
+    for (int i = tid; i < 766; i += nt) dtab[i] = __ddiv_rn((double)i, 3.0);
+    __syncthreads();
+
+    for (int c0 = 0; c0 < W; c0 += kCW) {
+        // phase 1: differences p[i+2] - p[i-1] (independent of the chain)
+        for (int i = tid; i < kRB * kCW; i += nt) {
+            const int r = i / kCW, c = i - (i / kCW) * kCW;
+            const int y = y0 + r, x = c0 + c;
+            if (y >= H || x >= W) continue;
+            const uint16_t* row = sd + (size_t)y * W;
+            buf[r][c] = __dsub_rn(dtab[row[min(x + 1, W - 1)]], dtab[row[max(x - 2, 0)]]);
+        }
+        __syncthreads();
+        // phase 2: the order-dependent running sum, one thread per row
+        if (tid < kRB && y0 + tid < H) {
+            const int r = tid;
+            double tmp = c0 == 0 ? 0.0 : tmp_carry[r];
+            const uint16_t* row = sd + (size_t)(y0 + r) * W;
+            const int n = min(kCW, W - c0);
+            for (int c = 0; c < n; c++) {
+                if (c0 + c == 0) {
+                    tmp = __dadd_rn(__dadd_rn(dtab[row[0]], dtab[row[0]]), dtab[row[min(1, W - 1)]]);
+                } else {
+                    tmp = __dadd_rn(tmp, buf[r][c]);
+                }
+                buf[r][c] = tmp;
+            }
+            tmp_carry[r] = tmp;
+        }
+        __syncthreads();
+        // phase 3: mask + blend of luma / RGB
+        for (int i = tid; i < kRB * kCW; i += nt) {
+            const int r = i / kCW, c = i - (i / kCW) * kCW;
+            const int y = y0 + r, x = c0 + c;
+            if (y >= H || x >= W) continue;
+            const size_t o = (size_t)y * W + x;
+            const double D = __ddiv_rn(buf[r][c], 3.0);
+            const float ql = __fadd_rn(0.5f, __fmul_rn(4.0f, ol[o]));
+            const float qr = __fadd_rn(0.5f, __fmul_rn(4.0f, orr[o]));
+            const double el = __dmul_rn(D, (double)ql);
+            const double er = __dmul_rn(D, (double)qr);
+            double m = __ddiv_rn(__dadd_rn(er, g.eps), __dadd_rn(__dadd_rn(el, er), g.eps2));
+            m = fmin(fmax(m, 0.0), 1.0);
+            const double m1 = __dsub_rn(1.0, m);
+            if (!write_frame) {
+            } else if (g.fmt == FVV_RGB8) {
+                const uint8_t* px = cplane<uint8_t>(ws, P, P.wrgb, pair) + o * 6;
+#pragma unroll
+                for (int ch = 0; ch < 3; ch++)
+                    out[o * 3 + ch] = to_u8(__dadd_rn(__dmul_rn(m, (double)px[ch]),
+                                                      __dmul_rn(m1, (double)px[3 + ch])));
+            } else {
+                out[o] = to_u8(__dadd_rn(__dmul_rn(m, (double)wl[o]), __dmul_rn(m1, (double)wr[o])));
+            }
+            if (mask_out) mask_out[o] = m;
+            buf[r][c] = m;
+        }
+        __syncthreads();
+        // phase 4: chroma blend with the 2x2-mean mask (warp.py:83-88)
+        if (g.fmt == FVV_YUV420 && write_frame) {
+            const int cw = g.cw, chh = g.ch;
+            const uchar4* wc = cplane<uchar4>(ws, P, P.wc, pair);
+            uint8_t* uo = out + (size_t)W * H;
+            uint8_t* vo = uo + (size_t)cw * chh;
+            for (int i = tid; i < (kRB / 2) * (kCW / 2); i += nt) {
+                const int a = i / (kCW / 2), b = i - (i / (kCW / 2)) * (kCW / 2);
+                const int cy = y0 / 2 + a, cx = c0 / 2 + b;
+                if (cy >= chh || cx >= cw) continue;
+                const double s = __dadd_rn(__dadd_rn(buf[2 * a][2 * b], buf[2 * a][2 * b + 1]),
+                                           __dadd_rn(buf[2 * a + 1][2 * b], buf[2 * a + 1][2 * b + 1]));
+                const double mc = __ddiv_rn(s, 4.0);
+                const double mc1 = __dsub_rn(1.0, mc);
+                const uchar4 q = wc[(size_t)cy * cw + cx];
+                uo[(size_t)cy * cw + cx] = to_u8(__dadd_rn(__dmul_rn(mc, (double)q.x),
+                                                           __dmul_rn(mc1, (double)q.y)));
+                vo[(size_t)cy * cw + cx] = to_u8(__dadd_rn(__dmul_rn(mc, (double)q.z),
+                                                           __dmul_rn(mc1, (double)q.w)));
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host-side launch helpers (called from api.cu)
+// ---------------------------------------------------------------------------
+template <int LEVEL, int KP, bool FULL8>
+static cudaError_t launch_sad_kp(const Geometry& g, const PairTable& pt, uint8_t* ws,
+                                 const Planes& P, SadLaunch sl, int npairs, cudaStream_t st) {
+    const Level& L = g.lv[LEVEL];
+    const int side = 2 * L.r + 1;
+    const int nbx = sl.bx_end - sl.bx_begin;
+    if (nbx <= 0) return cudaSuccess;
+    const int threads_needed = sl.nbx_cta * side * sl.groups;
+    const int threads = ((threads_needed + 31) / 32) * 32;
+    const int RW = sl.nbx_cta * L.block, PW = sl.pw, PH = L.block + 2 * L.r;
+    size_t smem = (size_t)L.block * RW * 4 + (size_t)PH * PW * 4;
+    smem = (smem + 7) & ~(size_t)7;
+    smem += (size_t)sl.nbx_cta * 8 + (size_t)sl.nbx_cta * 4 + (size_t)side * side * 2 + 16;
+    auto kern = k_sad<LEVEL, KP, FULL8>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    dim3 grid((nbx + sl.nbx_cta - 1) / sl.nbx_cta, L.nby, 2 * npairs);
+    kern<<<grid, threads, smem, st>>>(g, pt, ws, P, sl);
+    return cudaGetLastError();
+}
+
+template <int LEVEL, bool FULL8>
+static cudaError_t launch_sad_level(const Geometry& g, const PairTable& pt, uint8_t* ws,
+                                    const Planes& P, SadLaunch sl, int kp, int npairs,
+                                    cudaStream_t st) {
+    switch (kp) {
+        case 3: return launch_sad_kp<LEVEL, 3, FULL8>(g, pt, ws, P, sl, npairs, st);
+        case 5: return launch_sad_kp<LEVEL, 5, FULL8>(g, pt, ws, P, sl, npairs, st);
+        case 7: return launch_sad_kp<LEVEL, 7, FULL8>(g, pt, ws, P, sl, npairs, st);
+        case 9: return launch_sad_kp<LEVEL, 9, FULL8>(g, pt, ws, P, sl, npairs, st);
+        case 13: return launch_sad_kp<LEVEL, 13, FULL8>(g, pt, ws, P, sl, npairs, st);
+        default: return launch_sad_kp<LEVEL, 16, FULL8>(g, pt, ws, P, sl, npairs, st);
+    }
+}
+
+// Choose KP (candidate pairs per thread) and G (threads per dy row).
+static void pick_kp(int side, int* kp, int* groups) {
+    static const int opts[] = {3, 5, 7, 9, 13, 16};
+    const int need = (side + 1) / 2;  // candidate pairs per dy row
+    int best_kp = 16, best_g = (need + 15) / 16, best_waste = 1 << 30;
+    for (int o : opts) {
+        int gcount = (need + o - 1) / o;
+        int waste = gcount * o - need;
+        if (waste < best_waste || (waste == best_waste && gcount < best_g)) {
+            best_waste = waste; best_kp = o; best_g = gcount;
+        }
+    }
+    *kp = best_kp;
+    *groups = best_g;
+}
+
+template <int LEVEL>
+static cudaError_t run_sad(const Geometry& g, const PairTable& pt, uint8_t* ws, const Planes& P,
+                           const int16_t* rank_of, const int16_t* cand_of_rank, int npairs,
+                           cudaStream_t st) {
+    const Level& L = g.lv[LEVEL];
+    const int side = 2 * L.r + 1;
+    int kp, groups;
+    pick_kp(side, &kp, &groups);
+    SadLaunch sl;
+    sl.groups = groups;
+    sl.rank_of = rank_of;
+    sl.cand_of_rank = cand_of_rank;
+    int per_block = side * groups;
+    sl.nbx_cta = per_block >= 256 ? 1 : (256 / per_block < 32 ? 256 / per_block : 32);
+    // every thread reads pair columns [kb*B + dxo, kb*B + dxo + 2*KP + 6)
+    sl.pw = sl.nbx_cta * L.block + std::max(2 * L.r + 1, 2 * kp * groups + 6) + 1;
+    if ((sl.pw & 1) == 0) sl.pw += 1;  // odd pitch: dy rows fall in distinct banks
+    const bool fast = L.block == 8;
+    const int full_cols = fast ? L.w / 8 : 0;  // block columns with 8 valid columns
+    cudaError_t e;
+    // interior: rows may be ragged only in the last block row -> FULL8 path
+    // handles the row guard itself; ragged columns go to the general path.
+    if (full_cols > 0) {
+        sl.bx_begin = 0;
+        sl.bx_end = full_cols;
+        e = launch_sad_level<LEVEL, true>(g, pt, ws, P, sl, kp, npairs, st);
+        if (e != cudaSuccess) return e;
+    }
+    if (full_cols < L.nbx) {
+        sl.bx_begin = full_cols;
+        sl.bx_end = L.nbx;
+        e = launch_sad_level<LEVEL, false>(g, pt, ws, P, sl, kp, npairs, st);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+cudaError_t run_interp_stage(const Geometry& g, const PairTable& pt, uint8_t* ws, const Planes& P,
+                             const int16_t* const* rank_of, const int16_t* const* cand_of_rank,
+                             int npairs, double* mask_out, cudaStream_t st) {
+    cudaError_t e;
+    {
+        dim3 blk(32, 8);
+        dim3 grd((g.lv[0].w + 31) / 32, (g.lv[0].h + 7) / 8, 2 * npairs);
+        k_pyramid<<<grd, blk, 0, st>>>(g, pt, ws, P);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    if ((e = run_sad<0>(g, pt, ws, P, rank_of[0], cand_of_rank[0], npairs, st)) != cudaSuccess)
+        return e;
+    {
+        dim3 grd((g.lv[0].w * g.lv[0].h + 255) / 256, 1, 2 * npairs);
+        k_flow<0><<<grd, 256, 0, st>>>(g, ws, P);
+        dim3 grd1((g.lv[1].w * g.lv[1].h + 255) / 256, 1, 2 * npairs);
+        k_warpq<1><<<grd1, 256, 0, st>>>(g, pt, ws, P);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    if ((e = run_sad<1>(g, pt, ws, P, rank_of[1], cand_of_rank[1], npairs, st)) != cudaSuccess)
+        return e;
+    {
+        dim3 grd((g.lv[1].w * g.lv[1].h + 255) / 256, 1, 2 * npairs);
+        k_flow<1><<<grd, 256, 0, st>>>(g, ws, P);
+        dim3 grd2((g.lv[2].w * g.lv[2].h + 255) / 256, 1, 2 * npairs);
+        k_warpq<2><<<grd2, 256, 0, st>>>(g, pt, ws, P);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    if ((e = run_sad<2>(g, pt, ws, P, rank_of[2], cand_of_rank[2], npairs, st)) != cudaSuccess)
+        return e;
+    {
+        dim3 grd((g.W + kTW - 1) / kTW, (g.H + kTH - 1) / kTH, npairs);
+        k_mask_prod<<<grd, 256, 0, st>>>(g, pt, ws, P);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        dim3 grd2((g.H + kRB - 1) / kRB, npairs);
+        k_rowscan<<<grd2, 128, 0, st>>>(g, pt, ws, P, 0, true, mask_out);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+// diagnostics: final flows (InterpDiagnostics.scales[-1].flow_lr/rl) and mask
+__global__ void k_diag_flow(Geometry g, const uint8_t* __restrict__ ws, Planes P, int pair,
+                            float2* flow_lr, float2* flow_rl) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int d = blockIdx.z;
+    if (i >= g.W * g.H) return;
+    float2* out = d ? flow_rl : flow_lr;
+    if (!out) return;
+    const int y = i / g.W, x = i - (i / g.W) * g.W;
+    const Level L1 = g.lv[1], L2 = g.lv[2];
+    const float2 base = upscale_at(cplane<float2>(ws, P, P.flow1[d], pair), L1.h, L1.w, g.H, g.W,
+                                   y, x);
+    const float2 res = block_to_pixel_at(cplane<BlockHit>(ws, P, P.hit[2][d], pair), L2.nby,
+                                         L2.nbx, L2.block, y, x);
+    out[i] = make_float2(__fadd_rn(base.x, res.x), __fadd_rn(base.y, res.y));
+}
+
+cudaError_t run_diag(const Geometry& g, const PairTable& pt, uint8_t* ws, const Planes& P, int pair,
+                     float* flow_lr, float* flow_rl, double* mask, cudaStream_t st) {
+    if (flow_lr || flow_rl) {
+        dim3 grd((g.W * g.H + 255) / 256, 1, 2);
+        k_diag_flow<<<grd, 256, 0, st>>>(g, ws, P, pair, reinterpret_cast<float2*>(flow_lr),
+                                         reinterpret_cast<float2*>(flow_rl));
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    if (mask) {
+        dim3 grd2((g.H + kRB - 1) / kRB, 1);
+        k_rowscan<<<grd2, 128, 0, st>>>(g, pt, ws, P, pair, false, mask);
+        return cudaGetLastError();
+    }
+    return cudaSuccess;
+}
+
+}  // namespace fvv

@@ -1,0 +1,293 @@
+"""Midpoint view interpolation and recursive dense views on the B200.
+
+Drop-in mirror of the reference's public interpolation API (fvv.interp,
+interp.py:24-170): same entry points (`interpolate`, `dense_views`), same
+`InterpConfig` fields and validation, same Frame layouts and error classes.
+The compute is the CUDA path in libfvv_b200.so (csrc/interp_kernels.cu)
+reached through the C ABI (include/fvv_b200.h); there is no CPU fallback.
+
+Batched device entry points (`Interpolator.pairs`, `Interpolator.dense`) take
+torch uint8 tensors of packed frames already resident in HBM.
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass, field
+from typing import Callable
+
+import numpy as np
+
+from . import _lib
+from .frame import Frame, PixelFormat, frame_from_packed, packed
+
+SCALE_FACTORS = (4, 2, 1)  # coarse to fine (interp.py:21)
+
+
+@dataclass(frozen=True)
+class InterpConfig:
+    """interp.py:24-46 -- identical fields, defaults and validation."""
+
+    block_size: tuple = (8, 8, 8)
+    search_radius: tuple = (12, 4, 2)
+    mask_epsilon: float = 1e-3
+    border_band: int = 8
+    refine: Callable | None = None
+
+    def __post_init__(self) -> None:
+        if len(self.block_size) != 3 or len(self.search_radius) != 3:
+            raise ValueError("three scales need three block sizes and radii")
+        if min(self.block_size) < 2 or min(self.search_radius) < 1:
+            raise ValueError("degenerate block size or search radius")
+
+    @property
+    def max_span(self) -> int:
+        r0, r1, r2 = self.search_radius
+        return 4 * r0 + 2 * r1 + r2
+
+
+@dataclass(frozen=True)
+class FlowField:
+    """flow.py:23-44: per-pixel (dx, dy) f32 offsets, (h, w, 2)."""
+
+    width: int
+    height: int
+    vectors: np.ndarray
+
+    def __post_init__(self) -> None:
+        if self.vectors.shape != (self.height, self.width, 2):
+            raise ValueError(f"flow vectors {self.vectors.shape} != {(self.height, self.width, 2)}")
+
+    @staticmethod
+    def zero(width: int, height: int) -> "FlowField":
+        return FlowField(width, height, np.zeros((height, width, 2), dtype=np.float32))
+
+    def scaled(self, factor: float) -> "FlowField":
+        return FlowField(self.width, self.height, self.vectors * np.float32(factor))
+
+    def max_magnitude(self) -> float:
+        return float(np.max(np.abs(self.vectors))) if self.vectors.size else 0.0
+
+
+@dataclass
+class ScaleDiagnostics:  # interp.py:49-56
+    flow_lr: FlowField
+    flow_rl: FlowField
+    match_error_lr: np.ndarray | None = None
+    match_error_rl: np.ndarray | None = None
+    mask: np.ndarray | None = None
+    blend_luma: np.ndarray | None = None
+
+
+@dataclass
+class InterpDiagnostics:  # interp.py:59-64
+    scales: list = field(default_factory=list)
+    flow_mid_left: FlowField | None = None
+    flow_mid_right: FlowField | None = None
+    mask: np.ndarray | None = None
+
+
+# ---------------------------------------------------------------------------
+# Device engine
+# ---------------------------------------------------------------------------
+class Interpolator:
+    """One geometry + config + workspace (fvv_engine) on the current CUDA device.
+
+    `max_pairs` bounds the interpolations run per recursion stage; a rig of
+    C cameras at `stages` needs (C-1) * 2**(stages-1).
+    """
+
+    def __init__(self, width: int, height: int, fmt, config: InterpConfig | None = None,
+                 max_pairs: int = 1, device=None):
+        import torch
+        L = _lib.require_cuda()
+        self.config = config or InterpConfig()
+        self.width, self.height, self.format = int(width), int(height), PixelFormat(int(fmt))
+        self.max_pairs = int(max_pairs)
+        self._desc = _lib.desc(width, height, int(fmt))
+        self._params = _lib.params(self.config)
+        _lib.check(L.fvv_validate_params(ctypes.byref(self._params)))
+        if width % 4 or height % 4:
+            raise ValueError("frame dimensions must be divisible by 4 for the 3-scale pyramid")
+        self.frame_bytes = int(L.fvv_frame_bytes(ctypes.byref(self._desc)))
+        ws = int(L.fvv_engine_workspace_size(ctypes.byref(self._desc), ctypes.byref(self._params),
+                                             self.max_pairs))
+        if ws == 0:
+            _lib.check(-1)
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self._ws = torch.empty(ws, dtype=torch.uint8, device=self.device)
+        h = ctypes.c_void_p()
+        _lib.check(L.fvv_engine_create(ctypes.byref(self._desc), ctypes.byref(self._params),
+                                       self.max_pairs, ctypes.c_void_p(self._ws.data_ptr()), ws,
+                                       ctypes.byref(h)))
+        self._h = h
+        self._L = L
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                self._L.fvv_engine_destroy(self._h)
+                self._h = None
+        except Exception:  # noqa: BLE001
+            pass
+
+    @property
+    def workspace_bytes(self) -> int:
+        return int(self._ws.numel())
+
+    @staticmethod
+    def _stream():
+        import torch
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def _check_frames(self, t, n=None):
+        import torch
+        if t.dtype != torch.uint8 or not t.is_cuda or not t.is_contiguous():
+            raise ValueError("frames must be contiguous uint8 CUDA tensors of packed planes")
+        if t.shape[-1] != self.frame_bytes:
+            raise ValueError(f"packed frame is {t.shape[-1]} bytes, expected {self.frame_bytes}")
+
+    def pairs(self, left, right, out=None):
+        """interpolate() over a batch: left/right (n, frame_bytes) -> out (n, frame_bytes)."""
+        import torch
+        self._check_frames(left)
+        self._check_frames(right)
+        if left.shape != right.shape:
+            raise ValueError("interpolation inputs must share size and format")
+        n = left.shape[0]
+        if out is None:
+            out = torch.empty_like(left)
+        fb = self.frame_bytes
+        lp = _lib.ptr_array([left.data_ptr() + i * fb for i in range(n)])
+        rp = _lib.ptr_array([right.data_ptr() + i * fb for i in range(n)])
+        op = _lib.ptr_array([out.data_ptr() + i * fb for i in range(n)])
+        _lib.check(self._L.fvv_interpolate_pairs(self._h, lp, rp, op, n, self._stream()))
+        return out
+
+    def diagnostics(self, pair: int = 0):
+        """Final flows + mask of pair `pair` of the most recent `pairs` call (device tensors)."""
+        import torch
+        H, W = self.height, self.width
+        flr = torch.empty((H, W, 2), dtype=torch.float32, device=self.device)
+        frl = torch.empty_like(flr)
+        m = torch.empty((H, W), dtype=torch.float64, device=self.device)
+        _lib.check(self._L.fvv_interp_diagnostics(self._h, pair, ctypes.c_void_p(flr.data_ptr()),
+                                                  ctypes.c_void_p(frl.data_ptr()),
+                                                  ctypes.c_void_p(m.data_ptr()), self._stream()))
+        return flr, frl, m
+
+    def dense(self, left, right, stages: int, views=None):
+        """dense_views() on device: left/right (frame_bytes,) -> (2**stages - 1, frame_bytes)."""
+        import torch
+        if stages < 1:
+            raise ValueError("stages must be >= 1")
+        if stages > 6:
+            raise ValueError("stages > 6 refused: 2**n - 1 views grows too fast")
+        self._check_frames(left)
+        self._check_frames(right)
+        if views is None:
+            views = torch.empty(((1 << stages) - 1, self.frame_bytes), dtype=torch.uint8, device=left.device)
+        _lib.check(self._L.fvv_dense_views(self._h, ctypes.c_void_p(left.data_ptr()),
+                                           ctypes.c_void_p(right.data_ptr()), stages,
+                                           ctypes.c_void_p(views.data_ptr()), self._stream()))
+        return views
+
+    def rig(self, cams, stages: int, views=None):
+        """server/pipeline.py:254-271: cams (C, fb) -> all global views (T, fb)."""
+        import torch
+        self._check_frames(cams)
+        C = cams.shape[0]
+        total = (C - 1) * (1 << stages) + 1
+        if views is None:
+            views = torch.empty((total, self.frame_bytes), dtype=torch.uint8, device=cams.device)
+        _lib.check(self._L.fvv_rig_views(self._h, ctypes.c_void_p(cams.data_ptr()), C, stages,
+                                         ctypes.c_void_p(views.data_ptr()), self._stream()))
+        return views
+
+
+_engines: dict = {}
+_engines_lock = threading.Lock()
+
+
+def _engine(width, height, fmt, cfg: InterpConfig, max_pairs: int) -> Interpolator:
+    import torch
+    _lib.require_cuda()
+    key = (width, height, int(fmt), tuple(cfg.block_size), tuple(cfg.search_radius),
+           float(cfg.mask_epsilon), max_pairs, torch.cuda.current_device())
+    with _engines_lock:
+        eng = _engines.get(key)
+        if eng is None:
+            eng = Interpolator(width, height, fmt, cfg, max_pairs)
+            _engines[key] = eng
+        return eng
+
+
+def _to_device(frame, device=None):
+    import torch
+    host = torch.from_numpy(packed(frame))
+    return host.pin_memory().to("cuda", non_blocking=True)
+
+
+def _check_pair(left, right):
+    if (left.width, left.height, int(left.format)) != (right.width, right.height, int(right.format)):
+        raise ValueError("interpolation inputs must share size and format")
+    if left.width % 4 or left.height % 4:
+        raise ValueError("frame dimensions must be divisible by 4 for the 3-scale pyramid")
+
+
+# ---------------------------------------------------------------------------
+# Reference-facing API (interp.py:97-170)
+# ---------------------------------------------------------------------------
+def interpolate(left, right, config: InterpConfig | None = None, diagnostics: bool = False):
+    """Synthesize the midpoint view between two same-size views (interp.py:97-148).
+
+    Returns the interpolated Frame, or (Frame, InterpDiagnostics).  Bit-exact
+    with the reference on the same inputs (tests/test_gpu_parity.py).
+    """
+    cfg = config or InterpConfig()
+    _check_pair(left, right)
+    eng = _engine(left.width, left.height, left.format, cfg, 1)
+    dl = _to_device(left)[None]
+    dr = _to_device(right)[None]
+    out = eng.pairs(dl, dr)
+    res = frame_from_packed(out[0].cpu().numpy(), left.width, left.height, left.format,
+                            left.timestamp)
+    diag = InterpDiagnostics()
+    if diagnostics or cfg.refine is not None:
+        flr, frl, m = eng.diagnostics(0)
+        flr, frl, m = flr.cpu().numpy(), frl.cpu().numpy(), m.cpu().numpy()
+        W, H = left.width, left.height
+        f_lr, f_rl = FlowField(W, H, flr), FlowField(W, H, frl)
+        diag.scales.append(ScaleDiagnostics(f_lr, f_rl, mask=m))
+        diag.flow_mid_left = f_lr.scaled(-0.5)
+        diag.flow_mid_right = f_rl.scaled(-0.5)
+        diag.mask = m
+    if cfg.refine is not None:  # the reference's one plugin hook (interp.py:144-145)
+        res = cfg.refine(res, diag)
+    if diagnostics:
+        return res, diag
+    return res
+
+
+def dense_views(left, right, stages: int, config: InterpConfig | None = None) -> list:
+    """Recursive midpoint interpolation: 2**stages - 1 views, left to right (interp.py:151-170)."""
+    if stages < 1:
+        raise ValueError("stages must be >= 1")
+    if stages > 6:
+        raise ValueError("stages > 6 refused: 2**n - 1 views grows too fast")
+    cfg = config or InterpConfig()
+    _check_pair(left, right)
+    if cfg.refine is not None:
+        # the hook runs on every intermediate view, so recursion goes pair by pair
+        seq = [left, right]
+        for _ in range(stages):
+            nxt = []
+            for a, b in zip(seq, seq[1:]):
+                nxt.append(a)
+                nxt.append(interpolate(a, b, cfg))
+            nxt.append(seq[-1])
+            seq = nxt
+        return seq[1:-1]
+    eng = _engine(left.width, left.height, left.format, cfg, 1 << (stages - 1))
+    views = eng.dense(_to_device(left), _to_device(right), stages).cpu().numpy()
+    return [frame_from_packed(v, left.width, left.height, left.format, left.timestamp) for v in views]

@@ -1,0 +1,79 @@
+"""CPU-side checks of the C ABI: the library loads, exports exactly what
+include/fvv_b200.h declares, and its host-only entry points behave like the
+reference's validation (no GPU needed)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2112_10603_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "fvv_b200.h")).read()
+    return set(re.findall(r"\b(fvv_[a-z_0-9]+)\s*\(", src))
+
+
+def test_library_exports_every_declared_symbol():
+    L = _lib.load()
+    declared = header_symbols()
+    assert declared == set(_lib.EXPORTS)
+    for name in declared:
+        assert hasattr(L, name), name
+
+
+def test_frame_bytes_and_geometry():
+    L = _lib.load()
+    for w, h, fmt, n in [(1920, 1080, 1, 1920 * 1080 * 3 // 2), (448, 256, 2, 448 * 256 * 3),
+                         (64, 48, 0, 64 * 48), (5, 3, 1, 15 + 2 * 3 * 2)]:
+        d = _lib.desc(w, h, fmt)
+        assert L.fvv_frame_bytes(ctypes.byref(d)) == n
+    assert L.fvv_cluster_width(1920, 32) == 1920 + 8 * 480
+    d = _lib.desc(1920, 1080, 1)
+    # cfg3: 4 cameras, 4 stages, vps 16 -> tiles [17, 33, 33, 17]
+    widths = [L.fvv_rig_cluster_bytes(ctypes.byref(d), 4, 4, 16, c) for c in range(4)]
+    assert widths[0] == widths[3] and widths[1] == widths[2]
+    assert widths[1] == 5760 * 1080 * 3 // 2
+
+
+def test_validate_params_matches_reference_errors():
+    from paper_2112_10603_b200.interp import InterpConfig
+    L = _lib.load()
+    assert L.fvv_validate_params(ctypes.byref(_lib.params(InterpConfig()))) == 0
+    bad = _lib.InterpParams()
+    for i in range(3):
+        bad.block_size[i] = 8
+        bad.search_radius[i] = 0
+    bad.mask_epsilon = 1e-3
+    assert L.fvv_validate_params(ctypes.byref(bad)) == _lib.FVV_EINVAL
+    assert b"degenerate" in L.fvv_last_error()
+    with pytest.raises(ValueError):
+        InterpConfig(block_size=(8, 1, 8))
+    odd = _lib.params(InterpConfig(block_size=(8, 6, 8)))
+    assert L.fvv_validate_params(ctypes.byref(odd)) == _lib.FVV_EUNSUPPORTED
+
+
+def test_workspace_size_and_interp_dims():
+    from paper_2112_10603_b200.interp import InterpConfig
+    L = _lib.load()
+    p = _lib.params(InterpConfig())
+    d = _lib.desc(1920, 1080, 1)
+    s1 = L.fvv_engine_workspace_size(ctypes.byref(d), ctypes.byref(p), 1)
+    s4 = L.fvv_engine_workspace_size(ctypes.byref(d), ctypes.byref(p), 4)
+    assert s1 > 0 and s4 > 3 * s1
+    bad = _lib.desc(1922, 1080, 1)  # not divisible by 4
+    assert L.fvv_engine_workspace_size(ctypes.byref(bad), ctypes.byref(p), 1) == 0
+
+
+def test_product_path_refuses_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import paper_2112_10603_b200 as fv
+    import numpy as np
+    img = fv.gray(np.zeros((8, 8), np.uint8))
+    with pytest.raises(RuntimeError, match="CUDA"):
+        fv.interpolate(img, img)

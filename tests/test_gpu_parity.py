@@ -1,0 +1,174 @@
+"""Parity of the CUDA path (through the C ABI) with the reference.
+
+Bit-exact on every byte: uint8 output planes, f32 flows, f64 mask.  The
+checker is the golden vectors the reference produced (tests/golden/) and
+the CPU oracle (oracle/, itself pinned to those vectors by
+tests/test_oracle_golden.py) on seeded inputs.
+"""
+import numpy as np
+import pytest
+
+from conftest import golden_names, load_golden
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+FMT_NAMES = {0: "gray8", 1: "yuv420", 2: "rgb8"}
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    return torch
+
+
+def _run_pairs(torch, w, h, fmt, lefts, rights, cfg=None):
+    from paper_2112_10603_b200.interp import Interpolator
+    eng = Interpolator(w, h, fmt, cfg, max_pairs=len(lefts))
+    L = torch.from_numpy(np.stack(lefts)).cuda()
+    R = torch.from_numpy(np.stack(rights)).cuda()
+    out = eng.pairs(L, R)
+    torch.cuda.synchronize()
+    return eng, out.cpu().numpy()
+
+
+@pytest.mark.parametrize("name", golden_names("interp"))
+def test_interpolate_bit_exact_vs_golden(torch_cuda, name):
+    g = load_golden(name)
+    w, h, fmt = int(g["w"]), int(g["h"]), int(g["fmt"])
+    eng, out = _run_pairs(torch_cuda, w, h, fmt, [g["left"]], [g["right"]])
+    assert np.array_equal(out[0], g["out"]), f"{name}: {np.count_nonzero(out[0] != g['out'])} bytes differ"
+    if "flow_lr" in g:
+        flr, frl, m = eng.diagnostics(0)
+        assert np.array_equal(flr.cpu().numpy(), g["flow_lr"])
+        assert np.array_equal(frl.cpu().numpy(), g["flow_rl"])
+        assert np.array_equal(m.cpu().numpy(), g["mask"])
+
+
+def _rand_frames(rng, w, h, fmt, n):
+    fb = O.frame_bytes(w, h, fmt)
+    return [rng.integers(0, 256, fb, dtype=np.uint8) for _ in range(n)]
+
+
+def _smooth_pair(rng, w, h, fmt, shift):
+    """Smooth texture + its shifted copy (realistic flow), packed in `fmt`."""
+    from scipy.ndimage import gaussian_filter
+    big = gaussian_filter(rng.random((h + 8, w + 2 * abs(shift) + 8)) * 255.0, 3.0)
+    big = (big - big.min()) / (np.ptp(big) + 1e-9) * 230 + 12
+    a = big[4:4 + h, 4:4 + w]
+    b = big[4:4 + h, 4 + shift:4 + shift + w]
+
+    def pack(plane):
+        p = np.rint(plane).astype(np.uint8)
+        if fmt == 0:
+            return p.reshape(-1)
+        if fmt == 2:
+            return np.stack([p, np.roll(p, 3, 1), 255 - p], -1).reshape(-1)
+        c = p[::2, ::2]
+        return np.concatenate([p.reshape(-1), c.reshape(-1), (255 - c).reshape(-1)])
+    return pack(a), pack(b)
+
+
+@pytest.mark.parametrize("w,h,fmt", [(64, 48, 0), (120, 68, 1), (100, 36, 2), (200, 140, 1),
+                                     (36, 20, 0), (8, 8, 1), (4, 4, 0), (44, 12, 2)])
+def test_random_pairs_batched_vs_oracle(torch_cuda, w, h, fmt):
+    rng = np.random.default_rng(w * 1000 + h * 10 + fmt)
+    lefts, rights = [], []
+    for i in range(3):
+        a, b = _smooth_pair(rng, w, h, fmt, shift=i * 3 - 2)
+        lefts.append(a)
+        rights.append(b)
+    ln, rn = _rand_frames(rng, w, h, fmt, 2)
+    lefts.append(ln)
+    rights.append(rn)
+    _, out = _run_pairs(torch_cuda, w, h, fmt, lefts, rights)
+    for i in range(len(lefts)):
+        ref = O.interpolate(lefts[i], rights[i], w, h, fmt)
+        assert np.array_equal(out[i], ref), f"pair {i}: {np.count_nonzero(out[i] != ref)} bytes differ"
+
+
+@pytest.mark.parametrize("cfg", [dict(block_size=(4, 8, 2), search_radius=(6, 3, 1)),
+                                 dict(block_size=(8, 4, 4), search_radius=(3, 2, 5)),
+                                 dict(search_radius=(15, 6, 3), mask_epsilon=0.25)])
+def test_nondefault_config_vs_oracle(torch_cuda, cfg):
+    from paper_2112_10603_b200.interp import InterpConfig
+    c = InterpConfig(**cfg)
+    rng = np.random.default_rng(7)
+    w, h, fmt = 96, 64, 1
+    a, b = _smooth_pair(rng, w, h, fmt, 5)
+    _, out = _run_pairs(torch_cuda, w, h, fmt, [a], [b], c)
+    ref = O.interpolate(a, b, w, h, fmt, block_size=c.block_size, search_radius=c.search_radius,
+                        eps=c.mask_epsilon)
+    assert np.array_equal(out[0], ref)
+
+
+def test_dense_views_vs_golden(torch_cuda):
+    from paper_2112_10603_b200.interp import Interpolator
+    g = load_golden("dense3_yuv420_64x48")
+    eng = Interpolator(64, 48, 1, max_pairs=4)
+    v = eng.dense(torch_cuda.from_numpy(g["left"]).cuda(), torch_cuda.from_numpy(g["right"]).cuda(), 3)
+    assert np.array_equal(v.cpu().numpy(), g["out"])
+
+
+def test_rig_views_and_clusters_vs_golden(torch_cuda):
+    from paper_2112_10603_b200.interp import Interpolator
+    from paper_2112_10603_b200.cluster import rig_clusters, downscale_device
+    g = load_golden("rig3_s2_vps2_yuv420_64x48")
+    w, h, fmt, stages, vps = 64, 48, 1, int(g["stages"]), int(g["vps"])
+    cams = torch_cuda.from_numpy(g["cams"]).cuda()
+    eng = Interpolator(w, h, fmt, max_pairs=2 * (1 << (stages - 1)))
+    views = eng.rig(cams, stages)
+    assert np.array_equal(views.cpu().numpy(), g["views"])
+    q = downscale_device(views, w, h, fmt, 4)
+    assert np.array_equal(q.cpu().numpy(), g["quarters"])
+    out, sizes = rig_clusters(views, w, h, fmt, 3, stages, vps)
+    assert list(sizes) == list(g["cluster_sizes"])
+    assert np.array_equal(out.cpu().numpy(), g["clusters"])
+
+
+def test_reference_api_roundtrip(torch_cuda):
+    """interpolate()/dense_views() on host Frames, as the reference is called."""
+    import paper_2112_10603_b200 as fv
+    g = load_golden("scene_yuv420_96x72")
+    L = fv.frame_from_packed(g["left"], 96, 72, 1)
+    R = fv.frame_from_packed(g["right"], 96, 72, 1)
+    out, diag = fv.interpolate(L, R, diagnostics=True)
+    assert np.array_equal(fv.packed(out), g["out"])
+    assert np.array_equal(diag.mask, g["mask"])
+    assert diag.mask.min() >= 0.0 and diag.mask.max() <= 1.0
+    views = fv.dense_views(L, R, 2)
+    ref = O.dense_views(g["left"], g["right"], 96, 72, 1, 2)
+    assert np.array_equal(np.stack([fv.packed(v) for v in views]), ref)
+    seen = []
+    cfg = fv.InterpConfig(refine=lambda f, d: (seen.append(d), f)[1])
+    fv.interpolate(L, R, cfg)
+    assert len(seen) == 1 and seen[0].mask is not None
+
+
+def test_identity_and_errors(torch_cuda):
+    import paper_2112_10603_b200 as fv
+    rng = np.random.default_rng(3)
+    img = fv.gray(rng.integers(0, 256, (48, 64), dtype=np.uint8))
+    assert np.array_equal(fv.interpolate(img, img).planes[0], img.planes[0])
+    with pytest.raises(ValueError):
+        fv.interpolate(img, fv.gray(np.zeros((48, 60), np.uint8)))
+    with pytest.raises(ValueError):
+        fv.interpolate(fv.gray(np.zeros((30, 64), np.uint8)), fv.gray(np.zeros((30, 64), np.uint8)))
+    with pytest.raises(ValueError):
+        fv.dense_views(img, img, 0)
+    with pytest.raises(ValueError):
+        fv.dense_views(img, img, 7)
+
+
+def test_full_1080p_pair_vs_oracle(torch_cuda):
+    """BASELINE config size: one 1920x1080 YUV420 pair, bit-exact to the oracle."""
+    rng = np.random.default_rng(1080)
+    w, h, fmt = 1920, 1080, 1
+    a, b = _smooth_pair(rng, w, h, fmt, 9)
+    _, out = _run_pairs(torch_cuda, w, h, fmt, [a, b], [b, a])
+    ref = O.interpolate(a, b, w, h, fmt)
+    assert np.array_equal(out[0], ref), f"{np.count_nonzero(out[0] != ref)} bytes differ"
+    ref2 = O.interpolate(b, a, w, h, fmt)
+    assert np.array_equal(out[1], ref2)
