@@ -1,0 +1,471 @@
+#!/usr/bin/env python
+"""Benchmark of the dense view-synthesis hot path (BASELINE.json metric:
+synthesized virtual views/s at 1080p; per-rig-frame latency).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl b200|reference]
+
+One step = one rig frame per rank: every dense view of every camera gap
+(recursive midpoints, server/pipeline.py:254-271) plus every cluster frame
+(server/pipeline.py:273-292).  Default workload = BASELINE config 4 (8-camera
+1080p YUV420 rig, 7 gaps x 15 views = 105 views, 8 cluster frames), which
+fits one B200.  Multi-GPU: one process per GPU (torchrun), each rank owns
+its own rig frames (frame sharding, weak scaling) and the cluster frames are
+gathered to the encoder-feeding rank 0 with NCCL send/recv.
+
+`--impl reference` times the reference algorithm's CPU implementation (the
+oracle port in oracle/, all host threads) on a bounded sample of the same
+workload: each step = one interpolate() at the config's resolution.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "cfg1": dict(desc="single camera pair 256x448 RGB, 1 midpoint virtual view", W=448, H=256, fmt=2,
+                 cams=2, stages=1, vps=0),
+    "cfg2": dict(desc="single camera pair 1920x1080, 7 dense intermediate views per pair", W=1920, H=1080,
+                 fmt=1, cams=2, stages=3, vps=0),
+    "cfg3": dict(desc="4-camera linear rig 1920x1080, 3 pairs x 15 intermediate views, tiled output frame",
+                 W=1920, H=1080, fmt=1, cams=4, stages=4, vps=16),
+    "cfg4": dict(desc="8-camera arc rig 1920x1080, 7 pairs x 15 views, pairs sharded across B200s",
+                 W=1920, H=1080, fmt=1, cams=8, stages=4, vps=16),
+    "cfg5": dict(desc="16-camera rig 3840x2160, 15 pairs x 31 views, batched multi-frame live stream",
+                 W=3840, H=2160, fmt=1, cams=16, stages=5, vps=32),
+}
+FMT_NAME = {0: "gray8", 1: "yuv420", 2: "rgb8"}
+METRIC = "synthesized virtual views/sec at 1080p"
+
+
+# ---------------------------------------------------------------------------
+# synthetic multi-view input (deterministic parallax scene, numpy)
+# ---------------------------------------------------------------------------
+def _texture(rng, h, w):
+    from scipy.ndimage import gaussian_filter
+    t = gaussian_filter(rng.random((h, w)), 6.0) * 0.6 + gaussian_filter(rng.random((h, w)), 1.5) * 0.4
+    t = (t - t.min()) / (np.ptp(t) + 1e-12)
+    return 28.0 + 190.0 * t
+
+
+def synth_rig(W, H, fmt, cams, seed=42):
+    """cams packed frames of a planar-parallax scene: far background plus two
+    near sprites, disparities growing with camera index."""
+    rng = np.random.default_rng(seed)
+    d_bg, d_sp = max(1, round(1.5 * W / 640)), [round(6 * W / 640), round(4 * W / 640)]
+    pad = (cams + 1) * max(d_sp) + 8
+    bg = _texture(rng, H, W + pad)
+    sprites = []
+    for k, d in enumerate(d_sp):
+        sh, sw = H // (3 + k), W // (5 + k)
+        sprites.append((_texture(rng, sh, sw) * 0.8 + 30, d, H // 4 + k * H // 3, W // 4 + k * W // 3))
+    frames = []
+    for c in range(cams):
+        y = bg[:, c * d_bg:c * d_bg + W].copy()
+        for tex, d, top, left in sprites:
+            x0 = left - c * d
+            sh, sw = tex.shape
+            xs, xe = max(0, x0), min(W, x0 + sw)
+            if xe > xs:
+                y[top:top + sh, xs:xe] = tex[:, xs - x0:xe - x0]
+        yp = np.clip(np.rint(y), 0, 255).astype(np.uint8)
+        if fmt == 0:
+            frames.append(yp.reshape(-1))
+        elif fmt == 2:
+            rgb = np.stack([yp, np.clip(yp.astype(int) + 20, 0, 255), 255 - yp], -1).astype(np.uint8)
+            frames.append(rgb.reshape(-1))
+        else:
+            c2 = yp[::2, ::2].astype(np.int32)
+            u = np.clip(128 + (c2 - 128) // 5, 0, 255).astype(np.uint8)
+            v = np.clip(128 - (c2 - 128) // 6, 0, 255).astype(np.uint8)
+            frames.append(np.concatenate([yp.reshape(-1), u.reshape(-1), v.reshape(-1)]))
+    return np.stack(frames)
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md clocks line)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# algorithmic work per kernel class
+# ---------------------------------------------------------------------------
+def kernel_figures(cfg, npairs_total):
+    """{class: (bound, unit, algorithmic amount over all launches of one step)}"""
+    W, H, fmt = cfg["W"], cfg["H"], cfg["fmt"]
+    bframe = {0: 1.0, 1: 1.5, 2: 3.0}[fmt] * W * H
+    r = (12, 4, 2)
+    lv = [(W // 4, H // 4), (W // 2, H // 2), (W, H)]
+    sad = [2 * (2 * r[s] + 1) ** 2 * lv[s][0] * lv[s][1] * npairs_total for s in range(3)]
+    return {
+        "k_sad<0>": ("int", "Gop/s", sad[0]),
+        "k_sad<1>": ("int", "Gop/s", sad[1]),
+        "k_sad<2>": ("int", "Gop/s", sad[2]),
+        # warp + mask + blend: 2 source frames read, 1 view written (compulsory)
+        "k_mask_prod": ("hbm", "GB/s", 2 * bframe * npairs_total),
+        "k_rowscan": ("hbm", "GB/s", bframe * npairs_total),
+        "k_warpq<2>": ("hbm", "GB/s", (2 * W * H + 2 * 2 * W * H + 16 * W * H / 4) * npairs_total),
+    }
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle port) -- cpu_baseline and --impl reference
+# ---------------------------------------------------------------------------
+def cpu_interp_rate(cfg, budget_s=10.0, min_reps=1):
+    from oracle import oracle as O
+    O.set_threads(os.cpu_count() or 1)
+    W, H, fmt = cfg["W"], cfg["H"], cfg["fmt"]
+    fr = synth_rig(W, H, fmt, 2, seed=7)
+    O.interpolate(fr[0], fr[1], W, H, fmt)  # warm (first-touch, thread pool)
+    n, t0 = 0, time.perf_counter()
+    while n < min_reps or time.perf_counter() - t0 < budget_s:
+        O.interpolate(fr[0], fr[1], W, H, fmt)
+        n += 1
+    dt = time.perf_counter() - t0
+    return n / dt, n, dt, O.num_threads()
+
+
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+    O.set_threads(os.cpu_count() or 1)
+    W, H, fmt = cfg["W"], cfg["H"], cfg["fmt"]
+    fr = synth_rig(W, H, fmt, 2, seed=7)
+    for _ in range(args.warmup):
+        O.interpolate(fr[0], fr[1], W, H, fmt)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.interpolate(fr[0], fr[1], W, H, fmt)
+    dt = time.perf_counter() - t0
+    rate = args.steps / dt
+    sample = f"{args.steps} x interpolate() {W}x{H} {FMT_NAME[fmt]} (one view each) from {args.config}"
+    line = {
+        "metric": METRIC, "value": rate, "unit": "views/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8/i32/f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": args.config, "desc": cfg["desc"], "width": W, "height": H,
+                   "format": FMT_NAME[fmt], "step": "one interpolate() per step (bounded CPU sample)"},
+        "cpu_baseline": {"value": rate, "unit": "views/s", "cores": O.num_threads(), "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": rate, "unit": "views/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+def run_b200(args, cfg, rank, world, local_rank):
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+    from paper_2112_10603_b200 import _lib
+    from paper_2112_10603_b200.cluster import rig_cluster_sizes, rig_clusters
+    from paper_2112_10603_b200.interp import Interpolator
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    W, H, fmt, C, S, vps = cfg["W"], cfg["H"], cfg["fmt"], cfg["cams"], cfg["stages"], cfg["vps"]
+    step_views = (C - 1) * ((1 << S) - 1)
+    total_views = (C - 1) * (1 << S) + 1
+    max_pairs = (C - 1) * (1 << (S - 1))
+    npairs_total = step_views  # interpolations per rig frame
+    eng = Interpolator(W, H, fmt, max_pairs=max_pairs, device=dev)
+    fb = eng.frame_bytes
+
+    host_cams = torch.from_numpy(synth_rig(W, H, fmt, C, seed=42 + rank)).pin_memory()
+    cams = host_cams.to(dev)
+    views = torch.empty((total_views, fb), dtype=torch.uint8, device=dev)
+    if vps:
+        sizes = rig_cluster_sizes(W, H, fmt, C, S, vps)
+        clusters = torch.empty(sum(sizes), dtype=torch.uint8, device=dev)
+        result = clusters
+    else:
+        result = views
+    host_out = torch.empty(result.numel(), dtype=torch.uint8).pin_memory()
+
+    def compute():
+        eng.rig(cams, S, views)
+        if vps:
+            rig_clusters(views, W, H, fmt, C, S, vps, out=clusters)
+
+    gather_bufs = None
+    if world > 1 and rank == 0:
+        gather_bufs = [torch.empty_like(result) for _ in range(world - 1)]
+
+    def gather():
+        # cluster frames of every rank -> the encoder-feeding rank 0 (NCCL over NVLink)
+        if world == 1:
+            return
+        ops = []
+        if rank == 0:
+            for src in range(1, world):
+                ops.append(dist.P2POp(dist.irecv, gather_bufs[src - 1], src))
+        else:
+            ops.append(dist.P2POp(dist.isend, result, 0))
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.synchronize()
+    # capture one rig frame of compute as a CUDA graph (kills ~50 launches/step of host overhead)
+    graph = None
+    if not args.no_graph:
+        with torch.cuda.stream(stream):
+            compute()  # first run outside capture (lazy attributes, allocator)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            compute()
+        torch.cuda.synchronize()
+
+    def step():
+        if graph is not None:
+            graph.replay()
+        else:
+            compute()
+        gather()
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(args.warmup, 3)):
+            step()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- timed region: device-resident inputs --------------------------------
+    clocks = ClockSampler(local_rank)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    with torch.cuda.stream(stream):
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for _ in range(args.steps):
+            step()
+        t_end.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    barrier()
+    ms = max_over_ranks(t_start.elapsed_time(t_end))
+    ms_per_step = ms / args.steps
+    value = world * step_views * args.steps / (ms / 1e3)
+
+    # ---- e2e: host buffers through the public API, copies inside the region --
+    e2e_steps = max(3, args.steps // 2)
+    barrier()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            cams.copy_(host_cams, non_blocking=True)
+            step()
+            host_out.copy_(result, non_blocking=True)
+        e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1))
+    e2e_value = world * step_views * e2e_steps / (e2e_ms / 1e3)
+
+    if rank != 0:
+        return 0
+
+    # ---- per-kernel live timing (CUDA events around every stage kernel) -----
+    prof_steps = 3
+    L = _lib.load()
+    _lib.check(L.fvv_profile_enable(eng._h, 4096))
+    with torch.cuda.stream(stream):
+        for _ in range(prof_steps):
+            compute()
+    torch.cuda.synchronize()
+    n = 10
+    ms_k = (ctypes.c_double * n)()
+    cnt_k = (ctypes.c_int * n)()
+    _lib.check(L.fvv_profile_read(eng._h, ms_k, cnt_k, n))
+    L.fvv_profile_enable(eng._h, 0)
+    per_class = {L.fvv_kernel_class_name(i).decode(): (ms_k[i] / prof_steps, cnt_k[i] // prof_steps)
+                 for i in range(n)}
+    tile_ms = 0.0
+    if vps:
+        with torch.cuda.stream(stream):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(prof_steps):
+                rig_clusters(views, W, H, fmt, C, S, vps, out=clusters)
+            b.record(stream)
+        torch.cuda.synchronize()
+        tile_ms = a.elapsed_time(b) / prof_steps
+        per_class["k_rig_clusters"] = (tile_ms, 1)
+    step_kernel_ms = sum(v[0] for v in per_class.values())
+    figs = kernel_figures(cfg, npairs_total)
+    dom = max((k for k in per_class if k in figs), key=lambda k: per_class[k][0])
+    bound, unit, amount = figs[dom]
+    peaks, peak_src = measured_peaks()
+    dom_ms = per_class[dom][0]
+    if bound == "hbm":
+        achieved = amount / (dom_ms / 1e3) / 1e9
+        peak = float(peaks["hbm_gbs"])
+        peak_note = f"{peak_src} HBM copy bandwidth (MEASURED_PEAKS.json)"
+    else:
+        achieved = amount / (dom_ms / 1e3) / 1e9
+        sm_mhz = clk.get("sm_mhz") or float(peaks.get("sm_max_mhz", 1965.0))
+        # issue-rate ceiling for packed-u16 SAD: 148 SMs x 128 lanes/clk x 2 diffs per lane
+        peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e9
+        peak_note = ("derived: 148 SMs x 128 lanes x 2 (u16x2) abs-diffs/clk at the median SM clock "
+                     "under load; no measured INT peak in MEASURED_PEAKS.json")
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get(args.config, {}).get(dom)
+    except OSError:
+        pass
+    roofline = {"bound": bound, "kernel": dom, "achieved": achieved, "peak": peak, "unit": unit,
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_note,
+                "kernel_ms_per_step": dom_ms, "kernel_share_of_step": dom_ms / step_kernel_ms,
+                "per_kernel_ms_per_step": {k: round(v[0], 4) for k, v in per_class.items()}}
+
+    launches_per_step = sum(v[1] for v in per_class.values())
+    # SAD classes launch a second (ragged-column) kernel when the level width is not a multiple of 8
+    for s, (lw, _lh) in enumerate([(W // 4, H // 4), (W // 2, H // 2), (W, H)]):
+        if lw % 8:
+            launches_per_step += per_class[f"k_sad<{s}>"][1]
+    gpu_launches = launches_per_step * args.steps
+
+    # CPU baseline: oracle port on this box's host cores, bounded sample
+    rate, reps, dt, threads = cpu_interp_rate(cfg, budget_s=args.cpu_budget)
+    cpu = {"value": rate, "unit": "views/s", "cores": threads, "kind": "port",
+           "sample": f"{reps} x interpolate() {W}x{H} {FMT_NAME[fmt]} in {dt:.1f}s (oracle/, C port of "
+                     f"the reference path, {threads} threads)"}
+
+    h2d = host_cams.numel()
+    d2h = host_out.numel()
+    line = {
+        "metric": METRIC, "value": value, "unit": "views/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8/i32/f64", "data": "synthetic",
+        "config": {"workload": args.config, "desc": cfg["desc"], "width": W, "height": H,
+                   "format": FMT_NAME[fmt], "cameras": C, "stages": S, "views_per_side": vps,
+                   "views_per_rig_frame": step_views, "rig_frame_latency_ms": ms_per_step,
+                   "parallelism": f"frame-sharded x{world}" + (" + NCCL gather to rank 0" if world > 1 else ""),
+                   "cuda_graph": graph is not None,
+                   "l2": "working set > L2 (views %.0f MB + workspace %.0f MB per rank)" % (
+                       views.numel() / 1e6, eng.workspace_bytes / 1e6)},
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "views/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / e2e_steps},
+        "gpu_launches": gpu_launches,
+        "clocks": clk,
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, cfg, rank, world)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        return run_b200(args, cfg, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

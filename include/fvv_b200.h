@@ -93,6 +93,17 @@ int fvv_interpolate_pairs(fvv_engine* engine, const uint8_t* const* left,
 int fvv_interp_diagnostics(fvv_engine* engine, int pair, float* flow_lr, float* flow_rl,
                            double* mask, void* stream);
 
+/* Per-kernel timing of the stage kernels (bench.py's roofline figure):
+ * while enabled, every stage-kernel launch is bracketed by a cudaEvent pair
+ * on the launching stream (at most `capacity` launches are recorded).
+ * fvv_profile_read synchronises on the recorded events, returns the summed
+ * milliseconds and launch counts per kernel class and resets the record.
+ * capacity <= 0 disables.  Not for use under CUDA-graph capture. */
+#define FVV_NUM_KERNEL_CLASSES 10
+int fvv_profile_enable(fvv_engine* engine, int capacity);
+int fvv_profile_read(fvv_engine* engine, double* ms, int* launches, int nclasses);
+const char* fvv_kernel_class_name(int kernel_class);
+
 /* interp.py:151-170: views = (2^stages - 1) frames, contiguous, left -> right.
  * Requires max_pairs >= 2^(stages-1). */
 int fvv_dense_views(fvv_engine* engine, const uint8_t* left, const uint8_t* right, int stages,

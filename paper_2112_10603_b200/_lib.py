@@ -21,6 +21,7 @@ EXPORTS = (
     "fvv_engine_max_pairs", "fvv_interpolate_pairs", "fvv_interp_diagnostics",
     "fvv_dense_views", "fvv_rig_views", "fvv_downscale", "fvv_cluster_width",
     "fvv_assemble_cluster", "fvv_rig_cluster_bytes", "fvv_rig_clusters",
+    "fvv_profile_enable", "fvv_profile_read", "fvv_kernel_class_name",
 )
 
 
@@ -74,6 +75,9 @@ def load():
         "fvv_assemble_cluster": (I, [pd, P, PP, I, P, P]),
         "fvv_rig_cluster_bytes": (Z, [pd, I, I, I, I]),
         "fvv_rig_clusters": (I, [pd, I, I, I, P, P, P]),
+        "fvv_profile_enable": (I, [P, I]),
+        "fvv_profile_read": (I, [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I), I]),
+        "fvv_kernel_class_name": (ctypes.c_char_p, [I]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -14,7 +14,7 @@
 namespace fvv {
 cudaError_t run_interp_stage(const Geometry& g, const PairTable& pt, uint8_t* ws, const Planes& P,
                              const int16_t* const* rank_of, const int16_t* const* cand_of_rank,
-                             int npairs, double* mask_out, cudaStream_t st);
+                             int npairs, double* mask_out, Prof* prof, cudaStream_t st);
 cudaError_t run_diag(const Geometry& g, const PairTable& pt, uint8_t* ws, const Planes& P, int pair,
                      float* flow_lr, float* flow_rl, double* mask, cudaStream_t st);
 cudaError_t launch_downscale(int W, int H, int fmt, const uint8_t* frames, int n, int f,
@@ -157,6 +157,16 @@ struct fvv_engine {
     const int16_t* cand_of_rank[3];
     PairTable last;  // frame pointers of the most recent batch (diagnostics)
     int last_npairs;
+    Prof prof;
+    bool profiling = false;
+    ~fvv_engine() { free_prof(); }
+    void free_prof() {
+        for (int i = 0; i < 2 * prof.capacity; i++) cudaEventDestroy(prof.ev[i]);
+        delete[] prof.ev;
+        delete[] prof.cls;
+        prof = Prof();
+        profiling = false;
+    }
 };
 
 extern "C" {
@@ -264,12 +274,55 @@ static int run_pairs(fvv_engine* e, const uint8_t* const* L, const uint8_t* cons
             pt.out[i] = O[b + i];
         }
         cudaError_t ce = run_interp_stage(e->g, pt, e->slots, e->P, e->rank_of, e->cand_of_rank, n,
-                                          nullptr, st);
+                                          nullptr, e->profiling ? &e->prof : nullptr, st);
         if (ce != cudaSuccess) return cuda_fail(ce, "interpolate");
         e->last = pt;
         e->last_npairs = n;
     }
     return FVV_OK;
+}
+
+int fvv_profile_enable(fvv_engine* e, int capacity) {
+    if (!e) return fail(FVV_EINVAL, "null engine");
+    e->free_prof();
+    if (capacity <= 0) return FVV_OK;
+    e->prof.ev = new cudaEvent_t[2 * capacity];
+    e->prof.cls = new int[capacity];
+    for (int i = 0; i < 2 * capacity; i++) {
+        cudaError_t ce = cudaEventCreate(&e->prof.ev[i]);
+        if (ce != cudaSuccess) {
+            e->prof.capacity = i / 2;
+            e->free_prof();
+            return cuda_fail(ce, "fvv_profile_enable");
+        }
+    }
+    e->prof.capacity = capacity;
+    e->prof.n = 0;
+    e->profiling = true;
+    return FVV_OK;
+}
+
+int fvv_profile_read(fvv_engine* e, double* ms, int* launches, int nclasses) {
+    if (!e || !ms || !launches) return fail(FVV_EINVAL, "null argument");
+    for (int c = 0; c < nclasses; c++) { ms[c] = 0.0; launches[c] = 0; }
+    for (int i = 0; i < e->prof.n; i++) {
+        cudaError_t ce = cudaEventSynchronize(e->prof.ev[2 * i + 1]);
+        if (ce != cudaSuccess) return cuda_fail(ce, "fvv_profile_read");
+        float t = 0.f;
+        ce = cudaEventElapsedTime(&t, e->prof.ev[2 * i], e->prof.ev[2 * i + 1]);
+        if (ce != cudaSuccess) return cuda_fail(ce, "fvv_profile_read");
+        const int c = e->prof.cls[i];
+        if (c < nclasses) { ms[c] += t; launches[c] += 1; }
+    }
+    e->prof.n = 0;
+    return FVV_OK;
+}
+
+const char* fvv_kernel_class_name(int c) {
+    static const char* names[KC_COUNT] = {"k_pyramid", "k_sad<0>", "k_flow<0>", "k_warpq<1>",
+                                          "k_sad<1>", "k_flow<1>", "k_warpq<2>", "k_sad<2>",
+                                          "k_mask_prod", "k_rowscan"};
+    return c >= 0 && c < KC_COUNT ? names[c] : "";
 }
 
 int fvv_interpolate_pairs(fvv_engine* e, const uint8_t* const* left, const uint8_t* const* right,

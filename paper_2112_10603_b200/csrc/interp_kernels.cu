@@ -694,8 +694,8 @@ static cudaError_t run_sad(const Geometry& g, const PairTable& pt, uint8_t* ws, 
     const bool fast = L.block == 8;
     const int full_cols = fast ? L.w / 8 : 0;  // block columns with 8 valid columns
     cudaError_t e;
-    // interior: rows may be ragged only in the last block row -> FULL8 path
-    // handles the row guard itself; ragged columns go to the general path.
+    // full block columns take the FULL8 path (it guards ragged rows itself);
+    // a ragged last block column or other block sizes take the general path
     if (full_cols > 0) {
         sl.bx_begin = 0;
         sl.bx_end = full_cols;
@@ -713,43 +713,53 @@ static cudaError_t run_sad(const Geometry& g, const PairTable& pt, uint8_t* ws, 
 
 cudaError_t run_interp_stage(const Geometry& g, const PairTable& pt, uint8_t* ws, const Planes& P,
                              const int16_t* const* rank_of, const int16_t* const* cand_of_rank,
-                             int npairs, double* mask_out, cudaStream_t st) {
-    cudaError_t e;
-    {
-        dim3 blk(32, 8);
-        dim3 grd((g.lv[0].w + 31) / 32, (g.lv[0].h + 7) / 8, 2 * npairs);
-        k_pyramid<<<grd, blk, 0, st>>>(g, pt, ws, P);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    }
-    if ((e = run_sad<0>(g, pt, ws, P, rank_of[0], cand_of_rank[0], npairs, st)) != cudaSuccess)
-        return e;
-    {
-        dim3 grd((g.lv[0].w * g.lv[0].h + 255) / 256, 1, 2 * npairs);
-        k_flow<0><<<grd, 256, 0, st>>>(g, ws, P);
-        dim3 grd1((g.lv[1].w * g.lv[1].h + 255) / 256, 1, 2 * npairs);
-        k_warpq<1><<<grd1, 256, 0, st>>>(g, pt, ws, P);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    }
-    if ((e = run_sad<1>(g, pt, ws, P, rank_of[1], cand_of_rank[1], npairs, st)) != cudaSuccess)
-        return e;
-    {
-        dim3 grd((g.lv[1].w * g.lv[1].h + 255) / 256, 1, 2 * npairs);
-        k_flow<1><<<grd, 256, 0, st>>>(g, ws, P);
-        dim3 grd2((g.lv[2].w * g.lv[2].h + 255) / 256, 1, 2 * npairs);
-        k_warpq<2><<<grd2, 256, 0, st>>>(g, pt, ws, P);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    }
-    if ((e = run_sad<2>(g, pt, ws, P, rank_of[2], cand_of_rank[2], npairs, st)) != cudaSuccess)
-        return e;
-    {
-        dim3 grd((g.W + kTW - 1) / kTW, (g.H + kTH - 1) / kTH, npairs);
-        k_mask_prod<<<grd, 256, 0, st>>>(g, pt, ws, P);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        dim3 grd2((g.H + kRB - 1) / kRB, npairs);
-        k_rowscan<<<grd2, 128, 0, st>>>(g, pt, ws, P, 0, true, mask_out);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    }
-    return cudaSuccess;
+                             int npairs, double* mask_out, Prof* prof, cudaStream_t st) {
+    cudaError_t e = cudaSuccess;
+    auto B = [&](int c) { if (prof) prof->begin(c, st); };
+    auto E = [&]() { if (prof) prof->end(st); return cudaGetLastError(); };
+    const int n0 = g.lv[0].w * g.lv[0].h, n1 = g.lv[1].w * g.lv[1].h, n2 = g.lv[2].w * g.lv[2].h;
+
+    B(KC_PYRAMID);
+    k_pyramid<<<dim3((g.lv[0].w + 31) / 32, (g.lv[0].h + 7) / 8, 2 * npairs), dim3(32, 8), 0, st>>>(
+        g, pt, ws, P);
+    if ((e = E()) != cudaSuccess) return e;
+
+    B(KC_SAD0);
+    e = run_sad<0>(g, pt, ws, P, rank_of[0], cand_of_rank[0], npairs, st);
+    if (e != cudaSuccess || (e = E()) != cudaSuccess) return e;
+
+    B(KC_FLOW0);
+    k_flow<0><<<dim3((n0 + 255) / 256, 1, 2 * npairs), 256, 0, st>>>(g, ws, P);
+    if ((e = E()) != cudaSuccess) return e;
+
+    B(KC_WARPQ1);
+    k_warpq<1><<<dim3((n1 + 255) / 256, 1, 2 * npairs), 256, 0, st>>>(g, pt, ws, P);
+    if ((e = E()) != cudaSuccess) return e;
+
+    B(KC_SAD1);
+    e = run_sad<1>(g, pt, ws, P, rank_of[1], cand_of_rank[1], npairs, st);
+    if (e != cudaSuccess || (e = E()) != cudaSuccess) return e;
+
+    B(KC_FLOW1);
+    k_flow<1><<<dim3((n1 + 255) / 256, 1, 2 * npairs), 256, 0, st>>>(g, ws, P);
+    if ((e = E()) != cudaSuccess) return e;
+
+    B(KC_WARPQ2);
+    k_warpq<2><<<dim3((n2 + 255) / 256, 1, 2 * npairs), 256, 0, st>>>(g, pt, ws, P);
+    if ((e = E()) != cudaSuccess) return e;
+
+    B(KC_SAD2);
+    e = run_sad<2>(g, pt, ws, P, rank_of[2], cand_of_rank[2], npairs, st);
+    if (e != cudaSuccess || (e = E()) != cudaSuccess) return e;
+
+    B(KC_MASK_PROD);
+    k_mask_prod<<<dim3((g.W + kTW - 1) / kTW, (g.H + kTH - 1) / kTH, npairs), 256, 0, st>>>(g, pt,
+                                                                                         ws, P);
+    if ((e = E()) != cudaSuccess) return e;
+
+    B(KC_ROWSCAN);
+    k_rowscan<<<dim3((g.H + kRB - 1) / kRB, npairs), 128, 0, st>>>(g, pt, ws, P, 0, true, mask_out);
+    return E();
 }
 
 // diagnostics: final flows (InterpDiagnostics.scales[-1].flow_lr/rl) and mask
