@@ -246,7 +246,7 @@ def run_b200(args, cfg, rank, world, local_rank):
         result = clusters
     else:
         result = views
-    host_out = torch.empty(result.numel(), dtype=torch.uint8).pin_memory()
+    host_out = torch.empty(result.shape, dtype=torch.uint8).pin_memory()
 
     def compute():
         eng.rig(cams, S, views)

@@ -95,6 +95,15 @@ void make_geometry(const fvv_frame_desc* d, const fvv_interp_params* p, Geometry
     }
     g->eps = p->mask_epsilon;
     g->eps2 = 2.0 * p->mask_epsilon;
+    // exact fixed-point units (fvv_device.cuh)
+    for (int s = 0; s < 3; s++) {
+        int lb = 0;
+        while ((1 << lb) < 2 * p->block_size[s]) lb++;
+        g->rb[s] = 2 * lb;
+    }
+    g->fb[0] = g->rb[0];
+    g->fb[1] = std::max(g->fb[0] + 3, g->rb[1]);
+    g->fb[2] = std::max(g->fb[1] + 3, g->rb[2]);
 }
 
 // workspace = [header: candidate tables][pair slot 0][pair slot 1]...

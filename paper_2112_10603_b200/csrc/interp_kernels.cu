@@ -294,7 +294,8 @@ __global__ void __launch_bounds__(256) k_sad(Geometry g, PairTable pt, uint8_t* 
 
 // ---------------------------------------------------------------------------
 // k_flow<L>: flow_L = base + f32(block_to_pixel(offsets))  (flow.py:122-129)
-// base = 0 at level 0, f32(2 * upscale(flow_{L-1})) otherwise.
+// base = 0 at level 0, f32(2 * upscale(flow_{L-1})) otherwise.  Computed in
+// exact fixed point (units 2^-fb[L]); equal to the reference's f32 values.
 // ---------------------------------------------------------------------------
 template <int LEVEL>
 __global__ void k_flow(Geometry g, uint8_t* __restrict__ ws, Planes P) {
@@ -303,20 +304,25 @@ __global__ void k_flow(Geometry g, uint8_t* __restrict__ ws, Planes P) {
     const int pair = blockIdx.z >> 1, d = blockIdx.z & 1;
     if (i >= L.w * L.h) return;
     const int y = i / L.w, x = i - (i / L.w) * L.w;
-    const float2 res = block_to_pixel_at(cplane<BlockHit>(ws, P, P.hit[LEVEL][d], pair), L.nby,
-                                         L.nbx, L.block, y, x);
-    float2 base = make_float2(0.0f, 0.0f);
+    const int2 res = b2p_fixed(cplane<BlockHit>(ws, P, P.hit[LEVEL][d], pair), L.nby, L.nbx, L.block,
+                               y, x);
+    const int rs = g.fb[LEVEL] - g.rb[LEVEL];
+    int2 f = make_int2(res.x << rs, res.y << rs);
     if (LEVEL > 0) {
         const Level Lp = g.lv[LEVEL - 1];
-        base = upscale_at(cplane<float2>(ws, P, P.flow0[d], pair), Lp.h, Lp.w, L.h, L.w, y, x);
+        const int2 base = up2_fixed(cplane<int2>(ws, P, P.flow0[d], pair), Lp.h, Lp.w, y, x);
+        const int bs = g.fb[LEVEL] - (g.fb[LEVEL - 1] + 3);
+        f.x += base.x << bs;
+        f.y += base.y << bs;
     }
-    float2 f = make_float2(__fadd_rn(base.x, res.x), __fadd_rn(base.y, res.y));
-    plane<float2>(ws, P, LEVEL == 0 ? P.flow0[d] : P.flow1[d], pair)[i] = f;
+    plane<int2>(ws, P, LEVEL == 0 ? P.flow0[d] : P.flow1[d], pair)[i] = f;
 }
 
 // ---------------------------------------------------------------------------
 // k_warpq<L> (L = 1, 2): pad_q source = rint(8 * warp_plane(target, base))
 // (flow.py:123-124 then :78); the edge padding is applied by the search.
+// Exact integer bilinear: base in units 2^-(fb[L-1]+3), level-1 samples in
+// units 1/4 (s4), level-2 samples integral (luma).
 // ---------------------------------------------------------------------------
 template <int LEVEL>
 __global__ void k_warpq(Geometry g, PairTable pt, uint8_t* __restrict__ ws, Planes P) {
@@ -326,23 +332,33 @@ __global__ void k_warpq(Geometry g, PairTable pt, uint8_t* __restrict__ ws, Plan
     const int pair = blockIdx.z >> 1, d = blockIdx.z & 1;
     if (i >= L.w * L.h) return;
     const int y = i / L.w, x = i - (i / L.w) * L.w;
-    const float2* prev = cplane<float2>(ws, P, LEVEL == 1 ? P.flow0[d] : P.flow1[d], pair);
-    const float2 base = upscale_at(prev, Lp.h, Lp.w, L.h, L.w, y, x);
-    double v;
+    const int2* prev = cplane<int2>(ws, P, LEVEL == 1 ? P.flow0[d] : P.flow1[d], pair);
+    const int2 base = up2_fixed(prev, Lp.h, Lp.w, y, x);
+    const int vb = g.fb[LEVEL - 1] + 3;
+    const int w = L.w;
+    int q;
     if (LEVEL == 1) {
         const uint16_t* s4 = cplane<uint16_t>(ws, P, P.s4[1 - d], pair);
-        const int w = L.w;
-        auto src = [&](int yy, int xx) { return __dmul_rn((double)s4[yy * w + xx], 0.25); };
-        v = warp_at(src, L.h, L.w, y, x, base);
+        auto src = [&](int yy, int xx) { return (int)s4[yy * w + xx]; };
+        // value = v / (4 * 2^(2vb)); rint(8 * value) = rint(v / 2^(2vb - 1))
+        q = rne_shift(warp_fixed(src, L.h, w, y, x, base.x, base.y, vb), 2 * vb - 1);
     } else {
         const uint8_t* yp = g.fmt == FVV_RGB8 ? cplane<uint8_t>(ws, P, P.luma[1 - d], pair)
                                               : (d ? pt.left[pair] : pt.right[pair]);
-        const int w = L.w;
-        auto src = [&](int yy, int xx) { return (double)yp[yy * w + xx]; };
-        v = warp_at(src, L.h, L.w, y, x, base);
+        auto src = [&](int yy, int xx) { return (int)yp[yy * w + xx]; };
+        q = rne_shift(warp_fixed(src, L.h, w, y, x, base.x, base.y, vb), 2 * vb - 3);
     }
-    plane<uint16_t>(ws, P, LEVEL == 1 ? P.tq1[d] : P.tq2[d], pair)[i] =
-        (uint16_t)rint_i(__dmul_rn(v, 8.0));
+    plane<uint16_t>(ws, P, LEVEL == 1 ? P.tq1[d] : P.tq2[d], pair)[i] = (uint16_t)q;
+}
+
+// f32(f64(S / 3)) for S = sn * 2^-k exact (the column / row pass of
+// uniform_filter1d on the occlusion cue).  When sn < 2^24, S is an exact
+// f32 and f64 rounding cannot land on an f32 midpoint (S/3 has a periodic
+// binary expansion), so one correctly rounded f32 division gives the
+// reference's double-rounded result; otherwise divide in f64.
+__device__ __forceinline__ float third_f32(int sn, float scale) {
+    if (sn < (1 << 24)) return __fmul_rn(__fdiv_rn((float)sn, 3.0f), scale);
+    return (float)__ddiv_rn(__dmul_rn((double)sn, (double)scale), 3.0);
 }
 
 // ---------------------------------------------------------------------------
@@ -363,9 +379,9 @@ constexpr int kOH = kTH + 2, kOW = kTW + 2;  // occlusion region (+-1)
 
 __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
                                                    uint8_t* __restrict__ ws, Planes P) {
-    __shared__ float2 fm[2][kRH][kRW];       // mid flows f_ml, f_mr (x -0.5)
-    __shared__ float occ[2][kOH][kOW];       // max(0, -div)
-    __shared__ float o0[2][kTH][kOW];        // column pass
+    __shared__ int2 fm[2][kRH][kRW];         // mid flows -flow/2, units 2^-(fb2+1)
+    __shared__ int occ[2][kOH][kOW];         // max(0, -div), units 2^-(fb2+2)
+    __shared__ float o0[2][kTH][kOW];        // column pass (f32, as scipy stores it)
     __shared__ uint8_t dd[kTH + 2][kTW];     // |wl - wr| rows -1..TH
     const int W = g.W, H = g.H;
     const int x0 = blockIdx.x * kTW, y0 = blockIdx.y * kTH;
@@ -374,6 +390,8 @@ __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
     const Level L1 = g.lv[1], L2 = g.lv[2];
     const uint8_t* frL = pt.left[pair];
     const uint8_t* frR = pt.right[pair];
+    const int mb = g.fb[2] + 1;                      // mid-flow fraction bits
+    const int bs = g.fb[2] - (g.fb[1] + 3), rs = g.fb[2] - g.rb[2];
 
     // (a) final flows (flow.py:122-129 at level 2) and mid flows (interp.py:131-132)
     for (int i = tid; i < 2 * kRH * kRW; i += nt) {
@@ -381,61 +399,62 @@ __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
         const int j = i - d * (kRH * kRW);
         const int ry = j / kRW, rx = j - (j / kRW) * kRW;
         const int yi = clampi(y0 - 2 + ry, 0, H - 1), xi = clampi(x0 - 2 + rx, 0, W - 1);
-        const float2 base = upscale_at(cplane<float2>(ws, P, P.flow1[d], pair), L1.h, L1.w, H, W,
-                                       yi, xi);
-        const float2 res = block_to_pixel_at(cplane<BlockHit>(ws, P, P.hit[2][d], pair), L2.nby,
-                                             L2.nbx, L2.block, yi, xi);
-        float2 f = make_float2(__fadd_rn(base.x, res.x), __fadd_rn(base.y, res.y));
-        fm[d][ry][rx] = make_float2(__fmul_rn(f.x, -0.5f), __fmul_rn(f.y, -0.5f));
+        const int2 base = up2_fixed(cplane<int2>(ws, P, P.flow1[d], pair), L1.h, L1.w, yi, xi);
+        const int2 res = b2p_fixed(cplane<BlockHit>(ws, P, P.hit[2][d], pair), L2.nby, L2.nbx,
+                                   L2.block, yi, xi);
+        // f_m = flow * -0.5: in units 2^-(fb2+1) that is -flow_n
+        fm[d][ry][rx] = make_int2(-((base.x << bs) + (res.x << rs)), -((base.y << bs) + (res.y << rs)));
     }
     __syncthreads();
 
-    // (b) occlusion cue at clamped image positions (np.gradient, edge order 1)
+    // (b) occlusion cue at clamped image positions (np.gradient, edge order 1),
+    //     in units 2^-(mb+1): interior (f[i+1]-f[i-1])/2 -> diff, edges f[1]-f[0] -> 2*diff
     for (int i = tid; i < 2 * kOH * kOW; i += nt) {
         const int d = i / (kOH * kOW);
         const int j = i - d * (kOH * kOW);
         const int qy = j / kOW, qx = j - (j / kOW) * kOW;
         const int yi = clampi(y0 - 1 + qy, 0, H - 1), xi = clampi(x0 - 1 + qx, 0, W - 1);
         const int ry = yi - (y0 - 2), rx = xi - (x0 - 2);
-        float gx, gy;
-        if (W < 2) gx = 0.0f;
-        else if (xi == 0) gx = __fsub_rn(fm[d][ry][rx + 1].x, fm[d][ry][rx].x);
-        else if (xi == W - 1) gx = __fsub_rn(fm[d][ry][rx].x, fm[d][ry][rx - 1].x);
-        else gx = __fdiv_rn(__fsub_rn(fm[d][ry][rx + 1].x, fm[d][ry][rx - 1].x), 2.0f);
-        if (H < 2) gy = 0.0f;
-        else if (yi == 0) gy = __fsub_rn(fm[d][ry + 1][rx].y, fm[d][ry][rx].y);
-        else if (yi == H - 1) gy = __fsub_rn(fm[d][ry][rx].y, fm[d][ry - 1][rx].y);
-        else gy = __fdiv_rn(__fsub_rn(fm[d][ry + 1][rx].y, fm[d][ry - 1][rx].y), 2.0f);
-        const float v = -__fadd_rn(gx, gy);
-        occ[d][qy][qx] = v > 0.0f ? v : 0.0f;
+        int gx, gy;
+        if (W < 2) gx = 0;
+        else if (xi == 0) gx = 2 * (fm[d][ry][rx + 1].x - fm[d][ry][rx].x);
+        else if (xi == W - 1) gx = 2 * (fm[d][ry][rx].x - fm[d][ry][rx - 1].x);
+        else gx = fm[d][ry][rx + 1].x - fm[d][ry][rx - 1].x;
+        if (H < 2) gy = 0;
+        else if (yi == 0) gy = 2 * (fm[d][ry + 1][rx].y - fm[d][ry][rx].y);
+        else if (yi == H - 1) gy = 2 * (fm[d][ry][rx].y - fm[d][ry - 1][rx].y);
+        else gy = fm[d][ry + 1][rx].y - fm[d][ry - 1][rx].y;
+        const int v = -(gx + gy);
+        occ[d][qy][qx] = v > 0 ? v : 0;
     }
     __syncthreads();
-    // (c) column pass of smooth3 on occ (exact sums; f32 result of the f64 /3)
+    const float oscale = 1.0f / (float)(1 << (mb + 1));
+    // (c) column pass of smooth3 on occ: exact sum, f32(f64(sum / 3))
     for (int i = tid; i < 2 * kTH * kOW; i += nt) {
         const int d = i / (kTH * kOW);
         const int j = i - d * (kTH * kOW);
         const int ty = j / kOW, qx = j - (j / kOW) * kOW;
-        const double s = __dadd_rn(__dadd_rn((double)occ[d][ty][qx], (double)occ[d][ty + 1][qx]),
-                                   (double)occ[d][ty + 2][qx]);
-        o0[d][ty][qx] = (float)__ddiv_rn(s, 3.0);
+        const int sn = occ[d][ty][qx] + occ[d][ty + 1][qx] + occ[d][ty + 2][qx];
+        o0[d][ty][qx] = sn ? third_f32(sn, oscale) : 0.0f;
     }
     // (e) luma warps for rows -1..TH (clamped), d = |wl - wr|
+    const int kY = 2 * mb;  // luma warp result units 2^-(2 mb)
     for (int i = tid; i < (kTH + 2) * kTW; i += nt) {
         const int qy = i / kTW, tx = i - (i / kTW) * kTW;
         const int yi = clampi(y0 - 1 + qy, 0, H - 1), xi = x0 + tx;
         if (xi >= W) continue;
         const int ry = yi - (y0 - 2), rx = xi - (x0 - 2);
-        const float2 fl = fm[0][ry][rx], fr = fm[1][ry][rx];
+        const int2 fl = fm[0][ry][rx], fr = fm[1][ry][rx];
         const bool center = qy >= 1 && qy <= kTH && y0 - 1 + qy < H;
         uint8_t wl, wr;
         if (g.fmt == FVV_RGB8) {
             uint8_t cl[3], cr[3];
 #pragma unroll
             for (int c = 0; c < 3; c++) {
-                auto sl = [&](int yy, int xx) { return (double)frL[((size_t)yy * W + xx) * 3 + c]; };
-                auto sr = [&](int yy, int xx) { return (double)frR[((size_t)yy * W + xx) * 3 + c]; };
-                cl[c] = to_u8(warp_at(sl, H, W, yi, xi, fl));
-                cr[c] = to_u8(warp_at(sr, H, W, yi, xi, fr));
+                auto sl = [&](int yy, int xx) { return (int)frL[((size_t)yy * W + xx) * 3 + c]; };
+                auto sr = [&](int yy, int xx) { return (int)frR[((size_t)yy * W + xx) * 3 + c]; };
+                cl[c] = (uint8_t)rne_shift(warp_fixed(sl, H, W, yi, xi, fl.x, fl.y, mb), kY);
+                cr[c] = (uint8_t)rne_shift(warp_fixed(sr, H, W, yi, xi, fr.x, fr.y, mb), kY);
             }
             wl = bt601(cl[0], cl[1], cl[2]);
             wr = bt601(cr[0], cr[1], cr[2]);
@@ -445,10 +464,10 @@ __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
                 for (int c = 0; c < 3; c++) { o[c] = cl[c]; o[3 + c] = cr[c]; }
             }
         } else {
-            auto sl = [&](int yy, int xx) { return (double)frL[(size_t)yy * W + xx]; };
-            auto sr = [&](int yy, int xx) { return (double)frR[(size_t)yy * W + xx]; };
-            wl = to_u8(warp_at(sl, H, W, yi, xi, fl));
-            wr = to_u8(warp_at(sr, H, W, yi, xi, fr));
+            auto sl = [&](int yy, int xx) { return (int)frL[(size_t)yy * W + xx]; };
+            auto sr = [&](int yy, int xx) { return (int)frR[(size_t)yy * W + xx]; };
+            wl = (uint8_t)rne_shift(warp_fixed(sl, H, W, yi, xi, fl.x, fl.y, mb), kY);
+            wr = (uint8_t)rne_shift(warp_fixed(sr, H, W, yi, xi, fr.x, fr.y, mb), kY);
         }
         dd[qy][tx] = (uint8_t)abs((int)wl - (int)wr);
         if (center) {
@@ -457,41 +476,40 @@ __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
         }
     }
     // (g) chroma warps with the half-resolution, half-magnitude flow
-    //     (imageops.py:40-48; f32 pairwise mean, exact here)
+    //     (imageops.py:40-48): ((a+b)+(c+d))/4 * 0.5 of units 2^-mb = sum in units 2^-(mb+3)
     if (g.fmt == FVV_YUV420) {
         const int cw = g.cw, chh = g.ch;
         const uint8_t* uL = frL + (size_t)W * H;
         const uint8_t* uR = frR + (size_t)W * H;
         const size_t cplane_sz = (size_t)cw * chh;
+        const int cb = mb + 3, kC = 2 * cb;
         for (int i = tid; i < (kTH / 2) * (kTW / 2); i += nt) {
             const int cy = y0 / 2 + i / (kTW / 2), cx = x0 / 2 + i % (kTW / 2);
             if (cy >= chh || cx >= cw) continue;
             const int ry = 2 * cy - (y0 - 2), rx = 2 * cx - (x0 - 2);
-            float2 cv[2];
+            int2 cv[2];
 #pragma unroll
             for (int d = 0; d < 2; d++) {
-                const float2 a = fm[d][ry][rx], b = fm[d][ry][rx + 1];
-                const float2 c = fm[d][ry + 1][rx], e = fm[d][ry + 1][rx + 1];
-                const float sx = __fadd_rn(__fadd_rn(a.x, b.x), __fadd_rn(c.x, e.x));
-                const float sy = __fadd_rn(__fadd_rn(a.y, b.y), __fadd_rn(c.y, e.y));
-                cv[d] = make_float2(__fmul_rn(__fdiv_rn(sx, 4.0f), 0.5f),
-                                    __fmul_rn(__fdiv_rn(sy, 4.0f), 0.5f));
+                const int2 a = fm[d][ry][rx], b = fm[d][ry][rx + 1];
+                const int2 c = fm[d][ry + 1][rx], e = fm[d][ry + 1][rx + 1];
+                cv[d] = make_int2(a.x + b.x + c.x + e.x, a.y + b.y + c.y + e.y);
             }
             uint8_t o[4];
 #pragma unroll
             for (int p = 0; p < 2; p++) {
                 const uint8_t* pl = uL + p * cplane_sz;
                 const uint8_t* pr = uR + p * cplane_sz;
-                auto sl = [&](int yy, int xx) { return (double)pl[(size_t)yy * cw + xx]; };
-                auto sr = [&](int yy, int xx) { return (double)pr[(size_t)yy * cw + xx]; };
-                o[2 * p] = to_u8(warp_at(sl, chh, cw, cy, cx, cv[0]));
-                o[2 * p + 1] = to_u8(warp_at(sr, chh, cw, cy, cx, cv[1]));
+                auto sl = [&](int yy, int xx) { return (int)pl[(size_t)yy * cw + xx]; };
+                auto sr = [&](int yy, int xx) { return (int)pr[(size_t)yy * cw + xx]; };
+                o[2 * p] = (uint8_t)rne_shift(warp_fixed(sl, chh, cw, cy, cx, cv[0].x, cv[0].y, cb), kC);
+                o[2 * p + 1] = (uint8_t)rne_shift(warp_fixed(sr, chh, cw, cy, cx, cv[1].x, cv[1].y, cb), kC);
             }
             plane<uchar4>(ws, P, P.wc, pair)[(size_t)cy * cw + cx] = make_uchar4(o[0], o[1], o[2], o[3]);
         }
     }
     __syncthreads();
-    // (d) row pass of smooth3 on occ; (f) column sums of |wl - wr|
+    // (d) row pass of smooth3 on occ (exact f64 sum of three f32, /3 in f64);
+    // (f) column sums of |wl - wr|
     for (int i = tid; i < kTH * kTW; i += nt) {
         const int ty = i / kTW, tx = i - (i / kTW) * kTW;
         const int yi = y0 + ty, xi = x0 + tx;
@@ -499,9 +517,13 @@ __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
         const size_t o = (size_t)yi * W + xi;
 #pragma unroll
         for (int d = 0; d < 2; d++) {
-            const double s = __dadd_rn(__dadd_rn((double)o0[d][ty][tx], (double)o0[d][ty][tx + 1]),
-                                       (double)o0[d][ty][tx + 2]);
-            plane<float>(ws, P, d ? P.occ_r : P.occ_l, pair)[o] = (float)__ddiv_rn(s, 3.0);
+            const float a = o0[d][ty][tx], b = o0[d][ty][tx + 1], c = o0[d][ty][tx + 2];
+            float v = 0.0f;
+            if (a != 0.0f || b != 0.0f || c != 0.0f) {
+                const double s = __dadd_rn(__dadd_rn((double)a, (double)b), (double)c);
+                v = (float)__ddiv_rn(s, 3.0);
+            }
+            plane<float>(ws, P, d ? P.occ_r : P.occ_l, pair)[o] = v;
         }
         plane<uint16_t>(ws, P, P.sd, pair)[o] =
             (uint16_t)((int)dd[ty][tx] + (int)dd[ty + 1][tx] + (int)dd[ty + 2][tx]);
@@ -547,18 +569,33 @@ __global__ void __launch_bounds__(128) k_rowscan(Geometry g, PairTable pt,
             buf[r][c] = __dsub_rn(dtab[row[min(x + 1, W - 1)]], dtab[row[max(x - 2, 0)]]);
         }
         __syncthreads();
-        // phase 2: the order-dependent running sum, one thread per row
+        // phase 2: the order-dependent running sum, one thread per row; the
+        // deltas are batched into registers so only the DADD chain is serial
         if (tid < kRB && y0 + tid < H) {
             const int r = tid;
             double tmp = c0 == 0 ? 0.0 : tmp_carry[r];
             const uint16_t* row = sd + (size_t)(y0 + r) * W;
             const int n = min(kCW, W - c0);
-            for (int c = 0; c < n; c++) {
-                if (c0 + c == 0) {
-                    tmp = __dadd_rn(__dadd_rn(dtab[row[0]], dtab[row[0]]), dtab[row[min(1, W - 1)]]);
-                } else {
-                    tmp = __dadd_rn(tmp, buf[r][c]);
+            int c = 0;
+            if (c0 == 0) {
+                tmp = __dadd_rn(__dadd_rn(dtab[row[0]], dtab[row[0]]), dtab[row[min(1, W - 1)]]);
+                buf[r][0] = tmp;
+                c = 1;
+            }
+            for (; c + 16 <= n; c += 16) {
+                double v[16];
+#pragma unroll
+                for (int j = 0; j < 16; j++) v[j] = buf[r][c + j];
+#pragma unroll
+                for (int j = 0; j < 16; j++) {
+                    tmp = __dadd_rn(tmp, v[j]);
+                    v[j] = tmp;
                 }
+#pragma unroll
+                for (int j = 0; j < 16; j++) buf[r][c + j] = v[j];
+            }
+            for (; c < n; c++) {
+                tmp = __dadd_rn(tmp, buf[r][c]);
                 buf[r][c] = tmp;
             }
             tmp_carry[r] = tmp;
@@ -772,11 +809,13 @@ __global__ void k_diag_flow(Geometry g, const uint8_t* __restrict__ ws, Planes P
     if (!out) return;
     const int y = i / g.W, x = i - (i / g.W) * g.W;
     const Level L1 = g.lv[1], L2 = g.lv[2];
-    const float2 base = upscale_at(cplane<float2>(ws, P, P.flow1[d], pair), L1.h, L1.w, g.H, g.W,
-                                   y, x);
-    const float2 res = block_to_pixel_at(cplane<BlockHit>(ws, P, P.hit[2][d], pair), L2.nby,
-                                         L2.nbx, L2.block, y, x);
-    out[i] = make_float2(__fadd_rn(base.x, res.x), __fadd_rn(base.y, res.y));
+    const int2 base = up2_fixed(cplane<int2>(ws, P, P.flow1[d], pair), L1.h, L1.w, y, x);
+    const int2 res = b2p_fixed(cplane<BlockHit>(ws, P, P.hit[2][d], pair), L2.nby, L2.nbx, L2.block,
+                               y, x);
+    const int bs = g.fb[2] - (g.fb[1] + 3), rs = g.fb[2] - g.rb[2];
+    const float sc = 1.0f / (float)(1 << g.fb[2]);  // exact: values < 2^24 units
+    out[i] = make_float2((float)((base.x << bs) + (res.x << rs)) * sc,
+                         (float)((base.y << bs) + (res.y << rs)) * sc);
 }
 
 cudaError_t run_diag(const Geometry& g, const PairTable& pt, uint8_t* ws, const Planes& P, int pair,
