@@ -219,6 +219,9 @@ static int check_interp_desc(const fvv_frame_desc* d) {
     if (rc) return rc;
     if (d->width % 4 || d->height % 4)
         return fail(FVV_EINVAL, "frame dimensions must be divisible by 4 for the 3-scale pyramid");
+    if (d->width > 8192 || d->height > 8192)
+        return fail(FVV_EUNSUPPORTED, "frames wider or taller than 8192 px are outside the B200 path "
+                                      "(32-bit fixed-point coordinates)");
     return FVV_OK;
 }
 

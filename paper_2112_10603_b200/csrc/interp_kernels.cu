@@ -373,16 +373,44 @@ __device__ __forceinline__ float third_f32(int sn, float scale) {
 // can be evaluated tile by tile.  |wl - wr| is integral, so its column pass
 // is exact too; only its row pass (k_rowscan) must replay scipy in order.
 // ---------------------------------------------------------------------------
-constexpr int kTH = 16, kTW = 32;           // output tile
+constexpr int kTH = 16, kTW = 64;           // output tile
 constexpr int kRH = kTH + 4, kRW = kTW + 4;  // flow region (+-2)
 constexpr int kOH = kTH + 2, kOW = kTW + 2;  // occlusion region (+-1)
+constexpr int kH1 = 13;                      // level-1 rows feeding the region (<= 12)
+constexpr int kHB = 13;                      // block rows feeding the region (<= 12, B >= 2)
+
+struct MaskSmem {
+    int2 fm[2][kRH][kRW];  // mid flows -flow/2, units 2^-(fb2+1)
+    union {
+        struct {           // separable passes (x-lerp of the source rows)
+            int2 h1[2][kH1][kRW];
+            int2 hb[2][kHB][kRW];
+        } sep;
+        struct {
+            int occ[2][kOH][kOW];    // max(0, -div), units 2^-(fb2+2)
+            float o0[2][kTH][kOW];   // column pass (f32, as scipy stores it)
+        } occ;
+    } u;
+    uint8_t dd[kTH + 2][kTW];  // |wl - wr| rows -1..TH
+};
+
+// warp_fixed with 32-bit coordinates (frames <= 8192 px, validated on the host)
+template <typename Src>
+__device__ __forceinline__ long long warp_fixed32(const Src& src, int h, int w, int y, int x,
+                                                  int fxn, int fyn, int vb) {
+    const ITap tx = clamp_itap32((x << vb) + fxn, vb, w);
+    const ITap ty = clamp_itap32((y << vb) + fyn, vb, h);
+    const int V = 1 << vb;
+    const int top = (V - tx.f) * src(ty.i0, tx.i0) + tx.f * src(ty.i0, tx.i1);
+    const int bot = (V - tx.f) * src(ty.i1, tx.i0) + tx.f * src(ty.i1, tx.i1);
+    // (V - fy) * top + fy * bot == V * top + fy * (bot - top), exact in 64 bits
+    return ((long long)top << vb) + (long long)ty.f * (long long)(bot - top);
+}
 
 __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
                                                    uint8_t* __restrict__ ws, Planes P) {
-    __shared__ int2 fm[2][kRH][kRW];         // mid flows -flow/2, units 2^-(fb2+1)
-    __shared__ int occ[2][kOH][kOW];         // max(0, -div), units 2^-(fb2+2)
-    __shared__ float o0[2][kTH][kOW];        // column pass (f32, as scipy stores it)
-    __shared__ uint8_t dd[kTH + 2][kTW];     // |wl - wr| rows -1..TH
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    MaskSmem& S = *reinterpret_cast<MaskSmem*>(smem_raw);
     const int W = g.W, H = g.H;
     const int x0 = blockIdx.x * kTW, y0 = blockIdx.y * kTH;
     const int pair = blockIdx.z;
@@ -392,18 +420,47 @@ __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
     const uint8_t* frR = pt.right[pair];
     const int mb = g.fb[2] + 1;                      // mid-flow fraction bits
     const int bs = g.fb[2] - (g.fb[1] + 3), rs = g.fb[2] - g.rb[2];
+    const int B2 = L2.block, D2 = 2 * B2, lgD2 = 31 - __clz(D2);
 
-    // (a) final flows (flow.py:122-129 at level 2) and mid flows (interp.py:131-132)
+    // (a) final flows (flow.py:122-129 at level 2) and mid flows (interp.py:131-132),
+    //     separably: x-lerp the source rows once, then y-lerp (the reference's order)
+    const int ylo = clampi(y0 - 2, 0, H - 1), yhi = clampi(y0 + kTH + 1, 0, H - 1);
+    const int s_lo = clamp_itap32(2 * ylo - 1, 2, L1.h).i0;
+    const int s_n = clamp_itap32(2 * yhi - 1, 2, L1.h).i1 - s_lo + 1;
+    const int b_lo = clamp_itap32(2 * ylo - B2 + 1, lgD2, L2.nby).i0;
+    const int b_n = clamp_itap32(2 * yhi - B2 + 1, lgD2, L2.nby).i1 - b_lo + 1;
+    for (int i = tid; i < 2 * (s_n + b_n) * kRW; i += nt) {
+        const int d = i / ((s_n + b_n) * kRW);
+        const int j = i - d * ((s_n + b_n) * kRW);
+        const int row = j / kRW, rx = j - row * kRW;
+        const int xi = clampi(x0 - 2 + rx, 0, W - 1);
+        if (row < s_n) {
+            const int2* f1 = cplane<int2>(ws, P, P.flow1[d], pair) + (size_t)(s_lo + row) * L1.w;
+            const ITap tx = clamp_itap32(2 * xi - 1, 2, L1.w);
+            const int2 a = f1[tx.i0], b = f1[tx.i1];
+            S.u.sep.h1[d][row][rx] = make_int2((4 - tx.f) * a.x + tx.f * b.x, (4 - tx.f) * a.y + tx.f * b.y);
+        } else {
+            const int br = row - s_n;
+            const BlockHit* hr = cplane<BlockHit>(ws, P, P.hit[2][d], pair) + (size_t)(b_lo + br) * L2.nbx;
+            const ITap tx = clamp_itap32(2 * xi - B2 + 1, lgD2, L2.nbx);
+            const BlockHit a = hr[tx.i0], b = hr[tx.i1];
+            S.u.sep.hb[d][br][rx] = make_int2((D2 - tx.f) * a.dx + tx.f * b.dx, (D2 - tx.f) * a.dy + tx.f * b.dy);
+        }
+    }
+    __syncthreads();
     for (int i = tid; i < 2 * kRH * kRW; i += nt) {
         const int d = i / (kRH * kRW);
         const int j = i - d * (kRH * kRW);
-        const int ry = j / kRW, rx = j - (j / kRW) * kRW;
-        const int yi = clampi(y0 - 2 + ry, 0, H - 1), xi = clampi(x0 - 2 + rx, 0, W - 1);
-        const int2 base = up2_fixed(cplane<int2>(ws, P, P.flow1[d], pair), L1.h, L1.w, yi, xi);
-        const int2 res = b2p_fixed(cplane<BlockHit>(ws, P, P.hit[2][d], pair), L2.nby, L2.nbx,
-                                   L2.block, yi, xi);
+        const int ry = j / kRW, rx = j - ry * kRW;
+        const int yi = clampi(y0 - 2 + ry, 0, H - 1);
+        const ITap ty = clamp_itap32(2 * yi - 1, 2, L1.h);
+        const int2 t = S.u.sep.h1[d][ty.i0 - s_lo][rx], u = S.u.sep.h1[d][ty.i1 - s_lo][rx];
+        const ITap tb = clamp_itap32(2 * yi - B2 + 1, lgD2, L2.nby);
+        const int2 p = S.u.sep.hb[d][tb.i0 - b_lo][rx], q = S.u.sep.hb[d][tb.i1 - b_lo][rx];
+        const int bx_ = (4 - ty.f) * t.x + ty.f * u.x, by_ = (4 - ty.f) * t.y + ty.f * u.y;
+        const int rx_ = (D2 - tb.f) * p.x + tb.f * q.x, ry_ = (D2 - tb.f) * p.y + tb.f * q.y;
         // f_m = flow * -0.5: in units 2^-(fb2+1) that is -flow_n
-        fm[d][ry][rx] = make_int2(-((base.x << bs) + (res.x << rs)), -((base.y << bs) + (res.y << rs)));
+        S.fm[d][ry][rx] = make_int2(-((bx_ << bs) + (rx_ << rs)), -((by_ << bs) + (ry_ << rs)));
     }
     __syncthreads();
 
@@ -412,20 +469,20 @@ __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
     for (int i = tid; i < 2 * kOH * kOW; i += nt) {
         const int d = i / (kOH * kOW);
         const int j = i - d * (kOH * kOW);
-        const int qy = j / kOW, qx = j - (j / kOW) * kOW;
+        const int qy = j / kOW, qx = j - qy * kOW;
         const int yi = clampi(y0 - 1 + qy, 0, H - 1), xi = clampi(x0 - 1 + qx, 0, W - 1);
         const int ry = yi - (y0 - 2), rx = xi - (x0 - 2);
         int gx, gy;
         if (W < 2) gx = 0;
-        else if (xi == 0) gx = 2 * (fm[d][ry][rx + 1].x - fm[d][ry][rx].x);
-        else if (xi == W - 1) gx = 2 * (fm[d][ry][rx].x - fm[d][ry][rx - 1].x);
-        else gx = fm[d][ry][rx + 1].x - fm[d][ry][rx - 1].x;
+        else if (xi == 0) gx = 2 * (S.fm[d][ry][rx + 1].x - S.fm[d][ry][rx].x);
+        else if (xi == W - 1) gx = 2 * (S.fm[d][ry][rx].x - S.fm[d][ry][rx - 1].x);
+        else gx = S.fm[d][ry][rx + 1].x - S.fm[d][ry][rx - 1].x;
         if (H < 2) gy = 0;
-        else if (yi == 0) gy = 2 * (fm[d][ry + 1][rx].y - fm[d][ry][rx].y);
-        else if (yi == H - 1) gy = 2 * (fm[d][ry][rx].y - fm[d][ry - 1][rx].y);
-        else gy = fm[d][ry + 1][rx].y - fm[d][ry - 1][rx].y;
+        else if (yi == 0) gy = 2 * (S.fm[d][ry + 1][rx].y - S.fm[d][ry][rx].y);
+        else if (yi == H - 1) gy = 2 * (S.fm[d][ry][rx].y - S.fm[d][ry - 1][rx].y);
+        else gy = S.fm[d][ry + 1][rx].y - S.fm[d][ry - 1][rx].y;
         const int v = -(gx + gy);
-        occ[d][qy][qx] = v > 0 ? v : 0;
+        S.u.occ.occ[d][qy][qx] = v > 0 ? v : 0;
     }
     __syncthreads();
     const float oscale = 1.0f / (float)(1 << (mb + 1));
@@ -433,18 +490,18 @@ __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
     for (int i = tid; i < 2 * kTH * kOW; i += nt) {
         const int d = i / (kTH * kOW);
         const int j = i - d * (kTH * kOW);
-        const int ty = j / kOW, qx = j - (j / kOW) * kOW;
-        const int sn = occ[d][ty][qx] + occ[d][ty + 1][qx] + occ[d][ty + 2][qx];
-        o0[d][ty][qx] = sn ? third_f32(sn, oscale) : 0.0f;
+        const int ty = j / kOW, qx = j - ty * kOW;
+        const int sn = S.u.occ.occ[d][ty][qx] + S.u.occ.occ[d][ty + 1][qx] + S.u.occ.occ[d][ty + 2][qx];
+        S.u.occ.o0[d][ty][qx] = sn ? third_f32(sn, oscale) : 0.0f;
     }
     // (e) luma warps for rows -1..TH (clamped), d = |wl - wr|
     const int kY = 2 * mb;  // luma warp result units 2^-(2 mb)
     for (int i = tid; i < (kTH + 2) * kTW; i += nt) {
-        const int qy = i / kTW, tx = i - (i / kTW) * kTW;
+        const int qy = i / kTW, tx = i - qy * kTW;
         const int yi = clampi(y0 - 1 + qy, 0, H - 1), xi = x0 + tx;
         if (xi >= W) continue;
         const int ry = yi - (y0 - 2), rx = xi - (x0 - 2);
-        const int2 fl = fm[0][ry][rx], fr = fm[1][ry][rx];
+        const int2 fl = S.fm[0][ry][rx], fr = S.fm[1][ry][rx];
         const bool center = qy >= 1 && qy <= kTH && y0 - 1 + qy < H;
         uint8_t wl, wr;
         if (g.fmt == FVV_RGB8) {
@@ -453,8 +510,8 @@ __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
             for (int c = 0; c < 3; c++) {
                 auto sl = [&](int yy, int xx) { return (int)frL[((size_t)yy * W + xx) * 3 + c]; };
                 auto sr = [&](int yy, int xx) { return (int)frR[((size_t)yy * W + xx) * 3 + c]; };
-                cl[c] = (uint8_t)rne_shift(warp_fixed(sl, H, W, yi, xi, fl.x, fl.y, mb), kY);
-                cr[c] = (uint8_t)rne_shift(warp_fixed(sr, H, W, yi, xi, fr.x, fr.y, mb), kY);
+                cl[c] = (uint8_t)rne_shift(warp_fixed32(sl, H, W, yi, xi, fl.x, fl.y, mb), kY);
+                cr[c] = (uint8_t)rne_shift(warp_fixed32(sr, H, W, yi, xi, fr.x, fr.y, mb), kY);
             }
             wl = bt601(cl[0], cl[1], cl[2]);
             wr = bt601(cr[0], cr[1], cr[2]);
@@ -466,10 +523,10 @@ __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
         } else {
             auto sl = [&](int yy, int xx) { return (int)frL[(size_t)yy * W + xx]; };
             auto sr = [&](int yy, int xx) { return (int)frR[(size_t)yy * W + xx]; };
-            wl = (uint8_t)rne_shift(warp_fixed(sl, H, W, yi, xi, fl.x, fl.y, mb), kY);
-            wr = (uint8_t)rne_shift(warp_fixed(sr, H, W, yi, xi, fr.x, fr.y, mb), kY);
+            wl = (uint8_t)rne_shift(warp_fixed32(sl, H, W, yi, xi, fl.x, fl.y, mb), kY);
+            wr = (uint8_t)rne_shift(warp_fixed32(sr, H, W, yi, xi, fr.x, fr.y, mb), kY);
         }
-        dd[qy][tx] = (uint8_t)abs((int)wl - (int)wr);
+        S.dd[qy][tx] = (uint8_t)abs((int)wl - (int)wr);
         if (center) {
             plane<uint8_t>(ws, P, P.wl, pair)[(size_t)yi * W + xi] = wl;
             plane<uint8_t>(ws, P, P.wr, pair)[(size_t)yi * W + xi] = wr;
@@ -490,8 +547,8 @@ __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
             int2 cv[2];
 #pragma unroll
             for (int d = 0; d < 2; d++) {
-                const int2 a = fm[d][ry][rx], b = fm[d][ry][rx + 1];
-                const int2 c = fm[d][ry + 1][rx], e = fm[d][ry + 1][rx + 1];
+                const int2 a = S.fm[d][ry][rx], b = S.fm[d][ry][rx + 1];
+                const int2 c = S.fm[d][ry + 1][rx], e = S.fm[d][ry + 1][rx + 1];
                 cv[d] = make_int2(a.x + b.x + c.x + e.x, a.y + b.y + c.y + e.y);
             }
             uint8_t o[4];
@@ -501,8 +558,8 @@ __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
                 const uint8_t* pr = uR + p * cplane_sz;
                 auto sl = [&](int yy, int xx) { return (int)pl[(size_t)yy * cw + xx]; };
                 auto sr = [&](int yy, int xx) { return (int)pr[(size_t)yy * cw + xx]; };
-                o[2 * p] = (uint8_t)rne_shift(warp_fixed(sl, chh, cw, cy, cx, cv[0].x, cv[0].y, cb), kC);
-                o[2 * p + 1] = (uint8_t)rne_shift(warp_fixed(sr, chh, cw, cy, cx, cv[1].x, cv[1].y, cb), kC);
+                o[2 * p] = (uint8_t)rne_shift(warp_fixed32(sl, chh, cw, cy, cx, cv[0].x, cv[0].y, cb), kC);
+                o[2 * p + 1] = (uint8_t)rne_shift(warp_fixed32(sr, chh, cw, cy, cx, cv[1].x, cv[1].y, cb), kC);
             }
             plane<uchar4>(ws, P, P.wc, pair)[(size_t)cy * cw + cx] = make_uchar4(o[0], o[1], o[2], o[3]);
         }
@@ -511,13 +568,13 @@ __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
     // (d) row pass of smooth3 on occ (exact f64 sum of three f32, /3 in f64);
     // (f) column sums of |wl - wr|
     for (int i = tid; i < kTH * kTW; i += nt) {
-        const int ty = i / kTW, tx = i - (i / kTW) * kTW;
+        const int ty = i / kTW, tx = i - ty * kTW;
         const int yi = y0 + ty, xi = x0 + tx;
         if (yi >= H || xi >= W) continue;
         const size_t o = (size_t)yi * W + xi;
 #pragma unroll
         for (int d = 0; d < 2; d++) {
-            const float a = o0[d][ty][tx], b = o0[d][ty][tx + 1], c = o0[d][ty][tx + 2];
+            const float a = S.u.occ.o0[d][ty][tx], b = S.u.occ.o0[d][ty][tx + 1], c = S.u.occ.o0[d][ty][tx + 2];
             float v = 0.0f;
             if (a != 0.0f || b != 0.0f || c != 0.0f) {
                 const double s = __dadd_rn(__dadd_rn((double)a, (double)b), (double)c);
@@ -526,7 +583,7 @@ __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
             plane<float>(ws, P, d ? P.occ_r : P.occ_l, pair)[o] = v;
         }
         plane<uint16_t>(ws, P, P.sd, pair)[o] =
-            (uint16_t)((int)dd[ty][tx] + (int)dd[ty + 1][tx] + (int)dd[ty + 2][tx]);
+            (uint16_t)((int)S.dd[ty][tx] + (int)S.dd[ty + 1][tx] + (int)S.dd[ty + 2][tx]);
     }
 }
 
@@ -534,80 +591,114 @@ __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
 // k_rowscan: the row pass of smooth3(|wl - wr|) replayed in scipy's order
 // (tmp = (p0+p1)+p2; tmp += p[i+2]-p[i-1]; out = tmp/3, all f64), then the
 // mask (warp.py:49-63) and the blend of every plane (warp.py:66-88).
-// One CTA = 32 rows of one pair; 64-column chunks; one thread per row runs
-// the sequential chain, all threads do the per-pixel work around it.
+//
+// Warp-specialised pipeline over 64-column chunks of a 32-row band:
+//   warp 0 (one lane per row) runs the order-dependent DADD chain of chunk k
+//   warps 1-7 meanwhile build the differences of chunk k+1, then -- once the
+//   chain has released chunk k -- evaluate mask and blend for it.
+// Named barriers hand the double-buffered chunk back and forth.
 // ---------------------------------------------------------------------------
 constexpr int kRB = 32, kCW = 64;
+constexpr int kRowscanThreads = 256, kWorkers = kRowscanThreads - 32;
 
-__global__ void __launch_bounds__(128) k_rowscan(Geometry g, PairTable pt,
-                                                 const uint8_t* __restrict__ ws, Planes P,
-                                                 int pair_base, bool write_frame,
-                                                 double* mask_out /* nullable: one pair */) {
-    __shared__ double dtab[766];          // s/3.0 for the integral column sums
-    __shared__ double buf[kRB][kCW + 1];  // deltas, then running sums, then masks
-    __shared__ double tmp_carry[kRB];
+__device__ __forceinline__ void bar_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__global__ void __launch_bounds__(kRowscanThreads) k_rowscan(Geometry g, PairTable pt,
+                                                              const uint8_t* __restrict__ ws, Planes P,
+                                                              int pair_base, bool write_frame,
+                                                              double* mask_out /* nullable: one pair */) {
+    __shared__ double dtab[766];                // s/3.0 for the integral column sums
+    __shared__ double buf[2][kRB][kCW + 1];     // deltas -> running sums -> masks
     const int W = g.W, H = g.H;
     const int pair = blockIdx.y + pair_base;
     const int y0 = blockIdx.x * kRB;
-    const int tid = threadIdx.x, nt = blockDim.x;
+    const int tid = threadIdx.x;
+    const int nchunks = (W + kCW - 1) / kCW;
     const uint16_t* sd = cplane<uint16_t>(ws, P, P.sd, pair);
+    for (int i = tid; i < 766; i += kRowscanThreads) dtab[i] = __ddiv_rn((double)i, 3.0);
+    __syncthreads();
+
+    if (tid < 32) {
+        // ---------------- chain warp: lane = row ----------------
+        const int r = tid;
+        const bool live = y0 + r < H;
+        const uint16_t* row = sd + (size_t)(live ? y0 + r : 0) * W;
+        double tmp = 0.0;
+        for (int k = 0; k < nchunks; k++) {
+            const int b = k & 1, c0 = k * kCW;
+            bar_sync(1 + b, kRowscanThreads);  // deltas of chunk k ready
+            if (live) {
+                double* br = buf[b][r];
+                const int n = min(kCW, W - c0);
+                int c = 0;
+                if (c0 == 0) {
+                    tmp = __dadd_rn(__dadd_rn(dtab[row[0]], dtab[row[0]]), dtab[row[min(1, W - 1)]]);
+                    br[0] = tmp;
+                    c = 1;
+                }
+                for (; c + 16 <= n; c += 16) {
+                    double v[16];
+#pragma unroll
+                    for (int j = 0; j < 16; j++) v[j] = br[c + j];
+#pragma unroll
+                    for (int j = 0; j < 16; j++) {
+                        tmp = __dadd_rn(tmp, v[j]);
+                        v[j] = tmp;
+                    }
+#pragma unroll
+                    for (int j = 0; j < 16; j++) br[c + j] = v[j];
+                }
+                for (; c < n; c++) {
+                    tmp = __dadd_rn(tmp, br[c]);
+                    br[c] = tmp;
+                }
+            }
+            bar_arrive(3 + b, kRowscanThreads);  // running sums of chunk k ready
+        }
+        return;
+    }
+
+    // ---------------- worker warps ----------------
+    const int wt = tid - 32;
     const float* ol = cplane<float>(ws, P, P.occ_l, pair);
     const float* orr = cplane<float>(ws, P, P.occ_r, pair);
     const uint8_t* wl = cplane<uint8_t>(ws, P, P.wl, pair);
     const uint8_t* wr = cplane<uint8_t>(ws, P, P.wr, pair);
     uint8_t* out = pt.out[pair];
-    for (int i = tid; i < 766; i += nt) dtab[i] = __ddiv_rn((double)i, 3.0);
-    __syncthreads();
 
-    for (int c0 = 0; c0 < W; c0 += kCW) {
-        // phase 1: differences p[i+2] - p[i-1] (independent of the chain)
-        for (int i = tid; i < kRB * kCW; i += nt) {
-            const int r = i / kCW, c = i - (i / kCW) * kCW;
+    auto deltas = [&](int k) {  // p[i+2] - p[i-1] of chunk k (independent of the chain)
+        const int b = k & 1, c0 = k * kCW;
+        for (int i = wt; i < kRB * kCW; i += kWorkers) {
+            const int r = i / kCW, c = i - r * kCW;
             const int y = y0 + r, x = c0 + c;
             if (y >= H || x >= W) continue;
             const uint16_t* row = sd + (size_t)y * W;
-            buf[r][c] = __dsub_rn(dtab[row[min(x + 1, W - 1)]], dtab[row[max(x - 2, 0)]]);
+            buf[b][r][c] = __dsub_rn(dtab[row[min(x + 1, W - 1)]], dtab[row[max(x - 2, 0)]]);
         }
-        __syncthreads();
-        // phase 2: the order-dependent running sum, one thread per row; the
-        // deltas are batched into registers so only the DADD chain is serial
-        if (tid < kRB && y0 + tid < H) {
-            const int r = tid;
-            double tmp = c0 == 0 ? 0.0 : tmp_carry[r];
-            const uint16_t* row = sd + (size_t)(y0 + r) * W;
-            const int n = min(kCW, W - c0);
-            int c = 0;
-            if (c0 == 0) {
-                tmp = __dadd_rn(__dadd_rn(dtab[row[0]], dtab[row[0]]), dtab[row[min(1, W - 1)]]);
-                buf[r][0] = tmp;
-                c = 1;
-            }
-            for (; c + 16 <= n; c += 16) {
-                double v[16];
-#pragma unroll
-                for (int j = 0; j < 16; j++) v[j] = buf[r][c + j];
-#pragma unroll
-                for (int j = 0; j < 16; j++) {
-                    tmp = __dadd_rn(tmp, v[j]);
-                    v[j] = tmp;
-                }
-#pragma unroll
-                for (int j = 0; j < 16; j++) buf[r][c + j] = v[j];
-            }
-            for (; c < n; c++) {
-                tmp = __dadd_rn(tmp, buf[r][c]);
-                buf[r][c] = tmp;
-            }
-            tmp_carry[r] = tmp;
+    };
+
+    deltas(0);
+    bar_arrive(1, kRowscanThreads);
+    for (int k = 0; k < nchunks; k++) {
+        const int b = k & 1, c0 = k * kCW;
+        if (k + 1 < nchunks) {
+            if (k >= 1) bar_sync(5, kWorkers);  // every worker is done with chunk k-1's buffer
+            deltas(k + 1);
+            bar_arrive(1 + (b ^ 1), kRowscanThreads);
         }
-        __syncthreads();
-        // phase 3: mask + blend of luma / RGB
-        for (int i = tid; i < kRB * kCW; i += nt) {
-            const int r = i / kCW, c = i - (i / kCW) * kCW;
+        bar_sync(3 + b, kRowscanThreads);  // the chain released chunk k
+        // mask + blend of luma / RGB
+        for (int i = wt; i < kRB * kCW; i += kWorkers) {
+            const int r = i / kCW, c = i - r * kCW;
             const int y = y0 + r, x = c0 + c;
             if (y >= H || x >= W) continue;
             const size_t o = (size_t)y * W + x;
-            const double D = __ddiv_rn(buf[r][c], 3.0);
+            const double D = __ddiv_rn(buf[b][r][c], 3.0);
             const float ql = __fadd_rn(0.5f, __fmul_rn(4.0f, ol[o]));
             const float qr = __fadd_rn(0.5f, __fmul_rn(4.0f, orr[o]));
             const double el = __dmul_rn(D, (double)ql);
@@ -626,21 +717,21 @@ __global__ void __launch_bounds__(128) k_rowscan(Geometry g, PairTable pt,
                 out[o] = to_u8(__dadd_rn(__dmul_rn(m, (double)wl[o]), __dmul_rn(m1, (double)wr[o])));
             }
             if (mask_out) mask_out[o] = m;
-            buf[r][c] = m;
+            buf[b][r][c] = m;
         }
-        __syncthreads();
-        // phase 4: chroma blend with the 2x2-mean mask (warp.py:83-88)
+        // chroma blend with the 2x2-mean mask (warp.py:83-88)
         if (g.fmt == FVV_YUV420 && write_frame) {
+            bar_sync(6, kWorkers);  // masks of the whole chunk are in smem
             const int cw = g.cw, chh = g.ch;
             const uchar4* wc = cplane<uchar4>(ws, P, P.wc, pair);
             uint8_t* uo = out + (size_t)W * H;
             uint8_t* vo = uo + (size_t)cw * chh;
-            for (int i = tid; i < (kRB / 2) * (kCW / 2); i += nt) {
-                const int a = i / (kCW / 2), b = i - (i / (kCW / 2)) * (kCW / 2);
-                const int cy = y0 / 2 + a, cx = c0 / 2 + b;
+            for (int i = wt; i < (kRB / 2) * (kCW / 2); i += kWorkers) {
+                const int a = i / (kCW / 2), bb = i - a * (kCW / 2);
+                const int cy = y0 / 2 + a, cx = c0 / 2 + bb;
                 if (cy >= chh || cx >= cw) continue;
-                const double s = __dadd_rn(__dadd_rn(buf[2 * a][2 * b], buf[2 * a][2 * b + 1]),
-                                           __dadd_rn(buf[2 * a + 1][2 * b], buf[2 * a + 1][2 * b + 1]));
+                const double s = __dadd_rn(__dadd_rn(buf[b][2 * a][2 * bb], buf[b][2 * a][2 * bb + 1]),
+                                           __dadd_rn(buf[b][2 * a + 1][2 * bb], buf[b][2 * a + 1][2 * bb + 1]));
                 const double mc = __dmul_rn(s, 0.25);  // /4 == *0.25 exactly
                 const double mc1 = __dsub_rn(1.0, mc);
                 const uchar4 q = wc[(size_t)cy * cw + cx];
@@ -649,7 +740,6 @@ __global__ void __launch_bounds__(128) k_rowscan(Geometry g, PairTable pt,
                 vo[(size_t)cy * cw + cx] = to_u8(__dadd_rn(__dmul_rn(mc, (double)q.z),
                                                            __dmul_rn(mc1, (double)q.w)));
             }
-            __syncthreads();
         }
     }
 }
@@ -790,12 +880,22 @@ cudaError_t run_interp_stage(const Geometry& g, const PairTable& pt, uint8_t* ws
     if (e != cudaSuccess || (e = E()) != cudaSuccess) return e;
 
     B(KC_MASK_PROD);
-    k_mask_prod<<<dim3((g.W + kTW - 1) / kTW, (g.H + kTH - 1) / kTH, npairs), 256, 0, st>>>(g, pt,
-                                                                                         ws, P);
+    {
+        static bool attr_set = false;  // idempotent; racing threads set the same value
+        if (!attr_set) {
+            e = cudaFuncSetAttribute(k_mask_prod, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(MaskSmem));
+            if (e != cudaSuccess) return e;
+            attr_set = true;
+        }
+    }
+    k_mask_prod<<<dim3((g.W + kTW - 1) / kTW, (g.H + kTH - 1) / kTH, npairs), 256, sizeof(MaskSmem),
+                  st>>>(g, pt, ws, P);
     if ((e = E()) != cudaSuccess) return e;
 
     B(KC_ROWSCAN);
-    k_rowscan<<<dim3((g.H + kRB - 1) / kRB, npairs), 128, 0, st>>>(g, pt, ws, P, 0, true, mask_out);
+    k_rowscan<<<dim3((g.H + kRB - 1) / kRB, npairs), kRowscanThreads, 0, st>>>(g, pt, ws, P, 0, true,
+                                                                              mask_out);
     return E();
 }
 
@@ -829,7 +929,7 @@ cudaError_t run_diag(const Geometry& g, const PairTable& pt, uint8_t* ws, const 
     }
     if (mask) {
         dim3 grd2((g.H + kRB - 1) / kRB, 1);
-        k_rowscan<<<grd2, 128, 0, st>>>(g, pt, ws, P, pair, false, mask);
+        k_rowscan<<<grd2, kRowscanThreads, 0, st>>>(g, pt, ws, P, pair, false, mask);
         return cudaGetLastError();
     }
     return cudaSuccess;
