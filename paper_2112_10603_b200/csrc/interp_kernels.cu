@@ -318,37 +318,77 @@ __global__ void k_flow(Geometry g, uint8_t* __restrict__ ws, Planes P) {
     plane<int2>(ws, P, LEVEL == 0 ? P.flow0[d] : P.flow1[d], pair)[i] = f;
 }
 
+// warp_fixed with 32-bit coordinates (frames <= 8192 px, validated on the host)
+template <typename Src>
+__device__ __forceinline__ long long warp_fixed32(const Src& src, int h, int w, int y, int x,
+                                                  int fxn, int fyn, int vb) {
+    const ITap tx = clamp_itap32((x << vb) + fxn, vb, w);
+    const ITap ty = clamp_itap32((y << vb) + fyn, vb, h);
+    const int V = 1 << vb;
+    const int top = (V - tx.f) * src(ty.i0, tx.i0) + tx.f * src(ty.i0, tx.i1);
+    const int bot = (V - tx.f) * src(ty.i1, tx.i0) + tx.f * src(ty.i1, tx.i1);
+    // (V - fy) * top + fy * bot == V * top + fy * (bot - top), exact in 64 bits
+    return ((long long)top << vb) + (long long)ty.f * (long long)(bot - top);
+}
+
+__device__ __forceinline__ int2 lerp_i2(int2 a, int2 b, int den, int f) {
+    return make_int2((den - f) * a.x + f * b.x, (den - f) * a.y + f * b.y);
+}
+
 // ---------------------------------------------------------------------------
 // k_warpq<L> (L = 1, 2): pad_q source = rint(8 * warp_plane(target, base))
 // (flow.py:123-124 then :78); the edge padding is applied by the search.
-// Exact integer bilinear: base in units 2^-(fb[L-1]+3), level-1 samples in
+// Exact integer bilinear: base = 2x upscale of flow_{L-1} (units
+// 2^-(fb[L-1]+3)), computed separably per 16x64 tile; level-1 samples in
 // units 1/4 (s4), level-2 samples integral (luma).
 // ---------------------------------------------------------------------------
+constexpr int kQH = 16, kQW = 64;
 template <int LEVEL>
-__global__ void k_warpq(Geometry g, PairTable pt, uint8_t* __restrict__ ws, Planes P) {
+__global__ void __launch_bounds__(256) k_warpq(Geometry g, PairTable pt, uint8_t* __restrict__ ws,
+                                               Planes P) {
+    __shared__ int2 h[kQH / 2 + 3][kQW];
+    __shared__ ITap cxt[kQW];
     const Level L = g.lv[LEVEL];
     const Level Lp = g.lv[LEVEL - 1];
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int pair = blockIdx.z >> 1, d = blockIdx.z & 1;
-    if (i >= L.w * L.h) return;
-    const int y = i / L.w, x = i - (i / L.w) * L.w;
+    const int x0 = blockIdx.x * kQW, y0 = blockIdx.y * kQH;
+    const int tid = threadIdx.x, tx = tid & 63, tg = tid >> 6;
     const int2* prev = cplane<int2>(ws, P, LEVEL == 1 ? P.flow0[d] : P.flow1[d], pair);
-    const int2 base = up2_fixed(prev, Lp.h, Lp.w, y, x);
+    if (tid < kQW) cxt[tid] = clamp_itap32(2 * min(x0 + tid, L.w - 1) - 1, 2, Lp.w);
+    const int ylast = min(y0 + kQH - 1, L.h - 1);
+    const int s_lo = clamp_itap32(2 * y0 - 1, 2, Lp.h).i0;
+    const int s_n = clamp_itap32(2 * ylast - 1, 2, Lp.h).i1 - s_lo + 1;
+    __syncthreads();
+    for (int row = tg; row < s_n; row += 4) {
+        const int2* pr = prev + (size_t)(s_lo + row) * Lp.w;
+        const ITap t = cxt[tx];
+        h[row][tx] = lerp_i2(pr[t.i0], pr[t.i1], 4, t.f);
+    }
+    __syncthreads();
+    const int x = x0 + tx;
+    if (x >= L.w) return;
     const int vb = g.fb[LEVEL - 1] + 3;
     const int w = L.w;
-    int q;
-    if (LEVEL == 1) {
-        const uint16_t* s4 = cplane<uint16_t>(ws, P, P.s4[1 - d], pair);
-        auto src = [&](int yy, int xx) { return (int)s4[yy * w + xx]; };
-        // value = v / (4 * 2^(2vb)); rint(8 * value) = rint(v / 2^(2vb - 1))
-        q = rne_shift(warp_fixed(src, L.h, w, y, x, base.x, base.y, vb), 2 * vb - 1);
-    } else {
-        const uint8_t* yp = g.fmt == FVV_RGB8 ? cplane<uint8_t>(ws, P, P.luma[1 - d], pair)
-                                              : (d ? pt.left[pair] : pt.right[pair]);
-        auto src = [&](int yy, int xx) { return (int)yp[yy * w + xx]; };
-        q = rne_shift(warp_fixed(src, L.h, w, y, x, base.x, base.y, vb), 2 * vb - 3);
+    uint16_t* outp = plane<uint16_t>(ws, P, LEVEL == 1 ? P.tq1[d] : P.tq2[d], pair);
+    const uint16_t* s4 = cplane<uint16_t>(ws, P, P.s4[1 - d], pair);
+    const uint8_t* yp = g.fmt == FVV_RGB8 ? cplane<uint8_t>(ws, P, P.luma[1 - d], pair)
+                                          : (d ? pt.left[pair] : pt.right[pair]);
+    for (int ty = tg; ty < kQH; ty += 4) {
+        const int y = y0 + ty;
+        if (y >= L.h) break;
+        const ITap t = clamp_itap32(2 * y - 1, 2, Lp.h);
+        const int2 base = lerp_i2(h[t.i0 - s_lo][tx], h[t.i1 - s_lo][tx], 4, t.f);
+        int q;
+        if (LEVEL == 1) {
+            auto src = [&](int yy, int xx) { return (int)s4[yy * w + xx]; };
+            // value = v / (4 * 2^(2vb)); rint(8 * value) = rint(v / 2^(2vb - 1))
+            q = rne_shift(warp_fixed32(src, L.h, w, y, x, base.x, base.y, vb), 2 * vb - 1);
+        } else {
+            auto src = [&](int yy, int xx) { return (int)yp[yy * w + xx]; };
+            q = rne_shift(warp_fixed32(src, L.h, w, y, x, base.x, base.y, vb), 2 * vb - 3);
+        }
+        outp[(size_t)y * w + x] = (uint16_t)q;
     }
-    plane<uint16_t>(ws, P, LEVEL == 1 ? P.tq1[d] : P.tq2[d], pair)[i] = (uint16_t)q;
 }
 
 // f32(f64(S / 3)) for S = sn * 2^-k exact (the column / row pass of
@@ -373,7 +413,7 @@ __device__ __forceinline__ float third_f32(int sn, float scale) {
 // can be evaluated tile by tile.  |wl - wr| is integral, so its column pass
 // is exact too; only its row pass (k_rowscan) must replay scipy in order.
 // ---------------------------------------------------------------------------
-constexpr int kTH = 16, kTW = 64;           // output tile
+constexpr int kTH = 16, kTW = 64;           // output tile (256 threads = 4 row groups x 64 cols)
 constexpr int kRH = kTH + 4, kRW = kTW + 4;  // flow region (+-2)
 constexpr int kOH = kTH + 2, kOW = kTW + 2;  // occlusion region (+-1)
 constexpr int kH1 = 13;                      // level-1 rows feeding the region (<= 12)
@@ -391,21 +431,11 @@ struct MaskSmem {
             float o0[2][kTH][kOW];   // column pass (f32, as scipy stores it)
         } occ;
     } u;
-    uint8_t dd[kTH + 2][kTW];  // |wl - wr| rows -1..TH
+    ITap cx_up[kRW], cx_b[kRW];     // per region column: upscale / block taps
+    ITap ry_up[kRH], ry_b[kRH];     // per region row
+    int cx_i[kRW];                  // clamped image column of each region column
+    uint8_t dd[kTH + 2][kTW];       // |wl - wr| rows -1..TH
 };
-
-// warp_fixed with 32-bit coordinates (frames <= 8192 px, validated on the host)
-template <typename Src>
-__device__ __forceinline__ long long warp_fixed32(const Src& src, int h, int w, int y, int x,
-                                                  int fxn, int fyn, int vb) {
-    const ITap tx = clamp_itap32((x << vb) + fxn, vb, w);
-    const ITap ty = clamp_itap32((y << vb) + fyn, vb, h);
-    const int V = 1 << vb;
-    const int top = (V - tx.f) * src(ty.i0, tx.i0) + tx.f * src(ty.i0, tx.i1);
-    const int bot = (V - tx.f) * src(ty.i1, tx.i0) + tx.f * src(ty.i1, tx.i1);
-    // (V - fy) * top + fy * bot == V * top + fy * (bot - top), exact in 64 bits
-    return ((long long)top << vb) + (long long)ty.f * (long long)(bot - top);
-}
 
 __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
                                                    uint8_t* __restrict__ ws, Planes P) {
@@ -414,7 +444,7 @@ __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
     const int W = g.W, H = g.H;
     const int x0 = blockIdx.x * kTW, y0 = blockIdx.y * kTH;
     const int pair = blockIdx.z;
-    const int tid = threadIdx.x, nt = blockDim.x;
+    const int tid = threadIdx.x, tx = tid & 63, tg = tid >> 6;
     const Level L1 = g.lv[1], L2 = g.lv[2];
     const uint8_t* frL = pt.left[pair];
     const uint8_t* frR = pt.right[pair];
@@ -422,127 +452,143 @@ __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
     const int bs = g.fb[2] - (g.fb[1] + 3), rs = g.fb[2] - g.rb[2];
     const int B2 = L2.block, D2 = 2 * B2, lgD2 = 31 - __clz(D2);
 
+    // tap tables: the x-taps are shared by every row, the y-taps by every column
+    if (tid < kRW) {
+        const int xi = clampi(x0 - 2 + tid, 0, W - 1);
+        S.cx_i[tid] = xi;
+        S.cx_up[tid] = clamp_itap32(2 * xi - 1, 2, L1.w);
+        S.cx_b[tid] = clamp_itap32(2 * xi - B2 + 1, lgD2, L2.nbx);
+    } else if (tid >= 128 && tid < 128 + kRH) {
+        const int yi = clampi(y0 - 2 + (tid - 128), 0, H - 1);
+        S.ry_up[tid - 128] = clamp_itap32(2 * yi - 1, 2, L1.h);
+        S.ry_b[tid - 128] = clamp_itap32(2 * yi - B2 + 1, lgD2, L2.nby);
+    }
+    __syncthreads();
+    const int s_lo = S.ry_up[0].i0, s_n = S.ry_up[kRH - 1].i1 - s_lo + 1;
+    const int b_lo = S.ry_b[0].i0, b_n = S.ry_b[kRH - 1].i1 - b_lo + 1;
+
     // (a) final flows (flow.py:122-129 at level 2) and mid flows (interp.py:131-132),
-    //     separably: x-lerp the source rows once, then y-lerp (the reference's order)
-    const int ylo = clampi(y0 - 2, 0, H - 1), yhi = clampi(y0 + kTH + 1, 0, H - 1);
-    const int s_lo = clamp_itap32(2 * ylo - 1, 2, L1.h).i0;
-    const int s_n = clamp_itap32(2 * yhi - 1, 2, L1.h).i1 - s_lo + 1;
-    const int b_lo = clamp_itap32(2 * ylo - B2 + 1, lgD2, L2.nby).i0;
-    const int b_n = clamp_itap32(2 * yhi - B2 + 1, lgD2, L2.nby).i1 - b_lo + 1;
-    for (int i = tid; i < 2 * (s_n + b_n) * kRW; i += nt) {
-        const int d = i / ((s_n + b_n) * kRW);
-        const int j = i - d * ((s_n + b_n) * kRW);
-        const int row = j / kRW, rx = j - row * kRW;
-        const int xi = clampi(x0 - 2 + rx, 0, W - 1);
-        if (row < s_n) {
-            const int2* f1 = cplane<int2>(ws, P, P.flow1[d], pair) + (size_t)(s_lo + row) * L1.w;
-            const ITap tx = clamp_itap32(2 * xi - 1, 2, L1.w);
-            const int2 a = f1[tx.i0], b = f1[tx.i1];
-            S.u.sep.h1[d][row][rx] = make_int2((4 - tx.f) * a.x + tx.f * b.x, (4 - tx.f) * a.y + tx.f * b.y);
-        } else {
-            const int br = row - s_n;
-            const BlockHit* hr = cplane<BlockHit>(ws, P, P.hit[2][d], pair) + (size_t)(b_lo + br) * L2.nbx;
-            const ITap tx = clamp_itap32(2 * xi - B2 + 1, lgD2, L2.nbx);
-            const BlockHit a = hr[tx.i0], b = hr[tx.i1];
-            S.u.sep.hb[d][br][rx] = make_int2((D2 - tx.f) * a.dx + tx.f * b.dx, (D2 - tx.f) * a.dy + tx.f * b.dy);
+    //     separably: x-lerp every source row once, then y-lerp (the reference's order)
+#pragma unroll
+    for (int d = 0; d < 2; d++) {
+        const int2* f1 = cplane<int2>(ws, P, P.flow1[d], pair);
+        const BlockHit* hb = cplane<BlockHit>(ws, P, P.hit[2][d], pair);
+        for (int row = tg; row < s_n + b_n; row += 4) {
+            for (int rx = tx; rx < kRW; rx += 64) {
+                if (row < s_n) {
+                    const int2* fr = f1 + (size_t)(s_lo + row) * L1.w;
+                    const ITap t = S.cx_up[rx];
+                    S.u.sep.h1[d][row][rx] = lerp_i2(fr[t.i0], fr[t.i1], 4, t.f);
+                } else {
+                    const BlockHit* hr = hb + (size_t)(b_lo + row - s_n) * L2.nbx;
+                    const ITap t = S.cx_b[rx];
+                    const BlockHit p = hr[t.i0], q = hr[t.i1];
+                    S.u.sep.hb[d][row - s_n][rx] =
+                        lerp_i2(make_int2(p.dx, p.dy), make_int2(q.dx, q.dy), D2, t.f);
+                }
+            }
         }
     }
     __syncthreads();
-    for (int i = tid; i < 2 * kRH * kRW; i += nt) {
-        const int d = i / (kRH * kRW);
-        const int j = i - d * (kRH * kRW);
-        const int ry = j / kRW, rx = j - ry * kRW;
-        const int yi = clampi(y0 - 2 + ry, 0, H - 1);
-        const ITap ty = clamp_itap32(2 * yi - 1, 2, L1.h);
-        const int2 t = S.u.sep.h1[d][ty.i0 - s_lo][rx], u = S.u.sep.h1[d][ty.i1 - s_lo][rx];
-        const ITap tb = clamp_itap32(2 * yi - B2 + 1, lgD2, L2.nby);
-        const int2 p = S.u.sep.hb[d][tb.i0 - b_lo][rx], q = S.u.sep.hb[d][tb.i1 - b_lo][rx];
-        const int bx_ = (4 - ty.f) * t.x + ty.f * u.x, by_ = (4 - ty.f) * t.y + ty.f * u.y;
-        const int rx_ = (D2 - tb.f) * p.x + tb.f * q.x, ry_ = (D2 - tb.f) * p.y + tb.f * q.y;
-        // f_m = flow * -0.5: in units 2^-(fb2+1) that is -flow_n
-        S.fm[d][ry][rx] = make_int2(-((bx_ << bs) + (rx_ << rs)), -((by_ << bs) + (ry_ << rs)));
+    for (int ry = tg; ry < kRH; ry += 4) {
+        const ITap tu = S.ry_up[ry], tb = S.ry_b[ry];
+        for (int rx = tx; rx < kRW; rx += 64) {
+#pragma unroll
+            for (int d = 0; d < 2; d++) {
+                const int2 base = lerp_i2(S.u.sep.h1[d][tu.i0 - s_lo][rx], S.u.sep.h1[d][tu.i1 - s_lo][rx], 4, tu.f);
+                const int2 res = lerp_i2(S.u.sep.hb[d][tb.i0 - b_lo][rx], S.u.sep.hb[d][tb.i1 - b_lo][rx], D2, tb.f);
+                // f_m = flow * -0.5: in units 2^-(fb2+1) that is -flow_n
+                S.fm[d][ry][rx] = make_int2(-((base.x << bs) + (res.x << rs)), -((base.y << bs) + (res.y << rs)));
+            }
+        }
     }
     __syncthreads();
 
     // (b) occlusion cue at clamped image positions (np.gradient, edge order 1),
     //     in units 2^-(mb+1): interior (f[i+1]-f[i-1])/2 -> diff, edges f[1]-f[0] -> 2*diff
-    for (int i = tid; i < 2 * kOH * kOW; i += nt) {
-        const int d = i / (kOH * kOW);
-        const int j = i - d * (kOH * kOW);
-        const int qy = j / kOW, qx = j - qy * kOW;
-        const int yi = clampi(y0 - 1 + qy, 0, H - 1), xi = clampi(x0 - 1 + qx, 0, W - 1);
-        const int ry = yi - (y0 - 2), rx = xi - (x0 - 2);
-        int gx, gy;
-        if (W < 2) gx = 0;
-        else if (xi == 0) gx = 2 * (S.fm[d][ry][rx + 1].x - S.fm[d][ry][rx].x);
-        else if (xi == W - 1) gx = 2 * (S.fm[d][ry][rx].x - S.fm[d][ry][rx - 1].x);
-        else gx = S.fm[d][ry][rx + 1].x - S.fm[d][ry][rx - 1].x;
-        if (H < 2) gy = 0;
-        else if (yi == 0) gy = 2 * (S.fm[d][ry + 1][rx].y - S.fm[d][ry][rx].y);
-        else if (yi == H - 1) gy = 2 * (S.fm[d][ry][rx].y - S.fm[d][ry - 1][rx].y);
-        else gy = S.fm[d][ry + 1][rx].y - S.fm[d][ry - 1][rx].y;
-        const int v = -(gx + gy);
-        S.u.occ.occ[d][qy][qx] = v > 0 ? v : 0;
+    for (int qy = tg; qy < kOH; qy += 4) {
+        const int yi = clampi(y0 - 1 + qy, 0, H - 1);
+        const int ry = yi - (y0 - 2);
+        for (int qx = tx; qx < kOW; qx += 64) {
+            const int xi = S.cx_i[qx + 1];
+            const int rx = xi - (x0 - 2);
+#pragma unroll
+            for (int d = 0; d < 2; d++) {
+                int gx, gy;
+                if (W < 2) gx = 0;
+                else if (xi == 0) gx = 2 * (S.fm[d][ry][rx + 1].x - S.fm[d][ry][rx].x);
+                else if (xi == W - 1) gx = 2 * (S.fm[d][ry][rx].x - S.fm[d][ry][rx - 1].x);
+                else gx = S.fm[d][ry][rx + 1].x - S.fm[d][ry][rx - 1].x;
+                if (H < 2) gy = 0;
+                else if (yi == 0) gy = 2 * (S.fm[d][ry + 1][rx].y - S.fm[d][ry][rx].y);
+                else if (yi == H - 1) gy = 2 * (S.fm[d][ry][rx].y - S.fm[d][ry - 1][rx].y);
+                else gy = S.fm[d][ry + 1][rx].y - S.fm[d][ry - 1][rx].y;
+                const int v = -(gx + gy);
+                S.u.occ.occ[d][qy][qx] = v > 0 ? v : 0;
+            }
+        }
     }
     __syncthreads();
     const float oscale = 1.0f / (float)(1 << (mb + 1));
     // (c) column pass of smooth3 on occ: exact sum, f32(f64(sum / 3))
-    for (int i = tid; i < 2 * kTH * kOW; i += nt) {
-        const int d = i / (kTH * kOW);
-        const int j = i - d * (kTH * kOW);
-        const int ty = j / kOW, qx = j - ty * kOW;
-        const int sn = S.u.occ.occ[d][ty][qx] + S.u.occ.occ[d][ty + 1][qx] + S.u.occ.occ[d][ty + 2][qx];
-        S.u.occ.o0[d][ty][qx] = sn ? third_f32(sn, oscale) : 0.0f;
-    }
+    for (int ty = tg; ty < kTH; ty += 4)
+        for (int qx = tx; qx < kOW; qx += 64)
+#pragma unroll
+            for (int d = 0; d < 2; d++) {
+                const int sn = S.u.occ.occ[d][ty][qx] + S.u.occ.occ[d][ty + 1][qx] + S.u.occ.occ[d][ty + 2][qx];
+                S.u.occ.o0[d][ty][qx] = sn ? third_f32(sn, oscale) : 0.0f;
+            }
     // (e) luma warps for rows -1..TH (clamped), d = |wl - wr|
     const int kY = 2 * mb;  // luma warp result units 2^-(2 mb)
-    for (int i = tid; i < (kTH + 2) * kTW; i += nt) {
-        const int qy = i / kTW, tx = i - qy * kTW;
-        const int yi = clampi(y0 - 1 + qy, 0, H - 1), xi = x0 + tx;
-        if (xi >= W) continue;
-        const int ry = yi - (y0 - 2), rx = xi - (x0 - 2);
-        const int2 fl = S.fm[0][ry][rx], fr = S.fm[1][ry][rx];
-        const bool center = qy >= 1 && qy <= kTH && y0 - 1 + qy < H;
-        uint8_t wl, wr;
-        if (g.fmt == FVV_RGB8) {
-            uint8_t cl[3], cr[3];
+    {
+        const int xi = x0 + tx;
+        const int rx = tx + 2;
+        for (int qy = tg; qy < kTH + 2; qy += 4) {
+            if (xi >= W) break;
+            const int yi = clampi(y0 - 1 + qy, 0, H - 1);
+            const int ry = yi - (y0 - 2);
+            const int2 fl = S.fm[0][ry][rx], fr = S.fm[1][ry][rx];
+            const bool center = qy >= 1 && qy <= kTH && y0 - 1 + qy < H;
+            uint8_t wl, wr;
+            if (g.fmt == FVV_RGB8) {
+                uint8_t cl[3], cr[3];
 #pragma unroll
-            for (int c = 0; c < 3; c++) {
-                auto sl = [&](int yy, int xx) { return (int)frL[((size_t)yy * W + xx) * 3 + c]; };
-                auto sr = [&](int yy, int xx) { return (int)frR[((size_t)yy * W + xx) * 3 + c]; };
-                cl[c] = (uint8_t)rne_shift(warp_fixed32(sl, H, W, yi, xi, fl.x, fl.y, mb), kY);
-                cr[c] = (uint8_t)rne_shift(warp_fixed32(sr, H, W, yi, xi, fr.x, fr.y, mb), kY);
+                for (int c = 0; c < 3; c++) {
+                    auto sl = [&](int yy, int xx) { return (int)frL[((size_t)yy * W + xx) * 3 + c]; };
+                    auto sr = [&](int yy, int xx) { return (int)frR[((size_t)yy * W + xx) * 3 + c]; };
+                    cl[c] = (uint8_t)rne_shift(warp_fixed32(sl, H, W, yi, xi, fl.x, fl.y, mb), kY);
+                    cr[c] = (uint8_t)rne_shift(warp_fixed32(sr, H, W, yi, xi, fr.x, fr.y, mb), kY);
+                }
+                wl = bt601(cl[0], cl[1], cl[2]);
+                wr = bt601(cr[0], cr[1], cr[2]);
+                if (center) {
+                    uint8_t* o = plane<uint8_t>(ws, P, P.wrgb, pair) + ((size_t)yi * W + xi) * 6;
+#pragma unroll
+                    for (int c = 0; c < 3; c++) { o[c] = cl[c]; o[3 + c] = cr[c]; }
+                }
+            } else {
+                auto sl = [&](int yy, int xx) { return (int)frL[(size_t)yy * W + xx]; };
+                auto sr = [&](int yy, int xx) { return (int)frR[(size_t)yy * W + xx]; };
+                wl = (uint8_t)rne_shift(warp_fixed32(sl, H, W, yi, xi, fl.x, fl.y, mb), kY);
+                wr = (uint8_t)rne_shift(warp_fixed32(sr, H, W, yi, xi, fr.x, fr.y, mb), kY);
             }
-            wl = bt601(cl[0], cl[1], cl[2]);
-            wr = bt601(cr[0], cr[1], cr[2]);
+            S.dd[qy][tx] = (uint8_t)abs((int)wl - (int)wr);
             if (center) {
-                uint8_t* o = plane<uint8_t>(ws, P, P.wrgb, pair) + ((size_t)yi * W + xi) * 6;
-#pragma unroll
-                for (int c = 0; c < 3; c++) { o[c] = cl[c]; o[3 + c] = cr[c]; }
+                plane<uint8_t>(ws, P, P.wl, pair)[(size_t)yi * W + xi] = wl;
+                plane<uint8_t>(ws, P, P.wr, pair)[(size_t)yi * W + xi] = wr;
             }
-        } else {
-            auto sl = [&](int yy, int xx) { return (int)frL[(size_t)yy * W + xx]; };
-            auto sr = [&](int yy, int xx) { return (int)frR[(size_t)yy * W + xx]; };
-            wl = (uint8_t)rne_shift(warp_fixed32(sl, H, W, yi, xi, fl.x, fl.y, mb), kY);
-            wr = (uint8_t)rne_shift(warp_fixed32(sr, H, W, yi, xi, fr.x, fr.y, mb), kY);
-        }
-        S.dd[qy][tx] = (uint8_t)abs((int)wl - (int)wr);
-        if (center) {
-            plane<uint8_t>(ws, P, P.wl, pair)[(size_t)yi * W + xi] = wl;
-            plane<uint8_t>(ws, P, P.wr, pair)[(size_t)yi * W + xi] = wr;
         }
     }
     // (g) chroma warps with the half-resolution, half-magnitude flow
     //     (imageops.py:40-48): ((a+b)+(c+d))/4 * 0.5 of units 2^-mb = sum in units 2^-(mb+3)
     if (g.fmt == FVV_YUV420) {
         const int cw = g.cw, chh = g.ch;
-        const uint8_t* uL = frL + (size_t)W * H;
-        const uint8_t* uR = frR + (size_t)W * H;
-        const size_t cplane_sz = (size_t)cw * chh;
-        const int cb = mb + 3, kC = 2 * cb;
-        for (int i = tid; i < (kTH / 2) * (kTW / 2); i += nt) {
-            const int cy = y0 / 2 + i / (kTW / 2), cx = x0 / 2 + i % (kTW / 2);
-            if (cy >= chh || cx >= cw) continue;
+        const int cy = y0 / 2 + (tid >> 5), cx = x0 / 2 + (tid & 31);  // 8 x 32 chroma px
+        if (cy < chh && cx < cw) {
+            const uint8_t* uL = frL + (size_t)W * H;
+            const uint8_t* uR = frR + (size_t)W * H;
+            const size_t cplane_sz = (size_t)cw * chh;
+            const int cb = mb + 3, kC = 2 * cb;
             const int ry = 2 * cy - (y0 - 2), rx = 2 * cx - (x0 - 2);
             int2 cv[2];
 #pragma unroll
@@ -567,23 +613,25 @@ __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
     __syncthreads();
     // (d) row pass of smooth3 on occ (exact f64 sum of three f32, /3 in f64);
     // (f) column sums of |wl - wr|
-    for (int i = tid; i < kTH * kTW; i += nt) {
-        const int ty = i / kTW, tx = i - ty * kTW;
-        const int yi = y0 + ty, xi = x0 + tx;
-        if (yi >= H || xi >= W) continue;
-        const size_t o = (size_t)yi * W + xi;
+    const int xi = x0 + tx;
+    if (xi < W) {
+        for (int ty = tg; ty < kTH; ty += 4) {
+            const int yi = y0 + ty;
+            if (yi >= H) break;
+            const size_t o = (size_t)yi * W + xi;
 #pragma unroll
-        for (int d = 0; d < 2; d++) {
-            const float a = S.u.occ.o0[d][ty][tx], b = S.u.occ.o0[d][ty][tx + 1], c = S.u.occ.o0[d][ty][tx + 2];
-            float v = 0.0f;
-            if (a != 0.0f || b != 0.0f || c != 0.0f) {
-                const double s = __dadd_rn(__dadd_rn((double)a, (double)b), (double)c);
-                v = (float)__ddiv_rn(s, 3.0);
+            for (int d = 0; d < 2; d++) {
+                const float a = S.u.occ.o0[d][ty][tx], b = S.u.occ.o0[d][ty][tx + 1], c = S.u.occ.o0[d][ty][tx + 2];
+                float v = 0.0f;
+                if (a != 0.0f || b != 0.0f || c != 0.0f) {
+                    const double s3 = __dadd_rn(__dadd_rn((double)a, (double)b), (double)c);
+                    v = (float)__ddiv_rn(s3, 3.0);
+                }
+                plane<float>(ws, P, d ? P.occ_r : P.occ_l, pair)[o] = v;
             }
-            plane<float>(ws, P, d ? P.occ_r : P.occ_l, pair)[o] = v;
+            plane<uint16_t>(ws, P, P.sd, pair)[o] =
+                (uint16_t)((int)S.dd[ty][tx] + (int)S.dd[ty + 1][tx] + (int)S.dd[ty + 2][tx]);
         }
-        plane<uint16_t>(ws, P, P.sd, pair)[o] =
-            (uint16_t)((int)S.dd[ty][tx] + (int)S.dd[ty + 1][tx] + (int)S.dd[ty + 2][tx]);
     }
 }
 
@@ -599,7 +647,7 @@ __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
 // Named barriers hand the double-buffered chunk back and forth.
 // ---------------------------------------------------------------------------
 constexpr int kRB = 32, kCW = 64;
-constexpr int kRowscanThreads = 256, kWorkers = kRowscanThreads - 32;
+constexpr int kWorkers = 256, kRowscanThreads = kWorkers + 32;
 
 __device__ __forceinline__ void bar_sync(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -608,12 +656,27 @@ __device__ __forceinline__ void bar_arrive(int id, int n) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+// mask (warp.py:63) and clip for one pixel from the row-pass running sum
+__device__ __forceinline__ double mask_of(double tsum, float occ_l, float occ_r, const Geometry& g) {
+    const double D = __ddiv_rn(tsum, 3.0);
+    const float ql = __fadd_rn(0.5f, __fmul_rn(4.0f, occ_l));
+    const float qr = __fadd_rn(0.5f, __fmul_rn(4.0f, occ_r));
+    const double el = __dmul_rn(D, (double)ql);
+    const double er = __dmul_rn(D, (double)qr);
+    const double m = __ddiv_rn(__dadd_rn(er, g.eps), __dadd_rn(__dadd_rn(el, er), g.eps2));
+    return fmin(fmax(m, 0.0), 1.0);
+}
+// blend (warp.py:66-67): to_uint8(m * a + (1 - m) * b)
+__device__ __forceinline__ uint8_t blend_px(double m, int a, int b) {
+    return to_u8(__dadd_rn(__dmul_rn(m, (double)a), __dmul_rn(__dsub_rn(1.0, m), (double)b)));
+}
+
 __global__ void __launch_bounds__(kRowscanThreads) k_rowscan(Geometry g, PairTable pt,
                                                               const uint8_t* __restrict__ ws, Planes P,
                                                               int pair_base, bool write_frame,
                                                               double* mask_out /* nullable: one pair */) {
     __shared__ double dtab[766];                // s/3.0 for the integral column sums
-    __shared__ double buf[2][kRB][kCW + 1];     // deltas -> running sums -> masks
+    __shared__ double buf[2][kRB][kCW + 2];     // deltas -> running sums -> masks
     const int W = g.W, H = g.H;
     const int pair = blockIdx.y + pair_base;
     const int y0 = blockIdx.x * kRB;
@@ -623,9 +686,9 @@ __global__ void __launch_bounds__(kRowscanThreads) k_rowscan(Geometry g, PairTab
     for (int i = tid; i < 766; i += kRowscanThreads) dtab[i] = __ddiv_rn((double)i, 3.0);
     __syncthreads();
 
-    if (tid < 32) {
+    if (tid >= kWorkers) {
         // ---------------- chain warp: lane = row ----------------
-        const int r = tid;
+        const int r = tid - kWorkers;
         const bool live = y0 + r < H;
         const uint16_t* row = sd + (size_t)(live ? y0 + r : 0) * W;
         double tmp = 0.0;
@@ -663,82 +726,122 @@ __global__ void __launch_bounds__(kRowscanThreads) k_rowscan(Geometry g, PairTab
         return;
     }
 
-    // ---------------- worker warps ----------------
-    const int wt = tid - 32;
-    const float* ol = cplane<float>(ws, P, P.occ_l, pair);
-    const float* orr = cplane<float>(ws, P, P.occ_r, pair);
-    const uint8_t* wl = cplane<uint8_t>(ws, P, P.wl, pair);
-    const uint8_t* wr = cplane<uint8_t>(ws, P, P.wr, pair);
+    // ---------------- worker warps: thread = (row, 8 consecutive columns) ----------------
+    const int r = tid >> 3, cb = (tid & 7) * 8;
+    const int y = y0 + r;
+    const bool rowok = y < H;
+    const size_t rowoff = (size_t)(rowok ? y : 0) * W;
+    const uint16_t* srow = sd + rowoff;
+    const float* ol = cplane<float>(ws, P, P.occ_l, pair) + rowoff;
+    const float* orr = cplane<float>(ws, P, P.occ_r, pair) + rowoff;
+    const uint8_t* wl = cplane<uint8_t>(ws, P, P.wl, pair) + rowoff;
+    const uint8_t* wr = cplane<uint8_t>(ws, P, P.wr, pair) + rowoff;
     uint8_t* out = pt.out[pair];
 
     auto deltas = [&](int k) {  // p[i+2] - p[i-1] of chunk k (independent of the chain)
-        const int b = k & 1, c0 = k * kCW;
-        for (int i = wt; i < kRB * kCW; i += kWorkers) {
-            const int r = i / kCW, c = i - r * kCW;
-            const int y = y0 + r, x = c0 + c;
-            if (y >= H || x >= W) continue;
-            const uint16_t* row = sd + (size_t)y * W;
-            buf[b][r][c] = __dsub_rn(dtab[row[min(x + 1, W - 1)]], dtab[row[max(x - 2, 0)]]);
-        }
+        const int b = k & 1, x0 = k * kCW + cb;
+        if (!rowok || x0 >= W) return;
+        int s[11];  // sd at x0-2 .. x0+8 (clamped): all loads in flight together
+#pragma unroll
+        for (int j = 0; j < 11; j++) s[j] = srow[clampi(x0 - 2 + j, 0, W - 1)];
+#pragma unroll
+        for (int j = 0; j < 8; j++) buf[b][r][cb + j] = __dsub_rn(dtab[s[j + 3]], dtab[s[j]]);
     };
 
     deltas(0);
     bar_arrive(1, kRowscanThreads);
     for (int k = 0; k < nchunks; k++) {
-        const int b = k & 1, c0 = k * kCW;
+        const int b = k & 1, c0 = k * kCW, x0 = c0 + cb;
         if (k + 1 < nchunks) {
             if (k >= 1) bar_sync(5, kWorkers);  // every worker is done with chunk k-1's buffer
             deltas(k + 1);
             bar_arrive(1 + (b ^ 1), kRowscanThreads);
         }
-        bar_sync(3 + b, kRowscanThreads);  // the chain released chunk k
-        // mask + blend of luma / RGB
-        for (int i = wt; i < kRB * kCW; i += kWorkers) {
-            const int r = i / kCW, c = i - r * kCW;
-            const int y = y0 + r, x = c0 + c;
-            if (y >= H || x >= W) continue;
-            const size_t o = (size_t)y * W + x;
-            const double D = __ddiv_rn(buf[b][r][c], 3.0);
-            const float ql = __fadd_rn(0.5f, __fmul_rn(4.0f, ol[o]));
-            const float qr = __fadd_rn(0.5f, __fmul_rn(4.0f, orr[o]));
-            const double el = __dmul_rn(D, (double)ql);
-            const double er = __dmul_rn(D, (double)qr);
-            double m = __ddiv_rn(__dadd_rn(er, g.eps), __dadd_rn(__dadd_rn(el, er), g.eps2));
-            m = fmin(fmax(m, 0.0), 1.0);
-            const double m1 = __dsub_rn(1.0, m);
-            if (!write_frame) {
-            } else if (g.fmt == FVV_RGB8) {
-                const uint8_t* px = cplane<uint8_t>(ws, P, P.wrgb, pair) + o * 6;
-#pragma unroll
-                for (int ch = 0; ch < 3; ch++)
-                    out[o * 3 + ch] = to_u8(__dadd_rn(__dmul_rn(m, (double)px[ch]),
-                                                      __dmul_rn(m1, (double)px[3 + ch])));
-            } else {
-                out[o] = to_u8(__dadd_rn(__dmul_rn(m, (double)wl[o]), __dmul_rn(m1, (double)wr[o])));
+        // prefetch this thread's 8 pixels of inputs before waiting on the chain
+        const bool full = rowok && x0 + 8 <= W;
+        const bool any = rowok && x0 < W;
+        float4 ola = make_float4(0, 0, 0, 0), olb = ola, ora = ola, orb = ola;
+        uchar4 wla = make_uchar4(0, 0, 0, 0), wlb = wla, wra = wla, wrb = wla;
+        if (full) {
+            ola = *reinterpret_cast<const float4*>(ol + x0);
+            olb = *reinterpret_cast<const float4*>(ol + x0 + 4);
+            ora = *reinterpret_cast<const float4*>(orr + x0);
+            orb = *reinterpret_cast<const float4*>(orr + x0 + 4);
+            if (g.fmt != FVV_RGB8) {
+                wla = *reinterpret_cast<const uchar4*>(wl + x0);
+                wlb = *reinterpret_cast<const uchar4*>(wl + x0 + 4);
+                wra = *reinterpret_cast<const uchar4*>(wr + x0);
+                wrb = *reinterpret_cast<const uchar4*>(wr + x0 + 4);
             }
-            if (mask_out) mask_out[o] = m;
-            buf[b][r][c] = m;
+        } else if (any) {  // W % 4 == 0: exactly 4 valid columns
+            ola = *reinterpret_cast<const float4*>(ol + x0);
+            ora = *reinterpret_cast<const float4*>(orr + x0);
+            if (g.fmt != FVV_RGB8) {
+                wla = *reinterpret_cast<const uchar4*>(wl + x0);
+                wra = *reinterpret_cast<const uchar4*>(wr + x0);
+            }
         }
-        // chroma blend with the 2x2-mean mask (warp.py:83-88)
+        bar_sync(3 + b, kRowscanThreads);  // the chain released chunk k
+        if (any) {
+            const float vl[8] = {ola.x, ola.y, ola.z, ola.w, olb.x, olb.y, olb.z, olb.w};
+            const float vr[8] = {ora.x, ora.y, ora.z, ora.w, orb.x, orb.y, orb.z, orb.w};
+            const int n = full ? 8 : 4;
+            double m[8];
+#pragma unroll
+            for (int j = 0; j < 8; j++)
+                if (j < n) m[j] = mask_of(buf[b][r][cb + j], vl[j], vr[j], g);
+            if (write_frame) {
+                if (g.fmt == FVV_RGB8) {
+                    const uint8_t* px = cplane<uint8_t>(ws, P, P.wrgb, pair) + (rowoff + x0) * 6;
+                    uint8_t* o = out + (rowoff + x0) * 3;
+#pragma unroll
+                    for (int j = 0; j < 8; j++)
+                        if (j < n)
+#pragma unroll
+                            for (int ch = 0; ch < 3; ch++)
+                                o[3 * j + ch] = blend_px(m[j], px[6 * j + ch], px[6 * j + 3 + ch]);
+                } else {
+                    const uint8_t al[8] = {wla.x, wla.y, wla.z, wla.w, wlb.x, wlb.y, wlb.z, wlb.w};
+                    const uint8_t ar[8] = {wra.x, wra.y, wra.z, wra.w, wrb.x, wrb.y, wrb.z, wrb.w};
+                    uint8_t o8[8];
+#pragma unroll
+                    for (int j = 0; j < 8; j++) o8[j] = blend_px(m[j], al[j], ar[j]);
+                    *reinterpret_cast<uchar4*>(out + rowoff + x0) = make_uchar4(o8[0], o8[1], o8[2], o8[3]);
+                    if (full)
+                        *reinterpret_cast<uchar4*>(out + rowoff + x0 + 4) =
+                            make_uchar4(o8[4], o8[5], o8[6], o8[7]);
+                }
+            }
+            if (mask_out) {
+#pragma unroll
+                for (int j = 0; j < 8; j++)
+                    if (j < n) mask_out[rowoff + x0 + j] = m[j];
+            }
+#pragma unroll
+            for (int j = 0; j < 8; j++)
+                if (j < n) buf[b][r][cb + j] = m[j];
+        }
+        // chroma blend with the 2x2-mean mask (warp.py:83-88): thread = (chroma row, 2 columns)
         if (g.fmt == FVV_YUV420 && write_frame) {
             bar_sync(6, kWorkers);  // masks of the whole chunk are in smem
             const int cw = g.cw, chh = g.ch;
-            const uchar4* wc = cplane<uchar4>(ws, P, P.wc, pair);
-            uint8_t* uo = out + (size_t)W * H;
-            uint8_t* vo = uo + (size_t)cw * chh;
-            for (int i = wt; i < (kRB / 2) * (kCW / 2); i += kWorkers) {
-                const int a = i / (kCW / 2), bb = i - a * (kCW / 2);
-                const int cy = y0 / 2 + a, cx = c0 / 2 + bb;
-                if (cy >= chh || cx >= cw) continue;
-                const double s = __dadd_rn(__dadd_rn(buf[b][2 * a][2 * bb], buf[b][2 * a][2 * bb + 1]),
-                                           __dadd_rn(buf[b][2 * a + 1][2 * bb], buf[b][2 * a + 1][2 * bb + 1]));
-                const double mc = __dmul_rn(s, 0.25);  // /4 == *0.25 exactly
-                const double mc1 = __dsub_rn(1.0, mc);
-                const uchar4 q = wc[(size_t)cy * cw + cx];
-                uo[(size_t)cy * cw + cx] = to_u8(__dadd_rn(__dmul_rn(mc, (double)q.x),
-                                                           __dmul_rn(mc1, (double)q.y)));
-                vo[(size_t)cy * cw + cx] = to_u8(__dadd_rn(__dmul_rn(mc, (double)q.z),
-                                                           __dmul_rn(mc1, (double)q.w)));
+            const int a = tid >> 4, c2 = (tid & 15) * 2;  // 16 chroma rows x 32 chroma columns
+            const int cy = y0 / 2 + a, cx = c0 / 2 + c2;
+            if (cy < chh && cx < cw) {
+                const uchar4* wc = cplane<uchar4>(ws, P, P.wc, pair) + (size_t)cy * cw + cx;
+                uint8_t* uo = out + (size_t)W * H + (size_t)cy * cw + cx;
+                uint8_t* vo = uo + (size_t)cw * chh;
+#pragma unroll
+                for (int j = 0; j < 2; j++) {
+                    if (cx + j >= cw) break;
+                    const int bb = c2 + j;
+                    const double sm = __dadd_rn(__dadd_rn(buf[b][2 * a][2 * bb], buf[b][2 * a][2 * bb + 1]),
+                                                __dadd_rn(buf[b][2 * a + 1][2 * bb], buf[b][2 * a + 1][2 * bb + 1]));
+                    const double mc = __dmul_rn(sm, 0.25);  // /4 == *0.25 exactly
+                    const uchar4 q = wc[j];
+                    uo[j] = blend_px(mc, q.x, q.y);
+                    vo[j] = blend_px(mc, q.z, q.w);
+                }
             }
         }
     }
@@ -860,7 +963,8 @@ cudaError_t run_interp_stage(const Geometry& g, const PairTable& pt, uint8_t* ws
     if ((e = E()) != cudaSuccess) return e;
 
     B(KC_WARPQ1);
-    k_warpq<1><<<dim3((n1 + 255) / 256, 1, 2 * npairs), 256, 0, st>>>(g, pt, ws, P);
+    k_warpq<1><<<dim3((g.lv[1].w + kQW - 1) / kQW, (g.lv[1].h + kQH - 1) / kQH, 2 * npairs), 256, 0,
+                 st>>>(g, pt, ws, P);
     if ((e = E()) != cudaSuccess) return e;
 
     B(KC_SAD1);
@@ -872,7 +976,8 @@ cudaError_t run_interp_stage(const Geometry& g, const PairTable& pt, uint8_t* ws
     if ((e = E()) != cudaSuccess) return e;
 
     B(KC_WARPQ2);
-    k_warpq<2><<<dim3((n2 + 255) / 256, 1, 2 * npairs), 256, 0, st>>>(g, pt, ws, P);
+    k_warpq<2><<<dim3((g.lv[2].w + kQW - 1) / kQW, (g.lv[2].h + kQH - 1) / kQH, 2 * npairs), 256, 0,
+                 st>>>(g, pt, ws, P);
     if ((e = E()) != cudaSuccess) return e;
 
     B(KC_SAD2);
