@@ -292,32 +292,6 @@ __global__ void __launch_bounds__(256) k_sad(Geometry g, PairTable pt, uint8_t* 
     }
 }
 
-// ---------------------------------------------------------------------------
-// k_flow<L>: flow_L = base + f32(block_to_pixel(offsets))  (flow.py:122-129)
-// base = 0 at level 0, f32(2 * upscale(flow_{L-1})) otherwise.  Computed in
-// exact fixed point (units 2^-fb[L]); equal to the reference's f32 values.
-// ---------------------------------------------------------------------------
-template <int LEVEL>
-__global__ void k_flow(Geometry g, uint8_t* __restrict__ ws, Planes P) {
-    const Level L = g.lv[LEVEL];
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const int pair = blockIdx.z >> 1, d = blockIdx.z & 1;
-    if (i >= L.w * L.h) return;
-    const int y = i / L.w, x = i - (i / L.w) * L.w;
-    const int2 res = b2p_fixed(cplane<BlockHit>(ws, P, P.hit[LEVEL][d], pair), L.nby, L.nbx, L.block,
-                               y, x);
-    const int rs = g.fb[LEVEL] - g.rb[LEVEL];
-    int2 f = make_int2(res.x << rs, res.y << rs);
-    if (LEVEL > 0) {
-        const Level Lp = g.lv[LEVEL - 1];
-        const int2 base = up2_fixed(cplane<int2>(ws, P, P.flow0[d], pair), Lp.h, Lp.w, y, x);
-        const int bs = g.fb[LEVEL] - (g.fb[LEVEL - 1] + 3);
-        f.x += base.x << bs;
-        f.y += base.y << bs;
-    }
-    plane<int2>(ws, P, LEVEL == 0 ? P.flow0[d] : P.flow1[d], pair)[i] = f;
-}
-
 // warp_fixed with 32-bit coordinates (frames <= 8192 px, validated on the host)
 template <typename Src>
 __device__ __forceinline__ long long warp_fixed32(const Src& src, int h, int w, int y, int x,
@@ -333,6 +307,72 @@ __device__ __forceinline__ long long warp_fixed32(const Src& src, int h, int w, 
 
 __device__ __forceinline__ int2 lerp_i2(int2 a, int2 b, int den, int f) {
     return make_int2((den - f) * a.x + f * b.x, (den - f) * a.y + f * b.y);
+}
+
+// ---------------------------------------------------------------------------
+// k_flow<L>: flow_L = base + f32(block_to_pixel(offsets))  (flow.py:122-129)
+// base = 0 at level 0, f32(2 * upscale(flow_{L-1})) otherwise.  Exact fixed
+// point (units 2^-fb[L]), equal to the reference's f32 values; both bilinear
+// terms are evaluated separably per 16x64 tile (x-lerp rows, then y-lerp).
+// ---------------------------------------------------------------------------
+constexpr int kFH = 16, kFW = 64;
+template <int LEVEL>
+__global__ void __launch_bounds__(256) k_flow(Geometry g, uint8_t* __restrict__ ws, Planes P) {
+    __shared__ int2 hu[kFH / 2 + 3][kFW];   // x-lerped rows of flow_{L-1}
+    __shared__ int2 hb[kFH / 2 + 3][kFW];   // x-lerped block rows (B >= 2)
+    __shared__ ITap cu[kFW], cb[kFW];
+    const Level L = g.lv[LEVEL];
+    const int pair = blockIdx.z >> 1, d = blockIdx.z & 1;
+    const int x0 = blockIdx.x * kFW, y0 = blockIdx.y * kFH;
+    const int tid = threadIdx.x, tx = tid & 63, tg = tid >> 6;
+    const int B = L.block, D = 2 * B, lgD = 31 - __clz(D);
+    const Level Lp = g.lv[LEVEL > 0 ? LEVEL - 1 : 0];
+    const int xc = min(x0 + tx, L.w - 1);
+    if (tid < kFW) {
+        cb[tid] = clamp_itap32(2 * xc - B + 1, lgD, L.nbx);
+        if (LEVEL > 0) cu[tid] = clamp_itap32(2 * xc - 1, 2, Lp.w);
+    }
+    const int ylast = min(y0 + kFH - 1, L.h - 1);
+    const int b_lo = clamp_itap32(2 * y0 - B + 1, lgD, L.nby).i0;
+    const int b_n = clamp_itap32(2 * ylast - B + 1, lgD, L.nby).i1 - b_lo + 1;
+    const int s_lo = LEVEL > 0 ? clamp_itap32(2 * y0 - 1, 2, Lp.h).i0 : 0;
+    const int s_n = LEVEL > 0 ? clamp_itap32(2 * ylast - 1, 2, Lp.h).i1 - s_lo + 1 : 0;
+    __syncthreads();
+    const BlockHit* hit = cplane<BlockHit>(ws, P, P.hit[LEVEL][d], pair);
+    for (int row = tg; row < b_n; row += 4) {
+        const BlockHit* hr = hit + (size_t)(b_lo + row) * L.nbx;
+        const ITap t = cb[tx];
+        const BlockHit p = hr[t.i0], q = hr[t.i1];
+        hb[row][tx] = lerp_i2(make_int2(p.dx, p.dy), make_int2(q.dx, q.dy), D, t.f);
+    }
+    if (LEVEL > 0) {
+        const int2* prev = cplane<int2>(ws, P, P.flow0[d], pair);
+        for (int row = tg; row < s_n; row += 4) {
+            const int2* pr = prev + (size_t)(s_lo + row) * Lp.w;
+            const ITap t = cu[tx];
+            hu[row][tx] = lerp_i2(pr[t.i0], pr[t.i1], 4, t.f);
+        }
+    }
+    __syncthreads();
+    const int x = x0 + tx;
+    if (x >= L.w) return;
+    const int rs = g.fb[LEVEL] - g.rb[LEVEL];
+    const int bs = LEVEL > 0 ? g.fb[LEVEL] - (g.fb[LEVEL - 1] + 3) : 0;
+    int2* out = plane<int2>(ws, P, LEVEL == 0 ? P.flow0[d] : P.flow1[d], pair);
+    for (int ty = tg; ty < kFH; ty += 4) {
+        const int y = y0 + ty;
+        if (y >= L.h) break;
+        const ITap t = clamp_itap32(2 * y - B + 1, lgD, L.nby);
+        const int2 res = lerp_i2(hb[t.i0 - b_lo][tx], hb[t.i1 - b_lo][tx], D, t.f);
+        int2 f = make_int2(res.x << rs, res.y << rs);
+        if (LEVEL > 0) {
+            const ITap u = clamp_itap32(2 * y - 1, 2, Lp.h);
+            const int2 base = lerp_i2(hu[u.i0 - s_lo][tx], hu[u.i1 - s_lo][tx], 4, u.f);
+            f.x += base.x << bs;
+            f.y += base.y << bs;
+        }
+        out[(size_t)y * L.w + x] = f;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -646,8 +686,8 @@ __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
 //   chain has released chunk k -- evaluate mask and blend for it.
 // Named barriers hand the double-buffered chunk back and forth.
 // ---------------------------------------------------------------------------
-constexpr int kRB = 32, kCW = 64;
-constexpr int kWorkers = 256, kRowscanThreads = kWorkers + 32;
+constexpr int kRB = 16, kCW = 64;  // 16-row bands: enough CTAs to hide latency at small stages
+constexpr int kWorkers = kRB * 8, kRowscanThreads = kWorkers + 32;
 
 __device__ __forceinline__ void bar_sync(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -825,7 +865,7 @@ __global__ void __launch_bounds__(kRowscanThreads) k_rowscan(Geometry g, PairTab
         if (g.fmt == FVV_YUV420 && write_frame) {
             bar_sync(6, kWorkers);  // masks of the whole chunk are in smem
             const int cw = g.cw, chh = g.ch;
-            const int a = tid >> 4, c2 = (tid & 15) * 2;  // 16 chroma rows x 32 chroma columns
+            const int a = tid >> 4, c2 = (tid & 15) * 2;  // kRB/2 chroma rows x 32 chroma columns
             const int cy = y0 / 2 + a, cx = c0 / 2 + c2;
             if (cy < chh && cx < cw) {
                 const uchar4* wc = cplane<uchar4>(ws, P, P.wc, pair) + (size_t)cy * cw + cx;
@@ -959,7 +999,8 @@ cudaError_t run_interp_stage(const Geometry& g, const PairTable& pt, uint8_t* ws
     if (e != cudaSuccess || (e = E()) != cudaSuccess) return e;
 
     B(KC_FLOW0);
-    k_flow<0><<<dim3((n0 + 255) / 256, 1, 2 * npairs), 256, 0, st>>>(g, ws, P);
+    k_flow<0><<<dim3((g.lv[0].w + kFW - 1) / kFW, (g.lv[0].h + kFH - 1) / kFH, 2 * npairs), 256, 0,
+                st>>>(g, ws, P);
     if ((e = E()) != cudaSuccess) return e;
 
     B(KC_WARPQ1);
@@ -972,7 +1013,8 @@ cudaError_t run_interp_stage(const Geometry& g, const PairTable& pt, uint8_t* ws
     if (e != cudaSuccess || (e = E()) != cudaSuccess) return e;
 
     B(KC_FLOW1);
-    k_flow<1><<<dim3((n1 + 255) / 256, 1, 2 * npairs), 256, 0, st>>>(g, ws, P);
+    k_flow<1><<<dim3((g.lv[1].w + kFW - 1) / kFW, (g.lv[1].h + kFH - 1) / kFH, 2 * npairs), 256, 0,
+                st>>>(g, ws, P);
     if ((e = E()) != cudaSuccess) return e;
 
     B(KC_WARPQ2);

@@ -79,10 +79,9 @@ struct ClusterJobs {
     ClusterJob job[kMaxClusters];
 };
 
-// source for stitched byte at (plane p, y, x): anchor copy, quarter-tile
-// downscale of view `vi`, or padding (0 luma / 128 chroma)
-__global__ void k_rig_clusters(FrameDims fd, ClusterJobs jobs, const uint8_t* __restrict__ views,
-                               uint8_t* __restrict__ clusters) {
+// Scalar form: one thread = one stitched byte (any geometry the reference accepts).
+__global__ void k_rig_clusters_1(FrameDims fd, ClusterJobs jobs, const uint8_t* __restrict__ views,
+                                 uint8_t* __restrict__ clusters) {
     const ClusterJob jb = jobs.job[blockIdx.z];
     const int sw = jb.sw, sh = fd.H;
     const long ysz = (long)sw * sh;
@@ -90,22 +89,18 @@ __global__ void k_rig_clusters(FrameDims fd, ClusterJobs jobs, const uint8_t* __
     const long total = fd.fmt == FVV_YUV420 ? ysz + 2 * csz : ysz;
     const long o = (long)blockIdx.x * blockDim.x + threadIdx.x;
     if (o >= total) return;
-    int p = 0, x, y, pw, ph;
+    int p = 0;
     long r = o;
     if (o >= ysz) { p = 1 + (int)((o - ysz) / csz); r = (o - ysz) - (p - 1) * csz; }
-    pw = p ? sw / 2 : sw;
-    ph = p ? sh / 2 : sh;
-    (void)ph;
-    y = (int)(r / pw);
-    x = (int)(r % pw);
+    const int pw = p ? sw / 2 : sw;
+    const int y = (int)(r / pw), x = (int)(r % pw);
     const int W = fd.W, H = fd.H;
     const int cellw = W / 4, cellh = H / 4;
-    const int bx = p ? 2 * x : x, byy = p ? 2 * y : y;  // luma-grid position
+    const int bx = p ? 2 * x : x, byy = p ? 2 * y : y;
     uint8_t v;
     if (bx < W) {
         const uint8_t* a = views + (long)jb.anchor_view * fd.bytes;
-        v = p ? a[(long)W * H + (p - 1) * (long)fd.cw * fd.ch + (long)y * fd.cw + x]
-              : a[(long)y * W + x];
+        v = p ? a[(long)W * H + (p - 1) * (long)fd.cw * fd.ch + (long)y * fd.cw + x] : a[(long)y * W + x];
     } else {
         const int col = (bx - W) / cellw, row = byy / cellh;
         const int i = col * 4 + row;
@@ -115,19 +110,77 @@ __global__ void k_rig_clusters(FrameDims fd, ClusterJobs jobs, const uint8_t* __
             int vi = jb.first_small + i;
             if (vi >= jb.skip) vi += 1;
             const uint8_t* src = views + (long)vi * fd.bytes;
-            const int tx = (p ? x - (W + col * cellw) / 2 : x - (W + col * cellw));
-            const int ty = (p ? y - (row * cellh) / 2 : y - row * cellh);
+            const int tx = p ? x - (W + col * cellw) / 2 : x - (W + col * cellw);
+            const int ty = p ? y - (row * cellh) / 2 : y - row * cellh;
             const uint8_t* pl = p ? src + (long)W * H + (p - 1) * (long)fd.cw * fd.ch : src;
             const int spw = p ? fd.cw : W;
             int acc = 0;
-#pragma unroll
             for (int ii = 0; ii < 4; ii++)
-#pragma unroll
                 for (int jj = 0; jj < 4; jj++) acc += pl[(long)(ty * 4 + ii) * spw + tx * 4 + jj];
             v = box_round(acc, 16);
         }
     }
     clusters[jb.out_offset + o] = v;
+}
+
+// Vector form (W % 32 == 0): one thread = 4 consecutive bytes of one plane
+// row: anchor copy, quarter-tile 4x4 box mean of view `vi` (one 16-byte
+// read per source row), or padding (0 luma / 128 chroma).  With W % 32 == 0
+// every cell edge and source row is 16-byte aligned, so a group never
+// straddles a cell.
+__global__ void k_rig_clusters(FrameDims fd, ClusterJobs jobs, const uint8_t* __restrict__ views,
+                               uint8_t* __restrict__ clusters) {
+    const ClusterJob jb = jobs.job[blockIdx.z];
+    const int sw = jb.sw, sh = fd.H;
+    const long ysz = (long)sw * sh;
+    const long csz = (long)(sw / 2) * (sh / 2);
+    const long total = fd.fmt == FVV_YUV420 ? ysz + 2 * csz : ysz;
+    const long o = ((long)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    if (o >= total) return;
+    int p = 0;
+    long r = o;
+    if (o >= ysz) { p = 1 + (int)((o - ysz) / csz); r = (o - ysz) - (p - 1) * csz; }
+    const int pw = p ? sw / 2 : sw;
+    const int y = (int)(r / pw), x = (int)(r % pw);
+    const int W = fd.W, H = fd.H;
+    const int cellw = W / 4, cellh = H / 4;
+    const int bx = p ? 2 * x : x, byy = p ? 2 * y : y;  // luma-grid position
+    uchar4 v;
+    if (bx < W) {
+        const uint8_t* a = views + (long)jb.anchor_view * fd.bytes;
+        const uint8_t* src = p ? a + (long)W * H + (p - 1) * (long)fd.cw * fd.ch + (long)y * fd.cw + x
+                               : a + (long)y * W + x;
+        v = *reinterpret_cast<const uchar4*>(src);
+    } else {
+        const int col = (bx - W) / cellw, row = byy / cellh;
+        const int i = col * 4 + row;
+        if (i >= jb.nsmall) {
+            const uint8_t f = p ? 128 : 0;
+            v = make_uchar4(f, f, f, f);
+        } else {
+            int vi = jb.first_small + i;
+            if (vi >= jb.skip) vi += 1;
+            const uint8_t* src = views + (long)vi * fd.bytes;
+            const int tx = p ? x - (W + col * cellw) / 2 : x - (W + col * cellw);
+            const int ty = p ? y - (row * cellh) / 2 : y - row * cellh;
+            const uint8_t* pl = p ? src + (long)W * H + (p - 1) * (long)fd.cw * fd.ch : src;
+            const int spw = p ? fd.cw : W;
+            int acc[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int ii = 0; ii < 4; ii++) {
+                const uint8_t* rowp = pl + (long)(ty * 4 + ii) * spw + tx * 4;
+                const uint4 q = *reinterpret_cast<const uint4*>(rowp);  // 16 source bytes
+                const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                for (int k = 0; k < 4; k++)
+                    acc[k] += (int)(w4[k] & 0xFF) + (int)((w4[k] >> 8) & 0xFF) +
+                              (int)((w4[k] >> 16) & 0xFF) + (int)(w4[k] >> 24);
+            }
+            v = make_uchar4(box_round(acc[0], 16), box_round(acc[1], 16), box_round(acc[2], 16),
+                            box_round(acc[3], 16));
+        }
+    }
+    *reinterpret_cast<uchar4*>(clusters + jb.out_offset + o) = v;
 }
 
 // assemble_cluster_frame from explicit small tiles (already downscaled)
@@ -200,8 +253,13 @@ cudaError_t launch_rig_clusters(int W, int H, int fmt, const ClusterJob* jobs, i
         ClusterJobs cj;
         int n = njobs - b < kMaxClusters ? njobs - b : kMaxClusters;
         for (int i = 0; i < n; i++) cj.job[i] = jobs[b + i];
-        dim3 grd((unsigned)((max_cluster_bytes + 255) / 256), 1, n);
-        k_rig_clusters<<<grd, 256, 0, st>>>(fd, cj, views, out);
+        if (W % 32 == 0) {
+            dim3 grd((unsigned)((max_cluster_bytes / 4 + 255) / 256), 1, n);
+            k_rig_clusters<<<grd, 256, 0, st>>>(fd, cj, views, out);
+        } else {
+            dim3 grd((unsigned)((max_cluster_bytes + 255) / 256), 1, n);
+            k_rig_clusters_1<<<grd, 256, 0, st>>>(fd, cj, views, out);
+        }
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }

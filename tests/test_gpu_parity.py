@@ -172,3 +172,30 @@ def test_full_1080p_pair_vs_oracle(torch_cuda):
     assert np.array_equal(out[0], ref), f"{np.count_nonzero(out[0] != ref)} bytes differ"
     ref2 = O.interpolate(b, a, w, h, fmt)
     assert np.array_equal(out[1], ref2)
+
+
+@pytest.mark.parametrize("w,h,fmt,cams,stages,vps", [(40, 32, 1, 3, 2, 3), (96, 64, 0, 4, 3, 8),
+                                                      (128, 72, 1, 2, 1, 1)])
+def test_rig_clusters_vs_oracle(torch_cuda, w, h, fmt, cams, stages, vps):
+    """Views and cluster frames of whole rigs (scalar and vector tiling paths)."""
+    from paper_2112_10603_b200.interp import Interpolator
+    from paper_2112_10603_b200.cluster import rig_clusters
+    rng = np.random.default_rng(w + h + cams)
+    frames = [_smooth_pair(rng, w, h, fmt, 4)[0] for _ in range(cams)]
+    cams_np = np.stack(frames)
+    eng = Interpolator(w, h, fmt, max_pairs=(cams - 1) * (1 << (stages - 1)))
+    views = eng.rig(torch_cuda.from_numpy(cams_np).cuda(), stages)
+    ref_views = O.rig_dense_views(cams_np, w, h, fmt, stages)
+    assert np.array_equal(views.cpu().numpy(), ref_views)
+    out, sizes = rig_clusters(views, w, h, fmt, cams, stages, vps)
+    out = out.cpu().numpy()
+    total = ref_views.shape[0]
+    off = 0
+    for c in range(cams):
+        anchor = c << stages
+        lo, hi = max(0, anchor - vps), min(total - 1, anchor + vps)
+        smalls = np.stack([O.downscale(ref_views[i], w, h, fmt, 4) for i in range(lo, hi + 1) if i != anchor])
+        ref, sw = O.assemble_cluster(ref_views[anchor], w, h, fmt, smalls)
+        assert sizes[c] == ref.size
+        assert np.array_equal(out[off:off + sizes[c]], ref), f"cluster {c}"
+        off += sizes[c]
