@@ -729,7 +729,7 @@ __global__ void __launch_bounds__(kRowscanThreads) k_rowscan(Geometry g, PairTab
     if (tid >= kWorkers) {
         // ---------------- chain warp: lane = row ----------------
         const int r = tid - kWorkers;
-        const bool live = y0 + r < H;
+        const bool live = r < kRB && y0 + r < H;
         const uint16_t* row = sd + (size_t)(live ? y0 + r : 0) * W;
         double tmp = 0.0;
         for (int k = 0; k < nchunks; k++) {
