@@ -253,22 +253,13 @@ def run_b200(args, cfg, rank, world, local_rank):
         if vps:
             rig_clusters(views, W, H, fmt, C, S, vps, out=clusters)
 
-    gather_bufs = None
-    if world > 1 and rank == 0:
-        gather_bufs = [torch.empty_like(result) for _ in range(world - 1)]
+    from paper_2112_10603_b200.shard import gather_to_root
+    gather_bufs = [torch.empty_like(result) for _ in range(world - 1)] if world > 1 and rank == 0 else None
 
     def gather():
         # cluster frames of every rank -> the encoder-feeding rank 0 (NCCL over NVLink)
-        if world == 1:
-            return
-        ops = []
-        if rank == 0:
-            for src in range(1, world):
-                ops.append(dist.P2POp(dist.irecv, gather_bufs[src - 1], src))
-        else:
-            ops.append(dist.P2POp(dist.isend, result, 0))
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
+        if world > 1:
+            gather_to_root(result, rank, world, out=gather_bufs)
 
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.synchronize()
