@@ -310,6 +310,157 @@ __device__ __forceinline__ int2 lerp_i2(int2 a, int2 b, int den, int f) {
 }
 
 // ---------------------------------------------------------------------------
+// k_sad8: the 8x8-block search (every BASELINE config) -- same arithmetic as
+// k_sad, restructured for throughput: a CTA covers NBY x NBX blocks, the
+// window is staged with 2-D warp-row loops (no index division), and every
+// thread (one block, one dy, all 2r+1 dx) reads its reference row and its
+// candidate pairs with 16-byte LDS (pair-plane pitch = 4 mod 8 words: eight
+// consecutive dy rows hit eight distinct 16-byte bank groups).
+// ---------------------------------------------------------------------------
+struct Sad8Launch {
+    int nbx, nby;                // blocks per CTA (x, y)
+    int bx_begin, bx_end;        // block columns of this launch (full 8-wide columns)
+    int pw;                      // pair-plane pitch (u32 words), = 4 mod 8
+    int tw;                      // staged target window width (u16 samples)
+    const int16_t* rank_of;
+    const int16_t* cand_of_rank;
+};
+
+template <int LEVEL, int KP>
+__global__ void __launch_bounds__(256) k_sad8(Geometry g, PairTable pt, uint8_t* __restrict__ ws,
+                                              Planes P, Sad8Launch sl) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const Level L = g.lv[LEVEL];
+    const int r = L.r, side = 2 * r + 1;
+    const int pair = blockIdx.z >> 1, d = blockIdx.z & 1;
+    const int bx0 = sl.bx_begin + blockIdx.x * sl.nbx, by0 = blockIdx.y * sl.nby;
+    const int nbx = min(sl.nbx, sl.bx_end - bx0), nby = min(sl.nby, L.nby - by0);
+    const int RW = sl.nbx * 8, RH = sl.nby * 8;      // reference strip (u32 words, duplicated)
+    const int PW = sl.pw, PH = RH + 2 * r;           // pair plane
+    const int TW = sl.tw;                            // raw u16 target window width
+    uint32_t* Rs = reinterpret_cast<uint32_t*>(smem);            // RH x RW
+    uint32_t* Ps = Rs + RH * RW;                                  // PH x PW
+    uint16_t* Ts = reinterpret_cast<uint16_t*>(Ps + PH * PW);     // PH x TW (staging)
+    size_t off = ((size_t)(RH * RW + PH * PW) * 4 + (size_t)PH * TW * 2 + 15) & ~(size_t)15;
+    unsigned long long* best = reinterpret_cast<unsigned long long*>(smem + off);
+    int* suma = reinterpret_cast<int*>(best + sl.nbx * sl.nby);
+    int16_t* rk = reinterpret_cast<int16_t*>(suma + sl.nbx * sl.nby);
+
+    const SadSrc<LEVEL> src = make_src<LEVEL>(g, pt, ws, P, pair, d);
+    const int w = L.w, h = L.h;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    const int ys = by0 * 8, xs = bx0 * 8;
+
+    // raw target window (edge padded: np.pad mode="edge", flow.py:78) and reference strip
+    for (int yy = warp; yy < PH; yy += nwarps) {
+        const int gy = clampi(ys - r + yy, 0, h - 1);
+        for (int xx = lane; xx < TW; xx += 32)
+            Ts[yy * TW + xx] = (uint16_t)src.tgt(gy * w + clampi(xs - r + xx, 0, w - 1));
+    }
+    for (int yy = warp; yy < RH; yy += nwarps) {
+        const int gy = ys + yy;
+        for (int xx = lane; xx < RW; xx += 32) {
+            uint32_t q = 0;
+            if (gy < h && xx < nbx * 8) q = src.ref(gy * w + xs + xx);
+            Rs[yy * RW + xx] = q | (q << 16);
+        }
+    }
+    for (int i = tid; i < side * side; i += blockDim.x) rk[i] = sl.rank_of[i];
+    for (int i = tid; i < sl.nbx * sl.nby; i += blockDim.x) best[i] = ~0ull;
+    __syncthreads();
+    // pair plane: P[y][j] = T[y][j] | T[y][j+1] << 16 (candidates dx, dx+1 in one word)
+    for (int yy = warp; yy < PH; yy += nwarps)
+        for (int j = lane; j < PW; j += 32)
+            Ps[yy * PW + j] = j + 1 < TW ? (uint32_t)Ts[yy * TW + j] | ((uint32_t)Ts[yy * TW + j + 1] << 16) : 0u;
+    // sum of reference samples per block (valid rows only; columns are full here)
+    for (int k = tid; k < sl.nbx * sl.nby; k += blockDim.x) {
+        const int kbx = k % sl.nbx, kby = k / sl.nbx;
+        const int rows = min(8, h - (by0 + kby) * 8);
+        int sacc = 0;
+        for (int yy = 0; yy < rows; yy++)
+            for (int xx = 0; xx < 8; xx++) sacc += (int)(Rs[(kby * 8 + yy) * RW + kbx * 8 + xx] & 0xFFFFu);
+        suma[k] = sacc;
+    }
+    __syncthreads();
+
+    const int kb = tid / side, iy = tid - kb * side;   // block (in CTA), dy + r
+    const int kbx = kb % sl.nbx, kby = kb / sl.nbx;
+    const bool active = kb < sl.nbx * sl.nby && kbx < nbx && kby < nby;
+    if (active) {
+        const int rows = min(8, h - (by0 + kby) * 8);
+        const uint32_t* Rb = Rs + (kby * 8) * RW + kbx * 8;
+        const uint32_t* Pb = Ps + (kby * 8 + iy) * PW + kbx * 8;
+        int tot_lo[KP], tot_hi[KP];
+#pragma unroll
+        for (int k = 0; k < KP; k++) tot_lo[k] = tot_hi[k] = 0;
+#pragma unroll 1
+        for (int y0 = 0; y0 < 8; y0 += 4) {
+            uint32_t am[KP], ab[KP];
+#pragma unroll
+            for (int k = 0; k < KP; k++) am[k] = ab[k] = 0;
+#pragma unroll
+            for (int yy = y0; yy < y0 + 4; yy++) {
+                if (yy < rows) {
+                    constexpr int NP = (2 * KP + 6 + 3) / 4;  // 16-byte groups of candidate pairs
+                    uint32_t pv[4 * NP];
+#pragma unroll
+                    for (int q = 0; q < NP; q++) {
+                        const uint4 v = *reinterpret_cast<const uint4*>(Pb + yy * PW + 4 * q);
+                        pv[4 * q] = v.x; pv[4 * q + 1] = v.y; pv[4 * q + 2] = v.z; pv[4 * q + 3] = v.w;
+                    }
+                    const uint4 ra = *reinterpret_cast<const uint4*>(Rb + yy * RW);
+                    const uint4 rb = *reinterpret_cast<const uint4*>(Rb + yy * RW + 4);
+                    const uint32_t rv[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+#pragma unroll
+                    for (int xx = 0; xx < 8; xx++) {
+#pragma unroll
+                        for (int k = 0; k < KP; k++) {
+                            const uint32_t pp = pv[xx + 2 * k];
+                            am[k] += __vmaxu2(pp, rv[xx]);
+                            ab[k] += pp;
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < KP; k++) {
+                tot_lo[k] += 2 * (int)(am[k] & 0xFFFFu) - (int)(ab[k] & 0xFFFFu);
+                tot_hi[k] += 2 * (int)(am[k] >> 16) - (int)(ab[k] >> 16);
+            }
+        }
+        const int sa = suma[kb];
+        unsigned long long mine = ~0ull;
+#pragma unroll
+        for (int k = 0; k < KP; k++) {
+            const int c0 = 2 * k;
+            if (c0 < side) {
+                const unsigned long long key = ((unsigned long long)(uint32_t)(tot_lo[k] - sa) << 32) |
+                                               (uint32_t)rk[iy * side + c0];
+                mine = key < mine ? key : mine;
+            }
+            if (c0 + 1 < side) {
+                const unsigned long long key = ((unsigned long long)(uint32_t)(tot_hi[k] - sa) << 32) |
+                                               (uint32_t)rk[iy * side + c0 + 1];
+                mine = key < mine ? key : mine;
+            }
+        }
+        atomicMin(&best[kb], mine);
+    }
+    __syncthreads();
+    for (int k = tid; k < sl.nbx * sl.nby; k += blockDim.x) {
+        const int kx = k % sl.nbx, ky = k / sl.nbx;
+        if (kx >= nbx || ky >= nby) continue;
+        const unsigned long long key = best[k];
+        const int idx = sl.cand_of_rank[(int)(key & 0xFFFFFFFFu)];
+        BlockHit hit;
+        hit.dy = (int16_t)(idx / side - r);
+        hit.dx = (int16_t)(idx % side - r);
+        hit.sad = (int32_t)(key >> 32);
+        plane<BlockHit>(ws, P, P.hit[LEVEL][d], pair)[(by0 + ky) * L.nbx + bx0 + kx] = hit;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // k_flow<L>: flow_L = base + f32(block_to_pixel(offsets))  (flow.py:122-129)
 // base = 0 at level 0, f32(2 * upscale(flow_{L-1})) otherwise.  Exact fixed
 // point (units 2^-fb[L]), equal to the reference's f32 values; both bilinear
@@ -944,6 +1095,28 @@ static void pick_kp(int side, int* kp, int* groups) {
     *groups = best_g;
 }
 
+template <int LEVEL, int KP>
+static cudaError_t launch_sad8_kp(const Geometry& g, const PairTable& pt, uint8_t* ws, const Planes& P,
+                                  Sad8Launch sl, int npairs, cudaStream_t st) {
+    const Level& L = g.lv[LEVEL];
+    const int side = 2 * L.r + 1;
+    const int ncols = sl.bx_end - sl.bx_begin;
+    if (ncols <= 0) return cudaSuccess;
+    const int threads = ((sl.nbx * sl.nby * side + 31) / 32) * 32;
+    const int RW = sl.nbx * 8, RH = sl.nby * 8, PH = RH + 2 * L.r;
+    size_t smem = (size_t)(RH * RW + PH * sl.pw) * 4 + (size_t)PH * sl.tw * 2;
+    smem = (smem + 15) & ~(size_t)15;
+    smem += (size_t)sl.nbx * sl.nby * 12 + (size_t)side * side * 2 + 16;
+    auto kern = k_sad8<LEVEL, KP>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    dim3 grid((ncols + sl.nbx - 1) / sl.nbx, (L.nby + sl.nby - 1) / sl.nby, 2 * npairs);
+    kern<<<grid, threads, smem, st>>>(g, pt, ws, P, sl);
+    return cudaGetLastError();
+}
+
 template <int LEVEL>
 static cudaError_t run_sad(const Geometry& g, const PairTable& pt, uint8_t* ws, const Planes& P,
                            const int16_t* rank_of, const int16_t* cand_of_rank, int npairs,
@@ -952,6 +1125,40 @@ static cudaError_t run_sad(const Geometry& g, const PairTable& pt, uint8_t* ws, 
     const int side = 2 * L.r + 1;
     int kp, groups;
     pick_kp(side, &kp, &groups);
+    const bool fast = L.block == 8;
+    const int full_cols = fast ? L.w / 8 : 0;  // block columns with 8 valid columns
+    cudaError_t e;
+    if (full_cols > 0 && groups == 1) {
+        // k_sad8: CTA = nby x nbx blocks, one thread per (block, dy)
+        Sad8Launch s8;
+        s8.rank_of = rank_of;
+        s8.cand_of_rank = cand_of_rank;
+        s8.bx_begin = 0;
+        s8.bx_end = full_cols;
+        const int per_block = side;
+        int nbx = 256 / per_block;                        // blocks per CTA
+        if (nbx > 32) nbx = 32;
+        int nby = 1;
+        if (L.r <= 6) { nby = nbx >= 24 ? 3 : (nbx >= 16 ? 2 : 1); nbx /= nby; }
+        s8.nbx = nbx;
+        s8.nby = nby;
+        const int need = 8 * (nbx - 1) + ((2 * kp + 6 + 3) / 4) * 4;  // words read by the last block
+        int pw = std::max(8 * nbx + 2 * L.r, need);
+        while (pw % 8 != 4) pw++;
+        s8.pw = pw;
+        s8.tw = pw + 1;
+        e = [&]() -> cudaError_t {
+            switch (kp) {
+                case 3: return launch_sad8_kp<LEVEL, 3>(g, pt, ws, P, s8, npairs, st);
+                case 5: return launch_sad8_kp<LEVEL, 5>(g, pt, ws, P, s8, npairs, st);
+                case 7: return launch_sad8_kp<LEVEL, 7>(g, pt, ws, P, s8, npairs, st);
+                case 9: return launch_sad8_kp<LEVEL, 9>(g, pt, ws, P, s8, npairs, st);
+                case 13: return launch_sad8_kp<LEVEL, 13>(g, pt, ws, P, s8, npairs, st);
+                default: return launch_sad8_kp<LEVEL, 16>(g, pt, ws, P, s8, npairs, st);
+            }
+        }();
+        if (e != cudaSuccess) return e;
+    }
     SadLaunch sl;
     sl.groups = groups;
     sl.rank_of = rank_of;
@@ -961,12 +1168,9 @@ static cudaError_t run_sad(const Geometry& g, const PairTable& pt, uint8_t* ws, 
     // every thread reads pair columns [kb*B + dxo, kb*B + dxo + 2*KP + 6)
     sl.pw = sl.nbx_cta * L.block + std::max(2 * L.r + 1, 2 * kp * groups + 6) + 1;
     if ((sl.pw & 1) == 0) sl.pw += 1;  // odd pitch: dy rows fall in distinct banks
-    const bool fast = L.block == 8;
-    const int full_cols = fast ? L.w / 8 : 0;  // block columns with 8 valid columns
-    cudaError_t e;
     // full block columns take the FULL8 path (it guards ragged rows itself);
     // a ragged last block column or other block sizes take the general path
-    if (full_cols > 0) {
+    if (full_cols > 0 && groups != 1) {
         sl.bx_begin = 0;
         sl.bx_end = full_cols;
         e = launch_sad_level<LEVEL, true>(g, pt, ws, P, sl, kp, npairs, st);
