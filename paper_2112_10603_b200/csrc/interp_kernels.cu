@@ -571,12 +571,10 @@ __global__ void __launch_bounds__(256) k_warpq(Geometry g, PairTable pt, uint8_t
         const int2 base = lerp_i2(h[t.i0 - s_lo][tx], h[t.i1 - s_lo][tx], 4, t.f);
         int q;
         if (LEVEL == 1) {
-            auto src = [&](int yy, int xx) { return (int)s4[yy * w + xx]; };
             // value = v / (4 * 2^(2vb)); rint(8 * value) = rint(v / 2^(2vb - 1))
-            q = rne_shift(warp_fixed32(src, L.h, w, y, x, base.x, base.y, vb), 2 * vb - 1);
+            q = rne64(bilin_fixed(s4, w, L.h, w, y, x, base.x, base.y, vb), 2 * vb - 1);
         } else {
-            auto src = [&](int yy, int xx) { return (int)yp[yy * w + xx]; };
-            q = rne_shift(warp_fixed32(src, L.h, w, y, x, base.x, base.y, vb), 2 * vb - 3);
+            q = rne64(bilin_fixed(yp, w, L.h, w, y, x, base.x, base.y, vb), 2 * vb - 3);
         }
         outp[(size_t)y * w + x] = (uint16_t)q;
     }
@@ -747,8 +745,8 @@ __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
                 for (int c = 0; c < 3; c++) {
                     auto sl = [&](int yy, int xx) { return (int)frL[((size_t)yy * W + xx) * 3 + c]; };
                     auto sr = [&](int yy, int xx) { return (int)frR[((size_t)yy * W + xx) * 3 + c]; };
-                    cl[c] = (uint8_t)rne_shift(warp_fixed32(sl, H, W, yi, xi, fl.x, fl.y, mb), kY);
-                    cr[c] = (uint8_t)rne_shift(warp_fixed32(sr, H, W, yi, xi, fr.x, fr.y, mb), kY);
+                    cl[c] = (uint8_t)rne64(warp_fixed32(sl, H, W, yi, xi, fl.x, fl.y, mb), kY);
+                    cr[c] = (uint8_t)rne64(warp_fixed32(sr, H, W, yi, xi, fr.x, fr.y, mb), kY);
                 }
                 wl = bt601(cl[0], cl[1], cl[2]);
                 wr = bt601(cr[0], cr[1], cr[2]);
@@ -758,10 +756,8 @@ __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
                     for (int c = 0; c < 3; c++) { o[c] = cl[c]; o[3 + c] = cr[c]; }
                 }
             } else {
-                auto sl = [&](int yy, int xx) { return (int)frL[(size_t)yy * W + xx]; };
-                auto sr = [&](int yy, int xx) { return (int)frR[(size_t)yy * W + xx]; };
-                wl = (uint8_t)rne_shift(warp_fixed32(sl, H, W, yi, xi, fl.x, fl.y, mb), kY);
-                wr = (uint8_t)rne_shift(warp_fixed32(sr, H, W, yi, xi, fr.x, fr.y, mb), kY);
+                wl = (uint8_t)rne64(bilin_fixed(frL, W, H, W, yi, xi, fl.x, fl.y, mb), kY);
+                wr = (uint8_t)rne64(bilin_fixed(frR, W, H, W, yi, xi, fr.x, fr.y, mb), kY);
             }
             S.dd[qy][tx] = (uint8_t)abs((int)wl - (int)wr);
             if (center) {
@@ -793,10 +789,8 @@ __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
             for (int p = 0; p < 2; p++) {
                 const uint8_t* pl = uL + p * cplane_sz;
                 const uint8_t* pr = uR + p * cplane_sz;
-                auto sl = [&](int yy, int xx) { return (int)pl[(size_t)yy * cw + xx]; };
-                auto sr = [&](int yy, int xx) { return (int)pr[(size_t)yy * cw + xx]; };
-                o[2 * p] = (uint8_t)rne_shift(warp_fixed32(sl, chh, cw, cy, cx, cv[0].x, cv[0].y, cb), kC);
-                o[2 * p + 1] = (uint8_t)rne_shift(warp_fixed32(sr, chh, cw, cy, cx, cv[1].x, cv[1].y, cb), kC);
+                o[2 * p] = (uint8_t)rne64(bilin_fixed(pl, cw, chh, cw, cy, cx, cv[0].x, cv[0].y, cb), kC);
+                o[2 * p + 1] = (uint8_t)rne64(bilin_fixed(pr, cw, chh, cw, cy, cx, cv[1].x, cv[1].y, cb), kC);
             }
             plane<uchar4>(ws, P, P.wc, pair)[(size_t)cy * cw + cx] = make_uchar4(o[0], o[1], o[2], o[3]);
         }
