@@ -466,7 +466,7 @@ __global__ void __launch_bounds__(256) k_sad8(Geometry g, PairTable pt, uint8_t*
 // point (units 2^-fb[L]), equal to the reference's f32 values; both bilinear
 // terms are evaluated separably per 16x64 tile (x-lerp rows, then y-lerp).
 // ---------------------------------------------------------------------------
-constexpr int kFH = 16, kFW = 64;
+constexpr int kFH = 64, kFW = 64;
 template <int LEVEL>
 __global__ void __launch_bounds__(256) k_flow(Geometry g, uint8_t* __restrict__ ws, Planes P) {
     __shared__ int2 hu[kFH / 2 + 3][kFW];   // x-lerped rows of flow_{L-1}
@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(256) k_flow(Geometry g, uint8_t* __restrict__ 
 // 2^-(fb[L-1]+3)), computed separably per 16x64 tile; level-1 samples in
 // units 1/4 (s4), level-2 samples integral (luma).
 // ---------------------------------------------------------------------------
-constexpr int kQH = 16, kQW = 64;
+constexpr int kQH = 64, kQW = 64;  // 16 pixels per thread amortise the tile setup
 template <int LEVEL>
 __global__ void __launch_bounds__(256) k_warpq(Geometry g, PairTable pt, uint8_t* __restrict__ ws,
                                                Planes P) {
@@ -602,11 +602,11 @@ __device__ __forceinline__ float third_f32(int sn, float scale) {
 // can be evaluated tile by tile.  |wl - wr| is integral, so its column pass
 // is exact too; only its row pass (k_rowscan) must replay scipy in order.
 // ---------------------------------------------------------------------------
-constexpr int kTH = 16, kTW = 64;           // output tile (256 threads = 4 row groups x 64 cols)
+constexpr int kTH = 32, kTW = 64;           // output tile (256 threads = 4 row groups x 64 cols)
 constexpr int kRH = kTH + 4, kRW = kTW + 4;  // flow region (+-2)
 constexpr int kOH = kTH + 2, kOW = kTW + 2;  // occlusion region (+-1)
-constexpr int kH1 = 13;                      // level-1 rows feeding the region (<= 12)
-constexpr int kHB = 13;                      // block rows feeding the region (<= 12, B >= 2)
+constexpr int kH1 = kRH / 2 + 3;             // level-1 rows feeding the region
+constexpr int kHB = kRH / 2 + 3;             // block rows feeding the region (B >= 2)
 
 struct MaskSmem {
     int2 fm[2][kRH][kRW];  // mid flows -flow/2, units 2^-(fb2+1)
@@ -770,7 +770,8 @@ __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
     //     (imageops.py:40-48): ((a+b)+(c+d))/4 * 0.5 of units 2^-mb = sum in units 2^-(mb+3)
     if (g.fmt == FVV_YUV420) {
         const int cw = g.cw, chh = g.ch;
-        const int cy = y0 / 2 + (tid >> 5), cx = x0 / 2 + (tid & 31);  // 8 x 32 chroma px
+        for (int cyi = (tid >> 5); cyi < kTH / 2; cyi += 8) {  // kTH/2 x 32 chroma px
+        const int cy = y0 / 2 + cyi, cx = x0 / 2 + (tid & 31);
         if (cy < chh && cx < cw) {
             const uint8_t* uL = frL + (size_t)W * H;
             const uint8_t* uR = frR + (size_t)W * H;
@@ -793,6 +794,7 @@ __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
                 o[2 * p + 1] = (uint8_t)rne64(bilin_fixed(pr, cw, chh, cw, cy, cx, cv[1].x, cv[1].y, cb), kC);
             }
             plane<uchar4>(ws, P, P.wc, pair)[(size_t)cy * cw + cx] = make_uchar4(o[0], o[1], o[2], o[3]);
+        }
         }
     }
     __syncthreads();
