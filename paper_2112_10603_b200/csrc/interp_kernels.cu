@@ -602,7 +602,7 @@ __device__ __forceinline__ float third_f32(int sn, float scale) {
 // can be evaluated tile by tile.  |wl - wr| is integral, so its column pass
 // is exact too; only its row pass (k_rowscan) must replay scipy in order.
 // ---------------------------------------------------------------------------
-constexpr int kTH = 32, kTW = 64;           // output tile (256 threads = 4 row groups x 64 cols)
+constexpr int kTH = 16, kTW = 64;           // output tile (256 threads = 4 row groups x 64 cols)
 constexpr int kRH = kTH + 4, kRW = kTW + 4;  // flow region (+-2)
 constexpr int kOH = kTH + 2, kOW = kTW + 2;  // occlusion region (+-1)
 constexpr int kH1 = kRH / 2 + 3;             // level-1 rows feeding the region
