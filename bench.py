@@ -4,9 +4,12 @@ synthesized virtual views/s at 1080p; per-rig-frame latency).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl b200|reference]
 
-One step = one rig frame per rank: every dense view of every camera gap
-(recursive midpoints, server/pipeline.py:254-271) plus every cluster frame
-(server/pipeline.py:273-292).  Default workload = BASELINE config 4 (8-camera
+One step = a batch of F independent rig frames of the live stream per rank
+(--frames-in-flight, default 2, run concurrently on forked streams inside one
+CUDA graph): every dense view of every camera gap (recursive midpoints,
+server/pipeline.py:254-271) plus every cluster frame (server/pipeline.py:273-292).
+The per-rig-frame latency (one frame in flight) is measured separately and
+reported as config.rig_frame_latency_ms.  Default workload = BASELINE config 4 (8-camera
 1080p YUV420 rig, 7 gaps x 15 views = 105 views, 8 cluster frames), which
 fits one B200.  Multi-GPU: one process per GPU (torchrun), each rank owns
 its own rig frames (frame sharding, weak scaling) and the cluster frames are
@@ -234,51 +237,80 @@ def run_b200(args, cfg, rank, world, local_rank):
     total_views = (C - 1) * (1 << S) + 1
     max_pairs = (C - 1) * (1 << (S - 1))
     npairs_total = step_views  # interpolations per rig frame
-    eng = Interpolator(W, H, fmt, max_pairs=max_pairs, device=dev)
-    fb = eng.frame_bytes
-
-    host_cams = torch.from_numpy(synth_rig(W, H, fmt, C, seed=42 + rank)).pin_memory()
-    cams = host_cams.to(dev)
-    views = torch.empty((total_views, fb), dtype=torch.uint8, device=dev)
-    if vps:
-        sizes = rig_cluster_sizes(W, H, fmt, C, S, vps)
-        clusters = torch.empty(sum(sizes), dtype=torch.uint8, device=dev)
-        result = clusters
-    else:
-        result = views
-    host_out = torch.empty(result.shape, dtype=torch.uint8).pin_memory()
-
-    def compute():
-        eng.rig(cams, S, views)
+    F = max(1, args.frames_in_flight)
+    engines, cams_l, views_l, clusters_l, hosts = [], [], [], [], []
+    for i in range(F):
+        e = Interpolator(W, H, fmt, max_pairs=max_pairs, device=dev)
+        h = torch.from_numpy(synth_rig(W, H, fmt, C, seed=42 + rank * F + i)).pin_memory()
+        engines.append(e)
+        hosts.append(h)
+        cams_l.append(h.to(dev))
+        views_l.append(torch.empty((total_views, e.frame_bytes), dtype=torch.uint8, device=dev))
         if vps:
-            rig_clusters(views, W, H, fmt, C, S, vps, out=clusters)
+            sizes = rig_cluster_sizes(W, H, fmt, C, S, vps)
+            clusters_l.append(torch.empty(sum(sizes), dtype=torch.uint8, device=dev))
+    eng, cams, views = engines[0], cams_l[0], views_l[0]
+    clusters = clusters_l[0] if vps else None
+    results = clusters_l if vps else views_l
+    host_out = [torch.empty(r.shape, dtype=torch.uint8).pin_memory() for r in results]
+
+    def compute_one(i):
+        engines[i].rig(cams_l[i], S, views_l[i])
+        if vps:
+            rig_clusters(views_l[i], W, H, fmt, C, S, vps, out=clusters_l[i])
+
+    stream = torch.cuda.Stream(device=dev)
+    side = [torch.cuda.Stream(device=dev) for _ in range(F)]
+
+    def compute_all():
+        # F independent rig frames of the live stream, forked onto F streams and joined
+        if F == 1:
+            compute_one(0)
+            return
+        cur = torch.cuda.current_stream()
+        fork = torch.cuda.Event()
+        fork.record(cur)
+        joins = []
+        for i in range(F):
+            side[i].wait_event(fork)
+            with torch.cuda.stream(side[i]):
+                compute_one(i)
+                ev = torch.cuda.Event()
+                ev.record(side[i])
+                joins.append(ev)
+        for ev in joins:
+            cur.wait_event(ev)
 
     from paper_2112_10603_b200.shard import gather_to_root
-    gather_bufs = [torch.empty_like(result) for _ in range(world - 1)] if world > 1 and rank == 0 else None
+    gather_bufs = [[torch.empty_like(r) for _ in range(world - 1)] for r in results] \
+        if world > 1 and rank == 0 else None
 
     def gather():
         # cluster frames of every rank -> the encoder-feeding rank 0 (NCCL over NVLink)
         if world > 1:
-            gather_to_root(result, rank, world, out=gather_bufs)
+            for i, r in enumerate(results):
+                gather_to_root(r, rank, world, out=gather_bufs[i] if gather_bufs else None)
 
-    stream = torch.cuda.Stream(device=dev)
     torch.cuda.synchronize()
-    # capture one rig frame of compute as a CUDA graph (kills ~50 launches/step of host overhead)
-    graph = None
+    # capture the step (F rig frames) and a single rig frame as CUDA graphs
+    graph = graph1 = None
     if not args.no_graph:
         with torch.cuda.stream(stream):
-            compute()  # first run outside capture (lazy attributes, allocator)
+            compute_all()  # first run outside capture (lazy attributes, allocator)
         torch.cuda.synchronize()
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph, stream=stream):
-            compute()
+            compute_all()
+        graph1 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph1, stream=stream):
+            compute_one(0)
         torch.cuda.synchronize()
 
     def step():
         if graph is not None:
             graph.replay()
         else:
-            compute()
+            compute_all()
         gather()
 
     with torch.cuda.stream(stream):
@@ -314,7 +346,18 @@ def run_b200(args, cfg, rank, world, local_rank):
     barrier()
     ms = max_over_ranks(t_start.elapsed_time(t_end))
     ms_per_step = ms / args.steps
-    value = world * step_views * args.steps / (ms / 1e3)
+    value = world * F * step_views * args.steps / (ms / 1e3)
+
+    # ---- single rig frame in flight: per-rig-frame latency ------------------
+    with torch.cuda.stream(stream):
+        l0 = torch.cuda.Event(enable_timing=True)
+        l1 = torch.cuda.Event(enable_timing=True)
+        l0.record(stream)
+        for _ in range(max(3, args.steps // 3)):
+            graph1.replay() if graph1 is not None else compute_one(0)
+        l1.record(stream)
+    torch.cuda.synchronize()
+    latency_ms = max_over_ranks(l0.elapsed_time(l1)) / max(3, args.steps // 3)
 
     # ---- e2e: host buffers through the public API, copies inside the region --
     e2e_steps = max(3, args.steps // 2)
@@ -325,14 +368,16 @@ def run_b200(args, cfg, rank, world, local_rank):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(e2e_steps):
-            cams.copy_(host_cams, non_blocking=True)
+            for i in range(F):
+                cams_l[i].copy_(hosts[i], non_blocking=True)
             step()
-            host_out.copy_(result, non_blocking=True)
+            for i in range(F):
+                host_out[i].copy_(results[i], non_blocking=True)
         e1.record(stream)
     torch.cuda.synchronize()
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1))
-    e2e_value = world * step_views * e2e_steps / (e2e_ms / 1e3)
+    e2e_value = world * F * step_views * e2e_steps / (e2e_ms / 1e3)
 
     if rank != 0:
         return 0
@@ -343,7 +388,7 @@ def run_b200(args, cfg, rank, world, local_rank):
     _lib.check(L.fvv_profile_enable(eng._h, 4096))
     with torch.cuda.stream(stream):
         for _ in range(prof_steps):
-            compute()
+            compute_one(0)
     torch.cuda.synchronize()
     n = 10
     ms_k = (ctypes.c_double * n)()
@@ -397,7 +442,7 @@ def run_b200(args, cfg, rank, world, local_rank):
     for s, (lw, _lh) in enumerate([(W // 4, H // 4), (W // 2, H // 2), (W, H)]):
         if lw % 8:
             launches_per_step += per_class[f"k_sad<{s}>"][1]
-    gpu_launches = launches_per_step * args.steps
+    gpu_launches = launches_per_step * F * args.steps
 
     # CPU baseline: oracle port on this box's host cores, bounded sample
     rate, reps, dt, threads = cpu_interp_rate(cfg, budget_s=args.cpu_budget)
@@ -405,16 +450,18 @@ def run_b200(args, cfg, rank, world, local_rank):
            "sample": f"{reps} x interpolate() {W}x{H} {FMT_NAME[fmt]} in {dt:.1f}s (oracle/, C port of "
                      f"the reference path, {threads} threads)"}
 
-    h2d = host_cams.numel()
-    d2h = host_out.numel()
+    h2d = sum(h.numel() for h in hosts)
+    d2h = sum(h.numel() for h in host_out)
     line = {
         "metric": METRIC, "value": value, "unit": "views/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8/i32/f64", "data": "synthetic",
         "config": {"workload": args.config, "desc": cfg["desc"], "width": W, "height": H,
                    "format": FMT_NAME[fmt], "cameras": C, "stages": S, "views_per_side": vps,
-                   "views_per_rig_frame": step_views, "rig_frame_latency_ms": ms_per_step,
-                   "parallelism": f"frame-sharded x{world}" + (" + NCCL gather to rank 0" if world > 1 else ""),
+                   "views_per_rig_frame": step_views, "rig_frames_per_step": F,
+                   "rig_frame_latency_ms": latency_ms,
+                   "parallelism": f"frame-sharded x{world}, {F} rig frames in flight per rank" +
+                                  (" + NCCL gather to rank 0" if world > 1 else ""),
                    "cuda_graph": graph is not None,
                    "l2": "working set > L2 (views %.0f MB + workspace %.0f MB per rank)" % (
                        views.numel() / 1e6, eng.workspace_bytes / 1e6)},
@@ -437,6 +484,8 @@ def main():
     ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--frames-in-flight", type=int, default=2,
+                    help="independent rig frames of the live stream processed concurrently per step")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
