@@ -484,7 +484,7 @@ def main():
     ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-graph", action="store_true")
-    ap.add_argument("--frames-in-flight", type=int, default=2,
+    ap.add_argument("--frames-in-flight", type=int, default=1,
                     help="independent rig frames of the live stream processed concurrently per step")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     args = ap.parse_args()

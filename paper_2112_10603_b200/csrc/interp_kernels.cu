@@ -587,7 +587,7 @@ __global__ void __launch_bounds__(256) k_warpq(Geometry g, PairTable pt, uint8_t
 // reference's double-rounded result; otherwise divide in f64.
 __device__ __forceinline__ float third_f32(int sn, float scale) {
     if (sn < (1 << 24)) return __fmul_rn(__fdiv_rn((float)sn, 3.0f), scale);
-    return (float)__ddiv_rn(__dmul_rn((double)sn, (double)scale), 3.0);
+    return (float)div3(__dmul_rn((double)sn, (double)scale));
 }
 
 // ---------------------------------------------------------------------------
@@ -812,7 +812,7 @@ __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
                 float v = 0.0f;
                 if (a != 0.0f || b != 0.0f || c != 0.0f) {
                     const double s3 = __dadd_rn(__dadd_rn((double)a, (double)b), (double)c);
-                    v = (float)__ddiv_rn(s3, 3.0);
+                    v = (float)div3(s3);
                 }
                 plane<float>(ws, P, d ? P.occ_r : P.occ_l, pair)[o] = v;
             }
@@ -845,13 +845,13 @@ __device__ __forceinline__ void bar_arrive(int id, int n) {
 
 // mask (warp.py:63) and clip for one pixel from the row-pass running sum
 __device__ __forceinline__ double mask_of(double tsum, float occ_l, float occ_r, const Geometry& g) {
-    const double D = __ddiv_rn(tsum, 3.0);
+    const double D = div3(tsum);
     const float ql = __fadd_rn(0.5f, __fmul_rn(4.0f, occ_l));
     const float qr = __fadd_rn(0.5f, __fmul_rn(4.0f, occ_r));
     const double el = __dmul_rn(D, (double)ql);
     const double er = __dmul_rn(D, (double)qr);
     const double m = __ddiv_rn(__dadd_rn(er, g.eps), __dadd_rn(__dadd_rn(el, er), g.eps2));
-    return fmin(fmax(m, 0.0), 1.0);
+    return m < 0.0 ? 0.0 : (m > 1.0 ? 1.0 : m);  // np.clip (m is never NaN: den >= 2 eps)
 }
 // blend (warp.py:66-67): to_uint8(m * a + (1 - m) * b)
 __device__ __forceinline__ uint8_t blend_px(double m, int a, int b) {
