@@ -823,6 +823,220 @@ __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
 }
 
 // ---------------------------------------------------------------------------
+// k_mask_cols: the same computation as k_mask_prod, as a register-streaming
+// column walker.  A warp owns kMW output columns (lanes 2..kMW+1; two halo
+// lanes per side supply x-neighbours through shuffles) and walks down a
+// kMH-row band, carrying lagged sliding windows:
+//   F(y)      mid flows of both directions (separable: x-lerped source rows
+//             are cached and re-used until the row tap moves)
+//   gx(y)     x-gradient of f_m.x (shuffles), occ(y-1) = max(0, -(gx + gy))
+//   O0(y-2)   column pass of smooth3 on occ (exact), O(y-2) row pass (shuffles)
+//   d(y)      |wl - wr| of the luma warps at y, Sd(y-1) its column sum
+//   chroma    at odd rows, from the 2x2 mid flows of the lane pair (x, x+1)
+// Edge rows/columns follow the reference: one-sided np.gradient, nearest
+// padding for smooth3.  No shared memory, no index division.
+// ---------------------------------------------------------------------------
+constexpr int kMW = 28, kMWarps = 4, kMH = 64;
+
+__global__ void __launch_bounds__(kMWarps * 32) k_mask_cols(Geometry g, PairTable pt,
+                                                            uint8_t* __restrict__ ws, Planes P) {
+    const int W = g.W, H = g.H;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int pair = blockIdx.z;
+    const int y0 = blockIdx.y * kMH;
+    const int xw0 = (blockIdx.x * kMWarps + wid) * kMW;
+    if (xw0 >= W) return;  // whole warp outside the frame (no block-level sync in this kernel)
+    const int x = xw0 - 2 + lane;
+    const int xc = clampi(x, 0, W - 1);
+    const bool own = lane >= 2 && lane < 2 + kMW && x < W;
+    const Level L1 = g.lv[1], L2 = g.lv[2];
+    const int B2 = L2.block, D2 = 2 * B2, lgD2 = 31 - __clz(D2);
+    const int mb = g.fb[2] + 1, kY = 2 * mb;
+    const int bs = g.fb[2] - (g.fb[1] + 3), rs = g.fb[2] - g.rb[2];
+    const ITap tu = clamp_itap32(2 * xc - 1, 2, L1.w);
+    const ITap tb = clamp_itap32(2 * xc - B2 + 1, lgD2, L2.nbx);
+    const int2* f1[2] = {cplane<int2>(ws, P, P.flow1[0], pair), cplane<int2>(ws, P, P.flow1[1], pair)};
+    const BlockHit* hh[2] = {cplane<BlockHit>(ws, P, P.hit[2][0], pair),
+                             cplane<BlockHit>(ws, P, P.hit[2][1], pair)};
+    const uint8_t* frL = pt.left[pair];
+    const uint8_t* frR = pt.right[pair];
+    uint8_t* o_wl = plane<uint8_t>(ws, P, P.wl, pair);
+    uint8_t* o_wr = plane<uint8_t>(ws, P, P.wr, pair);
+    uint16_t* o_sd = plane<uint16_t>(ws, P, P.sd, pair);
+    float* o_ol = plane<float>(ws, P, P.occ_l, pair);
+    float* o_or = plane<float>(ws, P, P.occ_r, pair);
+    const float oscale = 1.0f / (float)(1 << (mb + 1));
+    const int ys = max(0, y0 - 2), ye = min(H - 1, y0 + kMH + 1);
+    const int yo1 = min(H, y0 + kMH);  // output rows [y0, yo1)
+
+    auto xl_u = [&](int d, int row) {
+        const int2* r = f1[d] + row * L1.w;
+        return lerp_i2(r[tu.i0], r[tu.i1], 4, tu.f);
+    };
+    auto xl_b = [&](int d, int row) {
+        const BlockHit* r = hh[d] + row * L2.nbx;
+        const BlockHit p = r[tb.i0], q = r[tb.i1];
+        return lerp_i2(make_int2(p.dx, p.dy), make_int2(q.dx, q.dy), D2, tb.f);
+    };
+    // exact f32(f64(a + b + c) / 3) of three f32 smooth3 column outputs
+    auto rowpass = [&](float o0v) {
+        const float l = __shfl_up_sync(0xffffffffu, o0v, 1), r = __shfl_down_sync(0xffffffffu, o0v, 1);
+        const float a = x == 0 ? o0v : l, c = x == W - 1 ? o0v : r;
+        if (a == 0.0f && o0v == 0.0f && c == 0.0f) return 0.0f;
+        return (float)div3(__dadd_rn(__dadd_rn((double)a, (double)o0v), (double)c));
+    };
+    auto colpass = [&](int a, int b, int c) {  // f32(f64(sum/3)) of occ in units 2^-(mb+1)
+        const int sn = a + b + c;
+        return sn ? third_f32(sn, oscale) : 0.0f;
+    };
+
+    int ua = -10, ba = -10;
+    int2 hu0[2], hu1[2], hb0[2], hb1[2];
+    int2 F0[2], F1[2], F2[2];
+    int gx1[2] = {0, 0}, gx2[2] = {0, 0};
+    int oc0[2] = {0, 0}, oc1[2] = {0, 0}, oc2[2] = {0, 0};
+    int d0 = 0, d1 = 0, d2 = 0;
+#pragma unroll
+    for (int d = 0; d < 2; d++) F0[d] = F1[d] = F2[d] = make_int2(0, 0);
+
+    auto emit_o = [&](int t, int a0, int a1, int b0, int b1, int c0, int c1) {
+        // O0(t) from occ(t-1), occ(t), occ(t+1) per direction, then the row pass
+        const float ol = rowpass(colpass(a0, b0, c0));
+        const float orr = rowpass(colpass(a1, b1, c1));
+        if (own) {
+            o_ol[(size_t)t * W + x] = ol;
+            o_or[(size_t)t * W + x] = orr;
+        }
+    };
+
+    for (int yy = ys; yy <= ye; yy++) {
+        // ---- mid flows F(yy) (flow.py:122-129 at level 2, interp.py:131-132) ----
+        const ITap ty = clamp_itap32(2 * yy - 1, 2, L1.h);
+        if (ty.i0 != ua) {
+#pragma unroll
+            for (int d = 0; d < 2; d++) {
+                if (ty.i0 == ua + 1) hu0[d] = hu1[d];
+                else hu0[d] = xl_u(d, ty.i0);
+                hu1[d] = xl_u(d, ty.i1);
+            }
+            ua = ty.i0;
+        }
+        const ITap tby = clamp_itap32(2 * yy - B2 + 1, lgD2, L2.nby);
+        if (tby.i0 != ba) {
+#pragma unroll
+            for (int d = 0; d < 2; d++) {
+                if (tby.i0 == ba + 1) hb0[d] = hb1[d];
+                else hb0[d] = xl_b(d, tby.i0);
+                hb1[d] = xl_b(d, tby.i1);
+            }
+            ba = tby.i0;
+        }
+#pragma unroll
+        for (int d = 0; d < 2; d++) {
+            const int2 base = lerp_i2(hu0[d], hu1[d], 4, ty.f);
+            const int2 res = lerp_i2(hb0[d], hb1[d], D2, tby.f);
+            F0[d] = F1[d];
+            F1[d] = F2[d];
+            F2[d] = make_int2(-((base.x << bs) + (res.x << rs)), -((base.y << bs) + (res.y << rs)));
+            // x-gradient at yy (np.gradient edge order 1), units 2^-(mb+1)
+            const int xl = __shfl_up_sync(0xffffffffu, F2[d].x, 1);
+            const int xr = __shfl_down_sync(0xffffffffu, F2[d].x, 1);
+            gx1[d] = gx2[d];
+            gx2[d] = W < 2 ? 0 : (x == 0 ? 2 * (xr - F2[d].x) : (x == W - 1 ? 2 * (F2[d].x - xl) : xr - xl));
+        }
+        // ---- luma warps at yy (warp.py:37), d = |wl - wr| ----
+        int wl, wr;
+        if (g.fmt == FVV_RGB8) {
+            uint8_t cl[3], cr[3];
+#pragma unroll
+            for (int c = 0; c < 3; c++) {
+                auto sl = [&](int a, int b) { return (int)frL[((size_t)a * W + b) * 3 + c]; };
+                auto sr = [&](int a, int b) { return (int)frR[((size_t)a * W + b) * 3 + c]; };
+                cl[c] = (uint8_t)rne64(warp_fixed32(sl, H, W, yy, xc, F2[0].x, F2[0].y, mb), kY);
+                cr[c] = (uint8_t)rne64(warp_fixed32(sr, H, W, yy, xc, F2[1].x, F2[1].y, mb), kY);
+            }
+            wl = bt601(cl[0], cl[1], cl[2]);
+            wr = bt601(cr[0], cr[1], cr[2]);
+            if (own && yy >= y0 && yy < yo1) {
+                uint8_t* o = plane<uint8_t>(ws, P, P.wrgb, pair) + ((size_t)yy * W + x) * 6;
+#pragma unroll
+                for (int c = 0; c < 3; c++) { o[c] = cl[c]; o[3 + c] = cr[c]; }
+            }
+        } else {
+            wl = rne64(bilin_fixed(frL, W, H, W, yy, xc, F2[0].x, F2[0].y, mb), kY);
+            wr = rne64(bilin_fixed(frR, W, H, W, yy, xc, F2[1].x, F2[1].y, mb), kY);
+        }
+        d0 = d1;
+        d1 = d2;
+        d2 = abs(wl - wr);
+        if (own && yy >= y0 && yy < yo1) {
+            o_wl[(size_t)yy * W + x] = (uint8_t)wl;
+            o_wr[(size_t)yy * W + x] = (uint8_t)wr;
+        }
+        // ---- Sd(yy-1): column sum of d with nearest padding ----
+        {
+            const int t = yy - 1;
+            if (t >= y0 && t < yo1 && own) o_sd[(size_t)t * W + x] = (uint16_t)((t == 0 ? d1 : d0) + d1 + d2);
+        }
+        // ---- occ(yy-1) then O0/O(yy-2) ----
+        {
+            const int r = yy - 1;
+            if (r >= ys && (r == 0 || r - 1 >= ys)) {
+#pragma unroll
+                for (int d = 0; d < 2; d++) {
+                    const int gy = H < 2 ? 0 : (r == 0 ? 2 * (F2[d].y - F1[d].y) : F2[d].y - F0[d].y);
+                    const int v = -(gx1[d] + gy);
+                    oc0[d] = oc1[d];
+                    oc1[d] = oc2[d];
+                    oc2[d] = v > 0 ? v : 0;
+                }
+                const int t2 = yy - 2;  // occ(t2 - 1) = oc0 (or occ(0) at the top), occ(t2) = oc1, occ(t2 + 1) = oc2
+                if (t2 >= y0 && t2 < yo1) {
+                    if (t2 == 0) emit_o(t2, oc1[0], oc1[1], oc1[0], oc1[1], oc2[0], oc2[1]);
+                    else emit_o(t2, oc0[0], oc0[1], oc1[0], oc1[1], oc2[0], oc2[1]);
+                }
+            }
+        }
+        // ---- chroma warps for chroma row (yy-1)/2 at odd yy (imageops.py:40-48) ----
+        if (g.fmt == FVV_YUV420 && (yy & 1) && yy - 1 >= y0 && yy - 1 < yo1 && yy - 1 >= ys) {
+            const int cw = g.cw, chh = g.ch, cb = mb + 3, kC = 2 * cb;
+            int2 cv[2];
+#pragma unroll
+            for (int d = 0; d < 2; d++) {
+                const int sx = F1[d].x + F2[d].x, sy = F1[d].y + F2[d].y;
+                cv[d] = make_int2(sx + __shfl_xor_sync(0xffffffffu, sx, 1),
+                                  sy + __shfl_xor_sync(0xffffffffu, sy, 1));
+            }
+            if (own) {
+                const int cy = (yy - 1) >> 1, cx = x >> 1;
+                const int p = x & 1;  // even lane: U plane, odd lane: V plane
+                const uint8_t* pl = frL + (size_t)W * H + (size_t)p * cw * chh;
+                const uint8_t* pr = frR + (size_t)W * H + (size_t)p * cw * chh;
+                const uint8_t vl = (uint8_t)rne64(bilin_fixed(pl, cw, chh, cw, cy, cx, cv[0].x, cv[0].y, cb), kC);
+                const uint8_t vr = (uint8_t)rne64(bilin_fixed(pr, cw, chh, cw, cy, cx, cv[1].x, cv[1].y, cb), kC);
+                uint8_t* wc = reinterpret_cast<uint8_t*>(plane<uchar4>(ws, P, P.wc, pair) + (size_t)cy * cw + cx);
+                wc[2 * p] = vl;
+                wc[2 * p + 1] = vr;
+            }
+        }
+    }
+    // ---- bottom edge: occ(H-1) (one-sided gy), O0/O(H-2), O0/O(H-1), Sd(H-1) ----
+    if (ye == H - 1) {
+#pragma unroll
+        for (int d = 0; d < 2; d++) {
+            const int gy = H < 2 ? 0 : 2 * (F2[d].y - F1[d].y);
+            const int v = -(gx2[d] + gy);
+            oc0[d] = oc1[d];
+            oc1[d] = oc2[d];
+            oc2[d] = v > 0 ? v : 0;
+        }
+        if (H - 2 >= y0 && H - 2 < yo1) emit_o(H - 2, oc0[0], oc0[1], oc1[0], oc1[1], oc2[0], oc2[1]);
+        if (H - 1 >= y0 && H - 1 < yo1) emit_o(H - 1, oc1[0], oc1[1], oc2[0], oc2[1], oc2[0], oc2[1]);
+        if (own && H - 1 >= y0 && H - 1 < yo1) o_sd[(size_t)(H - 1) * W + x] = (uint16_t)(d1 + d2 + d2);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // k_rowscan: the row pass of smooth3(|wl - wr|) replayed in scipy's order
 // (tmp = (p0+p1)+p2; tmp += p[i+2]-p[i-1]; out = tmp/3, all f64), then the
 // mask (warp.py:49-63) and the blend of every plane (warp.py:66-88).
@@ -1187,7 +1401,6 @@ cudaError_t run_interp_stage(const Geometry& g, const PairTable& pt, uint8_t* ws
     cudaError_t e = cudaSuccess;
     auto B = [&](int c) { if (prof) prof->begin(c, st); };
     auto E = [&]() { if (prof) prof->end(st); return cudaGetLastError(); };
-    const int n0 = g.lv[0].w * g.lv[0].h, n1 = g.lv[1].w * g.lv[1].h, n2 = g.lv[2].w * g.lv[2].h;
 
     B(KC_PYRAMID);
     k_pyramid<<<dim3((g.lv[0].w + 31) / 32, (g.lv[0].h + 7) / 8, 2 * npairs), dim3(32, 8), 0, st>>>(
@@ -1227,17 +1440,8 @@ cudaError_t run_interp_stage(const Geometry& g, const PairTable& pt, uint8_t* ws
     if (e != cudaSuccess || (e = E()) != cudaSuccess) return e;
 
     B(KC_MASK_PROD);
-    {
-        static bool attr_set = false;  // idempotent; racing threads set the same value
-        if (!attr_set) {
-            e = cudaFuncSetAttribute(k_mask_prod, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)sizeof(MaskSmem));
-            if (e != cudaSuccess) return e;
-            attr_set = true;
-        }
-    }
-    k_mask_prod<<<dim3((g.W + kTW - 1) / kTW, (g.H + kTH - 1) / kTH, npairs), 256, sizeof(MaskSmem),
-                  st>>>(g, pt, ws, P);
+    k_mask_cols<<<dim3((g.W + kMW * kMWarps - 1) / (kMW * kMWarps), (g.H + kMH - 1) / kMH, npairs),
+                  kMWarps * 32, 0, st>>>(g, pt, ws, P);
     if ((e = E()) != cudaSuccess) return e;
 
     B(KC_ROWSCAN);
