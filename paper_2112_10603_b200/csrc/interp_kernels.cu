@@ -586,7 +586,7 @@ __global__ void __launch_bounds__(256) k_warpq(Geometry g, PairTable pt, uint8_t
 // binary expansion), so one correctly rounded f32 division gives the
 // reference's double-rounded result; otherwise divide in f64.
 __device__ __forceinline__ float third_f32(int sn, float scale) {
-    if (sn < (1 << 24)) return __fmul_rn(__fdiv_rn((float)sn, 3.0f), scale);
+    if (sn < (1 << 24)) return __fmul_rn(div3f((float)sn), scale);
     return (float)div3(__dmul_rn((double)sn, (double)scale));
 }
 
@@ -838,7 +838,7 @@ __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
 // ---------------------------------------------------------------------------
 constexpr int kMW = 28, kMWarps = 4, kMH = 64;
 
-__global__ void __launch_bounds__(kMWarps * 32) k_mask_cols(Geometry g, PairTable pt,
+__global__ void __launch_bounds__(kMWarps * 32, 6) k_mask_cols(Geometry g, PairTable pt,
                                                             uint8_t* __restrict__ ws, Planes P) {
     const int W = g.W, H = g.H;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -855,6 +855,11 @@ __global__ void __launch_bounds__(kMWarps * 32) k_mask_cols(Geometry g, PairTabl
     const int bs = g.fb[2] - (g.fb[1] + 3), rs = g.fb[2] - g.rb[2];
     const ITap tu = clamp_itap32(2 * xc - 1, 2, L1.w);
     const ITap tb = clamp_itap32(2 * xc - B2 + 1, lgD2, L2.nbx);
+    // x-neighbour lanes with the reference's edge rules folded in: np.gradient is
+    // one-sided at x = 0 / W-1 (neighbour = self, difference doubled in our
+    // units), smooth3's nearest padding repeats the edge value (neighbour = self)
+    const int srcL = x <= 0 ? lane : lane - 1, srcR = x >= W - 1 ? lane : lane + 1;
+    const int gmul = (W >= 2 && (x == 0 || x == W - 1)) ? 2 : (W >= 2 ? 1 : 0);
     const int2* f1[2] = {cplane<int2>(ws, P, P.flow1[0], pair), cplane<int2>(ws, P, P.flow1[1], pair)};
     const BlockHit* hh[2] = {cplane<BlockHit>(ws, P, P.hit[2][0], pair),
                              cplane<BlockHit>(ws, P, P.hit[2][1], pair)};
@@ -880,8 +885,7 @@ __global__ void __launch_bounds__(kMWarps * 32) k_mask_cols(Geometry g, PairTabl
     };
     // exact f32(f64(a + b + c) / 3) of three f32 smooth3 column outputs
     auto rowpass = [&](float o0v) {
-        const float l = __shfl_up_sync(0xffffffffu, o0v, 1), r = __shfl_down_sync(0xffffffffu, o0v, 1);
-        const float a = x == 0 ? o0v : l, c = x == W - 1 ? o0v : r;
+        const float a = __shfl_sync(0xffffffffu, o0v, srcL), c = __shfl_sync(0xffffffffu, o0v, srcR);
         if (a == 0.0f && o0v == 0.0f && c == 0.0f) return 0.0f;
         return (float)div3(__dadd_rn(__dadd_rn((double)a, (double)o0v), (double)c));
     };
@@ -911,13 +915,13 @@ __global__ void __launch_bounds__(kMWarps * 32) k_mask_cols(Geometry g, PairTabl
 
     for (int yy = ys; yy <= ye; yy++) {
         // ---- mid flows F(yy) (flow.py:122-129 at level 2, interp.py:131-132) ----
-        const ITap ty = clamp_itap32(2 * yy - 1, 2, L1.h);
+        const Tap2 ty = tap2(2 * yy - 1, 2, L1.h);  // L1.h >= 2
         if (ty.i0 != ua) {
 #pragma unroll
             for (int d = 0; d < 2; d++) {
                 if (ty.i0 == ua + 1) hu0[d] = hu1[d];
                 else hu0[d] = xl_u(d, ty.i0);
-                hu1[d] = xl_u(d, ty.i1);
+                hu1[d] = xl_u(d, ty.i0 + 1);
             }
             ua = ty.i0;
         }
@@ -939,10 +943,10 @@ __global__ void __launch_bounds__(kMWarps * 32) k_mask_cols(Geometry g, PairTabl
             F1[d] = F2[d];
             F2[d] = make_int2(-((base.x << bs) + (res.x << rs)), -((base.y << bs) + (res.y << rs)));
             // x-gradient at yy (np.gradient edge order 1), units 2^-(mb+1)
-            const int xl = __shfl_up_sync(0xffffffffu, F2[d].x, 1);
-            const int xr = __shfl_down_sync(0xffffffffu, F2[d].x, 1);
+            const int xl = __shfl_sync(0xffffffffu, F2[d].x, srcL);
+            const int xr = __shfl_sync(0xffffffffu, F2[d].x, srcR);
             gx1[d] = gx2[d];
-            gx2[d] = W < 2 ? 0 : (x == 0 ? 2 * (xr - F2[d].x) : (x == W - 1 ? 2 * (F2[d].x - xl) : xr - xl));
+            gx2[d] = gmul * (xr - xl);
         }
         // ---- luma warps at yy (warp.py:37), d = |wl - wr| ----
         int wl, wr;
