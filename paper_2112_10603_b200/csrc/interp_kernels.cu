@@ -838,7 +838,7 @@ __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
 // ---------------------------------------------------------------------------
 constexpr int kMW = 28, kMWarps = 4, kMH = 64;
 
-__global__ void __launch_bounds__(kMWarps * 32, 5) k_mask_cols(Geometry g, PairTable pt,
+__global__ void __launch_bounds__(kMWarps * 32, 6) k_mask_cols(Geometry g, PairTable pt,
                                                             uint8_t* __restrict__ ws, Planes P) {
     const int W = g.W, H = g.H;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -913,9 +913,8 @@ __global__ void __launch_bounds__(kMWarps * 32, 5) k_mask_cols(Geometry g, PairT
         }
     };
 
-    // mid flows at row yy (flow.py:122-129 at level 2, interp.py:131-132); rows
-    // must be requested in increasing order (source-row caches)
-    auto flows_at = [&](int yy, int2* Fo) {
+    for (int yy = ys; yy <= ye; yy++) {
+        // ---- mid flows F(yy) (flow.py:122-129 at level 2, interp.py:131-132) ----
         const Tap2 ty = tap2(2 * yy - 1, 2, L1.h);  // L1.h >= 2
         if (ty.i0 != ua) {
 #pragma unroll
@@ -940,33 +939,9 @@ __global__ void __launch_bounds__(kMWarps * 32, 5) k_mask_cols(Geometry g, PairT
         for (int d = 0; d < 2; d++) {
             const int2 base = lerp_i2(hu0[d], hu1[d], 4, ty.f);
             const int2 res = lerp_i2(hb0[d], hb1[d], D2, tby.f);
-            Fo[d] = make_int2(-((base.x << bs) + (res.x << rs)), -((base.y << bs) + (res.y << rs)));
-        }
-    };
-    const bool rgb = g.fmt == FVV_RGB8;
-    int2 Fn[2];
-    Gath gl, gr;  // luma gathers of the next row, in flight across one iteration
-    flows_at(ys, Fn);
-    if (!rgb) {
-        gl = gather_bilin(frL, W, H, W, ys, xc, Fn[0].x, Fn[0].y, mb);
-        gr = gather_bilin(frR, W, H, W, ys, xc, Fn[1].x, Fn[1].y, mb);
-    }
-
-    for (int yy = ys; yy <= ye; yy++) {
-        const int2 Fc0 = Fn[0], Fc1 = Fn[1];
-        const Gath cl_ = gl, cr_ = gr;
-        if (yy < ye) {
-            flows_at(yy + 1, Fn);
-            if (!rgb) {
-                gl = gather_bilin(frL, W, H, W, yy + 1, xc, Fn[0].x, Fn[0].y, mb);
-                gr = gather_bilin(frR, W, H, W, yy + 1, xc, Fn[1].x, Fn[1].y, mb);
-            }
-        }
-#pragma unroll
-        for (int d = 0; d < 2; d++) {
             F0[d] = F1[d];
             F1[d] = F2[d];
-            F2[d] = d ? Fc1 : Fc0;
+            F2[d] = make_int2(-((base.x << bs) + (res.x << rs)), -((base.y << bs) + (res.y << rs)));
             // x-gradient at yy (np.gradient edge order 1), units 2^-(mb+1)
             const int xl = __shfl_sync(0xffffffffu, F2[d].x, srcL);
             const int xr = __shfl_sync(0xffffffffu, F2[d].x, srcR);
@@ -975,7 +950,7 @@ __global__ void __launch_bounds__(kMWarps * 32, 5) k_mask_cols(Geometry g, PairT
         }
         // ---- luma warps at yy (warp.py:37), d = |wl - wr| ----
         int wl, wr;
-        if (rgb) {
+        if (g.fmt == FVV_RGB8) {
             uint8_t cl[3], cr[3];
 #pragma unroll
             for (int c = 0; c < 3; c++) {
@@ -992,8 +967,8 @@ __global__ void __launch_bounds__(kMWarps * 32, 5) k_mask_cols(Geometry g, PairT
                 for (int c = 0; c < 3; c++) { o[c] = cl[c]; o[3 + c] = cr[c]; }
             }
         } else {
-            wl = rne64(finish_bilin(cl_, mb), kY);
-            wr = rne64(finish_bilin(cr_, mb), kY);
+            wl = rne64(bilin_fixed(frL, W, H, W, yy, xc, F2[0].x, F2[0].y, mb), kY);
+            wr = rne64(bilin_fixed(frR, W, H, W, yy, xc, F2[1].x, F2[1].y, mb), kY);
         }
         d0 = d1;
         d1 = d2;
