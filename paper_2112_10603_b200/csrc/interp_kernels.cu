@@ -461,6 +461,143 @@ __global__ void __launch_bounds__(256) k_sad8(Geometry g, PairTable pt, uint8_t*
 }
 
 // ---------------------------------------------------------------------------
+// k_sadp: 8x8-block search with PIXEL-pair packing.  One 32-bit register
+// holds two horizontally adjacent samples: the reference pair (R[x], R[x+1])
+// and, from the pair plane, the target pair (T[x+dx], T[x+dx+1]).  One
+// VIMNMX.U16x2 then gives max() of one candidate at two pixels, so a row of
+// 8 pixels costs 4 VIMNMX + 4 lane-wise adds per candidate, any (2r+1)
+// candidates, no wasted slot.  A lane sums at most 32 samples per block
+// (<= 32 * 2040 < 2^16): the accumulators never overflow, no flush needed.
+// One thread = one block, one dy, all 2r+1 dx (SIDE = 2r+1, compile time).
+// ---------------------------------------------------------------------------
+struct SadPLaunch {
+    int nbx, nby;         // blocks per CTA
+    int bx_begin, bx_end; // full 8-wide block columns of this launch
+    int pw;               // pair-plane pitch (words), = 4 mod 8
+    int tw;               // raw target window width
+    const int16_t* rank_of;
+    const int16_t* cand_of_rank;
+};
+
+template <int LEVEL, int SIDE>
+__global__ void __launch_bounds__(256) k_sadp(Geometry g, PairTable pt, uint8_t* __restrict__ ws,
+                                              Planes P, SadPLaunch sl) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const Level L = g.lv[LEVEL];
+    constexpr int r = SIDE / 2;
+    const int pair = blockIdx.z >> 1, d = blockIdx.z & 1;
+    const int bx0 = sl.bx_begin + blockIdx.x * sl.nbx, by0 = blockIdx.y * sl.nby;
+    const int nbx = min(sl.nbx, sl.bx_end - bx0), nby = min(sl.nby, L.nby - by0);
+    const int RW = sl.nbx * 4, RH = sl.nby * 8;      // reference pixel pairs (words)
+    const int PW = sl.pw, PH = RH + 2 * r;
+    const int TW = sl.tw;
+    uint32_t* Rs = reinterpret_cast<uint32_t*>(smem);            // RH x RW
+    uint32_t* Ps = Rs + RH * RW;                                  // PH x PW
+    uint16_t* Ts = reinterpret_cast<uint16_t*>(Ps + PH * PW);     // PH x TW (staging)
+    size_t off = ((size_t)(RH * RW + PH * PW) * 4 + (size_t)PH * TW * 2 + 15) & ~(size_t)15;
+    unsigned long long* best = reinterpret_cast<unsigned long long*>(smem + off);
+    int* suma = reinterpret_cast<int*>(best + sl.nbx * sl.nby);
+    int16_t* rk = reinterpret_cast<int16_t*>(suma + sl.nbx * sl.nby);
+
+    const SadSrc<LEVEL> src = make_src<LEVEL>(g, pt, ws, P, pair, d);
+    const int w = L.w, h = L.h;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    const int ys = by0 * 8, xs = bx0 * 8;
+
+    for (int yy = warp; yy < PH; yy += nwarps) {
+        const int gy = clampi(ys - r + yy, 0, h - 1);
+        for (int xx = lane; xx < TW; xx += 32)
+            Ts[yy * TW + xx] = (uint16_t)src.tgt(gy * w + clampi(xs - r + xx, 0, w - 1));
+    }
+    for (int yy = warp; yy < RH; yy += nwarps) {
+        const int gy = ys + yy;
+        for (int xx = lane; xx < RW; xx += 32) {
+            uint32_t q0 = 0, q1 = 0;
+            if (gy < h && 2 * xx < nbx * 8) {
+                q0 = src.ref(gy * w + xs + 2 * xx);
+                q1 = src.ref(gy * w + xs + 2 * xx + 1);
+            }
+            Rs[yy * RW + xx] = q0 | (q1 << 16);
+        }
+    }
+    for (int i = tid; i < SIDE * SIDE; i += blockDim.x) rk[i] = sl.rank_of[i];
+    for (int i = tid; i < sl.nbx * sl.nby; i += blockDim.x) best[i] = ~0ull;
+    __syncthreads();
+    for (int yy = warp; yy < PH; yy += nwarps)
+        for (int j = lane; j < PW; j += 32)
+            Ps[yy * PW + j] = j + 1 < TW ? (uint32_t)Ts[yy * TW + j] | ((uint32_t)Ts[yy * TW + j + 1] << 16) : 0u;
+    for (int k = tid; k < sl.nbx * sl.nby; k += blockDim.x) {
+        const int kbx = k % sl.nbx, kby = k / sl.nbx;
+        const int rows = min(8, h - (by0 + kby) * 8);
+        int sacc = 0;
+        for (int yy = 0; yy < rows; yy++)
+            for (int xx = 0; xx < 4; xx++) {
+                const uint32_t v = Rs[(kby * 8 + yy) * RW + kbx * 4 + xx];
+                sacc += (int)(v & 0xFFFFu) + (int)(v >> 16);
+            }
+        suma[k] = sacc;
+    }
+    __syncthreads();
+
+    const int kb = tid / SIDE, iy = tid - kb * SIDE;   // block (in CTA), dy + r
+    const int kbx = kb % sl.nbx, kby = kb / sl.nbx;
+    const bool active = kb < sl.nbx * sl.nby && kbx < nbx && kby < nby;
+    if (active) {
+        const int rows = min(8, h - (by0 + kby) * 8);
+        const uint32_t* Rb = Rs + (kby * 8) * RW + kbx * 4;
+        const uint32_t* Pb = Ps + (kby * 8 + iy) * PW + kbx * 8;
+        uint32_t am[SIDE], ab[SIDE];
+#pragma unroll
+        for (int c = 0; c < SIDE; c++) am[c] = ab[c] = 0;
+        constexpr int NP = (SIDE + 6 + 3) / 4;  // 16-byte groups covering words 0..SIDE+5
+#pragma unroll 2
+        for (int yy = 0; yy < 8; yy++) {
+            if (yy < rows) {
+                uint32_t pv[4 * NP];
+#pragma unroll
+                for (int q = 0; q < NP; q++) {
+                    const uint4 v = *reinterpret_cast<const uint4*>(Pb + yy * PW + 4 * q);
+                    pv[4 * q] = v.x; pv[4 * q + 1] = v.y; pv[4 * q + 2] = v.z; pv[4 * q + 3] = v.w;
+                }
+                const uint4 rq = *reinterpret_cast<const uint4*>(Rb + yy * RW);
+                const uint32_t rv[4] = {rq.x, rq.y, rq.z, rq.w};
+#pragma unroll
+                for (int k = 0; k < 4; k++)
+#pragma unroll
+                    for (int c = 0; c < SIDE; c++) {
+                        const uint32_t pp = pv[2 * k + c];
+                        am[c] += __vmaxu2(pp, rv[k]);
+                        ab[c] += pp;
+                    }
+            }
+        }
+        const int sa = suma[kb];
+        unsigned long long mine = ~0ull;
+#pragma unroll
+        for (int c = 0; c < SIDE; c++) {
+            const int sad = 2 * ((int)(am[c] & 0xFFFFu) + (int)(am[c] >> 16)) -
+                            ((int)(ab[c] & 0xFFFFu) + (int)(ab[c] >> 16)) - sa;
+            const unsigned long long key = ((unsigned long long)(uint32_t)sad << 32) |
+                                           (uint32_t)rk[iy * SIDE + c];
+            mine = key < mine ? key : mine;
+        }
+        atomicMin(&best[kb], mine);
+    }
+    __syncthreads();
+    for (int k = tid; k < sl.nbx * sl.nby; k += blockDim.x) {
+        const int kx = k % sl.nbx, ky = k / sl.nbx;
+        if (kx >= nbx || ky >= nby) continue;
+        const unsigned long long key = best[k];
+        const int idx = sl.cand_of_rank[(int)(key & 0xFFFFFFFFu)];
+        BlockHit hit;
+        hit.dy = (int16_t)(idx / SIDE - r);
+        hit.dx = (int16_t)(idx % SIDE - r);
+        hit.sad = (int32_t)(key >> 32);
+        plane<BlockHit>(ws, P, P.hit[LEVEL][d], pair)[(by0 + ky) * L.nbx + bx0 + kx] = hit;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // k_flow<L>: flow_L = base + f32(block_to_pixel(offsets))  (flow.py:122-129)
 // base = 0 at level 0, f32(2 * upscale(flow_{L-1})) otherwise.  Exact fixed
 // point (units 2^-fb[L]), equal to the reference's f32 values; both bilinear
@@ -1342,7 +1479,49 @@ static cudaError_t run_sad(const Geometry& g, const PairTable& pt, uint8_t* ws, 
     const bool fast = L.block == 8;
     const int full_cols = fast ? L.w / 8 : 0;  // block columns with 8 valid columns
     cudaError_t e;
-    if (full_cols > 0 && groups == 1) {
+    const bool pix = full_cols > 0 && (side == 3 || side == 5 || side == 9 || side == 13 ||
+                                       side == 17 || side == 25);
+    if (pix) {
+        SadPLaunch sp;
+        sp.rank_of = rank_of;
+        sp.cand_of_rank = cand_of_rank;
+        sp.bx_begin = 0;
+        sp.bx_end = full_cols;
+        int nbx = 256 / side;
+        if (nbx > 32) nbx = 32;
+        int nby = 1;
+        if (L.r <= 6) { nby = nbx >= 24 ? 3 : (nbx >= 16 ? 2 : 1); nbx /= nby; }
+        sp.nbx = nbx;
+        sp.nby = nby;
+        const int need = 8 * (nbx - 1) + ((side + 6 + 3) / 4) * 4;
+        int pw = std::max(8 * nbx + 2 * L.r, need);
+        while (pw % 8 != 4) pw++;
+        sp.pw = pw;
+        sp.tw = pw + 1;
+        const int threads = ((nbx * nby * side + 31) / 32) * 32;
+        const int RW = nbx * 4, RH = nby * 8, PH = RH + 2 * L.r;
+        size_t smem = (size_t)(RH * RW + PH * pw) * 4 + (size_t)PH * sp.tw * 2;
+        smem = (smem + 15) & ~(size_t)15;
+        smem += (size_t)nbx * nby * 12 + (size_t)side * side * 2 + 16;
+        dim3 grid((full_cols + nbx - 1) / nbx, (L.nby + nby - 1) / nby, 2 * npairs);
+        auto go = [&](auto kern) -> cudaError_t {
+            if (smem > 48 * 1024) {
+                cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                if (e2 != cudaSuccess) return e2;
+            }
+            kern<<<grid, threads, smem, st>>>(g, pt, ws, P, sp);
+            return cudaGetLastError();
+        };
+        switch (side) {
+            case 3: e = go(k_sadp<LEVEL, 3>); break;
+            case 5: e = go(k_sadp<LEVEL, 5>); break;
+            case 9: e = go(k_sadp<LEVEL, 9>); break;
+            case 13: e = go(k_sadp<LEVEL, 13>); break;
+            case 17: e = go(k_sadp<LEVEL, 17>); break;
+            default: e = go(k_sadp<LEVEL, 25>); break;
+        }
+        if (e != cudaSuccess) return e;
+    } else if (full_cols > 0 && groups == 1) {
         // k_sad8: CTA = nby x nbx blocks, one thread per (block, dy)
         Sad8Launch s8;
         s8.rank_of = rank_of;
@@ -1384,7 +1563,7 @@ static cudaError_t run_sad(const Geometry& g, const PairTable& pt, uint8_t* ws, 
     if ((sl.pw & 1) == 0) sl.pw += 1;  // odd pitch: dy rows fall in distinct banks
     // full block columns take the FULL8 path (it guards ragged rows itself);
     // a ragged last block column or other block sizes take the general path
-    if (full_cols > 0 && groups != 1) {
+    if (full_cols > 0 && groups != 1 && !pix) {
         sl.bx_begin = 0;
         sl.bx_end = full_cols;
         e = launch_sad_level<LEVEL, true>(g, pt, ws, P, sl, kp, npairs, st);
