@@ -1479,8 +1479,10 @@ static cudaError_t run_sad(const Geometry& g, const PairTable& pt, uint8_t* ws, 
     const bool fast = L.block == 8;
     const int full_cols = fast ? L.w / 8 : 0;  // block columns with 8 valid columns
     cudaError_t e;
+    // pixel-pair packing wins for small candidate rows; at 2r+1 = 25 its 50
+    // accumulators cost occupancy, and the candidate-pair kernel is faster
     const bool pix = full_cols > 0 && (side == 3 || side == 5 || side == 9 || side == 13 ||
-                                       side == 17 || side == 25);
+                                       side == 17);
     if (pix) {
         SadPLaunch sp;
         sp.rank_of = rank_of;
@@ -1517,8 +1519,7 @@ static cudaError_t run_sad(const Geometry& g, const PairTable& pt, uint8_t* ws, 
             case 5: e = go(k_sadp<LEVEL, 5>); break;
             case 9: e = go(k_sadp<LEVEL, 9>); break;
             case 13: e = go(k_sadp<LEVEL, 13>); break;
-            case 17: e = go(k_sadp<LEVEL, 17>); break;
-            default: e = go(k_sadp<LEVEL, 25>); break;
+            default: e = go(k_sadp<LEVEL, 17>); break;
         }
         if (e != cudaSuccess) return e;
     } else if (full_cols > 0 && groups == 1) {
