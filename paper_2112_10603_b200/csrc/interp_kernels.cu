@@ -975,8 +975,9 @@ __global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
 // ---------------------------------------------------------------------------
 constexpr int kMW = 28, kMWarps = 4, kMH = 64;
 
+template <int FMT>
 __global__ void __launch_bounds__(kMWarps * 32, 6) k_mask_cols(Geometry g, PairTable pt,
-                                                            uint8_t* __restrict__ ws, Planes P) {
+                                                               uint8_t* __restrict__ ws, Planes P) {
     const int W = g.W, H = g.H;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int pair = blockIdx.z;
@@ -1087,7 +1088,7 @@ __global__ void __launch_bounds__(kMWarps * 32, 6) k_mask_cols(Geometry g, PairT
         }
         // ---- luma warps at yy (warp.py:37), d = |wl - wr| ----
         int wl, wr;
-        if (g.fmt == FVV_RGB8) {
+        if (FMT == FVV_RGB8) {
             uint8_t cl[3], cr[3];
 #pragma unroll
             for (int c = 0; c < 3; c++) {
@@ -1139,7 +1140,7 @@ __global__ void __launch_bounds__(kMWarps * 32, 6) k_mask_cols(Geometry g, PairT
             }
         }
         // ---- chroma warps for chroma row (yy-1)/2 at odd yy (imageops.py:40-48) ----
-        if (g.fmt == FVV_YUV420 && (yy & 1) && yy - 1 >= y0 && yy - 1 < yo1 && yy - 1 >= ys) {
+        if (FMT == FVV_YUV420 && (yy & 1) && yy - 1 >= y0 && yy - 1 < yo1 && yy - 1 >= ys) {
             const int cw = g.cw, chh = g.ch, cb = mb + 3, kC = 2 * cb;
             int2 cv[2];
 #pragma unroll
@@ -1624,8 +1625,12 @@ cudaError_t run_interp_stage(const Geometry& g, const PairTable& pt, uint8_t* ws
     if (e != cudaSuccess || (e = E()) != cudaSuccess) return e;
 
     B(KC_MASK_PROD);
-    k_mask_cols<<<dim3((g.W + kMW * kMWarps - 1) / (kMW * kMWarps), (g.H + kMH - 1) / kMH, npairs),
-                  kMWarps * 32, 0, st>>>(g, pt, ws, P);
+    {
+        const dim3 grd((g.W + kMW * kMWarps - 1) / (kMW * kMWarps), (g.H + kMH - 1) / kMH, npairs);
+        if (g.fmt == FVV_YUV420) k_mask_cols<FVV_YUV420><<<grd, kMWarps * 32, 0, st>>>(g, pt, ws, P);
+        else if (g.fmt == FVV_RGB8) k_mask_cols<FVV_RGB8><<<grd, kMWarps * 32, 0, st>>>(g, pt, ws, P);
+        else k_mask_cols<FVV_GRAY8><<<grd, kMWarps * 32, 0, st>>>(g, pt, ws, P);
+    }
     if ((e = E()) != cudaSuccess) return e;
 
     B(KC_ROWSCAN);
