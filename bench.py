@@ -157,7 +157,7 @@ def kernel_figures(cfg, npairs_total):
         "k_sad<1>": ("int", "Gop/s", sad[1]),
         "k_sad<2>": ("int", "Gop/s", sad[2]),
         # warp + mask + blend: 2 source frames read, 1 view written (compulsory)
-        "k_mask_prod": ("hbm", "GB/s", 2 * bframe * npairs_total),
+        "k_mask_cols": ("hbm", "GB/s", 2 * bframe * npairs_total),
         "k_rowscan": ("hbm", "GB/s", bframe * npairs_total),
         "k_warpq<2>": ("hbm", "GB/s", (2 * W * H + 2 * 2 * W * H + 16 * W * H / 4) * npairs_total),
     }
@@ -426,14 +426,17 @@ def run_b200(args, cfg, rank, world, local_rank):
         peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e9
         peak_note = ("derived: 148 SMs x 128 lanes x 2 (u16x2) abs-diffs/clk at the median SM clock "
                      "under load; no measured INT peak in MEASURED_PEAKS.json")
-    traffic = None
+    traffic = None  # DRAM bytes per step of the dominant kernel class, from a committed ncu capture
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            traffic = json.load(f).get(args.config, {}).get(dom)
-    except OSError:
+            t = json.load(f).get(args.config, {}).get(dom)
+        if t:
+            traffic = t["dram_bytes_per_pair"] * npairs_total
+    except (OSError, KeyError, ValueError):
         pass
     roofline = {"bound": bound, "kernel": dom, "achieved": achieved, "peak": peak, "unit": unit,
-                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_note,
+                "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per step (ncu dram read+write)",
+                "peak_source": peak_note,
                 "kernel_ms_per_step": dom_ms, "kernel_share_of_step": dom_ms / step_kernel_ms,
                 "per_kernel_ms_per_step": {k: round(v[0], 4) for k, v in per_class.items()}}
 

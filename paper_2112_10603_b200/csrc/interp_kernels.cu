@@ -6,7 +6,7 @@
 //   k_sad<L>     exhaustive SAD block search + tie rule    flow.py:69-91, _kernels.py:28-49
 //   k_flow<L>    flow = upscale(prev) + block_to_pixel     flow.py:47-54, 94-98, 129
 //   k_warpq<L>   target warped by the base flow, *8, rint  flow.py:123-124, 77-78
-//   k_mask_prod  final flows, mid warps, |wl-wr| column    interp.py:131-136, 78-94
+//   k_mask_cols  final flows, mid warps, |wl-wr| column    interp.py:131-136, 78-94
 //                sums, occlusion cue (exact, order-free)   warp.py:27-46
 //   k_rowscan    scipy running-sum replay along rows,      imageops.py:51-52, warp.py:49-88
 //                mask, blend of every plane
@@ -728,239 +728,14 @@ __device__ __forceinline__ float third_f32(int sn, float scale) {
 }
 
 // ---------------------------------------------------------------------------
-// k_mask_prod: per 16x32 output tile, everything of _mask_inputs
-// (interp.py:78-94) that does not depend on scipy's order of summation,
-// plus the mid warps of every plane (warp.py:27-46).
-//
-// Exactness: with power-of-two blocks every flow value is
-// a dyadic rational with <= 24 significant bits, so np.gradient, the f32
-// occlusion cue and BOTH smoothing passes over it are exact sums -- the
-// running sum of uniform_filter1d equals the plain 3-tap sum bitwise and
-// can be evaluated tile by tile.  |wl - wr| is integral, so its column pass
-// is exact too; only its row pass (k_rowscan) must replay scipy in order.
-// ---------------------------------------------------------------------------
-constexpr int kTH = 16, kTW = 64;           // output tile (256 threads = 4 row groups x 64 cols)
-constexpr int kRH = kTH + 4, kRW = kTW + 4;  // flow region (+-2)
-constexpr int kOH = kTH + 2, kOW = kTW + 2;  // occlusion region (+-1)
-constexpr int kH1 = kRH / 2 + 3;             // level-1 rows feeding the region
-constexpr int kHB = kRH / 2 + 3;             // block rows feeding the region (B >= 2)
-
-struct MaskSmem {
-    int2 fm[2][kRH][kRW];  // mid flows -flow/2, units 2^-(fb2+1)
-    union {
-        struct {           // separable passes (x-lerp of the source rows)
-            int2 h1[2][kH1][kRW];
-            int2 hb[2][kHB][kRW];
-        } sep;
-        struct {
-            int occ[2][kOH][kOW];    // max(0, -div), units 2^-(fb2+2)
-            float o0[2][kTH][kOW];   // column pass (f32, as scipy stores it)
-        } occ;
-    } u;
-    ITap cx_up[kRW], cx_b[kRW];     // per region column: upscale / block taps
-    ITap ry_up[kRH], ry_b[kRH];     // per region row
-    int cx_i[kRW];                  // clamped image column of each region column
-    uint8_t dd[kTH + 2][kTW];       // |wl - wr| rows -1..TH
-};
-
-__global__ void __launch_bounds__(256) k_mask_prod(Geometry g, PairTable pt,
-                                                   uint8_t* __restrict__ ws, Planes P) {
-    extern __shared__ __align__(16) uint8_t smem_raw[];
-    MaskSmem& S = *reinterpret_cast<MaskSmem*>(smem_raw);
-    const int W = g.W, H = g.H;
-    const int x0 = blockIdx.x * kTW, y0 = blockIdx.y * kTH;
-    const int pair = blockIdx.z;
-    const int tid = threadIdx.x, tx = tid & 63, tg = tid >> 6;
-    const Level L1 = g.lv[1], L2 = g.lv[2];
-    const uint8_t* frL = pt.left[pair];
-    const uint8_t* frR = pt.right[pair];
-    const int mb = g.fb[2] + 1;                      // mid-flow fraction bits
-    const int bs = g.fb[2] - (g.fb[1] + 3), rs = g.fb[2] - g.rb[2];
-    const int B2 = L2.block, D2 = 2 * B2, lgD2 = 31 - __clz(D2);
-
-    // tap tables: the x-taps are shared by every row, the y-taps by every column
-    if (tid < kRW) {
-        const int xi = clampi(x0 - 2 + tid, 0, W - 1);
-        S.cx_i[tid] = xi;
-        S.cx_up[tid] = clamp_itap32(2 * xi - 1, 2, L1.w);
-        S.cx_b[tid] = clamp_itap32(2 * xi - B2 + 1, lgD2, L2.nbx);
-    } else if (tid >= 128 && tid < 128 + kRH) {
-        const int yi = clampi(y0 - 2 + (tid - 128), 0, H - 1);
-        S.ry_up[tid - 128] = clamp_itap32(2 * yi - 1, 2, L1.h);
-        S.ry_b[tid - 128] = clamp_itap32(2 * yi - B2 + 1, lgD2, L2.nby);
-    }
-    __syncthreads();
-    const int s_lo = S.ry_up[0].i0, s_n = S.ry_up[kRH - 1].i1 - s_lo + 1;
-    const int b_lo = S.ry_b[0].i0, b_n = S.ry_b[kRH - 1].i1 - b_lo + 1;
-
-    // (a) final flows (flow.py:122-129 at level 2) and mid flows (interp.py:131-132),
-    //     separably: x-lerp every source row once, then y-lerp (the reference's order)
-#pragma unroll
-    for (int d = 0; d < 2; d++) {
-        const int2* f1 = cplane<int2>(ws, P, P.flow1[d], pair);
-        const BlockHit* hb = cplane<BlockHit>(ws, P, P.hit[2][d], pair);
-        for (int row = tg; row < s_n + b_n; row += 4) {
-            for (int rx = tx; rx < kRW; rx += 64) {
-                if (row < s_n) {
-                    const int2* fr = f1 + (size_t)(s_lo + row) * L1.w;
-                    const ITap t = S.cx_up[rx];
-                    S.u.sep.h1[d][row][rx] = lerp_i2(fr[t.i0], fr[t.i1], 4, t.f);
-                } else {
-                    const BlockHit* hr = hb + (size_t)(b_lo + row - s_n) * L2.nbx;
-                    const ITap t = S.cx_b[rx];
-                    const BlockHit p = hr[t.i0], q = hr[t.i1];
-                    S.u.sep.hb[d][row - s_n][rx] =
-                        lerp_i2(make_int2(p.dx, p.dy), make_int2(q.dx, q.dy), D2, t.f);
-                }
-            }
-        }
-    }
-    __syncthreads();
-    for (int ry = tg; ry < kRH; ry += 4) {
-        const ITap tu = S.ry_up[ry], tb = S.ry_b[ry];
-        for (int rx = tx; rx < kRW; rx += 64) {
-#pragma unroll
-            for (int d = 0; d < 2; d++) {
-                const int2 base = lerp_i2(S.u.sep.h1[d][tu.i0 - s_lo][rx], S.u.sep.h1[d][tu.i1 - s_lo][rx], 4, tu.f);
-                const int2 res = lerp_i2(S.u.sep.hb[d][tb.i0 - b_lo][rx], S.u.sep.hb[d][tb.i1 - b_lo][rx], D2, tb.f);
-                // f_m = flow * -0.5: in units 2^-(fb2+1) that is -flow_n
-                S.fm[d][ry][rx] = make_int2(-((base.x << bs) + (res.x << rs)), -((base.y << bs) + (res.y << rs)));
-            }
-        }
-    }
-    __syncthreads();
-
-    // (b) occlusion cue at clamped image positions (np.gradient, edge order 1),
-    //     in units 2^-(mb+1): interior (f[i+1]-f[i-1])/2 -> diff, edges f[1]-f[0] -> 2*diff
-    for (int qy = tg; qy < kOH; qy += 4) {
-        const int yi = clampi(y0 - 1 + qy, 0, H - 1);
-        const int ry = yi - (y0 - 2);
-        for (int qx = tx; qx < kOW; qx += 64) {
-            const int xi = S.cx_i[qx + 1];
-            const int rx = xi - (x0 - 2);
-#pragma unroll
-            for (int d = 0; d < 2; d++) {
-                int gx, gy;
-                if (W < 2) gx = 0;
-                else if (xi == 0) gx = 2 * (S.fm[d][ry][rx + 1].x - S.fm[d][ry][rx].x);
-                else if (xi == W - 1) gx = 2 * (S.fm[d][ry][rx].x - S.fm[d][ry][rx - 1].x);
-                else gx = S.fm[d][ry][rx + 1].x - S.fm[d][ry][rx - 1].x;
-                if (H < 2) gy = 0;
-                else if (yi == 0) gy = 2 * (S.fm[d][ry + 1][rx].y - S.fm[d][ry][rx].y);
-                else if (yi == H - 1) gy = 2 * (S.fm[d][ry][rx].y - S.fm[d][ry - 1][rx].y);
-                else gy = S.fm[d][ry + 1][rx].y - S.fm[d][ry - 1][rx].y;
-                const int v = -(gx + gy);
-                S.u.occ.occ[d][qy][qx] = v > 0 ? v : 0;
-            }
-        }
-    }
-    __syncthreads();
-    const float oscale = 1.0f / (float)(1 << (mb + 1));
-    // (c) column pass of smooth3 on occ: exact sum, f32(f64(sum / 3))
-    for (int ty = tg; ty < kTH; ty += 4)
-        for (int qx = tx; qx < kOW; qx += 64)
-#pragma unroll
-            for (int d = 0; d < 2; d++) {
-                const int sn = S.u.occ.occ[d][ty][qx] + S.u.occ.occ[d][ty + 1][qx] + S.u.occ.occ[d][ty + 2][qx];
-                S.u.occ.o0[d][ty][qx] = sn ? third_f32(sn, oscale) : 0.0f;
-            }
-    // (e) luma warps for rows -1..TH (clamped), d = |wl - wr|
-    const int kY = 2 * mb;  // luma warp result units 2^-(2 mb)
-    {
-        const int xi = x0 + tx;
-        const int rx = tx + 2;
-        for (int qy = tg; qy < kTH + 2; qy += 4) {
-            if (xi >= W) break;
-            const int yi = clampi(y0 - 1 + qy, 0, H - 1);
-            const int ry = yi - (y0 - 2);
-            const int2 fl = S.fm[0][ry][rx], fr = S.fm[1][ry][rx];
-            const bool center = qy >= 1 && qy <= kTH && y0 - 1 + qy < H;
-            uint8_t wl, wr;
-            if (g.fmt == FVV_RGB8) {
-                uint8_t cl[3], cr[3];
-#pragma unroll
-                for (int c = 0; c < 3; c++) {
-                    auto sl = [&](int yy, int xx) { return (int)frL[((size_t)yy * W + xx) * 3 + c]; };
-                    auto sr = [&](int yy, int xx) { return (int)frR[((size_t)yy * W + xx) * 3 + c]; };
-                    cl[c] = (uint8_t)rne64(warp_fixed32(sl, H, W, yi, xi, fl.x, fl.y, mb), kY);
-                    cr[c] = (uint8_t)rne64(warp_fixed32(sr, H, W, yi, xi, fr.x, fr.y, mb), kY);
-                }
-                wl = bt601(cl[0], cl[1], cl[2]);
-                wr = bt601(cr[0], cr[1], cr[2]);
-                if (center) {
-                    uint8_t* o = plane<uint8_t>(ws, P, P.wrgb, pair) + ((size_t)yi * W + xi) * 6;
-#pragma unroll
-                    for (int c = 0; c < 3; c++) { o[c] = cl[c]; o[3 + c] = cr[c]; }
-                }
-            } else {
-                wl = (uint8_t)rne64(bilin_fixed(frL, W, H, W, yi, xi, fl.x, fl.y, mb), kY);
-                wr = (uint8_t)rne64(bilin_fixed(frR, W, H, W, yi, xi, fr.x, fr.y, mb), kY);
-            }
-            S.dd[qy][tx] = (uint8_t)abs((int)wl - (int)wr);
-            if (center) {
-                plane<uint8_t>(ws, P, P.wl, pair)[(size_t)yi * W + xi] = wl;
-                plane<uint8_t>(ws, P, P.wr, pair)[(size_t)yi * W + xi] = wr;
-            }
-        }
-    }
-    // (g) chroma warps with the half-resolution, half-magnitude flow
-    //     (imageops.py:40-48): ((a+b)+(c+d))/4 * 0.5 of units 2^-mb = sum in units 2^-(mb+3)
-    if (g.fmt == FVV_YUV420) {
-        const int cw = g.cw, chh = g.ch;
-        for (int cyi = (tid >> 5); cyi < kTH / 2; cyi += 8) {  // kTH/2 x 32 chroma px
-        const int cy = y0 / 2 + cyi, cx = x0 / 2 + (tid & 31);
-        if (cy < chh && cx < cw) {
-            const uint8_t* uL = frL + (size_t)W * H;
-            const uint8_t* uR = frR + (size_t)W * H;
-            const size_t cplane_sz = (size_t)cw * chh;
-            const int cb = mb + 3, kC = 2 * cb;
-            const int ry = 2 * cy - (y0 - 2), rx = 2 * cx - (x0 - 2);
-            int2 cv[2];
-#pragma unroll
-            for (int d = 0; d < 2; d++) {
-                const int2 a = S.fm[d][ry][rx], b = S.fm[d][ry][rx + 1];
-                const int2 c = S.fm[d][ry + 1][rx], e = S.fm[d][ry + 1][rx + 1];
-                cv[d] = make_int2(a.x + b.x + c.x + e.x, a.y + b.y + c.y + e.y);
-            }
-            uint8_t o[4];
-#pragma unroll
-            for (int p = 0; p < 2; p++) {
-                const uint8_t* pl = uL + p * cplane_sz;
-                const uint8_t* pr = uR + p * cplane_sz;
-                o[2 * p] = (uint8_t)rne64(bilin_fixed(pl, cw, chh, cw, cy, cx, cv[0].x, cv[0].y, cb), kC);
-                o[2 * p + 1] = (uint8_t)rne64(bilin_fixed(pr, cw, chh, cw, cy, cx, cv[1].x, cv[1].y, cb), kC);
-            }
-            plane<uchar4>(ws, P, P.wc, pair)[(size_t)cy * cw + cx] = make_uchar4(o[0], o[1], o[2], o[3]);
-        }
-        }
-    }
-    __syncthreads();
-    // (d) row pass of smooth3 on occ (exact f64 sum of three f32, /3 in f64);
-    // (f) column sums of |wl - wr|
-    const int xi = x0 + tx;
-    if (xi < W) {
-        for (int ty = tg; ty < kTH; ty += 4) {
-            const int yi = y0 + ty;
-            if (yi >= H) break;
-            const size_t o = (size_t)yi * W + xi;
-#pragma unroll
-            for (int d = 0; d < 2; d++) {
-                const float a = S.u.occ.o0[d][ty][tx], b = S.u.occ.o0[d][ty][tx + 1], c = S.u.occ.o0[d][ty][tx + 2];
-                float v = 0.0f;
-                if (a != 0.0f || b != 0.0f || c != 0.0f) {
-                    const double s3 = __dadd_rn(__dadd_rn((double)a, (double)b), (double)c);
-                    v = (float)div3(s3);
-                }
-                plane<float>(ws, P, d ? P.occ_r : P.occ_l, pair)[o] = v;
-            }
-            plane<uint16_t>(ws, P, P.sd, pair)[o] =
-                (uint16_t)((int)S.dd[ty][tx] + (int)S.dd[ty + 1][tx] + (int)S.dd[ty + 2][tx]);
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// k_mask_cols: the same computation as k_mask_prod, as a register-streaming
+// k_mask_cols: everything of _mask_inputs (interp.py:78-94) that does not
+// depend on scipy's order of summation, plus the mid warps of every plane
+// (warp.py:27-46).  Exactness: with power-of-two blocks
+// every flow value is a dyadic rational with <= 24 significant bits, so
+// np.gradient, the f32 occlusion cue and BOTH smoothing passes over it are
+// exact sums -- scipy's running sum equals the plain 3-tap sum bitwise.
+// |wl - wr| is integral, so its column pass is exact too; only its row pass
+// (k_rowscan) must replay scipy in order.  Structure: a register-streaming
 // column walker.  A warp owns kMW output columns (lanes 2..kMW+1; two halo
 // lanes per side supply x-neighbours through shuffles) and walks down a
 // kMH-row band, carrying lagged sliding windows:
