@@ -12,4 +12,6 @@ from .cluster import (ClusterFrame, ClusterLayout, LayoutError, TileRect, TileRe
                       assemble_cluster_frame, build_layouts, cluster_geometry, crop_frame, downscale,
                       rig_clusters, tile_rects)
 
+from .pipeline import RigPipeline  # noqa: F401
+
 __version__ = "0.1.0"

@@ -1,0 +1,120 @@
+"""Device-resident rig stages: the reference's `PipelineHandle._interp` and
+`_stitch` (server/pipeline.py:254-292) without byte bundling.
+
+The reference moves every rig frame through its stage threads as serialized
+bytes (server/pipeline.py:145-163) -- at 1080p the host (de)serialisation
+costs as much as the synthesis itself.  Here a
+rig frame stays in HBM from camera upload to cluster frames: one C-ABI call
+per stage (`fvv_rig_views`, `fvv_rig_clusters`), captured once as a CUDA
+graph and replayed per tick; host I/O goes through pinned staging buffers on
+the pipeline's own stream.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from .cluster import ClusterFrame, build_layouts, rig_cluster_sizes, rig_clusters, tile_rects
+from .frame import PixelFormat, frame_from_packed, frame_nbytes, packed
+from .interp import InterpConfig, Interpolator
+from .viewmodel import ViewIndexModel
+
+
+class RigPipeline:
+    """Camera frames of one tick -> every dense view and every cluster frame.
+
+    `process()` works on device tensors; `process_frames()` is the host-facing
+    form (reference Frames in, `ClusterFrame`s out).  Reentrant per instance;
+    use one instance per stream.
+    """
+
+    def __init__(self, width: int, height: int, fmt, camera_count: int, stages: int = 4,
+                 views_per_side: int = 16, config: InterpConfig | None = None, graph: bool = True,
+                 device=None):
+        import torch
+        _lib.require_cuda()
+        self.model = ViewIndexModel(camera_count, stages)
+        self.width, self.height, self.format = int(width), int(height), PixelFormat(int(fmt))
+        self.views_per_side = int(views_per_side)
+        self.layouts = build_layouts(self.model, self.views_per_side) if self.views_per_side else []
+        self.engine = Interpolator(width, height, fmt, config,
+                                   max_pairs=(camera_count - 1) << (stages - 1), device=device)
+        dev = self.engine.device
+        fb = self.engine.frame_bytes
+        self.cams = torch.empty((camera_count, fb), dtype=torch.uint8, device=dev)
+        self.views = torch.empty((self.model.total_views, fb), dtype=torch.uint8, device=dev)
+        tiled = self.views_per_side > 0 and int(fmt) != PixelFormat.RGB8
+        self.sizes = rig_cluster_sizes(width, height, fmt, camera_count, stages,
+                                       self.views_per_side) if tiled else []
+        self.clusters = torch.empty(max(1, sum(self.sizes)), dtype=torch.uint8, device=dev)
+        self.stream = torch.cuda.Stream(device=dev)
+        self._host_in = torch.empty((camera_count, fb), dtype=torch.uint8).pin_memory()
+        self._host_out = torch.empty(self.clusters.numel(), dtype=torch.uint8).pin_memory()
+        self._tiled = tiled
+        self._graph = None
+        if graph:
+            with torch.cuda.stream(self.stream):
+                self._compute()  # warm: lazy attributes, allocator
+            self.stream.synchronize()
+            self._graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self._graph, stream=self.stream):
+                self._compute()
+            self.stream.synchronize()
+
+    def _compute(self):
+        self.engine.rig(self.cams, self.model.stages, self.views)
+        if self._tiled:
+            rig_clusters(self.views, self.width, self.height, self.format, self.model.camera_count,
+                         self.model.stages, self.views_per_side, out=self.clusters)
+
+    def process(self, cams=None):
+        """Run one tick on the pipeline stream.  `cams` (C, frame_bytes) device or
+        host tensor; None means `self.cams` was filled by the caller.  Returns
+        (views, clusters) device tensors (valid once the stream reaches them)."""
+        import torch
+        with torch.cuda.stream(self.stream):
+            if cams is not None:
+                self.cams.copy_(cams, non_blocking=True)
+            if self._graph is not None:
+                self._graph.replay()
+            else:
+                self._compute()
+        return self.views, self.clusters
+
+    def process_frames(self, frames) -> list:
+        """Reference-facing form: C camera Frames -> C `ClusterFrame`s (host)."""
+        import torch
+        if len(frames) != self.model.camera_count:
+            raise ValueError(f"rig has {self.model.camera_count} cameras, got {len(frames)} frames")
+        for i, f in enumerate(frames):
+            if (f.width, f.height, int(f.format)) != (self.width, self.height, int(self.format)):
+                raise ValueError("camera frames must share the pipeline's size and format")
+            self._host_in[i].copy_(torch.from_numpy(packed(f)))
+        self.process(self._host_in)
+        if not self._tiled:
+            raise ValueError("pipeline built without tiling (RGB8 or views_per_side = 0)")
+        with torch.cuda.stream(self.stream):
+            self._host_out.copy_(self.clusters, non_blocking=True)
+        self.stream.synchronize()
+        host = self._host_out.numpy()
+        out, off = [], 0
+        for lay, size in zip(self.layouts, self.sizes):
+            sw = (size * 2) // (3 * self.height) if int(self.format) == PixelFormat.YUV420 \
+                else size // self.height
+            fr = frame_from_packed(host[off:off + size].copy(), sw, self.height, self.format,
+                                   frames[0].timestamp)
+            out.append(ClusterFrame(lay.cluster_id, fr, tile_rects(lay, self.width, self.height)))
+            off += size
+        return out
+
+    def views_host(self) -> np.ndarray:
+        self.stream.synchronize()
+        return self.views.cpu().numpy()
+
+    @property
+    def views_per_tick(self) -> int:
+        return (self.model.camera_count - 1) * self.model.views_per_gap
+
+    @property
+    def frame_bytes(self) -> int:
+        return frame_nbytes(self.width, self.height, self.format)

@@ -199,3 +199,21 @@ def test_rig_clusters_vs_oracle(torch_cuda, w, h, fmt, cams, stages, vps):
         assert sizes[c] == ref.size
         assert np.array_equal(out[off:off + sizes[c]], ref), f"cluster {c}"
         off += sizes[c]
+
+
+def test_rig_pipeline_device_resident_vs_golden(torch_cuda):
+    """server/pipeline.py _interp + _stitch as one graph-captured device pipeline."""
+    import paper_2112_10603_b200 as fv
+    from paper_2112_10603_b200.pipeline import RigPipeline
+    g = load_golden("rig3_s2_vps2_yuv420_64x48")
+    w, h, stages, vps = 64, 48, int(g["stages"]), int(g["vps"])
+    pipe = RigPipeline(w, h, 1, 3, stages, vps)
+    cams = [fv.frame_from_packed(c, w, h, 1) for c in g["cams"]]
+    for _ in range(2):  # replays of the captured graph give the same answer
+        out = pipe.process_frames(cams)
+        assert np.array_equal(pipe.views_host(), g["views"])
+        got = np.concatenate([fv.packed(c.frame) for c in out])
+        assert np.array_equal(got, g["clusters"])
+    rects = np.array([[r.index, r.tier == "full", r.x, r.y, r.width, r.height]
+                      for c in out for r in c.tile_map], np.int32)
+    assert np.array_equal(rects, g["rects"])
