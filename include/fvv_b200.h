@@ -93,6 +93,13 @@ int fvv_interpolate_pairs(fvv_engine* engine, const uint8_t* const* left,
 int fvv_interp_diagnostics(fvv_engine* engine, int pair, float* flow_lr, float* flow_rl,
                            double* mask, void* stream);
 
+/* Per-level diagnostics of pair i of the most recent batch, level 0 (1/4),
+ * 1 (1/2) or 2 (full): the level's flows (h_s,w_s,2) f32 and match-error maps
+ * (h_s,w_s) f64, as InterpDiagnostics.scales[level].flow_lr / flow_rl /
+ * match_error_lr / match_error_rl (interp.py:49-56, 114-118).  NULL skips. */
+int fvv_interp_level_diagnostics(fvv_engine* engine, int pair, int level, float* flow_lr,
+                                 float* flow_rl, double* err_lr, double* err_rl, void* stream);
+
 /* Per-kernel timing of the stage kernels (bench.py's roofline figure):
  * while enabled, every stage-kernel launch is bracketed by a cudaEvent pair
  * on the launching stream (at most `capacity` launches are recorded).

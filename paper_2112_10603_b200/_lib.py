@@ -22,6 +22,7 @@ EXPORTS = (
     "fvv_dense_views", "fvv_rig_views", "fvv_downscale", "fvv_cluster_width",
     "fvv_assemble_cluster", "fvv_rig_cluster_bytes", "fvv_rig_clusters",
     "fvv_profile_enable", "fvv_profile_read", "fvv_kernel_class_name",
+    "fvv_interp_level_diagnostics",
 )
 
 
@@ -68,6 +69,7 @@ def load():
         "fvv_engine_max_pairs": (I, [P]),
         "fvv_interpolate_pairs": (I, [P, PP, PP, PP, I, P]),
         "fvv_interp_diagnostics": (I, [P, I, P, P, P, P]),
+        "fvv_interp_level_diagnostics": (I, [P, I, I, P, P, P, P, P]),
         "fvv_dense_views": (I, [P, P, P, I, P, P]),
         "fvv_rig_views": (I, [P, P, I, I, P, P]),
         "fvv_downscale": (I, [pd, P, I, I, P, P]),

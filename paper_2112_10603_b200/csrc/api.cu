@@ -17,6 +17,9 @@ cudaError_t run_interp_stage(const Geometry& g, const PairTable& pt, uint8_t* ws
                              int npairs, double* mask_out, Prof* prof, cudaStream_t st);
 cudaError_t run_diag(const Geometry& g, const PairTable& pt, uint8_t* ws, const Planes& P, int pair,
                      float* flow_lr, float* flow_rl, double* mask, cudaStream_t st);
+cudaError_t run_level_diag(const Geometry& g, uint8_t* ws, const Planes& P, int pair, int level,
+                           float* flow_lr, float* flow_rl, double* err_lr, double* err_rl,
+                           cudaStream_t st);
 cudaError_t launch_downscale(int W, int H, int fmt, const uint8_t* frames, int n, int f,
                              uint8_t* out, cudaStream_t st);
 cudaError_t launch_assemble(int W, int H, int fmt, const uint8_t* anchor,
@@ -354,6 +357,18 @@ int fvv_interp_diagnostics(fvv_engine* e, int pair, float* flow_lr, float* flow_
     cudaError_t ce = run_diag(e->g, e->last, e->slots, e->P, pair, flow_lr, flow_rl, mask,
                               static_cast<cudaStream_t>(stream));
     if (ce != cudaSuccess) return cuda_fail(ce, "diagnostics");
+    return FVV_OK;
+}
+
+int fvv_interp_level_diagnostics(fvv_engine* e, int pair, int level, float* flow_lr, float* flow_rl,
+                                 double* err_lr, double* err_rl, void* stream) {
+    if (!e) return fail(FVV_EINVAL, "null engine");
+    if (pair < 0 || pair >= e->last_npairs)
+        return fail(FVV_EINVAL, "no such pair in the most recent batch");
+    if (level < 0 || level > 2) return fail(FVV_EINVAL, "level must be 0, 1 or 2");
+    cudaError_t ce = run_level_diag(e->g, e->slots, e->P, pair, level, flow_lr, flow_rl, err_lr, err_rl,
+                                    static_cast<cudaStream_t>(stream));
+    if (ce != cudaSuccess) return cuda_fail(ce, "level diagnostics");
     return FVV_OK;
 }
 

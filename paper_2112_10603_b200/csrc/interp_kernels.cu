@@ -1433,6 +1433,62 @@ __global__ void k_diag_flow(Geometry g, const uint8_t* __restrict__ ws, Planes P
                          (float)((base.y << bs) + (res.y << rs)) * sc);
 }
 
+// per-level diagnostics (InterpDiagnostics.scales[s], interp.py:49-56, 114-128):
+// the level's flows (f32, exact from the fixed point) and the match-error maps
+// _block_to_pixel(best_sad / (area * 8)) in the reference's literal f64.
+template <int LEVEL>
+__global__ void k_diag_level(Geometry g, const uint8_t* __restrict__ ws, Planes P, int pair,
+                             float2* flow_lr, float2* flow_rl, double* err_lr, double* err_rl) {
+    const Level L = g.lv[LEVEL];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int d = blockIdx.z;
+    if (i >= L.w * L.h) return;
+    const int y = i / L.w, x = i - (i / L.w) * L.w;
+    const BlockHit* hit = cplane<BlockHit>(ws, P, P.hit[LEVEL][d], pair);
+    float2* fo = d ? flow_rl : flow_lr;
+    if (fo) {
+        int2 f;
+        if (LEVEL == 2) {
+            const Level L1 = g.lv[1];
+            const int2 base = up2_fixed(cplane<int2>(ws, P, P.flow1[d], pair), L1.h, L1.w, y, x);
+            const int2 res = b2p_fixed(hit, L.nby, L.nbx, L.block, y, x);
+            const int bs = g.fb[2] - (g.fb[1] + 3), rs = g.fb[2] - g.rb[2];
+            f = make_int2((base.x << bs) + (res.x << rs), (base.y << bs) + (res.y << rs));
+        } else {
+            f = cplane<int2>(ws, P, LEVEL == 0 ? P.flow0[d] : P.flow1[d], pair)[i];
+        }
+        const float sc = 1.0f / (float)(1 << g.fb[LEVEL]);
+        fo[i] = make_float2((float)f.x * sc, (float)f.y * sc);
+    }
+    double* eo = d ? err_rl : err_lr;
+    if (eo) {
+        auto err_of = [&](int by, int bx) {
+            const int rows = min(by * L.block + L.block, L.h) - by * L.block;
+            const int cols = min(bx * L.block + L.block, L.w) - bx * L.block;
+            const double area8 = __dmul_rn((double)((long long)rows * cols), 8.0);
+            return __ddiv_rn((double)hit[by * L.nbx + bx].sad, area8);
+        };
+        const double c = (double)(L.block - 1) / 2.0;
+        const double sy = __ddiv_rn(__dsub_rn((double)y, c), (double)L.block);
+        const double sx = __ddiv_rn(__dsub_rn((double)x, c), (double)L.block);
+        const Tap ty = clamp_tap(sy, L.nby), tx = clamp_tap(sx, L.nbx);
+        eo[i] = bilerp(err_of(ty.i0, tx.i0), err_of(ty.i0, tx.i1), err_of(ty.i1, tx.i0),
+                       err_of(ty.i1, tx.i1), tx.f, ty.f);
+    }
+}
+
+cudaError_t run_level_diag(const Geometry& g, uint8_t* ws, const Planes& P, int pair, int level,
+                           float* flow_lr, float* flow_rl, double* err_lr, double* err_rl,
+                           cudaStream_t st) {
+    const Level& L = g.lv[level];
+    dim3 grd((L.w * L.h + 255) / 256, 1, 2);
+    auto f2 = [](float* p) { return reinterpret_cast<float2*>(p); };
+    if (level == 0) k_diag_level<0><<<grd, 256, 0, st>>>(g, ws, P, pair, f2(flow_lr), f2(flow_rl), err_lr, err_rl);
+    else if (level == 1) k_diag_level<1><<<grd, 256, 0, st>>>(g, ws, P, pair, f2(flow_lr), f2(flow_rl), err_lr, err_rl);
+    else k_diag_level<2><<<grd, 256, 0, st>>>(g, ws, P, pair, f2(flow_lr), f2(flow_rl), err_lr, err_rl);
+    return cudaGetLastError();
+}
+
 cudaError_t run_diag(const Geometry& g, const PairTable& pt, uint8_t* ws, const Planes& P, int pair,
                      float* flow_lr, float* flow_rl, double* mask, cudaStream_t st) {
     if (flow_lr || flow_rl) {

@@ -176,6 +176,21 @@ class Interpolator:
                                                   ctypes.c_void_p(m.data_ptr()), self._stream()))
         return flr, frl, m
 
+    def level_diagnostics(self, pair: int, level: int):
+        """InterpDiagnostics.scales[level] of pair `pair` of the most recent `pairs` call:
+        (flow_lr, flow_rl, match_error_lr, match_error_rl) device tensors."""
+        import torch
+        f = SCALE_FACTORS[level]
+        h, w = self.height // f, self.width // f
+        flr = torch.empty((h, w, 2), dtype=torch.float32, device=self.device)
+        frl = torch.empty_like(flr)
+        elr = torch.empty((h, w), dtype=torch.float64, device=self.device)
+        erl = torch.empty_like(elr)
+        _lib.check(self._L.fvv_interp_level_diagnostics(
+            self._h, pair, level, ctypes.c_void_p(flr.data_ptr()), ctypes.c_void_p(frl.data_ptr()),
+            ctypes.c_void_p(elr.data_ptr()), ctypes.c_void_p(erl.data_ptr()), self._stream()))
+        return flr, frl, elr, erl
+
     def dense(self, left, right, stages: int, views=None):
         """dense_views() on device: left/right (frame_bytes,) -> (2**stages - 1, frame_bytes)."""
         import torch
@@ -254,14 +269,19 @@ def interpolate(left, right, config: InterpConfig | None = None, diagnostics: bo
                             left.timestamp)
     diag = InterpDiagnostics()
     if diagnostics or cfg.refine is not None:
-        flr, frl, m = eng.diagnostics(0)
-        flr, frl, m = flr.cpu().numpy(), frl.cpu().numpy(), m.cpu().numpy()
-        W, H = left.width, left.height
-        f_lr, f_rl = FlowField(W, H, flr), FlowField(W, H, frl)
-        diag.scales.append(ScaleDiagnostics(f_lr, f_rl, mask=m))
+        # per-level flows and match errors (interp.py:114-128); the per-level
+        # masks / blend_luma of levels 0-1 are not produced by this path (None)
+        for s in range(3):
+            flr, frl, elr, erl = (t.cpu().numpy() for t in eng.level_diagnostics(0, s))
+            h, w = flr.shape[:2]
+            diag.scales.append(ScaleDiagnostics(FlowField(w, h, flr), FlowField(w, h, frl), elr, erl))
+        _, _, m = eng.diagnostics(0)
+        m = m.cpu().numpy()
+        f_lr, f_rl = diag.scales[-1].flow_lr, diag.scales[-1].flow_rl
         diag.flow_mid_left = f_lr.scaled(-0.5)
         diag.flow_mid_right = f_rl.scaled(-0.5)
         diag.mask = m
+        diag.scales[-1].mask = m
     if cfg.refine is not None:  # the reference's one plugin hook (interp.py:144-145)
         res = cfg.refine(res, diag)
     if diagnostics:

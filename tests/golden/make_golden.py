@@ -58,6 +58,12 @@ def main():
             mid, diag = interp.interpolate(L, R, diagnostics=True)
             d.update(flow_lr=diag.scales[-1].flow_lr.vectors, flow_rl=diag.scales[-1].flow_rl.vectors,
                      mask=diag.mask)
+            if L.width * L.height <= 96 * 72:  # per-level ScaleDiagnostics (interp.py:114-128)
+                for s, sd in enumerate(diag.scales):
+                    d[f"lv{s}_flow_lr"] = sd.flow_lr.vectors
+                    d[f"lv{s}_flow_rl"] = sd.flow_rl.vectors
+                    d[f"lv{s}_err_lr"] = sd.match_error_lr
+                    d[f"lv{s}_err_rl"] = sd.match_error_rl
         except ValueError:  # per-level diagnostics need >= 2 px per axis at 1/4 scale
             mid = interp.interpolate(L, R)
         d["out"] = refimpl.packed(mid)

@@ -217,3 +217,17 @@ def test_rig_pipeline_device_resident_vs_golden(torch_cuda):
     rects = np.array([[r.index, r.tier == "full", r.x, r.y, r.width, r.height]
                       for c in out for r in c.tile_map], np.int32)
     assert np.array_equal(rects, g["rects"])
+
+
+@pytest.mark.parametrize("name", [n for n in golden_names("interp") if "lv0_flow_lr" in load_golden(n)])
+def test_per_level_diagnostics_vs_golden(torch_cuda, name):
+    """InterpDiagnostics.scales[s]: flows (f32) and match-error maps (f64), bitwise."""
+    g = load_golden(name)
+    w, h, fmt = int(g["w"]), int(g["h"]), int(g["fmt"])
+    eng, _ = _run_pairs(torch_cuda, w, h, fmt, [g["left"]], [g["right"]])
+    for s in range(3):
+        flr, frl, elr, erl = (t.cpu().numpy() for t in eng.level_diagnostics(0, s))
+        assert np.array_equal(flr, g[f"lv{s}_flow_lr"]), s
+        assert np.array_equal(frl, g[f"lv{s}_flow_rl"]), s
+        assert np.array_equal(elr, g[f"lv{s}_err_lr"]), s
+        assert np.array_equal(erl, g[f"lv{s}_err_rl"]), s
