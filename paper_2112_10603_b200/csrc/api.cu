@@ -137,6 +137,7 @@ Layout make_layout(const Geometry& g) {
         P.luma[s] = g.fmt == FVV_RGB8 ? take(n2) : 0;
         P.s4[s] = take(n1 * 2);
         P.s16[s] = take(n0 * 2);
+        P.q0[s] = take(n0 * 2);
     }
     for (int d = 0; d < 2; d++) {
         for (int s = 0; s < 3; s++)

@@ -71,6 +71,9 @@ __global__ void k_pyramid(Geometry g, PairTable pt, uint8_t* __restrict__ ws, Pl
         s16 += s0 + s1;
     }
     plane<uint16_t>(ws, P, P.s16[side], pair)[(size_t)y * w0 + x] = (uint16_t)s16;
+    // rint(8 * s16/16) = rint(s16/2), half to even (flow.py:77-78 at level 0)
+    plane<uint16_t>(ws, P, P.q0[side], pair)[(size_t)y * w0 + x] =
+        (uint16_t)(((uint32_t)s16 + (((uint32_t)s16 >> 1) & 1u)) >> 1);
 }
 
 // rint(8 * s16/16) = rint(s16/2), half to even (flow.py:77-78 at level 0)
@@ -93,7 +96,6 @@ struct SadSrc {
         return 8u * y_ref[idx];
     }
     __device__ __forceinline__ uint32_t tgt(int idx) const {
-        if (LEVEL == 0) return q0_of(s16_tgt[idx]);
         return tq[idx];
     }
 };
@@ -107,7 +109,8 @@ __device__ __forceinline__ SadSrc<LEVEL> make_src(const Geometry& g, const PairT
     s.s4_ref = cplane<uint16_t>(ws, P, P.s4[d], pair);
     if (g.fmt == FVV_RGB8) s.y_ref = cplane<uint8_t>(ws, P, P.luma[d], pair);
     else s.y_ref = d ? pt.right[pair] : pt.left[pair];
-    s.tq = LEVEL == 1 ? cplane<uint16_t>(ws, P, P.tq1[d], pair)
+    s.tq = LEVEL == 0 ? cplane<uint16_t>(ws, P, P.q0[1 - d], pair)
+         : LEVEL == 1 ? cplane<uint16_t>(ws, P, P.tq1[d], pair)
                       : cplane<uint16_t>(ws, P, P.tq2[d], pair);
     return s;
 }
@@ -309,6 +312,41 @@ __device__ __forceinline__ int2 lerp_i2(int2 a, int2 b, int den, int f) {
     return make_int2((den - f) * a.x + f * b.x, (den - f) * a.y + f * b.y);
 }
 
+// Builds the edge-padded pair plane P[yy][j] = T[y][xs-r+j] | T[y][xs-r+j+1] << 16
+// of a search window.  Interior windows (no column clamping, even start)
+// read two 32-bit words of the u16 target row per pair of P words and form
+// the odd pair with one PRMT -- no u16 staging pass.  Edge windows take the
+// clamped path through `Ts`.
+template <int LEVEL>
+__device__ __forceinline__ void stage_pairs(const SadSrc<LEVEL>& src, int w, int h, int r, int ys, int xs,
+                                            int PH, int PW, uint32_t* Ps, uint16_t* Ts, int TW,
+                                            int warp, int nwarps, int lane) {
+    const int x0 = xs - r;
+    const bool interior = x0 >= 0 && ((x0 & 1) == 0) && x0 + PW + 3 <= w;  // reads T[x0 .. x0+PW+2]
+    if (interior) {
+        for (int yy = warp; yy < PH; yy += nwarps) {
+            const int gy = clampi(ys - r + yy, 0, h - 1);
+            const uint32_t* row = reinterpret_cast<const uint32_t*>(src.tq + (size_t)gy * w + x0);
+            for (int m = lane; 2 * m < PW; m += 32) {
+                const uint32_t w0 = row[m], w1 = row[m + 1];
+                Ps[yy * PW + 2 * m] = w0;
+                if (2 * m + 1 < PW) Ps[yy * PW + 2 * m + 1] = __byte_perm(w0, w1, 0x5432);
+            }
+        }
+        __syncthreads();
+        return;
+    }
+    for (int yy = warp; yy < PH; yy += nwarps) {
+        const int gy = clampi(ys - r + yy, 0, h - 1);
+        for (int xx = lane; xx < TW; xx += 32)
+            Ts[yy * TW + xx] = (uint16_t)src.tgt(gy * w + clampi(x0 + xx, 0, w - 1));
+    }
+    __syncthreads();
+    for (int yy = warp; yy < PH; yy += nwarps)
+        for (int j = lane; j < PW; j += 32)
+            Ps[yy * PW + j] = j + 1 < TW ? (uint32_t)Ts[yy * TW + j] | ((uint32_t)Ts[yy * TW + j + 1] << 16) : 0u;
+}
+
 // ---------------------------------------------------------------------------
 // k_sad8: the 8x8-block search (every BASELINE config) -- same arithmetic as
 // k_sad, restructured for throughput: a CTA covers NBY x NBX blocks, the
@@ -351,12 +389,7 @@ __global__ void __launch_bounds__(256) k_sad8(Geometry g, PairTable pt, uint8_t*
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     const int ys = by0 * 8, xs = bx0 * 8;
 
-    // raw target window (edge padded: np.pad mode="edge", flow.py:78) and reference strip
-    for (int yy = warp; yy < PH; yy += nwarps) {
-        const int gy = clampi(ys - r + yy, 0, h - 1);
-        for (int xx = lane; xx < TW; xx += 32)
-            Ts[yy * TW + xx] = (uint16_t)src.tgt(gy * w + clampi(xs - r + xx, 0, w - 1));
-    }
+    // reference strip (duplicated into both u16 lanes)
     for (int yy = warp; yy < RH; yy += nwarps) {
         const int gy = ys + yy;
         for (int xx = lane; xx < RW; xx += 32) {
@@ -367,11 +400,8 @@ __global__ void __launch_bounds__(256) k_sad8(Geometry g, PairTable pt, uint8_t*
     }
     for (int i = tid; i < side * side; i += blockDim.x) rk[i] = sl.rank_of[i];
     for (int i = tid; i < sl.nbx * sl.nby; i += blockDim.x) best[i] = ~0ull;
-    __syncthreads();
-    // pair plane: P[y][j] = T[y][j] | T[y][j+1] << 16 (candidates dx, dx+1 in one word)
-    for (int yy = warp; yy < PH; yy += nwarps)
-        for (int j = lane; j < PW; j += 32)
-            Ps[yy * PW + j] = j + 1 < TW ? (uint32_t)Ts[yy * TW + j] | ((uint32_t)Ts[yy * TW + j + 1] << 16) : 0u;
+    // edge-padded target window (np.pad mode="edge", flow.py:78) as candidate pairs
+    stage_pairs<LEVEL>(src, w, h, r, ys, xs, PH, PW, Ps, Ts, TW, warp, nwarps, lane);
     // sum of reference samples per block (valid rows only; columns are full here)
     for (int k = tid; k < sl.nbx * sl.nby; k += blockDim.x) {
         const int kbx = k % sl.nbx, kby = k / sl.nbx;
@@ -504,11 +534,6 @@ __global__ void __launch_bounds__(256) k_sadp(Geometry g, PairTable pt, uint8_t*
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     const int ys = by0 * 8, xs = bx0 * 8;
 
-    for (int yy = warp; yy < PH; yy += nwarps) {
-        const int gy = clampi(ys - r + yy, 0, h - 1);
-        for (int xx = lane; xx < TW; xx += 32)
-            Ts[yy * TW + xx] = (uint16_t)src.tgt(gy * w + clampi(xs - r + xx, 0, w - 1));
-    }
     for (int yy = warp; yy < RH; yy += nwarps) {
         const int gy = ys + yy;
         for (int xx = lane; xx < RW; xx += 32) {
@@ -522,10 +547,7 @@ __global__ void __launch_bounds__(256) k_sadp(Geometry g, PairTable pt, uint8_t*
     }
     for (int i = tid; i < SIDE * SIDE; i += blockDim.x) rk[i] = sl.rank_of[i];
     for (int i = tid; i < sl.nbx * sl.nby; i += blockDim.x) best[i] = ~0ull;
-    __syncthreads();
-    for (int yy = warp; yy < PH; yy += nwarps)
-        for (int j = lane; j < PW; j += 32)
-            Ps[yy * PW + j] = j + 1 < TW ? (uint32_t)Ts[yy * TW + j] | ((uint32_t)Ts[yy * TW + j + 1] << 16) : 0u;
+    stage_pairs<LEVEL>(src, w, h, r, ys, xs, PH, PW, Ps, Ts, TW, warp, nwarps, lane);
     for (int k = tid; k < sl.nbx * sl.nby; k += blockDim.x) {
         const int kbx = k % sl.nbx, kby = k / sl.nbx;
         const int rows = min(8, h - (by0 + kby) * 8);
