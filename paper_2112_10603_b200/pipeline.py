@@ -107,6 +107,72 @@ class RigPipeline:
             off += size
         return out
 
+    def stream_ticks(self, host_cams, host_out, slots: int = 2):
+        """Throughput form for a live stream: process len(host_cams) ticks with
+        the host->device copy of tick t+1 and the device->host copy of tick t-1
+        overlapping the synthesis of tick t.
+
+        host_cams: list of pinned uint8 tensors (C, frame_bytes); host_out: list
+        of pinned uint8 tensors (cluster bytes), same length.  Uses `slots`
+        device buffer sets (one CUDA graph each).  Returns when all copies are
+        enqueued; synchronise on `self.stream` (or the device) before reading.
+        """
+        import torch
+        if not self._tiled:
+            raise ValueError("stream_ticks needs a tiling pipeline")
+        if not hasattr(self, "_slots") or len(self._slots) != slots:
+            self._make_slots(slots)
+        h2d = torch.cuda.Stream(device=self.engine.device)
+        d2h = torch.cuda.Stream(device=self.engine.device)
+        done_in = [torch.cuda.Event() for _ in range(slots)]
+        done_cmp = [torch.cuda.Event() for _ in range(slots)]
+        done_out = [torch.cuda.Event() for _ in range(slots)]
+        for t, (hin, hout) in enumerate(zip(host_cams, host_out)):
+            k = t % slots
+            cams, clusters, graph = self._slots[k]
+            if t >= slots:
+                h2d.wait_event(done_cmp[k])          # the slot's previous tick has been consumed
+            with torch.cuda.stream(h2d):
+                cams.copy_(hin, non_blocking=True)
+                done_in[k].record(h2d)
+            self.stream.wait_event(done_in[k])
+            if t >= slots:
+                self.stream.wait_event(done_out[k])  # its clusters have left the device
+            with torch.cuda.stream(self.stream):
+                graph.replay()
+                done_cmp[k].record(self.stream)
+            d2h.wait_event(done_cmp[k])
+            with torch.cuda.stream(d2h):
+                hout.copy_(clusters, non_blocking=True)
+                done_out[k].record(d2h)
+        self.stream.wait_stream(d2h)
+
+    def _make_slots(self, slots: int):
+        import torch
+        self._slots = []
+        for k in range(slots):
+            if k == 0:
+                eng, cams, views, clusters = self.engine, self.cams, self.views, self.clusters
+            else:
+                eng = Interpolator(self.width, self.height, self.format, self.engine.config,
+                                   max_pairs=self.engine.max_pairs, device=self.engine.device)
+                cams = torch.empty_like(self.cams)
+                views = torch.empty_like(self.views)
+                clusters = torch.empty_like(self.clusters)
+
+            def run(eng=eng, cams=cams, views=views, clusters=clusters):
+                eng.rig(cams, self.model.stages, views)
+                rig_clusters(views, self.width, self.height, self.format, self.model.camera_count,
+                             self.model.stages, self.views_per_side, out=clusters)
+            with torch.cuda.stream(self.stream):
+                run()
+            self.stream.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=self.stream):
+                run()
+            self.stream.synchronize()
+            self._slots.append((cams, clusters, graph))
+
     def views_host(self) -> np.ndarray:
         self.stream.synchronize()
         return self.views.cpu().numpy()

@@ -231,3 +231,16 @@ def test_per_level_diagnostics_vs_golden(torch_cuda, name):
         assert np.array_equal(frl, g[f"lv{s}_flow_rl"]), s
         assert np.array_equal(elr, g[f"lv{s}_err_lr"]), s
         assert np.array_equal(erl, g[f"lv{s}_err_rl"]), s
+
+
+def test_rig_pipeline_stream_ticks_overlapped(torch_cuda):
+    """Double-buffered live-stream form: every tick's clusters equal the golden ones."""
+    from paper_2112_10603_b200.pipeline import RigPipeline
+    g = load_golden("rig3_s2_vps2_yuv420_64x48")
+    pipe = RigPipeline(64, 48, 1, 3, int(g["stages"]), int(g["vps"]))
+    cams = torch_cuda.from_numpy(g["cams"]).pin_memory()
+    outs = [torch_cuda.empty(pipe.clusters.numel(), dtype=torch_cuda.uint8).pin_memory() for _ in range(5)]
+    pipe.stream_ticks([cams] * 5, outs)
+    torch_cuda.cuda.synchronize()
+    for o in outs:
+        assert np.array_equal(o.numpy(), g["clusters"])
