@@ -739,13 +739,10 @@ __global__ void __launch_bounds__(256) k_warpq(Geometry g, PairTable pt, uint8_t
     }
 }
 
-// f32(f64(S / 3)) for S = sn * 2^-k exact (the column / row pass of
-// uniform_filter1d on the occlusion cue).  When sn < 2^24, S is an exact
-// f32 and f64 rounding cannot land on an f32 midpoint (S/3 has a periodic
-// binary expansion), so one correctly rounded f32 division gives the
-// reference's double-rounded result; otherwise divide in f64.
+// f32(f64(S / 3)) for S = sn * 2^-k exact (the column pass of uniform_filter1d
+// on the occlusion cue): S is exact in f64, div3 is the correctly rounded
+// quotient, the cast rounds once more -- exactly the reference's arithmetic.
 __device__ __forceinline__ float third_f32(int sn, float scale) {
-    if (sn < (1 << 24)) return __fmul_rn(div3f((float)sn), scale);
     return (float)div3(__dmul_rn((double)sn, (double)scale));
 }
 
@@ -829,8 +826,10 @@ __global__ void __launch_bounds__(kMWarps * 32, 6) k_mask_cols(Geometry g, PairT
         return sn ? third_f32(sn, oscale) : 0.0f;
     };
 
+    // source-row caches: rows ua, ua+1 in use, ua+2 already in flight (loaded two
+    // output rows before it is needed); the same for block rows ba..ba+2
     int ua = -10, ba = -10;
-    int2 hu0[2], hu1[2], hb0[2], hb1[2];
+    int2 hu0[2], hu1[2], hu2[2], hb0[2], hb1[2], hb2[2];
     int2 F0[2], F1[2], F2[2];
     int gx1[2] = {0, 0}, gx2[2] = {0, 0};
     int oc0[2] = {0, 0}, oc1[2] = {0, 0}, oc2[2] = {0, 0};
@@ -854,9 +853,14 @@ __global__ void __launch_bounds__(kMWarps * 32, 6) k_mask_cols(Geometry g, PairT
         if (ty.i0 != ua) {
 #pragma unroll
             for (int d = 0; d < 2; d++) {
-                if (ty.i0 == ua + 1) hu0[d] = hu1[d];
-                else hu0[d] = xl_u(d, ty.i0);
-                hu1[d] = xl_u(d, ty.i0 + 1);
+                if (ty.i0 == ua + 1) {
+                    hu0[d] = hu1[d];
+                    hu1[d] = hu2[d];
+                } else {
+                    hu0[d] = xl_u(d, ty.i0);
+                    hu1[d] = xl_u(d, ty.i0 + 1);
+                }
+                hu2[d] = xl_u(d, min(ty.i0 + 2, L1.h - 1));
             }
             ua = ty.i0;
         }
@@ -864,9 +868,14 @@ __global__ void __launch_bounds__(kMWarps * 32, 6) k_mask_cols(Geometry g, PairT
         if (tby.i0 != ba) {
 #pragma unroll
             for (int d = 0; d < 2; d++) {
-                if (tby.i0 == ba + 1) hb0[d] = hb1[d];
-                else hb0[d] = xl_b(d, tby.i0);
-                hb1[d] = xl_b(d, tby.i1);
+                if (tby.i0 == ba + 1) {
+                    hb0[d] = hb1[d];
+                    hb1[d] = hb2[d];
+                } else {
+                    hb0[d] = xl_b(d, tby.i0);
+                    hb1[d] = xl_b(d, tby.i1);
+                }
+                hb2[d] = xl_b(d, min(tby.i1 + 1, L2.nby - 1));
             }
             ba = tby.i0;
         }
