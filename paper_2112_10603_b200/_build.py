@@ -41,7 +41,8 @@ def stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not stale():
         return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", str(LIB) + ".tmp", *[str(CSRC / s) for s in SOURCES]]
+    extra = os.environ.get("FVV_NVCC_EXTRA", "").split()  # tuning sweeps only (e.g. -DFVV_MINB_MASK=8)
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-o", str(LIB) + ".tmp", *[str(CSRC / s) for s in SOURCES]]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)

@@ -20,6 +20,20 @@
 
 #include "fvv_device.cuh"
 
+// minimum resident CTAs per SM (register budgets), tuned on B200 -- see profiles/
+#ifndef FVV_MINB_MASK
+#define FVV_MINB_MASK 8
+#endif
+#ifndef FVV_MINB_ROWSCAN
+#define FVV_MINB_ROWSCAN 1
+#endif
+#ifndef FVV_MINB_SAD8
+#define FVV_MINB_SAD8 1
+#endif
+#ifndef FVV_MINB_SADP
+#define FVV_MINB_SADP 1
+#endif
+
 namespace fvv {
 
 // ---------------------------------------------------------------------------
@@ -365,7 +379,7 @@ struct Sad8Launch {
 };
 
 template <int LEVEL, int KP>
-__global__ void __launch_bounds__(256) k_sad8(Geometry g, PairTable pt, uint8_t* __restrict__ ws,
+__global__ void __launch_bounds__(256, FVV_MINB_SAD8) k_sad8(Geometry g, PairTable pt, uint8_t* __restrict__ ws,
                                               Planes P, Sad8Launch sl) {
     extern __shared__ __align__(16) uint8_t smem[];
     const Level L = g.lv[LEVEL];
@@ -510,7 +524,7 @@ struct SadPLaunch {
 };
 
 template <int LEVEL, int SIDE>
-__global__ void __launch_bounds__(256) k_sadp(Geometry g, PairTable pt, uint8_t* __restrict__ ws,
+__global__ void __launch_bounds__(256, FVV_MINB_SADP) k_sadp(Geometry g, PairTable pt, uint8_t* __restrict__ ws,
                                               Planes P, SadPLaunch sl) {
     extern __shared__ __align__(16) uint8_t smem[];
     const Level L = g.lv[LEVEL];
@@ -770,7 +784,7 @@ __device__ __forceinline__ float third_f32(int sn, float scale) {
 constexpr int kMW = 28, kMWarps = 4, kMH = 64;
 
 template <int FMT>
-__global__ void __launch_bounds__(kMWarps * 32, 6) k_mask_cols(Geometry g, PairTable pt,
+__global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geometry g, PairTable pt,
                                                                uint8_t* __restrict__ ws, Planes P) {
     const int W = g.W, H = g.H;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1020,7 +1034,7 @@ __device__ __forceinline__ uint8_t blend_px(double m, int a, int b) {
     return to_u8(__dadd_rn(__dmul_rn(m, (double)a), __dmul_rn(__dsub_rn(1.0, m), (double)b)));
 }
 
-__global__ void __launch_bounds__(kRowscanThreads) k_rowscan(Geometry g, PairTable pt,
+__global__ void __launch_bounds__(kRowscanThreads, FVV_MINB_ROWSCAN) k_rowscan(Geometry g, PairTable pt,
                                                               const uint8_t* __restrict__ ws, Planes P,
                                                               int pair_base, bool write_frame,
                                                               double* mask_out /* nullable: one pair */) {
