@@ -25,13 +25,13 @@
 #define FVV_MINB_MASK 8
 #endif
 #ifndef FVV_MINB_ROWSCAN
-#define FVV_MINB_ROWSCAN 1
+#define FVV_MINB_ROWSCAN 4
 #endif
 #ifndef FVV_MINB_SAD8
-#define FVV_MINB_SAD8 1
+#define FVV_MINB_SAD8 4
 #endif
 #ifndef FVV_MINB_SADP
-#define FVV_MINB_SADP 1
+#define FVV_MINB_SADP 6
 #endif
 
 namespace fvv {
