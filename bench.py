@@ -451,17 +451,25 @@ def run_b200(args, cfg, rank, world, local_rank):
         peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e9
         peak_note = ("derived: 148 SMs x 128 lanes x 2 (u16x2) abs-diffs/clk at the median SM clock "
                      "under load; no measured INT peak in MEASURED_PEAKS.json")
-    traffic = None  # DRAM bytes per step of the dominant kernel class, from a committed ncu capture
+    # DRAM bytes and warp instructions per step of the dominant kernel class,
+    # from the committed ncu launch list (profiles/traffic.json)
+    traffic, issue = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             t = json.load(f).get(args.config, {}).get(dom)
         if t:
             traffic = t["dram_bytes_per_pair"] * npairs_total
+            sm_mhz = clk.get("sm_mhz") or float(peaks.get("sm_max_mhz", 1965.0))
+            ach = t["warp_inst_per_pair"] * npairs_total / (dom_ms / 1e3) / 1e9
+            pk = 148 * 4 * sm_mhz * 1e6 / 1e9  # 4 schedulers x 1 warp-instruction per clock per SM
+            issue = {"achieved": ach, "peak": pk, "unit": "G warp-instr/s", "frac": ach / pk,
+                     "note": "the path's exact integer/f64 arithmetic makes this kernel issue-bound; "
+                             "ncu instruction count x live kernel time vs 148 SMs x 4 issue/clk"}
     except (OSError, KeyError, ValueError):
         pass
     roofline = {"bound": bound, "kernel": dom, "achieved": achieved, "peak": peak, "unit": unit,
                 "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per step (ncu dram read+write)",
-                "peak_source": peak_note,
+                "peak_source": peak_note, "issue": issue,
                 "kernel_ms_per_step": dom_ms, "kernel_share_of_step": dom_ms / step_kernel_ms,
                 "per_kernel_ms_per_step": {k: round(v[0], 4) for k, v in per_class.items()}}
 
