@@ -99,6 +99,7 @@ __device__ __forceinline__ uint32_t q0_of(uint32_t s) { return (s + ((s >> 1) & 
 // ---------------------------------------------------------------------------
 template <int LEVEL>
 struct SadSrc {
+    const uint16_t* q0_ref;   // level 0 (quantized, k_pyramid)
     const uint16_t* s16_ref;  // level 0
     const uint16_t* s16_tgt;
     const uint16_t* s4_ref;   // level 1
@@ -109,6 +110,13 @@ struct SadSrc {
         if (LEVEL == 1) return 2u * s4_ref[idx];
         return 8u * y_ref[idx];
     }
+    // reference samples (idx, idx+1) packed as u16 pair (idx even, 4-byte aligned)
+    __device__ __forceinline__ uint32_t ref_pair(int idx) const {
+        if (LEVEL == 0) return *reinterpret_cast<const uint32_t*>(q0_ref + idx);
+        if (LEVEL == 1) return *reinterpret_cast<const uint32_t*>(s4_ref + idx) << 1;  // 2*s <= 2040
+        const uint32_t y2 = *reinterpret_cast<const uint16_t*>(y_ref + idx);
+        return ((y2 & 0xFFu) | ((y2 & 0xFF00u) << 8)) << 3;                      // 8*Y pair
+    }
     __device__ __forceinline__ uint32_t tgt(int idx) const {
         return tq[idx];
     }
@@ -118,6 +126,7 @@ template <int LEVEL>
 __device__ __forceinline__ SadSrc<LEVEL> make_src(const Geometry& g, const PairTable& pt,
                                                   uint8_t* ws, const Planes& P, int pair, int d) {
     SadSrc<LEVEL> s;
+    s.q0_ref = cplane<uint16_t>(ws, P, P.q0[d], pair);
     s.s16_ref = cplane<uint16_t>(ws, P, P.s16[d], pair);
     s.s16_tgt = cplane<uint16_t>(ws, P, P.s16[1 - d], pair);
     s.s4_ref = cplane<uint16_t>(ws, P, P.s4[d], pair);
@@ -550,14 +559,8 @@ __global__ void __launch_bounds__(256, FVV_MINB_SADP) k_sadp(Geometry g, PairTab
 
     for (int yy = warp; yy < RH; yy += nwarps) {
         const int gy = ys + yy;
-        for (int xx = lane; xx < RW; xx += 32) {
-            uint32_t q0 = 0, q1 = 0;
-            if (gy < h && 2 * xx < nbx * 8) {
-                q0 = src.ref(gy * w + xs + 2 * xx);
-                q1 = src.ref(gy * w + xs + 2 * xx + 1);
-            }
-            Rs[yy * RW + xx] = q0 | (q1 << 16);
-        }
+        for (int xx = lane; xx < RW; xx += 32)
+            Rs[yy * RW + xx] = (gy < h && 2 * xx < nbx * 8) ? src.ref_pair(gy * w + xs + 2 * xx) : 0u;
     }
     for (int i = tid; i < SIDE * SIDE; i += blockDim.x) rk[i] = sl.rank_of[i];
     for (int i = tid; i < sl.nbx * sl.nby; i += blockDim.x) best[i] = ~0ull;
