@@ -244,3 +244,13 @@ def test_rig_pipeline_stream_ticks_overlapped(torch_cuda):
     torch_cuda.cuda.synchronize()
     for o in outs:
         assert np.array_equal(o.numpy(), g["clusters"])
+
+
+def test_4k_pair_vs_oracle(torch_cuda):
+    """BASELINE config 5 resolution (3840x2160 YUV420): one pair, bit-exact to the oracle."""
+    rng = np.random.default_rng(2160)
+    w, h, fmt = 3840, 2160, 1
+    a, b = _smooth_pair(rng, w, h, fmt, 17)
+    _, out = _run_pairs(torch_cuda, w, h, fmt, [a], [b])
+    ref = O.interpolate(a, b, w, h, fmt)
+    assert np.array_equal(out[0], ref), f"{np.count_nonzero(out[0] != ref)} bytes differ"
