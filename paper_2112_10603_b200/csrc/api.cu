@@ -154,6 +154,7 @@ Layout make_layout(const Geometry& g) {
     P.wr = take(n2);
     P.wc = g.fmt == FVV_YUV420 ? take((size_t)g.cw * g.ch * 4) : 0;
     P.wrgb = g.fmt == FVV_RGB8 ? take(n2 * 6) : 0;
+    P.carry = take((size_t)H * ((W + 7) / 8) * 8);
     P.stride = align_up(o, 4096);
     return lay;
 }

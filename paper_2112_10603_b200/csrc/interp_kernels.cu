@@ -1214,6 +1214,168 @@ __global__ void __launch_bounds__(kRowscanThreads, FVV_MINB_ROWSCAN) k_rowscan(G
 }
 
 // ---------------------------------------------------------------------------
+// Split row scan.  The only order-dependent part of the mask is scipy's
+// running sum along each row of smooth3(|wl - wr|) (tmp(x) = tmp(x-1) +
+// (p[x+2] - p[x-1]), f64).  k_scan_carry runs that chain once per row and
+// stores tmp at every 8th column; k_blend then replays the <= 7 chain steps
+// of its own 8-column group from the stored carry -- the same additions in
+// the same order, so the same doubles -- and evaluates mask + blend fully in
+// parallel (thread = 2 rows x 8 columns, chroma from the row pair).
+// ---------------------------------------------------------------------------
+constexpr int kCR = 32, kCC = 64;  // carry kernel: rows per CTA (one lane each), chunk columns
+
+__global__ void __launch_bounds__(kCR) k_scan_carry(Geometry g, const uint8_t* __restrict__ ws,
+                                                    Planes P) {
+    __shared__ double dtab[766];
+    __shared__ uint16_t tile[kCR][kCC + 4];  // sd[x-2 .. x+65] of the chunk, per row
+    const int W = g.W, H = g.H;
+    const int pair = blockIdx.y, y0 = blockIdx.x * kCR;
+    const int lane = threadIdx.x;
+    const uint16_t* sd = cplane<uint16_t>(ws, P, P.sd, pair);
+    double* carry = reinterpret_cast<double*>(const_cast<uint8_t*>(ws) + P.stride * (size_t)pair + P.carry);
+    const int ng = (W + 7) / 8;
+    for (int i = lane; i < 766; i += kCR) dtab[i] = __ddiv_rn((double)i, 3.0);
+    const int y = y0 + lane;
+    double tmp = 0.0;
+    for (int c0 = 0; c0 < W; c0 += kCC) {
+        __syncwarp();
+        // coalesced staging of sd[c0-2 .. c0+kCC+1] (clamped) for the warp's rows
+        for (int r = 0; r < kCR; r++) {
+            const int yy = min(y0 + r, H - 1);
+            const uint16_t* row = sd + (size_t)yy * W;
+            for (int j = lane; j < kCC + 4; j += 32) tile[r][j] = row[clampi(c0 - 2 + j, 0, W - 1)];
+        }
+        __syncwarp();
+        if (y < H) {
+            const int n = min(kCC, W - c0);
+            double* cr = carry + (size_t)y * ng + c0 / 8;
+            const uint16_t* t = tile[lane];  // t[j] = sd[c0 - 2 + j]
+            int c = 0;
+            if (c0 == 0) {
+                tmp = __dadd_rn(__dadd_rn(dtab[t[2]], dtab[t[2]]), dtab[t[min(3, W + 1)]]);
+                cr[0] = tmp;
+                c = 1;
+            }
+            for (; c < n; c++) {
+                // p[x+2] - p[x-1] = D0[sd[min(x+1, W-1)]] - D0[sd[max(x-2, 0)]]
+                tmp = __dadd_rn(tmp, __dsub_rn(dtab[t[c + 3]], dtab[t[c]]));
+                if ((c & 7) == 0) cr[c >> 3] = tmp;
+            }
+        }
+    }
+}
+
+template <int FMT>
+__global__ void __launch_bounds__(128) k_blend(Geometry g, PairTable pt, const uint8_t* __restrict__ ws,
+                                               Planes P, int pair_base, bool write_frame,
+                                               double* mask_out /* nullable: one pair */) {
+    __shared__ double dtab[766];
+    const int W = g.W, H = g.H;
+    const int pair = blockIdx.z + pair_base;
+    for (int i = threadIdx.x; i < 766; i += blockDim.x) dtab[i] = __ddiv_rn((double)i, 3.0);
+    __syncthreads();
+    const int ng = (W + 7) / 8;
+    const int gx = blockIdx.x * blockDim.x + threadIdx.x;  // 8-column group
+    const int yp = blockIdx.y;                              // row pair
+    if (gx >= ng) return;
+    const int x0 = gx * 8, n = min(8, W - x0);
+    const uint16_t* sd = cplane<uint16_t>(ws, P, P.sd, pair);
+    const double* carry = cplane<double>(ws, P, P.carry, pair);
+    const float* ol = cplane<float>(ws, P, P.occ_l, pair);
+    const float* orr = cplane<float>(ws, P, P.occ_r, pair);
+    const uint8_t* wl = cplane<uint8_t>(ws, P, P.wl, pair);
+    const uint8_t* wr = cplane<uint8_t>(ws, P, P.wr, pair);
+    uint8_t* out = pt.out[pair];
+    double mrow[2][8];
+#pragma unroll
+    for (int rr = 0; rr < 2; rr++) {
+        const int y = 2 * yp + rr;
+        const size_t ro = (size_t)y * W;
+        const uint16_t* srow = sd + ro;
+        int s[11];
+#pragma unroll
+        for (int j = 0; j < 11; j++) s[j] = srow[clampi(x0 - 2 + j, 0, W - 1)];
+        float vl[8], vr[8];
+        uint8_t al[8], ar[8];
+        if (n == 8) {
+            const float4 a = *reinterpret_cast<const float4*>(ol + ro + x0);
+            const float4 b = *reinterpret_cast<const float4*>(ol + ro + x0 + 4);
+            const float4 c = *reinterpret_cast<const float4*>(orr + ro + x0);
+            const float4 d = *reinterpret_cast<const float4*>(orr + ro + x0 + 4);
+            vl[0] = a.x; vl[1] = a.y; vl[2] = a.z; vl[3] = a.w; vl[4] = b.x; vl[5] = b.y; vl[6] = b.z; vl[7] = b.w;
+            vr[0] = c.x; vr[1] = c.y; vr[2] = c.z; vr[3] = c.w; vr[4] = d.x; vr[5] = d.y; vr[6] = d.z; vr[7] = d.w;
+            if (FMT != FVV_RGB8) {
+                const uint2 p = *reinterpret_cast<const uint2*>(wl + ro + x0);
+                const uint2 q = *reinterpret_cast<const uint2*>(wr + ro + x0);
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    al[j] = (p.x >> (8 * j)) & 0xFF; al[4 + j] = (p.y >> (8 * j)) & 0xFF;
+                    ar[j] = (q.x >> (8 * j)) & 0xFF; ar[4 + j] = (q.y >> (8 * j)) & 0xFF;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                const int xx = min(x0 + j, W - 1);
+                vl[j] = ol[ro + xx]; vr[j] = orr[ro + xx];
+                if (FMT != FVV_RGB8) { al[j] = wl[ro + xx]; ar[j] = wr[ro + xx]; }
+            }
+        }
+        // replay the running sum inside the group: tmp(x0) from the carry, then x0+1 ..
+        double tmp = carry[(size_t)y * ng + gx];
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            if (j > 0) tmp = __dadd_rn(tmp, __dsub_rn(dtab[s[j + 3]], dtab[s[j]]));
+            mrow[rr][j] = j < n ? mask_of(tmp, vl[j], vr[j], g) : 0.0;
+        }
+        if (write_frame) {
+            if (FMT == FVV_RGB8) {
+                const uint8_t* px = cplane<uint8_t>(ws, P, P.wrgb, pair) + (ro + x0) * 6;
+                uint8_t* o = out + (ro + x0) * 3;
+#pragma unroll
+                for (int j = 0; j < 8; j++)
+                    if (j < n)
+#pragma unroll
+                        for (int ch = 0; ch < 3; ch++)
+                            o[3 * j + ch] = blend_px(mrow[rr][j], px[6 * j + ch], px[6 * j + 3 + ch]);
+            } else {
+                uint32_t lo = 0, hi = 0;
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    lo |= (uint32_t)blend_px(mrow[rr][j], al[j], ar[j]) << (8 * j);
+                    hi |= (uint32_t)blend_px(mrow[rr][4 + j], al[4 + j], ar[4 + j]) << (8 * j);
+                }
+                if (n == 8) *reinterpret_cast<uint2*>(out + ro + x0) = make_uint2(lo, hi);
+                else *reinterpret_cast<uint32_t*>(out + ro + x0) = lo;  // W % 4 == 0: n == 4
+            }
+        }
+        if (mask_out) {
+#pragma unroll
+            for (int j = 0; j < 8; j++)
+                if (j < n) mask_out[ro + x0 + j] = mrow[rr][j];
+        }
+    }
+    // chroma blend with the 2x2-mean mask (warp.py:83-88)
+    if (FMT == FVV_YUV420 && write_frame) {
+        const int cw = g.cw, chh = g.ch;
+        const int cx0 = x0 / 2, nc = n / 2;
+        const uchar4* wc = cplane<uchar4>(ws, P, P.wc, pair) + (size_t)yp * cw + cx0;
+        uint8_t* uo = out + (size_t)W * H + (size_t)yp * cw + cx0;
+        uint8_t* vo = uo + (size_t)cw * chh;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            if (j >= nc) break;
+            const double sm = __dadd_rn(__dadd_rn(mrow[0][2 * j], mrow[0][2 * j + 1]),
+                                        __dadd_rn(mrow[1][2 * j], mrow[1][2 * j + 1]));
+            const double mc = __dmul_rn(sm, 0.25);  // /4 == *0.25 exactly
+            const uchar4 q = wc[j];
+            uo[j] = blend_px(mc, q.x, q.y);
+            vo[j] = blend_px(mc, q.z, q.w);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // host-side launch helpers (called from api.cu)
 // ---------------------------------------------------------------------------
 template <int LEVEL, int KP, bool FULL8>
@@ -1457,8 +1619,14 @@ cudaError_t run_interp_stage(const Geometry& g, const PairTable& pt, uint8_t* ws
     if ((e = E()) != cudaSuccess) return e;
 
     B(KC_ROWSCAN);
-    k_rowscan<<<dim3((g.H + kRB - 1) / kRB, npairs), kRowscanThreads, 0, st>>>(g, pt, ws, P, 0, true,
-                                                                              mask_out);
+    k_scan_carry<<<dim3((g.H + kCR - 1) / kCR, npairs), kCR, 0, st>>>(g, ws, P);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    {
+        const dim3 grd(((g.W + 7) / 8 + 127) / 128, g.H / 2, npairs);
+        if (g.fmt == FVV_YUV420) k_blend<FVV_YUV420><<<grd, 128, 0, st>>>(g, pt, ws, P, 0, true, mask_out);
+        else if (g.fmt == FVV_RGB8) k_blend<FVV_RGB8><<<grd, 128, 0, st>>>(g, pt, ws, P, 0, true, mask_out);
+        else k_blend<FVV_GRAY8><<<grd, 128, 0, st>>>(g, pt, ws, P, 0, true, mask_out);
+    }
     return E();
 }
 
@@ -1547,8 +1715,10 @@ cudaError_t run_diag(const Geometry& g, const PairTable& pt, uint8_t* ws, const 
         if (e != cudaSuccess) return e;
     }
     if (mask) {
-        dim3 grd2((g.H + kRB - 1) / kRB, 1);
-        k_rowscan<<<grd2, kRowscanThreads, 0, st>>>(g, pt, ws, P, pair, false, mask);
+        const dim3 grd(((g.W + 7) / 8 + 127) / 128, g.H / 2, 1);
+        if (g.fmt == FVV_YUV420) k_blend<FVV_YUV420><<<grd, 128, 0, st>>>(g, pt, ws, P, pair, false, mask);
+        else if (g.fmt == FVV_RGB8) k_blend<FVV_RGB8><<<grd, 128, 0, st>>>(g, pt, ws, P, pair, false, mask);
+        else k_blend<FVV_GRAY8><<<grd, 128, 0, st>>>(g, pt, ws, P, pair, false, mask);
         return cudaGetLastError();
     }
     return cudaSuccess;
