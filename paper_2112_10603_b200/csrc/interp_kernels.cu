@@ -1305,8 +1305,11 @@ __global__ void __launch_bounds__(128) k_blend(Geometry g, PairTable pt, const u
             vl[0] = a.x; vl[1] = a.y; vl[2] = a.z; vl[3] = a.w; vl[4] = b.x; vl[5] = b.y; vl[6] = b.z; vl[7] = b.w;
             vr[0] = c.x; vr[1] = c.y; vr[2] = c.z; vr[3] = c.w; vr[4] = d.x; vr[5] = d.y; vr[6] = d.z; vr[7] = d.w;
             if (FMT != FVV_RGB8) {
-                const uint2 p = *reinterpret_cast<const uint2*>(wl + ro + x0);
-                const uint2 q = *reinterpret_cast<const uint2*>(wr + ro + x0);
+                // u8 rows are only 4-byte aligned (W % 4 == 0)
+                const uint2 p = make_uint2(*reinterpret_cast<const uint32_t*>(wl + ro + x0),
+                                           *reinterpret_cast<const uint32_t*>(wl + ro + x0 + 4));
+                const uint2 q = make_uint2(*reinterpret_cast<const uint32_t*>(wr + ro + x0),
+                                           *reinterpret_cast<const uint32_t*>(wr + ro + x0 + 4));
 #pragma unroll
                 for (int j = 0; j < 4; j++) {
                     al[j] = (p.x >> (8 * j)) & 0xFF; al[4 + j] = (p.y >> (8 * j)) & 0xFF;
@@ -1345,8 +1348,8 @@ __global__ void __launch_bounds__(128) k_blend(Geometry g, PairTable pt, const u
                     lo |= (uint32_t)blend_px(mrow[rr][j], al[j], ar[j]) << (8 * j);
                     hi |= (uint32_t)blend_px(mrow[rr][4 + j], al[4 + j], ar[4 + j]) << (8 * j);
                 }
-                if (n == 8) *reinterpret_cast<uint2*>(out + ro + x0) = make_uint2(lo, hi);
-                else *reinterpret_cast<uint32_t*>(out + ro + x0) = lo;  // W % 4 == 0: n == 4
+                *reinterpret_cast<uint32_t*>(out + ro + x0) = lo;  // W % 4 == 0: n is 4 or 8
+                if (n == 8) *reinterpret_cast<uint32_t*>(out + ro + x0 + 4) = hi;
             }
         }
         if (mask_out) {
