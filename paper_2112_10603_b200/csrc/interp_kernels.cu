@@ -1223,11 +1223,20 @@ __global__ void __launch_bounds__(kRowscanThreads, FVV_MINB_ROWSCAN) k_rowscan(G
 // parallel (thread = 2 rows x 8 columns, chroma from the row pair).
 // ---------------------------------------------------------------------------
 constexpr int kCR = 32, kCC = 64;  // carry kernel: rows per CTA (one lane each), chunk columns
+constexpr int kCT = kCC + 16;       // staged u16 per row and chunk: sd[c0-8 .. c0+72)
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 __global__ void __launch_bounds__(kCR) k_scan_carry(Geometry g, const uint8_t* __restrict__ ws,
                                                     Planes P) {
     __shared__ double dtab[766];
-    __shared__ uint16_t tile[kCR][kCC + 4];  // sd[x-2 .. x+65] of the chunk, per row
+    __shared__ __align__(16) uint16_t tile[2][kCR][kCT];  // per lane: its own row segment
     const int W = g.W, H = g.H;
     const int pair = blockIdx.y, y0 = blockIdx.x * kCR;
     const int lane = threadIdx.x;
@@ -1235,33 +1244,55 @@ __global__ void __launch_bounds__(kCR) k_scan_carry(Geometry g, const uint8_t* _
     double* carry = reinterpret_cast<double*>(const_cast<uint8_t*>(ws) + P.stride * (size_t)pair + P.carry);
     const int ng = (W + 7) / 8;
     for (int i = lane; i < 766; i += kCR) dtab[i] = __ddiv_rn((double)i, 3.0);
-    const int y = y0 + lane;
+    const int y = min(y0 + lane, H - 1);
+    const bool live = y0 + lane < H;
+    const uint16_t* row = sd + (size_t)y * W;
+    const int nchunks = (W + kCC - 1) / kCC;
+    const bool vec = (W % 8) == 0;  // 16-byte aligned row segments
+    // stage chunk k into tile[k & 1][lane]: entry j holds sd[clamp(c0 - 8 + j)]
+    auto stage = [&](int k) {
+        const int c0 = k * kCC;
+        uint16_t* t = tile[k & 1][lane];
+        if (vec && c0 >= 8 && c0 - 8 + kCT <= W) {
+            const uint16_t* src = row + c0 - 8;
+#pragma unroll
+            for (int q = 0; q < kCT / 8; q++) cp_async16(t + 8 * q, src + 8 * q);
+        } else {
+            for (int j = 0; j < kCT; j++) t[j] = row[clampi(c0 - 8 + j, 0, W - 1)];
+        }
+        cp_async_commit();
+    };
+    stage(0);
     double tmp = 0.0;
-    for (int c0 = 0; c0 < W; c0 += kCC) {
-        __syncwarp();
-        // coalesced staging of sd[c0-2 .. c0+kCC+1] (clamped) for the warp's rows
-        for (int r = 0; r < kCR; r++) {
-            const int yy = min(y0 + r, H - 1);
-            const uint16_t* row = sd + (size_t)yy * W;
-            for (int j = lane; j < kCC + 4; j += 32) tile[r][j] = row[clampi(c0 - 2 + j, 0, W - 1)];
+    for (int k = 0; k < nchunks; k++) {
+        if (k + 1 < nchunks) {
+            stage(k + 1);
+            cp_async_wait_1();
+        } else {
+            cp_async_wait_0();
         }
         __syncwarp();
-        if (y < H) {
-            const int n = min(kCC, W - c0);
-            double* cr = carry + (size_t)y * ng + c0 / 8;
-            const uint16_t* t = tile[lane];  // t[j] = sd[c0 - 2 + j]
-            int c = 0;
-            if (c0 == 0) {
+        const int c0 = k * kCC;
+        const int n = min(kCC, W - c0);
+        const uint16_t* t = tile[k & 1][lane] + 6;  // t[j] = sd[clamp(c0 - 2 + j)]
+        double* cr = carry + (size_t)y * ng + c0 / 8;
+        for (int c8 = 0; c8 < n; c8 += 8) {
+            // p[x+2] - p[x-1] = D0[sd[min(x+1, W-1)]] - D0[sd[max(x-2, 0)]], x = c0 + c8 + j
+            double dl[8];
+#pragma unroll
+            for (int j = 0; j < 8; j++) dl[j] = __dsub_rn(dtab[t[c8 + j + 3]], dtab[t[c8 + j]]);
+            if (c0 + c8 == 0) {
                 tmp = __dadd_rn(__dadd_rn(dtab[t[2]], dtab[t[2]]), dtab[t[min(3, W + 1)]]);
-                cr[0] = tmp;
-                c = 1;
+            } else {
+                tmp = __dadd_rn(tmp, dl[0]);
             }
-            for (; c < n; c++) {
-                // p[x+2] - p[x-1] = D0[sd[min(x+1, W-1)]] - D0[sd[max(x-2, 0)]]
-                tmp = __dadd_rn(tmp, __dsub_rn(dtab[t[c + 3]], dtab[t[c]]));
-                if ((c & 7) == 0) cr[c >> 3] = tmp;
-            }
+            if (live) cr[c8 >> 3] = tmp;
+            const int m = min(8, n - c8);
+#pragma unroll
+            for (int j = 1; j < 8; j++)
+                if (j < m) tmp = __dadd_rn(tmp, dl[j]);
         }
+        __syncwarp();
     }
 }
 
