@@ -1224,31 +1224,36 @@ __global__ void __launch_bounds__(kRowscanThreads, FVV_MINB_ROWSCAN) k_rowscan(G
 // ---------------------------------------------------------------------------
 constexpr int kCR = 32, kCC = 64;  // carry kernel: rows per CTA (one lane each), chunk columns
 constexpr int kCT = kCC + 16;       // staged u16 per row and chunk: sd[c0-8 .. c0+72)
+constexpr int kCTP = kCT + 4;       // row pitch: 168 B = 21 x 8 B, 16 lanes hit 16 bank pairs
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
     const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
 }
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
+__device__ __forceinline__ double d0_of(int s) { return div3((double)s); }  // == s / 3.0 (IEEE)
+
 __global__ void __launch_bounds__(kCR) k_scan_carry(Geometry g, const uint8_t* __restrict__ ws,
                                                     Planes P) {
-    __shared__ double dtab[766];
-    __shared__ __align__(16) uint16_t tile[2][kCR][kCT];  // per lane: its own row segment
+    __shared__ __align__(16) uint16_t tile[2][kCR][kCTP];  // per lane: its own row segment
     const int W = g.W, H = g.H;
     const int pair = blockIdx.y, y0 = blockIdx.x * kCR;
     const int lane = threadIdx.x;
     const uint16_t* sd = cplane<uint16_t>(ws, P, P.sd, pair);
     double* carry = reinterpret_cast<double*>(const_cast<uint8_t*>(ws) + P.stride * (size_t)pair + P.carry);
     const int ng = (W + 7) / 8;
-    for (int i = lane; i < 766; i += kCR) dtab[i] = __ddiv_rn((double)i, 3.0);
     const int y = min(y0 + lane, H - 1);
     const bool live = y0 + lane < H;
     const uint16_t* row = sd + (size_t)y * W;
     const int nchunks = (W + kCC - 1) / kCC;
-    const bool vec = (W % 8) == 0;  // 16-byte aligned row segments
+    const bool vec = (W % 4) == 0;  // 8-byte aligned row segments (always, frames are W % 4 == 0)
     // stage chunk k into tile[k & 1][lane]: entry j holds sd[clamp(c0 - 8 + j)]
     auto stage = [&](int k) {
         const int c0 = k * kCC;
@@ -1256,7 +1261,7 @@ __global__ void __launch_bounds__(kCR) k_scan_carry(Geometry g, const uint8_t* _
         if (vec && c0 >= 8 && c0 - 8 + kCT <= W) {
             const uint16_t* src = row + c0 - 8;
 #pragma unroll
-            for (int q = 0; q < kCT / 8; q++) cp_async16(t + 8 * q, src + 8 * q);
+            for (int q = 0; q < kCT / 4; q++) cp_async8(t + 4 * q, src + 4 * q);
         } else {
             for (int j = 0; j < kCT; j++) t[j] = row[clampi(c0 - 8 + j, 0, W - 1)];
         }
@@ -1274,15 +1279,24 @@ __global__ void __launch_bounds__(kCR) k_scan_carry(Geometry g, const uint8_t* _
         __syncwarp();
         const int c0 = k * kCC;
         const int n = min(kCC, W - c0);
-        const uint16_t* t = tile[k & 1][lane] + 6;  // t[j] = sd[clamp(c0 - 2 + j)]
+        const uint16_t* tl = tile[k & 1][lane];  // tl[j] = sd[clamp(c0 - 8 + j)]
         double* cr = carry + (size_t)y * ng + c0 / 8;
         for (int c8 = 0; c8 < n; c8 += 8) {
-            // p[x+2] - p[x-1] = D0[sd[min(x+1, W-1)]] - D0[sd[max(x-2, 0)]], x = c0 + c8 + j
+            // sd[c0+c8-4 .. c0+c8+11] as four 64-bit quads: tl[c8+4 .. c8+19]
+            const uint2* q = reinterpret_cast<const uint2*>(tl + c8 + 4);
+            uint16_t v[16];
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                const uint2 w2 = q[i];
+                v[4 * i] = w2.x & 0xFFFF; v[4 * i + 1] = w2.x >> 16;
+                v[4 * i + 2] = w2.y & 0xFFFF; v[4 * i + 3] = w2.y >> 16;
+            }
+            // v[i] = sd[clamp(x0 - 4 + i)], x0 = c0 + c8; delta(x0+j) = D0[v[j+5]] - D0[v[j+2]]
             double dl[8];
 #pragma unroll
-            for (int j = 0; j < 8; j++) dl[j] = __dsub_rn(dtab[t[c8 + j + 3]], dtab[t[c8 + j]]);
+            for (int j = 0; j < 8; j++) dl[j] = __dsub_rn(d0_of(v[j + 5]), d0_of(v[j + 2]));
             if (c0 + c8 == 0) {
-                tmp = __dadd_rn(__dadd_rn(dtab[t[2]], dtab[t[2]]), dtab[t[min(3, W + 1)]]);
+                tmp = __dadd_rn(__dadd_rn(d0_of(v[4]), d0_of(v[4])), d0_of(v[W > 1 ? 5 : 4]));
             } else {
                 tmp = __dadd_rn(tmp, dl[0]);
             }
@@ -1300,11 +1314,8 @@ template <int FMT>
 __global__ void __launch_bounds__(128) k_blend(Geometry g, PairTable pt, const uint8_t* __restrict__ ws,
                                                Planes P, int pair_base, bool write_frame,
                                                double* mask_out /* nullable: one pair */) {
-    __shared__ double dtab[766];
     const int W = g.W, H = g.H;
     const int pair = blockIdx.z + pair_base;
-    for (int i = threadIdx.x; i < 766; i += blockDim.x) dtab[i] = __ddiv_rn((double)i, 3.0);
-    __syncthreads();
     const int ng = (W + 7) / 8;
     const int gx = blockIdx.x * blockDim.x + threadIdx.x;  // 8-column group
     const int yp = blockIdx.y;                              // row pair
@@ -1359,7 +1370,7 @@ __global__ void __launch_bounds__(128) k_blend(Geometry g, PairTable pt, const u
         double tmp = carry[(size_t)y * ng + gx];
 #pragma unroll
         for (int j = 0; j < 8; j++) {
-            if (j > 0) tmp = __dadd_rn(tmp, __dsub_rn(dtab[s[j + 3]], dtab[s[j]]));
+            if (j > 0) tmp = __dadd_rn(tmp, __dsub_rn(d0_of(s[j + 3]), d0_of(s[j])));
             mrow[rr][j] = j < n ? mask_of(tmp, vl[j], vr[j], g) : 0.0;
         }
         if (write_frame) {
