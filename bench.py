@@ -158,7 +158,7 @@ def kernel_figures(cfg, npairs_total):
         "k_sad<2>": ("int", "Gop/s", sad[2]),
         # warp + mask + blend: 2 source frames read, 1 view written (compulsory)
         "k_mask_cols": ("hbm", "GB/s", 2 * bframe * npairs_total),
-        "k_rowscan": ("hbm", "GB/s", bframe * npairs_total),
+        "k_scan_blend": ("hbm", "GB/s", bframe * npairs_total),
         "k_warpq<2>": ("hbm", "GB/s", (2 * W * H + 2 * 2 * W * H + 16 * W * H / 4) * npairs_total),
     }
 

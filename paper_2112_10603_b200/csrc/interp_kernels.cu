@@ -8,8 +8,9 @@
 //   k_warpq<L>   target warped by the base flow, *8, rint  flow.py:123-124, 77-78
 //   k_mask_cols  final flows, mid warps, |wl-wr| column    interp.py:131-136, 78-94
 //                sums, occlusion cue (exact, order-free)   warp.py:27-46
-//   k_rowscan    scipy running-sum replay along rows,      imageops.py:51-52, warp.py:49-88
-//                mask, blend of every plane
+//   k_scan_carry scipy's running sum along rows (ordered)  imageops.py:51-52
+//   k_blend      replay of 8-column chain segments, mask,  warp.py:49-88
+//                blend of every plane
 //
 // Numerics: see DESIGN.md sec. 3 -- integer SAD, literal f64 bilinear
 // arithmetic (no FMA), and the row-sequential replay of scipy's running sum
@@ -23,9 +24,6 @@
 // minimum resident CTAs per SM (register budgets), tuned on B200 -- see profiles/
 #ifndef FVV_MINB_MASK
 #define FVV_MINB_MASK 8
-#endif
-#ifndef FVV_MINB_ROWSCAN
-#define FVV_MINB_ROWSCAN 4
 #endif
 #ifndef FVV_MINB_SAD8
 #define FVV_MINB_SAD8 4
@@ -771,7 +769,7 @@ __device__ __forceinline__ float third_f32(int sn, float scale) {
 // np.gradient, the f32 occlusion cue and BOTH smoothing passes over it are
 // exact sums -- scipy's running sum equals the plain 3-tap sum bitwise.
 // |wl - wr| is integral, so its column pass is exact too; only its row pass
-// (k_rowscan) must replay scipy in order.  Structure: a register-streaming
+// (k_scan_carry / k_blend) must replay scipy in order.  Structure: a register-streaming
 // column walker.  A warp owns kMW output columns (lanes 2..kMW+1; two halo
 // lanes per side supply x-neighbours through shuffles) and walks down a
 // kMH-row band, carrying lagged sliding windows:
@@ -1002,26 +1000,8 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
 }
 
 // ---------------------------------------------------------------------------
-// k_rowscan: the row pass of smooth3(|wl - wr|) replayed in scipy's order
-// (tmp = (p0+p1)+p2; tmp += p[i+2]-p[i-1]; out = tmp/3, all f64), then the
-// mask (warp.py:49-63) and the blend of every plane (warp.py:66-88).
-//
-// Warp-specialised pipeline over 64-column chunks of a 32-row band:
-//   warp 0 (one lane per row) runs the order-dependent DADD chain of chunk k
-//   warps 1-7 meanwhile build the differences of chunk k+1, then -- once the
-//   chain has released chunk k -- evaluate mask and blend for it.
-// Named barriers hand the double-buffered chunk back and forth.
+// Per-pixel mask and blend (warp.py:49-88), shared by k_blend.
 // ---------------------------------------------------------------------------
-constexpr int kRB = 16, kCW = 64;  // 16-row bands: enough CTAs to hide latency at small stages
-constexpr int kWorkers = kRB * 8, kRowscanThreads = kWorkers + 32;
-
-__device__ __forceinline__ void bar_sync(int id, int n) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void bar_arrive(int id, int n) {
-    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
 // mask (warp.py:63) and clip for one pixel from the row-pass running sum
 __device__ __forceinline__ double mask_of(double tsum, float occ_l, float occ_r, const Geometry& g) {
     const double D = div3(tsum);
@@ -1035,182 +1015,6 @@ __device__ __forceinline__ double mask_of(double tsum, float occ_l, float occ_r,
 // blend (warp.py:66-67): to_uint8(m * a + (1 - m) * b)
 __device__ __forceinline__ uint8_t blend_px(double m, int a, int b) {
     return to_u8(__dadd_rn(__dmul_rn(m, (double)a), __dmul_rn(__dsub_rn(1.0, m), (double)b)));
-}
-
-__global__ void __launch_bounds__(kRowscanThreads, FVV_MINB_ROWSCAN) k_rowscan(Geometry g, PairTable pt,
-                                                              const uint8_t* __restrict__ ws, Planes P,
-                                                              int pair_base, bool write_frame,
-                                                              double* mask_out /* nullable: one pair */) {
-    __shared__ double dtab[766];                // s/3.0 for the integral column sums
-    __shared__ double buf[2][kRB][kCW + 2];     // deltas -> running sums -> masks
-    const int W = g.W, H = g.H;
-    const int pair = blockIdx.y + pair_base;
-    const int y0 = blockIdx.x * kRB;
-    const int tid = threadIdx.x;
-    const int nchunks = (W + kCW - 1) / kCW;
-    const uint16_t* sd = cplane<uint16_t>(ws, P, P.sd, pair);
-    for (int i = tid; i < 766; i += kRowscanThreads) dtab[i] = __ddiv_rn((double)i, 3.0);
-    __syncthreads();
-
-    if (tid >= kWorkers) {
-        // ---------------- chain warp: lane = row ----------------
-        const int r = tid - kWorkers;
-        const bool live = r < kRB && y0 + r < H;
-        const uint16_t* row = sd + (size_t)(live ? y0 + r : 0) * W;
-        double tmp = 0.0;
-        for (int k = 0; k < nchunks; k++) {
-            const int b = k & 1, c0 = k * kCW;
-            bar_sync(1 + b, kRowscanThreads);  // deltas of chunk k ready
-            if (live) {
-                double* br = buf[b][r];
-                const int n = min(kCW, W - c0);
-                int c = 0;
-                if (c0 == 0) {
-                    tmp = __dadd_rn(__dadd_rn(dtab[row[0]], dtab[row[0]]), dtab[row[min(1, W - 1)]]);
-                    br[0] = tmp;
-                    c = 1;
-                }
-                for (; c + 16 <= n; c += 16) {
-                    double v[16];
-#pragma unroll
-                    for (int j = 0; j < 16; j++) v[j] = br[c + j];
-#pragma unroll
-                    for (int j = 0; j < 16; j++) {
-                        tmp = __dadd_rn(tmp, v[j]);
-                        v[j] = tmp;
-                    }
-#pragma unroll
-                    for (int j = 0; j < 16; j++) br[c + j] = v[j];
-                }
-                for (; c < n; c++) {
-                    tmp = __dadd_rn(tmp, br[c]);
-                    br[c] = tmp;
-                }
-            }
-            bar_arrive(3 + b, kRowscanThreads);  // running sums of chunk k ready
-        }
-        return;
-    }
-
-    // ---------------- worker warps: thread = (row, 8 consecutive columns) ----------------
-    const int r = tid >> 3, cb = (tid & 7) * 8;
-    const int y = y0 + r;
-    const bool rowok = y < H;
-    const size_t rowoff = (size_t)(rowok ? y : 0) * W;
-    const uint16_t* srow = sd + rowoff;
-    const float* ol = cplane<float>(ws, P, P.occ_l, pair) + rowoff;
-    const float* orr = cplane<float>(ws, P, P.occ_r, pair) + rowoff;
-    const uint8_t* wl = cplane<uint8_t>(ws, P, P.wl, pair) + rowoff;
-    const uint8_t* wr = cplane<uint8_t>(ws, P, P.wr, pair) + rowoff;
-    uint8_t* out = pt.out[pair];
-
-    auto deltas = [&](int k) {  // p[i+2] - p[i-1] of chunk k (independent of the chain)
-        const int b = k & 1, x0 = k * kCW + cb;
-        if (!rowok || x0 >= W) return;
-        int s[11];  // sd at x0-2 .. x0+8 (clamped): all loads in flight together
-#pragma unroll
-        for (int j = 0; j < 11; j++) s[j] = srow[clampi(x0 - 2 + j, 0, W - 1)];
-#pragma unroll
-        for (int j = 0; j < 8; j++) buf[b][r][cb + j] = __dsub_rn(dtab[s[j + 3]], dtab[s[j]]);
-    };
-
-    deltas(0);
-    bar_arrive(1, kRowscanThreads);
-    for (int k = 0; k < nchunks; k++) {
-        const int b = k & 1, c0 = k * kCW, x0 = c0 + cb;
-        if (k + 1 < nchunks) {
-            if (k >= 1) bar_sync(5, kWorkers);  // every worker is done with chunk k-1's buffer
-            deltas(k + 1);
-            bar_arrive(1 + (b ^ 1), kRowscanThreads);
-        }
-        // prefetch this thread's 8 pixels of inputs before waiting on the chain
-        const bool full = rowok && x0 + 8 <= W;
-        const bool any = rowok && x0 < W;
-        float4 ola = make_float4(0, 0, 0, 0), olb = ola, ora = ola, orb = ola;
-        uchar4 wla = make_uchar4(0, 0, 0, 0), wlb = wla, wra = wla, wrb = wla;
-        if (full) {
-            ola = *reinterpret_cast<const float4*>(ol + x0);
-            olb = *reinterpret_cast<const float4*>(ol + x0 + 4);
-            ora = *reinterpret_cast<const float4*>(orr + x0);
-            orb = *reinterpret_cast<const float4*>(orr + x0 + 4);
-            if (g.fmt != FVV_RGB8) {
-                wla = *reinterpret_cast<const uchar4*>(wl + x0);
-                wlb = *reinterpret_cast<const uchar4*>(wl + x0 + 4);
-                wra = *reinterpret_cast<const uchar4*>(wr + x0);
-                wrb = *reinterpret_cast<const uchar4*>(wr + x0 + 4);
-            }
-        } else if (any) {  // W % 4 == 0: exactly 4 valid columns
-            ola = *reinterpret_cast<const float4*>(ol + x0);
-            ora = *reinterpret_cast<const float4*>(orr + x0);
-            if (g.fmt != FVV_RGB8) {
-                wla = *reinterpret_cast<const uchar4*>(wl + x0);
-                wra = *reinterpret_cast<const uchar4*>(wr + x0);
-            }
-        }
-        bar_sync(3 + b, kRowscanThreads);  // the chain released chunk k
-        if (any) {
-            const float vl[8] = {ola.x, ola.y, ola.z, ola.w, olb.x, olb.y, olb.z, olb.w};
-            const float vr[8] = {ora.x, ora.y, ora.z, ora.w, orb.x, orb.y, orb.z, orb.w};
-            const int n = full ? 8 : 4;
-            double m[8];
-#pragma unroll
-            for (int j = 0; j < 8; j++)
-                if (j < n) m[j] = mask_of(buf[b][r][cb + j], vl[j], vr[j], g);
-            if (write_frame) {
-                if (g.fmt == FVV_RGB8) {
-                    const uint8_t* px = cplane<uint8_t>(ws, P, P.wrgb, pair) + (rowoff + x0) * 6;
-                    uint8_t* o = out + (rowoff + x0) * 3;
-#pragma unroll
-                    for (int j = 0; j < 8; j++)
-                        if (j < n)
-#pragma unroll
-                            for (int ch = 0; ch < 3; ch++)
-                                o[3 * j + ch] = blend_px(m[j], px[6 * j + ch], px[6 * j + 3 + ch]);
-                } else {
-                    const uint8_t al[8] = {wla.x, wla.y, wla.z, wla.w, wlb.x, wlb.y, wlb.z, wlb.w};
-                    const uint8_t ar[8] = {wra.x, wra.y, wra.z, wra.w, wrb.x, wrb.y, wrb.z, wrb.w};
-                    uint8_t o8[8];
-#pragma unroll
-                    for (int j = 0; j < 8; j++) o8[j] = blend_px(m[j], al[j], ar[j]);
-                    *reinterpret_cast<uchar4*>(out + rowoff + x0) = make_uchar4(o8[0], o8[1], o8[2], o8[3]);
-                    if (full)
-                        *reinterpret_cast<uchar4*>(out + rowoff + x0 + 4) =
-                            make_uchar4(o8[4], o8[5], o8[6], o8[7]);
-                }
-            }
-            if (mask_out) {
-#pragma unroll
-                for (int j = 0; j < 8; j++)
-                    if (j < n) mask_out[rowoff + x0 + j] = m[j];
-            }
-#pragma unroll
-            for (int j = 0; j < 8; j++)
-                if (j < n) buf[b][r][cb + j] = m[j];
-        }
-        // chroma blend with the 2x2-mean mask (warp.py:83-88): thread = (chroma row, 2 columns)
-        if (g.fmt == FVV_YUV420 && write_frame) {
-            bar_sync(6, kWorkers);  // masks of the whole chunk are in smem
-            const int cw = g.cw, chh = g.ch;
-            const int a = tid >> 4, c2 = (tid & 15) * 2;  // kRB/2 chroma rows x 32 chroma columns
-            const int cy = y0 / 2 + a, cx = c0 / 2 + c2;
-            if (cy < chh && cx < cw) {
-                const uchar4* wc = cplane<uchar4>(ws, P, P.wc, pair) + (size_t)cy * cw + cx;
-                uint8_t* uo = out + (size_t)W * H + (size_t)cy * cw + cx;
-                uint8_t* vo = uo + (size_t)cw * chh;
-#pragma unroll
-                for (int j = 0; j < 2; j++) {
-                    if (cx + j >= cw) break;
-                    const int bb = c2 + j;
-                    const double sm = __dadd_rn(__dadd_rn(buf[b][2 * a][2 * bb], buf[b][2 * a][2 * bb + 1]),
-                                                __dadd_rn(buf[b][2 * a + 1][2 * bb], buf[b][2 * a + 1][2 * bb + 1]));
-                    const double mc = __dmul_rn(sm, 0.25);  // /4 == *0.25 exactly
-                    const uchar4 q = wc[j];
-                    uo[j] = blend_px(mc, q.x, q.y);
-                    vo[j] = blend_px(mc, q.z, q.w);
-                }
-            }
-        }
-    }
 }
 
 // ---------------------------------------------------------------------------
