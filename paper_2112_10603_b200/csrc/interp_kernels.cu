@@ -784,9 +784,7 @@ __device__ __forceinline__ float third_f32(int sn, float scale) {
 // ---------------------------------------------------------------------------
 constexpr int kMW = 28, kMWarps = 4, kMH = 64;
 
-// PART 0: flows + luma/chroma warps + |wl-wr| column sums; PART 1: flows + occlusion
-// chain; PART 2: both (one pass).
-template <int FMT, int PART>
+template <int FMT>
 __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geometry g, PairTable pt,
                                                                uint8_t* __restrict__ ws, Planes P) {
     const int W = g.W, H = g.H;
@@ -904,14 +902,11 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
             F1[d] = F2[d];
             F2[d] = make_int2(-((base.x << bs) + (res.x << rs)), -((base.y << bs) + (res.y << rs)));
             // x-gradient at yy (np.gradient edge order 1), units 2^-(mb+1)
-            if (PART != 0) {
-                const int xl = __shfl_sync(0xffffffffu, F2[d].x, srcL);
-                const int xr = __shfl_sync(0xffffffffu, F2[d].x, srcR);
-                gx1[d] = gx2[d];
-                gx2[d] = gmul * (xr - xl);
-            }
+            const int xl = __shfl_sync(0xffffffffu, F2[d].x, srcL);
+            const int xr = __shfl_sync(0xffffffffu, F2[d].x, srcR);
+            gx1[d] = gx2[d];
+            gx2[d] = gmul * (xr - xl);
         }
-        if (PART != 1) {
         // ---- luma warps at yy (warp.py:37), d = |wl - wr| ----
         int wl, wr;
         if (FMT == FVV_RGB8) {
@@ -946,8 +941,6 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
             const int t = yy - 1;
             if (t >= y0 && t < yo1 && own) o_sd[(size_t)t * W + x] = (uint16_t)((t == 0 ? d1 : d0) + d1 + d2);
         }
-        }
-        if (PART != 0) {
         // ---- occ(yy-1) then O0/O(yy-2) ----
         {
             const int r = yy - 1;
@@ -967,9 +960,8 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
                 }
             }
         }
-        }
         // ---- chroma warps for chroma row (yy-1)/2 at odd yy (imageops.py:40-48) ----
-        if (PART != 1 && FMT == FVV_YUV420 && (yy & 1) && yy - 1 >= y0 && yy - 1 < yo1 && yy - 1 >= ys) {
+        if (FMT == FVV_YUV420 && (yy & 1) && yy - 1 >= y0 && yy - 1 < yo1 && yy - 1 >= ys) {
             const int cw = g.cw, chh = g.ch, cb = mb + 3, kC = 2 * cb;
             int2 cv[2];
 #pragma unroll
@@ -992,7 +984,7 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
         }
     }
     // ---- bottom edge: occ(H-1) (one-sided gy), O0/O(H-2), O0/O(H-1), Sd(H-1) ----
-    if (ye == H - 1 && PART != 0) {
+    if (ye == H - 1) {
 #pragma unroll
         for (int d = 0; d < 2; d++) {
             const int gy = H < 2 ? 0 : 2 * (F2[d].y - F1[d].y);
@@ -1003,8 +995,6 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
         }
         if (H - 2 >= y0 && H - 2 < yo1) emit_o(H - 2, oc0[0], oc0[1], oc1[0], oc1[1], oc2[0], oc2[1]);
         if (H - 1 >= y0 && H - 1 < yo1) emit_o(H - 1, oc1[0], oc1[1], oc2[0], oc2[1], oc2[0], oc2[1]);
-    }
-    if (ye == H - 1 && PART != 1) {
         if (own && H - 1 >= y0 && H - 1 < yo1) o_sd[(size_t)(H - 1) * W + x] = (uint16_t)(d1 + d2 + d2);
     }
 }
@@ -1471,25 +1461,9 @@ cudaError_t run_interp_stage(const Geometry& g, const PairTable& pt, uint8_t* ws
     B(KC_MASK_PROD);
     {
         const dim3 grd((g.W + kMW * kMWarps - 1) / (kMW * kMWarps), (g.H + kMH - 1) / kMH, npairs);
-#ifndef FVV_MASK_SPLIT
-#define FVV_MASK_SPLIT 1
-#endif
-        if (FVV_MASK_SPLIT) {
-            if (g.fmt == FVV_YUV420) {
-                k_mask_cols<FVV_YUV420, 0><<<grd, kMWarps * 32, 0, st>>>(g, pt, ws, P);
-                k_mask_cols<FVV_YUV420, 1><<<grd, kMWarps * 32, 0, st>>>(g, pt, ws, P);
-            } else if (g.fmt == FVV_RGB8) {
-                k_mask_cols<FVV_RGB8, 0><<<grd, kMWarps * 32, 0, st>>>(g, pt, ws, P);
-                k_mask_cols<FVV_RGB8, 1><<<grd, kMWarps * 32, 0, st>>>(g, pt, ws, P);
-            } else {
-                k_mask_cols<FVV_GRAY8, 0><<<grd, kMWarps * 32, 0, st>>>(g, pt, ws, P);
-                k_mask_cols<FVV_GRAY8, 1><<<grd, kMWarps * 32, 0, st>>>(g, pt, ws, P);
-            }
-        } else {
-            if (g.fmt == FVV_YUV420) k_mask_cols<FVV_YUV420, 2><<<grd, kMWarps * 32, 0, st>>>(g, pt, ws, P);
-            else if (g.fmt == FVV_RGB8) k_mask_cols<FVV_RGB8, 2><<<grd, kMWarps * 32, 0, st>>>(g, pt, ws, P);
-            else k_mask_cols<FVV_GRAY8, 2><<<grd, kMWarps * 32, 0, st>>>(g, pt, ws, P);
-        }
+        if (g.fmt == FVV_YUV420) k_mask_cols<FVV_YUV420><<<grd, kMWarps * 32, 0, st>>>(g, pt, ws, P);
+        else if (g.fmt == FVV_RGB8) k_mask_cols<FVV_RGB8><<<grd, kMWarps * 32, 0, st>>>(g, pt, ws, P);
+        else k_mask_cols<FVV_GRAY8><<<grd, kMWarps * 32, 0, st>>>(g, pt, ws, P);
     }
     if ((e = E()) != cudaSuccess) return e;
 
