@@ -474,6 +474,7 @@ def run_b200(args, cfg, rank, world, local_rank):
                 "per_kernel_ms_per_step": {k: round(v[0], 4) for k, v in per_class.items()}}
 
     launches_per_step = sum(v[1] for v in per_class.values())
+    launches_per_step += per_class.get("k_scan_blend", (0, 0))[1]  # bracket = k_scan_carry + k_blend
     # SAD classes launch a second (ragged-column) kernel when the level width is not a multiple of 8
     for s, (lw, _lh) in enumerate([(W // 4, H // 4), (W // 2, H // 2), (W, H)]):
         if lw % 8:
