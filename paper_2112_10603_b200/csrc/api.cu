@@ -12,6 +12,7 @@
 #include "fvv_device.cuh"
 
 namespace fvv {
+extern int g_failed_class;
 cudaError_t run_interp_stage(const Geometry& g, const PairTable& pt, uint8_t* ws, const Planes& P,
                              const int16_t* const* rank_of, const int16_t* const* cand_of_rank,
                              int npairs, double* mask_out, Prof* prof, cudaStream_t st);
@@ -292,7 +293,12 @@ static int run_pairs(fvv_engine* e, const uint8_t* const* L, const uint8_t* cons
         }
         cudaError_t ce = run_interp_stage(e->g, pt, e->slots, e->P, e->rank_of, e->cand_of_rank, n,
                                           nullptr, e->profiling ? &e->prof : nullptr, st);
-        if (ce != cudaSuccess) return cuda_fail(ce, "interpolate");
+        if (ce != cudaSuccess) {
+            const int c = g_failed_class;
+            g_failed_class = -1;
+            return cuda_fail(ce, c >= 0 ? (std::string("interpolate (") + fvv_kernel_class_name(c) + ")").c_str()
+                                        : "interpolate");
+        }
         e->last = pt;
         e->last_npairs = n;
     }

@@ -17,6 +17,7 @@
 // where the reference's rounding is order dependent.
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "fvv_device.cuh"
@@ -796,7 +797,8 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
     const int x = xw0 - 2 + lane;
     const int xc = clampi(x, 0, W - 1);
     const bool own = lane >= 2 && lane < 2 + kMW && x < W;
-    const Level L1 = g.lv[1], L2 = g.lv[2];
+    const Level& L1 = g.lv[1];
+    const Level& L2 = g.lv[2];
     const int B2 = L2.block, D2 = 2 * B2, lgD2 = 31 - __clz(D2);
     const int mb = g.fb[2] + 1, kY = 2 * mb;
     const int bs = g.fb[2] - (g.fb[1] + 3), rs = g.fb[2] - g.rb[2];
@@ -841,10 +843,9 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
         return sn ? third_f32(sn, oscale) : 0.0f;
     };
 
-    // source-row caches: rows ua, ua+1 in use, ua+2 already in flight (loaded two
-    // output rows before it is needed); the same for block rows ba..ba+2
+    // source-row caches: x-lerped rows ua, ua+1 of flow1 and ba, ba+1 of the block grid
     int ua = -10, ba = -10;
-    int2 hu0[2], hu1[2], hu2[2], hb0[2], hb1[2], hb2[2];
+    int2 hu0[2], hu1[2], hb0[2], hb1[2];
     int2 F0[2], F1[2], F2[2];
     int gx1[2] = {0, 0}, gx2[2] = {0, 0};
     int oc0[2] = {0, 0}, oc1[2] = {0, 0}, oc2[2] = {0, 0};
@@ -868,14 +869,8 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
         if (ty.i0 != ua) {
 #pragma unroll
             for (int d = 0; d < 2; d++) {
-                if (ty.i0 == ua + 1) {
-                    hu0[d] = hu1[d];
-                    hu1[d] = hu2[d];
-                } else {
-                    hu0[d] = xl_u(d, ty.i0);
-                    hu1[d] = xl_u(d, ty.i0 + 1);
-                }
-                hu2[d] = xl_u(d, min(ty.i0 + 2, L1.h - 1));
+                hu0[d] = ty.i0 == ua + 1 ? hu1[d] : xl_u(d, ty.i0);
+                hu1[d] = xl_u(d, ty.i0 + 1);
             }
             ua = ty.i0;
         }
@@ -883,14 +878,8 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
         if (tby.i0 != ba) {
 #pragma unroll
             for (int d = 0; d < 2; d++) {
-                if (tby.i0 == ba + 1) {
-                    hb0[d] = hb1[d];
-                    hb1[d] = hb2[d];
-                } else {
-                    hb0[d] = xl_b(d, tby.i0);
-                    hb1[d] = xl_b(d, tby.i1);
-                }
-                hb2[d] = xl_b(d, min(tby.i1 + 1, L2.nby - 1));
+                hb0[d] = tby.i0 == ba + 1 ? hb1[d] : xl_b(d, tby.i0);
+                hb1[d] = xl_b(d, tby.i1);
             }
             ba = tby.i0;
         }
@@ -1227,6 +1216,250 @@ __global__ void __launch_bounds__(128) k_blend(Geometry g, PairTable pt, const u
 // ---------------------------------------------------------------------------
 // host-side launch helpers (called from api.cu)
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// k_sadw: the 8x8-block search for 8-aligned levels (w % 8 == 0) -- pixel-pair
+// packing as k_sadp, restructured so that nearly every issued instruction is
+// search arithmetic:
+//  * the target window is staged RAW (u16 samples, 16-byte cp.async straight
+//    into shared memory, edge replication at chunk granularity); the odd
+//    pixel pairs are formed in registers with one PRMT each;
+//  * the reference strip is staged once per block as pixel-pair words, with
+//    the per-block reference sum accumulated during staging;
+//  * sum(b) per candidate comes from per-thread column sums of the target
+//    pair words (SIDE + 6 adds per row instead of 4 * SIDE);
+//  * thread = (dy, dx group, block) with the block index fastest: the 8
+//    threads of a shared-memory phase read 8 consecutive 16-byte groups of
+//    one row (conflict-free by construction), the CTA is 8 x NBY blocks;
+//  * winner key = sad << 10 | tie-rule rank (< 2^27), 32-bit smem atomicMin.
+// Candidates of one thread: dx + r in [c0, c0 + CG); with more than one group
+// CG is even, so every group shares the pair parity of group 0.  Same exact integer SAD as k_sad.
+// ---------------------------------------------------------------------------
+#ifndef FVV_MINB_SADW
+#define FVV_MINB_SADW(side) ((side) > 13 ? 2 : ((side) > 9 ? 3 : 4))
+#endif
+#ifdef FVV_DEBUG
+#include <cassert>
+#define FVV_DBG_ALIGN(p, a) assert((reinterpret_cast<uintptr_t>(p) & ((a) - 1)) == 0)
+#else
+#define FVV_DBG_ALIGN(p, a) ((void)0)
+#endif
+template <int SIDE, int CG>
+struct SadW {
+    static constexpr int R = SIDE / 2;
+    static constexpr int NG = (SIDE + CG - 1) / CG;        // dx groups per dy row
+    static constexpr int NBY = (256 / (8 * SIDE * NG)) > 0 ? 256 / (8 * SIDE * NG) : 1;
+    static constexpr int NB = 8 * NBY;                     // blocks per CTA (8 x NBY)
+    static constexpr int TPG = ((NB * SIDE + 31) / 32) * 32; // threads per dx group (whole warps)
+    static constexpr int THREADS = TPG * NG;
+    static constexpr int XPAD = 8 * ((R + 7) / 8);         // left apron, chunk aligned
+    static constexpr int NPJ = CG + 6;                     // pair words per row and thread
+    static constexpr int LASTW = 4 * 7 + 4 * (((XPAD - R + (NG - 1) * CG + NPJ) / 2) / 4) + 3;  // last word read
+    static constexpr int WW = 8 * ((LASTW / 4) + 1) > 64 + 2 * XPAD ? 8 * ((LASTW / 4) + 1)
+                                                                    : 64 + 2 * XPAD;  // samples
+    static constexpr int TWW = WW / 2;                     // words per window row
+    static constexpr int WH = 8 * NBY + 2 * R;             // window rows
+    static constexpr size_t SMEM = (size_t)WH * TWW * 4 + (size_t)8 * NBY * 32 * 4 +
+                                   (size_t)NB * 8 + (size_t)SIDE * SIDE * 2;
+};
+
+struct SadWLaunch {
+    int bx_end;                  // full 8-wide block columns (w / 8)
+    const int16_t* rank_of;
+    const int16_t* cand_of_rank;
+};
+
+template <int LEVEL>
+__device__ __forceinline__ const uint16_t* sadw_tgt(const Geometry& g, const PairTable& pt, uint8_t* ws,
+                                                    const Planes& P, int pair, int d) {
+    return LEVEL == 0 ? cplane<uint16_t>(ws, P, P.q0[1 - d], pair)
+         : LEVEL == 1 ? cplane<uint16_t>(ws, P, P.tq1[d], pair)
+                      : cplane<uint16_t>(ws, P, P.tq2[d], pair);
+}
+
+// Full 16-byte shared load, never narrowed: a quarter-warp phase (8 blocks of
+// one block row) then reads 8 distinct 16-byte bank groups.  Narrowed 32-bit
+// loads would put the 4 block rows of a warp on the same banks.
+__device__ __forceinline__ uint4 lds128(const uint32_t* p) {
+    uint4 v;
+    const unsigned a = (unsigned)__cvta_generic_to_shared(p);
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+
+// One thread's search: dx + r in [G*CG, G*CG + CG), every row of its block.
+// Word offsets are compile time, so the window reads are aligned LDS.128.
+template <int SIDE, int CG, int G>
+__device__ __forceinline__ uint32_t sadw_group(const uint32_t* Rb, const uint32_t* Tb, int rows, int sa,
+                                               const int16_t* rki) {
+    using S = SadW<SIDE, CG>;
+    constexpr int base = S::XPAD - S::R + G * CG;          // window sample of pair 0
+    constexpr int ch0 = (base / 2) / 4, ch1 = ((base + S::NPJ) / 2) / 4;
+    uint32_t am[CG], cs[S::NPJ];
+#pragma unroll
+    for (int c = 0; c < CG; c++) am[c] = 0;
+#pragma unroll
+    for (int j = 0; j < S::NPJ; j++) cs[j] = 0;
+#pragma unroll 2
+    for (int yy = 0; yy < rows; yy++) {
+        uint32_t wv[4 * (ch1 - ch0 + 1)];
+#pragma unroll
+        for (int q = ch0; q <= ch1; q++) {
+            FVV_DBG_ALIGN(Tb + yy * S::TWW + 4 * q, 16);
+            const uint4 t4 = lds128(Tb + yy * S::TWW + 4 * q);
+            wv[4 * (q - ch0)] = t4.x; wv[4 * (q - ch0) + 1] = t4.y;
+            wv[4 * (q - ch0) + 2] = t4.z; wv[4 * (q - ch0) + 3] = t4.w;
+        }
+        FVV_DBG_ALIGN(Rb + yy * 32, 16);
+        const uint4 r4 = lds128(Rb + yy * 32);
+        const uint32_t rv[4] = {r4.x, r4.y, r4.z, r4.w};
+        uint32_t pv[S::NPJ];
+#pragma unroll
+        for (int j = 0; j < S::NPJ; j++) {
+            const int sidx = base + j;                           // compile time
+            const int wi = sidx / 2 - 4 * ch0;
+            pv[j] = (sidx & 1) ? __byte_perm(wv[wi], wv[wi + 1], 0x5432) : wv[wi];
+            cs[j] += pv[j];
+        }
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+#pragma unroll
+            for (int c = 0; c < CG; c++) am[c] += __vmaxu2(pv[2 * k + c], rv[k]);
+    }
+    uint32_t mine = 0xFFFFFFFFu;
+#pragma unroll
+    for (int c = 0; c < CG; c++) {
+        const int cc = G * CG + c;
+        if (cc < SIDE) {
+            const uint32_t ab = cs[c] + cs[c + 2] + cs[c + 4] + cs[c + 6];   // lanes <= 65280
+            const int sad = 2 * (int)((am[c] & 0xFFFFu) + (am[c] >> 16)) -
+                            (int)((ab & 0xFFFFu) + (ab >> 16)) - sa;
+            mine = min(mine, ((uint32_t)sad << 10) | (uint32_t)rki[cc]);
+        }
+    }
+    return mine;
+}
+
+template <int LEVEL, int SIDE, int CG>
+__global__ void __launch_bounds__(SadW<SIDE, CG>::THREADS, FVV_MINB_SADW(SIDE))
+k_sadw(Geometry g, PairTable pt, uint8_t* __restrict__ ws, Planes P, SadWLaunch sl) {
+    using S = SadW<SIDE, CG>;
+    static_assert(S::NG == 1 || CG % 2 == 0, "dx groups need an even width");
+    extern __shared__ __align__(16) uint8_t smem[];
+    uint32_t* Ts = reinterpret_cast<uint32_t*>(smem);              // WH x TWW raw words
+    uint32_t* Rs = Ts + S::WH * S::TWW;                            // 8*NBY x 32 pair words
+    uint32_t* best = Rs + 8 * S::NBY * 32;                         // NB keys
+    int* suma = reinterpret_cast<int*>(best + S::NB);              // NB reference sums
+    int16_t* rk = reinterpret_cast<int16_t*>(suma + S::NB);        // SIDE^2 ranks
+
+    const Level& L = g.lv[LEVEL];
+    const int w = L.w, h = L.h;
+    const int pair = blockIdx.z >> 1, d = blockIdx.z & 1;
+    const int bx0 = blockIdx.x * 8, by0 = blockIdx.y * S::NBY;
+    const int tid = threadIdx.x;
+
+    // ---- stage: target window (raw u16, edge replicated) -------------------
+    const uint16_t* tg = sadw_tgt<LEVEL>(g, pt, ws, P, pair, d);
+    const int xa = bx0 * 8 - S::XPAD, ya = by0 * 8 - S::R;
+    constexpr int NCH = S::WW / 8;                                  // 16-byte chunks per row
+    for (int i = tid; i < S::WH * NCH; i += S::THREADS) {
+        const int t = i / NCH, q = i - t * NCH;
+        const int gy = clampi(ya + t, 0, h - 1), gx = xa + 8 * q;
+        uint32_t* dst = Ts + t * S::TWW + 4 * q;
+        if (gx >= 0 && gx + 8 <= w) {
+            FVV_DBG_ALIGN(dst, 16); FVV_DBG_ALIGN(tg + (size_t)gy * w + gx, 16);
+            cp_async16(dst, tg + (size_t)gy * w + gx);
+        } else {
+            const uint32_t v = tg[(size_t)gy * w + (gx < 0 ? 0 : w - 1)];
+            const uint32_t vv = v | (v << 16);
+            *reinterpret_cast<uint4*>(dst) = make_uint4(vv, vv, vv, vv);
+        }
+    }
+    cp_async_commit();
+    // ---- stage: reference strip as pixel-pair words + per-block sums -------
+    for (int i = tid; i < S::NB; i += S::THREADS) { best[i] = 0xFFFFFFFFu; suma[i] = 0; }
+    for (int i = tid; i < SIDE * SIDE; i += S::THREADS) rk[i] = sl.rank_of[i];
+    __syncthreads();
+    for (int i = tid; i < 8 * S::NBY * 8; i += S::THREADS) {       // (row, block column)
+        const int kx = i & 7, yy = i >> 3;
+        const int gy = by0 * 8 + yy, gx = (bx0 + kx) * 8;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (gy < h && gx < w) {
+            const size_t o = (size_t)gy * w + gx;
+            if (LEVEL == 2) {
+                const uint8_t* yp = g.fmt == FVV_RGB8 ? cplane<uint8_t>(ws, P, P.luma[d], pair)
+                                                      : (d ? pt.right[pair] : pt.left[pair]);
+                uint2 b;
+                if ((reinterpret_cast<uintptr_t>(yp + o) & 7) == 0) {
+                    b = *reinterpret_cast<const uint2*>(yp + o);
+                } else {
+                    b.x = yp[o] | (yp[o + 1] << 8) | (yp[o + 2] << 16) | ((uint32_t)yp[o + 3] << 24);
+                    b.y = yp[o + 4] | (yp[o + 5] << 8) | (yp[o + 6] << 16) | ((uint32_t)yp[o + 7] << 24);
+                }
+                v.x = __byte_perm(b.x, 0, 0x4140) << 3; v.y = __byte_perm(b.x, 0, 0x4342) << 3;
+                v.z = __byte_perm(b.y, 0, 0x4140) << 3; v.w = __byte_perm(b.y, 0, 0x4342) << 3;
+            } else {
+                const uint16_t* rp = LEVEL == 0 ? cplane<uint16_t>(ws, P, P.q0[d], pair)
+                                                : cplane<uint16_t>(ws, P, P.s4[d], pair);
+                FVV_DBG_ALIGN(rp + o, 16);
+                v = *reinterpret_cast<const uint4*>(rp + o);
+                if (LEVEL == 1) { v.x <<= 1; v.y <<= 1; v.z <<= 1; v.w <<= 1; }  // 2 * s4 <= 2040
+            }
+            const uint32_t ps = v.x + v.y + v.z + v.w;                // lanes <= 4 * 2040
+            atomicAdd(&suma[(yy >> 3) * 8 + kx], (int)((ps & 0xFFFFu) + (ps >> 16)));
+        }
+        FVV_DBG_ALIGN(Rs + yy * 32 + 4 * kx, 16);
+        *reinterpret_cast<uint4*>(Rs + yy * 32 + 4 * kx) = v;
+    }
+    cp_async_wait_0();
+    __syncthreads();
+
+    // ---- search ---------------------------------------------------------------
+    const int gq = tid / S::TPG, rest = tid - gq * S::TPG;      // dx group is warp-uniform
+    const int kb = rest % S::NB, iy = rest / S::NB;
+    const int kx = kb & 7, ky = kb >> 3;
+    const bool active = iy < SIDE && bx0 + kx < sl.bx_end && by0 + ky < L.nby;
+    if (active) {
+        const int rows = min(8, h - (by0 + ky) * 8);
+        const uint32_t* Rb = Rs + (ky * 8) * 32 + 4 * kx;
+        const uint32_t* Tb = Ts + (ky * 8 + iy) * S::TWW + 4 * kx;
+        const int sa = suma[kb];
+        const int16_t* rki = rk + iy * SIDE;
+        uint32_t mine;
+        if (S::NG == 1 || gq == 0) mine = sadw_group<SIDE, CG, 0>(Rb, Tb, rows, sa, rki);
+        else mine = sadw_group<SIDE, CG, (S::NG > 1 ? 1 : 0)>(Rb, Tb, rows, sa, rki);
+        atomicMin(&best[kb], mine);
+    }
+    __syncthreads();
+    if (tid < S::NB) {
+        const int hx = bx0 + (tid & 7), hy = by0 + (tid >> 3);
+        if (hx < sl.bx_end && hy < L.nby) {
+            const uint32_t key = best[tid];
+            const int idx = sl.cand_of_rank[key & 1023u];
+            BlockHit hit;
+            hit.dy = (int16_t)(idx / SIDE - S::R);
+            hit.dx = (int16_t)(idx % SIDE - S::R);
+            hit.sad = (int32_t)(key >> 10);
+            plane<BlockHit>(ws, P, P.hit[LEVEL][d], pair)[hy * L.nbx + hx] = hit;
+        }
+    }
+}
+
+template <int LEVEL, int SIDE, int CG>
+static cudaError_t launch_sadw(const Geometry& g, const PairTable& pt, uint8_t* ws, const Planes& P,
+                               SadWLaunch sl, int npairs, cudaStream_t st) {
+    using S = SadW<SIDE, CG>;
+    const Level& L = g.lv[LEVEL];
+    auto kern = k_sadw<LEVEL, SIDE, CG>;
+    if (S::SMEM > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
+        if (e != cudaSuccess) return e;
+    }
+    dim3 grid((sl.bx_end + 7) / 8, (L.nby + S::NBY - 1) / S::NBY, 2 * npairs);
+    kern<<<grid, S::THREADS, S::SMEM, st>>>(g, pt, ws, P, sl);
+    return cudaGetLastError();
+}
+
 template <int LEVEL, int KP, bool FULL8>
 static cudaError_t launch_sad_kp(const Geometry& g, const PairTable& pt, uint8_t* ws,
                                  const Planes& P, SadLaunch sl, int npairs, cudaStream_t st) {
@@ -1318,6 +1551,21 @@ static cudaError_t run_sad(const Geometry& g, const PairTable& pt, uint8_t* ws, 
     // accumulators cost occupancy, and the candidate-pair kernel is faster
     const bool pix = full_cols > 0 && (side == 3 || side == 5 || side == 9 || side == 13 ||
                                        side == 17);
+    if (fast && (L.w & 7) == 0 && (side == 3 || side == 5 || side == 9 || side == 13 || side == 17 ||
+                                   side == 25)) {
+        SadWLaunch sw;
+        sw.bx_end = full_cols;
+        sw.rank_of = rank_of;
+        sw.cand_of_rank = cand_of_rank;
+        switch (side) {
+            case 3: return launch_sadw<LEVEL, 3, 3>(g, pt, ws, P, sw, npairs, st);
+            case 5: return launch_sadw<LEVEL, 5, 5>(g, pt, ws, P, sw, npairs, st);
+            case 9: return launch_sadw<LEVEL, 9, 9>(g, pt, ws, P, sw, npairs, st);
+            case 13: return launch_sadw<LEVEL, 13, 13>(g, pt, ws, P, sw, npairs, st);
+            case 17: return launch_sadw<LEVEL, 17, 17>(g, pt, ws, P, sw, npairs, st);
+            default: return launch_sadw<LEVEL, 25, 14>(g, pt, ws, P, sw, npairs, st);
+        }
+    }
     if (pix) {
         SadPLaunch sp;
         sp.rank_of = rank_of;
@@ -1414,12 +1662,27 @@ static cudaError_t run_sad(const Geometry& g, const PairTable& pt, uint8_t* ws, 
     return cudaSuccess;
 }
 
+int g_failed_class = -1;
+
 cudaError_t run_interp_stage(const Geometry& g, const PairTable& pt, uint8_t* ws, const Planes& P,
                              const int16_t* const* rank_of, const int16_t* const* cand_of_rank,
                              int npairs, double* mask_out, Prof* prof, cudaStream_t st) {
     cudaError_t e = cudaSuccess;
-    auto B = [&](int c) { if (prof) prof->begin(c, st); };
-    auto E = [&]() { if (prof) prof->end(st); return cudaGetLastError(); };
+    // FVV_SYNC_CHECK=1: synchronise after every kernel class and report the
+    // class that faulted (debugging aid; off by default, never in a graph)
+    static const bool sync_check = getenv("FVV_SYNC_CHECK") && *getenv("FVV_SYNC_CHECK") == '1';
+    int cur = -1;
+    auto B = [&](int c) { cur = c; if (prof) prof->begin(c, st); };
+    auto E = [&]() {
+        if (prof) prof->end(st);
+        cudaError_t ce = cudaGetLastError();
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        if (ce == cudaSuccess && sync_check && cudaStreamIsCapturing(st, &cap) == cudaSuccess &&
+            cap == cudaStreamCaptureStatusNone)
+            ce = cudaStreamSynchronize(st);
+        if (ce != cudaSuccess) g_failed_class = cur;
+        return ce;
+    };
 
     B(KC_PYRAMID);
     k_pyramid<<<dim3((g.lv[0].w + 31) / 32, (g.lv[0].h + 7) / 8, 2 * npairs), dim3(32, 8), 0, st>>>(
