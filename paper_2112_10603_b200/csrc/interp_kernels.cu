@@ -1225,6 +1225,9 @@ __global__ void __launch_bounds__(128) k_blend(Geometry g, PairTable pt, const u
 //    pixel pairs are formed in registers with one PRMT each;
 //  * the reference strip is staged once per block as pixel-pair words, with
 //    the per-block reference sum accumulated during staging;
+//  * sum(max) is accumulated with IDP.2A (lo + hi + acc, fma pipe) so that the
+//    alu pipe -- the bound: VIMNMX, PRMT, IADD3 all issue there at half rate --
+//    carries only the max and the column sums;
 //  * sum(b) per candidate comes from per-thread column sums of the target
 //    pair words (SIDE + 6 adds per row instead of 4 * SIDE);
 //  * thread = (dy, dx group, block) with the block index fastest: the 8
@@ -1282,7 +1285,7 @@ __device__ __forceinline__ const uint16_t* sadw_tgt(const Geometry& g, const Pai
 __device__ __forceinline__ uint4 lds128(const uint32_t* p) {
     uint4 v;
     const unsigned a = (unsigned)__cvta_generic_to_shared(p);
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
+    asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
     return v;
 }
@@ -1324,7 +1327,7 @@ __device__ __forceinline__ uint32_t sadw_group(const uint32_t* Rb, const uint32_
 #pragma unroll
         for (int k = 0; k < 4; k++)
 #pragma unroll
-            for (int c = 0; c < CG; c++) am[c] += __vmaxu2(pv[2 * k + c], rv[k]);
+            for (int c = 0; c < CG; c++) am[c] = __dp2a_lo(__vmaxu2(pv[2 * k + c], rv[k]), 0x0101u, am[c]);
     }
     uint32_t mine = 0xFFFFFFFFu;
 #pragma unroll
@@ -1332,8 +1335,7 @@ __device__ __forceinline__ uint32_t sadw_group(const uint32_t* Rb, const uint32_
         const int cc = G * CG + c;
         if (cc < SIDE) {
             const uint32_t ab = cs[c] + cs[c + 2] + cs[c + 4] + cs[c + 6];   // lanes <= 65280
-            const int sad = 2 * (int)((am[c] & 0xFFFFu) + (am[c] >> 16)) -
-                            (int)((ab & 0xFFFFu) + (ab >> 16)) - sa;
+            const int sad = 2 * (int)am[c] - (int)((ab & 0xFFFFu) + (ab >> 16)) - sa;
             mine = min(mine, ((uint32_t)sad << 10) | (uint32_t)rki[cc]);
         }
     }
@@ -1362,17 +1364,25 @@ k_sadw(Geometry g, PairTable pt, uint8_t* __restrict__ ws, Planes P, SadWLaunch 
     const uint16_t* tg = sadw_tgt<LEVEL>(g, pt, ws, P, pair, d);
     const int xa = bx0 * 8 - S::XPAD, ya = by0 * 8 - S::R;
     constexpr int NCH = S::WW / 8;                                  // 16-byte chunks per row
-    for (int i = tid; i < S::WH * NCH; i += S::THREADS) {
-        const int t = i / NCH, q = i - t * NCH;
-        const int gy = clampi(ya + t, 0, h - 1), gx = xa + 8 * q;
-        uint32_t* dst = Ts + t * S::TWW + 4 * q;
-        if (gx >= 0 && gx + 8 <= w) {
-            FVV_DBG_ALIGN(dst, 16); FVV_DBG_ALIGN(tg + (size_t)gy * w + gx, 16);
-            cp_async16(dst, tg + (size_t)gy * w + gx);
-        } else {
-            const uint32_t v = tg[(size_t)gy * w + (gx < 0 ? 0 : w - 1)];
-            const uint32_t vv = v | (v << 16);
-            *reinterpret_cast<uint4*>(dst) = make_uint4(vv, vv, vv, vv);
+    static_assert(NCH <= 16, "two window rows per warp pass");
+    {
+        const int lane = tid & 31, q = lane & 15;                   // chunk of this lane
+        const int gx = xa + 8 * q;
+        const bool inside = gx >= 0 && gx + 8 <= w;
+        const int cx = gx < 0 ? 0 : w - 1;                           // replicated edge column
+        if (q < NCH) {
+            for (int t = 2 * (tid >> 5) + (lane >> 4); t < S::WH; t += 2 * (S::THREADS / 32)) {
+                const uint16_t* row = tg + (size_t)clampi(ya + t, 0, h - 1) * w;
+                uint32_t* dst = Ts + t * S::TWW + 4 * q;
+                if (inside) {
+                    FVV_DBG_ALIGN(dst, 16); FVV_DBG_ALIGN(row + gx, 16);
+                    cp_async16(dst, row + gx);
+                } else {
+                    const uint32_t v = row[cx];
+                    const uint32_t vv = v | (v << 16);
+                    *reinterpret_cast<uint4*>(dst) = make_uint4(vv, vv, vv, vv);
+                }
+            }
         }
     }
     cp_async_commit();
@@ -1380,6 +1390,10 @@ k_sadw(Geometry g, PairTable pt, uint8_t* __restrict__ ws, Planes P, SadWLaunch 
     for (int i = tid; i < S::NB; i += S::THREADS) { best[i] = 0xFFFFFFFFu; suma[i] = 0; }
     for (int i = tid; i < SIDE * SIDE; i += S::THREADS) rk[i] = sl.rank_of[i];
     __syncthreads();
+    const uint8_t* yp = LEVEL != 2 ? nullptr
+                      : g.fmt == FVV_RGB8 ? cplane<uint8_t>(ws, P, P.luma[d], pair)
+                                          : (d ? pt.right[pair] : pt.left[pair]);
+    const bool yal = (reinterpret_cast<uintptr_t>(yp) & 7) == 0;  // w % 8 == 0: every row 8-aligned
     for (int i = tid; i < 8 * S::NBY * 8; i += S::THREADS) {       // (row, block column)
         const int kx = i & 7, yy = i >> 3;
         const int gy = by0 * 8 + yy, gx = (bx0 + kx) * 8;
@@ -1387,10 +1401,8 @@ k_sadw(Geometry g, PairTable pt, uint8_t* __restrict__ ws, Planes P, SadWLaunch 
         if (gy < h && gx < w) {
             const size_t o = (size_t)gy * w + gx;
             if (LEVEL == 2) {
-                const uint8_t* yp = g.fmt == FVV_RGB8 ? cplane<uint8_t>(ws, P, P.luma[d], pair)
-                                                      : (d ? pt.right[pair] : pt.left[pair]);
                 uint2 b;
-                if ((reinterpret_cast<uintptr_t>(yp + o) & 7) == 0) {
+                if (yal) {
                     b = *reinterpret_cast<const uint2*>(yp + o);
                 } else {
                     b.x = yp[o] | (yp[o + 1] << 8) | (yp[o + 2] << 16) | ((uint32_t)yp[o + 3] << 24);
