@@ -783,7 +783,10 @@ __device__ __forceinline__ float third_f32(int sn, float scale) {
 // Edge rows/columns follow the reference: one-sided np.gradient, nearest
 // padding for smooth3.  No shared memory, no index division.
 // ---------------------------------------------------------------------------
-constexpr int kMW = 28, kMWarps = 4, kMH = 64;
+#ifndef FVV_KMH
+#define FVV_KMH 64
+#endif
+constexpr int kMW = 28, kMWarps = 4, kMH = FVV_KMH;
 
 template <int FMT>
 __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geometry g, PairTable pt,
