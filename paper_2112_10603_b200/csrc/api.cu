@@ -108,6 +108,9 @@ void make_geometry(const fvv_frame_desc* d, const fvv_interp_params* p, Geometry
     g->fb[0] = g->rb[0];
     g->fb[1] = std::max(g->fb[0] + 3, g->rb[1]);
     g->fb[2] = std::max(g->fb[1] + 3, g->rb[2]);
+    g->qmargin[0] = 0;
+    g->qmargin[1] = 2 * p->search_radius[0];
+    g->qmargin[2] = 4 * p->search_radius[0] + 2 * p->search_radius[1];
 }
 
 // workspace = [header: candidate tables][pair slot 0][pair slot 1]...

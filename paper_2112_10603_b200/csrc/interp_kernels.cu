@@ -714,16 +714,21 @@ __global__ void __launch_bounds__(256) k_warpq(Geometry g, PairTable pt, uint8_t
                                                Planes P) {
     __shared__ int2 h[kQH / 2 + 3][kQW];
     __shared__ ITap cxt[kQW];
-    const Level L = g.lv[LEVEL];
-    const Level Lp = g.lv[LEVEL - 1];
+    __shared__ int4 rt[kQH];  // per tile row: base-flow y tap (i0 - s_lo, i1 - s_lo, f)
+    const Level& L = g.lv[LEVEL];
+    const Level& Lp = g.lv[LEVEL - 1];
     const int pair = blockIdx.z >> 1, d = blockIdx.z & 1;
     const int x0 = blockIdx.x * kQW, y0 = blockIdx.y * kQH;
     const int tid = threadIdx.x, tx = tid & 63, tg = tid >> 6;
     const int2* prev = cplane<int2>(ws, P, LEVEL == 1 ? P.flow0[d] : P.flow1[d], pair);
-    if (tid < kQW) cxt[tid] = clamp_itap32(2 * min(x0 + tid, L.w - 1) - 1, 2, Lp.w);
     const int ylast = min(y0 + kQH - 1, L.h - 1);
     const int s_lo = clamp_itap32(2 * y0 - 1, 2, Lp.h).i0;
     const int s_n = clamp_itap32(2 * ylast - 1, 2, Lp.h).i1 - s_lo + 1;
+    if (tid < kQW) {
+        cxt[tid] = clamp_itap32(2 * min(x0 + tid, L.w - 1) - 1, 2, Lp.w);
+        const ITap t = clamp_itap32(2 * min(y0 + tid, L.h - 1) - 1, 2, Lp.h);
+        rt[tid] = make_int4(t.i0 - s_lo, t.i1 - s_lo, t.f, 0);
+    }
     __syncthreads();
     for (int row = tg; row < s_n; row += 4) {
         const int2* pr = prev + (size_t)(s_lo + row) * Lp.w;
@@ -739,11 +744,44 @@ __global__ void __launch_bounds__(256) k_warpq(Geometry g, PairTable pt, uint8_t
     const uint16_t* s4 = cplane<uint16_t>(ws, P, P.s4[1 - d], pair);
     const uint8_t* yp = g.fmt == FVV_RGB8 ? cplane<uint8_t>(ws, P, P.luma[1 - d], pair)
                                           : (d ? pt.left[pair] : pt.right[pair]);
+    const int M = g.qmargin[LEVEL];
+    const bool interior = x0 >= M && x0 + kQW - 1 + M <= w - 2 && y0 >= M && y0 + kQH - 1 + M <= L.h - 2;
+    if (interior) {
+        // every sample position (x, y) + base lies in [0, n-2] + [0, 1): no clamping,
+        // taps are a shift and a mask (bit-identical to the clamped form here)
+        const int k = LEVEL == 1 ? 2 * vb - 1 : 2 * vb - 3;
+        const int fmask = (1 << vb) - 1;
+        const int xs = x << vb;
+        uint16_t* op = outp + (size_t)(y0 + tg) * w + x;
+#pragma unroll 4
+        for (int ty = tg; ty < kQH; ty += 4) {
+            const int y = y0 + ty;
+            const int4 r = rt[ty];
+            const int2 base = lerp_i2(h[r.x][tx], h[r.y][tx], 4, r.z);
+            const int sx = xs + base.x, sy = (y << vb) + base.y;
+            const int fx = sx & fmask, fy = sy & fmask;
+            const int off = (sy >> vb) * w + (sx >> vb);
+            int a, b, c, e;
+            if (LEVEL == 1) {
+                const uint16_t* p0 = s4 + off;
+                a = p0[0]; b = p0[1]; c = p0[w]; e = p0[w + 1];
+            } else {
+                const uint8_t* p0 = yp + off;
+                a = p0[0]; b = p0[1]; c = p0[w]; e = p0[w + 1];
+            }
+            const int top = (a << vb) + fx * (b - a);
+            const int bot = (c << vb) + fx * (e - c);
+            const long long v = ((long long)top << vb) + (long long)fy * (long long)(bot - top);
+            *op = (uint16_t)rne64(v, k);
+            op += 4 * (size_t)w;
+        }
+        return;
+    }
     for (int ty = tg; ty < kQH; ty += 4) {
         const int y = y0 + ty;
         if (y >= L.h) break;
-        const ITap t = clamp_itap32(2 * y - 1, 2, Lp.h);
-        const int2 base = lerp_i2(h[t.i0 - s_lo][tx], h[t.i1 - s_lo][tx], 4, t.f);
+        const int4 r = rt[ty];
+        const int2 base = lerp_i2(h[r.x][tx], h[r.y][tx], 4, r.z);
         int q;
         if (LEVEL == 1) {
             // value = v / (4 * 2^(2vb)); rint(8 * value) = rint(v / 2^(2vb - 1))
