@@ -158,7 +158,8 @@ def kernel_figures(cfg, npairs_total):
         "k_sad<2>": ("int", "Gop/s", sad[2]),
         # warp + mask + blend: 2 source frames read, 1 view written (compulsory)
         "k_mask_cols": ("hbm", "GB/s", 2 * bframe * npairs_total),
-        "k_scan_blend": ("hbm", "GB/s", bframe * npairs_total),
+        "k_scan_carry": ("hbm", "GB/s", 2 * W * H * npairs_total),
+        "k_blend": ("hbm", "GB/s", bframe * npairs_total),
         "k_warpq<2>": ("hbm", "GB/s", (2 * W * H + 2 * 2 * W * H + 16 * W * H / 4) * npairs_total),
     }
 
@@ -415,7 +416,7 @@ def run_b200(args, cfg, rank, world, local_rank):
         for _ in range(prof_steps):
             compute_one(0)
     torch.cuda.synchronize()
-    n = 10
+    n = 11  # FVV_NUM_KERNEL_CLASSES
     ms_k = (ctypes.c_double * n)()
     cnt_k = (ctypes.c_int * n)()
     _lib.check(L.fvv_profile_read(eng._h, ms_k, cnt_k, n))
@@ -474,7 +475,6 @@ def run_b200(args, cfg, rank, world, local_rank):
                 "per_kernel_ms_per_step": {k: round(v[0], 4) for k, v in per_class.items()}}
 
     launches_per_step = sum(v[1] for v in per_class.values())
-    launches_per_step += per_class.get("k_scan_blend", (0, 0))[1]  # bracket = k_scan_carry + k_blend
     # SAD classes launch a second (ragged-column) kernel when the level width is not a multiple of 8
     for s, (lw, _lh) in enumerate([(W // 4, H // 4), (W // 2, H // 2), (W, H)]):
         if lw % 8:

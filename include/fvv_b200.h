@@ -106,7 +106,7 @@ int fvv_interp_level_diagnostics(fvv_engine* engine, int pair, int level, float*
  * fvv_profile_read synchronises on the recorded events, returns the summed
  * milliseconds and launch counts per kernel class and resets the record.
  * capacity <= 0 disables.  Not for use under CUDA-graph capture. */
-#define FVV_NUM_KERNEL_CLASSES 10
+#define FVV_NUM_KERNEL_CLASSES 11
 int fvv_profile_enable(fvv_engine* engine, int capacity);
 int fvv_profile_read(fvv_engine* engine, double* ms, int* launches, int nclasses);
 const char* fvv_kernel_class_name(int kernel_class);

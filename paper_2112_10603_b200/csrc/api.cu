@@ -347,7 +347,7 @@ int fvv_profile_read(fvv_engine* e, double* ms, int* launches, int nclasses) {
 const char* fvv_kernel_class_name(int c) {
     static const char* names[KC_COUNT] = {"k_pyramid", "k_sad<0>", "k_flow<0>", "k_warpq<1>",
                                           "k_sad<1>", "k_flow<1>", "k_warpq<2>", "k_sad<2>",
-                                          "k_mask_cols", "k_scan_blend"};
+                                          "k_mask_cols", "k_scan_carry", "k_blend"};
     return c >= 0 && c < KC_COUNT ? names[c] : "";
 }
 

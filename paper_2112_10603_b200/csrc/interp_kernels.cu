@@ -1037,14 +1037,14 @@ __device__ __forceinline__ double mask_of(double tsum, float occ_l, float occ_r,
     const double D = div3(tsum);
     const float ql = __fadd_rn(0.5f, __fmul_rn(4.0f, occ_l));
     const float qr = __fadd_rn(0.5f, __fmul_rn(4.0f, occ_r));
-    const double el = __dmul_rn(D, (double)ql);
-    const double er = __dmul_rn(D, (double)qr);
+    const double el = __dmul_rn(D, f2d_posnormal(ql));  // ql, qr >= 0.5
+    const double er = __dmul_rn(D, f2d_posnormal(qr));
     const double m = __ddiv_rn(__dadd_rn(er, g.eps), __dadd_rn(__dadd_rn(el, er), g.eps2));
     return m < 0.0 ? 0.0 : (m > 1.0 ? 1.0 : m);  // np.clip (m is never NaN: den >= 2 eps)
 }
 // blend (warp.py:66-67): to_uint8(m * a + (1 - m) * b)
 __device__ __forceinline__ uint8_t blend_px(double m, int a, int b) {
-    return to_u8(__dadd_rn(__dmul_rn(m, (double)a), __dmul_rn(__dsub_rn(1.0, m), (double)b)));
+    return to_u8_small(__dadd_rn(__dmul_rn(m, u2d_exact(a)), __dmul_rn(__dsub_rn(1.0, m), u2d_exact(b))));
 }
 
 // ---------------------------------------------------------------------------
@@ -1072,7 +1072,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
-__device__ __forceinline__ double d0_of(int s) { return div3((double)s); }  // == s / 3.0 (IEEE)
+__device__ __forceinline__ double d0_of(int s) { return div3(u2d_exact(s)); }  // == s / 3.0 (IEEE)
 
 __global__ void __launch_bounds__(kCR) k_scan_carry(Geometry g, const uint8_t* __restrict__ ws,
                                                     Planes P) {
@@ -1088,14 +1088,24 @@ __global__ void __launch_bounds__(kCR) k_scan_carry(Geometry g, const uint8_t* _
     const uint16_t* row = sd + (size_t)y * W;
     const int nchunks = (W + kCC - 1) / kCC;
     const bool vec = (W % 4) == 0;  // 8-byte aligned row segments (always, frames are W % 4 == 0)
-    // stage chunk k into tile[k & 1][lane]: entry j holds sd[clamp(c0 - 8 + j)]
+    // stage chunk k into tile[k & 1][lane]: entry j holds sd[clamp(c0 - 8 + j)].
+    // In-range entries come in 8-byte cp.async pieces (c0 - 8 and W are
+    // multiples of 4); only the clamped ends are written with plain stores.
     auto stage = [&](int k) {
         const int c0 = k * kCC;
         uint16_t* t = tile[k & 1][lane];
-        if (vec && c0 >= 8 && c0 - 8 + kCT <= W) {
-            const uint16_t* src = row + c0 - 8;
-#pragma unroll
-            for (int q = 0; q < kCT / 4; q++) cp_async8(t + 4 * q, src + 4 * q);
+        if (vec) {
+            const int jlo = max(0, 8 - c0);                  // first in-range entry
+            const int jhi = min(kCT, W - (c0 - 8));          // one past the last
+            for (int j = jlo; j < jhi; j += 4) cp_async8(t + j, row + c0 - 8 + j);
+            if (jlo > 0) {
+                const uint16_t v = row[0];
+                for (int j = 0; j < jlo; j++) t[j] = v;
+            }
+            if (jhi < kCT) {
+                const uint16_t v = row[W - 1];
+                for (int j = max(jhi, 0); j < kCT; j++) t[j] = v;
+            }
         } else {
             for (int j = 0; j < kCT; j++) t[j] = row[clampi(c0 - 8 + j, 0, W - 1)];
         }
@@ -1103,6 +1113,7 @@ __global__ void __launch_bounds__(kCR) k_scan_carry(Geometry g, const uint8_t* _
     };
     stage(0);
     double tmp = 0.0;
+    double ep[3] = {0.0, 0.0, 0.0};  // D0 of sd[x0-2 .. x0] carried from the previous group
     for (int k = 0; k < nchunks; k++) {
         if (k + 1 < nchunks) {
             stage(k + 1);
@@ -1115,37 +1126,69 @@ __global__ void __launch_bounds__(kCR) k_scan_carry(Geometry g, const uint8_t* _
         const int n = min(kCC, W - c0);
         const uint16_t* tl = tile[k & 1][lane];  // tl[j] = sd[clamp(c0 - 8 + j)]
         double* cr = carry + (size_t)y * ng + c0 / 8;
-        for (int c8 = 0; c8 < n; c8 += 8) {
-            // sd[c0+c8-4 .. c0+c8+11] as four 64-bit quads: tl[c8+4 .. c8+19]
-            const uint2* q = reinterpret_cast<const uint2*>(tl + c8 + 4);
-            uint16_t v[16];
+        double cv[kCC / 8];   // this chunk's carries: one 64-byte row segment per lane
 #pragma unroll
-            for (int i = 0; i < 4; i++) {
-                const uint2 w2 = q[i];
-                v[4 * i] = w2.x & 0xFFFF; v[4 * i + 1] = w2.x >> 16;
-                v[4 * i + 2] = w2.y & 0xFFFF; v[4 * i + 3] = w2.y >> 16;
-            }
-            // v[i] = sd[clamp(x0 - 4 + i)], x0 = c0 + c8; delta(x0+j) = D0[v[j+5]] - D0[v[j+2]]
-            double dl[8];
+        for (int i = 0; i < kCC / 8; i++) cv[i] = 0.0;
 #pragma unroll
-            for (int j = 0; j < 8; j++) dl[j] = __dsub_rn(d0_of(v[j + 5]), d0_of(v[j + 2]));
-            if (c0 + c8 == 0) {
-                tmp = __dadd_rn(__dadd_rn(d0_of(v[4]), d0_of(v[4])), d0_of(v[W > 1 ? 5 : 4]));
+        for (int c8 = 0; c8 < kCC; c8 += 8) {
+            if (c8 >= n) break;
+            const int x0 = c0 + c8;
+            // sd[x0+1 .. x0+8] = tl[c8+9 .. c8+16]: new D0 values of this group
+            double e[11];                       // e[i] = D0(sd[clamp(x0 - 2 + i)])
+            if (x0 == 0) {
+                const uint2 h = *reinterpret_cast<const uint2*>(tl + c8 + 8);  // sd[0..3]
+                e[2] = d0_of(h.x & 0xFFFF);
+                e[0] = e[1] = e[2];
             } else {
-                tmp = __dadd_rn(tmp, dl[0]);
+                e[0] = ep[0]; e[1] = ep[1]; e[2] = ep[2];
             }
-            if (live) cr[c8 >> 3] = tmp;
-            const int m = min(8, n - c8);
+            {
+                const uint2 qa = *reinterpret_cast<const uint2*>(tl + c8 + 8);   // sd[x0 .. x0+3]
+                const uint2 qb = *reinterpret_cast<const uint2*>(tl + c8 + 12);  // sd[x0+4 .. x0+7]
+                const uint2 qc = *reinterpret_cast<const uint2*>(tl + c8 + 16);  // sd[x0+8 .. x0+11]
+                e[3] = d0_of(qa.x >> 16);    e[4] = d0_of(qa.y & 0xFFFF); e[5] = d0_of(qa.y >> 16);
+                e[6] = d0_of(qb.x & 0xFFFF); e[7] = d0_of(qb.x >> 16);    e[8] = d0_of(qb.y & 0xFFFF);
+                e[9] = d0_of(qb.y >> 16);    e[10] = d0_of(qc.x & 0xFFFF);
+            }
+            ep[0] = e[8]; ep[1] = e[9]; ep[2] = e[10];
+            // delta(x0 + j) = D0(sd[x0+j+1]) - D0(sd[x0+j-2]) = e[j+3] - e[j]
+            if (x0 == 0) {
+                tmp = __dadd_rn(__dadd_rn(e[2], e[2]), W > 1 ? e[3] : e[2]);
+            } else {
+                tmp = __dadd_rn(tmp, __dsub_rn(e[3], e[0]));
+            }
+            cv[c8 >> 3] = tmp;
+            if (n - c8 >= 8) {
 #pragma unroll
-            for (int j = 1; j < 8; j++)
-                if (j < m) tmp = __dadd_rn(tmp, dl[j]);
+                for (int j = 1; j < 8; j++) tmp = __dadd_rn(tmp, __dsub_rn(e[j + 3], e[j]));
+            } else {
+                const int m = n - c8;
+#pragma unroll
+                for (int j = 1; j < 8; j++)
+                    if (j < m) tmp = __dadd_rn(tmp, __dsub_rn(e[j + 3], e[j]));
+            }
+        }
+        if (live) {
+            const int ngc = (n + 7) / 8;
+            if (ngc == kCC / 8 && (ng & 1) == 0) {   // 16-byte aligned full segment
+#pragma unroll
+                for (int i = 0; i < kCC / 8; i += 2)
+                    *reinterpret_cast<double2*>(cr + i) = make_double2(cv[i], cv[i + 1]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < kCC / 8; i++)
+                    if (i < ngc) cr[i] = cv[i];
+            }
         }
         __syncwarp();
     }
 }
 
+#ifndef FVV_MINB_BLEND
+#define FVV_MINB_BLEND 5
+#endif
 template <int FMT>
-__global__ void __launch_bounds__(128) k_blend(Geometry g, PairTable pt, const uint8_t* __restrict__ ws,
+__global__ void __launch_bounds__(128, FVV_MINB_BLEND) k_blend(Geometry g, PairTable pt, const uint8_t* __restrict__ ws,
                                                Planes P, int pair_base, bool write_frame,
                                                double* mask_out /* nullable: one pair */) {
     const int W = g.W, H = g.H;
@@ -1162,7 +1205,7 @@ __global__ void __launch_bounds__(128) k_blend(Geometry g, PairTable pt, const u
     const uint8_t* wl = cplane<uint8_t>(ws, P, P.wl, pair);
     const uint8_t* wr = cplane<uint8_t>(ws, P, P.wr, pair);
     uint8_t* out = pt.out[pair];
-    double mrow[2][8];
+    double csum[4];  // chroma: per column pair, m(2j) + m(2j+1) of the upper row
 #pragma unroll
     for (int rr = 0; rr < 2; rr++) {
         const int y = 2 * yp + rr;
@@ -1202,10 +1245,11 @@ __global__ void __launch_bounds__(128) k_blend(Geometry g, PairTable pt, const u
         }
         // replay the running sum inside the group: tmp(x0) from the carry, then x0+1 ..
         double tmp = carry[(size_t)y * ng + gx];
+        double mrow[8];
 #pragma unroll
         for (int j = 0; j < 8; j++) {
             if (j > 0) tmp = __dadd_rn(tmp, __dsub_rn(d0_of(s[j + 3]), d0_of(s[j])));
-            mrow[rr][j] = j < n ? mask_of(tmp, vl[j], vr[j], g) : 0.0;
+            mrow[j] = j < n ? mask_of(tmp, vl[j], vr[j], g) : 0.0;
         }
         if (write_frame) {
             if (FMT == FVV_RGB8) {
@@ -1216,13 +1260,13 @@ __global__ void __launch_bounds__(128) k_blend(Geometry g, PairTable pt, const u
                     if (j < n)
 #pragma unroll
                         for (int ch = 0; ch < 3; ch++)
-                            o[3 * j + ch] = blend_px(mrow[rr][j], px[6 * j + ch], px[6 * j + 3 + ch]);
+                            o[3 * j + ch] = blend_px(mrow[j], px[6 * j + ch], px[6 * j + 3 + ch]);
             } else {
                 uint32_t lo = 0, hi = 0;
 #pragma unroll
                 for (int j = 0; j < 4; j++) {
-                    lo |= (uint32_t)blend_px(mrow[rr][j], al[j], ar[j]) << (8 * j);
-                    hi |= (uint32_t)blend_px(mrow[rr][4 + j], al[4 + j], ar[4 + j]) << (8 * j);
+                    lo |= (uint32_t)blend_px(mrow[j], al[j], ar[j]) << (8 * j);
+                    hi |= (uint32_t)blend_px(mrow[4 + j], al[4 + j], ar[4 + j]) << (8 * j);
                 }
                 *reinterpret_cast<uint32_t*>(out + ro + x0) = lo;  // W % 4 == 0: n is 4 or 8
                 if (n == 8) *reinterpret_cast<uint32_t*>(out + ro + x0 + 4) = hi;
@@ -1231,7 +1275,14 @@ __global__ void __launch_bounds__(128) k_blend(Geometry g, PairTable pt, const u
         if (mask_out) {
 #pragma unroll
             for (int j = 0; j < 8; j++)
-                if (j < n) mask_out[ro + x0 + j] = mrow[rr][j];
+                if (j < n) mask_out[ro + x0 + j] = mrow[j];
+        }
+        if (FMT == FVV_YUV420) {
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const double p = __dadd_rn(mrow[2 * j], mrow[2 * j + 1]);
+                csum[j] = rr == 0 ? p : __dadd_rn(csum[j], p);   // (a + b) + (c + d)
+            }
         }
     }
     // chroma blend with the 2x2-mean mask (warp.py:83-88)
@@ -1244,9 +1295,7 @@ __global__ void __launch_bounds__(128) k_blend(Geometry g, PairTable pt, const u
 #pragma unroll
         for (int j = 0; j < 4; j++) {
             if (j >= nc) break;
-            const double sm = __dadd_rn(__dadd_rn(mrow[0][2 * j], mrow[0][2 * j + 1]),
-                                        __dadd_rn(mrow[1][2 * j], mrow[1][2 * j + 1]));
-            const double mc = __dmul_rn(sm, 0.25);  // /4 == *0.25 exactly
+            const double mc = __dmul_rn(csum[j], 0.25);  // /4 == *0.25 exactly
             const uchar4 q = wc[j];
             uo[j] = blend_px(mc, q.x, q.y);
             vo[j] = blend_px(mc, q.z, q.w);
@@ -1783,9 +1832,10 @@ cudaError_t run_interp_stage(const Geometry& g, const PairTable& pt, uint8_t* ws
     }
     if ((e = E()) != cudaSuccess) return e;
 
-    B(KC_ROWSCAN);
+    B(KC_SCAN);
     k_scan_carry<<<dim3((g.H + kCR - 1) / kCR, npairs), kCR, 0, st>>>(g, ws, P);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = E()) != cudaSuccess) return e;
+    B(KC_BLEND);
     {
         const dim3 grd(((g.W + 7) / 8 + 127) / 128, g.H / 2, npairs);
         if (g.fmt == FVV_YUV420) k_blend<FVV_YUV420><<<grd, 128, 0, st>>>(g, pt, ws, P, 0, true, mask_out);
