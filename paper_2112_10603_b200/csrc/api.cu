@@ -99,6 +99,7 @@ void make_geometry(const fvv_frame_desc* d, const fvv_interp_params* p, Geometry
     }
     g->eps = p->mask_epsilon;
     g->eps2 = 2.0 * p->mask_epsilon;
+    g->fastdiv = p->mask_epsilon >= 1e-30 && p->mask_epsilon <= 1e30;
     // exact fixed-point units (fvv_device.cuh)
     for (int s = 0; s < 3; s++) {
         int lb = 0;

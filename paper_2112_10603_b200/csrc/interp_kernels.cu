@@ -1039,7 +1039,8 @@ __device__ __forceinline__ double mask_of(double tsum, float occ_l, float occ_r,
     const float qr = __fadd_rn(0.5f, __fmul_rn(4.0f, occ_r));
     const double el = __dmul_rn(D, f2d_posnormal(ql));  // ql, qr >= 0.5
     const double er = __dmul_rn(D, f2d_posnormal(qr));
-    const double m = __ddiv_rn(__dadd_rn(er, g.eps), __dadd_rn(__dadd_rn(el, er), g.eps2));
+    const double num = __dadd_rn(er, g.eps), den = __dadd_rn(__dadd_rn(el, er), g.eps2);
+    const double m = g.fastdiv ? ddiv_fast(num, den) : __ddiv_rn(num, den);
     return m < 0.0 ? 0.0 : (m > 1.0 ? 1.0 : m);  // np.clip (m is never NaN: den >= 2 eps)
 }
 // blend (warp.py:66-67): to_uint8(m * a + (1 - m) * b)
@@ -1185,7 +1186,7 @@ __global__ void __launch_bounds__(kCR) k_scan_carry(Geometry g, const uint8_t* _
 }
 
 #ifndef FVV_MINB_BLEND
-#define FVV_MINB_BLEND 5
+#define FVV_MINB_BLEND 6
 #endif
 template <int FMT>
 __global__ void __launch_bounds__(128, FVV_MINB_BLEND) k_blend(Geometry g, PairTable pt, const uint8_t* __restrict__ ws,
@@ -1211,9 +1212,19 @@ __global__ void __launch_bounds__(128, FVV_MINB_BLEND) k_blend(Geometry g, PairT
         const int y = 2 * yp + rr;
         const size_t ro = (size_t)y * W;
         const uint16_t* srow = sd + ro;
-        int s[11];
+        int s[11];  // sd[clamp(x0 - 2 + j)]
+        if ((W & 7) == 0 && x0 >= 2 && x0 + 8 < W) {
+            // interior: sd[x0-2 .. x0-1] (4-byte aligned), sd[x0 .. x0+7] (16-byte), sd[x0+8]
+            const uint32_t a = *reinterpret_cast<const uint32_t*>(srow + x0 - 2);
+            const uint4 b = *reinterpret_cast<const uint4*>(srow + x0);
+            s[0] = a & 0xFFFF; s[1] = a >> 16;
+            s[2] = b.x & 0xFFFF; s[3] = b.x >> 16; s[4] = b.y & 0xFFFF; s[5] = b.y >> 16;
+            s[6] = b.z & 0xFFFF; s[7] = b.z >> 16; s[8] = b.w & 0xFFFF; s[9] = b.w >> 16;
+            s[10] = srow[x0 + 8];
+        } else {
 #pragma unroll
-        for (int j = 0; j < 11; j++) s[j] = srow[clampi(x0 - 2 + j, 0, W - 1)];
+            for (int j = 0; j < 11; j++) s[j] = srow[clampi(x0 - 2 + j, 0, W - 1)];
+        }
         float vl[8], vr[8];
         uint8_t al[8], ar[8];
         if (n == 8) {
