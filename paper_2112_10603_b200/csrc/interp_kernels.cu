@@ -1399,6 +1399,7 @@ __device__ __forceinline__ uint32_t sadw_group(const uint32_t* Rb, const uint32_
     using S = SadW<SIDE, CG>;
     constexpr int base = S::XPAD - S::R + G * CG;          // window sample of pair 0
     constexpr int ch0 = (base / 2) / 4, ch1 = ((base + S::NPJ) / 2) / 4;
+    constexpr int JF = (2 * S::NPJ) / 3;   // alu : fma balance of the inner loop
     uint32_t am[CG], cs[S::NPJ];
 #pragma unroll
     for (int c = 0; c < CG; c++) am[c] = 0;
@@ -1423,7 +1424,10 @@ __device__ __forceinline__ uint32_t sadw_group(const uint32_t* Rb, const uint32_
             const int sidx = base + j;                           // compile time
             const int wi = sidx / 2 - 4 * ch0;
             pv[j] = (sidx & 1) ? __byte_perm(wv[wi], wv[wi + 1], 0x5432) : wv[wi];
-            cs[j] += pv[j];
+            // pipe balance: the first JF column sums go to the fma pipe as lo + hi
+            // (IDP), the rest stay packed on the alu pipe (one IADD3 per two rows)
+            if (j < JF) cs[j] = __dp2a_lo(pv[j], 0x0101u, cs[j]);
+            else cs[j] += pv[j];
         }
 #pragma unroll
         for (int k = 0; k < 4; k++)
@@ -1435,8 +1439,13 @@ __device__ __forceinline__ uint32_t sadw_group(const uint32_t* Rb, const uint32_
     for (int c = 0; c < CG; c++) {
         const int cc = G * CG + c;
         if (cc < SIDE) {
-            const uint32_t ab = cs[c] + cs[c + 2] + cs[c + 4] + cs[c + 6];   // lanes <= 65280
-            const int sad = 2 * (int)am[c] - (int)((ab & 0xFFFFu) + (ab >> 16)) - sa;
+            int ab = 0;  // sum of the target samples of candidate c
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const int j = c + 2 * k;
+                ab += j < JF ? (int)cs[j] : (int)((cs[j] & 0xFFFFu) + (cs[j] >> 16));
+            }
+            const int sad = 2 * (int)am[c] - ab - sa;
             mine = min(mine, ((uint32_t)sad << 10) | (uint32_t)rki[cc]);
         }
     }
