@@ -16,6 +16,7 @@
 // arithmetic (no FMA), and the row-sequential replay of scipy's running sum
 // where the reference's rounding is order dependent.
 #include <algorithm>
+#include <type_traits>
 #include <cstdint>
 #include <cstdlib>
 #include <cuda_runtime.h>
@@ -904,7 +905,10 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
         }
     };
 
-    for (int yy = ys; yy <= ye; yy++) {
+    // one walker row; GEN = general row (band edges, image top), else every
+    // output of the row is in range and no edge rule applies (the band interior)
+    auto step = [&](int yy, auto gen) {
+        constexpr bool GEN = decltype(gen)::value;
         // ---- mid flows F(yy) (flow.py:122-129 at level 2, interp.py:131-132) ----
         const Tap2 ty = tap2(2 * yy - 1, 2, L1.h);  // L1.h >= 2
         if (ty.i0 != ua) {
@@ -950,7 +954,7 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
             }
             wl = bt601(cl[0], cl[1], cl[2]);
             wr = bt601(cr[0], cr[1], cr[2]);
-            if (own && yy >= y0 && yy < yo1) {
+            if (own && (!GEN || (yy >= y0 && yy < yo1))) {
                 uint8_t* o = plane<uint8_t>(ws, P, P.wrgb, pair) + ((size_t)yy * W + x) * 6;
 #pragma unroll
                 for (int c = 0; c < 3; c++) { o[c] = cl[c]; o[3 + c] = cr[c]; }
@@ -962,36 +966,36 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
         d0 = d1;
         d1 = d2;
         d2 = abs(wl - wr);
-        if (own && yy >= y0 && yy < yo1) {
+        if (own && (!GEN || (yy >= y0 && yy < yo1))) {
             o_wl[(size_t)yy * W + x] = (uint8_t)wl;
             o_wr[(size_t)yy * W + x] = (uint8_t)wr;
         }
         // ---- Sd(yy-1): column sum of d with nearest padding ----
         {
             const int t = yy - 1;
-            if (t >= y0 && t < yo1 && own) o_sd[(size_t)t * W + x] = (uint16_t)((t == 0 ? d1 : d0) + d1 + d2);
+            if (own && (!GEN || (t >= y0 && t < yo1))) o_sd[(size_t)t * W + x] = (uint16_t)(((GEN && t == 0) ? d1 : d0) + d1 + d2);
         }
         // ---- occ(yy-1) then O0/O(yy-2) ----
         {
             const int r = yy - 1;
-            if (r >= ys && (r == 0 || r - 1 >= ys)) {
+            if (!GEN || (r >= ys && (r == 0 || r - 1 >= ys))) {
 #pragma unroll
                 for (int d = 0; d < 2; d++) {
-                    const int gy = H < 2 ? 0 : (r == 0 ? 2 * (F2[d].y - F1[d].y) : F2[d].y - F0[d].y);
+                    const int gy = H < 2 ? 0 : ((GEN && r == 0) ? 2 * (F2[d].y - F1[d].y) : F2[d].y - F0[d].y);
                     const int v = -(gx1[d] + gy);
                     oc0[d] = oc1[d];
                     oc1[d] = oc2[d];
                     oc2[d] = v > 0 ? v : 0;
                 }
                 const int t2 = yy - 2;  // occ(t2 - 1) = oc0 (or occ(0) at the top), occ(t2) = oc1, occ(t2 + 1) = oc2
-                if (t2 >= y0 && t2 < yo1) {
-                    if (t2 == 0) emit_o(t2, oc1[0], oc1[1], oc1[0], oc1[1], oc2[0], oc2[1]);
+                if (!GEN || (t2 >= y0 && t2 < yo1)) {
+                    if (GEN && t2 == 0) emit_o(t2, oc1[0], oc1[1], oc1[0], oc1[1], oc2[0], oc2[1]);
                     else emit_o(t2, oc0[0], oc0[1], oc1[0], oc1[1], oc2[0], oc2[1]);
                 }
             }
         }
         // ---- chroma warps for chroma row (yy-1)/2 at odd yy (imageops.py:40-48) ----
-        if (FMT == FVV_YUV420 && (yy & 1) && yy - 1 >= y0 && yy - 1 < yo1 && yy - 1 >= ys) {
+        if (FMT == FVV_YUV420 && (yy & 1) && (!GEN || (yy - 1 >= y0 && yy - 1 < yo1 && yy - 1 >= ys))) {
             const int cw = g.cw, chh = g.ch, cb = mb + 3, kC = 2 * cb;
             int2 cv[2];
 #pragma unroll
@@ -1012,7 +1016,12 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
                 wc[2 * p + 1] = vr;
             }
         }
-    }
+    };
+    const int b0 = min(max(y0 + 2, 3), yo1), b1 = max(b0, yo1);  // interior rows [b0, b1)
+    int yy = ys;
+    for (; yy < b0; yy++) step(yy, std::true_type{});
+    for (; yy < b1; yy++) step(yy, std::false_type{});
+    for (; yy <= ye; yy++) step(yy, std::true_type{});
     // ---- bottom edge: occ(H-1) (one-sided gy), O0/O(H-2), O0/O(H-1), Sd(H-1) ----
     if (ye == H - 1) {
 #pragma unroll
