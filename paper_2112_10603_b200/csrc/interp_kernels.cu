@@ -325,10 +325,9 @@ __device__ __forceinline__ long long warp_fixed32(const Src& src, int h, int w, 
     const ITap tx = clamp_itap32((x << vb) + fxn, vb, w);
     const ITap ty = clamp_itap32((y << vb) + fyn, vb, h);
     const int V = 1 << vb;
-    const int top = (V - tx.f) * src(ty.i0, tx.i0) + tx.f * src(ty.i0, tx.i1);
-    const int bot = (V - tx.f) * src(ty.i1, tx.i0) + tx.f * src(ty.i1, tx.i1);
-    // (V - fy) * top + fy * bot == V * top + fy * (bot - top), exact in 64 bits
-    return ((long long)top << vb) + (long long)ty.f * (long long)(bot - top);
+    (void)V;
+    return (long long)bilerp_u(src(ty.i0, tx.i0), src(ty.i0, tx.i1), src(ty.i1, tx.i0), src(ty.i1, tx.i1),
+                               tx.f, ty.f, vb);
 }
 
 __device__ __forceinline__ int2 lerp_i2(int2 a, int2 b, int den, int f) {
@@ -770,10 +769,7 @@ __global__ void __launch_bounds__(256) k_warpq(Geometry g, PairTable pt, uint8_t
                 const uint8_t* p0 = yp + off;
                 a = p0[0]; b = p0[1]; c = p0[w]; e = p0[w + 1];
             }
-            const int top = (a << vb) + fx * (b - a);
-            const int bot = (c << vb) + fx * (e - c);
-            const long long v = ((long long)top << vb) + (long long)fy * (long long)(bot - top);
-            *op = (uint16_t)rne64(v, k);
+            *op = (uint16_t)rne64((long long)bilerp_u(a, b, c, e, fx, fy, vb), k);
             op += 4 * (size_t)w;
         }
         return;
