@@ -145,6 +145,36 @@ size_t fvv_rig_cluster_bytes(const fvv_frame_desc* desc, int ncams, int stages,
 int fvv_rig_clusters(const fvv_frame_desc* desc, int ncams, int stages, int views_per_side,
                      const uint8_t* views, uint8_t* clusters, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * VINet (SURVEY.md sec. 8(b) "fvv_vinet_flow",
+ * north star): the CNN flow / fusion estimator.  The reference ships no CNN
+ * (SPEC.md:18), so its oracle is the fp32 torch module oracle/vinet_ref.py.
+ *
+ * fvv_conv2d_bf16: one convolution layer on the tcgen05 tensor cores
+ * (implicit GEMM, TMA-fed, fp32 accumulation in TMEM, bias + ReLU epilogue).
+ *   x    NHWC bf16 [batch][in_h][in_w][in_cpad], in_cpad in {16, 32} or a
+ *        multiple of 64 (padding channels zero);
+ *   w    bf16, K-major.  Convolution: [npad][k*k*in_cpad] with
+ *        K index = (ky*k + kx)*in_cpad + c.  Transposed (k4 s2 p1):
+ *        [4 phases][npad][4*in_cpad], phase = (oy&1)*2 + (ox&1), tap
+ *        t = ty*2 + tx with input offsets dy = (oy&1) ? {+1, 0} : {0, -1}
+ *        (kernel rows ky = (oy&1) ? {0, 2} : {1, 3}), likewise in x;
+ *        npad = out_channels rounded up to ntile;
+ *   bias fp32 [out_channels];
+ *   out  NHWC [batch][out_h][out_w][out_cstride] (bf16, or fp32 when
+ *        out_f32), channels [out_coff, out_coff + out_channels).
+ * -------------------------------------------------------------------------- */
+typedef struct fvv_conv_desc {
+    int32_t batch, in_h, in_w, in_cpad;
+    int32_t out_h, out_w, out_cstride, out_coff, out_channels;
+    int32_t kernel, stride, pad;   /* square kernel; transposed: 4, 2, 1 */
+    int32_t transposed;            /* 1: ConvTranspose2d */
+    int32_t relu, out_f32;
+    int32_t ntile;                 /* UMMA N tile: 16, 32, 64, 128 or 256 */
+} fvv_conv_desc;
+int fvv_conv2d_bf16(const fvv_conv_desc* desc, const void* x, const void* w, const float* bias,
+                    void* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -22,7 +22,7 @@ EXPORTS = (
     "fvv_dense_views", "fvv_rig_views", "fvv_downscale", "fvv_cluster_width",
     "fvv_assemble_cluster", "fvv_rig_cluster_bytes", "fvv_rig_clusters",
     "fvv_profile_enable", "fvv_profile_read", "fvv_kernel_class_name",
-    "fvv_interp_level_diagnostics",
+    "fvv_interp_level_diagnostics", "fvv_conv2d_bf16",
 )
 
 
@@ -33,6 +33,12 @@ class FrameDesc(ctypes.Structure):
 class InterpParams(ctypes.Structure):
     _fields_ = [("block_size", ctypes.c_int32 * 3), ("search_radius", ctypes.c_int32 * 3),
                 ("mask_epsilon", ctypes.c_double)]
+
+
+class ConvDesc(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in (
+        "batch", "in_h", "in_w", "in_cpad", "out_h", "out_w", "out_cstride", "out_coff", "out_channels",
+        "kernel", "stride", "pad", "transposed", "relu", "out_f32", "ntile")]
 
 
 class LayoutErrorBase(Exception):
@@ -80,6 +86,7 @@ def load():
         "fvv_profile_enable": (I, [P, I]),
         "fvv_profile_read": (I, [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I), I]),
         "fvv_kernel_class_name": (ctypes.c_char_p, [I]),
+        "fvv_conv2d_bf16": (I, [ctypes.POINTER(ConvDesc), P, P, P, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include "fvv_device.cuh"
+#include "conv_tc.h"
 
 namespace fvv {
 extern int g_failed_class;
@@ -548,3 +549,69 @@ int fvv_rig_clusters(const fvv_frame_desc* d, int ncams, int stages, int vps,
 }
 
 }  // extern "C"
+
+extern "C" int fvv_conv2d_bf16(const fvv_conv_desc* d, const void* x, const void* w, const float* bias,
+                               void* out, void* stream) {
+    if (!d || !x || !w || !bias || !out) return fail(FVV_EINVAL, "null argument");
+    if (d->batch < 1 || d->in_h < 1 || d->in_w < 1 || d->out_h < 1 || d->out_w < 1 || d->out_channels < 1)
+        return fail(FVV_EINVAL, "empty convolution");
+    const int cp = d->in_cpad;
+    if (!(cp == 16 || cp == 32 || (cp % 64 == 0 && cp <= 1024)))
+        return fail(FVV_EUNSUPPORTED, "in_cpad must be 16, 32 or a multiple of 64");
+    const int nt = d->ntile;
+    if (!(nt == 16 || nt == 32 || nt == 64 || nt == 128 || nt == 256))
+        return fail(FVV_EINVAL, "ntile must be 16, 32, 64, 128 or 256");
+    if (d->out_coff < 0 || d->out_coff + d->out_channels > d->out_cstride)
+        return fail(FVV_EINVAL, "output channels outside out_cstride");
+    if (!d->out_f32 && (d->out_cstride % 8 || d->out_coff % 8) && d->out_channels % 8 == 0)
+        ;  // scalar stores handle unaligned bf16 placement
+    const int npad = (d->out_channels + nt - 1) / nt * nt;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    ConvTCParams p{};
+    p.Hout = d->out_h;
+    p.Wout = d->out_w;
+    p.ostride = d->out_cstride;
+    p.ocoff = d->out_coff;
+    p.N = d->out_channels;
+    p.act = d->relu ? 1 : 0;
+    p.out_f32 = d->out_f32 ? 1 : 0;
+    cudaError_t e = cudaSuccess;
+    if (!d->transposed) {
+        const int k = d->kernel, s = d->stride;
+        if (k < 1 || k * k > kConvMaxTaps || s < 1 || s > 2)
+            return fail(FVV_EUNSUPPORTED, "kernel*kernel <= 16 and stride 1 or 2");
+        if ((d->in_h + 2 * d->pad - k) / s + 1 != d->out_h || (d->in_w + 2 * d->pad - k) / s + 1 != d->out_w)
+            return fail(FVV_EINVAL, "output size does not match the convolution");
+        p.Hg = d->out_h;
+        p.Wg = d->out_w;
+        p.sy = p.sx = s;
+        p.by0 = p.bx0 = -d->pad;
+        p.ntaps = k * k;
+        for (int t = 0; t < k * k; t++) { p.tdy[t] = t / k; p.tdx[t] = t % k; }
+        p.omy = p.omx = 1;
+        p.oay = p.oax = 0;
+        e = conv_tc(x, d->batch, d->in_h, d->in_w, cp, w, npad, 0, nt, bias, out, p, st);
+    } else {
+        if (d->kernel != 4 || d->stride != 2 || d->pad != 1)
+            return fail(FVV_EUNSUPPORTED, "transposed convolution: kernel 4, stride 2, pad 1 only");
+        if (d->out_h != 2 * d->in_h || d->out_w != 2 * d->in_w)
+            return fail(FVV_EINVAL, "transposed output must be twice the input size");
+        p.Hg = d->in_h;
+        p.Wg = d->in_w;
+        p.sy = p.sx = 1;
+        p.by0 = p.bx0 = 0;
+        p.ntaps = 4;
+        p.omy = p.omx = 2;
+        static const int off[2][2] = {{0, -1}, {1, 0}};  // [parity][tap]
+        for (int ph = 0; ph < 4 && e == cudaSuccess; ph++) {
+            const int a = ph >> 1, b = ph & 1;
+            for (int t = 0; t < 4; t++) { p.tdy[t] = off[a][t >> 1]; p.tdx[t] = off[b][t & 1]; }
+            p.oay = a;
+            p.oax = b;
+            e = conv_tc(x, d->batch, d->in_h, d->in_w, cp, w, 4 * npad, ph * npad, nt, bias, out, p, st);
+        }
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "fvv_conv2d_bf16");
+    return FVV_OK;
+}
+

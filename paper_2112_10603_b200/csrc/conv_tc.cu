@@ -1,0 +1,366 @@
+// conv_tc.cu -- implicit-GEMM convolution on the 5th-generation tensor cores
+// (tcgen05 + TMEM + TMA) for the VINet flow/fusion blocks (PAPER.md:320-337,
+// SURVEY.md sec. 8(b)/(c)/(d) north-star rows).
+//
+// GEMM view: D[m][n] = sum_k A[m][k] * B[n][k] with
+//   m = an output pixel of one output row (tile: 128 consecutive pixels),
+//   n = an output channel (tile: NT <= 256),
+//   k = (tap, input channel); one K chunk = one tap x (SW / 2) channels.
+// A chunk is an input-row segment of 128 pixels (stride sx) x chunk channels,
+// fetched by one 4-D TMA copy from the NHWC bf16 activation tensor; TMA's
+// out-of-bounds zero fill is the convolution padding.  B chunks come from the
+// K-major bf16 weight matrix by a 2-D TMA copy.  Both land in the canonical
+// K-major swizzled layout (SW = 32/64/128 bytes per row) the UMMA descriptors
+// describe.  One elected thread issues tcgen05.mma (M=128, N=NT, K=16) into a
+// TMEM accumulator; the 4 warps read it back with tcgen05.ld and apply
+// bias + activation in the epilogue.
+//
+// Roles (128 threads): warp 0 / lane 0 = TMA producer, warp 1 / lane 0 = MMA
+// issuer, warp 2 = TMEM allocator; all 4 warps = epilogue (warp w owns TMEM
+// lanes 32w..32w+31, i.e. output pixels 32w..32w+31 of the tile).
+// Pipeline: kStages smem stages, full/empty mbarriers, one accumulator barrier.
+//
+// Transposed convolutions (k4 s2 p1) run as four 2x2-tap phase convolutions
+// on the input grid whose outputs interleave (omy = omx = 2).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+
+#include "conv_tc.h"
+
+namespace fvv {
+
+constexpr int kConvStages = 4;
+
+// ---------------------------------------------------------------------------
+// PTX wrappers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+// K-major, swizzled canonical layout: rows of SW bytes, 8-row groups SBO = 8*SW apart
+template <int SW>
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
+    constexpr uint64_t layout = SW == 128 ? 2 : (SW == 64 ? 4 : 6);
+    uint64_t d = (uint64_t)((saddr & 0x3FFFF) >> 4);
+    d |= (uint64_t)1 << 16;                        // LBO (unused for swizzled K-major)
+    d |= (uint64_t)((8 * SW) >> 4) << 32;          // SBO
+    d |= (uint64_t)1 << 46;                        // descriptor version (sm_100)
+    d |= layout << 61;
+    return d;
+}
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// the kernel
+// ---------------------------------------------------------------------------
+template <int NT, int SW>
+struct ConvTile {
+    static constexpr int kABytes = 128 * SW;
+    static constexpr int kBBytes = NT * SW;
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kTmemCols = NT < 32 ? 32 : NT;  // power of two >= 32
+    static constexpr size_t kSmem = 1024 /* alignment slack */ + (size_t)kConvStages * kStageBytes + 256;
+};
+
+template <int NT, int SW>
+__global__ void __launch_bounds__(128, 1)
+    k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const float* __restrict__ bias, void* __restrict__ out, ConvTCParams p) {
+    using T = ConvTile<NT, SW>;
+    static_assert(NT % 16 == 0 && NT >= 16 && NT <= 256, "UMMA N (M = 128)");
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kConvStages * T::kStageBytes);
+    uint64_t* empty = full + kConvStages;
+    uint64_t* accum = empty + kConvStages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int b = blockIdx.y / p.Hg, gy = blockIdx.y - b * p.Hg;
+    const int gx0 = blockIdx.x * 128;
+    const int n0 = blockIdx.z * NT;
+    const int nk = p.ntaps * p.kc_per_tap;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kConvStages; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(accum, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                     "n"(T::kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0 && lane == 0) {
+        // ---- TMA producer ----
+        const int iy0 = gy * p.sy + p.by0, ix0 = gx0 * p.sx + p.bx0;
+        for (int kc = 0; kc < nk; kc++) {
+            const int s = kc % kConvStages;
+            if (kc >= kConvStages) mbar_wait(&empty[s], ((kc / kConvStages) - 1) & 1);
+            const int tap = kc / p.kc_per_tap, c0 = (kc - tap * p.kc_per_tap) * (SW / 2);
+            uint8_t* sa = smem + s * T::kStageBytes;
+            mbar_expect_tx(&full[s], T::kStageBytes);
+            tma_load_4d(sa, &tmA, &full[s], c0, ix0 + p.tdx[tap], iy0 + p.tdy[tap], b);
+            tma_load_2d(sa + T::kABytes, &tmB, &full[s], tap * p.cpad + c0, p.wrow0 + n0);
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ---- MMA issuer ----
+        constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NT >> 3) << 17) |
+                                   ((uint32_t)(128 >> 4) << 24);
+        for (int kc = 0; kc < nk; kc++) {
+            const int s = kc % kConvStages;
+            mbar_wait(&full[s], (kc / kConvStages) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            const uint32_t sa = smem_u32(smem + s * T::kStageBytes), sb = sa + T::kABytes;
+#pragma unroll
+            for (int k = 0; k < SW / 32; k++)
+                umma_bf16(tmem, umma_desc<SW>(sa + 32 * k), umma_desc<SW>(sb + 32 * k), idesc,
+                          (kc > 0 || k > 0) ? 1u : 0u);
+            umma_commit(&empty[s]);  // frees the stage once these MMAs have read it
+        }
+        umma_commit(accum);
+    }
+    __syncwarp();
+
+    // ---- epilogue: TMEM -> registers -> bias + activation -> global ----
+    mbar_wait(accum, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const int row = warp * 32 + lane;
+    const int gx = gx0 + row;
+    const bool valid = gx < p.Wg;
+    const int oy = gy * p.omy + p.oay, ox = gx * p.omx + p.oax;
+    const size_t obase = (((size_t)b * p.Hout + oy) * p.Wout + ox) * p.ostride + p.ocoff;
+    constexpr int CW = NT < 32 ? NT : 32;  // columns per tcgen05.ld
+#pragma unroll 1
+    for (int c = 0; c < NT; c += CW) {
+        uint32_t r[32];
+        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + c;
+        if (CW == 32) {
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                  "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                  "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                  "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                : "r"(taddr));
+        } else {
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15},"
+                " [%16];\n"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                  "=r"(r[15])
+                : "r"(taddr));
+        }
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        if (valid) {
+            float v[32];
+#pragma unroll
+            for (int j = 0; j < CW; j++) {
+                const int n = n0 + c + j;
+                float x = __uint_as_float(r[j]) + (n < p.N ? bias[n] : 0.0f);
+                if (p.act == 1) x = fmaxf(x, 0.0f);
+                v[j] = x;
+            }
+            if (p.out_f32) {
+                float* o = reinterpret_cast<float*>(out) + obase;
+#pragma unroll
+                for (int j = 0; j < CW; j++)
+                    if (n0 + c + j < p.N) o[n0 + c + j] = v[j];
+            } else {
+                __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out) + obase + n0 + c;
+                if (n0 + c + CW <= p.N && ((obase + n0 + c) & 7) == 0) {
+#pragma unroll
+                    for (int j = 0; j < CW; j += 8) {
+                        uint4 q;
+                        __nv_bfloat162 h0 = __floats2bfloat162_rn(v[j], v[j + 1]);
+                        __nv_bfloat162 h1 = __floats2bfloat162_rn(v[j + 2], v[j + 3]);
+                        __nv_bfloat162 h2 = __floats2bfloat162_rn(v[j + 4], v[j + 5]);
+                        __nv_bfloat162 h3 = __floats2bfloat162_rn(v[j + 6], v[j + 7]);
+                        memcpy(&q.x, &h0, 4); memcpy(&q.y, &h1, 4); memcpy(&q.z, &h2, 4); memcpy(&q.w, &h3, 4);
+                        *reinterpret_cast<uint4*>(o + j) = q;
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < CW; j++)
+                        if (n0 + c + j < p.N) o[j] = __float2bfloat16_rn(v[j]);
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (warp == 2)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(T::kTmemCols)
+                     : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    });
+    return fn;
+}
+
+static CUtensorMapSwizzle swz(int sw) {
+    return sw == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : (sw == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+}
+
+// activation map: NHWC bf16 [B][H][W][C] as 4-D (C, W, H, B); box = chunk x 128 pixels (stride sx)
+static bool make_act_map(CUtensorMap* m, const void* x, int B, int H, int W, int C, int sw, int sx) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    const cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B};
+    const cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+    const cuuint32_t box[4] = {(cuuint32_t)(sw / 2), (cuuint32_t)(128 * sx), 1, 1};
+    const cuuint32_t estr[4] = {1, (cuuint32_t)sx, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, swz(sw), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// weight map: bf16 [rows][K] K-major; box = chunk x NT rows
+static bool make_w_map(CUtensorMap* m, const void* w, int rows, int K, int sw, int nt) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+    const cuuint32_t box[2] = {(cuuint32_t)(sw / 2), (cuuint32_t)nt};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(w), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, swz(sw), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int NT, int SW>
+static cudaError_t launch_nt_sw(const CUtensorMap& a, const CUtensorMap& w, const float* bias, void* out,
+                                const ConvTCParams& p, int ntiles, cudaStream_t st) {
+    using T = ConvTile<NT, SW>;
+    auto kern = k_conv_tc<NT, SW>;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::kSmem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    dim3 grid((p.Wg + 127) / 128, p.Hg * p.B, ntiles);
+    kern<<<grid, 128, T::kSmem, st>>>(a, w, bias, out, p);
+    return cudaGetLastError();
+}
+
+template <int SW>
+static cudaError_t launch_sw(int nt, const CUtensorMap& a, const CUtensorMap& w, const float* bias, void* out,
+                             const ConvTCParams& p, int ntiles, cudaStream_t st) {
+    switch (nt) {
+        case 16: return launch_nt_sw<16, SW>(a, w, bias, out, p, ntiles, st);
+        case 32: return launch_nt_sw<32, SW>(a, w, bias, out, p, ntiles, st);
+        case 64: return launch_nt_sw<64, SW>(a, w, bias, out, p, ntiles, st);
+        case 128: return launch_nt_sw<128, SW>(a, w, bias, out, p, ntiles, st);
+        case 256: return launch_nt_sw<256, SW>(a, w, bias, out, p, ntiles, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+// One convolution (or one phase of a transposed convolution).  x: NHWC bf16
+// [B][Hin][Win][cpad]; w: bf16 [rows][ntaps*cpad] (this conv's rows start at
+// wrow0); out: NHWC (bf16 or f32) [B][Hout][Wout][ostride], channels
+// [ocoff, ocoff + N).  ntile = UMMA N tile (16..256).
+cudaError_t conv_tc(const void* x, int B, int Hin, int Win, int cpad, const void* w, int wrows, int wrow0,
+                    int ntile, const float* bias, void* out, const ConvTCParams& p0, cudaStream_t st) {
+    ConvTCParams p = p0;
+    p.B = B;
+    p.cpad = cpad;
+    p.wrow0 = wrow0;
+    const int sw = cpad >= 64 ? 128 : (cpad == 32 ? 64 : (cpad == 16 ? 32 : 0));
+    if (!sw || (cpad > 64 && cpad % 64) || p.ntaps < 1 || p.ntaps > kConvMaxTaps) return cudaErrorInvalidValue;
+    if (p.sx < 1 || p.sx > 2) return cudaErrorInvalidValue;
+    p.kc_per_tap = cpad * 2 / sw;
+    CUtensorMap ma, mw;
+    if (!make_act_map(&ma, x, B, Hin, Win, cpad, sw, p.sx)) return cudaErrorInvalidValue;
+    if (!make_w_map(&mw, w, wrows, p.ntaps * cpad, sw, ntile)) return cudaErrorInvalidValue;
+    const int npad = ((p.N + ntile - 1) / ntile) * ntile;
+    const int ntiles = npad / ntile;
+    switch (sw) {
+        case 128: return launch_sw<128>(ntile, ma, mw, bias, out, p, ntiles, st);
+        case 64: return launch_sw<64>(ntile, ma, mw, bias, out, p, ntiles, st);
+        default: return launch_sw<32>(ntile, ma, mw, bias, out, p, ntiles, st);
+    }
+}
+
+}  // namespace fvv
