@@ -175,6 +175,27 @@ typedef struct fvv_conv_desc {
 int fvv_conv2d_bf16(const fvv_conv_desc* desc, const void* x, const void* w, const float* bias,
                     void* out, void* stream);
 
+/* VINet forward, batched over camera pairs.  Weights: 3 blocks x 10 layers
+ * (c0, c1, r1..r6, u0, u1; paper_2112_10603_b200/vinet_params.py), each packed
+ * as documented for fvv_conv2d_bf16 with ntile 128 (c0, u0), 256 (c1, r*) and
+ * 16 (u1) and in_cpad 16 / 32 for block 0 / blocks 1-2 c0.
+ * flows: [npairs][5][H][W] fp32 = F_m->l (x, y), F_m->r (x, y), mask logit.
+ * The workspace holds fvv_vinet_workspace_size(desc, max_pairs) bytes; larger
+ * batches run in chunks of max_pairs. */
+typedef struct fvv_vinet_weights {
+    const void* w[3][10];
+    const float* b[3][10];
+} fvv_vinet_weights;
+size_t fvv_vinet_workspace_size(const fvv_frame_desc* desc, int max_pairs);
+int fvv_vinet_flow(const fvv_frame_desc* desc, const fvv_vinet_weights* weights, const uint8_t* const* left,
+                   const uint8_t* const* right, int npairs, float* flows, void* workspace,
+                   size_t workspace_bytes, void* stream);
+/* Direct-t synthesis: for every pair the nviews views at t = j/(nviews+1),
+ * j = 1..nviews, from one flow field in one pass (warp both frames, sigmoid-
+ * mask blend, rint/clip).  views: [npairs][nviews][frame_bytes]. */
+int fvv_vinet_synth(const fvv_frame_desc* desc, const uint8_t* const* left, const uint8_t* const* right,
+                    const float* flows, int npairs, int nviews, uint8_t* views, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

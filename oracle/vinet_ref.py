@@ -1,0 +1,184 @@
+"""fp32 torch reference of VINet -- the oracle of the north-star CNN path.
+
+TEST INFRASTRUCTURE ONLY (tests/, __graft_entry__.smoke(), bench.py's CPU
+legs).  The reference package has no CNN; SURVEY.md sec. 8(c)
+prescribes this oracle: a torch fp32 module written from PAPER.md:100-126,
+320-337 with seeded random weights (paper_2112_10603_b200/vinet_params.py).
+Every operation is spelled out (no grid_sample / interpolate) so the CUDA
+engine restates the same arithmetic:
+
+  pool2(x)     2x2 mean ((a + b) + (c + d)) * 0.25            image pyramid
+  up2(x)       2x bilinear, align_corners=False: grid ((i + 0.5) / 2 - 0.5),
+               clamped, x-lerp then y-lerp                     flow / mask
+  warp(I, F)   backward bilinear at (x + fx, y + fy), clamped to the plane,
+               i0 = min(floor(s), n - 2), out = (1-ay)((1-ax)a + ax b) + ay((1-ax)c + ax d)
+  canvas       the network runs on the image edge-padded (replicate, bottom/right) to
+               multiples of 64 (three 2x pools + four stride-2 layers); the flows
+               are cropped back to H x W before synthesis
+  synth        m = sigmoid(M); for view t: F_l,t = 2t F_l, F_r,t = 2(1-t) F_r,
+               w_t = (1-t) m / ((1-t) m + t (1-m)); out = w_t warp(I_l) + (1-w_t) warp(I_r)
+               per plane (chroma: flow = 2x2 mean * 0.5, mask = 2x2 mean), rint, clip.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.nn.functional as Fn
+
+GRAY8, YUV420, RGB8 = 0, 1, 2
+
+
+def planes_of(frame: np.ndarray, w: int, h: int, fmt: int):
+    """Packed frame bytes -> list of uint8 planes (H, W[, 3])."""
+    if fmt == GRAY8:
+        return [frame[:w * h].reshape(h, w)]
+    if fmt == RGB8:
+        return [frame[:w * h * 3].reshape(h, w, 3)]
+    cw, ch = (w + 1) // 2, (h + 1) // 2
+    y = frame[:w * h].reshape(h, w)
+    u = frame[w * h:w * h + cw * ch].reshape(ch, cw)
+    v = frame[w * h + cw * ch:w * h + 2 * cw * ch].reshape(ch, cw)
+    return [y, u, v]
+
+
+def net_image(frame: np.ndarray, w: int, h: int, fmt: int) -> torch.Tensor:
+    """(3, H, W) float32 in [0, 1] (vinet_params docstring)."""
+    p = planes_of(frame, w, h, fmt)
+    if fmt == RGB8:
+        x = torch.from_numpy(p[0].astype(np.float32)).permute(2, 0, 1)
+    elif fmt == YUV420:
+        u = np.repeat(np.repeat(p[1], 2, 0), 2, 1)[:h, :w]
+        v = np.repeat(np.repeat(p[2], 2, 0), 2, 1)[:h, :w]
+        x = torch.from_numpy(np.stack([p[0], u, v]).astype(np.float32))
+    else:
+        y = p[0].astype(np.float32)
+        x = torch.from_numpy(np.stack([y, np.full_like(y, 127.5), np.full_like(y, 127.5)]))
+    return x * (1.0 / 255.0)
+
+
+def pool2(x: torch.Tensor) -> torch.Tensor:
+    a, b = x[..., 0::2, 0::2], x[..., 0::2, 1::2]
+    c, d = x[..., 1::2, 0::2], x[..., 1::2, 1::2]
+    return ((a + b) + (c + d)) * 0.25
+
+
+def _taps(n_out: int, n_in: int):
+    s = (torch.arange(n_out, dtype=torch.float32) + 0.5) * 0.5 - 0.5
+    s = s.clamp(0.0, float(n_in - 1))
+    i0 = torch.clamp(torch.floor(s), max=max(n_in - 2, 0)).long()
+    i1 = torch.clamp(i0 + 1, max=n_in - 1)
+    return i0, i1, s - i0.float()
+
+
+def up2(x: torch.Tensor) -> torch.Tensor:
+    """(..., h, w) -> (..., 2h, 2w) bilinear, align_corners=False."""
+    h, w = x.shape[-2:]
+    y0, y1, fy = _taps(2 * h, h)
+    x0, x1, fx = _taps(2 * w, w)
+    top = x[..., y0, :]
+    bot = x[..., y1, :]
+    rows = (1.0 - fy)[:, None] * top + fy[:, None] * bot
+    left, right = rows[..., x0], rows[..., x1]
+    return (1.0 - fx) * left + fx * right
+
+
+def warp(img: torch.Tensor, fx: torch.Tensor, fy: torch.Tensor) -> torch.Tensor:
+    """img (..., H, W), flow (H, W): backward bilinear with clamped coordinates."""
+    H, W = img.shape[-2:]
+    ys = torch.arange(H, dtype=torch.float32)[:, None]
+    xs = torch.arange(W, dtype=torch.float32)[None, :]
+    sx = (xs + fx).clamp(0.0, float(W - 1))
+    sy = (ys + fy).clamp(0.0, float(H - 1))
+    x0 = torch.clamp(torch.floor(sx), max=W - 2).long()
+    y0 = torch.clamp(torch.floor(sy), max=H - 2).long()
+    ax, ay = sx - x0.float(), sy - y0.float()
+    flat = img.reshape(*img.shape[:-2], H * W)
+
+    def at(yy, xx):
+        return flat[..., (yy * W + xx).reshape(-1)].reshape(*img.shape[:-2], H, W)
+
+    a, b = at(y0, x0), at(y0, x0 + 1)
+    c, d = at(y0 + 1, x0), at(y0 + 1, x0 + 1)
+    top = (1.0 - ax) * a + ax * b
+    bot = (1.0 - ax) * c + ax * d
+    return (1.0 - ay) * top + ay * bot
+
+
+def block_forward(x: torch.Tensor, layers) -> torch.Tensor:
+    """One VIBlock on (1, cin, h, w) -> (1, 5, h, w)."""
+    (w0, b0), (w1, b1) = layers[0], layers[1]
+    y = torch.relu(Fn.conv2d(x, w0, b0, stride=2, padding=1))
+    y = torch.relu(Fn.conv2d(y, w1, b1, stride=2, padding=1))
+    for k in range(2, 8):
+        w, b = layers[k]
+        y = torch.relu(Fn.conv2d(y, w, b, stride=1, padding=1))
+    w, b = layers[8]
+    y = torch.relu(Fn.conv_transpose2d(y, w, b, stride=2, padding=1))
+    w, b = layers[9]
+    return Fn.conv_transpose2d(y, w, b, stride=2, padding=1)
+
+
+def canvas(w: int, h: int):
+    return (w + 63) // 64 * 64, (h + 63) // 64 * 64
+
+
+def pad_canvas(x: torch.Tensor, w: int, h: int) -> torch.Tensor:
+    wp, hp = canvas(w, h)
+    ys = torch.clamp(torch.arange(hp), max=h - 1)
+    xs = torch.clamp(torch.arange(wp), max=w - 1)
+    return x[..., ys, :][..., xs]
+
+
+@torch.no_grad()
+def flows(left: np.ndarray, right: np.ndarray, w: int, h: int, fmt: int, params):
+    """VINet on one pair -> (5, H, W) float32: F_l (2), F_r (2), mask logit (1) at full resolution."""
+    il = [pad_canvas(net_image(left, w, h, fmt), w, h)]
+    ir = [pad_canvas(net_image(right, w, h, fmt), w, h)]
+    for _ in range(2):
+        il.insert(0, pool2(il[0]))
+        ir.insert(0, pool2(ir[0]))
+    state = None
+    for i in range(3):
+        a, b = il[i], ir[i]
+        if state is None:
+            x = torch.cat([a, b], 0)
+        else:
+            st = up2(state)
+            st[0:4] = st[0:4] * 2.0
+            wl = warp(a, st[0], st[1])
+            wr = warp(b, st[2], st[3])
+            x = torch.cat([a, b, wl, wr, st], 0)
+            state = st
+        res = block_forward(x[None], params[i])[0]
+        state = res if state is None else state + res
+    return state[:, :h, :w].contiguous()
+
+
+def _synth_plane(pl: torch.Tensor, pr: torch.Tensor, fl, fr, wgt, t: float) -> torch.Tensor:
+    a = warp(pl, fl[0] * (2.0 * t), fl[1] * (2.0 * t))
+    b = warp(pr, fr[0] * (2.0 * (1.0 - t)), fr[1] * (2.0 * (1.0 - t)))
+    v = wgt * a + (1.0 - wgt) * b
+    return torch.clamp(torch.round(v), 0.0, 255.0)  # torch.round: half to even
+
+
+@torch.no_grad()
+def synth(left: np.ndarray, right: np.ndarray, w: int, h: int, fmt: int, state: torch.Tensor, t: float):
+    """Direct-t view at t in (0, 1) from the VINet state -> packed uint8 frame."""
+    m = torch.sigmoid(state[4])
+    wt = (1.0 - t) * m / ((1.0 - t) * m + t * (1.0 - m))
+    pls, prs = planes_of(left, w, h, fmt), planes_of(right, w, h, fmt)
+    out = []
+    if fmt == RGB8:
+        pl = torch.from_numpy(pls[0].astype(np.float32)).permute(2, 0, 1)
+        pr = torch.from_numpy(prs[0].astype(np.float32)).permute(2, 0, 1)
+        out.append(_synth_plane(pl, pr, state[0:2], state[2:4], wt, t).permute(1, 2, 0))
+    else:
+        out.append(_synth_plane(torch.from_numpy(pls[0].astype(np.float32)),
+                                torch.from_numpy(prs[0].astype(np.float32)), state[0:2], state[2:4], wt, t))
+        if fmt == YUV420:
+            fc = pool2(state[0:4]) * 0.5
+            wc = pool2(wt)
+            for k in (1, 2):
+                out.append(_synth_plane(torch.from_numpy(pls[k].astype(np.float32)),
+                                        torch.from_numpy(prs[k].astype(np.float32)), fc[0:2], fc[2:4], wc, t))
+    return np.concatenate([o.numpy().astype(np.uint8).reshape(-1) for o in out])

@@ -14,7 +14,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libfvv_b200.so"
-SOURCES = ["interp_kernels.cu", "tile_kernels.cu", "conv_tc.cu", "api.cu"]
+SOURCES = ["interp_kernels.cu", "tile_kernels.cu", "conv_tc.cu", "vinet_kernels.cu", "api.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
@@ -34,7 +34,7 @@ def stale() -> bool:
     if not LIB.exists():
         return True
     t = LIB.stat().st_mtime
-    deps = [CSRC / s for s in SOURCES] + list(CSRC.glob("*.cuh")) + [PKG.parent / "include" / "fvv_b200.h"]
+    deps = [CSRC / s for s in SOURCES] + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + [PKG.parent / "include" / "fvv_b200.h"]
     return any(d.stat().st_mtime > t for d in deps if d.exists())
 
 

@@ -11,6 +11,7 @@
 
 #include "fvv_device.cuh"
 #include "conv_tc.h"
+#include "vinet.h"
 
 namespace fvv {
 extern int g_failed_class;
@@ -612,6 +613,80 @@ extern "C" int fvv_conv2d_bf16(const fvv_conv_desc* d, const void* x, const void
         }
     }
     if (e != cudaSuccess) return cuda_fail(e, "fvv_conv2d_bf16");
+    return FVV_OK;
+}
+
+static int vin_check_desc(const fvv_frame_desc* d) {
+    if (!d) return fail(FVV_EINVAL, "null frame descriptor");
+    if (d->width < 64 || d->height < 64 || d->width % 4 || d->height % 4)
+        return fail(FVV_EINVAL, "VINet frames need width, height >= 64 and multiples of 4");
+    if (d->format != FVV_GRAY8 && d->format != FVV_YUV420 && d->format != FVV_RGB8)
+        return fail(FVV_EINVAL, "unknown pixel format");
+    return FVV_OK;
+}
+
+extern "C" size_t fvv_vinet_workspace_size(const fvv_frame_desc* d, int max_pairs) {
+    if (vin_check_desc(d) || max_pairs < 1) return 0;
+    return vin_layout(d->width, d->height, std::min(max_pairs, kVinMaxPairs)).bytes;
+}
+
+extern "C" int fvv_vinet_flow(const fvv_frame_desc* d, const fvv_vinet_weights* wts, const uint8_t* const* left,
+                              const uint8_t* const* right, int npairs, float* flows, void* ws, size_t ws_bytes,
+                              void* stream) {
+    int rc;
+    if ((rc = vin_check_desc(d))) return rc;
+    if (!wts || !left || !right || !flows || !ws) return fail(FVV_EINVAL, "null argument");
+    if (npairs < 1) return fail(FVV_EINVAL, "npairs must be >= 1");
+    int B = std::min(npairs, kVinMaxPairs);
+    while (B > 1 && vin_layout(d->width, d->height, B).bytes > ws_bytes) B--;
+    const VinLayout L = vin_layout(d->width, d->height, B);
+    if (L.bytes > ws_bytes) return fail(FVV_EINVAL, "workspace too small for one pair");
+    VinWeights vw;
+    for (int i = 0; i < 3; i++)
+        for (int k = 0; k < 10; k++) {
+            if (!wts->w[i][k] || !wts->b[i][k]) return fail(FVV_EINVAL, "null layer weights");
+            vw.w[i][k] = wts->w[i][k];
+            vw.b[i][k] = wts->b[i][k];
+        }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t plane = (size_t)5 * d->width * d->height;
+    for (int p0 = 0; p0 < npairs; p0 += B) {
+        const int n = std::min(B, npairs - p0);
+        VinLayout Ln = vin_layout(d->width, d->height, n);
+        VinPairs pp{};
+        for (int i = 0; i < n; i++) {
+            if (!left[p0 + i] || !right[p0 + i]) return fail(FVV_EINVAL, "null frame pointer");
+            pp.left[i] = left[p0 + i];
+            pp.right[i] = right[p0 + i];
+        }
+        cudaError_t e = vin_flows(Ln, vw, pp, d->format, static_cast<uint8_t*>(ws), flows + plane * p0, nullptr, st);
+        if (e != cudaSuccess) return cuda_fail(e, "fvv_vinet_flow");
+    }
+    return FVV_OK;
+}
+
+extern "C" int fvv_vinet_synth(const fvv_frame_desc* d, const uint8_t* const* left, const uint8_t* const* right,
+                               const float* flows, int npairs, int nviews, uint8_t* views, void* stream) {
+    int rc;
+    if ((rc = vin_check_desc(d))) return rc;
+    if (!left || !right || !flows || !views) return fail(FVV_EINVAL, "null argument");
+    if (npairs < 1 || nviews < 1) return fail(FVV_EINVAL, "npairs and nviews must be >= 1");
+    fvv_frame_desc dd = *d;
+    const size_t fb = fvv_frame_bytes(&dd);
+    const size_t plane = (size_t)5 * d->width * d->height;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    for (int p0 = 0; p0 < npairs; p0 += kVinMaxPairs) {
+        const int n = std::min(kVinMaxPairs, npairs - p0);
+        VinPairs pp{};
+        for (int i = 0; i < n; i++) {
+            if (!left[p0 + i] || !right[p0 + i]) return fail(FVV_EINVAL, "null frame pointer");
+            pp.left[i] = left[p0 + i];
+            pp.right[i] = right[p0 + i];
+        }
+        cudaError_t e = vin_synth(pp, n, flows + plane * p0, d->format, d->width, d->height, nviews,
+                                  views + (size_t)p0 * nviews * fb, fb, st);
+        if (e != cudaSuccess) return cuda_fail(e, "fvv_vinet_synth");
+    }
     return FVV_OK;
 }
 

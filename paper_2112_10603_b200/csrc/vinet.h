@@ -1,0 +1,37 @@
+// vinet.h -- host interface of the VINet engine (vinet_kernels.cu)
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "fvv_device.cuh"
+
+namespace fvv {
+
+constexpr int kVinMaxPairs = 64;
+
+struct VinPairs {
+    const uint8_t* left[kVinMaxPairs];
+    const uint8_t* right[kVinMaxPairs];
+};
+
+struct VinWeights {                 // packed layer weights (convtc.py layouts), 3 blocks x 10 layers
+    const void* w[3][10];
+    const float* b[3][10];
+};
+
+struct VinLayout {
+    int W, H, Wp, Hp, B;            // frame, 64-aligned canvas, pairs per chunk
+    size_t img[3], state[3];        // per level: images (B, 2, 3, h, w) f32, state (B, 5, h, w) f32
+    size_t xin, a0, a1, a2, head;   // block input (bf16 NHWC, cpad <= 32), activations, head (f32)
+    size_t bytes;
+};
+
+VinLayout vin_layout(int W, int H, int B);
+cudaError_t vin_flows(const VinLayout& L, const VinWeights& w, const VinPairs& pp, int fmt, uint8_t* ws, float* out,
+                      Prof* prof, cudaStream_t st);
+cudaError_t vin_synth(const VinPairs& pp, int npairs, const float* state, int fmt, int W, int H, int nviews,
+                      uint8_t* views, size_t frame_bytes, cudaStream_t st);
+
+}  // namespace fvv

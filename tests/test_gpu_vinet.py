@@ -1,0 +1,104 @@
+"""VINet (north-star CNN path) on B200 vs the fp32 torch oracle (oracle/vinet_ref.py).
+
+The convolutions run bf16 x bf16 -> fp32 on tcgen05, so the flows match the
+fp32 oracle within a tolerance; the synthesis kernel restates the oracle's
+fp32 arithmetic and is checked on the oracle's own flows.
+"""
+import numpy as np
+import pytest
+
+from oracle import vinet_ref as V
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    return torch
+
+
+def _pair(w, h, fmt, shift, seed):
+    from scipy.ndimage import gaussian_filter
+    rng = np.random.default_rng(seed)
+    big = gaussian_filter(rng.random((h + 8, w + 2 * abs(shift) + 8)) * 255.0, 2.5)
+    big = (big - big.min()) / (np.ptp(big) + 1e-9) * 230 + 12
+    a, b = big[4:4 + h, 4:4 + w], big[4:4 + h, 4 + shift:4 + shift + w]
+
+    def pack(p):
+        p = np.rint(p).astype(np.uint8)
+        if fmt == 0:
+            return p.reshape(-1)
+        if fmt == 2:
+            return np.stack([p, np.roll(p, 5, 1), 255 - p], -1).reshape(-1)
+        cw, ch = w // 2, h // 2
+        u = p.reshape(ch, 2, cw, 2).mean((1, 3)).astype(np.uint8)
+        return np.concatenate([p.reshape(-1), u.reshape(-1), (255 - u).reshape(-1)])
+    return pack(a), pack(b)
+
+
+CASES = [(448, 256, 2, 3), (256, 192, 1, 4), (192, 128, 0, -2)]
+
+
+@pytest.fixture(scope="module")
+def params():
+    from paper_2112_10603_b200.vinet_params import make_params
+    return make_params(0)
+
+
+@pytest.mark.parametrize("w,h,fmt,shift", CASES)
+def test_vinet_flows_match_fp32_oracle(torch_cuda, params, w, h, fmt, shift):
+    torch = torch_cuda
+    from paper_2112_10603_b200.vinet import VINet
+    l, r = _pair(w, h, fmt, shift, seed=w + fmt)
+    ref = V.flows(l, r, w, h, fmt, params).numpy()
+    net = VINet(w, h, fmt, params=params, max_pairs=2)
+    L = torch.from_numpy(np.stack([l, r])).cuda()
+    R = torch.from_numpy(np.stack([r, l])).cuda()
+    got = net.flows(L, R)
+    torch.cuda.synchronize()
+    g0 = got[0].cpu().numpy()
+    err = np.abs(g0 - ref).max()
+    scale = np.abs(ref).max()
+    # bf16 operands through 30 layers: relative error of the residual flows
+    assert err <= 0.03 * scale + 1e-3, (err, scale)
+    # batch independence: pair 1 (swapped inputs) equals a single-pair run
+    ref1 = V.flows(r, l, w, h, fmt, params).numpy()
+    assert np.abs(got[1].cpu().numpy() - ref1).max() <= 0.03 * np.abs(ref1).max() + 1e-3
+
+
+@pytest.mark.parametrize("w,h,fmt,shift", CASES)
+def test_vinet_synth_on_oracle_flows(torch_cuda, params, w, h, fmt, shift):
+    torch = torch_cuda
+    from paper_2112_10603_b200.vinet import VINet
+    l, r = _pair(w, h, fmt, shift, seed=w + fmt + 1)
+    st = V.flows(l, r, w, h, fmt, params)
+    st = st * 8.0  # exercise real displacements (several pixels) in the warp
+    net = VINet(w, h, fmt, params=params, max_pairs=1)
+    n = 5
+    got = net.synth(torch.from_numpy(l[None]).cuda(), torch.from_numpy(r[None]).cuda(),
+                    st[None].contiguous().cuda(), n)
+    torch.cuda.synchronize()
+    got = got[0].cpu().numpy()
+    for j in range(1, n + 1):
+        ref = V.synth(l, r, w, h, fmt, st, j / (n + 1))
+        d = np.abs(got[j - 1].astype(int) - ref.astype(int))
+        # identical fp32 formula; expf / division ulps can flip a rounding at .5
+        assert d.max() <= 1 and (d > 0).mean() < 1e-3, (j, d.max(), (d > 0).mean())
+
+
+def test_vinet_end_to_end_psnr(torch_cuda, params):
+    torch = torch_cuda
+    from paper_2112_10603_b200.vinet import VINet
+    w, h, fmt = 448, 256, 2
+    l, r = _pair(w, h, fmt, 3, seed=7)
+    st = V.flows(l, r, w, h, fmt, params)
+    net = VINet(w, h, fmt, params=params)
+    got = net.dense_views(torch.from_numpy(l[None]).cuda(), torch.from_numpy(r[None]).cuda(), 3)[0].cpu().numpy()
+    for j in range(1, 4):
+        ref = V.synth(l, r, w, h, fmt, st, j / 4).astype(np.float64)
+        mse = np.mean((got[j - 1].astype(np.float64) - ref) ** 2)
+        psnr = 99.0 if mse == 0 else 10 * np.log10(255.0 ** 2 / mse)
+        assert psnr >= 50.0, psnr
