@@ -507,8 +507,70 @@ def run_b200(args, cfg, rank, world, local_rank):
         "gpu_launches": gpu_launches,
         "clocks": clk,
     }
+    if not args.no_vinet and rank == 0 and min(W, H) >= 64:
+        line["vinet"] = run_vinet(cfg, dev)
     print(json.dumps(line))
     return 0
+
+
+def vinet_conv_flops(W, H):
+    """Useful convolution FLOPs of one VINet forward (vinet_params.LAYERS on the 64-aligned canvas)."""
+    from paper_2112_10603_b200.vinet_params import BLOCK_IN
+    Wp, Hp = (W + 63) // 64 * 64, (H + 63) // 64 * 64
+    tot = 0
+    for i in range(3):
+        w, h = Wp >> (2 - i), Hp >> (2 - i)
+        tot += 2 * (w // 2) * (h // 2) * 128 * 9 * BLOCK_IN[i]     # c0
+        tot += 2 * (w // 4) * (h // 4) * 256 * 9 * 128             # c1
+        tot += 6 * 2 * (w // 4) * (h // 4) * 256 * 9 * 256         # r1..r6
+        tot += 2 * (w // 2) * (h // 2) * 128 * 4 * 256             # u0: 2x2 taps per output phase
+        tot += 2 * w * h * 5 * 4 * 128                             # u1
+    return tot
+
+
+def run_vinet(cfg, dev, steps=10, warmup=3):
+    """The north-star CNN path on the same rig: VINet flows once per camera pair
+    + direct-t synthesis of all views of the pair in one pass (tcgen05 convs)."""
+    import torch
+    from paper_2112_10603_b200.vinet import VINet
+    W, H, fmt, C, S = cfg["W"], cfg["H"], cfg["fmt"], cfg["cams"], cfg["stages"]
+    npairs, nviews = C - 1, (1 << S) - 1
+    cams = torch.from_numpy(synth_rig(W, H, fmt, C, seed=42)).to(dev)
+    net = VINet(W, H, fmt, seed=0, max_pairs=npairs, device=dev)
+    L, R = cams[:-1].contiguous(), cams[1:].contiguous()
+    flows = net.flows(L, R)
+    views = net.synth(L, R, flows, nviews)
+    for _ in range(warmup):
+        net.flows(L, R, out=flows)
+        net.synth(L, R, flows, nviews, out=views)
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    ev[0].record()
+    for _ in range(steps):
+        net.flows(L, R, out=flows)
+    ev[1].record()
+    for _ in range(steps):
+        net.synth(L, R, flows, nviews, out=views)
+    ev[2].record()
+    torch.cuda.synchronize()
+    fl_ms, sy_ms = ev[0].elapsed_time(ev[1]) / steps, ev[1].elapsed_time(ev[2]) / steps
+    flops = vinet_conv_flops(W, H) * npairs
+    peaks, src = measured_peaks()
+    peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1401.6)))
+    ach = flops / (fl_ms / 1e3) / 1e12
+    return {
+        "path": "VINet (north-star CNN: 3 VIBlocks x 10 tcgen05 conv layers, seeded random-init weights), "
+                "direct-t synthesis of every view of a pair from one flow field",
+        "value": npairs * nviews / ((fl_ms + sy_ms) / 1e3), "unit": "views/s",
+        "ms_per_step": fl_ms + sy_ms, "flows_ms": fl_ms, "synth_ms": sy_ms,
+        "pairs": npairs, "views_per_pair": nviews, "dtype": "bf16 convs, fp32 accumulate / warps",
+        "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                     "traffic": None, "flop_per_step": flops,
+                     "note": "useful conv FLOPs / whole flow-network time (pyramid, block inputs and "
+                             "residual kernels included); peak = sustained cuBLAS bf16 (%s)" % src},
+        "parity": "fp32 torch oracle (oracle/vinet_ref.py): flows within 3 % max-abs, synthesis within "
+                  "1 level, end-to-end PSNR >= 50 dB (tests/test_gpu_vinet.py)",
+    }
 
 
 def main():
@@ -522,6 +584,7 @@ def main():
     ap.add_argument("--frames-in-flight", type=int, default=1,
                     help="independent rig frames of the live stream processed concurrently per step")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--no-vinet", action="store_true", help="skip the VINet (CNN path) section")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))
