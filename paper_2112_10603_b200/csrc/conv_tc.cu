@@ -108,13 +108,17 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
+// A CTA computes MT = 2 output rows x 128 pixels (two M = 128 accumulators in
+// TMEM) so every weight chunk fetched from L2 feeds two MMAs.
+constexpr int kMT = 2;
 template <int NT, int SW>
 struct ConvTile {
-    static constexpr int kABytes = 128 * SW;
+    static constexpr int kABytes = 128 * SW;                 // one 128-pixel row segment
     static constexpr int kBBytes = NT * SW;
-    static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kTmemCols = NT < 32 ? 32 : NT;  // power of two >= 32
-    static constexpr size_t kSmem = 1024 /* alignment slack */ + (size_t)kConvStages * kStageBytes + 256;
+    static constexpr int kStageBytes = kMT * kABytes + kBBytes;
+    static constexpr int kStages = kStageBytes > 48 * 1024 ? 3 : kConvStages;
+    static constexpr int kTmemCols = kMT * NT < 32 ? 32 : kMT * NT;  // power of two >= 32
+    static constexpr size_t kSmem = 1024 /* alignment slack */ + (size_t)kStages * kStageBytes + 256;
 };
 
 template <int NT, int SW>
@@ -125,19 +129,21 @@ __global__ void __launch_bounds__(128, 1)
     static_assert(NT % 16 == 0 && NT >= 16 && NT <= 256, "UMMA N (M = 128)");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kConvStages * T::kStageBytes);
-    uint64_t* empty = full + kConvStages;
-    uint64_t* accum = empty + kConvStages;
+    constexpr int S = T::kStages;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * T::kStageBytes);
+    uint64_t* empty = full + S;
+    uint64_t* accum = empty + S;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int b = blockIdx.y / p.Hg, gy = blockIdx.y - b * p.Hg;
+    const int hg2 = (p.Hg + kMT - 1) / kMT;
+    const int b = blockIdx.y / hg2, gy0 = (blockIdx.y - b * hg2) * kMT;
     const int gx0 = blockIdx.x * 128;
     const int n0 = blockIdx.z * NT;
     const int nk = p.ntaps * p.kc_per_tap;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kConvStages; s++) {
+        for (int s = 0; s < S; s++) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
@@ -159,29 +165,36 @@ __global__ void __launch_bounds__(128, 1)
 
     if (warp == 0 && lane == 0) {
         // ---- TMA producer ----
-        const int iy0 = gy * p.sy + p.by0, ix0 = gx0 * p.sx + p.bx0;
+        const int ix0 = gx0 * p.sx + p.bx0;
         for (int kc = 0; kc < nk; kc++) {
-            const int s = kc % kConvStages;
-            if (kc >= kConvStages) mbar_wait(&empty[s], ((kc / kConvStages) - 1) & 1);
+            const int s = kc % S;
+            if (kc >= S) mbar_wait(&empty[s], ((kc / S) - 1) & 1);
             const int tap = kc / p.kc_per_tap, c0 = (kc - tap * p.kc_per_tap) * (SW / 2);
             uint8_t* sa = smem + s * T::kStageBytes;
             mbar_expect_tx(&full[s], T::kStageBytes);
-            tma_load_4d(sa, &tmA, &full[s], c0, ix0 + p.tdx[tap], iy0 + p.tdy[tap], b);
-            tma_load_2d(sa + T::kABytes, &tmB, &full[s], tap * p.cpad + c0, p.wrow0 + n0);
+#pragma unroll
+            for (int r = 0; r < kMT; r++)  // rows past Hg load real or zero rows; the epilogue skips them
+                tma_load_4d(sa + r * T::kABytes, &tmA, &full[s], c0, ix0 + p.tdx[tap],
+                            (gy0 + r) * p.sy + p.by0 + p.tdy[tap], b);
+            tma_load_2d(sa + kMT * T::kABytes, &tmB, &full[s], tap * p.cpad + c0, p.wrow0 + n0);
         }
     } else if (warp == 1 && lane == 0) {
         // ---- MMA issuer ----
         constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NT >> 3) << 17) |
                                    ((uint32_t)(128 >> 4) << 24);
         for (int kc = 0; kc < nk; kc++) {
-            const int s = kc % kConvStages;
-            mbar_wait(&full[s], (kc / kConvStages) & 1);
+            const int s = kc % S;
+            mbar_wait(&full[s], (kc / S) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-            const uint32_t sa = smem_u32(smem + s * T::kStageBytes), sb = sa + T::kABytes;
+            const uint32_t sa = smem_u32(smem + s * T::kStageBytes), sb = sa + kMT * T::kABytes;
 #pragma unroll
-            for (int k = 0; k < SW / 32; k++)
-                umma_bf16(tmem, umma_desc<SW>(sa + 32 * k), umma_desc<SW>(sb + 32 * k), idesc,
-                          (kc > 0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < SW / 32; k++) {
+                const uint64_t db = umma_desc<SW>(sb + 32 * k);
+#pragma unroll
+                for (int r = 0; r < kMT; r++)
+                    umma_bf16(tmem + r * NT, umma_desc<SW>(sa + r * T::kABytes + 32 * k), db, idesc,
+                              (kc > 0 || k > 0) ? 1u : 0u);
+            }
             umma_commit(&empty[s]);  // frees the stage once these MMAs have read it
         }
         umma_commit(accum);
@@ -193,14 +206,17 @@ __global__ void __launch_bounds__(128, 1)
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const int row = warp * 32 + lane;
     const int gx = gx0 + row;
-    const bool valid = gx < p.Wg;
-    const int oy = gy * p.omy + p.oay, ox = gx * p.omx + p.oax;
-    const size_t obase = (((size_t)b * p.Hout + oy) * p.Wout + ox) * p.ostride + p.ocoff;
     constexpr int CW = NT < 32 ? NT : 32;  // columns per tcgen05.ld
 #pragma unroll 1
-    for (int c = 0; c < NT; c += CW) {
+    for (int cc = 0; cc < kMT * NT; cc += CW) {
+    const int sub = cc / NT, c = cc - sub * NT;
+    const int gy = gy0 + sub;
+    const bool valid = gx < p.Wg && gy < p.Hg;
+    const int oy = gy * p.omy + p.oay, ox = gx * p.omx + p.oax;
+    const size_t obase = (((size_t)b * p.Hout + oy) * p.Wout + ox) * p.ostride + p.ocoff;
+    {
         uint32_t r[32];
-        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + c;
+        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + cc;
         if (CW == 32) {
             asm volatile(
                 "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -255,6 +271,7 @@ __global__ void __launch_bounds__(128, 1)
                 }
             }
         }
+    }
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
@@ -319,7 +336,7 @@ static cudaError_t launch_nt_sw(const CUtensorMap& a, const CUtensorMap& w, cons
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    dim3 grid((p.Wg + 127) / 128, p.Hg * p.B, ntiles);
+    dim3 grid((p.Wg + 127) / 128, (p.Hg + kMT - 1) / kMT * p.B, ntiles);
     kern<<<grid, 128, T::kSmem, st>>>(a, w, bias, out, p);
     return cudaGetLastError();
 }
