@@ -35,7 +35,6 @@
 
 namespace fvv {
 
-constexpr int kConvStages = 4;
 
 // ---------------------------------------------------------------------------
 // PTX wrappers
@@ -106,40 +105,58 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 }
 
 // ---------------------------------------------------------------------------
-// the kernel
+// the kernel: persistent, warp-specialised, double-buffered accumulators
 // ---------------------------------------------------------------------------
-// A CTA computes MT = 2 output rows x 128 pixels (two M = 128 accumulators in
-// TMEM) so every weight chunk fetched from L2 feeds two MMAs.
-constexpr int kMT = 2;
+// A CTA loops over output tiles (128 pixels of one output row x NT channels).
+// Warp 0 / lane 0 streams K chunks with TMA into kStages smem stages; warp 1 /
+// lane 0 issues the MMAs of tile i into TMEM accumulator i % 2; warps 2-5 drain
+// accumulator (i - 1) % 2 meanwhile (tcgen05.ld, bias, ReLU, stores) -- the
+// epilogue of one tile overlaps the MMAs of the next.
 template <int NT, int SW>
 struct ConvTile {
     static constexpr int kABytes = 128 * SW;                 // one 128-pixel row segment
     static constexpr int kBBytes = NT * SW;
-    static constexpr int kStageBytes = kMT * kABytes + kBBytes;
-    static constexpr int kStages = kStageBytes > 48 * 1024 ? 3 : kConvStages;
-    static constexpr int kTmemCols = kMT * NT < 32 ? 32 : kMT * NT;  // power of two >= 32
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kStages = kStageBytes > 40 * 1024 ? 4 : 6;
+    static constexpr int kTmemCols = 2 * NT < 32 ? 32 : 2 * NT;  // two accumulators, power of two >= 32
     static constexpr size_t kSmem = 1024 /* alignment slack */ + (size_t)kStages * kStageBytes + 256;
 };
+constexpr int kConvThreads = 192;
+
+struct TileCoord {
+    int b, gy, gx0, n0;
+};
+__device__ __forceinline__ TileCoord tile_of(int t, const ConvTCParams& p, int ntx, int nn, int NT) {
+    TileCoord c;
+    const int tn = t % nn;
+    t /= nn;
+    const int tx = t % ntx;
+    t /= ntx;
+    c.gy = t % p.Hg;
+    c.b = t / p.Hg;
+    c.gx0 = tx * 128;
+    c.n0 = tn * NT;
+    return c;
+}
 
 template <int NT, int SW>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(kConvThreads, 1)
     k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const float* __restrict__ bias, void* __restrict__ out, ConvTCParams p) {
     using T = ConvTile<NT, SW>;
     static_assert(NT % 16 == 0 && NT >= 16 && NT <= 256, "UMMA N (M = 128)");
+    constexpr int S = T::kStages;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-    constexpr int S = T::kStages;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * T::kStageBytes);
     uint64_t* empty = full + S;
-    uint64_t* accum = empty + S;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+    uint64_t* tfull = empty + S;    // [2] accumulator ready
+    uint64_t* tempty = tfull + 2;   // [2] accumulator drained
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int hg2 = (p.Hg + kMT - 1) / kMT;
-    const int b = blockIdx.y / hg2, gy0 = (blockIdx.y - b * hg2) * kMT;
-    const int gx0 = blockIdx.x * 128;
-    const int n0 = blockIdx.z * NT;
+    const int ntx = (p.Wg + 127) / 128, nn = (p.N + NT - 1) / NT;
+    const int ntiles = ntx * nn * p.Hg * p.B;
     const int nk = p.ntaps * p.kc_per_tap;
 
     if (threadIdx.x == 0) {
@@ -147,7 +164,10 @@ __global__ void __launch_bounds__(128, 1)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(accum, 1);
+        for (int a = 0; a < 2; a++) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 4);  // one arrival per epilogue warp
+        }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmA) : "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
@@ -163,116 +183,131 @@ __global__ void __launch_bounds__(128, 1)
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == 0 && lane == 0) {
-        // ---- TMA producer ----
-        const int ix0 = gx0 * p.sx + p.bx0;
-        for (int kc = 0; kc < nk; kc++) {
-            const int s = kc % S;
-            if (kc >= S) mbar_wait(&empty[s], ((kc / S) - 1) & 1);
-            const int tap = kc / p.kc_per_tap, c0 = (kc - tap * p.kc_per_tap) * (SW / 2);
-            uint8_t* sa = smem + s * T::kStageBytes;
-            mbar_expect_tx(&full[s], T::kStageBytes);
-#pragma unroll
-            for (int r = 0; r < kMT; r++)  // rows past Hg load real or zero rows; the epilogue skips them
-                tma_load_4d(sa + r * T::kABytes, &tmA, &full[s], c0, ix0 + p.tdx[tap],
-                            (gy0 + r) * p.sy + p.by0 + p.tdy[tap], b);
-            tma_load_2d(sa + kMT * T::kABytes, &tmB, &full[s], tap * p.cpad + c0, p.wrow0 + n0);
-        }
-    } else if (warp == 1 && lane == 0) {
-        // ---- MMA issuer ----
-        constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NT >> 3) << 17) |
-                                   ((uint32_t)(128 >> 4) << 24);
-        for (int kc = 0; kc < nk; kc++) {
-            const int s = kc % S;
-            mbar_wait(&full[s], (kc / S) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-            const uint32_t sa = smem_u32(smem + s * T::kStageBytes), sb = sa + kMT * T::kABytes;
-#pragma unroll
-            for (int k = 0; k < SW / 32; k++) {
-                const uint64_t db = umma_desc<SW>(sb + 32 * k);
-#pragma unroll
-                for (int r = 0; r < kMT; r++)
-                    umma_bf16(tmem + r * NT, umma_desc<SW>(sa + r * T::kABytes + 32 * k), db, idesc,
-                              (kc > 0 || k > 0) ? 1u : 0u);
-            }
-            umma_commit(&empty[s]);  // frees the stage once these MMAs have read it
-        }
-        umma_commit(accum);
-    }
-    __syncwarp();
-
-    // ---- epilogue: TMEM -> registers -> bias + activation -> global ----
-    mbar_wait(accum, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    const int row = warp * 32 + lane;
-    const int gx = gx0 + row;
-    constexpr int CW = NT < 32 ? NT : 32;  // columns per tcgen05.ld
-#pragma unroll 1
-    for (int cc = 0; cc < kMT * NT; cc += CW) {
-    const int sub = cc / NT, c = cc - sub * NT;
-    const int gy = gy0 + sub;
-    const bool valid = gx < p.Wg && gy < p.Hg;
-    const int oy = gy * p.omy + p.oay, ox = gx * p.omx + p.oax;
-    const size_t obase = (((size_t)b * p.Hout + oy) * p.Wout + ox) * p.ostride + p.ocoff;
-    {
-        uint32_t r[32];
-        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + cc;
-        if (CW == 32) {
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-                  "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-                  "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
-                  "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-                : "r"(taddr));
-        } else {
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15},"
-                " [%16];\n"
-                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-                  "=r"(r[15])
-                : "r"(taddr));
-        }
-        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-        if (valid) {
-            float v[32];
-#pragma unroll
-            for (int j = 0; j < CW; j++) {
-                const int n = n0 + c + j;
-                float x = __uint_as_float(r[j]) + (n < p.N ? bias[n] : 0.0f);
-                if (p.act == 1) x = fmaxf(x, 0.0f);
-                v[j] = x;
-            }
-            if (p.out_f32) {
-                float* o = reinterpret_cast<float*>(out) + obase;
-#pragma unroll
-                for (int j = 0; j < CW; j++)
-                    if (n0 + c + j < p.N) o[n0 + c + j] = v[j];
-            } else {
-                __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out) + obase + n0 + c;
-                if (n0 + c + CW <= p.N && ((obase + n0 + c) & 7) == 0) {
-#pragma unroll
-                    for (int j = 0; j < CW; j += 8) {
-                        uint4 q;
-                        __nv_bfloat162 h0 = __floats2bfloat162_rn(v[j], v[j + 1]);
-                        __nv_bfloat162 h1 = __floats2bfloat162_rn(v[j + 2], v[j + 3]);
-                        __nv_bfloat162 h2 = __floats2bfloat162_rn(v[j + 4], v[j + 5]);
-                        __nv_bfloat162 h3 = __floats2bfloat162_rn(v[j + 6], v[j + 7]);
-                        memcpy(&q.x, &h0, 4); memcpy(&q.y, &h1, 4); memcpy(&q.z, &h2, 4); memcpy(&q.w, &h3, 4);
-                        *reinterpret_cast<uint4*>(o + j) = q;
-                    }
-                } else {
-#pragma unroll
-                    for (int j = 0; j < CW; j++)
-                        if (n0 + c + j < p.N) o[j] = __float2bfloat16_rn(v[j]);
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---- TMA producer ----
+            int kg = 0;  // global K-chunk counter (stage / phase continue across tiles)
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const TileCoord c = tile_of(t, p, ntx, nn, NT);
+                const int ix0 = c.gx0 * p.sx + p.bx0, iy0 = c.gy * p.sy + p.by0;
+                for (int kc = 0; kc < nk; kc++, kg++) {
+                    const int s = kg % S;
+                    if (kg >= S) mbar_wait(&empty[s], ((kg / S) - 1) & 1);
+                    const int tap = kc / p.kc_per_tap, c0 = (kc - tap * p.kc_per_tap) * (SW / 2);
+                    uint8_t* sa = smem + s * T::kStageBytes;
+                    mbar_expect_tx(&full[s], T::kStageBytes);
+                    tma_load_4d(sa, &tmA, &full[s], c0, ix0 + p.tdx[tap], iy0 + p.tdy[tap], c.b);
+                    tma_load_2d(sa + T::kABytes, &tmB, &full[s], tap * p.cpad + c0, p.wrow0 + c.n0);
                 }
             }
         }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ---- MMA issuer ----
+            constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NT >> 3) << 17) |
+                                       ((uint32_t)(128 >> 4) << 24);
+            int kg = 0, i = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, i++) {
+                const int acc = i & 1;
+                if (i >= 2) mbar_wait(&tempty[acc], ((i >> 1) - 1) & 1);  // drained by the epilogue
+                asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+                const uint32_t td = tmem + acc * NT;
+                for (int kc = 0; kc < nk; kc++, kg++) {
+                    const int s = kg % S;
+                    mbar_wait(&full[s], (kg / S) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+                    const uint32_t sa = smem_u32(smem + s * T::kStageBytes), sb = sa + T::kABytes;
+#pragma unroll
+                    for (int k = 0; k < SW / 32; k++)
+                        umma_bf16(td, umma_desc<SW>(sa + 32 * k), umma_desc<SW>(sb + 32 * k), idesc,
+                                  (kc > 0 || k > 0) ? 1u : 0u);
+                    umma_commit(&empty[s]);  // frees the stage once these MMAs have read it
+                }
+                umma_commit(&tfull[acc]);
+            }
+        }
+    } else {
+        // ---- epilogue warps 2..5: TMEM lanes 32 * (warp % 4) .. +31 ----
+        const int q = warp & 3;
+        const int row = q * 32 + lane;
+        constexpr int CW = NT < 32 ? NT : 32;  // columns per tcgen05.ld
+        int i = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, i++) {
+            const TileCoord c = tile_of(t, p, ntx, nn, NT);
+            const int acc = i & 1;
+            mbar_wait(&tfull[acc], (i >> 1) & 1);
+            __syncwarp();
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            const int gx = c.gx0 + row;
+            const bool valid = gx < p.Wg;
+            const int oy = c.gy * p.omy + p.oay, ox = gx * p.omx + p.oax;
+            const size_t obase = (((size_t)c.b * p.Hout + oy) * p.Wout + ox) * p.ostride + p.ocoff;
+#pragma unroll 1
+            for (int cc = 0; cc < NT; cc += CW) {
+                uint32_t r[32];
+                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + acc * NT + cc;
+                if (CW == 32) {
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+                        "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+                        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+                          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+                          "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+                          "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                        : "r"(taddr));
+                } else {
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+                        "%14,%15}, [%16];\n"
+                        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+                          "=r"(r[14]), "=r"(r[15])
+                        : "r"(taddr));
+                }
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                if (valid) {
+                    const int nb = c.n0 + cc;
+                    float v[32];
+#pragma unroll
+                    for (int j = 0; j < CW; j++) {
+                        float x = __uint_as_float(r[j]) + (nb + j < p.N ? bias[nb + j] : 0.0f);
+                        if (p.act == 1) x = fmaxf(x, 0.0f);
+                        v[j] = x;
+                    }
+                    if (p.out_f32) {
+                        float* o = reinterpret_cast<float*>(out) + obase;
+#pragma unroll
+                        for (int j = 0; j < CW; j++)
+                            if (nb + j < p.N) o[nb + j] = v[j];
+                    } else {
+                        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out) + obase + nb;
+                        if (nb + CW <= p.N && ((obase + nb) & 7) == 0) {
+#pragma unroll
+                            for (int j = 0; j < CW; j += 8) {
+                                uint4 u;
+                                __nv_bfloat162 h0 = __floats2bfloat162_rn(v[j], v[j + 1]);
+                                __nv_bfloat162 h1 = __floats2bfloat162_rn(v[j + 2], v[j + 3]);
+                                __nv_bfloat162 h2 = __floats2bfloat162_rn(v[j + 4], v[j + 5]);
+                                __nv_bfloat162 h3 = __floats2bfloat162_rn(v[j + 6], v[j + 7]);
+                                memcpy(&u.x, &h0, 4); memcpy(&u.y, &h1, 4); memcpy(&u.z, &h2, 4); memcpy(&u.w, &h3, 4);
+                                *reinterpret_cast<uint4*>(o + j) = u;
+                            }
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < CW; j++)
+                                if (nb + j < p.N) o[j] = __float2bfloat16_rn(v[j]);
+                        }
+                    }
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&tempty[acc]))
+                                        : "memory");
+        }
     }
-    }
+    __syncwarp();
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
     if (warp == 2)
@@ -336,8 +371,15 @@ static cudaError_t launch_nt_sw(const CUtensorMap& a, const CUtensorMap& w, cons
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    dim3 grid((p.Wg + 127) / 128, (p.Hg + kMT - 1) / kMT * p.B, ntiles);
-    kern<<<grid, 128, T::kSmem, st>>>(a, w, bias, out, p);
+    (void)ntiles;
+    static int nsm = 0;
+    if (!nsm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int tiles = (p.Wg + 127) / 128 * p.Hg * p.B * ((p.N + NT - 1) / NT);
+    kern<<<tiles < nsm ? tiles : nsm, kConvThreads, T::kSmem, st>>>(a, w, bias, out, p);
     return cudaGetLastError();
 }
 
