@@ -196,6 +196,12 @@ int fvv_vinet_flow(const fvv_frame_desc* desc, const fvv_vinet_weights* weights,
 int fvv_vinet_synth(const fvv_frame_desc* desc, const uint8_t* const* left, const uint8_t* const* right,
                     const float* flows, int npairs, int nviews, uint8_t* views, void* stream);
 
+/* The rig with VINet: ncams cameras (contiguous frames) -> the global views
+ * buffer of fvv_rig_views (anchor c at index c*2^stages, the 2^stages-1
+ * direct-t views of gap c after it), ready for fvv_rig_clusters. */
+int fvv_vinet_rig(const fvv_frame_desc* desc, const fvv_vinet_weights* weights, const uint8_t* cams, int ncams,
+                  int stages, uint8_t* views, void* workspace, size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

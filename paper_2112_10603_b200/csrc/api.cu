@@ -684,8 +684,53 @@ extern "C" int fvv_vinet_synth(const fvv_frame_desc* d, const uint8_t* const* le
             pp.right[i] = right[p0 + i];
         }
         cudaError_t e = vin_synth(pp, n, flows + plane * p0, d->format, d->width, d->height, nviews,
-                                  views + (size_t)p0 * nviews * fb, fb, st);
+                                  views + (size_t)p0 * nviews * fb, fb, (size_t)nviews * fb, st);
         if (e != cudaSuccess) return cuda_fail(e, "fvv_vinet_synth");
+    }
+    return FVV_OK;
+}
+
+extern "C" int fvv_vinet_rig(const fvv_frame_desc* d, const fvv_vinet_weights* wts, const uint8_t* cams, int ncams,
+                             int stages, uint8_t* views, void* ws, size_t ws_bytes, void* stream) {
+    int rc;
+    if ((rc = vin_check_desc(d))) return rc;
+    if (!wts || !cams || !views || !ws) return fail(FVV_EINVAL, "null argument");
+    if (ncams < 2) return fail(FVV_EINVAL, "a rig needs at least two cameras");
+    if (stages < 1 || stages > 6) return fail(FVV_EINVAL, "stages must be in [1, 6]");
+    fvv_frame_desc dd = *d;
+    const size_t fb = fvv_frame_bytes(&dd);
+    const int nv = (1 << stages) - 1, npairs = ncams - 1;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // anchors: camera c lands at global view index c * 2^stages (ViewIndexModel, viewmodel.py:23-71)
+    for (int c = 0; c < ncams; c++) {
+        cudaError_t e = cudaMemcpyAsync(views + (size_t)c * (nv + 1) * fb, cams + (size_t)c * fb, fb,
+                                        cudaMemcpyDeviceToDevice, st);
+        if (e != cudaSuccess) return cuda_fail(e, "fvv_vinet_rig");
+    }
+    int B = std::min(npairs, kVinMaxPairs);
+    while (B > 1 && vin_layout(d->width, d->height, B).bytes > ws_bytes) B--;
+    if (vin_layout(d->width, d->height, B).bytes > ws_bytes) return fail(FVV_EINVAL, "workspace too small for one pair");
+    VinWeights vw;
+    for (int i = 0; i < 3; i++)
+        for (int k = 0; k < 10; k++) {
+            if (!wts->w[i][k] || !wts->b[i][k]) return fail(FVV_EINVAL, "null layer weights");
+            vw.w[i][k] = wts->w[i][k];
+            vw.b[i][k] = wts->b[i][k];
+        }
+    for (int p0 = 0; p0 < npairs; p0 += B) {
+        const int n = std::min(B, npairs - p0);
+        const VinLayout L = vin_layout(d->width, d->height, n);
+        VinPairs pp{};
+        for (int i = 0; i < n; i++) {
+            pp.left[i] = cams + (size_t)(p0 + i) * fb;
+            pp.right[i] = cams + (size_t)(p0 + i + 1) * fb;
+        }
+        float* fl = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + L.flows);
+        cudaError_t e = vin_flows(L, vw, pp, d->format, static_cast<uint8_t*>(ws), fl, nullptr, st);
+        if (e == cudaSuccess)
+            e = vin_synth(pp, n, fl, d->format, d->width, d->height, nv, views + ((size_t)p0 * (nv + 1) + 1) * fb, fb,
+                          (size_t)(nv + 1) * fb, st);
+        if (e != cudaSuccess) return cuda_fail(e, "fvv_vinet_rig");
     }
     return FVV_OK;
 }

@@ -25,6 +25,7 @@ struct VinLayout {
     int W, H, Wp, Hp, B;            // frame, 64-aligned canvas, pairs per chunk
     size_t img[3], state[3];        // per level: images (B, 2, 3, h, w) f32, state (B, 5, h, w) f32
     size_t xin, a0, a1, a2, head;   // block input (bf16 NHWC, cpad <= 32), activations, head (f32)
+    size_t flows;                   // (B, 5, H, W) f32 scratch for fvv_vinet_rig
     size_t bytes;
 };
 
@@ -32,6 +33,6 @@ VinLayout vin_layout(int W, int H, int B);
 cudaError_t vin_flows(const VinLayout& L, const VinWeights& w, const VinPairs& pp, int fmt, uint8_t* ws, float* out,
                       Prof* prof, cudaStream_t st);
 cudaError_t vin_synth(const VinPairs& pp, int npairs, const float* state, int fmt, int W, int H, int nviews,
-                      uint8_t* views, size_t frame_bytes, cudaStream_t st);
+                      uint8_t* views, size_t frame_bytes, size_t pair_stride, cudaStream_t st);
 
 }  // namespace fvv

@@ -37,6 +37,8 @@ def _sig(L):
     L.fvv_vinet_flow.argtypes = [pd, ctypes.POINTER(_Weights), PP, PP, I, P, P, Z, P]
     L.fvv_vinet_synth.restype = I
     L.fvv_vinet_synth.argtypes = [pd, PP, PP, P, I, I, P, P]
+    L.fvv_vinet_rig.restype = I
+    L.fvv_vinet_rig.argtypes = [pd, ctypes.POINTER(_Weights), P, I, I, P, P, Z, P]
 
 
 class VINet:
@@ -105,3 +107,19 @@ class VINet:
     def dense_views(self, left, right, nviews: int):
         """flows + synth: the nviews direct-t views of every pair."""
         return self.synth(left, right, self.flows(left, right), nviews)
+
+    def rig(self, cams, stages: int, views=None):
+        """Rig frame: cams (C, frame_bytes) -> global views ((C-1)*2^stages + 1, frame_bytes) in the
+        fvv_rig_views layout (anchors + direct-t views per gap), ready for cluster.rig_clusters."""
+        import torch
+        C = cams.shape[0]
+        if cams.shape[1] != self.frame_bytes:
+            raise ValueError(f"cams must be (C, {self.frame_bytes}) uint8")
+        if views is None:
+            views = torch.empty((((C - 1) << stages) + 1, self.frame_bytes), dtype=torch.uint8, device=self.device)
+        _lib.check(self._L.fvv_vinet_rig(ctypes.byref(self._desc), ctypes.byref(self._w),
+                                         ctypes.c_void_p(cams.data_ptr()), C, int(stages),
+                                         ctypes.c_void_p(views.data_ptr()), ctypes.c_void_p(self._ws.data_ptr()),
+                                         self._ws.numel(), self._stream()))
+        return views
+

@@ -102,3 +102,22 @@ def test_vinet_end_to_end_psnr(torch_cuda, params):
         mse = np.mean((got[j - 1].astype(np.float64) - ref) ** 2)
         psnr = 99.0 if mse == 0 else 10 * np.log10(255.0 ** 2 / mse)
         assert psnr >= 50.0, psnr
+
+
+def test_vinet_rig_layout(torch_cuda, params):
+    """fvv_vinet_rig = anchors + per-gap direct-t views in the fvv_rig_views layout."""
+    torch = torch_cuda
+    from paper_2112_10603_b200.vinet import VINet
+    w, h, fmt, C, S = 192, 128, 1, 3, 2
+    frames = [_pair(w, h, fmt, 2 * c, seed=30 + c)[0] for c in range(C)]
+    cams = torch.from_numpy(np.stack(frames)).cuda()
+    net = VINet(w, h, fmt, params=params, max_pairs=2)
+    views = net.rig(cams, S)
+    L, R = cams[:-1].contiguous(), cams[1:].contiguous()
+    per_pair = net.dense_views(L, R, (1 << S) - 1)
+    torch.cuda.synchronize()
+    nv = (1 << S) - 1
+    for c in range(C):
+        assert torch.equal(views[c * (nv + 1)], cams[c])
+    for c in range(C - 1):
+        assert torch.equal(views[c * (nv + 1) + 1:c * (nv + 1) + 1 + nv], per_pair[c])
