@@ -177,8 +177,12 @@ int fvv_conv2d_bf16(const fvv_conv_desc* desc, const void* x, const void* w, con
 
 /* VINet forward, batched over camera pairs.  Weights: 3 blocks x 10 layers
  * (c0, c1, r1..r6, u0, u1; paper_2112_10603_b200/vinet_params.py), each packed
- * as documented for fvv_conv2d_bf16 with ntile 128 (c0, u0), 256 (c1, r*) and
- * 16 (u1) and in_cpad 16 / 32 for block 0 / blocks 1-2 c0.
+ * as documented for fvv_conv2d_bf16 with ntile 128 (c0, u0), 256 (c1, r*)
+ * and in_cpad 16 / 32 for block 0 / blocks 1-2 c0.  u1 (ConvTranspose2d
+ * 128->5) runs as one 3x3 sub-pixel convolution: weights [32][9*128] with row
+ * n = phase*5 + c (phase = (oy&1)*2 + (ox&1)) and tap (ty, tx) reading input
+ * offset (ty-1, tx-1) (convtc.pack_convT_subpixel); its bias has 20 entries
+ * (the 5 biases once per phase).
  * flows: [npairs][5][H][W] fp32 = F_m->l (x, y), F_m->r (x, y), mask logit.
  * The workspace holds fvv_vinet_workspace_size(desc, max_pairs) bytes; larger
  * batches run in chunks of max_pairs. */

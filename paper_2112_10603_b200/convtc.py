@@ -58,6 +58,27 @@ def pack_convT(weight, cpad: int, ntile: int):
     return w.reshape(4, npad, 4 * cpad).to(torch.bfloat16).contiguous()
 
 
+def pack_convT_subpixel(weight, cpad: int, ntile: int = 32):
+    """ConvTranspose2d(k4 s2 p1) [Cin][Cout][4][4] as ONE 3x3 stride-1 convolution with 4*Cout
+    outputs (sub-pixel form): row n = phase*Cout + c, phase = (oy&1)*2 + (ox&1); tap (ty, tx) reads
+    input offset (ty-1, tx-1).  -> bf16 [npad][9*cpad]."""
+    import torch
+    cin, cout, k, _ = weight.shape
+    assert k == 4
+    n = 4 * cout
+    npad = (n + ntile - 1) // ntile * ntile
+    w = torch.zeros((npad, 9, cpad), dtype=torch.float32, device=weight.device)
+    wf = weight.detach().float()
+    kof = {0: {0: 1, -1: 3}, 1: {1: 0, 0: 2}}  # parity -> input offset -> kernel index
+    for ph in range(4):
+        a, b = ph >> 1, ph & 1
+        for t in range(9):
+            dy, dx = t // 3 - 1, t % 3 - 1
+            if dy in kof[a] and dx in kof[b]:
+                w[ph * cout:(ph + 1) * cout, t, :cin] = wf[:, :, kof[a][dy], kof[b][dx]].t()
+    return w.reshape(npad, 9 * cpad).to(torch.bfloat16).contiguous()
+
+
 def conv2d(x, w_packed, bias, cout: int, kernel: int, stride: int, pad: int, *, transposed: bool = False,
            relu: bool = True, out=None, out_coff: int = 0, out_f32: bool = False, ntile: int | None = None,
            stream=None):

@@ -275,7 +275,19 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                         if (p.act == 1) x = fmaxf(x, 0.0f);
                         v[j] = x;
                     }
-                    if (p.out_f32) {
+                    if (p.shuffle_c) {
+                        // sub-pixel (transposed-conv) head: one 3x3 GEMM emits all 4 output phases
+#pragma unroll
+                        for (int j = 0; j < CW; j++) {
+                            const int n = nb + j;
+                            if (n < p.N) {
+                                const int ph = n / p.shuffle_c, ch = n - ph * p.shuffle_c;
+                                const size_t o = (((size_t)c.b * p.Hout + 2 * c.gy + (ph >> 1)) * p.Wout + 2 * gx +
+                                                  (ph & 1)) * p.ostride + p.ocoff + ch;
+                                reinterpret_cast<float*>(out)[o] = v[j];
+                            }
+                        }
+                    } else if (p.out_f32) {
                         float* o = reinterpret_cast<float*>(out) + obase;
 #pragma unroll
                         for (int j = 0; j < CW; j++)

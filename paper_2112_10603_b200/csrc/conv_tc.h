@@ -15,6 +15,8 @@ struct ConvTCParams {
     int omy, omx, oay, oax;                  // output coordinate = g * om + oa
     int Hout, Wout, ostride, ocoff, N;       // output tensor, channel placement, real channels
     int act, out_f32;                        // 1 = ReLU; 1 = fp32 output (else bf16)
+    int shuffle_c;                           // > 0: sub-pixel output (fp32): channel n = phase * shuffle_c + c
+                                             // lands at (2 gy + phase / 2, 2 gx + phase % 2), channel c
 };
 
 cudaError_t conv_tc(const void* x, int B, int Hin, int Win, int cpad, const void* w, int wrows, int wrow0,

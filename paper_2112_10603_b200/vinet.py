@@ -16,7 +16,7 @@ from __future__ import annotations
 import ctypes
 
 from . import _lib
-from .convtc import cpad_of, pack_conv, pack_convT
+from .convtc import cpad_of, pack_conv, pack_convT, pack_convT_subpixel
 from .frame import PixelFormat, frame_nbytes
 from .vinet_params import BLOCK_IN, LAYERS, make_params
 
@@ -62,8 +62,15 @@ class VINet:
                 cin = BLOCK_IN[i] if cin is None else cin
                 nt = NTILE.get(name, 256)
                 wd = w.to(self.device)
-                packed = pack_convT(wd, cpad_of(cin), nt) if kind == "convT" else pack_conv(wd, cpad_of(cin), nt)
-                bias = b.to(self.device, torch.float32).contiguous()
+                if name == "u1":  # the head: one sub-pixel 3x3 GEMM for all 4 output phases
+                    packed = pack_convT_subpixel(wd, cpad_of(cin), 32)
+                    bias = b.to(self.device, torch.float32).repeat(4).contiguous()
+                elif kind == "convT":
+                    packed = pack_convT(wd, cpad_of(cin), nt)
+                    bias = b.to(self.device, torch.float32).contiguous()
+                else:
+                    packed = pack_conv(wd, cpad_of(cin), nt)
+                    bias = b.to(self.device, torch.float32).contiguous()
                 self._keep += [packed, bias]
                 self._w.w[i][k] = packed.data_ptr()
                 self._w.b[i][k] = bias.data_ptr()

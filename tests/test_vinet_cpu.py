@@ -97,3 +97,23 @@ def test_oracle_flows_small():
     assert st.shape == (5, h, w) and torch.isfinite(st).all()
     v = V.synth(a, a, w, h, 1, st, 0.5)
     assert v.shape == a.shape
+
+
+def test_pack_convT_subpixel_layout():
+    """ConvTranspose2d(k4 s2 p1) == one 3x3 conv with 4*Cout sub-pixel outputs (the u1 head)."""
+    g = torch.Generator().manual_seed(3)
+    cin, cout, H, W = 16, 5, 4, 6
+    x = torch.randn((1, cin, H, W), generator=g).to(torch.bfloat16).float()
+    w = torch.randn((cin, cout, 4, 4), generator=g).to(torch.bfloat16).float()
+    cp = convtc.cpad_of(cin)
+    wp = convtc.pack_convT_subpixel(w, cp, 32)
+    assert wp.shape == (32, 9 * cp)
+    ref = Fn.conv_transpose2d(x, w, stride=2, padding=1).permute(0, 2, 3, 1)
+    xn = torch.zeros((1, H, W, cp))
+    xn[..., :cin] = x.permute(0, 2, 3, 1)
+    taps = [(t // 3, t % 3) for t in range(9)]
+    g20 = _gemm_conv(xn, wp, 4 * cout, 3, 1, 1, taps, -1, (H, W), 1, (0, 0), (1, H, W, 4 * cout))
+    got = torch.zeros((1, 2 * H, 2 * W, cout))
+    for ph in range(4):
+        got[:, (ph >> 1)::2, (ph & 1)::2, :] = g20[..., ph * cout:(ph + 1) * cout]
+    assert torch.allclose(got, ref, atol=1e-4, rtol=1e-4)
