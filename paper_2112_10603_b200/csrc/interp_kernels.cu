@@ -763,10 +763,10 @@ __global__ void __launch_bounds__(256) k_warpq(Geometry g, PairTable pt, uint8_t
             const int off = (sy >> vb) * w + (sx >> vb);
             int a, b, c, e;
             if (LEVEL == 1) {
-                const uint16_t* p0 = s4 + off;
+                const uint16_t* p0 = s4 + (unsigned)off;
                 a = p0[0]; b = p0[1]; c = p0[w]; e = p0[w + 1];
             } else {
-                const uint8_t* p0 = yp + off;
+                const uint8_t* p0 = yp + (unsigned)off;
                 a = p0[0]; b = p0[1]; c = p0[w]; e = p0[w + 1];
             }
             *op = (uint16_t)rne64((long long)bilerp_u(a, b, c, e, fx, fy, vb), k);
