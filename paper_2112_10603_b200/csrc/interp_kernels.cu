@@ -896,8 +896,8 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
         const float ol = rowpass(colpass(a0, b0, c0));
         const float orr = rowpass(colpass(a1, b1, c1));
         if (own) {
-            o_ol[(size_t)t * W + x] = ol;
-            o_or[(size_t)t * W + x] = orr;
+            o_ol[(unsigned)(t * W + x)] = ol;
+            o_or[(unsigned)(t * W + x)] = orr;
         }
     };
 
@@ -963,13 +963,13 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
         d1 = d2;
         d2 = abs(wl - wr);
         if (own && (!GEN || (yy >= y0 && yy < yo1))) {
-            o_wl[(size_t)yy * W + x] = (uint8_t)wl;
-            o_wr[(size_t)yy * W + x] = (uint8_t)wr;
+            o_wl[(unsigned)(yy * W + x)] = (uint8_t)wl;
+            o_wr[(unsigned)(yy * W + x)] = (uint8_t)wr;
         }
         // ---- Sd(yy-1): column sum of d with nearest padding ----
         {
             const int t = yy - 1;
-            if (own && (!GEN || (t >= y0 && t < yo1))) o_sd[(size_t)t * W + x] = (uint16_t)(((GEN && t == 0) ? d1 : d0) + d1 + d2);
+            if (own && (!GEN || (t >= y0 && t < yo1))) o_sd[(unsigned)(t * W + x)] = (uint16_t)(((GEN && t == 0) ? d1 : d0) + d1 + d2);
         }
         // ---- occ(yy-1) then O0/O(yy-2) ----
         {
@@ -1007,7 +1007,7 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
                 const uint8_t* pr = frR + (size_t)W * H + (size_t)p * cw * chh;
                 const uint8_t vl = (uint8_t)rne64(bilin_fixed(pl, cw, chh, cw, cy, cx, cv[0].x, cv[0].y, cb), kC);
                 const uint8_t vr = (uint8_t)rne64(bilin_fixed(pr, cw, chh, cw, cy, cx, cv[1].x, cv[1].y, cb), kC);
-                uint8_t* wc = reinterpret_cast<uint8_t*>(plane<uchar4>(ws, P, P.wc, pair) + (size_t)cy * cw + cx);
+                uint8_t* wc = reinterpret_cast<uint8_t*>(plane<uchar4>(ws, P, P.wc, pair) + (unsigned)(cy * cw + cx));
                 wc[2 * p] = vl;
                 wc[2 * p + 1] = vr;
             }
