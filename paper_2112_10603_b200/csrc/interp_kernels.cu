@@ -1191,18 +1191,24 @@ __global__ void __launch_bounds__(kCR) k_scan_carry(Geometry g, const uint8_t* _
 }
 
 #ifndef FVV_MINB_BLEND
-#define FVV_MINB_BLEND 6
+#define FVV_MINB_BLEND 10
 #endif
 template <int FMT>
 __global__ void __launch_bounds__(128, FVV_MINB_BLEND) k_blend(Geometry g, PairTable pt, const uint8_t* __restrict__ ws,
                                                Planes P, int pair_base, bool write_frame,
                                                double* mask_out /* nullable: one pair */) {
+    // thread = one 8-column group of ONE row; a warp holds 16 groups x the 2 rows
+    // of a row pair (lanes 0-15: upper row, 16-31: lower row), so the chroma
+    // 2x2-mean mask comes from a shuffle and each thread keeps one row's state
     const int W = g.W, H = g.H;
     const int pair = blockIdx.z + pair_base;
     const int ng = (W + 7) / 8;
-    const int gx = blockIdx.x * blockDim.x + threadIdx.x;  // 8-column group
-    const int yp = blockIdx.y;                              // row pair
-    if (gx >= ng) return;
+    const int lane = threadIdx.x & 31;
+    const int rr = lane >> 4;                                               // row within the pair
+    const int gxr = blockIdx.x * (blockDim.x / 2) + (threadIdx.x >> 5) * 16 + (lane & 15);
+    const bool active = gxr < ng;
+    const int gx = active ? gxr : ng - 1;                                   // 8-column group
+    const int yp = blockIdx.y;                                              // row pair
     const int x0 = gx * 8, n = min(8, W - x0);
     const uint16_t* sd = cplane<uint16_t>(ws, P, P.sd, pair);
     const double* carry = cplane<double>(ws, P, P.carry, pair);
@@ -1211,9 +1217,8 @@ __global__ void __launch_bounds__(128, FVV_MINB_BLEND) k_blend(Geometry g, PairT
     const uint8_t* wl = cplane<uint8_t>(ws, P, P.wl, pair);
     const uint8_t* wr = cplane<uint8_t>(ws, P, P.wr, pair);
     uint8_t* out = pt.out[pair];
-    double csum[4];  // chroma: per column pair, m(2j) + m(2j+1) of the upper row
-#pragma unroll
-    for (int rr = 0; rr < 2; rr++) {
+    double csum[4];  // chroma: per column pair, m(2j) + m(2j+1) of this thread's row
+    {
         const int y = 2 * yp + rr;
         const size_t ro = (size_t)y * W;
         const uint16_t* srow = sd + ro;
@@ -1267,7 +1272,7 @@ __global__ void __launch_bounds__(128, FVV_MINB_BLEND) k_blend(Geometry g, PairT
             if (j > 0) tmp = __dadd_rn(tmp, __dsub_rn(d0_of(s[j + 3]), d0_of(s[j])));
             mrow[j] = j < n ? mask_of(tmp, vl[j], vr[j], g) : 0.0;
         }
-        if (write_frame) {
+        if (write_frame && active) {
             if (FMT == FVV_RGB8) {
                 const uint8_t* px = cplane<uint8_t>(ws, P, P.wrgb, pair) + (ro + x0) * 6;
                 uint8_t* o = out + (ro + x0) * 3;
@@ -1288,7 +1293,7 @@ __global__ void __launch_bounds__(128, FVV_MINB_BLEND) k_blend(Geometry g, PairT
                 if (n == 8) *reinterpret_cast<uint32_t*>(out + ro + x0 + 4) = hi;
             }
         }
-        if (mask_out) {
+        if (mask_out && active) {
 #pragma unroll
             for (int j = 0; j < 8; j++)
                 if (j < n) mask_out[ro + x0 + j] = mrow[j];
@@ -1297,12 +1302,13 @@ __global__ void __launch_bounds__(128, FVV_MINB_BLEND) k_blend(Geometry g, PairT
 #pragma unroll
             for (int j = 0; j < 4; j++) {
                 const double p = __dadd_rn(mrow[2 * j], mrow[2 * j + 1]);
-                csum[j] = rr == 0 ? p : __dadd_rn(csum[j], p);   // (a + b) + (c + d)
+                const double up = __shfl_xor_sync(0xffffffffu, p, 16);  // the other row's pair sum
+                csum[j] = rr == 0 ? p : __dadd_rn(up, p);                // (a + b) + (c + d)
             }
         }
     }
     // chroma blend with the 2x2-mean mask (warp.py:83-88)
-    if (FMT == FVV_YUV420 && write_frame) {
+    if (FMT == FVV_YUV420 && write_frame && active && rr == 1) {
         const int cw = g.cw, chh = g.ch;
         const int cx0 = x0 / 2, nc = n / 2;
         const uchar4* wc = cplane<uchar4>(ws, P, P.wc, pair) + (size_t)yp * cw + cx0;
@@ -1862,7 +1868,7 @@ cudaError_t run_interp_stage(const Geometry& g, const PairTable& pt, uint8_t* ws
     if ((e = E()) != cudaSuccess) return e;
     B(KC_BLEND);
     {
-        const dim3 grd(((g.W + 7) / 8 + 127) / 128, g.H / 2, npairs);
+        const dim3 grd(((g.W + 7) / 8 + 63) / 64, g.H / 2, npairs);
         if (g.fmt == FVV_YUV420) k_blend<FVV_YUV420><<<grd, 128, 0, st>>>(g, pt, ws, P, 0, true, mask_out);
         else if (g.fmt == FVV_RGB8) k_blend<FVV_RGB8><<<grd, 128, 0, st>>>(g, pt, ws, P, 0, true, mask_out);
         else k_blend<FVV_GRAY8><<<grd, 128, 0, st>>>(g, pt, ws, P, 0, true, mask_out);
@@ -1955,7 +1961,7 @@ cudaError_t run_diag(const Geometry& g, const PairTable& pt, uint8_t* ws, const 
         if (e != cudaSuccess) return e;
     }
     if (mask) {
-        const dim3 grd(((g.W + 7) / 8 + 127) / 128, g.H / 2, 1);
+        const dim3 grd(((g.W + 7) / 8 + 63) / 64, g.H / 2, 1);
         if (g.fmt == FVV_YUV420) k_blend<FVV_YUV420><<<grd, 128, 0, st>>>(g, pt, ws, P, pair, false, mask);
         else if (g.fmt == FVV_RGB8) k_blend<FVV_RGB8><<<grd, 128, 0, st>>>(g, pt, ws, P, pair, false, mask);
         else k_blend<FVV_GRAY8><<<grd, 128, 0, st>>>(g, pt, ws, P, pair, false, mask);
