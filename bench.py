@@ -508,7 +508,10 @@ def run_b200(args, cfg, rank, world, local_rank):
         "clocks": clk,
     }
     if not args.no_vinet and rank == 0 and min(W, H) >= 64:
-        line["vinet"] = run_vinet(cfg, dev)
+        try:
+            line["vinet"] = run_vinet(cfg, dev)
+        except Exception as exc:  # the headline line must survive a failure of the secondary path
+            line["vinet"] = {"error": f"{type(exc).__name__}: {exc}"}
     print(json.dumps(line))
     return 0
 
