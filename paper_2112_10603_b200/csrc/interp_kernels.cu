@@ -1372,9 +1372,13 @@ struct SadW {
     static constexpr int WW = 8 * ((LASTW / 4) + 1) > 64 + 2 * XPAD ? 8 * ((LASTW / 4) + 1)
                                                                     : 64 + 2 * XPAD;  // samples
     static constexpr int TWW = WW / 2;                     // words per window row
-    static constexpr int WH = 8 * NBY + 2 * R;             // window rows
-    static constexpr size_t SMEM = (size_t)WH * TWW * 4 + (size_t)8 * NBY * 32 * 4 +
-                                   (size_t)NB * 8 + (size_t)SIDE * SIDE * 2;
+    // each thread searches RB blocks stacked vertically (NBY block rows apart):
+    // setup, rank table and the window apron are shared by twice the work
+    static constexpr int RB = SIDE <= 9 ? 2 : 1;
+    static constexpr int NBYT = NBY * RB;                  // block rows per CTA
+    static constexpr int WH = 8 * NBYT + 2 * R;            // window rows
+    static constexpr size_t SMEM = (size_t)WH * TWW * 4 + (size_t)8 * NBYT * 32 * 4 +
+                                   (size_t)NB * RB * 8 + (size_t)SIDE * SIDE * 2;
 };
 
 struct SadWLaunch {
@@ -1470,15 +1474,15 @@ k_sadw(Geometry g, PairTable pt, uint8_t* __restrict__ ws, Planes P, SadWLaunch 
     static_assert(S::NG == 1 || CG % 2 == 0, "dx groups need an even width");
     extern __shared__ __align__(16) uint8_t smem[];
     uint32_t* Ts = reinterpret_cast<uint32_t*>(smem);              // WH x TWW raw words
-    uint32_t* Rs = Ts + S::WH * S::TWW;                            // 8*NBY x 32 pair words
-    uint32_t* best = Rs + 8 * S::NBY * 32;                         // NB keys
-    int* suma = reinterpret_cast<int*>(best + S::NB);              // NB reference sums
-    int16_t* rk = reinterpret_cast<int16_t*>(suma + S::NB);        // SIDE^2 ranks
+    uint32_t* Rs = Ts + S::WH * S::TWW;                            // 8*NBYT x 32 pair words
+    uint32_t* best = Rs + 8 * S::NBYT * 32;                        // NB*RB keys
+    int* suma = reinterpret_cast<int*>(best + S::NB * S::RB);      // NB*RB reference sums
+    int16_t* rk = reinterpret_cast<int16_t*>(suma + S::NB * S::RB);  // SIDE^2 ranks
 
     const Level& L = g.lv[LEVEL];
     const int w = L.w, h = L.h;
     const int pair = blockIdx.z >> 1, d = blockIdx.z & 1;
-    const int bx0 = blockIdx.x * 8, by0 = blockIdx.y * S::NBY;
+    const int bx0 = blockIdx.x * 8, by0 = blockIdx.y * S::NBYT;
     const int tid = threadIdx.x;
 
     // ---- stage: target window (raw u16, edge replicated) -------------------
@@ -1508,14 +1512,14 @@ k_sadw(Geometry g, PairTable pt, uint8_t* __restrict__ ws, Planes P, SadWLaunch 
     }
     cp_async_commit();
     // ---- stage: reference strip as pixel-pair words + per-block sums -------
-    for (int i = tid; i < S::NB; i += S::THREADS) { best[i] = 0xFFFFFFFFu; suma[i] = 0; }
+    for (int i = tid; i < S::NB * S::RB; i += S::THREADS) { best[i] = 0xFFFFFFFFu; suma[i] = 0; }
     for (int i = tid; i < SIDE * SIDE; i += S::THREADS) rk[i] = sl.rank_of[i];
     __syncthreads();
     const uint8_t* yp = LEVEL != 2 ? nullptr
                       : g.fmt == FVV_RGB8 ? cplane<uint8_t>(ws, P, P.luma[d], pair)
                                           : (d ? pt.right[pair] : pt.left[pair]);
     const bool yal = (reinterpret_cast<uintptr_t>(yp) & 7) == 0;  // w % 8 == 0: every row 8-aligned
-    for (int i = tid; i < 8 * S::NBY * 8; i += S::THREADS) {       // (row, block column)
+    for (int i = tid; i < 8 * S::NBYT * 8; i += S::THREADS) {      // (row, block column)
         const int kx = i & 7, yy = i >> 3;
         const int gy = by0 * 8 + yy, gx = (bx0 + kx) * 8;
         uint4 v = make_uint4(0, 0, 0, 0);
@@ -1551,23 +1555,27 @@ k_sadw(Geometry g, PairTable pt, uint8_t* __restrict__ ws, Planes P, SadWLaunch 
     const int gq = tid / S::TPG, rest = tid - gq * S::TPG;      // dx group is warp-uniform
     const int kb = rest % S::NB, iy = rest / S::NB;
     const int kx = kb & 7, ky = kb >> 3;
-    const bool active = iy < SIDE && bx0 + kx < sl.bx_end && by0 + ky < L.nby;
-    if (active) {
-        const int rows = min(8, h - (by0 + ky) * 8);
-        const uint32_t* Rb = Rs + (ky * 8) * 32 + 4 * kx;
-        const uint32_t* Tb = Ts + (ky * 8 + iy) * S::TWW + 4 * kx;
-        const int sa = suma[kb];
-        const int16_t* rki = rk + iy * SIDE;
-        uint32_t mine;
-        if (S::NG == 1 || gq == 0) mine = sadw_group<SIDE, CG, 0>(Rb, Tb, rows, sa, rki);
-        else mine = sadw_group<SIDE, CG, (S::NG > 1 ? 1 : 0)>(Rb, Tb, rows, sa, rki);
-        atomicMin(&best[kb], mine);
+#pragma unroll 1
+    for (int rb = 0; rb < S::RB; rb++) {
+        const int kyr = ky + rb * S::NBY, kbr = kb + rb * S::NB;    // block row / slot of this pass
+        const bool active = iy < SIDE && bx0 + kx < sl.bx_end && by0 + kyr < L.nby;
+        if (active) {
+            const int rows = min(8, h - (by0 + kyr) * 8);
+            const uint32_t* Rb = Rs + (kyr * 8) * 32 + 4 * kx;
+            const uint32_t* Tb = Ts + (kyr * 8 + iy) * S::TWW + 4 * kx;
+            const int sa = suma[kbr];
+            const int16_t* rki = rk + iy * SIDE;
+            uint32_t mine;
+            if (S::NG == 1 || gq == 0) mine = sadw_group<SIDE, CG, 0>(Rb, Tb, rows, sa, rki);
+            else mine = sadw_group<SIDE, CG, (S::NG > 1 ? 1 : 0)>(Rb, Tb, rows, sa, rki);
+            atomicMin(&best[kbr], mine);
+        }
     }
     __syncthreads();
-    if (tid < S::NB) {
-        const int hx = bx0 + (tid & 7), hy = by0 + (tid >> 3);
+    for (int i = tid; i < S::NB * S::RB; i += S::THREADS) {
+        const int hx = bx0 + (i & 7), hy = by0 + (i >> 3);
         if (hx < sl.bx_end && hy < L.nby) {
-            const uint32_t key = best[tid];
+            const uint32_t key = best[i];
             const int idx = sl.cand_of_rank[key & 1023u];
             BlockHit hit;
             hit.dy = (int16_t)(idx / SIDE - S::R);
@@ -1588,7 +1596,7 @@ static cudaError_t launch_sadw(const Geometry& g, const PairTable& pt, uint8_t* 
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
         if (e != cudaSuccess) return e;
     }
-    dim3 grid((sl.bx_end + 7) / 8, (L.nby + S::NBY - 1) / S::NBY, 2 * npairs);
+    dim3 grid((sl.bx_end + 7) / 8, (L.nby + S::NBYT - 1) / S::NBYT, 2 * npairs);
     kern<<<grid, S::THREADS, S::SMEM, st>>>(g, pt, ws, P, sl);
     return cudaGetLastError();
 }
