@@ -1374,7 +1374,13 @@ struct SadW {
     static constexpr int TWW = WW / 2;                     // words per window row
     // each thread searches RB blocks stacked vertically (NBY block rows apart):
     // setup, rank table and the window apron are shared by twice the work
-    static constexpr int RB = SIDE <= 9 ? 2 : 1;
+#ifndef FVV_SADW_RB5
+#define FVV_SADW_RB5 3
+#endif
+#ifndef FVV_SADW_RB9
+#define FVV_SADW_RB9 4
+#endif
+    static constexpr int RB = SIDE <= 5 ? FVV_SADW_RB5 : (SIDE <= 9 ? FVV_SADW_RB9 : 1);
     static constexpr int NBYT = NBY * RB;                  // block rows per CTA
     static constexpr int WH = 8 * NBYT + 2 * R;            // window rows
     static constexpr size_t SMEM = (size_t)WH * TWW * 4 + (size_t)8 * NBYT * 32 * 4 +
