@@ -1380,7 +1380,10 @@ struct SadW {
 #ifndef FVV_SADW_RB9
 #define FVV_SADW_RB9 4
 #endif
-    static constexpr int RB = SIDE <= 5 ? FVV_SADW_RB5 : (SIDE <= 9 ? FVV_SADW_RB9 : 1);
+#ifndef FVV_SADW_RB25
+#define FVV_SADW_RB25 4
+#endif
+    static constexpr int RB = SIDE <= 5 ? FVV_SADW_RB5 : (SIDE <= 9 ? FVV_SADW_RB9 : (SIDE == 25 ? FVV_SADW_RB25 : 1));
     static constexpr int NBYT = NBY * RB;                  // block rows per CTA
     static constexpr int WH = 8 * NBYT + 2 * R;            // window rows
     static constexpr size_t SMEM = (size_t)WH * TWW * 4 + (size_t)8 * NBYT * 32 * 4 +
