@@ -1358,7 +1358,7 @@ __global__ void __launch_bounds__(128, FVV_MINB_BLEND) k_blend(Geometry g, PairT
 #else
 #define FVV_DBG_ALIGN(p, a) ((void)0)
 #endif
-template <int SIDE, int CG>
+template <int SIDE, int CG, int RB_ = 0>
 struct SadW {
     static constexpr int R = SIDE / 2;
     static constexpr int NG = (SIDE + CG - 1) / CG;        // dx groups per dy row
@@ -1383,7 +1383,8 @@ struct SadW {
 #ifndef FVV_SADW_RB25
 #define FVV_SADW_RB25 4
 #endif
-    static constexpr int RB = SIDE <= 5 ? FVV_SADW_RB5 : (SIDE <= 9 ? FVV_SADW_RB9 : (SIDE == 25 ? FVV_SADW_RB25 : 1));
+    static constexpr int RB = RB_ > 0 ? RB_
+                            : (SIDE <= 5 ? FVV_SADW_RB5 : (SIDE <= 9 ? FVV_SADW_RB9 : (SIDE == 25 ? FVV_SADW_RB25 : 1)));
     static constexpr int NBYT = NBY * RB;                  // block rows per CTA
     static constexpr int WH = 8 * NBYT + 2 * R;            // window rows
     static constexpr size_t SMEM = (size_t)WH * TWW * 4 + (size_t)8 * NBYT * 32 * 4 +
@@ -1476,10 +1477,10 @@ __device__ __forceinline__ uint32_t sadw_group(const uint32_t* Rb, const uint32_
     return mine;
 }
 
-template <int LEVEL, int SIDE, int CG>
-__global__ void __launch_bounds__(SadW<SIDE, CG>::THREADS, FVV_MINB_SADW(SIDE))
+template <int LEVEL, int SIDE, int CG, int RB_>
+__global__ void __launch_bounds__(SadW<SIDE, CG, RB_>::THREADS, FVV_MINB_SADW(SIDE))
 k_sadw(Geometry g, PairTable pt, uint8_t* __restrict__ ws, Planes P, SadWLaunch sl) {
-    using S = SadW<SIDE, CG>;
+    using S = SadW<SIDE, CG, RB_>;
     static_assert(S::NG == 1 || CG % 2 == 0, "dx groups need an even width");
     extern __shared__ __align__(16) uint8_t smem[];
     uint32_t* Ts = reinterpret_cast<uint32_t*>(smem);              // WH x TWW raw words
@@ -1595,12 +1596,12 @@ k_sadw(Geometry g, PairTable pt, uint8_t* __restrict__ ws, Planes P, SadWLaunch 
     }
 }
 
-template <int LEVEL, int SIDE, int CG>
-static cudaError_t launch_sadw(const Geometry& g, const PairTable& pt, uint8_t* ws, const Planes& P,
-                               SadWLaunch sl, int npairs, cudaStream_t st) {
-    using S = SadW<SIDE, CG>;
+template <int LEVEL, int SIDE, int CG, int RB_>
+static cudaError_t launch_sadw_rb(const Geometry& g, const PairTable& pt, uint8_t* ws, const Planes& P,
+                                  SadWLaunch sl, int npairs, cudaStream_t st) {
+    using S = SadW<SIDE, CG, RB_>;
     const Level& L = g.lv[LEVEL];
-    auto kern = k_sadw<LEVEL, SIDE, CG>;
+    auto kern = k_sadw<LEVEL, SIDE, CG, RB_>;
     if (S::SMEM > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
         if (e != cudaSuccess) return e;
@@ -1608,6 +1609,18 @@ static cudaError_t launch_sadw(const Geometry& g, const PairTable& pt, uint8_t* 
     dim3 grid((sl.bx_end + 7) / 8, (L.nby + S::NBYT - 1) / S::NBYT, 2 * npairs);
     kern<<<grid, S::THREADS, S::SMEM, st>>>(g, pt, ws, P, sl);
     return cudaGetLastError();
+}
+
+// Stacked blocks per thread (RB) trade parallelism for amortised setup: small
+// launches (fewer than two CTAs per SM with stacking) take RB = 1.
+template <int LEVEL, int SIDE, int CG>
+static cudaError_t launch_sadw(const Geometry& g, const PairTable& pt, uint8_t* ws, const Planes& P,
+                               SadWLaunch sl, int npairs, cudaStream_t st) {
+    using S = SadW<SIDE, CG>;
+    const Level& L = g.lv[LEVEL];
+    const long ctas = (long)((sl.bx_end + 7) / 8) * ((L.nby + S::NBYT - 1) / S::NBYT) * 2 * npairs;
+    if (S::RB > 1 && ctas < 2 * 148) return launch_sadw_rb<LEVEL, SIDE, CG, 1>(g, pt, ws, P, sl, npairs, st);
+    return launch_sadw_rb<LEVEL, SIDE, CG, S::RB>(g, pt, ws, P, sl, npairs, st);
 }
 
 template <int LEVEL, int KP, bool FULL8>
