@@ -112,13 +112,16 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 // lane 0 issues the MMAs of tile i into TMEM accumulator i % 2; warps 2-5 drain
 // accumulator (i - 1) % 2 meanwhile (tcgen05.ld, bias, ReLU, stores) -- the
 // epilogue of one tile overlaps the MMAs of the next.
+// MT output rows per tile (MT accumulators of 128 x NT per buffer) share each
+// weight chunk; MT = 2 whenever two double-buffered sets fit TMEM (NT <= 128).
 template <int NT, int SW>
 struct ConvTile {
+    static constexpr int MT = NT <= 128 ? 2 : 1;
     static constexpr int kABytes = 128 * SW;                 // one 128-pixel row segment
     static constexpr int kBBytes = NT * SW;
-    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kStageBytes = MT * kABytes + kBBytes;
     static constexpr int kStages = kStageBytes > 40 * 1024 ? 4 : 6;
-    static constexpr int kTmemCols = 2 * NT < 32 ? 32 : 2 * NT;  // two accumulators, power of two >= 32
+    static constexpr int kTmemCols = 2 * MT * NT < 32 ? 32 : 2 * MT * NT;  // two accumulator sets
     static constexpr size_t kSmem = 1024 /* alignment slack */ + (size_t)kStages * kStageBytes + 256;
 };
 constexpr int kConvThreads = 192;
@@ -126,14 +129,15 @@ constexpr int kConvThreads = 192;
 struct TileCoord {
     int b, gy, gx0, n0;
 };
-__device__ __forceinline__ TileCoord tile_of(int t, const ConvTCParams& p, int ntx, int nn, int NT) {
+__device__ __forceinline__ TileCoord tile_of(int t, const ConvTCParams& p, int ntx, int nn, int NT, int MT) {
     TileCoord c;
     const int tn = t % nn;
     t /= nn;
     const int tx = t % ntx;
     t /= ntx;
-    c.gy = t % p.Hg;
-    c.b = t / p.Hg;
+    const int nty = (p.Hg + MT - 1) / MT;
+    c.gy = (t % nty) * MT;
+    c.b = t / nty;
     c.gx0 = tx * 128;
     c.n0 = tn * NT;
     return c;
@@ -156,7 +160,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntx = (p.Wg + 127) / 128, nn = (p.N + NT - 1) / NT;
-    const int ntiles = ntx * nn * p.Hg * p.B;
+    constexpr int MT = T::MT;
+    const int ntiles = ntx * nn * ((p.Hg + MT - 1) / MT) * p.B;
     const int nk = p.ntaps * p.kc_per_tap;
 
     if (threadIdx.x == 0) {
@@ -188,7 +193,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             // ---- TMA producer ----
             int kg = 0;  // global K-chunk counter (stage / phase continue across tiles)
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-                const TileCoord c = tile_of(t, p, ntx, nn, NT);
+                const TileCoord c = tile_of(t, p, ntx, nn, NT, MT);
                 const int ix0 = c.gx0 * p.sx + p.bx0, iy0 = c.gy * p.sy + p.by0;
                 for (int kc = 0; kc < nk; kc++, kg++) {
                     const int s = kg % S;
@@ -196,8 +201,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                     const int tap = kc / p.kc_per_tap, c0 = (kc - tap * p.kc_per_tap) * (SW / 2);
                     uint8_t* sa = smem + s * T::kStageBytes;
                     mbar_expect_tx(&full[s], T::kStageBytes);
-                    tma_load_4d(sa, &tmA, &full[s], c0, ix0 + p.tdx[tap], iy0 + p.tdy[tap], c.b);
-                    tma_load_2d(sa + T::kABytes, &tmB, &full[s], tap * p.cpad + c0, p.wrow0 + c.n0);
+#pragma unroll
+                    for (int r = 0; r < MT; r++)  // rows past Hg load real or zero rows; the epilogue skips them
+                        tma_load_4d(sa + r * T::kABytes, &tmA, &full[s], c0, ix0 + p.tdx[tap],
+                                    iy0 + r * p.sy + p.tdy[tap], c.b);
+                    tma_load_2d(sa + MT * T::kABytes, &tmB, &full[s], tap * p.cpad + c0, p.wrow0 + c.n0);
                 }
             }
         }
@@ -211,16 +219,20 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                 const int acc = i & 1;
                 if (i >= 2) mbar_wait(&tempty[acc], ((i >> 1) - 1) & 1);  // drained by the epilogue
                 asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-                const uint32_t td = tmem + acc * NT;
+                const uint32_t td = tmem + acc * MT * NT;
                 for (int kc = 0; kc < nk; kc++, kg++) {
                     const int s = kg % S;
                     mbar_wait(&full[s], (kg / S) & 1);
                     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-                    const uint32_t sa = smem_u32(smem + s * T::kStageBytes), sb = sa + T::kABytes;
+                    const uint32_t sa = smem_u32(smem + s * T::kStageBytes), sb = sa + MT * T::kABytes;
 #pragma unroll
-                    for (int k = 0; k < SW / 32; k++)
-                        umma_bf16(td, umma_desc<SW>(sa + 32 * k), umma_desc<SW>(sb + 32 * k), idesc,
-                                  (kc > 0 || k > 0) ? 1u : 0u);
+                    for (int k = 0; k < SW / 32; k++) {
+                        const uint64_t db = umma_desc<SW>(sb + 32 * k);
+#pragma unroll
+                        for (int r = 0; r < MT; r++)
+                            umma_bf16(td + r * NT, umma_desc<SW>(sa + r * T::kABytes + 32 * k), db, idesc,
+                                      (kc > 0 || k > 0) ? 1u : 0u);
+                    }
                     umma_commit(&empty[s]);  // frees the stage once these MMAs have read it
                 }
                 umma_commit(&tfull[acc]);
@@ -233,19 +245,22 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         constexpr int CW = NT < 32 ? NT : 32;  // columns per tcgen05.ld
         int i = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, i++) {
-            const TileCoord c = tile_of(t, p, ntx, nn, NT);
+            const TileCoord c0t = tile_of(t, p, ntx, nn, NT, MT);
             const int acc = i & 1;
             mbar_wait(&tfull[acc], (i >> 1) & 1);
             __syncwarp();
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-            const int gx = c.gx0 + row;
-            const bool valid = gx < p.Wg;
-            const int oy = c.gy * p.omy + p.oay, ox = gx * p.omx + p.oax;
-            const size_t obase = (((size_t)c.b * p.Hout + oy) * p.Wout + ox) * p.ostride + p.ocoff;
+            const int gx = c0t.gx0 + row;
 #pragma unroll 1
-            for (int cc = 0; cc < NT; cc += CW) {
+            for (int ccm = 0; ccm < MT * NT; ccm += CW) {
+                const int sub = ccm / NT, cc = ccm - sub * NT;
+                TileCoord c = c0t;
+                c.gy += sub;
+                const bool valid = gx < p.Wg && c.gy < p.Hg;
+                const int oy = c.gy * p.omy + p.oay, ox = gx * p.omx + p.oax;
+                const size_t obase = (((size_t)c.b * p.Hout + oy) * p.Wout + ox) * p.ostride + p.ocoff;
                 uint32_t r[32];
-                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + acc * NT + cc;
+                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + acc * MT * NT + ccm;
                 if (CW == 32) {
                     asm volatile(
                         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
@@ -390,7 +405,7 @@ static cudaError_t launch_nt_sw(const CUtensorMap& a, const CUtensorMap& w, cons
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     }
-    const int tiles = (p.Wg + 127) / 128 * p.Hg * p.B * ((p.N + NT - 1) / NT);
+    const int tiles = (p.Wg + 127) / 128 * ((p.Hg + T::MT - 1) / T::MT) * p.B * ((p.N + NT - 1) / NT);
     kern<<<tiles < nsm ? tiles : nsm, kConvThreads, T::kSmem, st>>>(a, w, bias, out, p);
     return cudaGetLastError();
 }
