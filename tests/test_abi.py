@@ -77,3 +77,24 @@ def test_product_path_refuses_without_gpu():
     img = fv.gray(np.zeros((8, 8), np.uint8))
     with pytest.raises(RuntimeError, match="CUDA"):
         fv.interpolate(img, img)
+
+
+def test_vinet_entry_points_validate_on_the_host():
+    """The CNN-path entry points reject bad arguments before touching the device."""
+    L = _lib.load()
+    from paper_2112_10603_b200 import vinet  # declares the VINet signatures
+    vinet._sig(L)
+    d = _lib.desc(1920, 1080, 1)
+    s1 = L.fvv_vinet_workspace_size(ctypes.byref(d), 1)
+    s2 = L.fvv_vinet_workspace_size(ctypes.byref(d), 2)
+    assert s1 > 0 and s2 > 1.9 * s1
+    small = _lib.desc(32, 32, 1)  # below the 64-px minimum of the 64-aligned canvas
+    assert L.fvv_vinet_workspace_size(ctypes.byref(small), 1) == 0
+    conv = _lib.ConvDesc(1, 8, 8, 24, 8, 8, 128, 0, 128, 3, 1, 1, 0, 1, 0, 128)  # in_cpad 24: unsupported
+    assert L.fvv_conv2d_bf16(ctypes.byref(conv), 1, 1, 1, 1, None) == _lib.FVV_EUNSUPPORTED
+    conv = _lib.ConvDesc(1, 8, 8, 64, 8, 8, 128, 0, 128, 3, 1, 1, 0, 1, 0, 48)   # ntile 48: invalid
+    assert L.fvv_conv2d_bf16(ctypes.byref(conv), 1, 1, 1, 1, None) == _lib.FVV_EINVAL
+    conv = _lib.ConvDesc(1, 8, 8, 64, 5, 5, 128, 0, 128, 3, 1, 1, 0, 1, 0, 128)  # wrong output size
+    assert L.fvv_conv2d_bf16(ctypes.byref(conv), 1, 1, 1, 1, None) == _lib.FVV_EINVAL
+    conv = _lib.ConvDesc(1, 8, 8, 64, 16, 16, 128, 0, 128, 3, 2, 1, 1, 1, 0, 128)  # transposed must be k4 s2 p1
+    assert L.fvv_conv2d_bf16(ctypes.byref(conv), 1, 1, 1, 1, None) == _lib.FVV_EUNSUPPORTED
