@@ -1481,7 +1481,6 @@ template <int LEVEL, int SIDE, int CG, int RB_>
 __global__ void __launch_bounds__(SadW<SIDE, CG, RB_>::THREADS, FVV_MINB_SADW(SIDE))
 k_sadw(Geometry g, PairTable pt, uint8_t* __restrict__ ws, Planes P, SadWLaunch sl) {
     using S = SadW<SIDE, CG, RB_>;
-    static_assert(S::NG == 1 || CG % 2 == 0, "dx groups need an even width");
     extern __shared__ __align__(16) uint8_t smem[];
     uint32_t* Ts = reinterpret_cast<uint32_t*>(smem);              // WH x TWW raw words
     uint32_t* Rs = Ts + S::WH * S::TWW;                            // 8*NBYT x 32 pair words
@@ -1726,7 +1725,7 @@ static cudaError_t run_sad(const Geometry& g, const PairTable& pt, uint8_t* ws, 
             case 9: return launch_sadw<LEVEL, 9, 9>(g, pt, ws, P, sw, npairs, st);
             case 13: return launch_sadw<LEVEL, 13, 13>(g, pt, ws, P, sw, npairs, st);
             case 17: return launch_sadw<LEVEL, 17, 17>(g, pt, ws, P, sw, npairs, st);
-            default: return launch_sadw<LEVEL, 25, 14>(g, pt, ws, P, sw, npairs, st);
+            default: return launch_sadw<LEVEL, 25, 13>(g, pt, ws, P, sw, npairs, st);
         }
     }
     if (pix) {
