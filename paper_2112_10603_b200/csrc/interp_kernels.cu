@@ -1135,6 +1135,30 @@ __global__ void __launch_bounds__(kCR) k_scan_carry(Geometry g, const uint8_t* _
         double cv[kCC / 8];   // this chunk's carries: one 64-byte row segment per lane
 #pragma unroll
         for (int i = 0; i < kCC / 8; i++) cv[i] = 0.0;
+        if (n == kCC && c0 > 0) {
+            // full interior chunk: no data-dependent exits, so the D0 work of every
+            // group is free to be scheduled ahead of the ordered DADD chain
+#pragma unroll
+            for (int c8 = 0; c8 < kCC; c8 += 8) {
+                const int x0 = c0 + c8;
+                double e[11];                       // e[i] = D0(sd[clamp(x0 - 2 + i)])
+                e[0] = ep[0]; e[1] = ep[1]; e[2] = ep[2];
+                {
+                    const uint2 qa = *reinterpret_cast<const uint2*>(tl + c8 + 8);   // sd[x0 .. x0+3]
+                    const uint2 qb = *reinterpret_cast<const uint2*>(tl + c8 + 12);  // sd[x0+4 .. x0+7]
+                    const uint2 qc = *reinterpret_cast<const uint2*>(tl + c8 + 16);  // sd[x0+8 .. x0+11]
+                    e[3] = d0_of(qa.x >> 16);    e[4] = d0_of(qa.y & 0xFFFF); e[5] = d0_of(qa.y >> 16);
+                    e[6] = d0_of(qb.x & 0xFFFF); e[7] = d0_of(qb.x >> 16);    e[8] = d0_of(qb.y & 0xFFFF);
+                    e[9] = d0_of(qb.y >> 16);    e[10] = d0_of(qc.x & 0xFFFF);
+                }
+                ep[0] = e[8]; ep[1] = e[9]; ep[2] = e[10];
+                (void)x0;
+                tmp = __dadd_rn(tmp, __dsub_rn(e[3], e[0]));
+                cv[c8 >> 3] = tmp;
+#pragma unroll
+                for (int j = 1; j < 8; j++) tmp = __dadd_rn(tmp, __dsub_rn(e[j + 3], e[j]));
+            }
+        } else {
 #pragma unroll
         for (int c8 = 0; c8 < kCC; c8 += 8) {
             if (c8 >= n) break;
@@ -1173,6 +1197,7 @@ __global__ void __launch_bounds__(kCR) k_scan_carry(Geometry g, const uint8_t* _
                 for (int j = 1; j < 8; j++)
                     if (j < m) tmp = __dadd_rn(tmp, __dsub_rn(e[j + 3], e[j]));
             }
+        }
         }
         if (live) {
             const int ngc = (n + 7) / 8;
