@@ -39,7 +39,7 @@ def _pair(w, h, fmt, shift, seed):
     return pack(a), pack(b)
 
 
-CASES = [(448, 256, 2, 3), (256, 192, 1, 4), (192, 128, 0, -2)]
+CASES = [(448, 256, 2, 3), (256, 192, 1, 4), (192, 128, 0, -2), (200, 124, 1, 5)]  # last: canvas padding
 
 
 @pytest.fixture(scope="module")
