@@ -206,6 +206,17 @@ int fvv_vinet_synth(const fvv_frame_desc* desc, const uint8_t* const* left, cons
 int fvv_vinet_rig(const fvv_frame_desc* desc, const fvv_vinet_weights* weights, const uint8_t* cams, int ncams,
                   int stages, uint8_t* views, void* workspace, size_t workspace_bytes, void* stream);
 
+/* fvv_vinet_rig followed by fvv_rig_clusters in one call, with the cluster
+ * tiling fused into the synthesis epilogue: each direct-t view's 4x4 box-mean
+ * quarter tiles are written into the cluster frames straight from the
+ * synthesis kernel (no re-read of the views); a reduced cluster pass adds the
+ * anchors and padding.  `views` and `clusters` are byte-identical to the
+ * two-call path (PipelineHandle.process_frame + _stitch, server/pipeline.py:
+ * 199-292).  At most 8192 global views per rig frame. */
+int fvv_vinet_rig_clusters(const fvv_frame_desc* desc, const fvv_vinet_weights* weights, const uint8_t* cams,
+                           int ncams, int stages, int views_per_side, uint8_t* views, uint8_t* clusters,
+                           void* workspace, size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

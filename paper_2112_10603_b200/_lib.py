@@ -23,7 +23,7 @@ EXPORTS = (
     "fvv_assemble_cluster", "fvv_rig_cluster_bytes", "fvv_rig_clusters",
     "fvv_profile_enable", "fvv_profile_read", "fvv_kernel_class_name",
     "fvv_interp_level_diagnostics", "fvv_conv2d_bf16", "fvv_vinet_workspace_size", "fvv_vinet_flow",
-    "fvv_vinet_synth", "fvv_vinet_rig",
+    "fvv_vinet_synth", "fvv_vinet_rig", "fvv_vinet_rig_clusters",
 )
 
 

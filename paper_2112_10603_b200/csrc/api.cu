@@ -30,7 +30,7 @@ cudaError_t launch_assemble(int W, int H, int fmt, const uint8_t* anchor,
                             cudaStream_t st);
 cudaError_t launch_rig_clusters(int W, int H, int fmt, const ClusterJob* jobs, int njobs,
                                 long max_cluster_bytes, const uint8_t* views, uint8_t* out,
-                                cudaStream_t st);
+                                cudaStream_t st, int skip_period = 0);
 }  // namespace fvv
 
 using namespace fvv;
@@ -513,8 +513,12 @@ size_t fvv_rig_cluster_bytes(const fvv_frame_desc* d, int ncams, int stages, int
     return fvv_frame_bytes(&s);
 }
 
-int fvv_rig_clusters(const fvv_frame_desc* d, int ncams, int stages, int vps,
-                     const uint8_t* views, uint8_t* clusters, void* stream) {
+}  // extern "C"
+
+// Validates a rig clustering request (PipelineHandle._stitch, server/pipeline.py:273-292)
+// and, when `jobs` is given, lays out one ClusterJob per camera.
+static int cluster_jobs_of(const fvv_frame_desc* d, int ncams, int stages, int vps, std::vector<ClusterJob>* jobs,
+                           long* maxb) {
     int rc = check_desc(d);
     if (rc) return rc;
     if (ncams < 2) return fail(FVV_EINVAL, "need at least 2 cameras");
@@ -527,12 +531,14 @@ int fvv_rig_clusters(const fvv_frame_desc* d, int ncams, int stages, int vps,
     if (d->format == FVV_RGB8) return fail(FVV_ELAYOUT, "cluster frames are gray or 4:2:0");
     if (d->width % 8 || d->height % 8)
         return fail(FVV_ELAYOUT, "anchor dimensions must be divisible by 8");
-    std::vector<ClusterJob> jobs(ncams);
-    long off = 0, maxb = 0;
+    if (!jobs) return FVV_OK;
+    jobs->assign(ncams, ClusterJob{});
+    long off = 0;
+    *maxb = 0;
     for (int c = 0; c < ncams; c++) {
         int lo, hi;
         layout_of(ncams, stages, vps, c, &lo, &hi);
-        ClusterJob& j = jobs[c];
+        ClusterJob& j = (*jobs)[c];
         j.anchor_view = c << stages;
         j.first_small = lo;
         j.nsmall = hi - lo;
@@ -541,8 +547,19 @@ int fvv_rig_clusters(const fvv_frame_desc* d, int ncams, int stages, int vps,
         j.out_offset = off;
         const long b = (long)fvv_rig_cluster_bytes(d, ncams, stages, vps, c);
         off += b;
-        maxb = std::max(maxb, b);
+        *maxb = std::max(*maxb, b);
     }
+    return FVV_OK;
+}
+
+extern "C" {
+
+int fvv_rig_clusters(const fvv_frame_desc* d, int ncams, int stages, int vps,
+                     const uint8_t* views, uint8_t* clusters, void* stream) {
+    std::vector<ClusterJob> jobs;
+    long maxb = 0;
+    int rc = cluster_jobs_of(d, ncams, stages, vps, &jobs, &maxb);
+    if (rc) return rc;
     cudaError_t ce = launch_rig_clusters(d->width, d->height, d->format, jobs.data(), ncams, maxb,
                                          views, clusters, static_cast<cudaStream_t>(stream));
     if (ce != cudaSuccess) return cuda_fail(ce, "rig_clusters");
@@ -690,22 +707,19 @@ extern "C" int fvv_vinet_synth(const fvv_frame_desc* d, const uint8_t* const* le
     return FVV_OK;
 }
 
-extern "C" int fvv_vinet_rig(const fvv_frame_desc* d, const fvv_vinet_weights* wts, const uint8_t* cams, int ncams,
-                             int stages, uint8_t* views, void* ws, size_t ws_bytes, void* stream) {
-    int rc;
-    if ((rc = vin_check_desc(d))) return rc;
-    if (!wts || !cams || !views || !ws) return fail(FVV_EINVAL, "null argument");
-    if (ncams < 2) return fail(FVV_EINVAL, "a rig needs at least two cameras");
-    if (stages < 1 || stages > 6) return fail(FVV_EINVAL, "stages must be in [1, 6]");
+// camera anchors + per-chunk flows and direct-t views of a rig frame; with
+// `tab` the synthesis also writes the views' quarter tiles into `clusters`.
+static int vin_rig_run(const fvv_frame_desc* d, const fvv_vinet_weights* wts, const uint8_t* cams, int ncams,
+                       int stages, uint8_t* views, void* ws, size_t ws_bytes, cudaStream_t st, const char* who,
+                       const VinTileDst* tab, uint8_t* clusters) {
     fvv_frame_desc dd = *d;
     const size_t fb = fvv_frame_bytes(&dd);
     const int nv = (1 << stages) - 1, npairs = ncams - 1;
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
     // anchors: camera c lands at global view index c * 2^stages (ViewIndexModel, viewmodel.py:23-71)
     for (int c = 0; c < ncams; c++) {
         cudaError_t e = cudaMemcpyAsync(views + (size_t)c * (nv + 1) * fb, cams + (size_t)c * fb, fb,
                                         cudaMemcpyDeviceToDevice, st);
-        if (e != cudaSuccess) return cuda_fail(e, "fvv_vinet_rig");
+        if (e != cudaSuccess) return cuda_fail(e, who);
     }
     int B = std::min(npairs, kVinMaxPairs);
     while (B > 1 && vin_layout(d->width, d->height, B).bytes > ws_bytes) B--;
@@ -726,12 +740,66 @@ extern "C" int fvv_vinet_rig(const fvv_frame_desc* d, const fvv_vinet_weights* w
             pp.right[i] = cams + (size_t)(p0 + i + 1) * fb;
         }
         float* fl = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + L.flows);
+        uint8_t* vout = views + ((size_t)p0 * (nv + 1) + 1) * fb;
         cudaError_t e = vin_flows(L, vw, pp, d->format, static_cast<uint8_t*>(ws), fl, nullptr, st);
-        if (e == cudaSuccess)
-            e = vin_synth(pp, n, fl, d->format, d->width, d->height, nv, views + ((size_t)p0 * (nv + 1) + 1) * fb, fb,
-                          (size_t)(nv + 1) * fb, st);
-        if (e != cudaSuccess) return cuda_fail(e, "fvv_vinet_rig");
+        if (e == cudaSuccess) {
+            if (tab)
+                e = vin_synth_tiled(pp, n, fl, d->format, d->width, d->height, nv, vout, fb, (size_t)(nv + 1) * fb,
+                                    tab, p0 * (nv + 1), nv + 1, clusters, st);
+            else
+                e = vin_synth(pp, n, fl, d->format, d->width, d->height, nv, vout, fb, (size_t)(nv + 1) * fb, st);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, who);
     }
     return FVV_OK;
 }
 
+extern "C" int fvv_vinet_rig(const fvv_frame_desc* d, const fvv_vinet_weights* wts, const uint8_t* cams, int ncams,
+                             int stages, uint8_t* views, void* ws, size_t ws_bytes, void* stream) {
+    int rc;
+    if ((rc = vin_check_desc(d))) return rc;
+    if (!wts || !cams || !views || !ws) return fail(FVV_EINVAL, "null argument");
+    if (ncams < 2) return fail(FVV_EINVAL, "a rig needs at least two cameras");
+    if (stages < 1 || stages > 6) return fail(FVV_EINVAL, "stages must be in [1, 6]");
+    return vin_rig_run(d, wts, cams, ncams, stages, views, ws, ws_bytes, static_cast<cudaStream_t>(stream),
+                       "fvv_vinet_rig", nullptr, nullptr);
+}
+
+extern "C" int fvv_vinet_rig_clusters(const fvv_frame_desc* d, const fvv_vinet_weights* wts, const uint8_t* cams,
+                                      int ncams, int stages, int vps, uint8_t* views, uint8_t* clusters, void* ws,
+                                      size_t ws_bytes, void* stream) {
+    int rc;
+    if ((rc = vin_check_desc(d))) return rc;
+    if (!wts || !cams || !views || !clusters || !ws) return fail(FVV_EINVAL, "null argument");
+    if (ncams < 2) return fail(FVV_EINVAL, "a rig needs at least two cameras");
+    if (stages < 1 || stages > 6) return fail(FVV_EINVAL, "stages must be in [1, 6]");
+    if ((rc = cluster_jobs_of(d, ncams, stages, vps, nullptr, nullptr))) return rc;
+    const int total = ((ncams - 1) << stages) + 1;
+    if (total > kVinMaxViews)
+        return fail(FVV_EINVAL, "fused tiling supports at most " + std::to_string(kVinMaxViews) + " views per rig frame");
+    std::vector<ClusterJob> jobs;
+    long maxb = 0;
+    cluster_jobs_of(d, ncams, stages, vps, &jobs, &maxb);
+    // the tile table lives in the workspace: size it for the largest chunk that fits
+    int B = std::min(ncams - 1, kVinMaxPairs);
+    while (B > 1 && vin_layout(d->width, d->height, B).bytes > ws_bytes) B--;
+    const VinLayout L = vin_layout(d->width, d->height, B);
+    if (L.bytes > ws_bytes) return fail(FVV_EINVAL, "workspace too small for one pair");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    VinTileDst* tab = reinterpret_cast<VinTileDst*>(static_cast<uint8_t*>(ws) + L.tiles);
+    cudaError_t e = cudaMemsetAsync(tab, 0xFF, (size_t)2 * total * sizeof(VinTileDst), st);
+    for (size_t b = 0; b < jobs.size() && e == cudaSuccess; b += kMaxClusters) {
+        ClusterJobs cj;
+        const int n = (int)std::min<size_t>(kMaxClusters, jobs.size() - b);
+        for (int k = 0; k < n; k++) cj.job[k] = jobs[b + k];
+        e = vin_tile_table(cj, n, total, tab, st);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "fvv_vinet_rig_clusters");
+    if ((rc = vin_rig_run(d, wts, cams, ncams, stages, views, ws, ws_bytes, st, "fvv_vinet_rig_clusters", tab,
+                          clusters)))
+        return rc;
+    e = launch_rig_clusters(d->width, d->height, d->format, jobs.data(), ncams, maxb, views, clusters, st,
+                            1 << stages);
+    if (e != cudaSuccess) return cuda_fail(e, "fvv_vinet_rig_clusters");
+    return FVV_OK;
+}

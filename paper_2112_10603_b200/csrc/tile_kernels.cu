@@ -74,14 +74,13 @@ __global__ void k_downscale(FrameDims s, FrameDims q, int f, const uint8_t* __re
 }
 
 // --- cluster geometry (cluster.py:135-140, 143-191) -------------------------
-constexpr int kMaxClusters = 64;
-struct ClusterJobs {
-    ClusterJob job[kMaxClusters];
-};
+
 
 // Scalar form: one thread = one stitched byte (any geometry the reference accepts).
+// skip_period > 0: tiles of views whose index is not a multiple of skip_period
+// (the synthesized ones) were written by the synthesis kernel (fused tiling).
 __global__ void k_rig_clusters_1(FrameDims fd, ClusterJobs jobs, const uint8_t* __restrict__ views,
-                                 uint8_t* __restrict__ clusters) {
+                                 uint8_t* __restrict__ clusters, int skip_period) {
     const ClusterJob jb = jobs.job[blockIdx.z];
     const int sw = jb.sw, sh = fd.H;
     const long ysz = (long)sw * sh;
@@ -109,6 +108,7 @@ __global__ void k_rig_clusters_1(FrameDims fd, ClusterJobs jobs, const uint8_t* 
         } else {
             int vi = jb.first_small + i;
             if (vi >= jb.skip) vi += 1;
+            if (skip_period && vi % skip_period) return;
             const uint8_t* src = views + (long)vi * fd.bytes;
             const int tx = p ? x - (W + col * cellw) / 2 : x - (W + col * cellw);
             const int ty = p ? y - (row * cellh) / 2 : y - row * cellh;
@@ -129,7 +129,7 @@ __global__ void k_rig_clusters_1(FrameDims fd, ClusterJobs jobs, const uint8_t* 
 // every cell edge and source row is 16-byte aligned, so a group never
 // straddles a cell.
 __global__ void k_rig_clusters(FrameDims fd, ClusterJobs jobs, const uint8_t* __restrict__ views,
-                               uint8_t* __restrict__ clusters) {
+                               uint8_t* __restrict__ clusters, int skip_period) {
     const ClusterJob jb = jobs.job[blockIdx.z];
     const int sw = jb.sw, sh = fd.H;
     const long ysz = (long)sw * sh;
@@ -160,6 +160,7 @@ __global__ void k_rig_clusters(FrameDims fd, ClusterJobs jobs, const uint8_t* __
         } else {
             int vi = jb.first_small + i;
             if (vi >= jb.skip) vi += 1;
+            if (skip_period && vi % skip_period) return;
             const uint8_t* src = views + (long)vi * fd.bytes;
             const int tx = p ? x - (W + col * cellw) / 2 : x - (W + col * cellw);
             const int ty = p ? y - (row * cellh) / 2 : y - row * cellh;
@@ -247,7 +248,7 @@ cudaError_t launch_assemble(int W, int H, int fmt, const uint8_t* anchor,
 
 cudaError_t launch_rig_clusters(int W, int H, int fmt, const ClusterJob* jobs, int njobs,
                                 long max_cluster_bytes, const uint8_t* views, uint8_t* out,
-                                cudaStream_t st) {
+                                cudaStream_t st, int skip_period) {
     FrameDims fd = dims_of(W, H, fmt);
     for (int b = 0; b < njobs; b += kMaxClusters) {
         ClusterJobs cj;
@@ -255,10 +256,10 @@ cudaError_t launch_rig_clusters(int W, int H, int fmt, const ClusterJob* jobs, i
         for (int i = 0; i < n; i++) cj.job[i] = jobs[b + i];
         if (W % 32 == 0) {
             dim3 grd((unsigned)((max_cluster_bytes / 4 + 255) / 256), 1, n);
-            k_rig_clusters<<<grd, 256, 0, st>>>(fd, cj, views, out);
+            k_rig_clusters<<<grd, 256, 0, st>>>(fd, cj, views, out, skip_period);
         } else {
             dim3 grd((unsigned)((max_cluster_bytes + 255) / 256), 1, n);
-            k_rig_clusters_1<<<grd, 256, 0, st>>>(fd, cj, views, out);
+            k_rig_clusters_1<<<grd, 256, 0, st>>>(fd, cj, views, out, skip_period);
         }
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;

@@ -39,6 +39,8 @@ def _sig(L):
     L.fvv_vinet_synth.argtypes = [pd, PP, PP, P, I, I, P, P]
     L.fvv_vinet_rig.restype = I
     L.fvv_vinet_rig.argtypes = [pd, ctypes.POINTER(_Weights), P, I, I, P, P, Z, P]
+    L.fvv_vinet_rig_clusters.restype = I
+    L.fvv_vinet_rig_clusters.argtypes = [pd, ctypes.POINTER(_Weights), P, I, I, I, P, P, P, Z, P]
 
 
 class VINet:
@@ -130,3 +132,23 @@ class VINet:
                                          self._ws.numel(), self._stream()))
         return views
 
+
+    def rig_clusters(self, cams, stages: int, views_per_side: int = 16, views=None, out=None):
+        """rig + cluster.rig_clusters in one call with the tiling fused into the synthesis
+        (fvv_vinet_rig_clusters).  Returns (views, clusters, sizes); both buffers are
+        byte-identical to rig() followed by cluster.rig_clusters()."""
+        import torch
+        from .cluster import rig_cluster_sizes
+        C = cams.shape[0]
+        if cams.shape[1] != self.frame_bytes:
+            raise ValueError(f"cams must be (C, {self.frame_bytes}) uint8")
+        sizes = rig_cluster_sizes(self.width, self.height, self.format, C, stages, views_per_side)
+        if views is None:
+            views = torch.empty((((C - 1) << stages) + 1, self.frame_bytes), dtype=torch.uint8, device=self.device)
+        if out is None:
+            out = torch.empty(sum(sizes), dtype=torch.uint8, device=self.device)
+        _lib.check(self._L.fvv_vinet_rig_clusters(
+            ctypes.byref(self._desc), ctypes.byref(self._w), ctypes.c_void_p(cams.data_ptr()), C, int(stages),
+            int(views_per_side), ctypes.c_void_p(views.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+            ctypes.c_void_p(self._ws.data_ptr()), self._ws.numel(), self._stream()))
+        return views, out, sizes

@@ -121,3 +121,23 @@ def test_vinet_rig_layout(torch_cuda, params):
         assert torch.equal(views[c * (nv + 1)], cams[c])
     for c in range(C - 1):
         assert torch.equal(views[c * (nv + 1) + 1:c * (nv + 1) + 1 + nv], per_pair[c])
+
+
+@pytest.mark.parametrize("w,h,fmt,C,S,vps", [(192, 128, 1, 4, 2, 4), (200, 128, 0, 3, 3, 5),
+                                             (256, 192, 1, 5, 2, 1), (128, 64, 1, 3, 1, 2)])
+def test_vinet_rig_clusters_fused_tiling(torch_cuda, params, w, h, fmt, C, S, vps):
+    """fvv_vinet_rig_clusters (quarter tiles written by the synthesis epilogue) is
+    byte-identical to fvv_vinet_rig + fvv_rig_clusters (server/pipeline.py:199-292)."""
+    torch = torch_cuda
+    from paper_2112_10603_b200.cluster import rig_clusters
+    from paper_2112_10603_b200.vinet import VINet
+    frames = [_pair(w, h, fmt, 2 * c + 1, seed=50 + c)[0] for c in range(C)]
+    cams = torch.from_numpy(np.stack(frames)).cuda()
+    net = VINet(w, h, fmt, params=params, max_pairs=2)  # C - 1 > 2 pairs: several chunks
+    ref_views = net.rig(cams, S)
+    ref_cl, ref_sizes = rig_clusters(ref_views, w, h, fmt, C, S, vps)
+    views, cl, sizes = net.rig_clusters(cams, S, vps, out=torch.full_like(ref_cl, 77))
+    torch.cuda.synchronize()
+    assert sizes == ref_sizes
+    assert torch.equal(views, ref_views)
+    assert torch.equal(cl, ref_cl)
