@@ -821,7 +821,10 @@ __device__ __forceinline__ float third_f32(int sn, float scale) {
 #ifndef FVV_KMH
 #define FVV_KMH 64
 #endif
-constexpr int kMW = 28, kMWarps = 4, kMH = FVV_KMH;
+#ifndef FVV_MASK_UNROLL
+#define FVV_MASK_UNROLL 1
+#endif
+constexpr int kMW = 28, kMWarps = 4, kMH = FVV_KMH, kMaskUnroll = FVV_MASK_UNROLL;
 
 template <int FMT>
 __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geometry g, PairTable pt,
@@ -1016,6 +1019,7 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
     const int b0 = min(max(y0 + 2, 3), yo1), b1 = max(b0, yo1);  // interior rows [b0, b1)
     int yy = ys;
     for (; yy < b0; yy++) step(yy, std::true_type{});
+#pragma unroll kMaskUnroll
     for (; yy < b1; yy++) step(yy, std::false_type{});
     for (; yy <= ye; yy++) step(yy, std::true_type{});
     // ---- bottom edge: occ(H-1) (one-sided gy), O0/O(H-2), O0/O(H-1), Sd(H-1) ----

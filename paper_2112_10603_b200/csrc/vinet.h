@@ -36,7 +36,11 @@ struct VinTileDst {                 // one cluster tile of a synthesized view (f
     int cell;                       // small-tile index (col * 4 + row), -1 = none
     int pad;
 };
-constexpr int kVinMaxViews = 8192;  // tile-table capacity (global views per rig frame)
+constexpr int kVinMaxViews = 8192;
+constexpr int kVinViewTab = 64;      // per-view synthesis constants passed as a kernel parameter
+struct VinViewK {
+    float t[kVinViewTab], kl[kVinViewTab], kr[kVinViewTab];
+};  // tile-table capacity (global views per rig frame)
 
 VinLayout vin_layout(int W, int H, int B);
 cudaError_t vin_flows(const VinLayout& L, const VinWeights& w, const VinPairs& pp, int fmt, uint8_t* ws, float* out,

@@ -1,6 +1,6 @@
 """Static SASS loop bodies of one kernel (backward branches), with an opcode histogram.
 
-usage: sass_loops.py MANGLED_SUBSTRING [cubin-name-prefix]
+usage: sass_loops.py MANGLED_SUBSTRING [cubin-name-prefix | path.cubin]
 Disassembles the in-tree libfvv_b200.so."""
 import collections
 import os
@@ -11,11 +11,14 @@ import tempfile
 
 name = sys.argv[1]
 prefix = sys.argv[2] if len(sys.argv) > 2 else "interp_kernels"
-tmp = tempfile.mkdtemp()
-subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath("paper_2112_10603_b200/libfvv_b200.so")], cwd=tmp,
-               capture_output=True)
-cub = [f for f in os.listdir(tmp) if f.startswith(prefix) and f.endswith(".cubin")][0]
-dis = subprocess.run(["nvdisasm", "-c", os.path.join(tmp, cub)], capture_output=True, text=True).stdout
+if prefix.endswith(".cubin"):  # a cubin built by hand (e.g. nvcc -cubin -D... for a variant)
+    cubp = prefix
+else:
+    tmp = tempfile.mkdtemp()
+    subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath("paper_2112_10603_b200/libfvv_b200.so")], cwd=tmp,
+                   capture_output=True)
+    cubp = os.path.join(tmp, [f for f in os.listdir(tmp) if f.startswith(prefix) and f.endswith(".cubin")][0])
+dis = subprocess.run(["nvdisasm", "-c", cubp], capture_output=True, text=True).stdout
 i = dis.index(".text." + name)
 j = dis.find("//-----", i + 10)
 sec = dis[i:j].split("\n")

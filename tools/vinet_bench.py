@@ -51,3 +51,14 @@ fl_ = conv_flops(W, H) * npairs
 print(f"{W}x{H} pairs {npairs}: flows {tf:.2f} ms ({fl_ / tf / 1e9:.0f} TFLOP/s conv-equivalent, "
       f"{fl_ / 1e12:.2f} TFLOP), synth {nviews} views {ts:.2f} ms -> "
       f"{npairs * nviews / ((tf + ts) / 1e3):.0f} views/s")
+
+# the fused rig path (flows + synthesis with the cluster tiles in its epilogue + anchors/padding)
+cams = torch.cat([L, R[-1:]], 0).contiguous()
+views, cl, _ = net.rig_clusters(cams, 4, 16)
+torch.cuda.synchronize()
+ev[0].record()
+for _ in range(K):
+    net.rig_clusters(cams, 4, 16, views=views, out=cl)
+ev[1].record()
+torch.cuda.synchronize()
+print(f"rig_clusters (8 cams, 4 stages, vps 16): {ev[0].elapsed_time(ev[1]) / K:.2f} ms")
