@@ -32,6 +32,12 @@ net = VINet(W, H, fmt, max_pairs=npairs)
 rng = np.random.default_rng(0)
 L = torch.from_numpy(rng.integers(0, 256, (npairs, fb), dtype=np.uint8)).cuda()
 R = torch.roll(L, 3, 1)
+if len(sys.argv) > 4 and sys.argv[4] == "rig2":  # two fused rig frames only (ncu launch lists: keep the 2nd)
+    cams = torch.cat([L, R[-1:]], 0).contiguous()
+    for _ in range(2):
+        net.rig_clusters(cams, 4, 16)
+    torch.cuda.synchronize()
+    sys.exit(0)
 fl = net.flows(L, R)
 views = net.synth(L, R, fl, nviews)
 torch.cuda.synchronize()
@@ -62,3 +68,11 @@ for _ in range(K):
 ev[1].record()
 torch.cuda.synchronize()
 print(f"rig_clusters (8 cams, 4 stages, vps 16): {ev[0].elapsed_time(ev[1]) / K:.2f} ms")
+from paper_2112_10603_b200.cluster import rig_clusters  # noqa: E402
+ev[0].record()
+for _ in range(K):
+    net.rig(cams, 4, views=views)
+    rig_clusters(views, W, H, fmt, cams.shape[0], 4, 16, out=cl)
+ev[1].record()
+torch.cuda.synchronize()
+print(f"rig + rig_clusters, unfused: {ev[0].elapsed_time(ev[1]) / K:.2f} ms")
