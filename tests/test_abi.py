@@ -98,3 +98,28 @@ def test_vinet_entry_points_validate_on_the_host():
     assert L.fvv_conv2d_bf16(ctypes.byref(conv), 1, 1, 1, 1, None) == _lib.FVV_EINVAL
     conv = _lib.ConvDesc(1, 8, 8, 64, 16, 16, 128, 0, 128, 3, 2, 1, 1, 1, 0, 128)  # transposed must be k4 s2 p1
     assert L.fvv_conv2d_bf16(ctypes.byref(conv), 1, 1, 1, 1, None) == _lib.FVV_EUNSUPPORTED
+
+
+def test_vinet_rig_clusters_validates_on_the_host():
+    """fvv_vinet_rig_clusters applies fvv_rig_clusters' layout rules (cluster.py:148-183,
+    server/pipeline.py:273-292) before any device work; pointers are never dereferenced."""
+    L = _lib.load()
+    from paper_2112_10603_b200 import vinet
+    vinet._sig(L)
+    w = vinet._Weights()
+    fake = 16  # a non-null address: validation fails before anything is read
+
+    def call(d, ncams=8, stages=4, vps=16):
+        return L.fvv_vinet_rig_clusters(ctypes.byref(d), ctypes.byref(w), fake, ncams, stages, vps, fake, fake,
+                                        fake, 1 << 30, None)
+    rgb = _lib.desc(1920, 1080, 2)
+    assert call(rgb) == _lib.FVV_ELAYOUT                      # cluster frames are gray or 4:2:0
+    d = _lib.desc(1920, 1080, 1)
+    assert call(d, vps=17) == _lib.FVV_ELAYOUT                # more than 2^stages views per side
+    assert call(d, vps=0) == _lib.FVV_ELAYOUT
+    assert call(d, ncams=1) == _lib.FVV_EINVAL
+    assert call(d, stages=7) == _lib.FVV_EINVAL
+    odd = _lib.desc(1916, 1080, 1)                            # VINet takes W % 4 == 0, clusters need W % 8
+    assert call(odd) == _lib.FVV_ELAYOUT
+    assert call(d, ncams=600, stages=4) == _lib.FVV_EINVAL     # > 8192 global views for the tile table
+    assert "8192" in L.fvv_last_error().decode()
