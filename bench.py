@@ -509,7 +509,7 @@ def run_b200(args, cfg, rank, world, local_rank):
     }
     if not args.no_vinet and rank == 0 and min(W, H) >= 64:
         try:
-            line["vinet"] = run_vinet(cfg, dev)
+            line["vinet"] = run_vinet(cfg, dev, use_graph=not args.no_graph)
         except Exception as exc:  # the headline line must survive a failure of the secondary path
             line["vinet"] = {"error": f"{type(exc).__name__}: {exc}"}
     print(json.dumps(line))
@@ -531,7 +531,7 @@ def vinet_conv_flops(W, H):
     return tot
 
 
-def run_vinet(cfg, dev, steps=10, warmup=3):
+def run_vinet(cfg, dev, steps=10, warmup=3, use_graph=True):
     """The north-star CNN path on the same rig: VINet flows once per camera gap
     + direct-t synthesis of all views of the gap in one pass (tcgen05 convs),
     written into the global views buffer, then the cluster frames."""
@@ -559,21 +559,44 @@ def run_vinet(cfg, dev, steps=10, warmup=3):
         net.rig(cams, S, views=views)
         if tiled:
             rig_clusters(views, W, H, fmt, C, S, vps, out=clusters)
+    def flows_only():
+        net.flows(L, R, out=flows)
     for _ in range(warmup):
         step()
         step_unfused()
-        net.flows(L, R, out=flows)
+        flows_only()
+    torch.cuda.synchronize()
+    # one CUDA graph per variant: the ~150 launches of a rig frame replay without host work
+    graphs, graph_note = {}, None
+    if use_graph:
+        try:
+            for name, fn in (("fused", step), ("flows", flows_only), ("unfused", step_unfused)):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    fn()
+                graphs[name] = g
+            torch.cuda.synchronize()
+        except Exception as ex:  # keep the eager numbers rather than none
+            graphs, graph_note = {}, f"capture failed, eager: {type(ex).__name__}: {ex}"
+
+    def run(name, fn):
+        if name in graphs:
+            graphs[name].replay()
+        else:
+            fn()
+    for name, fn in (("fused", step), ("flows", flows_only), ("unfused", step_unfused)):
+        run(name, fn)
     torch.cuda.synchronize()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     ev[0].record()
     for _ in range(steps):
-        step()
+        run("fused", step)
     ev[1].record()
     for _ in range(steps):
-        net.flows(L, R, out=flows)
+        run("flows", flows_only)
     ev[2].record()
     for _ in range(steps):
-        step_unfused()
+        run("unfused", step_unfused)
     ev[3].record()
     torch.cuda.synchronize()
     unfused_ms = ev[2].elapsed_time(ev[3]) / steps
@@ -588,6 +611,7 @@ def run_vinet(cfg, dev, steps=10, warmup=3):
         "value": npairs * nviews / (rig_ms / 1e3), "unit": "views/s",
         "ms_per_step": rig_ms, "flows_ms": fl_ms, "synth_and_tiling_ms": rig_ms - fl_ms,
         "unfused_ms_per_step": unfused_ms, "tiling": "fused into the synthesis epilogue" if tiled else "none",
+        "cuda_graph": bool(graphs), **({"graph_note": graph_note} if graph_note else {}),
         "pairs": npairs, "views_per_pair": nviews, "dtype": "bf16 convs, fp32 accumulate / warps",
         "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
                      "traffic": None, "flop_per_step": flops,
