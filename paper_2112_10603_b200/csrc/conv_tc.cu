@@ -28,6 +28,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -114,13 +115,20 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 // epilogue of one tile overlaps the MMAs of the next.
 // MT output rows per tile (MT accumulators of 128 x NT per buffer) share each
 // weight chunk; MT = 2 whenever two double-buffered sets fit TMEM (NT <= 128).
-template <int NT, int SW>
+// RR > 0 (row reuse, 3x3 stride-1 convolutions with a small N): a tile is RR output rows;
+// one stage holds the RR + 2 input-row segments of one (dx, channel chunk) and the three
+// weight chunks of taps (0..2, dx), and output row r takes rows r + dy with B_dy -- every
+// input row segment is fetched once per tile instead of once per (row, dy) tap.
+template <int NT, int SW, int RR = 0>
 struct ConvTile {
-    static constexpr int MT = NT <= 128 ? 2 : 1;
+    static constexpr int MT = RR > 0 ? RR : (NT <= 128 ? 2 : 1);
+    static constexpr int kARows = RR > 0 ? RR + 2 : MT;
+    static constexpr int kBChunks = RR > 0 ? 3 : 1;
     static constexpr int kABytes = 128 * SW;                 // one 128-pixel row segment
     static constexpr int kBBytes = NT * SW;
-    static constexpr int kStageBytes = MT * kABytes + kBBytes;
-    static constexpr int kStages = kStageBytes > 40 * 1024 ? 4 : 6;
+    static constexpr int kStageBytes = kARows * kABytes + kBChunks * kBBytes;
+    static constexpr int kStages = RR > 0 ? (2 * kStageBytes + 1280 <= 232448 ? 2 : 1)
+                                          : (kStageBytes > 40 * 1024 ? 4 : 6);
     static constexpr int kTmemCols = 2 * MT * NT < 32 ? 32 : 2 * MT * NT;  // two accumulator sets
     static constexpr size_t kSmem = 1024 /* alignment slack */ + (size_t)kStages * kStageBytes + 256;
 };
@@ -143,11 +151,11 @@ __device__ __forceinline__ TileCoord tile_of(int t, const ConvTCParams& p, int n
     return c;
 }
 
-template <int NT, int SW>
+template <int NT, int SW, int RR = 0>
 __global__ void __launch_bounds__(kConvThreads, 1)
     k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const float* __restrict__ bias, void* __restrict__ out, ConvTCParams p) {
-    using T = ConvTile<NT, SW>;
+    using T = ConvTile<NT, SW, RR>;
     static_assert(NT % 16 == 0 && NT >= 16 && NT <= 256, "UMMA N (M = 128)");
     constexpr int S = T::kStages;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -162,7 +170,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     const int ntx = (p.Wg + 127) / 128, nn = (p.N + NT - 1) / NT;
     constexpr int MT = T::MT;
     const int ntiles = ntx * nn * ((p.Hg + MT - 1) / MT) * p.B;
-    const int nk = p.ntaps * p.kc_per_tap;
+    const int nk = (RR > 0 ? 3 : p.ntaps) * p.kc_per_tap;  // RR: K chunks = (dx, channel chunk)
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; s++) {
@@ -201,11 +209,22 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                     const int tap = kc / p.kc_per_tap, c0 = (kc - tap * p.kc_per_tap) * (SW / 2);
                     uint8_t* sa = smem + s * T::kStageBytes;
                     mbar_expect_tx(&full[s], T::kStageBytes);
+                    if constexpr (RR > 0) {
+                        // tap = dx here: input rows iy0 .. iy0 + RR + 1, weights of taps (dy, dx)
 #pragma unroll
-                    for (int r = 0; r < MT; r++)  // rows past Hg load real or zero rows; the epilogue skips them
-                        tma_load_4d(sa + r * T::kABytes, &tmA, &full[s], c0, ix0 + p.tdx[tap],
-                                    iy0 + r * p.sy + p.tdy[tap], c.b);
-                    tma_load_2d(sa + MT * T::kABytes, &tmB, &full[s], tap * p.cpad + c0, p.wrow0 + c.n0);
+                        for (int j = 0; j < T::kARows; j++)
+                            tma_load_4d(sa + j * T::kABytes, &tmA, &full[s], c0, ix0 + p.tdx[tap], iy0 + j, c.b);
+#pragma unroll
+                        for (int dy = 0; dy < 3; dy++)
+                            tma_load_2d(sa + T::kARows * T::kABytes + dy * T::kBBytes, &tmB, &full[s],
+                                        (dy * 3 + tap) * p.cpad + c0, p.wrow0 + c.n0);
+                    } else {
+#pragma unroll
+                        for (int r = 0; r < MT; r++)  // rows past Hg load real or zero rows; the epilogue skips them
+                            tma_load_4d(sa + r * T::kABytes, &tmA, &full[s], c0, ix0 + p.tdx[tap],
+                                        iy0 + r * p.sy + p.tdy[tap], c.b);
+                        tma_load_2d(sa + MT * T::kABytes, &tmB, &full[s], tap * p.cpad + c0, p.wrow0 + c.n0);
+                    }
                 }
             }
         }
@@ -224,14 +243,27 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                     const int s = kg % S;
                     mbar_wait(&full[s], (kg / S) & 1);
                     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-                    const uint32_t sa = smem_u32(smem + s * T::kStageBytes), sb = sa + MT * T::kABytes;
+                    const uint32_t sa = smem_u32(smem + s * T::kStageBytes), sb = sa + T::kARows * T::kABytes;
+                    if constexpr (RR > 0) {
 #pragma unroll
-                    for (int k = 0; k < SW / 32; k++) {
-                        const uint64_t db = umma_desc<SW>(sb + 32 * k);
+                        for (int k = 0; k < SW / 32; k++)
 #pragma unroll
-                        for (int r = 0; r < MT; r++)
-                            umma_bf16(td + r * NT, umma_desc<SW>(sa + r * T::kABytes + 32 * k), db, idesc,
-                                      (kc > 0 || k > 0) ? 1u : 0u);
+                            for (int dy = 0; dy < 3; dy++) {
+                                const uint64_t db = umma_desc<SW>(sb + dy * T::kBBytes + 32 * k);
+#pragma unroll
+                                for (int r = 0; r < MT; r++)
+                                    umma_bf16(td + r * NT, umma_desc<SW>(sa + (r + dy) * T::kABytes + 32 * k), db,
+                                              idesc, (kc > 0 || k > 0 || dy > 0) ? 1u : 0u);
+                            }
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < SW / 32; k++) {
+                            const uint64_t db = umma_desc<SW>(sb + 32 * k);
+#pragma unroll
+                            for (int r = 0; r < MT; r++)
+                                umma_bf16(td + r * NT, umma_desc<SW>(sa + r * T::kABytes + 32 * k), db, idesc,
+                                          (kc > 0 || k > 0) ? 1u : 0u);
+                        }
                     }
                     umma_commit(&empty[s]);  // frees the stage once these MMAs have read it
                 }
@@ -358,6 +390,11 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
+static bool getenv_flag_off(const char* name) {  // NAME=0 disables a fast path (A/B timing only)
+    const char* v = getenv(name);
+    return v && v[0] == '0';
+}
+
 static CUtensorMapSwizzle swz(int sw) {
     return sw == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : (sw == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
 }
@@ -387,11 +424,11 @@ static bool make_w_map(CUtensorMap* m, const void* w, int rows, int K, int sw, i
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int NT, int SW>
+template <int NT, int SW, int RR = 0>
 static cudaError_t launch_nt_sw(const CUtensorMap& a, const CUtensorMap& w, const float* bias, void* out,
                                 const ConvTCParams& p, int ntiles, cudaStream_t st) {
-    using T = ConvTile<NT, SW>;
-    auto kern = k_conv_tc<NT, SW>;
+    using T = ConvTile<NT, SW, RR>;
+    auto kern = k_conv_tc<NT, SW, RR>;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::kSmem);
@@ -442,6 +479,11 @@ cudaError_t conv_tc(const void* x, int B, int Hin, int Win, int cpad, const void
     if (!make_w_map(&mw, w, wrows, p.ntaps * cpad, sw, ntile)) return cudaErrorInvalidValue;
     const int npad = ((p.N + ntile - 1) / ntile) * ntile;
     const int ntiles = npad / ntile;
+    // small-N 3x3 stride-1 convolutions (the VINet head) are A-load bound: row-reuse tiles
+    bool std3x3 = p.ntaps == 9 && p.sy == 1 && p.sx == 1 && p.omy == 1 && p.omx == 1;
+    for (int t = 0; t < 9 && std3x3; t++) std3x3 = p.tdy[t] == t / 3 && p.tdx[t] == t % 3;
+    if (std3x3 && ntile == 32 && sw == 128 && !getenv_flag_off("FVV_CONV_RR"))
+        return launch_nt_sw<32, 128, 4>(ma, mw, bias, out, p, ntiles, st);
     switch (sw) {
         case 128: return launch_sw<128>(ntile, ma, mw, bias, out, p, ntiles, st);
         case 64: return launch_sw<64>(ntile, ma, mw, bias, out, p, ntiles, st);

@@ -36,6 +36,8 @@ def _check(torch, got_nhwc, ref_nchw, cout, out_f32):
     (128, 256, 3, 2, 20, 66, True, False),     # conv1 (cpad 128, SW128, N = 256)
     (256, 256, 3, 1, 10, 260, True, False),    # residual 256x256, two pixel tiles per row
     (64, 16, 3, 1, 9, 17, False, True),        # fp32 output, N = 16 tile
+    (128, 20, 3, 1, 13, 150, False, True),     # N = 32 tile, SW128: row-reuse tiles (4 rows, ragged H)
+    (128, 32, 3, 1, 6, 40, True, False),       # row-reuse, bf16 output
 ])
 def test_conv_matches_torch(torch_cuda, cin, cout, k, s, H, W, relu, out_f32):
     torch = torch_cuda
