@@ -244,24 +244,27 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                     mbar_wait(&full[s], (kg / S) & 1);
                     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
                     const uint32_t sa = smem_u32(smem + s * T::kStageBytes), sb = sa + T::kARows * T::kABytes;
+                    // descriptors of the stage's operands: base + (byte offset >> 4) in the start-address
+                    // field (smem < 256 KB, so the 14-bit field never carries) -- one add per MMA
+                    const uint64_t da0 = umma_desc<SW>(sa), db0 = umma_desc<SW>(sb);
                     if constexpr (RR > 0) {
 #pragma unroll
                         for (int k = 0; k < SW / 32; k++)
 #pragma unroll
                             for (int dy = 0; dy < 3; dy++) {
-                                const uint64_t db = umma_desc<SW>(sb + dy * T::kBBytes + 32 * k);
+                                const uint64_t db = db0 + (uint64_t)((dy * T::kBBytes + 32 * k) >> 4);
 #pragma unroll
                                 for (int r = 0; r < MT; r++)
-                                    umma_bf16(td + r * NT, umma_desc<SW>(sa + (r + dy) * T::kABytes + 32 * k), db,
-                                              idesc, (kc > 0 || k > 0 || dy > 0) ? 1u : 0u);
+                                    umma_bf16(td + r * NT, da0 + (uint64_t)(((r + dy) * T::kABytes + 32 * k) >> 4),
+                                              db, idesc, (kc > 0 || k > 0 || dy > 0) ? 1u : 0u);
                             }
                     } else {
 #pragma unroll
                         for (int k = 0; k < SW / 32; k++) {
-                            const uint64_t db = umma_desc<SW>(sb + 32 * k);
+                            const uint64_t db = db0 + (uint64_t)((32 * k) >> 4);
 #pragma unroll
                             for (int r = 0; r < MT; r++)
-                                umma_bf16(td + r * NT, umma_desc<SW>(sa + r * T::kABytes + 32 * k), db, idesc,
+                                umma_bf16(td + r * NT, da0 + (uint64_t)((r * T::kABytes + 32 * k) >> 4), db, idesc,
                                           (kc > 0 || k > 0) ? 1u : 0u);
                         }
                     }
