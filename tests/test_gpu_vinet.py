@@ -124,7 +124,8 @@ def test_vinet_rig_layout(torch_cuda, params):
 
 
 @pytest.mark.parametrize("w,h,fmt,C,S,vps", [(192, 128, 1, 4, 2, 4), (200, 128, 0, 3, 3, 5),
-                                             (256, 192, 1, 5, 2, 1), (128, 64, 1, 3, 1, 2)])
+                                             (256, 192, 1, 5, 2, 1), (128, 64, 1, 3, 1, 2),
+                                             (1920, 1080, 1, 3, 4, 16)])  # BASELINE 1080p geometry
 def test_vinet_rig_clusters_fused_tiling(torch_cuda, params, w, h, fmt, C, S, vps):
     """fvv_vinet_rig_clusters (quarter tiles written by the synthesis epilogue) is
     byte-identical to fvv_vinet_rig + fvv_rig_clusters (server/pipeline.py:199-292)."""
