@@ -1066,7 +1066,10 @@ __device__ __forceinline__ uint8_t blend_px(double m, int a, int b) {
 // the same order, so the same doubles -- and evaluates mask + blend fully in
 // parallel (thread = 2 rows x 8 columns, chroma from the row pair).
 // ---------------------------------------------------------------------------
-constexpr int kCR = 32, kCC = 64;  // carry kernel: rows per CTA (one lane each), chunk columns
+#ifndef FVV_KCC
+#define FVV_KCC 64
+#endif
+constexpr int kCR = 32, kCC = FVV_KCC;  // carry kernel: rows per CTA (one lane each), chunk columns
 constexpr int kCT = kCC + 16;       // staged u16 per row and chunk: sd[c0-8 .. c0+72)
 constexpr int kCTP = kCT + 4;       // row pitch: 168 B = 21 x 8 B, 16 lanes hit 16 bank pairs
 
