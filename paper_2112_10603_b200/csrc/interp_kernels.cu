@@ -1101,16 +1101,35 @@ __global__ void __launch_bounds__(kCR) k_scan_carry(Geometry g, const uint8_t* _
     const uint16_t* row = sd + (size_t)y * W;
     const int nchunks = (W + kCC - 1) / kCC;
     const bool vec = (W % 4) == 0;  // 8-byte aligned row segments (always, frames are W % 4 == 0)
-    // stage chunk k into tile[k & 1][lane]: entry j holds sd[clamp(c0 - 8 + j)].
-    // In-range entries come in 8-byte cp.async pieces (c0 - 8 and W are
-    // multiples of 4); only the clamped ends are written with plain stores.
+    // stage chunk k into tile[k & 1][r] for the warp's 32 rows r: entry j holds
+    // sd[clamp(c0 - 8 + j)].  In-range entries come in 8-byte cp.async pieces
+    // (c0 - 8 and W are multiples of 4), issued cooperatively: consecutive
+    // lanes take consecutive pieces of the same row, so one instruction touches
+    // ~2 rows' contiguous bytes instead of 32 rows (r1 v21 ncu: the per-lane-row
+    // staging was MIO/LSU-throttled).  Only the clamped ends are written with
+    // plain stores, each lane into its own row (the only row it reads).
     auto stage = [&](int k) {
         const int c0 = k * kCC;
         uint16_t* t = tile[k & 1][lane];
         if (vec) {
             const int jlo = max(0, 8 - c0);                  // first in-range entry
             const int jhi = min(kCT, W - (c0 - 8));          // one past the last
-            for (int j = jlo; j < jhi; j += 4) cp_async8(t + j, row + c0 - 8 + j);
+            if (jlo == 0 && jhi == kCT) {
+                constexpr int NP = kCT / 4;                   // pieces per row
+#pragma unroll 4
+                for (int i = lane; i < kCR * NP; i += 32) {
+                    const int r = i / NP, j = 4 * (i - r * NP);
+                    const uint16_t* rw = sd + (size_t)min(y0 + r, H - 1) * W;
+                    cp_async8(&tile[k & 1][r][j], rw + c0 - 8 + j);
+                }
+            } else {
+                const int np = (jhi - jlo) >> 2;
+                for (int r = 0; r < kCR; r++) {
+                    const uint16_t* rw = sd + (size_t)min(y0 + r, H - 1) * W;
+                    for (int q = lane; q < np; q += 32)
+                        cp_async8(&tile[k & 1][r][jlo + 4 * q], rw + c0 - 8 + jlo + 4 * q);
+                }
+            }
             if (jlo > 0) {
                 const uint16_t v = row[0];
                 for (int j = 0; j < jlo; j++) t[j] = v;
