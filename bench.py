@@ -5,7 +5,7 @@ synthesized virtual views/s at 1080p; per-rig-frame latency).
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl b200|reference]
 
 One step = a batch of F independent rig frames of the live stream per rank
-(--frames-in-flight, default 2, run concurrently on forked streams inside one
+(--frames-in-flight, default 1; F > 1 run concurrently on forked streams inside one
 CUDA graph): every dense view of every camera gap (recursive midpoints,
 server/pipeline.py:254-271) plus every cluster frame (server/pipeline.py:273-292).
 The per-rig-frame latency (one frame in flight) is measured separately and

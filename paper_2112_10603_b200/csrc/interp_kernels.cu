@@ -1069,6 +1069,12 @@ __device__ __forceinline__ uint8_t blend_px(double m, int a, int b) {
 #ifndef FVV_KCC
 #define FVV_KCC 64
 #endif
+#ifndef FVV_SCAN_COOP_MIN
+#define FVV_SCAN_COOP_MIN 600  // CTAs (one warp each): ~4 per SM; r1 v21 sweep 0/600/1200/never
+#endif
+#ifndef FVV_SCAN_TSTORE
+#define FVV_SCAN_TSTORE 1
+#endif
 constexpr int kCR = 32, kCC = FVV_KCC;  // carry kernel: rows per CTA (one lane each), chunk columns
 constexpr int kCT = kCC + 16;       // staged u16 per row and chunk: sd[c0-8 .. c0+72)
 constexpr int kCTP = kCT + 4;       // row pitch: 168 B = 21 x 8 B, 16 lanes hit 16 bank pairs
@@ -1087,9 +1093,13 @@ __device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_
 
 __device__ __forceinline__ double d0_of(int s) { return div3(u2d_exact(s)); }  // == s / 3.0 (IEEE)
 
+template <bool COOP>
 __global__ void __launch_bounds__(kCR) k_scan_carry(Geometry g, const uint8_t* __restrict__ ws,
                                                     Planes P) {
     __shared__ __align__(16) uint16_t tile[2][kCR][kCTP];  // per lane: its own row segment
+#if FVV_SCAN_TSTORE
+    __shared__ __align__(16) double ctile[kCR][kCC / 8 + 2];  // carry transpose (80 B pitch: no conflicts)
+#endif
     const int W = g.W, H = g.H;
     const int pair = blockIdx.y, y0 = blockIdx.x * kCR;
     const int lane = threadIdx.x;
@@ -1114,7 +1124,9 @@ __global__ void __launch_bounds__(kCR) k_scan_carry(Geometry g, const uint8_t* _
         if (vec) {
             const int jlo = max(0, 8 - c0);                  // first in-range entry
             const int jhi = min(kCT, W - (c0 - 8));          // one past the last
-            if (jlo == 0 && jhi == kCT) {
+            if (!COOP) {
+                for (int j = jlo; j < jhi; j += 4) cp_async8(t + j, row + c0 - 8 + j);
+            } else if (jlo == 0 && jhi == kCT) {
                 constexpr int NP = kCT / 4;                   // pieces per row
 #pragma unroll 4
                 for (int i = lane; i < kCR * NP; i += 32) {
@@ -1225,6 +1237,23 @@ __global__ void __launch_bounds__(kCR) k_scan_carry(Geometry g, const uint8_t* _
             }
         }
         }
+#if FVV_SCAN_TSTORE
+        if (COOP && n == kCC && (ng & 1) == 0 && y0 + kCR <= H) {
+            // full chunk of 32 live rows: transpose the carries through shared memory so
+            // consecutive lanes store consecutive 16-byte pieces of the same row
+            double2* cs = reinterpret_cast<double2*>(&ctile[lane][0]);
+#pragma unroll
+            for (int i = 0; i < kCC / 8; i += 2) cs[i / 2] = make_double2(cv[i], cv[i + 1]);
+            __syncwarp();
+            constexpr int PR = kCC / 16;  // double2 pieces per row
+#pragma unroll
+            for (int i = lane; i < kCR * PR; i += 32) {
+                const int r = i / PR, q = i - (i / PR) * PR;
+                *reinterpret_cast<double2*>(carry + (size_t)(y0 + r) * ng + c0 / 8 + 2 * q) =
+                    reinterpret_cast<const double2*>(&ctile[r][0])[q];
+            }
+        } else
+#endif
         if (live) {
             const int ngc = (n + 7) / 8;
             if (ngc == kCC / 8 && (ng & 1) == 0) {   // 16-byte aligned full segment
@@ -1944,7 +1973,15 @@ cudaError_t run_interp_stage(const Geometry& g, const PairTable& pt, uint8_t* ws
     if ((e = E()) != cudaSuccess) return e;
 
     B(KC_SCAN);
-    k_scan_carry<<<dim3((g.H + kCR - 1) / kCR, npairs), kCR, 0, st>>>(g, ws, P);
+    {
+        // cooperative row staging pays once the launch has several warps per SM;
+        // below that the per-warp critical path (its index math) dominates
+        const dim3 grid((g.H + kCR - 1) / kCR, npairs);
+        if ((int)(grid.x * grid.y) >= FVV_SCAN_COOP_MIN)
+            k_scan_carry<true><<<grid, kCR, 0, st>>>(g, ws, P);
+        else
+            k_scan_carry<false><<<grid, kCR, 0, st>>>(g, ws, P);
+    }
     if ((e = E()) != cudaSuccess) return e;
     B(KC_BLEND);
     {
