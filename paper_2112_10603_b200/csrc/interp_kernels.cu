@@ -1113,7 +1113,7 @@ __global__ void __launch_bounds__(kCR) k_scan_carry(Geometry g, const uint8_t* _
     const bool vec = (W % 4) == 0;  // 8-byte aligned row segments (always, frames are W % 4 == 0)
     // stage chunk k into tile[k & 1][r] for the warp's 32 rows r: entry j holds
     // sd[clamp(c0 - 8 + j)].  In-range entries come in 8-byte cp.async pieces
-    // (c0 - 8 and W are multiples of 4), issued cooperatively: consecutive
+    // (c0 - 8 and W are multiples of 4), issued cooperatively when COOP: consecutive
     // lanes take consecutive pieces of the same row, so one instruction touches
     // ~2 rows' contiguous bytes instead of 32 rows (r1 v21 ncu: the per-lane-row
     // staging was MIO/LSU-throttled).  Only the clamped ends are written with
