@@ -80,6 +80,17 @@ int fvv_engine_create(const fvv_frame_desc* desc, const fvv_interp_params* param
 void fvv_engine_destroy(fvv_engine* engine);
 int fvv_engine_max_pairs(const fvv_engine* engine);
 
+/* Launch-variant thresholds of an engine (no effect on results: every variant
+ * is bit-exact; tests force each one).  value < 0 restores the default.
+ *   FVV_TUNE_SCAN_COOP_MIN     cooperative-staging k_scan_carry from this many
+ *                              one-warp CTAs per launch (default 600)
+ *   FVV_TUNE_SADW_RB_MIN_CTAS  stacked-block k_sadw from this many CTAs
+ *                              (default 296 = 2 per SM)
+ * Not thread-safe against a concurrent call on the same engine. */
+#define FVV_TUNE_SCAN_COOP_MIN 0
+#define FVV_TUNE_SADW_RB_MIN_CTAS 1
+int fvv_engine_set_tuning(fvv_engine* engine, int key, int value);
+
 /* interp.py:97-148, batched: out[i] = interpolate(left[i], right[i]).
  * npairs <= max_pairs.  Outputs may not alias inputs. */
 int fvv_interpolate_pairs(fvv_engine* engine, const uint8_t* const* left,

@@ -39,12 +39,29 @@ def stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
+    """Compile every translation unit to an object in parallel, then link the .so."""
     if not force and not stale():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
     extra = os.environ.get("FVV_NVCC_EXTRA", "").split()  # tuning sweeps only (e.g. -DFVV_MINB_MASK=8)
-    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-o", str(LIB) + ".tmp", *[str(CSRC / s) for s in SOURCES]]
+    objdir = PKG / "_obj"
+    objdir.mkdir(exist_ok=True)
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+
+    def one(src: str) -> Path:
+        obj = objdir / (Path(src).stem + ".o")
+        cmd = [nvcc(), *compile_flags, *extra, "-c", "-o", str(obj), str(CSRC / src)]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+        return obj
+
+    with ThreadPoolExecutor(len(SOURCES)) as ex:
+        objs = list(ex.map(one, SOURCES))
+    cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
+           "-o", str(LIB) + ".tmp", *map(str, objs)]
     if verbose:
-        print(" ".join(cmd))
+        print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
     os.replace(str(LIB) + ".tmp", LIB)
     return LIB

@@ -13,12 +13,13 @@ from pathlib import Path
 from ._build import LIB
 
 FVV_OK, FVV_EINVAL, FVV_ELAYOUT, FVV_ECUDA, FVV_EUNSUPPORTED = 0, -1, -2, -3, -4
+FVV_TUNE_SCAN_COOP_MIN, FVV_TUNE_SADW_RB_MIN_CTAS = 0, 1
 
 # every symbol include/fvv_b200.h declares (tests/test_abi.py checks both ways)
 EXPORTS = (
     "fvv_last_error", "fvv_build_info", "fvv_frame_bytes", "fvv_validate_params",
     "fvv_engine_workspace_size", "fvv_engine_create", "fvv_engine_destroy",
-    "fvv_engine_max_pairs", "fvv_interpolate_pairs", "fvv_interp_diagnostics",
+    "fvv_engine_max_pairs", "fvv_engine_set_tuning", "fvv_interpolate_pairs", "fvv_interp_diagnostics",
     "fvv_dense_views", "fvv_rig_views", "fvv_downscale", "fvv_cluster_width",
     "fvv_assemble_cluster", "fvv_rig_cluster_bytes", "fvv_rig_clusters",
     "fvv_profile_enable", "fvv_profile_read", "fvv_kernel_class_name",
@@ -74,6 +75,7 @@ def load():
         "fvv_engine_create": (I, [pd, pp, I, P, Z, ctypes.POINTER(P)]),
         "fvv_engine_destroy": (None, [P]),
         "fvv_engine_max_pairs": (I, [P]),
+        "fvv_engine_set_tuning": (I, [P, I, I]),
         "fvv_interpolate_pairs": (I, [P, PP, PP, PP, I, P]),
         "fvv_interp_diagnostics": (I, [P, I, P, P, P, P]),
         "fvv_interp_level_diagnostics": (I, [P, I, I, P, P, P, P, P]),

@@ -14,7 +14,7 @@
 #include "vinet.h"
 
 namespace fvv {
-extern int g_failed_class;
+extern thread_local int g_failed_class;
 cudaError_t run_interp_stage(const Geometry& g, const PairTable& pt, uint8_t* ws, const Planes& P,
                              const int16_t* const* rank_of, const int16_t* const* cand_of_rank,
                              int npairs, double* mask_out, Prof* prof, cudaStream_t st);
@@ -114,6 +114,8 @@ void make_geometry(const fvv_frame_desc* d, const fvv_interp_params* p, Geometry
     g->qmargin[0] = 0;
     g->qmargin[1] = 2 * p->search_radius[0];
     g->qmargin[2] = 4 * p->search_radius[0] + 2 * p->search_radius[1];
+    g->scan_coop_min = kScanCoopMinDefault;
+    g->sadw_rb_min_ctas = kSadwRbMinCtasDefault;
 }
 
 // workspace = [header: candidate tables][pair slot 0][pair slot 1]...
@@ -286,6 +288,16 @@ int fvv_engine_create(const fvv_frame_desc* d, const fvv_interp_params* p, int m
 void fvv_engine_destroy(fvv_engine* e) { delete e; }
 
 int fvv_engine_max_pairs(const fvv_engine* e) { return e ? e->max_pairs : 0; }
+
+int fvv_engine_set_tuning(fvv_engine* e, int key, int value) {
+    if (!e) return fail(FVV_EINVAL, "null engine");
+    switch (key) {
+        case FVV_TUNE_SCAN_COOP_MIN: e->g.scan_coop_min = value < 0 ? kScanCoopMinDefault : value; break;
+        case FVV_TUNE_SADW_RB_MIN_CTAS: e->g.sadw_rb_min_ctas = value < 0 ? kSadwRbMinCtasDefault : value; break;
+        default: return fail(FVV_EINVAL, "unknown tuning key " + std::to_string(key));
+    }
+    return FVV_OK;
+}
 
 static int run_pairs(fvv_engine* e, const uint8_t* const* L, const uint8_t* const* R,
                      uint8_t* const* O, int npairs, cudaStream_t st) {

@@ -30,6 +30,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 
 #include "conv_tc.h"
@@ -393,6 +394,17 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
+static int sm_count(int dev) {
+    static std::atomic<int> cache[64];
+    int n = cache[dev & 63].load(std::memory_order_relaxed);
+    if (!n) {
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+        cache[dev & 63].store(n, std::memory_order_relaxed);
+    }
+    return n;
+}
+
 static bool getenv_flag_off(const char* name) {  // NAME=0 disables a fast path (A/B timing only)
     const char* v = getenv(name);
     return v && v[0] == '0';
@@ -432,19 +444,20 @@ static cudaError_t launch_nt_sw(const CUtensorMap& a, const CUtensorMap& w, cons
                                 const ConvTCParams& p, int ntiles, cudaStream_t st) {
     using T = ConvTile<NT, SW, RR>;
     auto kern = k_conv_tc<NT, SW, RR>;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::kSmem);
+    // per-device state: the >48 KB shared-memory attribute is a property of the
+    // function on each device, and SM counts may differ between devices
+    static std::atomic<unsigned long long> attr_done{0};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(attr_done.load(std::memory_order_acquire) & bit)) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::kSmem);
         if (e != cudaSuccess) return e;
-        attr = true;
+        attr_done.fetch_or(bit, std::memory_order_release);
     }
     (void)ntiles;
-    static int nsm = 0;
-    if (!nsm) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int nsm = sm_count(dev);
     const int tiles = (p.Wg + 127) / 128 * ((p.Hg + T::MT - 1) / T::MT) * p.B * ((p.N + NT - 1) / NT);
     kern<<<tiles < nsm ? tiles : nsm, kConvThreads, T::kSmem, st>>>(a, w, bias, out, p);
     return cudaGetLastError();

@@ -1069,15 +1069,15 @@ __device__ __forceinline__ uint8_t blend_px(double m, int a, int b) {
 #ifndef FVV_KCC
 #define FVV_KCC 64
 #endif
-#ifndef FVV_SCAN_COOP_MIN
-#define FVV_SCAN_COOP_MIN 600  // CTAs (one warp each): ~4 per SM; r1 v21 sweep 0/600/1200/never
-#endif
 #ifndef FVV_SCAN_TSTORE
 #define FVV_SCAN_TSTORE 1
 #endif
 constexpr int kCR = 32, kCC = FVV_KCC;  // carry kernel: rows per CTA (one lane each), chunk columns
 constexpr int kCT = kCC + 16;       // staged u16 per row and chunk: sd[c0-8 .. c0+72)
-constexpr int kCTP = kCT + 4;       // row pitch: 168 B = 21 x 8 B, 16 lanes hit 16 bank pairs
+constexpr int kCTP = kCT + 4;       // row pitch: 2*kCTP B (168 B = 21 x 8 B at kCC 64): odd 8-byte count, 16 lanes hit 16 bank pairs
+// the double2 carry stores step by 2 up to kCC/8 and the transpose moves kCC/16 pieces per row
+static_assert(kCC % 16 == 0 && kCC >= 16, "FVV_KCC must be a positive multiple of 16");
+static_assert(((2 * kCTP) / 8) % 2 == 1 && (2 * kCTP) % 8 == 0, "carry row pitch must be an odd number of 8-byte words");
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
     const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
@@ -1698,7 +1698,7 @@ static cudaError_t launch_sadw(const Geometry& g, const PairTable& pt, uint8_t* 
     using S = SadW<SIDE, CG>;
     const Level& L = g.lv[LEVEL];
     const long ctas = (long)((sl.bx_end + 7) / 8) * ((L.nby + S::NBYT - 1) / S::NBYT) * 2 * npairs;
-    if (S::RB > 1 && ctas < 2 * 148) return launch_sadw_rb<LEVEL, SIDE, CG, 1>(g, pt, ws, P, sl, npairs, st);
+    if (S::RB > 1 && ctas < g.sadw_rb_min_ctas) return launch_sadw_rb<LEVEL, SIDE, CG, 1>(g, pt, ws, P, sl, npairs, st);
     return launch_sadw_rb<LEVEL, SIDE, CG, S::RB>(g, pt, ws, P, sl, npairs, st);
 }
 
@@ -1904,7 +1904,7 @@ static cudaError_t run_sad(const Geometry& g, const PairTable& pt, uint8_t* ws, 
     return cudaSuccess;
 }
 
-int g_failed_class = -1;
+thread_local int g_failed_class = -1;
 
 cudaError_t run_interp_stage(const Geometry& g, const PairTable& pt, uint8_t* ws, const Planes& P,
                              const int16_t* const* rank_of, const int16_t* const* cand_of_rank,
@@ -1977,7 +1977,7 @@ cudaError_t run_interp_stage(const Geometry& g, const PairTable& pt, uint8_t* ws
         // cooperative row staging pays once the launch has several warps per SM;
         // below that the per-warp critical path (its index math) dominates
         const dim3 grid((g.H + kCR - 1) / kCR, npairs);
-        if ((int)(grid.x * grid.y) >= FVV_SCAN_COOP_MIN)
+        if ((int)(grid.x * grid.y) >= g.scan_coop_min)
             k_scan_carry<true><<<grid, kCR, 0, st>>>(g, ws, P);
         else
             k_scan_carry<false><<<grid, kCR, 0, st>>>(g, ws, P);

@@ -131,6 +131,17 @@ class Interpolator:
         except Exception:  # noqa: BLE001
             pass
 
+    def set_tuning(self, scan_coop_min: int | None = None, sadw_rb_min_ctas: int | None = None):
+        """Launch-variant thresholds (fvv_engine_set_tuning); results are
+        identical for every setting -- the tests use it to force each variant.
+        None leaves a knob unchanged, -1 restores its default."""
+        if scan_coop_min is not None:
+            _lib.check(self._L.fvv_engine_set_tuning(self._h, _lib.FVV_TUNE_SCAN_COOP_MIN, int(scan_coop_min)))
+        if sadw_rb_min_ctas is not None:
+            _lib.check(self._L.fvv_engine_set_tuning(self._h, _lib.FVV_TUNE_SADW_RB_MIN_CTAS,
+                                                     int(sadw_rb_min_ctas)))
+        return self
+
     @property
     def workspace_bytes(self) -> int:
         return int(self._ws.numel())
@@ -220,8 +231,23 @@ class Interpolator:
         return views
 
 
-_engines: dict = {}
-_engines_lock = threading.Lock()
+class _ThreadState(threading.local):
+    """Per-thread engines, stream and pinned staging buffers.
+
+    The reference runs `dense_views` from a 2-worker ThreadPoolExecutor
+    (server/pipeline.py:219-220, 264-268) and ctypes releases the GIL, so two
+    calls can be in flight at once.  An engine's workspace holds the pair
+    slots of ONE batch, so every thread gets its own engines and its own CUDA
+    stream; nothing mutable is shared between threads.
+    """
+
+    def __init__(self):
+        self.engines: dict = {}
+        self.streams: dict = {}
+        self.pinned: dict = {}
+
+
+_tls = _ThreadState()
 
 
 def _engine(width, height, fmt, cfg: InterpConfig, max_pairs: int) -> Interpolator:
@@ -229,18 +255,55 @@ def _engine(width, height, fmt, cfg: InterpConfig, max_pairs: int) -> Interpolat
     _lib.require_cuda()
     key = (width, height, int(fmt), tuple(cfg.block_size), tuple(cfg.search_radius),
            float(cfg.mask_epsilon), max_pairs, torch.cuda.current_device())
-    with _engines_lock:
-        eng = _engines.get(key)
-        if eng is None:
-            eng = Interpolator(width, height, fmt, cfg, max_pairs)
-            _engines[key] = eng
-        return eng
+    eng = _tls.engines.get(key)
+    if eng is None:
+        eng = Interpolator(width, height, fmt, cfg, max_pairs)
+        _tls.engines[key] = eng
+    return eng
 
 
-def _to_device(frame, device=None):
+def _thread_stream():
+    """This thread's CUDA stream on the current device (created on first use)."""
     import torch
-    host = torch.from_numpy(packed(frame))
-    return host.pin_memory().to("cuda", non_blocking=True)
+    dev = torch.cuda.current_device()
+    s = _tls.streams.get(dev)
+    if s is None:
+        s = torch.cuda.Stream(device=dev)
+        _tls.streams[dev] = s
+    return s
+
+
+def _pinned(slot: str, nbytes: int):
+    """A reusable pinned host buffer of at least `nbytes` (per thread and slot).
+
+    Safe to reuse across calls: every drop-in call synchronises its stream
+    before it returns, so no copy from an earlier call is still in flight."""
+    import torch
+    buf = _tls.pinned.get(slot)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, pin_memory=True)
+        _tls.pinned[slot] = buf
+    return buf[:nbytes]
+
+
+def _to_device(frame, slot: str = "in0"):
+    """Frame -> packed device tensor on the current stream (pinned staging, async H2D)."""
+    import torch
+    src = packed(frame)
+    host = _pinned(slot, src.size)
+    host.numpy()[:] = src
+    return host.to("cuda", non_blocking=True)
+
+
+def _to_host(dev, slot: str = "out") -> np.ndarray:
+    """Device tensor -> numpy copy (pinned staging; synchronises this thread's stream)."""
+    import torch
+    flat = dev.contiguous().reshape(-1).view(torch.uint8)
+    host = _pinned(slot, flat.numel())
+    host.copy_(flat, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    np_dtype = torch.empty(0, dtype=dev.dtype).numpy().dtype
+    return host.numpy().copy().view(np_dtype).reshape(tuple(dev.shape))
 
 
 def _check_pair(left, right):
@@ -259,34 +322,42 @@ def interpolate(left, right, config: InterpConfig | None = None, diagnostics: bo
     Returns the interpolated Frame, or (Frame, InterpDiagnostics).  Bit-exact
     with the reference on the same inputs (tests/test_gpu_parity.py).
     """
+    import torch
     cfg = config or InterpConfig()
     _check_pair(left, right)
     eng = _engine(left.width, left.height, left.format, cfg, 1)
-    dl = _to_device(left)[None]
-    dr = _to_device(right)[None]
-    out = eng.pairs(dl, dr)
-    res = frame_from_packed(out[0].cpu().numpy(), left.width, left.height, left.format,
-                            left.timestamp)
-    diag = InterpDiagnostics()
-    if diagnostics or cfg.refine is not None:
-        # per-level flows and match errors (interp.py:114-128); the per-level
-        # masks / blend_luma of levels 0-1 are not produced by this path (None)
-        for s in range(3):
-            flr, frl, elr, erl = (t.cpu().numpy() for t in eng.level_diagnostics(0, s))
-            h, w = flr.shape[:2]
-            diag.scales.append(ScaleDiagnostics(FlowField(w, h, flr), FlowField(w, h, frl), elr, erl))
-        _, _, m = eng.diagnostics(0)
-        m = m.cpu().numpy()
-        f_lr, f_rl = diag.scales[-1].flow_lr, diag.scales[-1].flow_rl
-        diag.flow_mid_left = f_lr.scaled(-0.5)
-        diag.flow_mid_right = f_rl.scaled(-0.5)
-        diag.mask = m
-        diag.scales[-1].mask = m
+    with torch.cuda.stream(_thread_stream()):
+        dl = _to_device(left, "in0")[None]
+        dr = _to_device(right, "in1")[None]
+        out = eng.pairs(dl, dr)
+        res = frame_from_packed(_to_host(out[0]), left.width, left.height, left.format,
+                                left.timestamp)
+        diag = InterpDiagnostics()
+        if diagnostics or cfg.refine is not None:
+            diag = _diagnostics(eng)
     if cfg.refine is not None:  # the reference's one plugin hook (interp.py:144-145)
         res = cfg.refine(res, diag)
     if diagnostics:
         return res, diag
     return res
+
+
+def _diagnostics(eng: Interpolator) -> InterpDiagnostics:
+    """InterpDiagnostics of pair 0 of the engine's most recent batch (interp.py:114-141)."""
+    diag = InterpDiagnostics()
+    # per-level flows and match errors (interp.py:114-128)
+    for s in range(3):
+        flr, frl, elr, erl = (_to_host(t, "diag") for t in eng.level_diagnostics(0, s))
+        h, w = flr.shape[:2]
+        diag.scales.append(ScaleDiagnostics(FlowField(w, h, flr), FlowField(w, h, frl), elr, erl))
+    _, _, m = eng.diagnostics(0)
+    m = _to_host(m, "diag")
+    f_lr, f_rl = diag.scales[-1].flow_lr, diag.scales[-1].flow_rl
+    diag.flow_mid_left = f_lr.scaled(-0.5)
+    diag.flow_mid_right = f_rl.scaled(-0.5)
+    diag.mask = m
+    diag.scales[-1].mask = m
+    return diag
 
 
 def dense_views(left, right, stages: int, config: InterpConfig | None = None) -> list:
@@ -308,6 +379,8 @@ def dense_views(left, right, stages: int, config: InterpConfig | None = None) ->
             nxt.append(seq[-1])
             seq = nxt
         return seq[1:-1]
+    import torch
     eng = _engine(left.width, left.height, left.format, cfg, 1 << (stages - 1))
-    views = eng.dense(_to_device(left), _to_device(right), stages).cpu().numpy()
+    with torch.cuda.stream(_thread_stream()):
+        views = _to_host(eng.dense(_to_device(left, "in0"), _to_device(right, "in1"), stages))
     return [frame_from_packed(v, left.width, left.height, left.format, left.timestamp) for v in views]

@@ -1,0 +1,173 @@
+"""Parity of the code path the bench times, at the BASELINE sizes.
+
+The headline number runs launch variants that small inputs never reach
+(k_scan_carry's cooperative staging from ~600 one-warp CTAs, k_sadw's
+stacked blocks from 2 CTAs per SM).  These tests run:
+
+* the full cfg4 rig frame (8 cameras 1080p YUV420, 4 stages, 105 views, 8
+  cluster frames) through `RigPipeline` -- the graph the bench replays --
+  against the oracle, byte for byte (views and clusters);
+* cfg2's `dense_views(..., 3)` at 1080p;
+* every golden vector and ragged sizes with each launch variant FORCED on
+  and off (fvv_engine_set_tuning), including partial scan chunks;
+* `assemble_cluster_frame` (k_assemble, the kernel plugin.install binds into
+  the reference's `_stitch`) for gray and 4:2:0 with a part-empty last column;
+* the drop-in `dense_views` from a 2-worker ThreadPoolExecutor, as the
+  reference's `PipelineHandle._interp` calls it (server/pipeline.py:219-220,
+  264-268).
+"""
+import numpy as np
+import pytest
+
+from bench import synth_rig
+from conftest import golden_names, load_golden
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+VARIANTS = {"all_on": dict(scan_coop_min=0, sadw_rb_min_ctas=0),
+            "all_off": dict(scan_coop_min=1 << 30, sadw_rb_min_ctas=1 << 30)}
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    return torch
+
+
+def _pairs(torch, w, h, fmt, lefts, rights, cfg=None, **tuning):
+    from paper_2112_10603_b200.interp import Interpolator
+    eng = Interpolator(w, h, fmt, cfg, max_pairs=len(lefts)).set_tuning(**tuning)
+    out = eng.pairs(torch.from_numpy(np.stack(lefts)).cuda(), torch.from_numpy(np.stack(rights)).cuda())
+    torch.cuda.synchronize()
+    return eng, out.cpu().numpy()
+
+
+def test_cfg4_rig_frame_vs_oracle(torch_cuda):
+    """The bench's timed step (BASELINE config 4), default launch variants: the
+    56-pair stage runs k_scan_carry<COOP> (1904 CTAs) and stacked k_sadw."""
+    from paper_2112_10603_b200.pipeline import RigPipeline
+    import paper_2112_10603_b200 as fv
+    W, H, fmt, C, stages, vps = 1920, 1080, 1, 8, 4, 16
+    cams = synth_rig(W, H, fmt, C)
+    pipe = RigPipeline(W, H, fmt, C, stages, vps)
+    out = pipe.process_frames([fv.frame_from_packed(c, W, H, fmt) for c in cams])
+    views = pipe.views_host()
+    ref_views = O.rig_dense_views(cams, W, H, fmt, stages)
+    bad = [i for i in range(ref_views.shape[0]) if not np.array_equal(views[i], ref_views[i])]
+    assert not bad, f"views differing from the oracle: {bad}"
+    total = ref_views.shape[0]
+    for c, cf in enumerate(out):
+        anchor = c << stages
+        lo, hi = max(0, anchor - vps), min(total - 1, anchor + vps)
+        smalls = np.stack([O.downscale(ref_views[i], W, H, fmt, 4) for i in range(lo, hi + 1) if i != anchor])
+        ref, sw = O.assemble_cluster(ref_views[anchor], W, H, fmt, smalls)
+        assert cf.frame.width == sw
+        assert np.array_equal(fv.packed(cf.frame), ref), f"cluster {c}"
+
+
+def test_cfg2_dense_1080p_vs_oracle(torch_cuda):
+    """BASELINE config 2: one 1080p pair, dense_views(n=3) = 7 recursive views."""
+    from paper_2112_10603_b200.interp import Interpolator
+    cams = synth_rig(1920, 1080, 1, 2, seed=7)
+    eng = Interpolator(1920, 1080, 1, max_pairs=4)
+    v = eng.dense(torch_cuda.from_numpy(cams[0]).cuda(), torch_cuda.from_numpy(cams[1]).cuda(), 3)
+    ref = O.dense_views(cams[0], cams[1], 1920, 1080, 1, 3)
+    got = v.cpu().numpy()
+    for i in range(7):
+        assert np.array_equal(got[i], ref[i]), f"view {i + 1}: {np.count_nonzero(got[i] != ref[i])} bytes differ"
+
+
+@pytest.mark.parametrize("variant", sorted(VARIANTS))
+@pytest.mark.parametrize("name", golden_names("interp"))
+def test_goldens_with_forced_variants(torch_cuda, name, variant):
+    g = load_golden(name)
+    w, h, fmt = int(g["w"]), int(g["h"]), int(g["fmt"])
+    eng, out = _pairs(torch_cuda, w, h, fmt, [g["left"]], [g["right"]], **VARIANTS[variant])
+    assert np.array_equal(out[0], g["out"]), f"{name}/{variant}: {np.count_nonzero(out[0] != g['out'])} bytes differ"
+    if "mask" in g:
+        _, _, m = eng.diagnostics(0)
+        assert np.array_equal(m.cpu().numpy(), g["mask"])
+
+
+@pytest.mark.parametrize("variant", sorted(VARIANTS))
+@pytest.mark.parametrize("w,h,fmt", [(1000, 604, 1), (328, 200, 0), (264, 136, 2), (1920, 1080, 1)])
+def test_ragged_batches_with_forced_variants(torch_cuda, w, h, fmt, variant):
+    """Partial scan chunks (width % 64 != 0), ragged block grids, RGB: each
+    launch variant forced, several pairs per launch, vs the oracle."""
+    rng = np.random.default_rng(w * 7 + h + fmt)
+    cams = synth_rig(w, h, fmt, 3, seed=int(rng.integers(1 << 30)))
+    noise = rng.integers(0, 256, cams.shape[1], dtype=np.uint8)
+    lefts, rights = [cams[0], cams[1], cams[2], noise], [cams[1], cams[2], cams[0], cams[0]]
+    _, out = _pairs(torch_cuda, w, h, fmt, lefts, rights, **VARIANTS[variant])
+    for i in range(len(lefts)):
+        ref = O.interpolate(lefts[i], rights[i], w, h, fmt)
+        assert np.array_equal(out[i], ref), f"pair {i}: {np.count_nonzero(out[i] != ref)} bytes differ"
+
+
+def test_18_pair_1080p_batch_default_variants(torch_cuda):
+    """>= 18 1080p pairs in ONE launch: 34 x 18 = 612 scan CTAs, so the default
+    threshold (600) selects k_scan_carry<COOP> as in the timed cfg4 stages."""
+    W, H, fmt = 1920, 1080, 1
+    cams = synth_rig(W, H, fmt, 8, seed=18)
+    lefts = [cams[i] for i in range(7)] + [cams[i + 1] for i in range(7)] + [cams[i] for i in range(4)]
+    rights = [cams[i + 1] for i in range(7)] + [cams[i] for i in range(7)] + [cams[i + 2] for i in range(4)]
+    _, out = _pairs(torch_cuda, W, H, fmt, lefts, rights)
+    for i in range(len(lefts)):
+        ref = O.interpolate(lefts[i], rights[i], W, H, fmt)
+        assert np.array_equal(out[i], ref), f"pair {i}: {np.count_nonzero(out[i] != ref)} bytes differ"
+
+
+@pytest.mark.parametrize("fmt,nsmall", [(0, 5), (1, 5), (1, 16), (0, 1), (1, 0)])
+def test_assemble_cluster_frame_vs_oracle(torch_cuda, fmt, nsmall):
+    """cluster.py:143-191 through k_assemble (what plugin.install binds into
+    the reference's _stitch): anchor + quarter tiles, empty cells Y=0 / C=128."""
+    import paper_2112_10603_b200 as fv
+    from paper_2112_10603_b200.cluster import ClusterLayout, TileRef, assemble_cluster_frame
+    W, H = 96, 64
+    rng = np.random.default_rng(fmt * 100 + nsmall)
+    anchor = rng.integers(0, 256, O.frame_bytes(W, H, fmt), dtype=np.uint8)
+    smalls = [rng.integers(0, 256, O.frame_bytes(W // 4, H // 4, fmt), dtype=np.uint8) for _ in range(nsmall)]
+    tiles = [TileRef(i, "quarter") for i in range(nsmall // 2)] + [TileRef(nsmall // 2, "full")] + \
+            [TileRef(i + 1, "quarter") for i in range(nsmall // 2, nsmall)]
+    lay = ClusterLayout(3, nsmall // 2, 0, nsmall, 8, tuple(tiles))
+    cf = assemble_cluster_frame(fv.frame_from_packed(anchor, W, H, fmt),
+                                [fv.frame_from_packed(s, W // 4, H // 4, fmt) for s in smalls], lay)
+    ref, sw = O.assemble_cluster(anchor, W, H, fmt, np.stack(smalls) if smalls else np.zeros((0, 0), np.uint8))
+    assert cf.frame.width == sw and cf.cluster_id == 3
+    assert np.array_equal(fv.packed(cf.frame), ref)
+    full = [r for r in cf.tile_map if r.tier == "full"]
+    assert len(full) == 1 and (full[0].x, full[0].y, full[0].width, full[0].height) == (0, 0, W, H)
+    quarter = [r for r in cf.tile_map if r.tier == "quarter"]
+    for i, r in enumerate(quarter):
+        assert (r.x, r.y) == (W + (i // 4) * (W // 4), (i % 4) * (H // 4))
+        assert np.array_equal(fv.packed(cf.crop(r)), smalls[i])
+
+
+def test_drop_in_dense_views_from_two_threads(torch_cuda):
+    """20 concurrent dense_views calls on distinct pairs from a 2-worker pool
+    (the reference's PipelineHandle._interp pattern): every result bitwise."""
+    from concurrent.futures import ThreadPoolExecutor
+    import paper_2112_10603_b200 as fv
+    W, H, fmt = 160, 96, 1
+    cams = synth_rig(W, H, fmt, 21, seed=5)
+    frames = [fv.frame_from_packed(c, W, H, fmt) for c in cams]
+
+    def job(i):
+        views = fv.dense_views(frames[i], frames[i + 1], 2)
+        return np.stack([fv.packed(v) for v in views])
+
+    with ThreadPoolExecutor(max_workers=2) as ex:
+        got = list(ex.map(job, range(20)))
+    for i in range(20):
+        ref = O.dense_views(cams[i], cams[i + 1], W, H, fmt, 2)
+        assert np.array_equal(got[i], ref), f"gap {i}"
+    # interpolate() with diagnostics from two threads as well
+    with ThreadPoolExecutor(max_workers=2) as ex:
+        res = list(ex.map(lambda i: fv.interpolate(frames[i], frames[i + 1], diagnostics=True), range(8)))
+    for i, (f, d) in enumerate(res):
+        ref, diag = O.interpolate(cams[i], cams[i + 1], W, H, fmt, with_diag=True)
+        assert np.array_equal(fv.packed(f), ref)
+        assert np.array_equal(d.mask, diag["mask"])
