@@ -443,13 +443,61 @@ def run_b200(args, cfg, rank, world, local_rank):
     if rank != 0:
         return 0
 
-    # ---- per-kernel live timing (CUDA events around every stage kernel) -----
+    roofline, launches_per_step = kernel_roofline(
+        args, cfg, eng, lambda: compute_one(0), npairs_total, clk, stream,
+        (lambda: rig_clusters(views, W, H, fmt, C, S, vps, out=clusters)) if vps else None)
+    gpu_launches = launches_per_step * F * args.steps
+
+    # CPU baseline: oracle port on this box's host cores, bounded sample
+    rate, reps, dt, threads = cpu_interp_rate(cfg, budget_s=args.cpu_budget)
+    cpu = {"value": rate, "unit": "views/s", "cores": threads, "kind": "port",
+           "sample": f"{reps} x interpolate() {W}x{H} {FMT_NAME[fmt]} in {dt:.1f}s (oracle/, C port of "
+                     f"the reference path, {threads} threads)"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "views/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8/i32/f64", "data": "synthetic",
+        "config": {"workload": args.config, "desc": cfg["desc"], "width": W, "height": H,
+                   "format": FMT_NAME[fmt], "cameras": C, "stages": S, "views_per_side": vps,
+                   "views_per_rig_frame": step_views, "rig_frames_per_step": F,
+                   "rig_frame_latency_ms": latency_ms,
+                   "parallelism": f"frame-sharded x{world}, {F} rig frames in flight per rank" +
+                                  (" + NCCL gather to rank 0" if world > 1 else ""),
+                   "cuda_graph": graph is not None,
+                   "l2": "working set > L2 (views %.0f MB + workspace %.0f MB per rank)" % (
+                       views.numel() / 1e6, eng.workspace_bytes / 1e6)},
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "views/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / e2e_steps, **e2e_detail},
+        "gpu_launches": gpu_launches,
+        "clocks": clk,
+    }
+    if not args.no_vinet and rank == 0 and min(W, H) >= 64:
+        try:
+            line["vinet"] = run_vinet(cfg, dev, use_graph=not args.no_graph)
+        except Exception as exc:  # the headline line must survive a failure of the secondary path
+            line["vinet"] = {"error": f"{type(exc).__name__}: {exc}"}
+    print(json.dumps(line))
+    return 0
+
+
+def kernel_roofline(args, cfg, eng, run_once, npairs_total, clk, stream, tile_fn=None):
+    """Live per-kernel CUDA-event timing of one rig frame's stage kernels
+    (C-ABI profiling hook) -> the bench line's roofline object for the
+    dominant kernel, and the kernel launches of one rig frame."""
+    import ctypes
+
+    import torch
+    from paper_2112_10603_b200 import _lib
+    W, H = cfg["W"], cfg["H"]
     prof_steps = 3
     L = _lib.load()
     _lib.check(L.fvv_profile_enable(eng._h, 4096))
     with torch.cuda.stream(stream):
         for _ in range(prof_steps):
-            compute_one(0)
+            run_once()
     torch.cuda.synchronize()
     n = 11  # FVV_NUM_KERNEL_CLASSES
     ms_k = (ctypes.c_double * n)()
@@ -459,13 +507,13 @@ def run_b200(args, cfg, rank, world, local_rank):
     per_class = {L.fvv_kernel_class_name(i).decode(): (ms_k[i] / prof_steps, cnt_k[i] // prof_steps)
                  for i in range(n)}
     tile_ms = 0.0
-    if vps:
+    if tile_fn is not None:
         with torch.cuda.stream(stream):
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
             a.record(stream)
             for _ in range(prof_steps):
-                rig_clusters(views, W, H, fmt, C, S, vps, out=clusters)
+                tile_fn()
             b.record(stream)
         torch.cuda.synchronize()
         tile_ms = a.elapsed_time(b) / prof_steps
@@ -514,41 +562,8 @@ def run_b200(args, cfg, rank, world, local_rank):
     for s, (lw, _lh) in enumerate([(W // 4, H // 4), (W // 2, H // 2), (W, H)]):
         if lw % 8:
             launches_per_step += per_class[f"k_sad<{s}>"][1]
-    gpu_launches = launches_per_step * F * args.steps
+    return roofline, launches_per_step
 
-    # CPU baseline: oracle port on this box's host cores, bounded sample
-    rate, reps, dt, threads = cpu_interp_rate(cfg, budget_s=args.cpu_budget)
-    cpu = {"value": rate, "unit": "views/s", "cores": threads, "kind": "port",
-           "sample": f"{reps} x interpolate() {W}x{H} {FMT_NAME[fmt]} in {dt:.1f}s (oracle/, C port of "
-                     f"the reference path, {threads} threads)"}
-
-    line = {
-        "metric": METRIC, "value": value, "unit": "views/s", "n_gpus": world, "steps": args.steps,
-        "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u8/i32/f64", "data": "synthetic",
-        "config": {"workload": args.config, "desc": cfg["desc"], "width": W, "height": H,
-                   "format": FMT_NAME[fmt], "cameras": C, "stages": S, "views_per_side": vps,
-                   "views_per_rig_frame": step_views, "rig_frames_per_step": F,
-                   "rig_frame_latency_ms": latency_ms,
-                   "parallelism": f"frame-sharded x{world}, {F} rig frames in flight per rank" +
-                                  (" + NCCL gather to rank 0" if world > 1 else ""),
-                   "cuda_graph": graph is not None,
-                   "l2": "working set > L2 (views %.0f MB + workspace %.0f MB per rank)" % (
-                       views.numel() / 1e6, eng.workspace_bytes / 1e6)},
-        "roofline": roofline,
-        "cpu_baseline": cpu,
-        "e2e": {"value": e2e_value, "unit": "views/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / e2e_steps, **e2e_detail},
-        "gpu_launches": gpu_launches,
-        "clocks": clk,
-    }
-    if not args.no_vinet and rank == 0 and min(W, H) >= 64:
-        try:
-            line["vinet"] = run_vinet(cfg, dev, use_graph=not args.no_graph)
-        except Exception as exc:  # the headline line must survive a failure of the secondary path
-            line["vinet"] = {"error": f"{type(exc).__name__}: {exc}"}
-    print(json.dumps(line))
-    return 0
 
 
 def vinet_conv_flops(W, H):
@@ -694,6 +709,146 @@ def run_vinet(cfg, dev, steps=10, warmup=3, use_graph=True):
     }
 
 
+def run_b200_gap(args, cfg, rank, world, local_rank):
+    """Gap-sharded rig frame (SURVEY.md sec. 8(e) option 2; cfg3/cfg4 "pairs
+    sharded across B200s"): ONE rig frame per step split over the ranks by
+    contiguous camera gaps (shard.GapShardedRig).  Per step: each rank's dense
+    views + outgoing halo tiles (graph), the halo exchange (NCCL P2P), its
+    cluster frames (graph), the gather of every cluster frame to the
+    encoder-feeding rank 0 (NCCL P2P).  Total work per step is fixed, so the
+    per-rig-frame latency drops with N (scaling "strong")."""
+    import torch
+    import torch.distributed as dist
+    from paper_2112_10603_b200.shard import GapShardedRig, gap_plan
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    W, H, fmt, C, S, vps = cfg["W"], cfg["H"], cfg["fmt"], cfg["cams"], cfg["stages"], cfg["vps"]
+    step_views = (C - 1) * ((1 << S) - 1)
+    rig = GapShardedRig(W, H, fmt, C, S, vps, rank, world, device=dev)
+    p = rig.plan
+    all_cams = synth_rig(W, H, fmt, C, seed=42)
+    host_cams = torch.from_numpy(all_cams[p.cams.start:p.cams.stop] if p.active else all_cams[:1]).pin_memory()
+    ncam_local = len(p.cams)
+    if p.active:
+        rig.cams[:ncam_local].copy_(host_cams)
+    total_cluster_bytes = sum(rig.sizes_by_rank)
+    gathered = torch.empty(total_cluster_bytes, dtype=torch.uint8, device=dev) if rank == 0 else None
+    host_out = torch.empty(total_cluster_bytes, dtype=torch.uint8).pin_memory() if rank == 0 else None
+    stream = torch.cuda.Stream(device=dev)
+
+    def barrier():
+        if world > 1:
+            barrier()
+
+    barrier()  # communicators up before any rank-specific P2P
+
+    g_compute = g_stitch = None
+    if not args.no_graph:
+        with torch.cuda.stream(stream):
+            rig.compute()
+            rig.exchange()
+            rig.stitch()
+        torch.cuda.synchronize()
+        g_compute, g_stitch = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_compute, stream=stream):
+            rig.compute()
+        with torch.cuda.graph(g_stitch, stream=stream):
+            rig.stitch()
+        torch.cuda.synchronize()
+
+    def step(h2d=False, d2h=False):
+        if h2d and p.active:
+            rig.cams[:ncam_local].copy_(host_cams, non_blocking=True)
+        g_compute.replay() if g_compute is not None else rig.compute()
+        rig.exchange()
+        g_stitch.replay() if g_stitch is not None else rig.stitch()
+        res = rig.gather(out=gathered)
+        if d2h and rank == 0:
+            host_out.copy_(res[:total_cluster_bytes], non_blocking=True)
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(args.warmup, 3)):
+            step()
+    torch.cuda.synchronize()
+
+    def all_reduce(v, op="sum"):
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+        return float(t.item())
+
+    def max_over_ranks(v):
+        return all_reduce(v, "max")
+
+    clocks = ClockSampler(local_rank)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        t0.record(stream)
+        for _ in range(args.steps):
+            step()
+        t1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    barrier()
+    ms = max_over_ranks(t0.elapsed_time(t1))
+    ms_per_step = ms / args.steps
+    value = step_views * args.steps / (ms / 1e3)
+
+    # e2e: each rank's camera frames H2D from pinned host memory, rank 0's
+    # cluster frames D2H, every step, inside the timed region
+    e2e_steps = max(3, args.steps // 2)
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            step(h2d=True, d2h=True)
+        e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1))
+    h2d = int(all_reduce(host_cams.numel() if p.active else 0))
+
+    # per-rank kernel share (rank 0's gaps), profiled outside the timed region
+    roofline, launches = None, 0
+    if p.active:
+        npairs_rank = len(p.gaps) * ((1 << S) - 1)
+        roofline, launches = kernel_roofline(args, cfg, rig.engine, rig.compute, npairs_rank, clk, stream,
+                                             rig.stitch)
+    launches_all = int(all_reduce(launches))
+    if rank != 0:
+        return 0
+    gaps_per_rank = [len(gap_plan(C, S, vps, r, world).gaps) for r in range(world)]
+    line = {
+        "metric": METRIC, "value": value, "unit": "views/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u8/i32/f64", "data": "synthetic",
+        "config": {"workload": args.config, "desc": cfg["desc"], "width": W, "height": H,
+                   "format": FMT_NAME[fmt], "cameras": C, "stages": S, "views_per_side": vps,
+                   "views_per_rig_frame": step_views, "rig_frames_per_step": 1,
+                   "rig_frame_latency_ms": ms_per_step,
+                   "parallelism": f"gap-sharded x{world} (gaps per rank {gaps_per_rank}), halo quarter tiles "
+                                  "+ cluster gather to rank 0 over NCCL P2P",
+                   "cuda_graph": g_compute is not None,
+                   "l2": "working set > L2 (views %.0f MB + workspace %.0f MB on rank 0)" % (
+                       rig.views.numel() / 1e6, rig.engine.workspace_bytes / 1e6 if rig.engine else 0)},
+        "roofline": roofline,
+        "cpu_baseline": None,
+        "e2e": {"value": step_views * e2e_steps / (e2e_ms / 1e3), "unit": "views/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": total_cluster_bytes, "ms_per_step": e2e_ms / e2e_steps,
+                "api": "shard.GapShardedRig (compute / exchange / stitch / gather), copies not overlapped"},
+        "gpu_launches": launches_all * args.steps,
+        "clocks": clk,
+    }
+    print(json.dumps(line))
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -706,19 +861,40 @@ def main():
                     help="independent rig frames of the live stream processed concurrently per step")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-vinet", action="store_true", help="skip the VINet (CNN path) section")
+    ap.add_argument("--shard", default="auto", choices=["auto", "gap", "frame"],
+                    help="N>1 partition: gap = one rig frame split by camera gaps (latency; default for "
+                         "tiled rigs that fit, cfg3/cfg4), frame = whole rig frames per rank (throughput, cfg5)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-exec under torchrun (the driver's own launch form)
+        import socket
+        sock = socket.socket()
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+        sock.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        return subprocess.call(cmd)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference(args, cfg, rank, world)
+    shard = args.shard
+    if shard == "auto":
+        shard = "gap" if cfg["vps"] and args.config != "cfg5" else "frame"
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
+        if shard == "gap" and (world > 1 or args.shard == "gap"):
+            return run_b200_gap(args, cfg, rank, world, local_rank)
         return run_b200(args, cfg, rank, world, local_rank)
     finally:
         if world > 1:

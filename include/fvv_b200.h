@@ -156,6 +156,21 @@ size_t fvv_rig_cluster_bytes(const fvv_frame_desc* desc, int ncams, int stages,
 int fvv_rig_clusters(const fvv_frame_desc* desc, int ncams, int stages, int views_per_side,
                      const uint8_t* views, uint8_t* clusters, void* stream);
 
+/* The gap-sharded rig (SURVEY.md sec. 8(e) option 2; bench.py --shard gap):
+ * clusters [first_cluster, first_cluster + ncluster) of the rig's cluster
+ * frames, packed back to back, from a rank's LOCAL views (global indices
+ * [view_base, view_base + nviews)) plus halo tiles -- quarter frames
+ * (fvv_downscale factor 4) of global views [halo_first, halo_first +
+ * halo_count) received from the neighbouring rank.  Cluster c reads views
+ * of gaps c-1 and c (cluster.py:58-74), so the rank owning gap c needs the
+ * top views_per_side views of gap c-1 as halo.  Byte-identical to the
+ * matching clusters of fvv_rig_clusters.  FVV_EINVAL when a needed view is
+ * neither local nor in the halo. */
+int fvv_rig_clusters_shard(const fvv_frame_desc* desc, int ncams, int stages, int views_per_side,
+                           int first_cluster, int ncluster, const uint8_t* views, int view_base,
+                           int nviews, const uint8_t* halo, int halo_first, int halo_count,
+                           uint8_t* clusters, void* stream);
+
 /* ---------------------------------------------------------------------------
  * VINet (SURVEY.md sec. 8(b) "fvv_vinet_flow",
  * north star): the CNN flow / fusion estimator.  The reference ships no CNN

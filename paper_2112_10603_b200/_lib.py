@@ -21,7 +21,7 @@ EXPORTS = (
     "fvv_engine_workspace_size", "fvv_engine_create", "fvv_engine_destroy",
     "fvv_engine_max_pairs", "fvv_engine_set_tuning", "fvv_interpolate_pairs", "fvv_interp_diagnostics",
     "fvv_dense_views", "fvv_rig_views", "fvv_downscale", "fvv_cluster_width",
-    "fvv_assemble_cluster", "fvv_rig_cluster_bytes", "fvv_rig_clusters",
+    "fvv_assemble_cluster", "fvv_rig_cluster_bytes", "fvv_rig_clusters", "fvv_rig_clusters_shard",
     "fvv_profile_enable", "fvv_profile_read", "fvv_kernel_class_name",
     "fvv_interp_level_diagnostics", "fvv_conv2d_bf16", "fvv_vinet_workspace_size", "fvv_vinet_flow",
     "fvv_vinet_synth", "fvv_vinet_rig", "fvv_vinet_rig_clusters",
@@ -86,6 +86,7 @@ def load():
         "fvv_assemble_cluster": (I, [pd, P, PP, I, P, P]),
         "fvv_rig_cluster_bytes": (Z, [pd, I, I, I, I]),
         "fvv_rig_clusters": (I, [pd, I, I, I, P, P, P]),
+        "fvv_rig_clusters_shard": (I, [pd, I, I, I, I, I, P, I, I, P, I, I, P, P]),
         "fvv_profile_enable": (I, [P, I]),
         "fvv_profile_read": (I, [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I), I]),
         "fvv_kernel_class_name": (ctypes.c_char_p, [I]),

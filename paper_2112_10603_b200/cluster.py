@@ -212,3 +212,25 @@ def rig_clusters(views, width: int, height: int, fmt, camera_count: int, stages:
                                   ctypes.c_void_p(views.data_ptr()), ctypes.c_void_p(out.data_ptr()),
                                   _stream()))
     return out, sizes
+
+
+def rig_clusters_shard(views, view_base: int, width: int, height: int, fmt, camera_count: int,
+                       stages: int, views_per_side: int, first_cluster: int, ncluster: int,
+                       halo=None, halo_first: int = 0, halo_count: int = 0, out=None):
+    """Clusters [first_cluster, first_cluster + ncluster) of a rig frame from a
+    rank's local views (global indices view_base..) plus halo quarter tiles
+    (fvv_rig_clusters_shard; the gap-sharded rig of shard.GapShardedRig).
+    Returns (out, sizes)."""
+    import torch
+    L = _lib.require_cuda()
+    sizes = rig_cluster_sizes(width, height, fmt, camera_count, stages,
+                              views_per_side)[first_cluster:first_cluster + ncluster]
+    if out is None:
+        out = torch.empty(max(1, sum(sizes)), dtype=torch.uint8, device=views.device)
+    d = _lib.desc(width, height, int(fmt))
+    _lib.check(L.fvv_rig_clusters_shard(
+        ctypes.byref(d), camera_count, stages, views_per_side, first_cluster, ncluster,
+        ctypes.c_void_p(views.data_ptr()), view_base, views.shape[0],
+        ctypes.c_void_p(halo.data_ptr() if halo is not None else 0), halo_first, halo_count,
+        ctypes.c_void_p(out.data_ptr()), _stream()))
+    return out, sizes

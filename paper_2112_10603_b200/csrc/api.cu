@@ -31,6 +31,9 @@ cudaError_t launch_assemble(int W, int H, int fmt, const uint8_t* anchor,
 cudaError_t launch_rig_clusters(int W, int H, int fmt, const ClusterJob* jobs, int njobs,
                                 long max_cluster_bytes, const uint8_t* views, uint8_t* out,
                                 cudaStream_t st, int skip_period = 0);
+cudaError_t launch_rig_clusters_src(int W, int H, int fmt, const ClusterJob* jobs, int njobs,
+                                    long max_cluster_bytes, const ViewSrc& vs, uint8_t* out,
+                                    cudaStream_t st, int skip_period);
 }  // namespace fvv
 
 using namespace fvv;
@@ -575,6 +578,46 @@ int fvv_rig_clusters(const fvv_frame_desc* d, int ncams, int stages, int vps,
     cudaError_t ce = launch_rig_clusters(d->width, d->height, d->format, jobs.data(), ncams, maxb,
                                          views, clusters, static_cast<cudaStream_t>(stream));
     if (ce != cudaSuccess) return cuda_fail(ce, "rig_clusters");
+    return FVV_OK;
+}
+
+int fvv_rig_clusters_shard(const fvv_frame_desc* d, int ncams, int stages, int vps, int first_cluster,
+                           int ncluster, const uint8_t* views, int view_base, int nviews,
+                           const uint8_t* halo, int halo_first, int halo_count, uint8_t* clusters,
+                           void* stream) {
+    std::vector<ClusterJob> all;
+    long maxb = 0;
+    int rc = cluster_jobs_of(d, ncams, stages, vps, &all, &maxb);
+    if (rc) return rc;
+    if (ncluster == 0) return FVV_OK;
+    if (first_cluster < 0 || ncluster < 0 || first_cluster + ncluster > ncams)
+        return fail(FVV_EINVAL, "cluster range outside the rig");
+    if (!views || !clusters || nviews < 1 || view_base < 0)
+        return fail(FVV_EINVAL, "null or empty local views");
+    if (halo_count < 0 || (halo_count > 0 && !halo)) return fail(FVV_EINVAL, "bad halo tiles");
+    auto local = [&](int vi) { return vi >= view_base && vi < view_base + nviews; };
+    auto in_halo = [&](int vi) { return vi >= halo_first && vi < halo_first + halo_count; };
+    std::vector<ClusterJob> jobs(all.begin() + first_cluster, all.begin() + first_cluster + ncluster);
+    const long off0 = jobs[0].out_offset;
+    maxb = 0;
+    for (ClusterJob& j : jobs) {
+        j.out_offset -= off0;
+        if (!local(j.anchor_view))
+            return fail(FVV_EINVAL, "anchor view " + std::to_string(j.anchor_view) + " is not in the local views");
+        for (int i = 0; i < j.nsmall; i++) {
+            int vi = j.first_small + i;
+            if (vi >= j.skip) vi += 1;
+            if (!local(vi) && !in_halo(vi))
+                return fail(FVV_EINVAL, "view " + std::to_string(vi) + " of cluster " +
+                                            std::to_string(&j - jobs.data() + first_cluster) +
+                                            " is neither local nor in the halo");
+        }
+        maxb = std::max(maxb, (long)fvv_rig_cluster_bytes(d, ncams, stages, vps, (int)(&j - jobs.data()) + first_cluster));
+    }
+    ViewSrc vs{views, view_base, halo, halo_first, halo_count};
+    cudaError_t ce = launch_rig_clusters_src(d->width, d->height, d->format, jobs.data(), ncluster, maxb, vs,
+                                             clusters, static_cast<cudaStream_t>(stream), 0);
+    if (ce != cudaSuccess) return cuda_fail(ce, "rig_clusters_shard");
     return FVV_OK;
 }
 

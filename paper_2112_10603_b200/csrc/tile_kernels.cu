@@ -79,8 +79,9 @@ __global__ void k_downscale(FrameDims s, FrameDims q, int f, const uint8_t* __re
 // Scalar form: one thread = one stitched byte (any geometry the reference accepts).
 // skip_period > 0: tiles of views whose index is not a multiple of skip_period
 // (the synthesized ones) were written by the synthesis kernel (fused tiling).
-__global__ void k_rig_clusters_1(FrameDims fd, ClusterJobs jobs, const uint8_t* __restrict__ views,
+__global__ void k_rig_clusters_1(FrameDims fd, ClusterJobs jobs, ViewSrc vs,
                                  uint8_t* __restrict__ clusters, int skip_period) {
+    const uint8_t* __restrict__ views = vs.views;
     const ClusterJob jb = jobs.job[blockIdx.z];
     const int sw = jb.sw, sh = fd.H;
     const long ysz = (long)sw * sh;
@@ -98,7 +99,7 @@ __global__ void k_rig_clusters_1(FrameDims fd, ClusterJobs jobs, const uint8_t* 
     const int bx = p ? 2 * x : x, byy = p ? 2 * y : y;
     uint8_t v;
     if (bx < W) {
-        const uint8_t* a = views + (long)jb.anchor_view * fd.bytes;
+        const uint8_t* a = views + (long)(jb.anchor_view - vs.view_base) * fd.bytes;
         v = p ? a[(long)W * H + (p - 1) * (long)fd.cw * fd.ch + (long)y * fd.cw + x] : a[(long)y * W + x];
     } else {
         const int col = (bx - W) / cellw, row = byy / cellh;
@@ -109,15 +110,22 @@ __global__ void k_rig_clusters_1(FrameDims fd, ClusterJobs jobs, const uint8_t* 
             int vi = jb.first_small + i;
             if (vi >= jb.skip) vi += 1;
             if (skip_period && vi % skip_period) return;
-            const uint8_t* src = views + (long)vi * fd.bytes;
             const int tx = p ? x - (W + col * cellw) / 2 : x - (W + col * cellw);
             const int ty = p ? y - (row * cellh) / 2 : y - row * cellh;
-            const uint8_t* pl = p ? src + (long)W * H + (p - 1) * (long)fd.cw * fd.ch : src;
-            const int spw = p ? fd.cw : W;
-            int acc = 0;
-            for (int ii = 0; ii < 4; ii++)
-                for (int jj = 0; jj < 4; jj++) acc += pl[(long)(ty * 4 + ii) * spw + tx * 4 + jj];
-            v = box_round(acc, 16);
+            if (vi - vs.halo_first >= 0 && vi - vs.halo_first < vs.halo_count) {  // pre-downscaled
+                const FrameDims qd = dims_of(cellw, cellh, fd.fmt);
+                const uint8_t* q = vs.halo + (long)(vi - vs.halo_first) * qd.bytes;
+                v = p ? q[(long)cellw * cellh + (p - 1) * (long)qd.cw * qd.ch + (long)ty * qd.cw + tx]
+                      : q[(long)ty * cellw + tx];
+            } else {
+                const uint8_t* src = views + (long)(vi - vs.view_base) * fd.bytes;
+                const uint8_t* pl = p ? src + (long)W * H + (p - 1) * (long)fd.cw * fd.ch : src;
+                const int spw = p ? fd.cw : W;
+                int acc = 0;
+                for (int ii = 0; ii < 4; ii++)
+                    for (int jj = 0; jj < 4; jj++) acc += pl[(long)(ty * 4 + ii) * spw + tx * 4 + jj];
+                v = box_round(acc, 16);
+            }
         }
     }
     clusters[jb.out_offset + o] = v;
@@ -128,8 +136,9 @@ __global__ void k_rig_clusters_1(FrameDims fd, ClusterJobs jobs, const uint8_t* 
 // read per source row), or padding (0 luma / 128 chroma).  With W % 32 == 0
 // every cell edge and source row is 16-byte aligned, so a group never
 // straddles a cell.
-__global__ void k_rig_clusters(FrameDims fd, ClusterJobs jobs, const uint8_t* __restrict__ views,
+__global__ void k_rig_clusters(FrameDims fd, ClusterJobs jobs, ViewSrc vs,
                                uint8_t* __restrict__ clusters, int skip_period) {
+    const uint8_t* __restrict__ views = vs.views;
     const ClusterJob jb = jobs.job[blockIdx.z];
     const int sw = jb.sw, sh = fd.H;
     const long ysz = (long)sw * sh;
@@ -147,7 +156,7 @@ __global__ void k_rig_clusters(FrameDims fd, ClusterJobs jobs, const uint8_t* __
     const int bx = p ? 2 * x : x, byy = p ? 2 * y : y;  // luma-grid position
     uchar4 v;
     if (bx < W) {
-        const uint8_t* a = views + (long)jb.anchor_view * fd.bytes;
+        const uint8_t* a = views + (long)(jb.anchor_view - vs.view_base) * fd.bytes;
         const uint8_t* src = p ? a + (long)W * H + (p - 1) * (long)fd.cw * fd.ch + (long)y * fd.cw + x
                                : a + (long)y * W + x;
         v = *reinterpret_cast<const uchar4*>(src);
@@ -161,9 +170,17 @@ __global__ void k_rig_clusters(FrameDims fd, ClusterJobs jobs, const uint8_t* __
             int vi = jb.first_small + i;
             if (vi >= jb.skip) vi += 1;
             if (skip_period && vi % skip_period) return;
-            const uint8_t* src = views + (long)vi * fd.bytes;
             const int tx = p ? x - (W + col * cellw) / 2 : x - (W + col * cellw);
             const int ty = p ? y - (row * cellh) / 2 : y - row * cellh;
+            if (vi - vs.halo_first >= 0 && vi - vs.halo_first < vs.halo_count) {  // pre-downscaled
+                const FrameDims qd = dims_of(cellw, cellh, fd.fmt);
+                const uint8_t* q = vs.halo + (long)(vi - vs.halo_first) * qd.bytes;
+                const uint8_t* qs = p ? q + (long)cellw * cellh + (p - 1) * (long)qd.cw * qd.ch + (long)ty * qd.cw + tx
+                                      : q + (long)ty * cellw + tx;
+                *reinterpret_cast<uchar4*>(clusters + jb.out_offset + o) = *reinterpret_cast<const uchar4*>(qs);
+                return;
+            }
+            const uint8_t* src = views + (long)(vi - vs.view_base) * fd.bytes;
             const uint8_t* pl = p ? src + (long)W * H + (p - 1) * (long)fd.cw * fd.ch : src;
             const int spw = p ? fd.cw : W;
             int acc[4] = {0, 0, 0, 0};
@@ -226,6 +243,10 @@ __global__ void k_assemble(FrameDims fd, int nsmall, int sw, const uint8_t* __re
     out[o] = v;
 }
 
+cudaError_t launch_rig_clusters_src(int W, int H, int fmt, const ClusterJob* jobs, int njobs,
+                                    long max_cluster_bytes, const ViewSrc& vs, uint8_t* out,
+                                    cudaStream_t st, int skip_period);
+
 cudaError_t launch_downscale(int W, int H, int fmt, const uint8_t* frames, int n, int f,
                              uint8_t* out, cudaStream_t st) {
     FrameDims s = dims_of(W, H, fmt), q = dims_of(W / f, H / f, fmt);
@@ -249,6 +270,13 @@ cudaError_t launch_assemble(int W, int H, int fmt, const uint8_t* anchor,
 cudaError_t launch_rig_clusters(int W, int H, int fmt, const ClusterJob* jobs, int njobs,
                                 long max_cluster_bytes, const uint8_t* views, uint8_t* out,
                                 cudaStream_t st, int skip_period) {
+    ViewSrc vs{views, 0, nullptr, 0, 0};
+    return launch_rig_clusters_src(W, H, fmt, jobs, njobs, max_cluster_bytes, vs, out, st, skip_period);
+}
+
+cudaError_t launch_rig_clusters_src(int W, int H, int fmt, const ClusterJob* jobs, int njobs,
+                                    long max_cluster_bytes, const ViewSrc& vs, uint8_t* out,
+                                    cudaStream_t st, int skip_period) {
     FrameDims fd = dims_of(W, H, fmt);
     for (int b = 0; b < njobs; b += kMaxClusters) {
         ClusterJobs cj;
@@ -256,10 +284,10 @@ cudaError_t launch_rig_clusters(int W, int H, int fmt, const ClusterJob* jobs, i
         for (int i = 0; i < n; i++) cj.job[i] = jobs[b + i];
         if (W % 32 == 0) {
             dim3 grd((unsigned)((max_cluster_bytes / 4 + 255) / 256), 1, n);
-            k_rig_clusters<<<grd, 256, 0, st>>>(fd, cj, views, out, skip_period);
+            k_rig_clusters<<<grd, 256, 0, st>>>(fd, cj, vs, out, skip_period);
         } else {
             dim3 grd((unsigned)((max_cluster_bytes + 255) / 256), 1, n);
-            k_rig_clusters_1<<<grd, 256, 0, st>>>(fd, cj, views, out, skip_period);
+            k_rig_clusters_1<<<grd, 256, 0, st>>>(fd, cj, vs, out, skip_period);
         }
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;

@@ -171,3 +171,35 @@ def test_drop_in_dense_views_from_two_threads(torch_cuda):
         ref, diag = O.interpolate(cams[i], cams[i + 1], W, H, fmt, with_diag=True)
         assert np.array_equal(fv.packed(f), ref)
         assert np.array_equal(d.mask, diag["mask"])
+
+
+@pytest.mark.parametrize("world,W,H,C,stages,vps", [(2, 1920, 1080, 8, 4, 16), (3, 96, 64, 5, 2, 3),
+                                                     (8, 64, 48, 8, 2, 4)])
+def test_gap_sharded_rig_device_vs_unsharded(torch_cuda, world, W, H, C, stages, vps):
+    """Every rank's share of a gap-sharded rig frame (GapShardedRig), run one
+    rank after another on this GPU with the halo handed over by a device copy
+    (the NCCL exchange itself is covered on gloo): the gathered clusters equal
+    fvv_rig_clusters of the whole rig, byte for byte."""
+    import torch
+    from paper_2112_10603_b200.cluster import rig_clusters
+    from paper_2112_10603_b200.interp import Interpolator
+    from paper_2112_10603_b200.shard import GapShardedRig
+    fmt = 1
+    cams = torch.from_numpy(synth_rig(W, H, fmt, C, seed=3)).cuda()
+    ranks = [GapShardedRig(W, H, fmt, C, stages, vps, r, world) for r in range(world)]
+    for rk in ranks:
+        p = rk.plan
+        if p.active:
+            rk.cams[:len(p.cams)].copy_(cams[p.cams.start:p.cams.stop])
+        rk.compute()
+    for rk in ranks:
+        if rk.plan.halo_in is not None:
+            rk.halo_recv.copy_(ranks[rk.plan.halo_in[0]].halo_send)
+        rk.stitch()
+    torch.cuda.synchronize()
+    got = torch.cat([rk.clusters[:sum(rk.cluster_sizes)] for rk in ranks if rk.cluster_sizes]).cpu().numpy()
+    eng = Interpolator(W, H, fmt, max_pairs=(C - 1) << (stages - 1))
+    views = eng.rig(cams, stages)
+    ref, sizes = rig_clusters(views, W, H, fmt, C, stages, vps)
+    assert got.size == sum(sizes)
+    assert np.array_equal(got, ref.cpu().numpy())
