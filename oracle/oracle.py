@@ -5,7 +5,7 @@ and bench.py's cpu_baseline / ``--impl reference`` leg -- never from the
 product package ``paper_2112_10603_b200``.  It restates the reference path
 (/root/reference/pkg/src/fvv: interp.py:67-170, flow.py:40-131,
 warp.py:27-88, imageops.py:10-56, _kernels.py:28-193, cluster.py:77-191)
-literally in C; tests/test_oracle_vs_reference.py pins it against the
+literally in C; tests/test_oracle_vs_reference.py pins it against the live
 reference itself, and tests/golden/ holds vectors the reference produced.
 
 Frames cross this boundary as packed plane bytes in the reference's

@@ -203,3 +203,40 @@ def test_gap_sharded_rig_device_vs_unsharded(torch_cuda, world, W, H, C, stages,
     ref, sizes = rig_clusters(views, W, H, fmt, C, stages, vps)
     assert got.size == sum(sizes)
     assert np.array_equal(got, ref.cpu().numpy())
+
+
+def _sha(a) -> str:
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def test_1080p_pair_vs_reference_golden(torch_cuda):
+    """The CUDA path against the REFERENCE's own 1080p output (no oracle in
+    between): tests/golden/ref1080_pair.npz, inputs regenerated from the seed."""
+    g = load_golden("ref1080_pair")
+    w, h = int(g["w"]), int(g["h"])
+    cams = synth_rig(w, h, 1, int(g["cams"]), seed=int(g["seed"]))
+    eng, out = _pairs(torch_cuda, w, h, 1, [cams[0]], [cams[1]])
+    assert np.array_equal(out[0], g["out"])
+    flr, frl, m = (t.cpu().numpy() for t in eng.diagnostics(0))
+    assert _sha(flr) == str(g["flow_lr_sha"]) and _sha(frl) == str(g["flow_rl_sha"])
+    assert _sha(m) == str(g["mask_sha"])
+
+
+def test_cfg3_rig_vs_reference_golden(torch_cuda):
+    """BASELINE config 3 through RigPipeline (graph replay): all 45 views' and 4
+    cluster frames' SHA-256 equal the reference's (tests/golden/ref1080_cfg3.npz),
+    and the tile maps equal the reference's TileRects."""
+    import paper_2112_10603_b200 as fv
+    from paper_2112_10603_b200.pipeline import RigPipeline
+    g = load_golden("ref1080_cfg3")
+    w, h, C, S, vps = int(g["w"]), int(g["h"]), int(g["cams"]), int(g["stages"]), int(g["vps"])
+    cams = synth_rig(w, h, 1, C, seed=int(g["seed"]))
+    pipe = RigPipeline(w, h, 1, C, S, vps)
+    out = pipe.process_frames([fv.frame_from_packed(c, w, h, 1) for c in cams])
+    views = pipe.views_host()
+    assert [_sha(v) for v in views] == [str(s) for s in g["view_sha"]]
+    assert [_sha(fv.packed(c.frame)) for c in out] == [str(s) for s in g["cluster_sha"]]
+    rects = np.array([[r.index, r.tier == "full", r.x, r.y, r.width, r.height] for c in out for r in c.tile_map],
+                     np.int32)
+    assert np.array_equal(rects, g["rects"])
