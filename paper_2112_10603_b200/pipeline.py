@@ -184,3 +184,101 @@ class RigPipeline:
     @property
     def frame_bytes(self) -> int:
         return frame_nbytes(self.width, self.height, self.format)
+
+
+class DeviceRigStages:
+    """Device-resident state behind the reference pipeline's `_interp` and
+    `_stitch` stage workers (server/pipeline.py:254-292), installed by
+    `plugin.install(fvv, pipeline=True)`.
+
+    `interp(cams)` uploads one tick's camera Frames and synthesises every dense
+    view into a device slot (fvv_rig_views), returning the slot number -- the
+    only thing the views channel then carries (no byte bundling of 45-105
+    frames).  `stitch(slot)` builds every cluster frame of that slot on the
+    device (fvv_rig_clusters) and downloads them for the host encoder stage.
+    The two run on their own threads and CUDA streams; events order a slot's
+    views before its stitch and its stitch before the slot's reuse.  `slots`
+    must exceed the views channel's capacity + 1 (the pipeline's back-pressure
+    then guarantees a slot is stitched before it is rewritten).
+    """
+
+    def __init__(self, width: int, height: int, fmt, camera_count: int, stages: int, views_per_side: int,
+                 config: InterpConfig | None = None, slots: int = 6, device=None):
+        import torch
+        _lib.require_cuda()
+        self.model = ViewIndexModel(camera_count, stages)
+        self.width, self.height, self.format = int(width), int(height), PixelFormat(int(fmt))
+        self.views_per_side = int(views_per_side)
+        self.layouts = build_layouts(self.model, self.views_per_side)
+        self.engine = Interpolator(width, height, fmt, config, max_pairs=(camera_count - 1) << (stages - 1),
+                                   device=device)
+        dev = self.engine.device
+        fb = self.engine.frame_bytes
+        self.slots = int(slots)
+        self.cams = [torch.empty((camera_count, fb), dtype=torch.uint8, device=dev) for _ in range(self.slots)]
+        self.views = [torch.empty((self.model.total_views, fb), dtype=torch.uint8, device=dev)
+                      for _ in range(self.slots)]
+        self.tiled = int(fmt) != PixelFormat.RGB8
+        self.sizes = rig_cluster_sizes(width, height, fmt, camera_count, stages, self.views_per_side) \
+            if self.tiled else []
+        self.clusters = torch.empty(max(1, sum(self.sizes)), dtype=torch.uint8, device=dev)
+        self._host_in = torch.empty((camera_count, fb), dtype=torch.uint8).pin_memory()
+        self._host_out = torch.empty(self.clusters.numel(), dtype=torch.uint8).pin_memory()
+        self.s_interp = torch.cuda.Stream(device=dev)
+        self.s_stitch = torch.cuda.Stream(device=dev)
+        self._ev_views = [torch.cuda.Event() for _ in range(self.slots)]
+        self._ev_free = [None] * self.slots
+        self._stamps = [None] * self.slots
+        self._next = 0
+
+    def interp(self, frames) -> int:
+        """One tick's camera Frames -> every global view in a device slot."""
+        import torch
+        if len(frames) != self.model.camera_count:
+            raise ValueError(f"rig has {self.model.camera_count} cameras, got {len(frames)} frames")
+        for i, f in enumerate(frames):
+            if (f.width, f.height, int(f.format)) != (self.width, self.height, int(self.format)):
+                raise ValueError("interpolation inputs must share size and format")
+            self._host_in[i].copy_(torch.from_numpy(packed(f)))
+        k = self._next
+        self._next = (k + 1) % self.slots
+        with torch.cuda.stream(self.s_interp):
+            if self._ev_free[k] is not None:
+                self.s_interp.wait_event(self._ev_free[k])  # the slot's previous tick is stitched
+            self.cams[k].copy_(self._host_in, non_blocking=True)
+            self.engine.rig(self.cams[k], self.model.stages, self.views[k])
+            self._ev_views[k].record(self.s_interp)
+        self._stamps[k] = [f.timestamp for f in frames]
+        self.s_interp.synchronize()  # the stage's latency is real; the pinned input is free again
+        return k
+
+    def stitch(self, slot: int) -> list:
+        """Every cluster frame of the tick in `slot` (host ClusterFrames)."""
+        import torch
+        from .cluster import LayoutError
+        if not self.tiled:
+            raise LayoutError("cluster frames are gray or 4:2:0")
+        with torch.cuda.stream(self.s_stitch):
+            self.s_stitch.wait_event(self._ev_views[slot])
+            rig_clusters(self.views[slot], self.width, self.height, self.format, self.model.camera_count,
+                         self.model.stages, self.views_per_side, out=self.clusters)
+            ev = torch.cuda.Event()
+            ev.record(self.s_stitch)
+            self._ev_free[slot] = ev
+            self._host_out.copy_(self.clusters, non_blocking=True)
+        self.s_stitch.synchronize()
+        host = self._host_out.numpy()
+        stamps = self._stamps[slot]
+        out, off = [], 0
+        for lay, size in zip(self.layouts, self.sizes):
+            sw = (size * 2) // (3 * self.height) if int(self.format) == PixelFormat.YUV420 \
+                else size // self.height
+            fr = frame_from_packed(host[off:off + size].copy(), sw, self.height, self.format,
+                                   stamps[lay.anchor_index >> self.model.stages])
+            out.append(ClusterFrame(lay.cluster_id, fr, tile_rects(lay, self.width, self.height)))
+            off += size
+        return out
+
+    def views_host(self, slot: int) -> np.ndarray:
+        self.s_interp.synchronize()
+        return self.views[slot].cpu().numpy()

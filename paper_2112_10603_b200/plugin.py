@@ -13,10 +13,22 @@ CLI run the CUDA path unchanged:
 
 Frames flow in and out as the reference's own `fvv.frame.Frame` objects.
 `uninstall(fvv)` restores the originals.
+
+`install(fvv, pipeline=True)` additionally replaces the two GPU stage
+workers of the reference's live pipeline, `PipelineHandle._interp` and
+`PipelineHandle._stitch` (server/pipeline.py:254-292), with device-resident
+ones: the views of a tick stay in HBM between
+the two stages (pipeline.DeviceRigStages) and the views channel carries a
+slot number instead of a byte bundle of every view.  The channels, the
+stage-latency report, the trace stamps and the host stages around them
+(capture, encode, segment) are the reference's own.
 """
 from __future__ import annotations
 
 import importlib
+import struct
+import threading
+import time
 
 from . import cluster as _cluster
 from . import interp as _interp
@@ -31,7 +43,10 @@ def _ref_frame(fvv_frame_mod, ours, template):
                                tuple(ours.planes), ours.timestamp)
 
 
-def install(fvv) -> None:
+def install(fvv, pipeline: bool = False, stages_factory=None) -> None:
+    """Rebind the reference's path names (and, with `pipeline`, its stage
+    workers).  `stages_factory(width, height, fmt, cams, stages, vps, config,
+    slots)` builds the device stage state; default pipeline.DeviceRigStages."""
     frame_mod = importlib.import_module(fvv.__name__ + ".frame")
     interp_mod = importlib.import_module(fvv.__name__ + ".interp")
     cluster_mod = importlib.import_module(fvv.__name__ + ".cluster")
@@ -86,9 +101,72 @@ def install(fvv) -> None:
             if hasattr(m, n):
                 src = interp_mod if n in ("interpolate", "dense_views") else cluster_mod
                 repl[(m, n)] = repl[(src, n)]
+    if pipeline:
+        pl = importlib.import_module(fvv.__name__ + ".server.pipeline")
+        hooks = _pipeline_hooks(pl, frame_mod, stages_factory)
+        for n, f in hooks.items():
+            repl[(pl.PipelineHandle, n)] = f
     for (m, n), f in repl.items():
         _SAVED.setdefault((m, n), getattr(m, n))
         setattr(m, n, f)
+
+
+_TOKEN = struct.Struct("<4sI")  # views-channel payload: magic + device slot
+
+
+def _pipeline_hooks(pl, frame_mod, stages_factory):
+    """Device-resident replacements of PipelineHandle._interp / _stitch."""
+    if stages_factory is None:
+        from .pipeline import DeviceRigStages as stages_factory  # noqa: N813
+    from .interp import InterpConfig
+    lock = threading.Lock()
+
+    def stages_of(self, cams):
+        with lock:
+            st = getattr(self, "_b200_stages", None)
+            if st is None:
+                cfg = self.config
+                ic = cfg.interp
+                our_cfg = InterpConfig(ic.block_size, ic.search_radius, ic.mask_epsilon, ic.border_band) \
+                    if ic is not None else None
+                f0 = cams[0]
+                st = stages_factory(f0.width, f0.height, int(f0.format), len(cams), cfg.stages,
+                                    cfg.views_per_side, our_cfg, max(2, cfg.channel_capacity) + 2)
+                self._b200_stages = st
+            return st
+
+    def _interp(self) -> None:
+        """server/pipeline.py:254-271 with the views left on the device."""
+        if self.config.interp is not None and self.config.interp.refine is not None:
+            return _SAVED[(pl.PipelineHandle, "_interp")](self)  # per-view host hook: reference flow
+        for pack in self._subs["interp"]:
+            t0 = time.perf_counter()
+            cams = pl._unbundle_frames(pack.payload)
+            slot = stages_of(self, cams).interp(cams)
+            self.report.add(pl.STAGE_INTERP, time.perf_counter() - t0)
+            out = pl.UnifiedDataPack(pl.PackType.FRAME_RAW, _TOKEN.pack(b"B200", slot))
+            self.ch_views.put(out.stamped("interp-out"))
+
+    def _stitch(self) -> None:
+        """server/pipeline.py:273-292 on the device slot of the tick."""
+        if self.config.interp is not None and self.config.interp.refine is not None:
+            return _SAVED[(pl.PipelineHandle, "_stitch")](self)
+        for pack in self._subs["stitch"]:
+            t0 = time.perf_counter()
+            magic, slot = _TOKEN.unpack(pack.payload)
+            if magic != b"B200":
+                raise ValueError("views channel pack is not a device-slot token")
+            clusters = self._b200_stages.stitch(slot)
+            frames = []
+            for c in clusters:
+                f = c.frame
+                frames.append(frame_mod.Frame(f.width, f.height, frame_mod.PixelFormat(int(f.format)),
+                                              tuple(f.planes), f.timestamp))
+            self.report.add(pl.STAGE_STITCH, time.perf_counter() - t0)
+            out = pl.UnifiedDataPack(pl.PackType.FRAME_RAW, pl._bundle_frames(frames))
+            self.ch_clusters.put(out.stamped("stitch-out", time.perf_counter()))
+
+    return {"_interp": _interp, "_stitch": _stitch}
 
 
 def uninstall(fvv=None) -> None:

@@ -240,3 +240,50 @@ def test_cfg3_rig_vs_reference_golden(torch_cuda):
     rects = np.array([[r.index, r.tier == "full", r.x, r.y, r.width, r.height] for c in out for r in c.tile_map],
                      np.int32)
     assert np.array_equal(rects, g["rects"])
+
+
+def test_device_rig_stages_two_threads_vs_golden(torch_cuda):
+    """pipeline.DeviceRigStages as plugin.install(fvv, pipeline=True) drives it:
+    _interp and _stitch on their own threads joined by a bounded queue (the
+    reference's channel back-pressure), 8 ticks cycling 3 device slots; every
+    tick's cluster frames, tile maps and views equal the reference's golden."""
+    import queue
+    import threading
+    import paper_2112_10603_b200 as fv
+    from paper_2112_10603_b200.pipeline import DeviceRigStages
+    g = load_golden("rig3_s2_vps2_yuv420_64x48")
+    w, h, stages, vps = 64, 48, int(g["stages"]), int(g["vps"])
+    st = DeviceRigStages(w, h, 1, 3, stages, vps, slots=3)
+    cams = [fv.frame_from_packed(c, w, h, 1) for c in g["cams"]]
+    q, results, errors = queue.Queue(maxsize=1), [], []
+
+    def interp_worker():
+        try:
+            for t in range(8):
+                q.put(st.interp([c.with_timestamp(t) for c in cams]))
+            q.put(None)
+        except BaseException as e:  # noqa: BLE001
+            errors.append(e)
+            q.put(None)
+
+    def stitch_worker():
+        try:
+            while (slot := q.get()) is not None:
+                results.append((slot, st.stitch(slot)))
+        except BaseException as e:  # noqa: BLE001
+            errors.append(e)
+
+    th = [threading.Thread(target=interp_worker), threading.Thread(target=stitch_worker)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(120)
+    assert not errors, errors
+    assert len(results) == 8
+    for t, (slot, out) in enumerate(results):
+        assert np.array_equal(np.concatenate([fv.packed(c.frame) for c in out]), g["clusters"]), f"tick {t}"
+        assert all(c.frame.timestamp == t for c in out)
+        rects = np.array([[r.index, r.tier == "full", r.x, r.y, r.width, r.height] for c in out for r in c.tile_map],
+                         np.int32)
+        assert np.array_equal(rects, g["rects"])
+    assert np.array_equal(st.views_host(results[-1][0]), g["views"])
