@@ -117,8 +117,14 @@ void make_geometry(const fvv_frame_desc* d, const fvv_interp_params* p, Geometry
     g->qmargin[0] = 0;
     g->qmargin[1] = 2 * p->search_radius[0];
     g->qmargin[2] = 4 * p->search_radius[0] + 2 * p->search_radius[1];
+    {
+        const int span = 4 * p->search_radius[0] + 2 * p->search_radius[1] + p->search_radius[2];
+        g->mmargin = (span + 1) / 2 + 1;
+        g->cmargin = (span + 3) / 4 + 1;
+    }
     g->scan_coop_min = kScanCoopMinDefault;
     g->sadw_rb_min_ctas = kSadwRbMinCtasDefault;
+    g->mask_cols2 = FVV_MASK_COLS2;
 }
 
 // workspace = [header: candidate tables][pair slot 0][pair slot 1]...
@@ -297,6 +303,7 @@ int fvv_engine_set_tuning(fvv_engine* e, int key, int value) {
     switch (key) {
         case FVV_TUNE_SCAN_COOP_MIN: e->g.scan_coop_min = value < 0 ? kScanCoopMinDefault : value; break;
         case FVV_TUNE_SADW_RB_MIN_CTAS: e->g.sadw_rb_min_ctas = value < 0 ? kSadwRbMinCtasDefault : value; break;
+        case FVV_TUNE_MASK_COLS2: e->g.mask_cols2 = value < 0 ? FVV_MASK_COLS2 : (value != 0); break;
         default: return fail(FVV_EINVAL, "unknown tuning key " + std::to_string(key));
     }
     return FVV_OK;

@@ -824,6 +824,9 @@ __device__ __forceinline__ float third_f32(int sn, float scale) {
 #ifndef FVV_MASK_UNROLL
 #define FVV_MASK_UNROLL 1
 #endif
+#ifndef FVV_MASK_NC
+#define FVV_MASK_NC 0  // no-clamp interior rows: r2 sweep 4.02 -> 4.92 ms (register pressure), off
+#endif
 constexpr int kMW = 28, kMWarps = 4, kMH = FVV_KMH, kMaskUnroll = FVV_MASK_UNROLL;
 
 template <int FMT>
@@ -879,9 +882,10 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
         if (a == 0.0f && o0v == 0.0f && c == 0.0f) return 0.0f;
         return (float)div3(__dadd_rn(__dadd_rn((double)a, (double)o0v), (double)c));
     };
+    const double oscale_d = (double)oscale;
     auto colpass = [&](int a, int b, int c) {  // f32(f64(sum/3)) of occ in units 2^-(mb+1)
-        const int sn = a + b + c;
-        return sn ? third_f32(sn, oscale) : 0.0f;
+        const int sn = a + b + c;  // >= 0, < 2^31: (double)sn built exactly off the XU pipe
+        return sn ? (float)div3(__dmul_rn(u2d_exact((uint32_t)sn), oscale_d)) : 0.0f;
     };
 
     // source-row caches: x-lerped rows ua, ua+1 of flow1 and ba, ba+1 of the block grid
@@ -895,9 +899,14 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
     for (int d = 0; d < 2; d++) F0[d] = F1[d] = F2[d] = make_int2(0, 0);
 
     auto emit_o = [&](int t, int a0, int a1, int b0, int b1, int c0, int c1) {
-        // O0(t) from occ(t-1), occ(t), occ(t+1) per direction, then the row pass
-        const float ol = rowpass(colpass(a0, b0, c0));
-        const float orr = rowpass(colpass(a1, b1, c1));
+        // O0(t) from occ(t-1), occ(t), occ(t+1) per direction, then the row pass.
+        // Smooth flow has no convergence: when the occlusion cue of the warp's
+        // 3 rows is zero in every lane, both passes are exactly zero (warp-uniform skip)
+        float ol = 0.0f, orr = 0.0f;
+        if (__any_sync(0xffffffffu, (a0 | a1 | b0 | b1 | c0 | c1) != 0)) {
+            ol = rowpass(colpass(a0, b0, c0));
+            orr = rowpass(colpass(a1, b1, c1));
+        }
         if (own) {
             o_ol[(unsigned)(t * W + x)] = ol;
             o_or[(unsigned)(t * W + x)] = orr;
@@ -906,8 +915,12 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
 
     // one walker row; GEN = general row (band edges, image top), else every
     // output of the row is in range and no edge rule applies (the band interior)
-    auto step = [&](int yy, auto gen) {
+    auto step = [&](int yy, auto gen, auto nclamp) {
         constexpr bool GEN = decltype(gen)::value;
+        // NC: every bilinear tap of this row (luma and chroma, both directions,
+        // every lane) provably stays inside its plane (|mid flow| <= max_span / 2,
+        // Geometry::mmargin), so the clamps of tap2 are identities and are skipped
+        constexpr bool NC = decltype(nclamp)::value;
         // ---- mid flows F(yy) (flow.py:122-129 at level 2, interp.py:131-132) ----
         const Tap2 ty = tap2(2 * yy - 1, 2, L1.h);  // L1.h >= 2
         if (ty.i0 != ua) {
@@ -958,6 +971,15 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
 #pragma unroll
                 for (int c = 0; c < 3; c++) { o[c] = cl[c]; o[3 + c] = cr[c]; }
             }
+        } else if (NC) {
+            const int fm = (1 << mb) - 1;
+            auto nc = [&](const uint8_t* fr, int2 f) {
+                const int sx = (xc << mb) + f.x, sy = (yy << mb) + f.y;
+                const uint8_t* r0 = fr + (unsigned)((sy >> mb) * W + (sx >> mb));
+                return rne64((long long)bilerp_u(r0[0], r0[1], r0[W], r0[W + 1], sx & fm, sy & fm, mb), kY);
+            };
+            wl = nc(frL, F2[0]);
+            wr = nc(frR, F2[1]);
         } else {
             wl = rne64(bilin_fixed(frL, W, H, W, yy, xc, F2[0].x, F2[0].y, mb), kY);
             wr = rne64(bilin_fixed(frR, W, H, W, yy, xc, F2[1].x, F2[1].y, mb), kY);
@@ -1008,8 +1030,21 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
                 const int p = x & 1;  // even lane: U plane, odd lane: V plane
                 const uint8_t* pl = frL + (size_t)W * H + (size_t)p * cw * chh;
                 const uint8_t* pr = frR + (size_t)W * H + (size_t)p * cw * chh;
-                const uint8_t vl = (uint8_t)rne64(bilin_fixed(pl, cw, chh, cw, cy, cx, cv[0].x, cv[0].y, cb), kC);
-                const uint8_t vr = (uint8_t)rne64(bilin_fixed(pr, cw, chh, cw, cy, cx, cv[1].x, cv[1].y, cb), kC);
+                uint8_t vl, vr;
+                if (NC) {
+                    const int fm = (1 << cb) - 1;
+                    auto nc = [&](const uint8_t* pp, int2 f) {
+                        const int sx = (cx << cb) + f.x, sy = (cy << cb) + f.y;
+                        const uint8_t* r0 = pp + (unsigned)((sy >> cb) * cw + (sx >> cb));
+                        return (uint8_t)rne64((long long)bilerp_u(r0[0], r0[1], r0[cw], r0[cw + 1], sx & fm, sy & fm, cb),
+                                              kC);
+                    };
+                    vl = nc(pl, cv[0]);
+                    vr = nc(pr, cv[1]);
+                } else {
+                    vl = (uint8_t)rne64(bilin_fixed(pl, cw, chh, cw, cy, cx, cv[0].x, cv[0].y, cb), kC);
+                    vr = (uint8_t)rne64(bilin_fixed(pr, cw, chh, cw, cy, cx, cv[1].x, cv[1].y, cb), kC);
+                }
                 uint8_t* wc = reinterpret_cast<uint8_t*>(plane<uchar4>(ws, P, P.wc, pair) + (unsigned)(cy * cw + cx));
                 wc[2 * p] = vl;
                 wc[2 * p + 1] = vr;
@@ -1017,11 +1052,24 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
         }
     };
     const int b0 = min(max(y0 + 2, 3), yo1), b1 = max(b0, yo1);  // interior rows [b0, b1)
+    // rows whose taps (luma row yy, chroma row (yy-1)/2) stay inside their planes,
+    // and whether this warp's columns (all 32 lanes' luma taps, the owned lanes'
+    // chroma taps) do: the no-clamp walker runs on their intersection
+    const int mm = g.mmargin, cm = g.cmargin;
+    const bool cols_in = FMT != FVV_RGB8 && xw0 - 2 >= mm && xw0 + 29 <= W - 2 - mm &&
+                         (FMT != FVV_YUV420 || ((xw0 >> 1) >= cm && ((xw0 + kMW - 1) >> 1) <= g.cw - 2 - cm));
+    const int r_lo = FMT == FVV_YUV420 ? max(mm, 2 * cm + 1) : mm;
+    const int r_hi = FMT == FVV_YUV420 ? min(H - 2 - mm, 2 * (g.ch - 2 - cm) + 1) : H - 2 - mm;  // inclusive
     int yy = ys;
-    for (; yy < b0; yy++) step(yy, std::true_type{});
+    for (; yy < b0; yy++) step(yy, std::true_type{}, std::false_type{});
+    if (FVV_MASK_NC && cols_in && r_lo <= r_hi) {
+        const int n0 = min(b1, max(yy, r_lo)), n1 = min(b1, max(n0, r_hi + 1));
+        for (; yy < n0; yy++) step(yy, std::false_type{}, std::false_type{});
 #pragma unroll kMaskUnroll
-    for (; yy < b1; yy++) step(yy, std::false_type{});
-    for (; yy <= ye; yy++) step(yy, std::true_type{});
+        for (; yy < n1; yy++) step(yy, std::false_type{}, std::true_type{});
+    }
+    for (; yy < b1; yy++) step(yy, std::false_type{}, std::false_type{});
+    for (; yy <= ye; yy++) step(yy, std::true_type{}, std::false_type{});
     // ---- bottom edge: occ(H-1) (one-sided gy), O0/O(H-2), O0/O(H-1), Sd(H-1) ----
     if (ye == H - 1) {
 #pragma unroll
@@ -1035,6 +1083,292 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
         if (H - 2 >= y0 && H - 2 < yo1) emit_o(H - 2, oc0[0], oc0[1], oc1[0], oc1[1], oc2[0], oc2[1]);
         if (H - 1 >= y0 && H - 1 < yo1) emit_o(H - 1, oc1[0], oc1[1], oc2[0], oc2[1], oc2[0], oc2[1]);
         if (own && H - 1 >= y0 && H - 1 < yo1) o_sd[(size_t)(H - 1) * W + x] = (uint16_t)(d1 + d2 + d2);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_mask_cols2: the same computation as k_mask_cols (gray / 4:2:0), with each
+// lane walking TWO adjacent columns x = 2m, 2m+1.  A warp covers 64 columns
+// and owns 60 (one halo column pair per side instead of two halo lanes: 6 %
+// of the lanes' work is halo instead of 12.5 %); per-row uniform work, the
+// x-neighbour shuffles (one up + one down per direction serve both columns),
+// the stores (u8x2 / u16x2 / f32x2) and the chroma pixel (x/2: the lane's own
+// 2x2 block, no pair shuffle) are shared by the two columns.  Both columns'
+// windows live in registers (twice the state of k_mask_cols at half the warps).
+// Column semantics are identical to k_mask_cols: clamped sample column xc,
+// nearest / one-sided neighbours at the frame edges.
+// ---------------------------------------------------------------------------
+#ifndef FVV_MINB_MASK2
+#define FVV_MINB_MASK2 5  // r2 sweep: 4 (128 regs, no spills) 4.03 ms, 5 (96 regs) 3.85 ms per cfg4 step
+#endif
+#ifndef FVV_MASK2_HB_CACHE
+#define FVV_MASK2_HB_CACHE 1
+#endif
+constexpr int kM2Own = 60, kM2Warps = 4;
+
+template <int FMT>
+__global__ void __launch_bounds__(kM2Warps * 32, FVV_MINB_MASK2) k_mask_cols2(Geometry g, PairTable pt,
+                                                                  uint8_t* __restrict__ ws, Planes P) {
+    static_assert(FMT != FVV_RGB8, "RGB8 runs k_mask_cols");
+    const int W = g.W, H = g.H;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int pair = blockIdx.z;
+    const int y0 = blockIdx.y * kMH;
+    const int xw0 = (blockIdx.x * kM2Warps + wid) * kM2Own;  // even
+    if (xw0 >= W) return;
+    const int xa = xw0 - 2 + 2 * lane;  // this lane's columns xa, xa + 1 (xa even)
+    int xcl[2], gmul[2];
+    bool selfL[2], selfR[2];
+#pragma unroll
+    for (int c = 0; c < 2; c++) {
+        const int x = xa + c;
+        xcl[c] = clampi(x, 0, W - 1);
+        selfL[c] = x <= 0;
+        selfR[c] = x >= W - 1;
+        gmul[c] = (W >= 2 && (x == 0 || x == W - 1)) ? 2 : (W >= 2 ? 1 : 0);
+    }
+    const bool own = lane >= 1 && lane <= 30 && xa < W;  // W even: xa + 1 < W as well
+    const Level& L1 = g.lv[1];
+    const Level& L2 = g.lv[2];
+    const int B2 = L2.block, D2 = 2 * B2, lgD2 = 31 - __clz(D2);
+    const int mb = g.fb[2] + 1, kY = 2 * mb;
+    const int bs = g.fb[2] - (g.fb[1] + 3), rs = g.fb[2] - g.rb[2];
+    ITap tu[2], tb[2];
+#pragma unroll
+    for (int c = 0; c < 2; c++) {
+        tu[c] = clamp_itap32(2 * xcl[c] - 1, 2, L1.w);
+        tb[c] = clamp_itap32(2 * xcl[c] - B2 + 1, lgD2, L2.nbx);
+    }
+    const int2* f1[2] = {cplane<int2>(ws, P, P.flow1[0], pair), cplane<int2>(ws, P, P.flow1[1], pair)};
+    const BlockHit* hh[2] = {cplane<BlockHit>(ws, P, P.hit[2][0], pair),
+                             cplane<BlockHit>(ws, P, P.hit[2][1], pair)};
+    const uint8_t* frL = pt.left[pair];
+    const uint8_t* frR = pt.right[pair];
+    uint8_t* o_wl = plane<uint8_t>(ws, P, P.wl, pair);
+    uint8_t* o_wr = plane<uint8_t>(ws, P, P.wr, pair);
+    uint16_t* o_sd = plane<uint16_t>(ws, P, P.sd, pair);
+    float* o_ol = plane<float>(ws, P, P.occ_l, pair);
+    float* o_or = plane<float>(ws, P, P.occ_r, pair);
+    uchar4* o_wc = FMT == FVV_YUV420 ? plane<uchar4>(ws, P, P.wc, pair) : nullptr;
+    const double oscale_d = (double)(1.0f / (float)(1 << (mb + 1)));
+    const int ys = max(0, y0 - 2), ye = min(H - 1, y0 + kMH + 1);
+    const int yo1 = min(H, y0 + kMH);
+
+    // neighbour values of a per-column quantity v[2] with the edge rules folded in
+    auto nbrs = [&](const int (&v)[2], int (&l)[2], int (&r)[2]) {
+        const int up = __shfl_up_sync(0xffffffffu, v[1], 1);    // column xa - 1
+        const int dn = __shfl_down_sync(0xffffffffu, v[0], 1);  // column xa + 2
+        l[0] = selfL[0] ? v[0] : up;
+        r[0] = selfR[0] ? v[0] : v[1];
+        l[1] = selfL[1] ? v[1] : v[0];
+        r[1] = selfR[1] ? v[1] : dn;
+    };
+    auto colpass = [&](int a, int b, int c) {  // f32(f64(sum/3)) of occ in units 2^-(mb+1)
+        const int sn = a + b + c;
+        return sn ? (float)div3(__dmul_rn(u2d_exact((uint32_t)sn), oscale_d)) : 0.0f;
+    };
+    auto row3 = [&](float a, float b, float c) {  // f32(f64(a + b + c) / 3)
+        if (a == 0.0f && b == 0.0f && c == 0.0f) return 0.0f;
+        return (float)div3(__dadd_rn(__dadd_rn((double)a, (double)b), (double)c));
+    };
+
+    int ua = -10;
+#if FVV_MASK2_HB_CACHE
+    int ba = -10;
+#endif
+    int2 hu0[2][2], hu1[2][2];  // [dir][col]
+#if FVV_MASK2_HB_CACHE
+    int2 hb0[2][2], hb1[2][2];
+#endif
+    int2 Fp[2][2], Fc[2][2];                          // F(yy-1), F(yy)
+    int Fpp_y[2][2];                                  // F(yy-2).y
+    int gxp[2][2], gxc[2][2];                         // gx(yy-1), gx(yy)
+    int oc0[2][2], oc1[2][2], oc2[2][2];
+    uint32_t dp1 = 0, dp2 = 0;  // |wl - wr| of rows yy-2, yy-1, both columns packed (col 0 | col 1 << 16)
+#pragma unroll
+    for (int d = 0; d < 2; d++)
+#pragma unroll
+        for (int c = 0; c < 2; c++) {
+            Fp[d][c] = Fc[d][c] = make_int2(0, 0);
+            Fpp_y[d][c] = 0;
+            gxp[d][c] = gxc[d][c] = 0;
+            oc0[d][c] = oc1[d][c] = oc2[d][c] = 0;
+        }
+
+    auto xl_u = [&](int d, int row, int c) {
+        const int2* r = f1[d] + row * L1.w;
+        return lerp_i2(r[tu[c].i0], r[tu[c].i1], 4, tu[c].f);
+    };
+    auto xl_b = [&](int d, int row, int c) {
+        const BlockHit* r = hh[d] + row * L2.nbx;
+        const BlockHit p = r[tb[c].i0], q = r[tb[c].i1];
+        return lerp_i2(make_int2(p.dx, p.dy), make_int2(q.dx, q.dy), D2, tb[c].f);
+    };
+    auto emit_o = [&](int t, const int (&a)[2][2], const int (&b)[2][2], const int (&cc)[2][2]) {
+        float o[2][2] = {{0.0f, 0.0f}, {0.0f, 0.0f}};
+        if (__any_sync(0xffffffffu, (a[0][0] | a[0][1] | a[1][0] | a[1][1] | b[0][0] | b[0][1] | b[1][0] | b[1][1] |
+                                     cc[0][0] | cc[0][1] | cc[1][0] | cc[1][1]) != 0)) {
+#pragma unroll
+            for (int d = 0; d < 2; d++) {
+                float v[2];
+#pragma unroll
+                for (int c = 0; c < 2; c++) v[c] = colpass(a[d][c], b[d][c], cc[d][c]);
+                int vi[2] = {__float_as_int(v[0]), __float_as_int(v[1])}, li[2], ri[2];
+                nbrs(vi, li, ri);
+#pragma unroll
+                for (int c = 0; c < 2; c++) o[d][c] = row3(__int_as_float(li[c]), v[c], __int_as_float(ri[c]));
+            }
+        }
+        if (own) {
+            *reinterpret_cast<float2*>(o_ol + (unsigned)(t * W + xa)) = make_float2(o[0][0], o[0][1]);
+            *reinterpret_cast<float2*>(o_or + (unsigned)(t * W + xa)) = make_float2(o[1][0], o[1][1]);
+        }
+    };
+
+    auto step = [&](int yy, auto gen) {
+        constexpr bool GEN = decltype(gen)::value;
+        const Tap2 ty = tap2(2 * yy - 1, 2, L1.h);
+        if (ty.i0 != ua) {
+#pragma unroll
+            for (int d = 0; d < 2; d++)
+#pragma unroll
+                for (int c = 0; c < 2; c++) {
+                    hu0[d][c] = ty.i0 == ua + 1 ? hu1[d][c] : xl_u(d, ty.i0, c);
+                    hu1[d][c] = xl_u(d, ty.i0 + 1, c);
+                }
+            ua = ty.i0;
+        }
+        const ITap tby = clamp_itap32(2 * yy - B2 + 1, lgD2, L2.nby);
+#if FVV_MASK2_HB_CACHE
+        if (tby.i0 != ba) {
+#pragma unroll
+            for (int d = 0; d < 2; d++)
+#pragma unroll
+                for (int c = 0; c < 2; c++) {
+                    hb0[d][c] = tby.i0 == ba + 1 ? hb1[d][c] : xl_b(d, tby.i0, c);
+                    hb1[d][c] = xl_b(d, tby.i1, c);
+                }
+            ba = tby.i0;
+        }
+#else
+        // block-grid rows re-lerped every row from L1-resident hits (saves 16 registers)
+        int2 hb0[2][2], hb1[2][2];
+#pragma unroll
+        for (int d = 0; d < 2; d++)
+#pragma unroll
+            for (int c = 0; c < 2; c++) {
+                hb0[d][c] = xl_b(d, tby.i0, c);
+                hb1[d][c] = xl_b(d, tby.i1, c);
+            }
+#endif
+        // ---- mid flows F(yy), x-gradients gx(yy) ----
+#pragma unroll
+        for (int d = 0; d < 2; d++) {
+            int fx[2];
+#pragma unroll
+            for (int c = 0; c < 2; c++) {
+                const int2 base = lerp_i2(hu0[d][c], hu1[d][c], 4, ty.f);
+                const int2 res = lerp_i2(hb0[d][c], hb1[d][c], D2, tby.f);
+                Fpp_y[d][c] = Fp[d][c].y;
+                Fp[d][c] = Fc[d][c];
+                Fc[d][c] = make_int2(-((base.x << bs) + (res.x << rs)), -((base.y << bs) + (res.y << rs)));
+                fx[c] = Fc[d][c].x;
+            }
+            int l[2], r[2];
+            nbrs(fx, l, r);
+#pragma unroll
+            for (int c = 0; c < 2; c++) {
+                gxp[d][c] = gxc[d][c];
+                gxc[d][c] = gmul[c] * (r[c] - l[c]);
+            }
+        }
+        // ---- luma warps at yy, d = |wl - wr| ----
+        int wl[2], wr[2];
+#pragma unroll
+        for (int c = 0; c < 2; c++) {
+            wl[c] = rne64(bilin_fixed(frL, W, H, W, yy, xcl[c], Fc[0][c].x, Fc[0][c].y, mb), kY);
+            wr[c] = rne64(bilin_fixed(frR, W, H, W, yy, xcl[c], Fc[1][c].x, Fc[1][c].y, mb), kY);
+        }
+        const uint32_t dp0 = dp1;
+        dp1 = dp2;
+        dp2 = (uint32_t)abs(wl[0] - wr[0]) | ((uint32_t)abs(wl[1] - wr[1]) << 16);
+        if (own && (!GEN || (yy >= y0 && yy < yo1))) {
+            *reinterpret_cast<uint16_t*>(o_wl + (unsigned)(yy * W + xa)) = (uint16_t)(wl[0] | (wl[1] << 8));
+            *reinterpret_cast<uint16_t*>(o_wr + (unsigned)(yy * W + xa)) = (uint16_t)(wr[0] | (wr[1] << 8));
+        }
+        // ---- Sd(yy-1) ----
+        {
+            const int t = yy - 1;
+            if (own && (!GEN || (t >= y0 && t < yo1))) {  // lane-wise sums < 2^16: packed adds
+                const uint32_t sp = ((GEN && t == 0) ? dp1 : dp0) + dp1 + dp2;
+                *reinterpret_cast<uint32_t*>(o_sd + (unsigned)(t * W + xa)) = sp;
+            }
+        }
+        // ---- occ(yy-1) then O0/O(yy-2) ----
+        {
+            const int r = yy - 1;
+            if (!GEN || (r >= ys && (r == 0 || r - 1 >= ys))) {
+#pragma unroll
+                for (int d = 0; d < 2; d++) {
+#pragma unroll
+                    for (int c = 0; c < 2; c++) {
+                        const int gy = H < 2 ? 0 : ((GEN && r == 0) ? 2 * (Fc[d][c].y - Fp[d][c].y)
+                                                                    : Fc[d][c].y - Fpp_y[d][c]);
+                        const int v = -(gxp[d][c] + gy);
+                        oc0[d][c] = oc1[d][c];
+                        oc1[d][c] = oc2[d][c];
+                        oc2[d][c] = v > 0 ? v : 0;
+                    }
+                }
+                const int t2 = yy - 2;
+                if (!GEN || (t2 >= y0 && t2 < yo1)) {
+                    if (GEN && t2 == 0) emit_o(t2, oc1, oc1, oc2);
+                    else emit_o(t2, oc0, oc1, oc2);
+                }
+            }
+        }
+        // ---- chroma pixel (xa/2, (yy-1)/2) at odd yy: the lane's own 2x2 block ----
+        if (FMT == FVV_YUV420 && (yy & 1) && (!GEN || (yy - 1 >= y0 && yy - 1 < yo1 && yy - 1 >= ys))) {
+            if (own) {
+                const int cw = g.cw, chh = g.ch, cb = mb + 3, kC = 2 * cb;
+                const int cy = (yy - 1) >> 1, cx = xa >> 1;
+                int2 cv[2];
+#pragma unroll
+                for (int d = 0; d < 2; d++)
+                    cv[d] = make_int2((Fp[d][0].x + Fc[d][0].x) + (Fp[d][1].x + Fc[d][1].x),
+                                      (Fp[d][0].y + Fc[d][0].y) + (Fp[d][1].y + Fc[d][1].y));
+                const uint8_t* ul = frL + (size_t)W * H;
+                const uint8_t* ur = frR + (size_t)W * H;
+                const size_t cpl = (size_t)cw * chh;
+                const uint8_t a0 = (uint8_t)rne64(bilin_fixed(ul, cw, chh, cw, cy, cx, cv[0].x, cv[0].y, cb), kC);
+                const uint8_t a1 = (uint8_t)rne64(bilin_fixed(ur, cw, chh, cw, cy, cx, cv[1].x, cv[1].y, cb), kC);
+                const uint8_t b0 = (uint8_t)rne64(bilin_fixed(ul + cpl, cw, chh, cw, cy, cx, cv[0].x, cv[0].y, cb), kC);
+                const uint8_t b1 = (uint8_t)rne64(bilin_fixed(ur + cpl, cw, chh, cw, cy, cx, cv[1].x, cv[1].y, cb), kC);
+                o_wc[(unsigned)(cy * cw + cx)] = make_uchar4(a0, a1, b0, b1);
+            }
+        }
+    };
+    const int b0 = min(max(y0 + 2, 3), yo1), b1 = max(b0, yo1);
+    int yy = ys;
+    for (; yy < b0; yy++) step(yy, std::true_type{});
+    for (; yy < b1; yy++) step(yy, std::false_type{});
+    for (; yy <= ye; yy++) step(yy, std::true_type{});
+    if (ye == H - 1) {
+#pragma unroll
+        for (int d = 0; d < 2; d++) {
+#pragma unroll
+            for (int c = 0; c < 2; c++) {
+                const int gy = H < 2 ? 0 : 2 * (Fc[d][c].y - Fp[d][c].y);
+                const int v = -(gxc[d][c] + gy);
+                oc0[d][c] = oc1[d][c];
+                oc1[d][c] = oc2[d][c];
+                oc2[d][c] = v > 0 ? v : 0;
+            }
+        }
+        if (H - 2 >= y0 && H - 2 < yo1) emit_o(H - 2, oc0, oc1, oc2);
+        if (H - 1 >= y0 && H - 1 < yo1) emit_o(H - 1, oc1, oc2, oc2);
+        if (own && H - 1 >= y0 && H - 1 < yo1)
+            *reinterpret_cast<uint32_t*>(o_sd + (size_t)(H - 1) * W + xa) = dp1 + dp2 + dp2;
     }
 }
 
@@ -1964,7 +2298,11 @@ cudaError_t run_interp_stage(const Geometry& g, const PairTable& pt, uint8_t* ws
     if (e != cudaSuccess || (e = E()) != cudaSuccess) return e;
 
     B(KC_MASK_PROD);
-    {
+    if (g.fmt != FVV_RGB8 && g.mask_cols2) {
+        const dim3 grd((g.W + kM2Own * kM2Warps - 1) / (kM2Own * kM2Warps), (g.H + kMH - 1) / kMH, npairs);
+        if (g.fmt == FVV_YUV420) k_mask_cols2<FVV_YUV420><<<grd, kM2Warps * 32, 0, st>>>(g, pt, ws, P);
+        else k_mask_cols2<FVV_GRAY8><<<grd, kM2Warps * 32, 0, st>>>(g, pt, ws, P);
+    } else {
         const dim3 grd((g.W + kMW * kMWarps - 1) / (kMW * kMWarps), (g.H + kMH - 1) / kMH, npairs);
         if (g.fmt == FVV_YUV420) k_mask_cols<FVV_YUV420><<<grd, kMWarps * 32, 0, st>>>(g, pt, ws, P);
         else if (g.fmt == FVV_RGB8) k_mask_cols<FVV_RGB8><<<grd, kMWarps * 32, 0, st>>>(g, pt, ws, P);

@@ -131,7 +131,8 @@ class Interpolator:
         except Exception:  # noqa: BLE001
             pass
 
-    def set_tuning(self, scan_coop_min: int | None = None, sadw_rb_min_ctas: int | None = None):
+    def set_tuning(self, scan_coop_min: int | None = None, sadw_rb_min_ctas: int | None = None,
+                   mask_cols2: int | None = None):
         """Launch-variant thresholds (fvv_engine_set_tuning); results are
         identical for every setting -- the tests use it to force each variant.
         None leaves a knob unchanged, -1 restores its default."""
@@ -140,6 +141,8 @@ class Interpolator:
         if sadw_rb_min_ctas is not None:
             _lib.check(self._L.fvv_engine_set_tuning(self._h, _lib.FVV_TUNE_SADW_RB_MIN_CTAS,
                                                      int(sadw_rb_min_ctas)))
+        if mask_cols2 is not None:
+            _lib.check(self._L.fvv_engine_set_tuning(self._h, _lib.FVV_TUNE_MASK_COLS2, int(mask_cols2)))
         return self
 
     @property

@@ -25,8 +25,8 @@ from oracle import oracle as O
 
 pytestmark = pytest.mark.gpu
 
-VARIANTS = {"all_on": dict(scan_coop_min=0, sadw_rb_min_ctas=0),
-            "all_off": dict(scan_coop_min=1 << 30, sadw_rb_min_ctas=1 << 30)}
+VARIANTS = {"all_on": dict(scan_coop_min=0, sadw_rb_min_ctas=0, mask_cols2=1),
+            "all_off": dict(scan_coop_min=1 << 30, sadw_rb_min_ctas=1 << 30, mask_cols2=0)}
 
 
 @pytest.fixture(scope="module")
