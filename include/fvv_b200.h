@@ -246,6 +246,39 @@ int fvv_vinet_rig_clusters(const fvv_frame_desc* desc, const fvv_vinet_weights* 
                            int ncams, int stages, int views_per_side, uint8_t* views, uint8_t* clusters,
                            void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * RefineNet + ContextNet (vinet_params.py), the
+ * paper's context-aware residual U-Net after the VIBlocks.  The convolutions
+ * run through fvv_conv2d_bf16; these entry points are its other kernels
+ * (orchestration: paper_2112_10603_b200/refine.py; fp32 oracle:
+ * oracle/vinet_ref.py refine_view).  The network works on the 64-aligned
+ * canvas (Wp, Hp) of the frame, edge-replicated.
+ *
+ * fvv_refine_image     context-net input: canvas images of nsrc frames,
+ *                      NHWC bf16 [nsrc][Hp][Wp][16] (3 channels used)
+ * fvv_refine_inputs    per view i (t[i] in (0,1), state[i] = VINet flows
+ *                      (5,H,W)): U-Net input x0 NHWC bf16 [n][Hp][Wp][32]
+ *                      (17 used), merged blend (n,3,H,W) f32, canvas flows
+ *                      flow0 (n,4,Hp,Wp) f32 = (F_l,t, F_r,t)
+ * fvv_refine_flow_pool next context level's flows: 2x2 mean * 0.5
+ * fvv_refine_warp_features  warp channels [0,C) of NHWC bf16 features of
+ *                      source (b*src_mul + src_add) with flow channels
+ *                      (comp, comp+1) into dst channels [coff, coff+C)
+ * fvv_nhwc_copy        U-Net skip: channels [0,C) of src -> dst at coff
+ * fvv_refine_output    views = clip(merged + 2 sigmoid(r) - 1, 0, 1) packed
+ *                      as uint8 frames (r: NHWC f32 [n][Hp][Wp][rs])
+ * At most 64 views (128 sources) per call. */
+int fvv_refine_image(const fvv_frame_desc* desc, const uint8_t* const* frames, int nsrc, void* out, void* stream);
+int fvv_refine_inputs(const fvv_frame_desc* desc, const uint8_t* const* left, const uint8_t* const* right,
+                      const float* const* state, const float* t, int nviews, void* x0, float* merged, float* flow0,
+                      void* stream);
+int fvv_refine_flow_pool(const float* in, float* out, int w, int h, int nb, void* stream);
+int fvv_refine_warp_features(const void* feat, int fs, int channels, int w, int h, const float* flow, int comp,
+                             int src_mul, int src_add, void* dst, int ds, int coff, int nb, void* stream);
+int fvv_nhwc_copy(const void* src, int ss, int channels, void* dst, int ds, int coff, long long npix, void* stream);
+int fvv_refine_output(const fvv_frame_desc* desc, uint8_t* const* out, int nviews, const float* r, int rs,
+                      const float* merged, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

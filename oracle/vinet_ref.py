@@ -182,3 +182,73 @@ def synth(left: np.ndarray, right: np.ndarray, w: int, h: int, fmt: int, state: 
                 out.append(_synth_plane(torch.from_numpy(pls[k].astype(np.float32)),
                                         torch.from_numpy(prs[k].astype(np.float32)), fc[0:2], fc[2:4], wc, t))
     return np.concatenate([o.numpy().astype(np.uint8).reshape(-1) for o in out])
+
+
+# ---------------------------------------------------------------------------
+# RefineNet + ContextNet (vinet_params.CONTEXT_LAYERS / REFINE_LAYERS)
+# ---------------------------------------------------------------------------
+def _conv(x, wb, stride):
+    w, b = wb
+    return torch.relu(Fn.conv2d(x, w, b, stride=stride, padding=1))
+
+
+def contextnet(img: torch.Tensor, flow: torch.Tensor, layers):
+    """img (3, Hp, Wp) canvas image, flow (2, Hp, Wp) canvas flow -> 4 warped feature maps."""
+    f = img[None]
+    feats = []
+    for k in range(4):
+        f = _conv(f, layers[2 * k], 2)
+        f = _conv(f, layers[2 * k + 1], 1)
+        flow = pool2(flow) * 0.5
+        feats.append(warp(f[0], flow[0], flow[1]))
+    return feats
+
+
+def refine_inputs(left, right, w: int, h: int, fmt: int, state: torch.Tensor, t: float):
+    """(x0 (17, Hp, Wp) canvas U-Net input, merged (3, H, W), F_l,t, F_r,t canvas flows)."""
+    a, b = net_image(left, w, h, fmt), net_image(right, w, h, fmt)
+    fl, fr = state[0:2] * (2.0 * t), state[2:4] * (2.0 * (1.0 - t))
+    m = torch.sigmoid(state[4])
+    wt = (1.0 - t) * m / ((1.0 - t) * m + t * (1.0 - m))
+    wl = warp(a, fl[0], fl[1])
+    wr = warp(b, fr[0], fr[1])
+    merged = wt * wl + (1.0 - wt) * wr
+    x0 = torch.cat([a, b, wl, wr, wt[None], fl, fr], 0)
+    return pad_canvas(x0, w, h), merged, pad_canvas(fl, w, h), pad_canvas(fr, w, h)
+
+
+@torch.no_grad()
+def refine_view(left, right, w: int, h: int, fmt: int, state: torch.Tensor, t: float, rparams):
+    """Direct-t view at t refined by RefineNet -> (packed uint8 frame, refined (3, H, W) f32 in [0, 1])."""
+    x0, merged, fl, fr = refine_inputs(left, right, w, h, fmt, state, t)
+    il = pad_canvas(net_image(left, w, h, fmt), w, h)
+    ir = pad_canvas(net_image(right, w, h, fmt), w, h)
+    cl = contextnet(il, fl, rparams["context"])
+    cr = contextnet(ir, fr, rparams["context"])
+    u = rparams["unet"]
+    s0 = _conv(_conv(x0[None], u[0], 2), u[1], 1)
+    s1 = _conv(_conv(torch.cat([s0, cl[0][None], cr[0][None]], 1), u[2], 2), u[3], 1)
+    s2 = _conv(_conv(torch.cat([s1, cl[1][None], cr[1][None]], 1), u[4], 2), u[5], 1)
+    s3 = _conv(_conv(torch.cat([s2, cl[2][None], cr[2][None]], 1), u[6], 2), u[7], 1)
+
+    def up(x, wb):
+        return torch.relu(Fn.conv_transpose2d(x, wb[0], wb[1], stride=2, padding=1))
+    x = up(torch.cat([s3, cl[3][None], cr[3][None]], 1), u[8])
+    x = up(torch.cat([x, s2], 1), u[9])
+    x = up(torch.cat([x, s1], 1), u[10])
+    x = up(torch.cat([x, s0], 1), u[11])
+    r = torch.sigmoid(Fn.conv2d(x, u[12][0], u[12][1], padding=1))[0, :, :h, :w]
+    out = torch.clamp(merged + (r * 2.0 - 1.0), 0.0, 1.0)
+    return pack_image(out, w, h, fmt), out
+
+
+def pack_image(img: torch.Tensor, w: int, h: int, fmt: int) -> np.ndarray:
+    """(3, H, W) in [0, 1] -> packed uint8 frame: RGB interleaved, Y (+ 2x2-mean U, V), or Y."""
+    v = img * 255.0
+    if fmt == RGB8:
+        return torch.clamp(torch.round(v), 0, 255).permute(1, 2, 0).numpy().astype(np.uint8).reshape(-1)
+    y = torch.clamp(torch.round(v[0]), 0, 255).numpy().astype(np.uint8).reshape(-1)
+    if fmt == GRAY8:
+        return y
+    c = torch.clamp(torch.round(pool2(v[1:3])), 0, 255).numpy().astype(np.uint8)
+    return np.concatenate([y, c[0].reshape(-1), c[1].reshape(-1)])

@@ -25,6 +25,8 @@ EXPORTS = (
     "fvv_profile_enable", "fvv_profile_read", "fvv_kernel_class_name",
     "fvv_interp_level_diagnostics", "fvv_conv2d_bf16", "fvv_vinet_workspace_size", "fvv_vinet_flow",
     "fvv_vinet_synth", "fvv_vinet_rig", "fvv_vinet_rig_clusters",
+    "fvv_refine_image", "fvv_refine_inputs", "fvv_refine_flow_pool", "fvv_refine_warp_features",
+    "fvv_nhwc_copy", "fvv_refine_output",
 )
 
 

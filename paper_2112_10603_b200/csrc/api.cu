@@ -12,6 +12,7 @@
 #include "fvv_device.cuh"
 #include "conv_tc.h"
 #include "vinet.h"
+#include "refine.h"
 
 namespace fvv {
 extern thread_local int g_failed_class;
@@ -864,4 +865,86 @@ extern "C" int fvv_vinet_rig_clusters(const fvv_frame_desc* d, const fvv_vinet_w
                             1 << stages);
     if (e != cudaSuccess) return cuda_fail(e, "fvv_vinet_rig_clusters");
     return FVV_OK;
+}
+
+// ---------------------------------------------------------------------------
+// RefineNet + ContextNet (refine_kernels.cu; orchestration in refine.py)
+// ---------------------------------------------------------------------------
+static int ref_check(const fvv_frame_desc* d, int n, int cap) {
+    int rc = vin_check_desc(d);
+    if (rc) return rc;
+    if (n < 1 || n > cap) return fail(FVV_EINVAL, "batch must hold 1.." + std::to_string(cap) + " entries");
+    return FVV_OK;
+}
+
+extern "C" int fvv_refine_image(const fvv_frame_desc* d, const uint8_t* const* frames, int nsrc, void* out,
+                                void* stream) {
+    int rc = ref_check(d, nsrc, 2 * kRefMaxViews);
+    if (rc) return rc;
+    if (!frames || !out) return fail(FVV_EINVAL, "null argument");
+    RefSrc s{};
+    for (int i = 0; i < nsrc; i++) s.frame[i] = frames[i];
+    const int Wp = (d->width + 63) / 64 * 64, Hp = (d->height + 63) / 64 * 64;
+    cudaError_t e = ref_img(s, nsrc, d->format, d->width, d->height, Wp, Hp, out, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? FVV_OK : cuda_fail(e, "fvv_refine_image");
+}
+
+extern "C" int fvv_refine_inputs(const fvv_frame_desc* d, const uint8_t* const* left, const uint8_t* const* right,
+                                 const float* const* state, const float* t, int nviews, void* x0, float* merged,
+                                 float* flow0, void* stream) {
+    int rc = ref_check(d, nviews, kRefMaxViews);
+    if (rc) return rc;
+    if (!left || !right || !state || !t || !x0 || !merged || !flow0) return fail(FVV_EINVAL, "null argument");
+    RefViews rv{};
+    for (int i = 0; i < nviews; i++) {
+        if (!(t[i] > 0.0f && t[i] < 1.0f)) return fail(FVV_EINVAL, "view positions must lie in (0, 1)");
+        rv.left[i] = left[i];
+        rv.right[i] = right[i];
+        rv.state[i] = state[i];
+        rv.t[i] = t[i];
+    }
+    const int Wp = (d->width + 63) / 64 * 64, Hp = (d->height + 63) / 64 * 64;
+    cudaError_t e = ref_inputs(rv, nviews, d->format, d->width, d->height, Wp, Hp, x0, merged, flow0,
+                               static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? FVV_OK : cuda_fail(e, "fvv_refine_inputs");
+}
+
+extern "C" int fvv_refine_flow_pool(const float* in, float* out, int w, int h, int nb, void* stream) {
+    if (!in || !out || w < 2 || h < 2 || (w & 1) || (h & 1) || nb < 1) return fail(FVV_EINVAL, "bad flow pyramid level");
+    cudaError_t e = ref_flow_pool(in, out, w, h, nb, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? FVV_OK : cuda_fail(e, "fvv_refine_flow_pool");
+}
+
+extern "C" int fvv_refine_warp_features(const void* feat, int fs, int channels, int w, int h, const float* flow,
+                                        int comp, int src_mul, int src_add, void* dst, int ds, int coff, int nb,
+                                        void* stream) {
+    if (!feat || !flow || !dst || channels % 8 || fs % 8 || ds % 8 || coff % 8 || coff + channels > ds ||
+        channels > fs || w < 2 || h < 2 || nb < 1 || (comp != 0 && comp != 2))
+        return fail(FVV_EINVAL, "bad feature warp");
+    cudaError_t e = ref_warp_feat(feat, fs, channels, w, h, flow, comp, src_mul, src_add, dst, ds, coff, nb,
+                                  static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? FVV_OK : cuda_fail(e, "fvv_refine_warp_features");
+}
+
+extern "C" int fvv_nhwc_copy(const void* src, int ss, int channels, void* dst, int ds, int coff, long long npix,
+                             void* stream) {
+    if (!src || !dst || channels % 8 || ss % 8 || ds % 8 || coff % 8 || coff + channels > ds || channels > ss ||
+        npix < 0)
+        return fail(FVV_EINVAL, "bad channel copy");
+    if (npix == 0) return FVV_OK;
+    cudaError_t e = nhwc_copy(src, ss, channels, dst, ds, coff, npix, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? FVV_OK : cuda_fail(e, "fvv_nhwc_copy");
+}
+
+extern "C" int fvv_refine_output(const fvv_frame_desc* d, uint8_t* const* out, int nviews, const float* r, int rs,
+                                 const float* merged, void* stream) {
+    int rc = ref_check(d, nviews, kRefMaxViews);
+    if (rc) return rc;
+    if (!out || !r || !merged || rs < 3) return fail(FVV_EINVAL, "null argument");
+    RefViews rv{};
+    for (int i = 0; i < nviews; i++) rv.out[i] = out[i];
+    const int Wp = (d->width + 63) / 64 * 64, Hp = (d->height + 63) / 64 * 64;
+    cudaError_t e = ref_out(rv, nviews, d->format, d->width, d->height, Wp, Hp, r, rs, merged,
+                            static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? FVV_OK : cuda_fail(e, "fvv_refine_output");
 }

@@ -128,8 +128,9 @@ struct ConvTile {
     static constexpr int kABytes = 128 * SW;                 // one 128-pixel row segment
     static constexpr int kBBytes = NT * SW;
     static constexpr int kStageBytes = kARows * kABytes + kBChunks * kBBytes;
-    static constexpr int kStages = RR > 0 ? (2 * kStageBytes + 1280 <= 232448 ? 2 : 1)
-                                          : (kStageBytes > 40 * 1024 ? 4 : 6);
+    // as many stages as fit the 227 KB opt-in shared memory (1 KB alignment slack + barriers), at most 6
+    static constexpr int kFit = (232448 - 1280) / kStageBytes;
+    static constexpr int kStages = RR > 0 ? (kFit >= 2 ? 2 : 1) : (kFit < 6 ? kFit : 6);
     static constexpr int kTmemCols = 2 * MT * NT < 32 ? 32 : 2 * MT * NT;  // two accumulator sets
     static constexpr size_t kSmem = 1024 /* alignment slack */ + (size_t)kStages * kStageBytes + 256;
 };
@@ -453,7 +454,10 @@ static cudaError_t launch_nt_sw(const CUtensorMap& a, const CUtensorMap& w, cons
     const unsigned long long bit = 1ull << (dev & 63);
     if (!(attr_done.load(std::memory_order_acquire) & bit)) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::kSmem);
-        if (e != cudaSuccess) return e;
+        if (e != cudaSuccess) {
+            (void)cudaGetLastError();  // do not leave the error for the next launch check to find
+            return e;
+        }
         attr_done.fetch_or(bit, std::memory_order_release);
     }
     (void)ntiles;

@@ -85,6 +85,10 @@ class InterpDiagnostics:  # interp.py:59-64
     flow_mid_left: FlowField | None = None
     flow_mid_right: FlowField | None = None
     mask: np.ndarray | None = None
+    # the two source frames (not in the reference's class): what a refine hook
+    # such as refine.RefineNet.hook() needs besides the flows and the mask
+    left: object = None
+    right: object = None
 
 
 # ---------------------------------------------------------------------------
@@ -338,6 +342,7 @@ def interpolate(left, right, config: InterpConfig | None = None, diagnostics: bo
         diag = InterpDiagnostics()
         if diagnostics or cfg.refine is not None:
             diag = _diagnostics(eng)
+            diag.left, diag.right = left, right
     if cfg.refine is not None:  # the reference's one plugin hook (interp.py:144-145)
         res = cfg.refine(res, diag)
     if diagnostics:

@@ -64,3 +64,62 @@ def make_params(seed: int = 0):
             layers.append((w.float(), b.float()))
         blocks.append(layers)
     return blocks
+
+
+# ---------------------------------------------------------------------------
+# RefineNet + ContextNet ("Refinement Network", layer table
+# PAPER.md:340-365; context-aware residual U-Net after Niklaus & Liu 2018, as
+# in RIFE which the paper follows).  ContextNet runs on each source image;
+# after each of its 4 levels the features are backward-warped to the view
+# with the level's flow (2x2 mean of the finer flow, times 0.5).  The U-Net
+# input is (I_l, I_r, warp(I_l), warp(I_r), w_t, F_l,t, F_r,t) = 17 channels;
+# down_k concatenates the warped context features of level k-1, the decoder
+# concatenates the encoder skips; the head is conv 16 -> 3 + sigmoid and the
+# view is clip(merged + 2 sigmoid - 1, 0, 1).
+# ---------------------------------------------------------------------------
+CONTEXT_LAYERS = (  # name, stride, cin, cout
+    ("x0", 2, 3, 16), ("x1", 1, 16, 16),
+    ("x2", 2, 16, 32), ("x3", 1, 32, 32),
+    ("x4", 2, 32, 64), ("x5", 1, 64, 64),
+    ("x6", 2, 64, 128), ("x7", 1, 128, 128),
+)
+CONTEXT_CH = (16, 32, 64, 128)      # warped context features per level (1/2 .. 1/16)
+REFINE_IN = 17
+REFINE_LAYERS = (  # name, kind, cin, cout
+    ("d0a", "conv_s2", REFINE_IN, 32), ("d0b", "conv", 32, 32),
+    ("d1a", "conv_s2", 32 + 2 * 16, 64), ("d1b", "conv", 64, 64),
+    ("d2a", "conv_s2", 64 + 2 * 32, 128), ("d2b", "conv", 128, 128),
+    ("d3a", "conv_s2", 128 + 2 * 64, 256), ("d3b", "conv", 256, 256),
+    ("u0", "convT", 256 + 2 * 128, 128),
+    ("u1", "convT", 128 + 128, 64),
+    ("u2", "convT", 64 + 64, 32),
+    ("u3", "convT", 32 + 32, 16),
+    ("out", "conv", 16, 3),
+)
+REFINE_HEAD_SCALE = 0.1  # the residual starts small (sigmoid ~ 0.5), like the flow head
+
+
+def make_refine_params(seed: int = 1):
+    """Deterministic He-normal weights of ContextNet and the U-Net.
+
+    Returns {"context": [(w, b)] * 8, "unet": [(w, b)] * 13} (fp32 CPU tensors,
+    torch layouts as make_params)."""
+    import torch
+    g = torch.Generator().manual_seed(int(seed))
+
+    def conv(cin, cout, scale=1.0):
+        w = torch.randn((cout, cin, 3, 3), generator=g) * (2.0 / (cin * 9)) ** 0.5 * scale
+        return w.float(), (torch.randn((cout,), generator=g) * 0.01).float()
+
+    def convT(cin, cout):
+        w = torch.randn((cin, cout, 4, 4), generator=g) * (2.0 / (cin * 4)) ** 0.5
+        return w.float(), (torch.randn((cout,), generator=g) * 0.01).float()
+
+    ctx = [conv(cin, cout) for _, _, cin, cout in CONTEXT_LAYERS]
+    unet = []
+    for name, kind, cin, cout in REFINE_LAYERS:
+        if kind == "convT":
+            unet.append(convT(cin, cout))
+        else:
+            unet.append(conv(cin, cout, REFINE_HEAD_SCALE if name == "out" else 1.0))
+    return {"context": ctx, "unet": unet}
