@@ -279,6 +279,31 @@ int fvv_nhwc_copy(const void* src, int ss, int channels, void* dst, int ds, int 
 int fvv_refine_output(const fvv_frame_desc* desc, uint8_t* const* out, int nviews, const float* r, int rs,
                       const float* merged, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * FVT1 tile encoder, device stage (the hand-off
+ * after the tiling; codec.py:138-216 _encode_plane / encode_frame, dct.py).
+ * Per (tile, plane) job: edge-padded 8x8 blocks of the plane (minus the
+ * previous reconstruction for P records), orthonormal DCT, rint(c / step)
+ * (or the lossless lifting transform at quality 100), the committed
+ * reconstruction into `recon`, zigzag coefficients (int16, 64 per block) and
+ * the block's token count (nonzeros + EOB).  fvv_encode_tokens writes the
+ * 3-byte (run, level) token stream at tok_off[block] * 3; the caller DEFLATEs
+ * each plane's tokens and frames the record (paper_2112_10603_b200/encoder.py).
+ * fvv_encode_set_tables uploads the reference's DCT matrix and zigzag order. */
+typedef struct {
+    const uint8_t* src;    /* tile plane inside the stitched frame (device)      */
+    const uint8_t* prev;   /* previous reconstruction (w x h), NULL for I        */
+    uint8_t* recon;        /* committed reconstruction (w x h) out               */
+    long long block0;      /* first 8x8 block of the job in the batch (ascending) */
+    int32_t pitch, w, h;   /* row pitch of src, plane size (RGB: 3 * width)      */
+    int32_t nbx, nby;      /* ceil(w / 8), ceil(h / 8)                           */
+    int32_t is_p, step, pad;
+} fvv_enc_job;
+int fvv_encode_set_tables(const double* dct64, const uint8_t* zigzag64);
+int fvv_encode_blocks(const fvv_enc_job* jobs_dev, int njobs, long long total_blocks, int lossless, int16_t* zz,
+                      int* ntok, void* stream);
+int fvv_encode_tokens(const int16_t* zz, const long long* tok_off, long long nblocks, uint8_t* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

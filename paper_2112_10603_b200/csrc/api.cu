@@ -13,6 +13,7 @@
 #include "conv_tc.h"
 #include "vinet.h"
 #include "refine.h"
+#include "encode.h"
 
 namespace fvv {
 extern thread_local int g_failed_class;
@@ -947,4 +948,32 @@ extern "C" int fvv_refine_output(const fvv_frame_desc* d, uint8_t* const* out, i
     cudaError_t e = ref_out(rv, nviews, d->format, d->width, d->height, Wp, Hp, r, rs, merged,
                             static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? FVV_OK : cuda_fail(e, "fvv_refine_output");
+}
+
+// ---------------------------------------------------------------------------
+// FVT1 tile encoder, device stage (encode_kernels.cu; host framing in encoder.py)
+// ---------------------------------------------------------------------------
+static_assert(sizeof(EncJob) == sizeof(fvv_enc_job), "fvv_enc_job mirrors fvv::EncJob");
+
+extern "C" int fvv_encode_set_tables(const double* dct64, const uint8_t* zigzag64) {
+    if (!dct64 || !zigzag64) return fail(FVV_EINVAL, "null table");
+    for (int i = 0; i < 64; i++)
+        if (zigzag64[i] > 63) return fail(FVV_EINVAL, "zigzag index out of range");
+    cudaError_t e = enc_set_constants(dct64, zigzag64);
+    return e == cudaSuccess ? FVV_OK : cuda_fail(e, "fvv_encode_set_tables");
+}
+
+extern "C" int fvv_encode_blocks(const fvv_enc_job* jobs_dev, int njobs, long long total_blocks, int lossless,
+                                 int16_t* zz, int* ntok, void* stream) {
+    if (!jobs_dev || njobs < 1 || total_blocks < 0 || !zz || !ntok) return fail(FVV_EINVAL, "bad encode batch");
+    cudaError_t e = enc_blocks(reinterpret_cast<const EncJob*>(jobs_dev), njobs, total_blocks, lossless ? 1 : 0, zz,
+                               ntok, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? FVV_OK : cuda_fail(e, "fvv_encode_blocks");
+}
+
+extern "C" int fvv_encode_tokens(const int16_t* zz, const long long* tok_off, long long nblocks, uint8_t* out,
+                                 void* stream) {
+    if (!zz || !tok_off || !out || nblocks < 0) return fail(FVV_EINVAL, "bad token batch");
+    cudaError_t e = enc_tokens(zz, tok_off, nblocks, out, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? FVV_OK : cuda_fail(e, "fvv_encode_tokens");
 }
