@@ -221,13 +221,19 @@ class DeviceRigStages:
         self.tiled = int(fmt) != PixelFormat.RGB8
         self.sizes = rig_cluster_sizes(width, height, fmt, camera_count, stages, self.views_per_side) \
             if self.tiled else []
-        self.clusters = torch.empty(max(1, sum(self.sizes)), dtype=torch.uint8, device=dev)
+        # one cluster buffer per slot: with the encoder hand-off the clusters stay on
+        # the device until the encode stage has read them
+        self.clusters = [torch.empty(max(1, sum(self.sizes)), dtype=torch.uint8, device=dev)
+                         for _ in range(self.slots)]
         self._host_in = torch.empty((camera_count, fb), dtype=torch.uint8).pin_memory()
-        self._host_out = torch.empty(self.clusters.numel(), dtype=torch.uint8).pin_memory()
+        self._host_out = torch.empty(self.clusters[0].numel(), dtype=torch.uint8).pin_memory()
         self.s_interp = torch.cuda.Stream(device=dev)
         self.s_stitch = torch.cuda.Stream(device=dev)
+        self.s_encode = torch.cuda.Stream(device=dev)
         self._ev_views = [torch.cuda.Event() for _ in range(self.slots)]
+        self._ev_clusters = [torch.cuda.Event() for _ in range(self.slots)]
         self._ev_free = [None] * self.slots
+        self._encoder = None
         self._stamps = [None] * self.slots
         self._next = 0
 
@@ -252,8 +258,8 @@ class DeviceRigStages:
         self.s_interp.synchronize()  # the stage's latency is real; the pinned input is free again
         return k
 
-    def stitch(self, slot: int) -> list:
-        """Every cluster frame of the tick in `slot` (host ClusterFrames)."""
+    def stitch_device(self, slot: int) -> None:
+        """Every cluster frame of the tick in `slot`, left on the device (clusters[slot])."""
         import torch
         from .cluster import LayoutError
         if not self.tiled:
@@ -261,11 +267,35 @@ class DeviceRigStages:
         with torch.cuda.stream(self.s_stitch):
             self.s_stitch.wait_event(self._ev_views[slot])
             rig_clusters(self.views[slot], self.width, self.height, self.format, self.model.camera_count,
-                         self.model.stages, self.views_per_side, out=self.clusters)
+                         self.model.stages, self.views_per_side, out=self.clusters[slot])
             ev = torch.cuda.Event()
             ev.record(self.s_stitch)
             self._ev_free[slot] = ev
-            self._host_out.copy_(self.clusters, non_blocking=True)
+            self._ev_clusters[slot].record(self.s_stitch)
+        self.s_stitch.synchronize()  # the stage's latency is real
+
+    def encode(self, slot: int, quality: int, gop: int, encoder_factory=None) -> list:
+        """FVT1 records of every tile of every cluster frame of `slot`
+        (PipelineHandle._encode, server/pipeline.py:294-318): per cluster, the
+        record bytes of its tiles in tile-map order.  The transform stage runs on
+        the device (encoder.RigEncoder); one encoder per pipeline keeps every
+        tile's closed-loop reconstruction."""
+        import torch
+        if self._encoder is None:
+            if encoder_factory is None:
+                from .encoder import RigEncoder as encoder_factory  # noqa: N813
+            self._encoder = encoder_factory(self.layouts, self.width, self.height, self.format, quality, gop,
+                                            self.engine.device)
+        with torch.cuda.stream(self.s_encode):
+            self.s_encode.wait_event(self._ev_clusters[slot])
+            return self._encoder.encode(self.clusters[slot])
+
+    def stitch(self, slot: int) -> list:
+        """Every cluster frame of the tick in `slot` (host ClusterFrames)."""
+        import torch
+        self.stitch_device(slot)
+        with torch.cuda.stream(self.s_stitch):
+            self._host_out.copy_(self.clusters[slot], non_blocking=True)
         self.s_stitch.synchronize()
         host = self._host_out.numpy()
         stamps = self._stamps[slot]

@@ -43,10 +43,13 @@ def _ref_frame(fvv_frame_mod, ours, template):
                                tuple(ours.planes), ours.timestamp)
 
 
-def install(fvv, pipeline: bool = False, stages_factory=None) -> None:
+def install(fvv, pipeline: bool = False, stages_factory=None, encoder: bool = False, encoder_factory=None) -> None:
     """Rebind the reference's path names (and, with `pipeline`, its stage
     workers).  `stages_factory(width, height, fmt, cams, stages, vps, config,
-    slots)` builds the device stage state; default pipeline.DeviceRigStages."""
+    slots)` builds the device stage state; default pipeline.DeviceRigStages.
+    With `encoder` the encode stage's transform runs on the device too: the
+    cluster frames stay in HBM from _stitch to _encode (encoder.RigEncoder,
+    or `encoder_factory(layouts, width, height, fmt, quality, gop, device)`)."""
     frame_mod = importlib.import_module(fvv.__name__ + ".frame")
     interp_mod = importlib.import_module(fvv.__name__ + ".interp")
     cluster_mod = importlib.import_module(fvv.__name__ + ".cluster")
@@ -103,7 +106,7 @@ def install(fvv, pipeline: bool = False, stages_factory=None) -> None:
                 repl[(m, n)] = repl[(src, n)]
     if pipeline:
         pl = importlib.import_module(fvv.__name__ + ".server.pipeline")
-        hooks = _pipeline_hooks(pl, frame_mod, stages_factory)
+        hooks = _pipeline_hooks(pl, frame_mod, stages_factory, encoder, encoder_factory)
         for n, f in hooks.items():
             repl[(pl.PipelineHandle, n)] = f
     for (m, n), f in repl.items():
@@ -114,8 +117,8 @@ def install(fvv, pipeline: bool = False, stages_factory=None) -> None:
 _TOKEN = struct.Struct("<4sI")  # views-channel payload: magic + device slot
 
 
-def _pipeline_hooks(pl, frame_mod, stages_factory):
-    """Device-resident replacements of PipelineHandle._interp / _stitch."""
+def _pipeline_hooks(pl, frame_mod, stages_factory, encoder=False, encoder_factory=None):
+    """Device-resident replacements of PipelineHandle._interp / _stitch (/ _encode)."""
     if stages_factory is None:
         from .pipeline import DeviceRigStages as stages_factory  # noqa: N813
     from .interp import InterpConfig
@@ -166,6 +169,38 @@ def _pipeline_hooks(pl, frame_mod, stages_factory):
             out = pl.UnifiedDataPack(pl.PackType.FRAME_RAW, pl._bundle_frames(frames))
             self.ch_clusters.put(out.stamped("stitch-out", time.perf_counter()))
 
+    def _stitch_to_encoder(self) -> None:
+        """server/pipeline.py:273-292 with the cluster frames left on the device."""
+        if self.config.interp is not None and self.config.interp.refine is not None:
+            return _SAVED[(pl.PipelineHandle, "_stitch")](self)
+        for pack in self._subs["stitch"]:
+            t0 = time.perf_counter()
+            magic, slot = _TOKEN.unpack(pack.payload)
+            if magic != b"B200":
+                raise ValueError("views channel pack is not a device-slot token")
+            self._b200_stages.stitch_device(slot)
+            self.report.add(pl.STAGE_STITCH, time.perf_counter() - t0)
+            out = pl.UnifiedDataPack(pl.PackType.FRAME_RAW, _TOKEN.pack(b"B2CL", slot))
+            self.ch_clusters.put(out.stamped("stitch-out", time.perf_counter()))
+
+    def _encode(self) -> None:
+        """server/pipeline.py:294-318: every tile's FVT1 record, transform on the device."""
+        if self.config.interp is not None and self.config.interp.refine is not None:
+            return _SAVED[(pl.PipelineHandle, "_encode")](self)
+        cfg = self.config
+        for pack in self._subs["encode"]:
+            t0 = time.perf_counter()
+            self.report.add(pl.STAGE_SCHEDULE, t0 - pack.trace_time("stitch-out"))
+            magic, slot = _TOKEN.unpack(pack.payload)
+            if magic != b"B2CL":
+                raise ValueError("clusters channel pack is not a device-slot token")
+            per_cluster = self._b200_stages.encode(slot, cfg.quality, cfg.gop, encoder_factory)
+            self.report.add(pl.STAGE_ENCODE, time.perf_counter() - t0)
+            out = pl.UnifiedDataPack(pl.PackType.TILE_BITSTREAM, pl._bundle_records(per_cluster))
+            self.ch_encoded.put(out.stamped("encode-out"))
+
+    if encoder:
+        return {"_interp": _interp, "_stitch": _stitch_to_encoder, "_encode": _encode}
     return {"_interp": _interp, "_stitch": _stitch}
 
 

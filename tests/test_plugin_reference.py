@@ -106,6 +106,26 @@ class OracleStages:
         OracleStages.calls.append(("stitch", slot))
         return out
 
+    # encoder hand-off interface (DeviceRigStages.stitch_device / .encode)
+    def stitch_device(self, slot):
+        self.slots[slot] = self.slots[slot] + (self.stitch(slot),)
+
+    def encode(self, slot, quality, gop, encoder_factory=None):
+        from fvv.codec import TileEncoder
+        from fvv.frame import PixelFormat, frame_from_planes
+        encs = self.__dict__.setdefault("encs", {})
+        per_cluster = []
+        for cf in self.slots[slot][2]:
+            recs = []
+            for rect in cf.tile_map:
+                tile = cf.crop(rect)
+                ref = frame_from_planes(list(tile.planes), PixelFormat(int(tile.format)), tile.timestamp)
+                enc = encs.setdefault((cf.cluster_id, rect.index), TileEncoder(quality, gop))
+                recs.append(enc.encode(ref).to_bytes())
+            per_cluster.append(recs)
+        OracleStages.calls.append(("encode", slot))
+        return per_cluster
+
 
 def _run(fvv, ticks):
     from fvv.interp import InterpConfig
@@ -139,3 +159,24 @@ def test_pipeline_hooks_publish_reference_identical_segments(fvv):
         assert got_segs[k] == ref_segs[k], f"segment {k} differs"
     stats = handle.report.stats()
     assert stats["view interpolation"]["count"] == 6 and stats["adaptive stitch"]["count"] == 6
+
+
+def test_pipeline_hooks_with_encoder_hand_off(fvv):
+    """install(fvv, pipeline=True, encoder=True): _stitch leaves the cluster
+    frames on the device and _encode reads them there; the clusters channel
+    carries slot tokens.  Segments equal the unmodified reference pipeline's."""
+    from fvv.scene import SceneSpec, SyntheticScene, default_sprites_for
+    from paper_2112_10603_b200 import plugin
+    spec = SceneSpec(seed=7, camera_count=3, width=64, height=48, format="yuv420",
+                     sprites=default_sprites_for(64, 48))
+    scene = SyntheticScene(spec)
+    ticks = [[scene.render_view(float(c), t) for c in range(3)] for t in range(3)]
+    ref_segs, _ = _run(fvv, ticks)
+    OracleStages.calls = []
+    plugin.install(fvv, pipeline=True, stages_factory=OracleStages, encoder=True)
+    got_segs, handle = _run(fvv, ticks)
+    plugin.uninstall()
+    kinds = [c for c, _ in OracleStages.calls]
+    assert kinds.count("interp") == 6 and kinds.count("encode") == 6
+    assert got_segs == ref_segs
+    assert handle.report.stats()["encoder"]["count"] == 6
