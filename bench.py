@@ -474,6 +474,18 @@ def run_b200(args, cfg, rank, world, local_rank):
         "gpu_launches": gpu_launches,
         "clocks": clk,
     }
+    if vps and fmt != 2 and not args.no_encoder:
+        try:
+            # a second rig frame (another scene) so consecutive P records carry real residuals
+            cams2 = torch.from_numpy(synth_rig(W, H, fmt, C, seed=4242)).to(dev)
+            clusters2 = torch.empty_like(clusters)
+            with torch.cuda.stream(stream):
+                eng.rig(cams2, S, views)
+                rig_clusters(views, W, H, fmt, C, S, vps, out=clusters2)
+            torch.cuda.synchronize()
+            line["encoder"] = run_encoder(cfg, dev, [clusters, clusters2], stream)
+        except Exception as exc:  # the headline line must survive a failure of the secondary stage
+            line["encoder"] = {"error": f"{type(exc).__name__}: {exc}"}
     if not args.no_vinet and rank == 0 and min(W, H) >= 64:
         try:
             line["vinet"] = run_vinet(cfg, dev, use_graph=not args.no_graph)
@@ -714,6 +726,55 @@ def run_vinet(cfg, dev, steps=10, warmup=3, use_graph=True):
     }
 
 
+def run_encoder(cfg, dev, cluster_bufs, stream, ticks=4):
+    """The encoder hand-off: FVT1 records of every
+    tile of every cluster frame of the rig frame (server/pipeline.py:294-318),
+    transform stage on the device (encoder.RigEncoder), DEFLATE on the host
+    threads.  gop 30 (PipelineConfig default): tick 0 is intra, the rest P."""
+    import time
+
+    import torch
+    from paper_2112_10603_b200.cluster import build_layouts
+    from paper_2112_10603_b200.encoder import RigEncoder
+    from paper_2112_10603_b200.viewmodel import ViewIndexModel
+    W, H, fmt, C, S, vps = cfg["W"], cfg["H"], cfg["fmt"], cfg["cams"], cfg["stages"], cfg["vps"]
+    threads = os.cpu_count() or 8
+    enc = RigEncoder(build_layouts(ViewIndexModel(C, S), vps), W, H, fmt, quality=75, gop=30, device=dev,
+                     threads=threads)
+    with torch.cuda.stream(stream):
+        enc.encode(cluster_bufs[0])  # intra tick (warm-up)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        nbytes = 0
+        for k in range(ticks):
+            recs = enc.encode(cluster_bufs[(k + 1) % len(cluster_bufs)])
+            nbytes += sum(len(r) for c in recs for r in c)
+        wall = (time.perf_counter() - t0) / ticks
+        # device transform stage alone (blocks + tokens kernels), CUDA events
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        import ctypes
+        from paper_2112_10603_b200 import _lib
+        L = _lib.load()
+        jt = enc._last_jobs
+        a.record(stream)
+        for _ in range(ticks):
+            _lib.check(L.fvv_encode_blocks(ctypes.c_void_p(jt.data_ptr()), enc._last_njobs, enc.nblocks,
+                                           int(enc.lossless), ctypes.c_void_p(enc.zz.data_ptr()),
+                                           ctypes.c_void_p(enc.ntok.data_ptr()), ctypes.c_void_p(stream.cuda_stream)))
+        b.record(stream)
+        torch.cuda.synchronize()
+    dev_ms = a.elapsed_time(b) / ticks
+    tiles = sum(len(t) for t in enc.tiles)
+    return {"path": "FVT1 tile records (codec.TileEncoder-identical bytes) of every tile of the rig frame's "
+                    "cluster frames: 8x8 DCT / quant / reconstruction / zigzag / tokens on the device, "
+                    "DEFLATE on %d host threads" % threads,
+            "tiles_per_rig_frame": tiles, "quality": 75, "gop": 30, "record": "P (closed loop, device-resident "
+            "reconstruction)", "ms_per_rig_frame": wall * 1e3, "device_transform_ms": dev_ms,
+            "bytes_per_rig_frame": nbytes / ticks,
+            "parity": "byte-identical records vs reference-generated goldens, lossy I/P and lossless "
+                      "(tests/test_gpu_encoder.py)"}
+
+
 def refine_conv_flops(W, H, nviews, npairs=1):
     """Useful conv FLOPs of RefineNet (per view) + ContextNet (per pair, 2 images) on the 64-aligned canvas."""
     from paper_2112_10603_b200.vinet_params import CONTEXT_LAYERS, REFINE_LAYERS
@@ -939,6 +1000,7 @@ def main():
                     help="independent rig frames of the live stream processed concurrently per step")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-vinet", action="store_true", help="skip the VINet (CNN path) section")
+    ap.add_argument("--no-encoder", action="store_true", help="skip the encoder hand-off section")
     ap.add_argument("--shard", default="auto", choices=["auto", "gap", "frame"],
                     help="N>1 partition: gap = one rig frame split by camera gaps (latency; default for "
                          "tiled rigs that fit, cfg3/cfg4), frame = whole rig frames per rank (throughput, cfg5)")

@@ -176,6 +176,7 @@ class RigEncoder:
                     meta.append((c, ti, pi, block0, nbx * nby))
                     block0 += nbx * nby
         jt = torch.from_numpy(np.array(jobs, dtype=_JOB).view(np.uint8)).to(self.device, non_blocking=False)
+        self._last_jobs, self._last_njobs = jt, len(jobs)
         L, st = self._L, self._stream()
         _lib.check(L.fvv_encode_blocks(ctypes.c_void_p(jt.data_ptr()), len(jobs), block0, int(self.lossless),
                                        ctypes.c_void_p(self.zz.data_ptr()), ctypes.c_void_p(self.ntok.data_ptr()), st))
