@@ -304,6 +304,16 @@ int fvv_encode_blocks(const fvv_enc_job* jobs_dev, int njobs, long long total_bl
                       int* ntok, void* stream);
 int fvv_encode_tokens(const int16_t* zz, const long long* tok_off, long long nblocks, uint8_t* out, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * TS packaging (host code; mpegts.py:188-212
+ * mux_segment): one cluster's MPEG-TS segment from the tile records of its
+ * frames.  records[f * ntiles + k] / record_lens[...] are HOST pointers; pts[f]
+ * the frame's 90 kHz PTS.  0 ok, -1 bad arguments / short buffer, -2 frame 0
+ * is not intra on every tile.  Thread-safe (no shared state). */
+size_t fvv_ts_segment_bytes(const uint32_t* record_lens, int ntiles, int nframes);
+int fvv_ts_mux_segment(const uint8_t* const* records, const uint32_t* record_lens, int ntiles, int nframes,
+                       const int64_t* pts, uint8_t* out, size_t out_cap, size_t* written);
+
 #ifdef __cplusplus
 }
 #endif

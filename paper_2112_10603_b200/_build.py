@@ -14,7 +14,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libfvv_b200.so"
-SOURCES = ["interp_kernels.cu", "tile_kernels.cu", "conv_tc.cu", "vinet_kernels.cu", "refine_kernels.cu", "encode_kernels.cu", "api.cu"]
+SOURCES = ["interp_kernels.cu", "tile_kernels.cu", "conv_tc.cu", "vinet_kernels.cu", "refine_kernels.cu", "encode_kernels.cu", "ts_mux.cpp", "api.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
@@ -50,7 +50,10 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
     def one(src: str) -> Path:
         obj = objdir / (Path(src).stem + ".o")
-        cmd = [nvcc(), *compile_flags, *extra, "-c", "-o", str(obj), str(CSRC / src)]
+        if src.endswith(".cpp"):  # host-only translation unit
+            cmd = [shutil.which("g++") or "g++", "-O2", "-std=c++17", "-fPIC", "-c", "-o", str(obj), str(CSRC / src)]
+        else:
+            cmd = [nvcc(), *compile_flags, *extra, "-c", "-o", str(obj), str(CSRC / src)]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

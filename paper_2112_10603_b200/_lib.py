@@ -28,6 +28,7 @@ EXPORTS = (
     "fvv_refine_image", "fvv_refine_inputs", "fvv_refine_flow_pool", "fvv_refine_warp_features",
     "fvv_nhwc_copy", "fvv_refine_output",
     "fvv_encode_set_tables", "fvv_encode_blocks", "fvv_encode_tokens",
+    "fvv_ts_segment_bytes", "fvv_ts_mux_segment",
 )
 
 

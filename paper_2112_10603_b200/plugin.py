@@ -43,13 +43,18 @@ def _ref_frame(fvv_frame_mod, ours, template):
                                tuple(ours.planes), ours.timestamp)
 
 
-def install(fvv, pipeline: bool = False, stages_factory=None, encoder: bool = False, encoder_factory=None) -> None:
+def install(fvv, pipeline: bool = False, stages_factory=None, encoder: bool = False, encoder_factory=None,
+            segment: bool = False, names: bool = True) -> None:
     """Rebind the reference's path names (and, with `pipeline`, its stage
     workers).  `stages_factory(width, height, fmt, cams, stages, vps, config,
     slots)` builds the device stage state; default pipeline.DeviceRigStages.
     With `encoder` the encode stage's transform runs on the device too: the
     cluster frames stay in HBM from _stitch to _encode (encoder.RigEncoder,
-    or `encoder_factory(layouts, width, height, fmt, quality, gop, device)`)."""
+    or `encoder_factory(layouts, width, height, fmt, quality, gop, device)`).
+    With `segment` the TS stage (_segment) muxes every cluster of a segment
+    boundary concurrently with the native muxer (segmenter.py); host code,
+    independent of the other hooks.  names=False leaves the path's function
+    names alone (e.g. only the TS stage on a host without a GPU)."""
     frame_mod = importlib.import_module(fvv.__name__ + ".frame")
     interp_mod = importlib.import_module(fvv.__name__ + ".interp")
     cluster_mod = importlib.import_module(fvv.__name__ + ".cluster")
@@ -91,16 +96,18 @@ def install(fvv, pipeline: bool = False, stages_factory=None, encoder: bool = Fa
         return cluster_mod.ClusterFrame(cf.cluster_id, _ref_frame(frame_mod, cf.frame, anchor_frame),
                                         rects)
 
-    repl = {(interp_mod, "interpolate"): interpolate, (interp_mod, "dense_views"): dense_views,
+    repl = {} if not names else {(interp_mod, "interpolate"): interpolate, (interp_mod, "dense_views"): dense_views,
             (cluster_mod, "downscale"): downscale,
             (cluster_mod, "assemble_cluster_frame"): assemble_cluster_frame}
-    for modname, names in ((".server.pipeline", ("dense_views", "downscale", "assemble_cluster_frame")),
+    for modname, seams in ((".server.pipeline", ("dense_views", "downscale", "assemble_cluster_frame")),
                            (".report", ("dense_views",))):
+        if not names:
+            break
         try:
             m = importlib.import_module(fvv.__name__ + modname)
         except ImportError:
             continue
-        for n in names:
+        for n in seams:
             if hasattr(m, n):
                 src = interp_mod if n in ("interpolate", "dense_views") else cluster_mod
                 repl[(m, n)] = repl[(src, n)]
@@ -109,9 +116,44 @@ def install(fvv, pipeline: bool = False, stages_factory=None, encoder: bool = Fa
         hooks = _pipeline_hooks(pl, frame_mod, stages_factory, encoder, encoder_factory)
         for n, f in hooks.items():
             repl[(pl.PipelineHandle, n)] = f
+    if segment:
+        pl = importlib.import_module(fvv.__name__ + ".server.pipeline")
+        ts = importlib.import_module(fvv.__name__ + ".mpegts")
+        repl[(pl.PipelineHandle, "_segment")] = _segment_hook(pl, ts)
     for (m, n), f in repl.items():
         _SAVED.setdefault((m, n), getattr(m, n))
         setattr(m, n, f)
+
+
+def _segment_hook(pl, ts):
+    """server/pipeline.py:320-338 with the clusters of a segment boundary muxed
+    concurrently by the native muxer (byte-identical to mpegts.mux_segment)."""
+    from .segmenter import GopAlignmentError, SegmentMuxer
+
+    def _segment(self) -> None:
+        cfg = self.config
+        fper = cfg.frames_per_segment
+        muxer = SegmentMuxer(threads=max(1, len(self.layouts)))
+        pending = [[] for _ in self.layouts]
+        sequence = 0
+        for pack in self._subs["segment"]:
+            per_cluster = pl._unbundle_records(pack.payload)
+            for c, records in enumerate(per_cluster):
+                pending[c].append(records)
+            self.ticks_done += 1
+            if len(pending[0]) == fper:
+                start_pts = sequence * fper * round(pl.PTS_CLOCK / cfg.fps)
+                try:
+                    bodies = muxer.mux_clusters(pending, cfg.fps, start_pts)
+                except GopAlignmentError as e:
+                    raise ts.GopAlignmentError(str(e)) from None
+                for c, body in enumerate(bodies):
+                    self._on_segment(c, sequence, body, cfg.segment_duration)
+                    self.segments_published += 1
+                pending = [[] for _ in self.layouts]
+                sequence += 1
+        self._on_end()
+    return _segment
 
 
 _TOKEN = struct.Struct("<4sI")  # views-channel payload: magic + device slot

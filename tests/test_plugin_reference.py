@@ -180,3 +180,21 @@ def test_pipeline_hooks_with_encoder_hand_off(fvv):
     assert kinds.count("interp") == 6 and kinds.count("encode") == 6
     assert got_segs == ref_segs
     assert handle.report.stats()["encoder"]["count"] == 6
+
+
+def test_segment_hook_on_the_real_pipeline(fvv):
+    """install(fvv, segment=True, names=False) (host code, runs here): the reference's
+    own pipeline with the native concurrent TS muxer publishes the same bytes."""
+    from fvv.scene import SceneSpec, SyntheticScene, default_sprites_for
+    from paper_2112_10603_b200 import plugin
+    spec = SceneSpec(seed=3, camera_count=3, width=64, height=48, format="yuv420",
+                     sprites=default_sprites_for(64, 48))
+    scene = SyntheticScene(spec)
+    ticks = [[scene.render_view(float(c), t) for c in range(3)] for t in range(2)]
+    ref_segs, _ = _run(fvv, ticks)
+    plugin.install(fvv, segment=True, names=False)
+    h = importlib.import_module("fvv.server.pipeline").PipelineHandle
+    assert h._segment.__module__.startswith("paper_2112_10603_b200")
+    got_segs, handle = _run(fvv, ticks)
+    plugin.uninstall()
+    assert got_segs == ref_segs and handle.segments_published == 3
