@@ -114,6 +114,15 @@ int fvv_interp_diagnostics(fvv_engine* engine, int pair, float* flow_lr, float* 
 int fvv_interp_level_diagnostics(fvv_engine* engine, int pair, int level, float* flow_lr,
                                  float* flow_rl, double* err_lr, double* err_rl, void* stream);
 
+/* Coarse-scale diagnostics of pair i of the most recent batch (interp.py:119-127,
+ * what interpolate(..., diagnostics=True) stores in scales[0..1]): the level's
+ * blend mask (e_r + eps) / (e_l + e_r + 2 eps) and blend_luma, (h_s, w_s) f64,
+ * replayed literally in f64 (off the hot path).  Needs a device scratch of
+ * fvv_interp_level_mask_scratch(engine, level) bytes.  level 0 or 1. */
+size_t fvv_interp_level_mask_scratch(const fvv_engine* engine, int level);
+int fvv_interp_level_mask(fvv_engine* engine, int pair, int level, void* scratch, size_t scratch_bytes,
+                          double* mask, double* blend_luma, void* stream);
+
 /* Per-kernel timing of the stage kernels (bench.py's roofline figure):
  * while enabled, every stage-kernel launch is bracketed by a cudaEvent pair
  * on the launching stream (at most `capacity` launches are recorded).

@@ -51,6 +51,7 @@ def lib():
         L.fvvo_estimate_flow_level.argtypes = [P, P, i, i, P, P, i, i, i, i, P, P, P, P, P, P]
         L.fvvo_candidate_order.argtypes = [i, P, P, P]
         L.fvvo_sad_search.argtypes = [P, i, i, P, i, i, P]
+        L.fvvo_level_mask.argtypes = [P, P, i, i, P, P, ctypes.c_double, P, P]
         L.fvvo_num_threads.restype = i
         L.fvvo_set_threads.argtypes = [i]
         _lib = L
@@ -169,6 +170,33 @@ def estimate_flow_level(left32, right32, prev, radius, block):
                                    _p(prl) if prl is not None else None, ph, pw, radius, block,
                                    _p(flr), _p(frl), _p(olr), _p(orl), _p(elr), _p(erl))
     return (flr, frl), (olr, orl), (elr, erl)
+
+
+def level_mask(yl, yr, flow_lr, flow_rl, eps: float = 1e-3):
+    """interp.py:119-127 (coarse-scale diagnostics): (mask, blend_luma) f64 of one level."""
+    h, w = yl.shape
+    yl = np.ascontiguousarray(yl, np.float32)
+    yr = np.ascontiguousarray(yr, np.float32)
+    flr = np.ascontiguousarray(flow_lr, np.float32)
+    frl = np.ascontiguousarray(flow_rl, np.float32)
+    m = np.empty((h, w), np.float64)
+    b = np.empty((h, w), np.float64)
+    lib().fvvo_level_mask(_p(yl), _p(yr), h, w, _p(flr), _p(frl), float(eps), _p(m), _p(b))
+    return m, b
+
+
+def luma_pyramid(frame, w: int, h: int, fmt: int):
+    """interp.py:67-71 on a packed frame: [quarter, half, full] f32 planes."""
+    frame = np.ascontiguousarray(frame, np.uint8).reshape(-1)
+    if fmt == RGB8:
+        rgb = frame[:w * h * 3].reshape(h, w, 3).astype(np.float64)
+        y = np.rint(0.299 * rgb[..., 0] + 0.587 * rgb[..., 1] + 0.114 * rgb[..., 2]).astype(np.uint8)
+    else:
+        y = frame[:w * h].reshape(h, w)
+    full = y.astype(np.float32)
+    half = ((full[0::2, 0::2] + full[0::2, 1::2]) + (full[1::2, 0::2] + full[1::2, 1::2])) / np.float32(4)
+    quarter = ((half[0::2, 0::2] + half[0::2, 1::2]) + (half[1::2, 0::2] + half[1::2, 1::2])) / np.float32(4)
+    return [quarter.astype(np.float32), half.astype(np.float32), full]
 
 
 def candidate_order(radius: int):

@@ -23,7 +23,7 @@ EXPORTS = (
     "fvv_dense_views", "fvv_rig_views", "fvv_downscale", "fvv_cluster_width",
     "fvv_assemble_cluster", "fvv_rig_cluster_bytes", "fvv_rig_clusters", "fvv_rig_clusters_shard",
     "fvv_profile_enable", "fvv_profile_read", "fvv_kernel_class_name",
-    "fvv_interp_level_diagnostics", "fvv_conv2d_bf16", "fvv_vinet_workspace_size", "fvv_vinet_flow",
+    "fvv_interp_level_diagnostics", "fvv_interp_level_mask_scratch", "fvv_interp_level_mask", "fvv_conv2d_bf16", "fvv_vinet_workspace_size", "fvv_vinet_flow",
     "fvv_vinet_synth", "fvv_vinet_rig", "fvv_vinet_rig_clusters",
     "fvv_refine_image", "fvv_refine_inputs", "fvv_refine_flow_pool", "fvv_refine_warp_features",
     "fvv_nhwc_copy", "fvv_refine_output",
@@ -83,6 +83,8 @@ def load():
         "fvv_interpolate_pairs": (I, [P, PP, PP, PP, I, P]),
         "fvv_interp_diagnostics": (I, [P, I, P, P, P, P]),
         "fvv_interp_level_diagnostics": (I, [P, I, I, P, P, P, P, P]),
+        "fvv_interp_level_mask_scratch": (Z, [P, I]),
+        "fvv_interp_level_mask": (I, [P, I, I, P, Z, P, P, P]),
         "fvv_dense_views": (I, [P, P, P, I, P, P]),
         "fvv_rig_views": (I, [P, P, I, I, P, P]),
         "fvv_downscale": (I, [pd, P, I, I, P, P]),

@@ -25,6 +25,9 @@ cudaError_t run_diag(const Geometry& g, const PairTable& pt, uint8_t* ws, const 
 cudaError_t run_level_diag(const Geometry& g, uint8_t* ws, const Planes& P, int pair, int level,
                            float* flow_lr, float* flow_rl, double* err_lr, double* err_rl,
                            cudaStream_t st);
+size_t level_mask_scratch_bytes(const Geometry& g, int level);
+cudaError_t run_level_mask(const Geometry& g, uint8_t* ws, const Planes& P, int pair, int level, void* scratch,
+                           double* mask, double* blend, cudaStream_t st);
 cudaError_t launch_downscale(int W, int H, int fmt, const uint8_t* frames, int n, int f,
                              uint8_t* out, cudaStream_t st);
 cudaError_t launch_assemble(int W, int H, int fmt, const uint8_t* anchor,
@@ -407,6 +410,24 @@ int fvv_interp_level_diagnostics(fvv_engine* e, int pair, int level, float* flow
     cudaError_t ce = run_level_diag(e->g, e->slots, e->P, pair, level, flow_lr, flow_rl, err_lr, err_rl,
                                     static_cast<cudaStream_t>(stream));
     if (ce != cudaSuccess) return cuda_fail(ce, "level diagnostics");
+    return FVV_OK;
+}
+
+size_t fvv_interp_level_mask_scratch(const fvv_engine* e, int level) {
+    if (!e || level < 0 || level > 1) return 0;
+    return level_mask_scratch_bytes(e->g, level);
+}
+
+int fvv_interp_level_mask(fvv_engine* e, int pair, int level, void* scratch, size_t scratch_bytes, double* mask,
+                          double* blend_luma, void* stream) {
+    if (!e) return fail(FVV_EINVAL, "null engine");
+    if (pair < 0 || pair >= e->last_npairs) return fail(FVV_EINVAL, "no such pair in the most recent batch");
+    if (level < 0 || level > 1) return fail(FVV_EINVAL, "coarse-scale masks exist for levels 0 and 1");
+    if (!scratch || scratch_bytes < level_mask_scratch_bytes(e->g, level) || !mask || !blend_luma)
+        return fail(FVV_EINVAL, "scratch too small or null output");
+    cudaError_t ce = run_level_mask(e->g, e->slots, e->P, pair, level, scratch, mask, blend_luma,
+                                    static_cast<cudaStream_t>(stream));
+    if (ce != cudaSuccess) return cuda_fail(ce, "level mask diagnostics");
     return FVV_OK;
 }
 

@@ -209,6 +209,21 @@ class Interpolator:
             ctypes.c_void_p(elr.data_ptr()), ctypes.c_void_p(erl.data_ptr()), self._stream()))
         return flr, frl, elr, erl
 
+    def level_mask(self, pair: int, level: int):
+        """ScaleDiagnostics.mask / .blend_luma of level 0 or 1 (interp.py:119-127) of pair
+        `pair` of the most recent `pairs` call: (mask, blend_luma) f64 device tensors."""
+        import torch
+        f = SCALE_FACTORS[level]
+        h, w = self.height // f, self.width // f
+        nb = int(self._L.fvv_interp_level_mask_scratch(self._h, level))
+        scratch = torch.empty(max(1, nb), dtype=torch.uint8, device=self.device)
+        m = torch.empty((h, w), dtype=torch.float64, device=self.device)
+        b = torch.empty_like(m)
+        _lib.check(self._L.fvv_interp_level_mask(self._h, pair, level, ctypes.c_void_p(scratch.data_ptr()), nb,
+                                                 ctypes.c_void_p(m.data_ptr()), ctypes.c_void_p(b.data_ptr()),
+                                                 self._stream()))
+        return m, b
+
     def dense(self, left, right, stages: int, views=None):
         """dense_views() on device: left/right (frame_bytes,) -> (2**stages - 1, frame_bytes)."""
         import torch
@@ -341,7 +356,7 @@ def interpolate(left, right, config: InterpConfig | None = None, diagnostics: bo
                                 left.timestamp)
         diag = InterpDiagnostics()
         if diagnostics or cfg.refine is not None:
-            diag = _diagnostics(eng)
+            diag = _diagnostics(eng, coarse_masks=diagnostics)
             diag.left, diag.right = left, right
     if cfg.refine is not None:  # the reference's one plugin hook (interp.py:144-145)
         res = cfg.refine(res, diag)
@@ -350,14 +365,20 @@ def interpolate(left, right, config: InterpConfig | None = None, diagnostics: bo
     return res
 
 
-def _diagnostics(eng: Interpolator) -> InterpDiagnostics:
-    """InterpDiagnostics of pair 0 of the engine's most recent batch (interp.py:114-141)."""
+def _diagnostics(eng: Interpolator, coarse_masks: bool = True) -> InterpDiagnostics:
+    """InterpDiagnostics of pair 0 of the engine's most recent batch (interp.py:114-141).
+    coarse_masks: the levels 0-1 mask / blend_luma, which the reference fills only
+    when diagnostics were requested (interp.py:119)."""
     diag = InterpDiagnostics()
     # per-level flows and match errors (interp.py:114-128)
     for s in range(3):
         flr, frl, elr, erl = (_to_host(t, "diag") for t in eng.level_diagnostics(0, s))
         h, w = flr.shape[:2]
-        diag.scales.append(ScaleDiagnostics(FlowField(w, h, flr), FlowField(w, h, frl), elr, erl))
+        sd = ScaleDiagnostics(FlowField(w, h, flr), FlowField(w, h, frl), elr, erl)
+        if coarse_masks and s < 2:
+            m, b = eng.level_mask(0, s)
+            sd.mask, sd.blend_luma = _to_host(m, "diag"), _to_host(b, "diag")
+        diag.scales.append(sd)
     _, _, m = eng.diagnostics(0)
     m = _to_host(m, "diag")
     f_lr, f_rl = diag.scales[-1].flow_lr, diag.scales[-1].flow_rl

@@ -64,6 +64,9 @@ def main():
                     d[f"lv{s}_flow_rl"] = sd.flow_rl.vectors
                     d[f"lv{s}_err_lr"] = sd.match_error_lr
                     d[f"lv{s}_err_rl"] = sd.match_error_rl
+                    if s < 2:  # coarse-scale mask and blend (interp.py:119-127)
+                        d[f"lv{s}_mask"] = sd.mask
+                        d[f"lv{s}_blend"] = sd.blend_luma
         except ValueError:  # per-level diagnostics need >= 2 px per axis at 1/4 scale
             mid = interp.interpolate(L, R)
         d["out"] = refimpl.packed(mid)

@@ -254,3 +254,38 @@ def test_4k_pair_vs_oracle(torch_cuda):
     _, out = _run_pairs(torch_cuda, w, h, fmt, [a], [b])
     ref = O.interpolate(a, b, w, h, fmt)
     assert np.array_equal(out[0], ref), f"{np.count_nonzero(out[0] != ref)} bytes differ"
+
+
+@pytest.mark.parametrize("name", [n for n in golden_names("interp") if "lv0_mask" in load_golden(n)])
+def test_coarse_level_masks_vs_golden(torch_cuda, name):
+    """ScaleDiagnostics.mask / blend_luma of levels 0-1 (interp.py:119-127), bitwise,
+    through the engine and through interpolate(diagnostics=True)."""
+    import paper_2112_10603_b200 as fv
+    g = load_golden(name)
+    w, h, fmt = int(g["w"]), int(g["h"]), int(g["fmt"])
+    eng, _ = _run_pairs(torch_cuda, w, h, fmt, [g["left"]], [g["right"]])
+    for s in range(2):
+        m, b = (t.cpu().numpy() for t in eng.level_mask(0, s))
+        assert np.array_equal(m, g[f"lv{s}_mask"]), s
+        assert np.array_equal(b, g[f"lv{s}_blend"]), s
+    _, diag = fv.interpolate(fv.frame_from_packed(g["left"], w, h, fmt), fv.frame_from_packed(g["right"], w, h, fmt),
+                             diagnostics=True)
+    assert np.array_equal(diag.scales[0].mask, g["lv0_mask"]) and np.array_equal(diag.scales[1].blend_luma,
+                                                                                   g["lv1_blend"])
+    assert diag.scales[2].blend_luma is None
+
+
+def test_coarse_level_masks_1080p_vs_oracle(torch_cuda):
+    """Levels 0-1 diagnostics at the BASELINE size vs the oracle fed the engine's
+    (bitwise-verified) level flows."""
+    from bench import synth_rig
+    w, h, fmt = 1920, 1080, 1
+    cams = synth_rig(w, h, fmt, 2, seed=11)
+    eng, _ = _run_pairs(torch_cuda, w, h, fmt, [cams[0]], [cams[1]])
+    pl, pr = O.luma_pyramid(cams[0], w, h, fmt), O.luma_pyramid(cams[1], w, h, fmt)
+    for s in range(2):
+        flr, frl, _, _ = (t.cpu().numpy() for t in eng.level_diagnostics(0, s))
+        m_ref, b_ref = O.level_mask(pl[s], pr[s], flr, frl)
+        m, b = (t.cpu().numpy() for t in eng.level_mask(0, s))
+        assert np.array_equal(m, m_ref), s
+        assert np.array_equal(b, b_ref), s
