@@ -135,9 +135,19 @@ int fvv_profile_read(fvv_engine* engine, double* ms, int* launches, int nclasses
 const char* fvv_kernel_class_name(int kernel_class);
 
 /* interp.py:151-170: views = (2^stages - 1) frames, contiguous, left -> right.
- * Requires max_pairs >= 2^(stages-1). */
-int fvv_dense_views(fvv_engine* engine, const uint8_t* left, const uint8_t* right, int stages,
-                    uint8_t* views, void* stream);
+ * mode FVV_DENSE_RECURSIVE: the reference's recursive midpoints (bit-exact;
+ *   requires max_pairs >= 2^(stages-1); no scratch).
+ * mode FVV_DENSE_DIRECT: direct-t -- one interpolation of (left, right), whose
+ *   output is the t = 1/2 view bit-exactly (interp.py:131-132), and every other
+ *   view t = j / 2^stages from the same flows and mask in one fp32 synthesis
+ *   pass (F_t->l = 2t F_m->l, F_t->r = 2(1-t) F_m->r, w_t = (1-t)M/((1-t)M +
+ *   t(1-M))); the reference has no such mode, so there is no byte parity off
+ *   t = 1/2.  Needs fvv_dense_views_scratch(engine, mode) bytes of device scratch. */
+#define FVV_DENSE_RECURSIVE 0
+#define FVV_DENSE_DIRECT 1
+size_t fvv_dense_views_scratch(const fvv_engine* engine, int mode);
+int fvv_dense_views(fvv_engine* engine, const uint8_t* left, const uint8_t* right, int stages, int mode,
+                    uint8_t* views, void* scratch, size_t scratch_bytes, void* stream);
 
 /* server/pipeline.py:254-271: one rig frame.  cams = ncams contiguous frames;
  * views = (ncams-1)*2^stages + 1 contiguous frames in global view order

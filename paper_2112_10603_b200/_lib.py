@@ -14,13 +14,14 @@ from ._build import LIB
 
 FVV_OK, FVV_EINVAL, FVV_ELAYOUT, FVV_ECUDA, FVV_EUNSUPPORTED = 0, -1, -2, -3, -4
 FVV_TUNE_SCAN_COOP_MIN, FVV_TUNE_SADW_RB_MIN_CTAS, FVV_TUNE_MASK_COLS2 = 0, 1, 2
+FVV_DENSE_RECURSIVE, FVV_DENSE_DIRECT = 0, 1
 
 # every symbol include/fvv_b200.h declares (tests/test_abi.py checks both ways)
 EXPORTS = (
     "fvv_last_error", "fvv_build_info", "fvv_frame_bytes", "fvv_validate_params",
     "fvv_engine_workspace_size", "fvv_engine_create", "fvv_engine_destroy",
     "fvv_engine_max_pairs", "fvv_engine_set_tuning", "fvv_interpolate_pairs", "fvv_interp_diagnostics",
-    "fvv_dense_views", "fvv_rig_views", "fvv_downscale", "fvv_cluster_width",
+    "fvv_dense_views", "fvv_dense_views_scratch", "fvv_rig_views", "fvv_downscale", "fvv_cluster_width",
     "fvv_assemble_cluster", "fvv_rig_cluster_bytes", "fvv_rig_clusters", "fvv_rig_clusters_shard",
     "fvv_profile_enable", "fvv_profile_read", "fvv_kernel_class_name",
     "fvv_interp_level_diagnostics", "fvv_interp_level_mask_scratch", "fvv_interp_level_mask", "fvv_conv2d_bf16", "fvv_vinet_workspace_size", "fvv_vinet_flow",
@@ -85,7 +86,8 @@ def load():
         "fvv_interp_level_diagnostics": (I, [P, I, I, P, P, P, P, P]),
         "fvv_interp_level_mask_scratch": (Z, [P, I]),
         "fvv_interp_level_mask": (I, [P, I, I, P, Z, P, P, P]),
-        "fvv_dense_views": (I, [P, P, P, I, P, P]),
+        "fvv_dense_views": (I, [P, P, P, I, I, P, P, Z, P]),
+        "fvv_dense_views_scratch": (Z, [P, I]),
         "fvv_rig_views": (I, [P, P, I, I, P, P]),
         "fvv_downscale": (I, [pd, P, I, I, P, P]),
         "fvv_cluster_width": (I, [I, I]),

@@ -26,6 +26,8 @@ cudaError_t run_level_diag(const Geometry& g, uint8_t* ws, const Planes& P, int 
                            float* flow_lr, float* flow_rl, double* err_lr, double* err_rl,
                            cudaStream_t st);
 size_t level_mask_scratch_bytes(const Geometry& g, int level);
+cudaError_t run_direct_state(const Geometry& g, uint8_t* ws, const Planes& P, int pair, const double* mask,
+                             float* state, cudaStream_t st);
 cudaError_t run_level_mask(const Geometry& g, uint8_t* ws, const Planes& P, int pair, int level, void* scratch,
                            double* mask, double* blend, cudaStream_t st);
 cudaError_t launch_downscale(int W, int H, int fmt, const uint8_t* frames, int n, int f,
@@ -452,12 +454,57 @@ static int run_recursion(fvv_engine* e, uint8_t* base, long stride, int nslots, 
     return FVV_OK;
 }
 
-int fvv_dense_views(fvv_engine* e, const uint8_t* left, const uint8_t* right, int stages,
-                    uint8_t* views, void* stream) {
+size_t fvv_dense_views_scratch(const fvv_engine* e, int mode) {
+    if (!e) return 0;
+    if (mode == FVV_DENSE_RECURSIVE) return 0;
+    const size_t n = (size_t)e->g.W * e->g.H;
+    return align_up(n * 5 * sizeof(float)) + align_up(n * sizeof(double)) + align_up((size_t)e->g.frame_bytes);
+}
+
+// direct-t (mode 1): ONE interpolation of (left, right) -- its output is the
+// t = 1/2 view, bit-exact with interp.py:131-132 -- then every other view
+// t = j / 2^stages from the same flows and mask in one synthesis pass (the
+// VINet direct-t kernel: F_t->l = 2t F_m->l, F_t->r = 2(1-t) F_m->r,
+// w_t = (1-t) M / ((1-t) M + t (1-M)); fp32, oracle vinet_ref.synth)
+static int dense_direct(fvv_engine* e, const uint8_t* left, const uint8_t* right, int stages, uint8_t* views,
+                        void* scratch, size_t scratch_bytes, cudaStream_t st) {
+    if (!scratch || scratch_bytes < fvv_dense_views_scratch(e, FVV_DENSE_DIRECT))
+        return fail(FVV_EINVAL, "direct-t needs fvv_dense_views_scratch(engine, 1) bytes of scratch");
+    const size_t n = (size_t)e->g.W * e->g.H;
+    float* state = static_cast<float*>(scratch);
+    double* mask = reinterpret_cast<double*>(static_cast<uint8_t*>(scratch) + align_up(n * 5 * sizeof(float)));
+    uint8_t* mid = static_cast<uint8_t*>(scratch) + align_up(n * 5 * sizeof(float)) + align_up(n * sizeof(double));
+    PairTable pt;
+    pt.left[0] = left;
+    pt.right[0] = right;
+    pt.out[0] = mid;
+    cudaError_t ce = run_interp_stage(e->g, pt, e->slots, e->P, e->rank_of, e->cand_of_rank, 1, mask,
+                                      e->profiling ? &e->prof : nullptr, st);
+    if (ce != cudaSuccess) return cuda_fail(ce, "dense_views (direct-t): interpolate");
+    e->last = pt;
+    e->last_npairs = 1;
+    if ((ce = run_direct_state(e->g, e->slots, e->P, 0, mask, state, st)) != cudaSuccess)
+        return cuda_fail(ce, "dense_views (direct-t): state");
+    const int nv = (1 << stages) - 1;
+    VinPairs pp{};
+    pp.left[0] = left;
+    pp.right[0] = right;
+    const size_t fb = (size_t)e->g.frame_bytes;
+    if ((ce = vin_synth(pp, 1, state, e->g.fmt, e->g.W, e->g.H, nv, views, fb, (size_t)nv * fb, st)) != cudaSuccess)
+        return cuda_fail(ce, "dense_views (direct-t): synthesis");
+    ce = cudaMemcpyAsync(views + (size_t)(nv / 2) * fb, mid, fb, cudaMemcpyDeviceToDevice, st);
+    if (ce != cudaSuccess) return cuda_fail(ce, "dense_views (direct-t): midpoint");
+    return FVV_OK;
+}
+
+int fvv_dense_views(fvv_engine* e, const uint8_t* left, const uint8_t* right, int stages, int mode,
+                    uint8_t* views, void* scratch, size_t scratch_bytes, void* stream) {
     if (!e) return fail(FVV_EINVAL, "null engine");
     if (stages < 1) return fail(FVV_EINVAL, "stages must be >= 1");
     if (stages > 6) return fail(FVV_EINVAL, "stages > 6 refused: 2**n - 1 views grows too fast");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (mode == FVV_DENSE_DIRECT) return dense_direct(e, left, right, stages, views, scratch, scratch_bytes, st);
+    if (mode != FVV_DENSE_RECURSIVE) return fail(FVV_EINVAL, "mode must be 0 (recursive) or 1 (direct-t)");
     const long fb = e->g.frame_bytes;
     const int n = (1 << stages) - 1;
     // the recursion reads the endpoints from their own buffers: build a

@@ -2394,6 +2394,35 @@ __global__ void k_diag_level(Geometry g, const uint8_t* __restrict__ ws, Planes 
     }
 }
 
+// direct-t state of pair `pair` (fvv_dense_views mode 1): the VINet synthesis
+// state (5, H, W) f32 = (F_m->l, F_m->r, logit M) from the engine's final
+// flows (exact: FlowField.scaled(-0.5) of the level-2 flow) and the f64 mask
+__global__ void k_direct_state(Geometry g, const uint8_t* __restrict__ ws, Planes P, int pair,
+                               const double* __restrict__ mask, float* __restrict__ state) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t n = (size_t)g.W * g.H;
+    if (i >= (int)n) return;
+    const int y = i / g.W, x = i - (i / g.W) * g.W;
+    const Level L1 = g.lv[1], L2 = g.lv[2];
+    const float sc = 1.0f / (float)(1 << g.fb[2]);
+    for (int d = 0; d < 2; d++) {
+        const int2 base = up2_fixed(cplane<int2>(ws, P, P.flow1[d], pair), L1.h, L1.w, y, x);
+        const int2 res = b2p_fixed(cplane<BlockHit>(ws, P, P.hit[2][d], pair), L2.nby, L2.nbx, L2.block, y, x);
+        const int bs = g.fb[2] - (g.fb[1] + 3), rs = g.fb[2] - g.rb[2];
+        state[(size_t)(2 * d) * n + i] = ((float)((base.x << bs) + (res.x << rs)) * sc) * -0.5f;
+        state[(size_t)(2 * d + 1) * n + i] = ((float)((base.y << bs) + (res.y << rs)) * sc) * -0.5f;
+    }
+    const double m = fmin(fmax(mask[i], 1e-7), 1.0 - 1e-7);
+    state[4 * n + i] = (float)log(m / (1.0 - m));
+}
+
+cudaError_t run_direct_state(const Geometry& g, uint8_t* ws, const Planes& P, int pair, const double* mask,
+                             float* state, cudaStream_t st) {
+    const int n = g.W * g.H;
+    k_direct_state<<<(n + 255) / 256, 256, 0, st>>>(g, ws, P, pair, mask, state);
+    return cudaGetLastError();
+}
+
 cudaError_t run_level_diag(const Geometry& g, uint8_t* ws, const Planes& P, int pair, int level,
                            float* flow_lr, float* flow_rl, double* err_lr, double* err_rl,
                            cudaStream_t st) {

@@ -224,8 +224,12 @@ class Interpolator:
                                                  self._stream()))
         return m, b
 
-    def dense(self, left, right, stages: int, views=None):
-        """dense_views() on device: left/right (frame_bytes,) -> (2**stages - 1, frame_bytes)."""
+    def dense(self, left, right, stages: int, views=None, mode: int = 0):
+        """dense_views() on device: left/right (frame_bytes,) -> (2**stages - 1, frame_bytes).
+
+        mode 0 (FVV_DENSE_RECURSIVE): the reference's recursive midpoints, bit-exact.
+        mode 1 (FVV_DENSE_DIRECT): direct-t -- one interpolation (its output is the
+        t = 1/2 view, bit-exact) and every other view from the same flows and mask."""
         import torch
         if stages < 1:
             raise ValueError("stages must be >= 1")
@@ -235,9 +239,13 @@ class Interpolator:
         self._check_frames(right)
         if views is None:
             views = torch.empty(((1 << stages) - 1, self.frame_bytes), dtype=torch.uint8, device=left.device)
+        nb = int(self._L.fvv_dense_views_scratch(self._h, int(mode)))
+        scratch = torch.empty(max(1, nb), dtype=torch.uint8, device=left.device) if nb else None
         _lib.check(self._L.fvv_dense_views(self._h, ctypes.c_void_p(left.data_ptr()),
-                                           ctypes.c_void_p(right.data_ptr()), stages,
-                                           ctypes.c_void_p(views.data_ptr()), self._stream()))
+                                           ctypes.c_void_p(right.data_ptr()), stages, int(mode),
+                                           ctypes.c_void_p(views.data_ptr()),
+                                           ctypes.c_void_p(scratch.data_ptr() if scratch is not None else 0), nb,
+                                           self._stream()))
         return views
 
     def rig(self, cams, stages: int, views=None):
@@ -389,15 +397,23 @@ def _diagnostics(eng: Interpolator, coarse_masks: bool = True) -> InterpDiagnost
     return diag
 
 
-def dense_views(left, right, stages: int, config: InterpConfig | None = None) -> list:
-    """Recursive midpoint interpolation: 2**stages - 1 views, left to right (interp.py:151-170)."""
+def dense_views(left, right, stages: int, config: InterpConfig | None = None, mode: str = "recursive") -> list:
+    """2**stages - 1 views between left and right, left to right (interp.py:151-170).
+
+    mode "recursive" (the reference's algorithm, bit-exact), or -- extensions
+    the reference does not have -- "direct" (one SAD-flow interpolation per pair,
+    its t = 1/2 view bit-exact, the other views direct-t from the same flows and
+    mask) and "vinet" (the paper's CNN flows, direct-t synthesis; width and
+    height >= 64)."""
     if stages < 1:
         raise ValueError("stages must be >= 1")
     if stages > 6:
         raise ValueError("stages > 6 refused: 2**n - 1 views grows too fast")
+    if mode not in ("recursive", "direct", "vinet"):
+        raise ValueError(f"unknown dense_views mode {mode!r}")
     cfg = config or InterpConfig()
     _check_pair(left, right)
-    if cfg.refine is not None:
+    if cfg.refine is not None and mode == "recursive":
         # the hook runs on every intermediate view, so recursion goes pair by pair
         seq = [left, right]
         for _ in range(stages):
@@ -409,7 +425,25 @@ def dense_views(left, right, stages: int, config: InterpConfig | None = None) ->
             seq = nxt
         return seq[1:-1]
     import torch
-    eng = _engine(left.width, left.height, left.format, cfg, 1 << (stages - 1))
     with torch.cuda.stream(_thread_stream()):
-        views = _to_host(eng.dense(_to_device(left, "in0"), _to_device(right, "in1"), stages))
+        dl, dr = _to_device(left, "in0"), _to_device(right, "in1")
+        if mode == "vinet":
+            net = _vinet(left.width, left.height, left.format)
+            views = net.dense_views(dl[None], dr[None], (1 << stages) - 1)[0]
+        else:
+            eng = _engine(left.width, left.height, left.format, cfg, 1 << (stages - 1) if mode == "recursive" else 1)
+            views = eng.dense(dl, dr, stages, mode=0 if mode == "recursive" else 1)
+        views = _to_host(views)
     return [frame_from_packed(v, left.width, left.height, left.format, left.timestamp) for v in views]
+
+
+def _vinet(width, height, fmt):
+    """This thread's VINet engine for a geometry (seeded weights, vinet_params)."""
+    import torch
+    key = ("vinet", width, height, int(fmt), torch.cuda.current_device())
+    net = _tls.engines.get(key)
+    if net is None:
+        from .vinet import VINet
+        net = VINet(width, height, fmt, max_pairs=1)
+        _tls.engines[key] = net
+    return net

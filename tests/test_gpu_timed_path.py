@@ -287,3 +287,46 @@ def test_device_rig_stages_two_threads_vs_golden(torch_cuda):
                          np.int32)
         assert np.array_equal(rects, g["rects"])
     assert np.array_equal(st.views_host(results[-1][0]), g["views"])
+
+
+@pytest.mark.parametrize("w,h,fmt,stages", [(256, 192, 1, 3), (192, 128, 0, 2), (200, 124, 2, 4)])
+def test_direct_t_dense_views(torch_cuda, w, h, fmt, stages):
+    """dense_views mode "direct" (fvv_dense_views FVV_DENSE_DIRECT): the t = 1/2 view
+    is the reference's midpoint bit for bit; every other view equals the direct-t
+    synthesis of the oracle's flows and mask (vinet_ref.synth, fp32) within 1 level."""
+    import torch
+    from oracle import vinet_ref as V
+    from paper_2112_10603_b200.interp import Interpolator
+    cams = synth_rig(w, h, fmt, 2, seed=w + stages)
+    eng = Interpolator(w, h, fmt, max_pairs=1)
+    got = eng.dense(torch.from_numpy(cams[0]).cuda(), torch.from_numpy(cams[1]).cuda(), stages, mode=1).cpu().numpy()
+    nv = (1 << stages) - 1
+    mid, d = O.interpolate(cams[0], cams[1], w, h, fmt, with_diag=True)
+    assert np.array_equal(got[nv // 2], mid)
+    m = np.clip(d["mask"], 1e-7, 1 - 1e-7)
+    st = torch.from_numpy(np.concatenate([np.moveaxis(d["flow_lr"] * np.float32(-0.5), -1, 0),
+                                          np.moveaxis(d["flow_rl"] * np.float32(-0.5), -1, 0),
+                                          np.log(m / (1 - m))[None]]).astype(np.float32))
+    for j in range(nv):
+        if j == nv // 2:
+            continue
+        want = V.synth(cams[0], cams[1], w, h, fmt, st, (j + 1) / (nv + 1))
+        diff = np.abs(got[j].astype(int) - want.astype(int))
+        assert diff.max() <= 1 and np.mean(diff) < 0.01, (j, diff.max(), np.mean(diff))
+
+
+def test_dense_views_modes_through_the_reference_api(torch_cuda):
+    """dense_views(..., mode=) on host Frames: recursive (bit-exact vs the oracle),
+    direct (midpoint bit-exact) and vinet (the CNN path)."""
+    import paper_2112_10603_b200 as fv
+    w, h, fmt = 128, 96, 1
+    cams = synth_rig(w, h, fmt, 2, seed=9)
+    L, R = (fv.frame_from_packed(c, w, h, fmt) for c in cams)
+    rec = np.stack([fv.packed(v) for v in fv.dense_views(L, R, 2)])
+    assert np.array_equal(rec, O.dense_views(cams[0], cams[1], w, h, fmt, 2))
+    dir_ = np.stack([fv.packed(v) for v in fv.dense_views(L, R, 2, mode="direct")])
+    assert np.array_equal(dir_[1], rec[1])
+    vin = fv.dense_views(L, R, 2, mode="vinet")
+    assert len(vin) == 3 and vin[0].width == w
+    with pytest.raises(ValueError):
+        fv.dense_views(L, R, 2, mode="nope")
