@@ -474,6 +474,11 @@ def run_b200(args, cfg, rank, world, local_rank):
         "gpu_launches": gpu_launches,
         "clocks": clk,
     }
+    if not args.no_direct:
+        try:
+            line["direct_t"] = run_direct(cfg, eng, cams, views, clusters, stream, steps=max(3, args.steps // 2))
+        except Exception as exc:
+            line["direct_t"] = {"error": f"{type(exc).__name__}: {exc}"}
     if vps and fmt != 2 and not args.no_encoder:
         try:
             # a second rig frame (another scene) so consecutive P records carry real residuals
@@ -724,6 +729,43 @@ def run_vinet(cfg, dev, steps=10, warmup=3, use_graph=True):
                   "1 level, end-to-end PSNR >= 50 dB (tests/test_gpu_vinet.py)",
         "refine": refine,
     }
+
+
+def run_direct(cfg, eng, cams, views, clusters, stream, steps=10):
+    """Direct-t mode of the SAD path (fvv_rig_views_mode FVV_DENSE_DIRECT): per gap
+    one interpolation (its t = 1/2 view bit-exact with the reference) plus the
+    other views synthesized from its flows and mask, then the cluster frames;
+    the same rig frame as the headline, as one CUDA graph."""
+    import torch
+    from paper_2112_10603_b200.cluster import rig_clusters
+    W, H, fmt, C, S, vps = cfg["W"], cfg["H"], cfg["fmt"], cfg["cams"], cfg["stages"], cfg["vps"]
+    step_views = (C - 1) * ((1 << S) - 1)
+
+    def frame():
+        eng.rig(cams, S, views, mode=1)
+        if vps:
+            rig_clusters(views, W, H, fmt, C, S, vps, out=clusters)
+    with torch.cuda.stream(stream):
+        frame()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            frame()
+        for _ in range(3):
+            g.replay()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(steps):
+            g.replay()
+        b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    return {"path": "SAD flows, direct-t: one interpolation per camera gap (t = 1/2 bit-exact vs interp.py:131-132) "
+                    "+ the other views of the gap synthesized from its flows and mask in one pass, cluster frames",
+            "value": step_views / (ms / 1e3), "unit": "views/s", "ms_per_step": ms, "interpolations_per_step": C - 1,
+            "cuda_graph": True,
+            "parity": "t = 1/2 views bit-exact vs the oracle; other views within 1 level of the fp32 direct-t "
+                      "restatement (oracle/vinet_ref.synth) on the oracle's flows and mask (tests/test_gpu_timed_path.py)"}
 
 
 def run_encoder(cfg, dev, cluster_bufs, stream, ticks=4):
@@ -1001,6 +1043,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-vinet", action="store_true", help="skip the VINet (CNN path) section")
     ap.add_argument("--no-encoder", action="store_true", help="skip the encoder hand-off section")
+    ap.add_argument("--no-direct", action="store_true", help="skip the direct-t SAD-path section")
     ap.add_argument("--shard", default="auto", choices=["auto", "gap", "frame"],
                     help="N>1 partition: gap = one rig frame split by camera gaps (latency; default for "
                          "tiled rigs that fit, cfg3/cfg4), frame = whole rig frames per rank (throughput, cfg5)")

@@ -156,6 +156,15 @@ int fvv_dense_views(fvv_engine* engine, const uint8_t* left, const uint8_t* righ
 int fvv_rig_views(fvv_engine* engine, const uint8_t* cams, int ncams, int stages, uint8_t* views,
                   void* stream);
 
+/* fvv_rig_views with a dense-views mode: FVV_DENSE_RECURSIVE is fvv_rig_views;
+ * FVV_DENSE_DIRECT interpolates every gap once (all gaps in one launch; the
+ * t = 1/2 views are bit-exact) and synthesizes the other views of every gap
+ * direct-t from those flows and masks (see fvv_dense_views).  Direct-t needs
+ * max_pairs >= ncams - 1 and fvv_rig_views_scratch(engine, ncams, mode) bytes. */
+size_t fvv_rig_views_scratch(const fvv_engine* engine, int ncams, int mode);
+int fvv_rig_views_mode(fvv_engine* engine, const uint8_t* cams, int ncams, int stages, int mode, uint8_t* views,
+                       void* scratch, size_t scratch_bytes, void* stream);
+
 /* cluster.py:77-89, batched over nframes contiguous frames. */
 int fvv_downscale(const fvv_frame_desc* desc, const uint8_t* frames, int nframes, int factor,
                   uint8_t* out, void* stream);

@@ -21,7 +21,8 @@ EXPORTS = (
     "fvv_last_error", "fvv_build_info", "fvv_frame_bytes", "fvv_validate_params",
     "fvv_engine_workspace_size", "fvv_engine_create", "fvv_engine_destroy",
     "fvv_engine_max_pairs", "fvv_engine_set_tuning", "fvv_interpolate_pairs", "fvv_interp_diagnostics",
-    "fvv_dense_views", "fvv_dense_views_scratch", "fvv_rig_views", "fvv_downscale", "fvv_cluster_width",
+    "fvv_dense_views", "fvv_dense_views_scratch", "fvv_rig_views", "fvv_rig_views_scratch",
+    "fvv_rig_views_mode", "fvv_downscale", "fvv_cluster_width",
     "fvv_assemble_cluster", "fvv_rig_cluster_bytes", "fvv_rig_clusters", "fvv_rig_clusters_shard",
     "fvv_profile_enable", "fvv_profile_read", "fvv_kernel_class_name",
     "fvv_interp_level_diagnostics", "fvv_interp_level_mask_scratch", "fvv_interp_level_mask", "fvv_conv2d_bf16", "fvv_vinet_workspace_size", "fvv_vinet_flow",
@@ -88,6 +89,8 @@ def load():
         "fvv_interp_level_mask": (I, [P, I, I, P, Z, P, P, P]),
         "fvv_dense_views": (I, [P, P, P, I, I, P, P, Z, P]),
         "fvv_dense_views_scratch": (Z, [P, I]),
+        "fvv_rig_views_scratch": (Z, [P, I, I]),
+        "fvv_rig_views_mode": (I, [P, P, I, I, I, P, P, Z, P]),
         "fvv_rig_views": (I, [P, P, I, I, P, P]),
         "fvv_downscale": (I, [pd, P, I, I, P, P]),
         "fvv_cluster_width": (I, [I, I]),

@@ -545,6 +545,65 @@ int fvv_rig_views(fvv_engine* e, const uint8_t* cams, int ncams, int stages, uin
     return run_recursion(e, views, fb, (ncams - 1) * step + 1, stages, st);
 }
 
+size_t fvv_rig_views_scratch(const fvv_engine* e, int ncams, int mode) {
+    if (!e || ncams < 2 || mode == FVV_DENSE_RECURSIVE) return 0;
+    const size_t n = (size_t)e->g.W * e->g.H, np = (size_t)(ncams - 1);
+    return align_up(np * n * 5 * sizeof(float)) + align_up(np * n * sizeof(double)) +
+           np * align_up((size_t)e->g.frame_bytes);
+}
+
+int fvv_rig_views_mode(fvv_engine* e, const uint8_t* cams, int ncams, int stages, int mode, uint8_t* views,
+                       void* scratch, size_t scratch_bytes, void* stream) {
+    if (mode == FVV_DENSE_RECURSIVE) return fvv_rig_views(e, cams, ncams, stages, views, stream);
+    if (!e) return fail(FVV_EINVAL, "null engine");
+    if (mode != FVV_DENSE_DIRECT) return fail(FVV_EINVAL, "mode must be 0 (recursive) or 1 (direct-t)");
+    if (ncams < 2) return fail(FVV_EINVAL, "need at least 2 cameras");
+    if (stages < 1 || stages > 6) return fail(FVV_EINVAL, "stages must be in 1..6");
+    const int npairs = ncams - 1;
+    if (npairs > e->max_pairs || npairs > kVinMaxPairs)
+        return fail(FVV_EINVAL, "direct-t rig needs max_pairs >= ncams - 1 (at most 64)");
+    if (!scratch || scratch_bytes < fvv_rig_views_scratch(e, ncams, mode))
+        return fail(FVV_EINVAL, "direct-t rig needs fvv_rig_views_scratch(engine, ncams, 1) bytes of scratch");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t n = (size_t)e->g.W * e->g.H, fb = (size_t)e->g.frame_bytes;
+    const int step = 1 << stages, nv = step - 1;
+    uint8_t* sp = static_cast<uint8_t*>(scratch);
+    float* state = reinterpret_cast<float*>(sp);  // (npairs, 5, H, W): the layout vin_synth reads
+    double* mask = reinterpret_cast<double*>(sp + align_up((size_t)npairs * n * 5 * sizeof(float)));
+    uint8_t* mids = sp + align_up((size_t)npairs * n * 5 * sizeof(float)) + align_up((size_t)npairs * n * sizeof(double));
+    const size_t sstride = 5 * n;
+    for (int c = 0; c < ncams; c++) {
+        cudaError_t ce = cudaMemcpyAsync(views + (size_t)c * step * fb, cams + (size_t)c * fb, fb,
+                                         cudaMemcpyDeviceToDevice, st);
+        if (ce != cudaSuccess) return cuda_fail(ce, "rig_views (direct-t): camera copy");
+    }
+    // one interpolation per gap, all gaps in one launch: the t = 1/2 views and the masks
+    PairTable pt;
+    for (int c = 0; c < npairs; c++) {
+        pt.left[c] = cams + (size_t)c * fb;
+        pt.right[c] = cams + (size_t)(c + 1) * fb;
+        pt.out[c] = mids + (size_t)c * align_up(fb);
+    }
+    cudaError_t ce = run_interp_stage(e->g, pt, e->slots, e->P, e->rank_of, e->cand_of_rank, npairs, mask,
+                                      e->profiling ? &e->prof : nullptr, st);
+    if (ce != cudaSuccess) return cuda_fail(ce, "rig_views (direct-t): interpolate");
+    e->last = pt;
+    e->last_npairs = npairs;
+    VinPairs pp{};
+    for (int c = 0; c < npairs && ce == cudaSuccess; c++) {
+        pp.left[c] = pt.left[c];
+        pp.right[c] = pt.right[c];
+        ce = run_direct_state(e->g, e->slots, e->P, c, mask + (size_t)c * n, state + (size_t)c * sstride, st);
+    }
+    if (ce != cudaSuccess) return cuda_fail(ce, "rig_views (direct-t): state");
+    ce = vin_synth(pp, npairs, state, e->g.fmt, e->g.W, e->g.H, nv, views + fb, fb, (size_t)step * fb, st);
+    for (int c = 0; c < npairs && ce == cudaSuccess; c++)
+        ce = cudaMemcpyAsync(views + ((size_t)c * step + step / 2) * fb, mids + (size_t)c * align_up(fb), fb,
+                             cudaMemcpyDeviceToDevice, st);
+    if (ce != cudaSuccess) return cuda_fail(ce, "rig_views (direct-t): synthesis");
+    return FVV_OK;
+}
+
 int fvv_downscale(const fvv_frame_desc* d, const uint8_t* frames, int nframes, int factor,
                   uint8_t* out, void* stream) {
     int rc = check_desc(d);

@@ -1610,7 +1610,7 @@ __global__ void __launch_bounds__(kCR) k_scan_carry(Geometry g, const uint8_t* _
 template <int FMT>
 __global__ void __launch_bounds__(128, FVV_MINB_BLEND) k_blend(Geometry g, PairTable pt, const uint8_t* __restrict__ ws,
                                                Planes P, int pair_base, bool write_frame,
-                                               double* mask_out /* nullable: one pair */) {
+                                               double* mask_out /* nullable: (launch pairs, H, W) */) {
     // thread = one 8-column group of ONE row; a warp holds 16 groups x the 2 rows
     // of a row pair (lanes 0-15: upper row, 16-31: lower row), so the chroma
     // 2x2-mean mask comes from a shuffle and each thread keeps one row's state
@@ -1708,9 +1708,10 @@ __global__ void __launch_bounds__(128, FVV_MINB_BLEND) k_blend(Geometry g, PairT
             }
         }
         if (mask_out && active) {
+            double* mo = mask_out + (size_t)blockIdx.z * W * H;  // this launch's pair
 #pragma unroll
             for (int j = 0; j < 8; j++)
-                if (j < n) mask_out[ro + x0 + j] = mrow[j];
+                if (j < n) mo[ro + x0 + j] = mrow[j];
         }
         if (FMT == FVV_YUV420) {
 #pragma unroll

@@ -248,16 +248,25 @@ class Interpolator:
                                            self._stream()))
         return views
 
-    def rig(self, cams, stages: int, views=None):
-        """server/pipeline.py:254-271: cams (C, fb) -> all global views (T, fb)."""
+    def rig(self, cams, stages: int, views=None, mode: int = 0):
+        """server/pipeline.py:254-271: cams (C, fb) -> all global views (T, fb).
+        mode 1: direct-t gaps (fvv_rig_views_mode, see dense())."""
         import torch
         self._check_frames(cams)
         C = cams.shape[0]
         total = (C - 1) * (1 << stages) + 1
         if views is None:
             views = torch.empty((total, self.frame_bytes), dtype=torch.uint8, device=cams.device)
-        _lib.check(self._L.fvv_rig_views(self._h, ctypes.c_void_p(cams.data_ptr()), C, stages,
-                                         ctypes.c_void_p(views.data_ptr()), self._stream()))
+        if mode == 0:
+            _lib.check(self._L.fvv_rig_views(self._h, ctypes.c_void_p(cams.data_ptr()), C, stages,
+                                             ctypes.c_void_p(views.data_ptr()), self._stream()))
+            return views
+        nb = int(self._L.fvv_rig_views_scratch(self._h, C, int(mode)))
+        if getattr(self, "_rig_scratch", None) is None or self._rig_scratch.numel() < nb:
+            self._rig_scratch = torch.empty(max(1, nb), dtype=torch.uint8, device=cams.device)
+        _lib.check(self._L.fvv_rig_views_mode(self._h, ctypes.c_void_p(cams.data_ptr()), C, stages, int(mode),
+                                              ctypes.c_void_p(views.data_ptr()),
+                                              ctypes.c_void_p(self._rig_scratch.data_ptr()), nb, self._stream()))
         return views
 
 

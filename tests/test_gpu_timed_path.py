@@ -330,3 +330,21 @@ def test_dense_views_modes_through_the_reference_api(torch_cuda):
     assert len(vin) == 3 and vin[0].width == w
     with pytest.raises(ValueError):
         fv.dense_views(L, R, 2, mode="nope")
+
+
+@pytest.mark.parametrize("w,h,fmt,C,stages", [(200, 124, 1, 4, 3), (1920, 1080, 1, 3, 4)])
+def test_direct_t_rig_equals_per_gap_direct_dense(torch_cuda, w, h, fmt, C, stages):
+    """fvv_rig_views_mode(DIRECT): all gaps in one launch == fvv_dense_views(DIRECT)
+    gap by gap (anchors, bit-exact midpoints, synthesized views), byte for byte."""
+    import torch
+    from paper_2112_10603_b200.interp import Interpolator
+    cams = torch.from_numpy(synth_rig(w, h, fmt, C, seed=C + stages)).cuda()
+    eng = Interpolator(w, h, fmt, max_pairs=C - 1)
+    views = eng.rig(cams, stages, mode=1).cpu().numpy()
+    one = Interpolator(w, h, fmt, max_pairs=1)
+    step = 1 << stages
+    for c in range(C - 1):
+        d = one.dense(cams[c], cams[c + 1], stages, mode=1).cpu().numpy()
+        assert np.array_equal(views[c * step + 1:(c + 1) * step], d), c
+        assert np.array_equal(views[c * step], cams[c].cpu().numpy())
+    assert np.array_equal(views[-1], cams[-1].cpu().numpy())
