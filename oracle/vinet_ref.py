@@ -62,8 +62,8 @@ def pool2(x: torch.Tensor) -> torch.Tensor:
     return ((a + b) + (c + d)) * 0.25
 
 
-def _taps(n_out: int, n_in: int):
-    s = (torch.arange(n_out, dtype=torch.float32) + 0.5) * 0.5 - 0.5
+def _taps(n_out: int, n_in: int, device=None):
+    s = (torch.arange(n_out, dtype=torch.float32, device=device) + 0.5) * 0.5 - 0.5
     s = s.clamp(0.0, float(n_in - 1))
     i0 = torch.clamp(torch.floor(s), max=max(n_in - 2, 0)).long()
     i1 = torch.clamp(i0 + 1, max=n_in - 1)
@@ -73,8 +73,8 @@ def _taps(n_out: int, n_in: int):
 def up2(x: torch.Tensor) -> torch.Tensor:
     """(..., h, w) -> (..., 2h, 2w) bilinear, align_corners=False."""
     h, w = x.shape[-2:]
-    y0, y1, fy = _taps(2 * h, h)
-    x0, x1, fx = _taps(2 * w, w)
+    y0, y1, fy = _taps(2 * h, h, x.device)
+    x0, x1, fx = _taps(2 * w, w, x.device)
     top = x[..., y0, :]
     bot = x[..., y1, :]
     rows = (1.0 - fy)[:, None] * top + fy[:, None] * bot
@@ -85,8 +85,8 @@ def up2(x: torch.Tensor) -> torch.Tensor:
 def warp(img: torch.Tensor, fx: torch.Tensor, fy: torch.Tensor) -> torch.Tensor:
     """img (..., H, W), flow (H, W): backward bilinear with clamped coordinates."""
     H, W = img.shape[-2:]
-    ys = torch.arange(H, dtype=torch.float32)[:, None]
-    xs = torch.arange(W, dtype=torch.float32)[None, :]
+    ys = torch.arange(H, dtype=torch.float32, device=img.device)[:, None]
+    xs = torch.arange(W, dtype=torch.float32, device=img.device)[None, :]
     sx = (xs + fx).clamp(0.0, float(W - 1))
     sy = (ys + fy).clamp(0.0, float(H - 1))
     x0 = torch.clamp(torch.floor(sx), max=W - 2).long()
@@ -124,16 +124,20 @@ def canvas(w: int, h: int):
 
 def pad_canvas(x: torch.Tensor, w: int, h: int) -> torch.Tensor:
     wp, hp = canvas(w, h)
-    ys = torch.clamp(torch.arange(hp), max=h - 1)
-    xs = torch.clamp(torch.arange(wp), max=w - 1)
+    ys = torch.clamp(torch.arange(hp, device=x.device), max=h - 1)
+    xs = torch.clamp(torch.arange(wp, device=x.device), max=w - 1)
     return x[..., ys, :][..., xs]
 
 
 @torch.no_grad()
-def flows(left: np.ndarray, right: np.ndarray, w: int, h: int, fmt: int, params):
-    """VINet on one pair -> (5, H, W) float32: F_l (2), F_r (2), mask logit (1) at full resolution."""
-    il = [pad_canvas(net_image(left, w, h, fmt), w, h)]
-    ir = [pad_canvas(net_image(right, w, h, fmt), w, h)]
+def flows(left: np.ndarray, right: np.ndarray, w: int, h: int, fmt: int, params, device=None):
+    """VINet on one pair -> (5, H, W) float32: F_l (2), F_r (2), mask logit (1) at full resolution.
+    device: where the fp32 oracle runs (CPU by default; a CUDA device only speeds the checker up,
+    with TF32 disabled by the caller)."""
+    if device is not None:
+        params = [[(w_.to(device), b_.to(device)) for w_, b_ in blk] for blk in params]
+    il = [pad_canvas(net_image(left, w, h, fmt).to(device or "cpu"), w, h)]
+    ir = [pad_canvas(net_image(right, w, h, fmt).to(device or "cpu"), w, h)]
     for _ in range(2):
         il.insert(0, pool2(il[0]))
         ir.insert(0, pool2(ir[0]))
@@ -151,7 +155,7 @@ def flows(left: np.ndarray, right: np.ndarray, w: int, h: int, fmt: int, params)
             state = st
         res = block_forward(x[None], params[i])[0]
         state = res if state is None else state + res
-    return state[:, :h, :w].contiguous()
+    return state[:, :h, :w].contiguous().cpu()
 
 
 def _synth_plane(pl: torch.Tensor, pr: torch.Tensor, fl, fr, wgt, t: float) -> torch.Tensor:

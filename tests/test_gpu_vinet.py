@@ -142,3 +142,27 @@ def test_vinet_rig_clusters_fused_tiling(torch_cuda, params, w, h, fmt, C, S, vp
     assert sizes == ref_sizes
     assert torch.equal(views, ref_views)
     assert torch.equal(cl, ref_cl)
+
+
+def test_vinet_flows_1080p_match_fp32_oracle(torch_cuda, params):
+    """VINet at the BASELINE geometry (1920x1080 YUV420, canvas 1920x1088) vs the fp32
+    oracle (run on the GPU with TF32 off, only to keep the checker fast)."""
+    torch = torch_cuda
+    from bench import synth_rig
+    from paper_2112_10603_b200.vinet import VINet
+    w, h, fmt = 1920, 1080, 1
+    cams = synth_rig(w, h, fmt, 2, seed=1080)
+    old = (torch.backends.cudnn.allow_tf32, torch.backends.cuda.matmul.allow_tf32)
+    torch.backends.cudnn.allow_tf32 = torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        ref = V.flows(cams[0], cams[1], w, h, fmt, params, device="cuda").numpy()
+    finally:
+        torch.backends.cudnn.allow_tf32, torch.backends.cuda.matmul.allow_tf32 = old
+    net = VINet(w, h, fmt, params=params, max_pairs=1)
+    got = net.flows(torch.from_numpy(cams[:1]).cuda(), torch.from_numpy(cams[1:]).cuda())[0].cpu().numpy()
+    err = np.abs(got - ref)
+    scale = np.abs(ref).max()
+    assert err.max() <= 0.03 * scale + 1e-3, (err.max(), scale)
+    # the 64-aligned canvas edge (rows 1024..1079, the last column tile) is no worse than the interior
+    assert err[:, 1024:, :].max() <= 0.03 * scale + 1e-3
+    assert float(np.mean(err)) <= 0.003 * scale + 1e-4
