@@ -67,8 +67,11 @@ const char* fvv_build_info(void);
 /* frame.py:22-30 plane_shapes -> total bytes of a packed frame */
 size_t fvv_frame_bytes(const fvv_frame_desc* desc);
 
-/* interp.py:32-36 validation (ValueError) plus this path's limits
- * (FVV_EUNSUPPORTED): block sizes in {2,4,8}, max_span <= 120. */
+/* interp.py:32-36 validation (ValueError); mask_epsilon <= 0 is FVV_EUNSUPPORTED.
+ * Every block size >= 2 and radius >= 1 the reference accepts is supported:
+ * power-of-two blocks with max_span <= 120 run the exact fixed-point fast path
+ * (DESIGN.md sec. 3), anything else the literal path (literal_kernels.cu, the
+ * reference's f64/f32 arithmetic replayed one pair at a time; same results). */
 int fvv_validate_params(const fvv_interp_params* params);
 
 /* Engine = geometry + config + a caller-owned device workspace able to run

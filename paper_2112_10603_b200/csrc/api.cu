@@ -14,6 +14,7 @@
 #include "vinet.h"
 #include "refine.h"
 #include "encode.h"
+#include "literal.h"
 
 namespace fvv {
 extern thread_local int g_failed_class;
@@ -29,7 +30,7 @@ size_t level_mask_scratch_bytes(const Geometry& g, int level);
 cudaError_t run_direct_state(const Geometry& g, uint8_t* ws, const Planes& P, int pair, const double* mask,
                              float* state, cudaStream_t st);
 cudaError_t run_level_mask(const Geometry& g, uint8_t* ws, const Planes& P, int pair, int level, void* scratch,
-                           double* mask, double* blend, cudaStream_t st);
+                           double* mask, double* blend, const LDiagSrc& src, cudaStream_t st);
 cudaError_t launch_downscale(int W, int H, int fmt, const uint8_t* frames, int n, int f,
                              uint8_t* out, cudaStream_t st);
 cudaError_t launch_assemble(int W, int H, int fmt, const uint8_t* anchor,
@@ -187,6 +188,9 @@ Layout make_layout(const Geometry& g) {
 
 struct fvv_engine {
     Geometry g;
+    bool literal = false;  // outside the fixed-point domain: literal_kernels.cu, one pair at a time
+    LitLayout lit{};
+    int block[3], radius[3];
     Layout lay;
     Planes P;  // plane offsets relative to the first pair slot
     uint8_t* ws;
@@ -230,18 +234,19 @@ int fvv_validate_params(const fvv_interp_params* p) {
     int mb = std::min(std::min(p->block_size[0], p->block_size[1]), p->block_size[2]);
     int mr = std::min(std::min(p->search_radius[0], p->search_radius[1]), p->search_radius[2]);
     if (mb < 2 || mr < 1) return fail(FVV_EINVAL, "degenerate block size or search radius");
-    for (int s = 0; s < 3; s++)
-        if (!pow2_block(p->block_size[s]))
-            return fail(FVV_EUNSUPPORTED,
-                        "block sizes must be 2, 4 or 8 on the B200 path (bit-exact fixed-point "
-                        "argument, DESIGN.md sec. 3)");
-    const int span = 4 * p->search_radius[0] + 2 * p->search_radius[1] + p->search_radius[2];
-    if (span > 120)
-        return fail(FVV_EUNSUPPORTED, "max_span " + std::to_string(span) +
-                                          " > 120 is outside the B200 path's exactness range");
     if (!(p->mask_epsilon > 0.0))
         return fail(FVV_EUNSUPPORTED, "mask_epsilon must be positive on the B200 path");
     return FVV_OK;
+}
+
+// The fixed-point fast path's domain: power-of-two blocks make
+// every flow value a dyadic rational; max_span <= 120 keeps the 32-bit
+// coordinates.  Anything else the reference accepts runs the literal path
+// (literal_kernels.cu), same results, no speed claim.
+static bool fast_domain(const fvv_interp_params* p) {
+    for (int s = 0; s < 3; s++)
+        if (!pow2_block(p->block_size[s])) return false;
+    return 4 * p->search_radius[0] + 2 * p->search_radius[1] + p->search_radius[2] <= 120;
 }
 
 static int check_interp_desc(const fvv_frame_desc* d) {
@@ -261,6 +266,7 @@ size_t fvv_engine_workspace_size(const fvv_frame_desc* d, const fvv_interp_param
     Geometry g;
     make_geometry(d, p, &g);
     Layout lay = make_layout(g);
+    if (!fast_domain(p)) return lay.header + lit_layout(d->width, d->height, d->format, p->block_size).bytes;
     return lay.header + lay.P.stride * (size_t)max_pairs;
 }
 
@@ -282,6 +288,9 @@ int fvv_engine_create(const fvv_frame_desc* d, const fvv_interp_params* p, int m
     e->slots = e->ws + e->lay.header;
     e->max_pairs = max_pairs;
     e->last_npairs = 0;
+    e->literal = !fast_domain(p);
+    for (int s = 0; s < 3; s++) { e->block[s] = p->block_size[s]; e->radius[s] = p->search_radius[s]; }
+    if (e->literal) e->lit = lit_layout(d->width, d->height, d->format, p->block_size);
     for (int s = 0; s < 3; s++) {
         std::vector<int16_t> ro, cr;
         candidate_tables(e->g.lv[s].r, ro, cr);
@@ -318,6 +327,20 @@ int fvv_engine_set_tuning(fvv_engine* e, int key, int value) {
 
 static int run_pairs(fvv_engine* e, const uint8_t* const* L, const uint8_t* const* R,
                      uint8_t* const* O, int npairs, cudaStream_t st) {
+    if (e->literal) {
+        for (int i = 0; i < npairs; i++) {
+            cudaError_t ce = lit_interpolate(e->lit, e->slots, e->g.W, e->g.H, e->g.fmt, e->block, e->radius,
+                                             e->cand_of_rank, e->g.eps, L[i], R[i], O[i], st);
+            if (ce != cudaSuccess) return cuda_fail(ce, "interpolate (literal path)");
+        }
+        if (npairs > 0) {
+            e->last.left[0] = L[npairs - 1];
+            e->last.right[0] = R[npairs - 1];
+            e->last.out[0] = O[npairs - 1];
+            e->last_npairs = npairs;
+        }
+        return FVV_OK;
+    }
     for (int b = 0; b < npairs; b += std::min(e->max_pairs, kMaxPairsPerLaunch)) {
         const int n = std::min(std::min(e->max_pairs, kMaxPairsPerLaunch), npairs - b);
         PairTable pt;
@@ -392,11 +415,30 @@ int fvv_interpolate_pairs(fvv_engine* e, const uint8_t* const* left, const uint8
     return run_pairs(e, left, right, out, npairs, static_cast<cudaStream_t>(stream));
 }
 
+static int lit_pair_check(const fvv_engine* e, int pair) {
+    if (pair != e->last_npairs - 1)
+        return fail(FVV_EINVAL, "the literal path (non power-of-two blocks / max_span > 120) keeps the diagnostics "
+                                "of the last pair of a batch only");
+    return FVV_OK;
+}
+
 int fvv_interp_diagnostics(fvv_engine* e, int pair, float* flow_lr, float* flow_rl, double* mask,
                            void* stream) {
     if (!e) return fail(FVV_EINVAL, "null engine");
     if (pair < 0 || pair >= e->last_npairs)
         return fail(FVV_EINVAL, "no such pair in the most recent batch");
+    if (e->literal) {
+        int rc = lit_pair_check(e, pair);
+        if (rc) return rc;
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const size_t n = (size_t)e->g.W * e->g.H;
+        cudaError_t ce = cudaSuccess;
+        if (flow_lr) ce = cudaMemcpyAsync(flow_lr, e->slots + e->lit.flow[2][0], n * 8, cudaMemcpyDeviceToDevice, st);
+        if (ce == cudaSuccess && flow_rl)
+            ce = cudaMemcpyAsync(flow_rl, e->slots + e->lit.flow[2][1], n * 8, cudaMemcpyDeviceToDevice, st);
+        if (ce == cudaSuccess && mask) ce = cudaMemcpyAsync(mask, e->slots + e->lit.mask, n * 8, cudaMemcpyDeviceToDevice, st);
+        return ce == cudaSuccess ? FVV_OK : cuda_fail(ce, "diagnostics (literal path)");
+    }
     cudaError_t ce = run_diag(e->g, e->last, e->slots, e->P, pair, flow_lr, flow_rl, mask,
                               static_cast<cudaStream_t>(stream));
     if (ce != cudaSuccess) return cuda_fail(ce, "diagnostics");
@@ -409,6 +451,20 @@ int fvv_interp_level_diagnostics(fvv_engine* e, int pair, int level, float* flow
     if (pair < 0 || pair >= e->last_npairs)
         return fail(FVV_EINVAL, "no such pair in the most recent batch");
     if (level < 0 || level > 2) return fail(FVV_EINVAL, "level must be 0, 1 or 2");
+    if (e->literal) {
+        int rc = lit_pair_check(e, pair);
+        if (rc) return rc;
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const Level& L = e->g.lv[level];
+        const size_t n = (size_t)L.w * L.h;
+        cudaError_t ce = cudaSuccess;
+        if (flow_lr) ce = cudaMemcpyAsync(flow_lr, e->slots + e->lit.flow[level][0], n * 8, cudaMemcpyDeviceToDevice, st);
+        if (ce == cudaSuccess && flow_rl)
+            ce = cudaMemcpyAsync(flow_rl, e->slots + e->lit.flow[level][1], n * 8, cudaMemcpyDeviceToDevice, st);
+        if (ce == cudaSuccess && err_lr) ce = lit_level_err(e->lit, e->slots, e->g.W, e->g.H, e->block, level, 0, err_lr, st);
+        if (ce == cudaSuccess && err_rl) ce = lit_level_err(e->lit, e->slots, e->g.W, e->g.H, e->block, level, 1, err_rl, st);
+        return ce == cudaSuccess ? FVV_OK : cuda_fail(ce, "level diagnostics (literal path)");
+    }
     cudaError_t ce = run_level_diag(e->g, e->slots, e->P, pair, level, flow_lr, flow_rl, err_lr, err_rl,
                                     static_cast<cudaStream_t>(stream));
     if (ce != cudaSuccess) return cuda_fail(ce, "level diagnostics");
@@ -427,8 +483,17 @@ int fvv_interp_level_mask(fvv_engine* e, int pair, int level, void* scratch, siz
     if (level < 0 || level > 1) return fail(FVV_EINVAL, "coarse-scale masks exist for levels 0 and 1");
     if (!scratch || scratch_bytes < level_mask_scratch_bytes(e->g, level) || !mask || !blend_luma)
         return fail(FVV_EINVAL, "scratch too small or null output");
-    cudaError_t ce = run_level_mask(e->g, e->slots, e->P, pair, level, scratch, mask, blend_luma,
-                                    static_cast<cudaStream_t>(stream));
+    LDiagSrc src{};
+    if (e->literal) {
+        int rc = lit_pair_check(e, pair);
+        if (rc) return rc;
+        for (int side = 0; side < 2; side++) {
+            src.lum[side] = reinterpret_cast<const float*>(e->slots + e->lit.lum[level][side]);
+            src.flow[side] = reinterpret_cast<const float2*>(e->slots + e->lit.flow[level][side]);
+        }
+    }
+    cudaError_t ce = run_level_mask(e->g, e->slots, e->P, e->literal ? 0 : pair, level, scratch, mask, blend_luma,
+                                    src, static_cast<cudaStream_t>(stream));
     if (ce != cudaSuccess) return cuda_fail(ce, "level mask diagnostics");
     return FVV_OK;
 }
@@ -468,6 +533,7 @@ size_t fvv_dense_views_scratch(const fvv_engine* e, int mode) {
 // w_t = (1-t) M / ((1-t) M + t (1-M)); fp32, oracle vinet_ref.synth)
 static int dense_direct(fvv_engine* e, const uint8_t* left, const uint8_t* right, int stages, uint8_t* views,
                         void* scratch, size_t scratch_bytes, cudaStream_t st) {
+    if (e->literal) return fail(FVV_EUNSUPPORTED, "direct-t runs on the fixed-point path (power-of-two blocks)");
     if (!scratch || scratch_bytes < fvv_dense_views_scratch(e, FVV_DENSE_DIRECT))
         return fail(FVV_EINVAL, "direct-t needs fvv_dense_views_scratch(engine, 1) bytes of scratch");
     const size_t n = (size_t)e->g.W * e->g.H;
@@ -557,6 +623,7 @@ int fvv_rig_views_mode(fvv_engine* e, const uint8_t* cams, int ncams, int stages
     if (mode == FVV_DENSE_RECURSIVE) return fvv_rig_views(e, cams, ncams, stages, views, stream);
     if (!e) return fail(FVV_EINVAL, "null engine");
     if (mode != FVV_DENSE_DIRECT) return fail(FVV_EINVAL, "mode must be 0 (recursive) or 1 (direct-t)");
+    if (e->literal) return fail(FVV_EUNSUPPORTED, "direct-t runs on the fixed-point path (power-of-two blocks)");
     if (ncams < 2) return fail(FVV_EINVAL, "need at least 2 cameras");
     if (stages < 1 || stages > 6) return fail(FVV_EINVAL, "stages must be in 1..6");
     const int npairs = ncams - 1;

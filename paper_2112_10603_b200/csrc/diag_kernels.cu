@@ -23,21 +23,24 @@ struct LDiag {  // scratch planes (n = level pixels)
 };
 
 __device__ __forceinline__ double level_luma(const Geometry& g, const uint8_t* ws, const Planes& P, int pair,
-                                             int level, int side, int i) {
+                                             int level, int side, int i, const LDiagSrc& src) {
+    if (src.lum[side]) return (double)src.lum[side][i];
     if (level == 0) return (double)((float)cplane<uint16_t>(ws, P, P.s16[side], pair)[i] * 0.0625f);
     return (double)((float)cplane<uint16_t>(ws, P, P.s4[side], pair)[i] * 0.25f);
 }
 
 // the level's flow (f32, exact from the fixed point) times -0.5 (FlowField.scaled, f32)
 __device__ __forceinline__ float2 level_mid_flow(const Geometry& g, const uint8_t* ws, const Planes& P, int pair,
-                                                 int level, int d, int i) {
+                                                 int level, int d, int i, const LDiagSrc& src) {
+    if (src.flow[d]) return make_float2(src.flow[d][i].x * -0.5f, src.flow[d][i].y * -0.5f);
     const int2 v = cplane<int2>(ws, P, level == 0 ? P.flow0[d] : P.flow1[d], pair)[i];
     const float sc = 1.0f / (float)(1 << g.fb[level]);
     return make_float2(((float)v.x * sc) * -0.5f, ((float)v.y * sc) * -0.5f);
 }
 
 // pass 1 (per pixel): warped levels, |wl - wr|, occlusion cue inputs max(0, -div f_m)
-__global__ void k_ldiag_warp(Geometry g, const uint8_t* __restrict__ ws, Planes P, int pair, int level, LDiag s) {
+__global__ void k_ldiag_warp(Geometry g, const uint8_t* __restrict__ ws, Planes P, int pair, int level, LDiag s,
+                             LDiagSrc src) {
     const Level L = g.lv[level];
     const int h = L.h, w = L.w;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -45,7 +48,7 @@ __global__ void k_ldiag_warp(Geometry g, const uint8_t* __restrict__ ws, Planes 
     const int y = i / w, x = i - (i / w) * w;
     double wv[2];
     for (int d = 0; d < 2; d++) {
-        const float2 f = level_mid_flow(g, ws, P, pair, level, d, i);
+        const float2 f = level_mid_flow(g, ws, P, pair, level, d, i, src);
         double sx = (double)x + (double)f.x, sy = (double)y + (double)f.y;
         if (sx < 0.0) sx = 0.0; else if (sx > w - 1) sx = (double)(w - 1);
         if (sy < 0.0) sy = 0.0; else if (sy > h - 1) sy = (double)(h - 1);
@@ -54,12 +57,12 @@ __global__ void k_ldiag_warp(Geometry g, const uint8_t* __restrict__ ws, Planes 
         if (y0 > h - 2) y0 = h > 1 ? h - 2 : 0;
         const double fx = sx - x0, fy = sy - y0;
         const int x1 = w > 1 ? x0 + 1 : x0, y1 = h > 1 ? y0 + 1 : y0;
-        auto src = [&](int yy, int xx) { return level_luma(g, ws, P, pair, level, d, yy * w + xx); };
-        const double top = (1.0 - fx) * src(y0, x0) + fx * src(y0, x1);
-        const double bot = (1.0 - fx) * src(y1, x0) + fx * src(y1, x1);
+        auto sv = [&](int yy, int xx) { return level_luma(g, ws, P, pair, level, d, yy * w + xx, src); };
+        const double top = (1.0 - fx) * sv(y0, x0) + fx * sv(y0, x1);
+        const double bot = (1.0 - fx) * sv(y1, x0) + fx * sv(y1, x1);
         wv[d] = (1.0 - fy) * top + fy * bot;
         // np.gradient (f32, edge order 1) of f_m.x along x and f_m.y along y
-        auto fm = [&](int yy, int xx) { return level_mid_flow(g, ws, P, pair, level, d, yy * w + xx); };
+        auto fm = [&](int yy, int xx) { return level_mid_flow(g, ws, P, pair, level, d, yy * w + xx, src); };
         float gx, gy;
         if (w < 2) gx = 0.0f;
         else if (x == 0) gx = (fm(y, 1).x - fm(y, 0).x) / 1.0f;
@@ -124,7 +127,7 @@ size_t level_mask_scratch_bytes(const Geometry& g, int level) {
 }
 
 cudaError_t run_level_mask(const Geometry& g, uint8_t* ws, const Planes& P, int pair, int level, void* scratch,
-                           double* mask, double* blend, cudaStream_t st) {
+                           double* mask, double* blend, const LDiagSrc& src, cudaStream_t st) {
     const int h = g.lv[level].h, w = g.lv[level].w;
     const size_t n = (size_t)h * w;
     LDiag s;
@@ -132,7 +135,7 @@ cudaError_t run_level_mask(const Geometry& g, uint8_t* ws, const Planes& P, int 
     s.wl = dp; s.wr = dp + n; s.ad = dp + 2 * n; s.tad = dp + 3 * n;
     float* fp = reinterpret_cast<float*>(dp + 4 * n);
     s.ol = fp; s.orr = fp + n; s.tol = fp + 2 * n; s.tor = fp + 3 * n;
-    k_ldiag_warp<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g, ws, P, pair, level, s);
+    k_ldiag_warp<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g, ws, P, pair, level, s, src);
     k_ldiag_cols<<<(w + 63) / 64, 64, 0, st>>>(h, w, s);
     k_ldiag_rows<<<(h + 63) / 64, 64, 0, st>>>(h, w, s, g.eps, g.eps2, mask, blend);
     return cudaGetLastError();

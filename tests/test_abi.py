@@ -52,8 +52,16 @@ def test_validate_params_matches_reference_errors():
     assert b"degenerate" in L.fvv_last_error()
     with pytest.raises(ValueError):
         InterpConfig(block_size=(8, 1, 8))
+    # every block size / radius the reference accepts is valid (non power-of-two blocks and
+    # max_span > 120 run the literal path); only a non-positive epsilon is outside the path
     odd = _lib.params(InterpConfig(block_size=(8, 6, 8)))
-    assert L.fvv_validate_params(ctypes.byref(odd)) == _lib.FVV_EUNSUPPORTED
+    assert L.fvv_validate_params(ctypes.byref(odd)) == 0
+    wide = _lib.params(InterpConfig(search_radius=(30, 4, 2)))
+    assert L.fvv_validate_params(ctypes.byref(wide)) == 0
+    d = _lib.desc(64, 48, 1)
+    assert L.fvv_engine_workspace_size(ctypes.byref(d), ctypes.byref(odd), 4) > 0
+    zero = _lib.params(InterpConfig(mask_epsilon=0.0))
+    assert L.fvv_validate_params(ctypes.byref(zero)) == _lib.FVV_EUNSUPPORTED
 
 
 def test_workspace_size_and_interp_dims():

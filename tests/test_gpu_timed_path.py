@@ -348,3 +348,43 @@ def test_direct_t_rig_equals_per_gap_direct_dense(torch_cuda, w, h, fmt, C, stag
         assert np.array_equal(views[c * step + 1:(c + 1) * step], d), c
         assert np.array_equal(views[c * step], cams[c].cpu().numpy())
     assert np.array_equal(views[-1], cams[-1].cpu().numpy())
+
+
+@pytest.mark.parametrize("cfg,w,h,fmt", [
+    (dict(block_size=(6, 5, 3)), 96, 72, 1),
+    (dict(block_size=(8, 8, 6), search_radius=(12, 4, 3)), 120, 68, 0),
+    (dict(block_size=(3, 3, 3), search_radius=(4, 2, 1), mask_epsilon=0.05), 64, 48, 2),
+    (dict(search_radius=(30, 4, 2)), 128, 96, 1),      # max_span 130 > 120
+    (dict(block_size=(7, 9, 5)), 1920, 1080, 1),       # the literal path at the BASELINE size
+])
+def test_literal_path_for_any_config_vs_oracle(torch_cuda, cfg, w, h, fmt):
+    """InterpConfig values outside the fixed-point domain (interp.py:32-36 accepts any
+    block >= 2, radius >= 1): the literal path, bit-exact vs the oracle -- output
+    planes, final flows and mask, per-level flows / errors / coarse masks."""
+    import paper_2112_10603_b200 as fv
+    c = fv.InterpConfig(**cfg)
+    cams = synth_rig(w, h, fmt, 3, seed=w + fmt)
+    lefts, rights = [cams[0], cams[1]], [cams[1], cams[2]]
+    eng, out = _pairs(torch_cuda, w, h, fmt, lefts, rights, c)
+    kw = dict(block_size=c.block_size, search_radius=c.search_radius, eps=c.mask_epsilon)
+    for i in range(2):
+        ref = O.interpolate(lefts[i], rights[i], w, h, fmt, **kw)
+        assert np.array_equal(out[i], ref), f"pair {i}: {np.count_nonzero(out[i] != ref)} bytes differ"
+    ref, d = O.interpolate(lefts[1], rights[1], w, h, fmt, with_diag=True, **kw)
+    flr, frl, m = (t.cpu().numpy() for t in eng.diagnostics(1))
+    assert np.array_equal(flr, d["flow_lr"]) and np.array_equal(frl, d["flow_rl"]) and np.array_equal(m, d["mask"])
+    if w <= 128:  # reference-API route incl. per-level diagnostics
+        L, R = (fv.frame_from_packed(x, w, h, fmt) for x in (lefts[1], rights[1]))
+        res, diag = fv.interpolate(L, R, c, diagnostics=True)
+        assert np.array_equal(fv.packed(res), ref)
+        pl, pr = O.luma_pyramid(lefts[1], w, h, fmt), O.luma_pyramid(rights[1], w, h, fmt)
+        prev = None
+        for s in range(3):
+            (fl, fr), _, (el, er) = O.estimate_flow_level(pl[s], pr[s], prev, c.search_radius[s], c.block_size[s])
+            sd = diag.scales[s]
+            assert np.array_equal(sd.flow_lr.vectors, fl) and np.array_equal(sd.flow_rl.vectors, fr), s
+            assert np.array_equal(sd.match_error_lr, el) and np.array_equal(sd.match_error_rl, er), s
+            if s < 2:
+                mm, bb = O.level_mask(pl[s], pr[s], fl, fr, c.mask_epsilon)
+                assert np.array_equal(sd.mask, mm) and np.array_equal(sd.blend_luma, bb), s
+            prev = (fl, fr)
