@@ -706,7 +706,7 @@ def run_vinet(cfg, dev, steps=10, warmup=3, use_graph=True):
     dom = vinet_dominant_conv(W, H, npairs, dev)
     flops = vinet_conv_flops(W, H) * npairs
     try:
-        refine = run_refine(cfg, dev, net, cams, flows, steps=max(3, steps // 2), use_graph=use_graph)
+        refine = run_refine(cfg, dev, net, cams, flows, steps=3, use_graph=use_graph)
     except Exception as exc:  # keep the VINet numbers if the refinement stage fails
         refine = {"error": f"{type(exc).__name__}: {exc}"}
     peaks, src = measured_peaks()
@@ -768,7 +768,7 @@ def run_direct(cfg, eng, cams, views, clusters, stream, steps=10):
                       "restatement (oracle/vinet_ref.synth) on the oracle's flows and mask (tests/test_gpu_timed_path.py)"}
 
 
-def run_encoder(cfg, dev, cluster_bufs, stream, ticks=4):
+def run_encoder(cfg, dev, cluster_bufs, stream, ticks=2):
     """The encoder hand-off: FVT1 records of every
     tile of every cluster frame of the rig frame (server/pipeline.py:294-318),
     transform stage on the device (encoder.RigEncoder), DEFLATE on the host
@@ -844,7 +844,7 @@ def run_refine(cfg, dev, net, cams, flows, steps=5, use_graph=True):
     from paper_2112_10603_b200.refine import RefineNet
     W, H, fmt, C, S = cfg["W"], cfg["H"], cfg["fmt"], cfg["cams"], cfg["stages"]
     npairs, nviews = C - 1, (1 << S) - 1
-    ref = RefineNet(W, H, fmt, seed=1, max_views=nviews, device=dev)
+    ref = RefineNet(W, H, fmt, seed=1, max_views=min(nviews, 8), device=dev)
     L, R = cams[:-1].contiguous(), cams[1:].contiguous()
     out = torch.empty((npairs, nviews, ref.frame_bytes), dtype=torch.uint8, device=dev)
 

@@ -40,7 +40,7 @@ def kclass(name):
     m = re.match(r"fvv::(k_warpq|k_flow)<(\d)", s)
     if m:
         return f"{m.group(1)}<{m.group(2)}>"
-    m = re.match(r"fvv::(k_pyramid|k_mask_cols|k_scan_carry|k_blend|k_rig_clusters|k_sd)\b", s)
+    m = re.match(r"fvv::(k_pyramid|k_mask_cols|k_scan_carry|k_blend|k_rig_clusters|k_sd)(?:2)?\b", s)
     return m.group(1) if m else None
 
 
