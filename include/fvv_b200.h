@@ -228,7 +228,9 @@ typedef struct fvv_conv_desc {
     int32_t batch, in_h, in_w, in_cpad;
     int32_t out_h, out_w, out_cstride, out_coff, out_channels;
     int32_t kernel, stride, pad;   /* square kernel; transposed: 4, 2, 1 */
-    int32_t transposed;            /* 1: ConvTranspose2d */
+    int32_t transposed;            /* 1: ConvTranspose2d (4 phase GEMMs); 2: the same as one
+                                      3x3 sub-pixel GEMM, weights [npad(4 out)][9*in_cpad]
+                                      (row = phase*out_channels + c), bias 4*out_channels */
     int32_t relu, out_f32;
     int32_t ntile;                 /* UMMA N tile: 16, 32, 64, 128 or 256 */
 } fvv_conv_desc;

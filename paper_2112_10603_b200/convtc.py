@@ -81,8 +81,10 @@ def pack_convT_subpixel(weight, cpad: int, ntile: int = 32):
 
 def conv2d(x, w_packed, bias, cout: int, kernel: int, stride: int, pad: int, *, transposed: bool = False,
            relu: bool = True, out=None, out_coff: int = 0, out_f32: bool = False, ntile: int | None = None,
-           stream=None):
-    """One conv layer.  x: NHWC bf16 [B][H][W][cpad] (cuda); returns NHWC out."""
+           stream=None, subpixel: bool = False):
+    """One conv layer.  x: NHWC bf16 [B][H][W][cpad] (cuda); returns NHWC out.
+    subpixel (with transposed): the ConvTranspose2d runs as one 3x3 GEMM with 4*cout
+    outputs (weights from pack_convT_subpixel, bias repeated 4 times)."""
     import torch
     L = _lib.require_cuda()
     B, H, W, cpad = x.shape
@@ -90,14 +92,14 @@ def conv2d(x, w_packed, bias, cout: int, kernel: int, stride: int, pad: int, *, 
         Ho, Wo = 2 * H, 2 * W
     else:
         Ho, Wo = (H + 2 * pad - kernel) // stride + 1, (W + 2 * pad - kernel) // stride + 1
-    nt = ntile or ntile_of(cout)
+    nt = ntile or ntile_of(4 * cout if subpixel else cout)
     if out is None:
         out = torch.empty((B, Ho, Wo, cout if out_f32 else cpad_of(cout)),
                           dtype=torch.float32 if out_f32 else torch.bfloat16, device=x.device)
         if not out_f32 and out.shape[-1] != cout:
             out.zero_()
     d = _lib.ConvDesc(B, H, W, cpad, Ho, Wo, out.shape[-1], out_coff, cout, kernel, stride, pad,
-                      int(transposed), int(relu), int(out_f32), nt)
+                      (2 if subpixel else 1) if transposed else 0, int(relu), int(out_f32), nt)
     st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
     _lib.check(L.fvv_conv2d_bf16(ctypes.byref(d), ctypes.c_void_p(x.data_ptr()),
                                  ctypes.c_void_p(w_packed.data_ptr()), ctypes.c_void_p(bias.data_ptr()),

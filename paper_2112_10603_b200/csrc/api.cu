@@ -867,6 +867,26 @@ extern "C" int fvv_conv2d_bf16(const fvv_conv_desc* d, const void* x, const void
         p.omy = p.omx = 1;
         p.oay = p.oax = 0;
         e = conv_tc(x, d->batch, d->in_h, d->in_w, cp, w, npad, 0, nt, bias, out, p, st);
+    } else if (d->transposed == 2) {
+        // ConvTranspose2d(k4 s2 p1) as ONE 3x3 sub-pixel convolution on the input grid: N = 4 x
+        // out_channels (row n = phase * out_channels + c, convtc.pack_convT_subpixel), the epilogue
+        // scatters phase (oy&1, ox&1); every input row is read once for all four phases
+        if (d->kernel != 4 || d->stride != 2 || d->pad != 1)
+            return fail(FVV_EUNSUPPORTED, "transposed convolution: kernel 4, stride 2, pad 1 only");
+        if (d->out_h != 2 * d->in_h || d->out_w != 2 * d->in_w)
+            return fail(FVV_EINVAL, "transposed output must be twice the input size");
+        p.Hg = d->in_h;
+        p.Wg = d->in_w;
+        p.sy = p.sx = 1;
+        p.by0 = p.bx0 = -1;
+        p.ntaps = 9;
+        for (int t = 0; t < 9; t++) { p.tdy[t] = t / 3; p.tdx[t] = t % 3; }
+        p.omy = p.omx = 1;
+        p.oay = p.oax = 0;
+        p.N = 4 * d->out_channels;
+        p.shuffle_c = d->out_channels;
+        const int npad4 = (p.N + nt - 1) / nt * nt;
+        e = conv_tc(x, d->batch, d->in_h, d->in_w, cp, w, npad4, 0, nt, bias, out, p, st);
     } else {
         if (d->kernel != 4 || d->stride != 2 || d->pad != 1)
             return fail(FVV_EUNSUPPORTED, "transposed convolution: kernel 4, stride 2, pad 1 only");

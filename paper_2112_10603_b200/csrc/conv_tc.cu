@@ -120,6 +120,12 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 // one stage holds the RR + 2 input-row segments of one (dx, channel chunk) and the three
 // weight chunks of taps (0..2, dx), and output row r takes rows r + dy with B_dy -- every
 // input row segment is fetched once per tile instead of once per (row, dy) tap.
+#ifndef FVV_CONV_RR_STAGES
+#define FVV_CONV_RR_STAGES 4  // row-reuse stages when they fit (the 108 KB NT32/SW128 stage fits 2)
+#endif
+#ifndef FVV_CONV_RR_MAXN
+#define FVV_CONV_RR_MAXN 64   // row-reuse tiles for 3x3 stride-1 convolutions with ntile <= this
+#endif
 template <int NT, int SW, int RR = 0>
 struct ConvTile {
     static constexpr int MT = RR > 0 ? RR : (NT <= 128 ? 2 : 1);
@@ -130,7 +136,8 @@ struct ConvTile {
     static constexpr int kStageBytes = kARows * kABytes + kBChunks * kBBytes;
     // as many stages as fit the 227 KB opt-in shared memory (1 KB alignment slack + barriers), at most 6
     static constexpr int kFit = (232448 - 1280) / kStageBytes;
-    static constexpr int kStages = RR > 0 ? (kFit >= 2 ? 2 : 1) : (kFit < 6 ? kFit : 6);
+    static constexpr int kStages = RR > 0 ? (kFit < FVV_CONV_RR_STAGES ? (kFit >= 1 ? kFit : 1) : FVV_CONV_RR_STAGES)
+                                          : (kFit < 6 ? kFit : 6);
     static constexpr int kTmemCols = 2 * MT * NT < 32 ? 32 : 2 * MT * NT;  // two accumulator sets
     static constexpr size_t kSmem = 1024 /* alignment slack */ + (size_t)kStages * kStageBytes + 256;
 };
@@ -327,7 +334,24 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                         if (p.act == 1) x = fmaxf(x, 0.0f);
                         v[j] = x;
                     }
-                    if (p.shuffle_c) {
+                    if (p.shuffle_c && !p.out_f32 && (p.shuffle_c & 7) == 0 && (p.ostride & 7) == 0 &&
+                        (p.ocoff & 7) == 0 && (nb % p.shuffle_c) == 0 && nb + CW <= p.N) {
+                        // sub-pixel, bf16: 8 consecutive channels of one phase per 16-byte store
+#pragma unroll
+                        for (int j = 0; j < CW; j += 8) {
+                            const int n = nb + j;
+                            const int ph = n / p.shuffle_c, ch = n - ph * p.shuffle_c;
+                            const size_t o = (((size_t)c.b * p.Hout + 2 * c.gy + (ph >> 1)) * p.Wout + 2 * gx +
+                                              (ph & 1)) * p.ostride + p.ocoff + ch;
+                            uint4 u;
+                            __nv_bfloat162 h0 = __floats2bfloat162_rn(v[j], v[j + 1]);
+                            __nv_bfloat162 h1 = __floats2bfloat162_rn(v[j + 2], v[j + 3]);
+                            __nv_bfloat162 h2 = __floats2bfloat162_rn(v[j + 4], v[j + 5]);
+                            __nv_bfloat162 h3 = __floats2bfloat162_rn(v[j + 6], v[j + 7]);
+                            memcpy(&u.x, &h0, 4); memcpy(&u.y, &h1, 4); memcpy(&u.z, &h2, 4); memcpy(&u.w, &h3, 4);
+                            *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out) + o) = u;
+                        }
+                    } else if (p.shuffle_c) {
                         // sub-pixel (transposed-conv) head: one 3x3 GEMM emits all 4 output phases
 #pragma unroll
                         for (int j = 0; j < CW; j++) {
@@ -336,7 +360,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                                 const int ph = n / p.shuffle_c, ch = n - ph * p.shuffle_c;
                                 const size_t o = (((size_t)c.b * p.Hout + 2 * c.gy + (ph >> 1)) * p.Wout + 2 * gx +
                                                   (ph & 1)) * p.ostride + p.ocoff + ch;
-                                reinterpret_cast<float*>(out)[o] = v[j];
+                                if (p.out_f32) reinterpret_cast<float*>(out)[o] = v[j];
+                                else reinterpret_cast<__nv_bfloat16*>(out)[o] = __float2bfloat16_rn(v[j]);
                             }
                         }
                     } else if (p.out_f32) {
@@ -502,8 +527,21 @@ cudaError_t conv_tc(const void* x, int B, int Hin, int Win, int cpad, const void
     // small-N 3x3 stride-1 convolutions (the VINet head) are A-load bound: row-reuse tiles
     bool std3x3 = p.ntaps == 9 && p.sy == 1 && p.sx == 1 && p.omy == 1 && p.omx == 1;
     for (int t = 0; t < 9 && std3x3; t++) std3x3 = p.tdy[t] == t / 3 && p.tdx[t] == t % 3;
-    if (std3x3 && ntile == 32 && sw == 128 && !getenv_flag_off("FVV_CONV_RR"))
-        return launch_nt_sw<32, 128, 4>(ma, mw, bias, out, p, ntiles, st);
+    if (std3x3 && ntile <= FVV_CONV_RR_MAXN && !getenv_flag_off("FVV_CONV_RR")) {
+        // small-N 3x3 stride-1 layers (the VINet head, RefineNet's narrow full / half resolution
+        // layers) are A-load bound: row-reuse tiles fetch each input row once per (dx, chunk)
+        switch (ntile * 1000 + sw) {
+            case 16032: return launch_nt_sw<16, 32, 4>(ma, mw, bias, out, p, ntiles, st);
+            case 16064: return launch_nt_sw<16, 64, 4>(ma, mw, bias, out, p, ntiles, st);
+            case 16128: return launch_nt_sw<16, 128, 4>(ma, mw, bias, out, p, ntiles, st);
+            case 32032: return launch_nt_sw<32, 32, 4>(ma, mw, bias, out, p, ntiles, st);
+            case 32064: return launch_nt_sw<32, 64, 4>(ma, mw, bias, out, p, ntiles, st);
+            case 32128: return launch_nt_sw<32, 128, 4>(ma, mw, bias, out, p, ntiles, st);
+            case 64064: return launch_nt_sw<64, 64, 4>(ma, mw, bias, out, p, ntiles, st);
+            case 64128: return launch_nt_sw<64, 128, 4>(ma, mw, bias, out, p, ntiles, st);
+            default: break;
+        }
+    }
     switch (sw) {
         case 128: return launch_sw<128>(ntile, ma, mw, bias, out, p, ntiles, st);
         case 64: return launch_sw<64>(ntile, ma, mw, bias, out, p, ntiles, st);

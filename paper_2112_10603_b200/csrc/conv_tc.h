@@ -15,7 +15,7 @@ struct ConvTCParams {
     int omy, omx, oay, oax;                  // output coordinate = g * om + oa
     int Hout, Wout, ostride, ocoff, N;       // output tensor, channel placement, real channels
     int act, out_f32;                        // 1 = ReLU; 1 = fp32 output (else bf16)
-    int shuffle_c;                           // > 0: sub-pixel output (fp32): channel n = phase * shuffle_c + c
+    int shuffle_c;                           // > 0: sub-pixel output (fp32 or bf16): channel n = phase * shuffle_c + c
                                              // lands at (2 gy + phase / 2, 2 gx + phase % 2), channel c
 };
 

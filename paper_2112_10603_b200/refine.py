@@ -25,7 +25,7 @@ from __future__ import annotations
 import ctypes
 
 from . import _lib
-from .convtc import conv2d, cpad_of, ntile_of, pack_conv, pack_convT
+from .convtc import conv2d, cpad_of, ntile_of, pack_conv, pack_convT, pack_convT_subpixel
 from .frame import PixelFormat, frame_nbytes
 from .vinet_params import CONTEXT_CH, CONTEXT_LAYERS, REFINE_LAYERS, make_refine_params
 
@@ -46,6 +46,9 @@ def _sig(L):
     L.fvv_nhwc_copy.argtypes = [P, I, I, P, I, I, LL, P]
     L.fvv_refine_output.restype = I
     L.fvv_refine_output.argtypes = [pd, PP, I, P, I, P, P]
+
+
+SUBPIXEL_MAX_COUT = 32  # decoder layers up to this width run as sub-pixel 3x3 GEMMs (u2, u3)
 
 
 class RefineNet:
@@ -71,10 +74,16 @@ class RefineNet:
                              cout, stride, nt))
         self.unet = []
         for (name, kind, cin, cout), (w, b) in zip(REFINE_LAYERS, params["unet"]):
-            nt = ntile_of(cout)
             wd = w.to(self.device)
-            packed = pack_convT(wd, cpad_of(cin), nt) if kind == "convT" else pack_conv(wd, cpad_of(cin), nt)
-            self.unet.append((packed, b.to(self.device).contiguous(), cout, kind, nt))
+            if kind == "convT" and cout <= SUBPIXEL_MAX_COUT:
+                # narrow decoder layers: one 3x3 sub-pixel GEMM (input read once for all 4 phases)
+                nt = ntile_of(4 * cout)
+                packed, bias, kind = pack_convT_subpixel(wd, cpad_of(cin), nt), b.to(self.device).repeat(4), "convT_sp"
+            else:
+                nt = ntile_of(cout)
+                packed = pack_convT(wd, cpad_of(cin), nt) if kind == "convT" else pack_conv(wd, cpad_of(cin), nt)
+                bias = b.to(self.device)
+            self.unet.append((packed, bias.contiguous(), cout, kind, nt))
         self._bufs = None
 
     # -- buffers ------------------------------------------------------------
@@ -137,6 +146,9 @@ class RefineNet:
 
         def cv(i, x, out, coff=0, relu=True, out_f32=False):
             w, b, cout, kind, nt = u[i]
+            if kind == "convT_sp":
+                return conv2d(x[:B], w, b, cout, 4, 2, 1, transposed=True, subpixel=True, out=out[:B], out_coff=coff,
+                              ntile=nt)
             if kind == "convT":
                 return conv2d(x[:B], w, b, cout, 4, 2, 1, transposed=True, out=out[:B], out_coff=coff, ntile=nt)
             stride = 2 if kind == "conv_s2" else 1
