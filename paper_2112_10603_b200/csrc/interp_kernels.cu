@@ -1704,6 +1704,9 @@ __global__ void __launch_bounds__(kCR) k_scan_carry(Geometry g, const uint8_t* _
 #ifndef FVV_MINB_BLEND
 #define FVV_MINB_BLEND 10
 #endif
+#ifndef FVV_BLEND_HALF
+#define FVV_BLEND_HALF 0  // m = 1/2 shortcut for groups with equal cues: exact, but rare on the bench rig (1.16 -> 1.18 ms), off
+#endif
 template <int FMT>
 __global__ void __launch_bounds__(128, FVV_MINB_BLEND) k_blend(Geometry g, PairTable pt, const uint8_t* __restrict__ ws,
                                                Planes P, int pair_base, bool write_frame,
@@ -1733,19 +1736,6 @@ __global__ void __launch_bounds__(128, FVV_MINB_BLEND) k_blend(Geometry g, PairT
         const int y = 2 * yp + rr;
         const size_t ro = (size_t)y * W;
         const uint16_t* srow = sd + ro;
-        int s[11];  // sd[clamp(x0 - 2 + j)]
-        if ((W & 7) == 0 && x0 >= 2 && x0 + 8 < W) {
-            // interior: sd[x0-2 .. x0-1] (4-byte aligned), sd[x0 .. x0+7] (16-byte), sd[x0+8]
-            const uint32_t a = *reinterpret_cast<const uint32_t*>(srow + x0 - 2);
-            const uint4 b = *reinterpret_cast<const uint4*>(srow + x0);
-            s[0] = a & 0xFFFF; s[1] = a >> 16;
-            s[2] = b.x & 0xFFFF; s[3] = b.x >> 16; s[4] = b.y & 0xFFFF; s[5] = b.y >> 16;
-            s[6] = b.z & 0xFFFF; s[7] = b.z >> 16; s[8] = b.w & 0xFFFF; s[9] = b.w >> 16;
-            s[10] = srow[x0 + 8];
-        } else {
-#pragma unroll
-            for (int j = 0; j < 11; j++) s[j] = srow[clampi(x0 - 2 + j, 0, W - 1)];
-        }
         float vl[8], vr[8];
         uint8_t al[8], ar[8];
         if (n == 8) {
@@ -1775,13 +1765,37 @@ __global__ void __launch_bounds__(128, FVV_MINB_BLEND) k_blend(Geometry g, PairT
                 if (FMT != FVV_RGB8) { al[j] = wl[ro + xx]; ar[j] = wr[ro + xx]; }
             }
         }
-        // replay the running sum inside the group: tmp(x0) from the carry, then x0+1 ..
-        double tmp = carry[(size_t)y * ng + gx];
         double mrow[8];
+        // equal occlusion cues (in smooth flow both are 0): e_l == e_r, so den = (2 e_r) + 2 eps =
+        // 2 (e_r + eps) exactly and m = 1/2 whatever the smoothed difference is (warp.py:63) --
+        // the running-sum replay, its sd / carry loads and the mask division are skipped
+        bool half = FVV_BLEND_HALF != 0;
 #pragma unroll
-        for (int j = 0; j < 8; j++) {
-            if (j > 0) tmp = __dadd_rn(tmp, __dsub_rn(d0_of(s[j + 3]), d0_of(s[j])));
-            mrow[j] = j < n ? mask_of(tmp, vl[j], vr[j], g) : 0.0;
+        for (int j = 0; j < 8; j++) half = half && (j >= n || vl[j] == vr[j]);
+        if (half) {
+#pragma unroll
+            for (int j = 0; j < 8; j++) mrow[j] = j < n ? 0.5 : 0.0;
+        } else {
+            int s[11];  // sd[clamp(x0 - 2 + j)]
+            if ((W & 7) == 0 && x0 >= 2 && x0 + 8 < W) {
+                // interior: sd[x0-2 .. x0-1] (4-byte aligned), sd[x0 .. x0+7] (16-byte), sd[x0+8]
+                const uint32_t a = *reinterpret_cast<const uint32_t*>(srow + x0 - 2);
+                const uint4 b = *reinterpret_cast<const uint4*>(srow + x0);
+                s[0] = a & 0xFFFF; s[1] = a >> 16;
+                s[2] = b.x & 0xFFFF; s[3] = b.x >> 16; s[4] = b.y & 0xFFFF; s[5] = b.y >> 16;
+                s[6] = b.z & 0xFFFF; s[7] = b.z >> 16; s[8] = b.w & 0xFFFF; s[9] = b.w >> 16;
+                s[10] = srow[x0 + 8];
+            } else {
+#pragma unroll
+                for (int j = 0; j < 11; j++) s[j] = srow[clampi(x0 - 2 + j, 0, W - 1)];
+            }
+            // replay the running sum inside the group: tmp(x0) from the carry, then x0+1 ..
+            double tmp = carry[(size_t)y * ng + gx];
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                if (j > 0) tmp = __dadd_rn(tmp, __dsub_rn(d0_of(s[j + 3]), d0_of(s[j])));
+                mrow[j] = j < n ? mask_of(tmp, vl[j], vr[j], g) : 0.0;
+            }
         }
         if (write_frame && active) {
             if (FMT == FVV_RGB8) {
