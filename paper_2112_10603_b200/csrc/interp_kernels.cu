@@ -1104,6 +1104,15 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
 #ifndef FVV_MASK2_HB_CACHE
 #define FVV_MASK2_HB_CACHE 1
 #endif
+#ifndef FVV_MASK2_L1PF
+#define FVV_MASK2_L1PF 4  // prefetch.global.L1 of the luma rows 4 rows ahead: r2 sweep 3.83 -> 3.70 ms (2: 3.70, 8: 3.71)
+#endif
+#ifndef FVV_MASK2_L1PF_C
+#define FVV_MASK2_L1PF_C 0  // also the chroma rows
+#endif
+#ifndef FVV_MASK2_L2PF
+#define FVV_MASK2_L2PF 0  // > 0: prefetch.global.L2 of the luma rows this many rows ahead
+#endif
 #ifndef FVV_MASK2_PF
 #define FVV_MASK2_PF 0  // luma taps loaded one row ahead: r2 sweep 3.79 -> 3.94 ms (128 regs, spills), off
 #endif
@@ -1374,6 +1383,33 @@ __global__ void __launch_bounds__(kM2Warps * 32, FVV_MINB_MASK2) k_mask_cols2(Ge
                 gxc[d][c] = gmul[c] * (r[c] - l[c]);
             }
         }
+#if FVV_MASK2_L1PF
+        // pull the luma rows the walker reaches FVV_MASK2_L1PF rows from now into L1 (the
+        // gathers' long-scoreboard stalls are mostly first touches of a row's lines)
+        {
+            const int yq = yy + FVV_MASK2_L1PF;
+#pragma unroll
+            for (int d = 0; d < 2; d++) {
+                const int sy = min(max(yq + (Fc[d][0].y >> mb), 0), H - 1);
+                const int sx = min(max(xcl[0] + (Fc[d][0].x >> mb), 0), W - 1);
+                asm volatile("prefetch.global.L1 [%0];\n" ::"l"((d ? frR : frL) + (unsigned)(sy * W + sx)));
+#if FVV_MASK2_L2PF
+                const int sy2 = min(max(yy + FVV_MASK2_L2PF + (Fc[d][0].y >> mb), 0), H - 1);
+                asm volatile("prefetch.global.L2 [%0];\n" ::"l"((d ? frR : frL) + (unsigned)(sy2 * W + sx)));
+#endif
+#if FVV_MASK2_L1PF_C
+                if (FMT == FVV_YUV420 && (yy & 1)) {  // the chroma rows of the same 2x2 blocks
+                    const int cw = g.cw, chh = g.ch;
+                    const int cy = min(max((yq >> 1) + (Fc[d][0].y >> (mb + 1)), 0), chh - 1);
+                    const int cx = min(max((xa >> 1) + (Fc[d][0].x >> (mb + 1)), 0), cw - 1);
+                    const uint8_t* cp = (d ? frR : frL) + (size_t)W * H + (unsigned)(cy * cw + cx);
+                    asm volatile("prefetch.global.L1 [%0];\n" ::"l"(cp));
+                    asm volatile("prefetch.global.L1 [%0];\n" ::"l"(cp + (size_t)cw * chh));
+                }
+#endif
+            }
+        }
+#endif
         // ---- luma warps at yy, d = |wl - wr| ----
         int wl[2], wr[2];
 #pragma unroll
