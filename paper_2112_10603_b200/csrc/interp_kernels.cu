@@ -709,6 +709,9 @@ __global__ void __launch_bounds__(256) k_flow(Geometry g, uint8_t* __restrict__ 
 // units 1/4 (s4), level-2 samples integral (luma).
 // ---------------------------------------------------------------------------
 constexpr int kQH = 64, kQW = 64;  // 16 pixels per thread amortise the tile setup
+#ifndef FVV_WARPQ_L1PF
+#define FVV_WARPQ_L1PF 0  // > 0: L1 prefetch of the luma row this many iterations ahead (r2 sweep 1/2/4: no change), off
+#endif
 template <int LEVEL>
 __global__ void __launch_bounds__(256) k_warpq(Geometry g, PairTable pt, uint8_t* __restrict__ ws,
                                                Planes P) {
@@ -767,6 +770,11 @@ __global__ void __launch_bounds__(256) k_warpq(Geometry g, PairTable pt, uint8_t
                 a = p0[0]; b = p0[1]; c = p0[w]; e = p0[w + 1];
             } else {
                 const uint8_t* p0 = yp + (unsigned)off;
+#if FVV_WARPQ_L1PF
+                // this thread's row FVV_WARPQ_L1PF iterations ahead (4 tile rows per iteration)
+                if (ty + 4 * FVV_WARPQ_L1PF < kQH)
+                    asm volatile("prefetch.global.L1 [%0];\n" ::"l"(p0 + 4 * FVV_WARPQ_L1PF * (size_t)w));
+#endif
                 a = p0[0]; b = p0[1]; c = p0[w]; e = p0[w + 1];
             }
             *op = (uint16_t)rne64((long long)bilerp_u(a, b, c, e, fx, fy, vb), k);
