@@ -725,6 +725,7 @@ def run_vinet(cfg, dev, steps=10, warmup=3, use_graph=True):
                      "note": "useful conv FLOPs / whole flow-network time (pyramid, block inputs and "
                              "residual kernels included); peak = sustained cuBLAS bf16 (%s)" % src},
         "dominant_kernel": dom,
+        "synthesis": synth_roofline(cfg, rig_ms - fl_ms, npairs, nviews, tiled, peaks, src),
         "parity": "fp32 torch oracle (oracle/vinet_ref.py): flows within 3 % max-abs, synthesis within "
                   "1 level, end-to-end PSNR >= 50 dB (tests/test_gpu_vinet.py)",
         "refine": refine,
@@ -815,6 +816,21 @@ def run_encoder(cfg, dev, cluster_bufs, stream, ticks=2):
             "bytes_per_rig_frame": nbytes / ticks,
             "parity": "byte-identical records vs reference-generated goldens, lossy I/P and lossless "
                       "(tests/test_gpu_encoder.py)"}
+
+
+def synth_roofline(cfg, ms, npairs, nviews, tiled, peaks, src):
+    """HBM roofline of the direct-t synthesis (+ fused tiling): per pair both source
+    frames read once, every view written, plus its quarter tile when tiled."""
+    W, H, fmt = cfg["W"], cfg["H"], cfg["fmt"]
+    fb = {0: 1.0, 1: 1.5, 2: 3.0}[fmt] * W * H
+    nbytes = npairs * (2 * fb + nviews * fb * (1 + (1 / 16 if tiled else 0)))
+    ach = nbytes / (ms / 1e3) / 1e9 if ms > 0 else 0.0
+    peak = float(peaks["hbm_gbs"])
+    return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "bytes_per_step": nbytes, "ms_per_step": ms,
+            "note": "algorithmic bytes (2 frames read + views written per pair) / synthesis + tiling time; "
+                    "the 15 views of a pixel reuse its source taps from L1/L2, so the kernel is "
+                    "instruction-bound well below this (DESIGN.md sec. 9); peak: %s HBM copy bandwidth" % src}
 
 
 def refine_conv_flops(W, H, nviews, npairs=1):
