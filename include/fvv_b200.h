@@ -91,10 +91,14 @@ int fvv_engine_max_pairs(const fvv_engine* engine);
  *                              (default 296 = 2 per SM)
  *   FVV_TUNE_MASK_COLS2        gray / 4:2:0 mask producer: 1 = two-column
  *                              walker k_mask_cols2 (default), 0 = k_mask_cols
+ *   FVV_TUNE_PDL               1 = launch the stage kernels with programmatic
+ *                              dependent launch, 0 = plain launches (only in
+ *                              a library built with -DFVV_PDL=1; off by default)
  * Not thread-safe against a concurrent call on the same engine. */
 #define FVV_TUNE_SCAN_COOP_MIN 0
 #define FVV_TUNE_SADW_RB_MIN_CTAS 1
 #define FVV_TUNE_MASK_COLS2 2
+#define FVV_TUNE_PDL 3
 int fvv_engine_set_tuning(fvv_engine* engine, int key, int value);
 
 /* interp.py:97-148, batched: out[i] = interpolate(left[i], right[i]).

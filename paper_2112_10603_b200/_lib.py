@@ -13,7 +13,7 @@ from pathlib import Path
 from ._build import LIB
 
 FVV_OK, FVV_EINVAL, FVV_ELAYOUT, FVV_ECUDA, FVV_EUNSUPPORTED = 0, -1, -2, -3, -4
-FVV_TUNE_SCAN_COOP_MIN, FVV_TUNE_SADW_RB_MIN_CTAS, FVV_TUNE_MASK_COLS2 = 0, 1, 2
+FVV_TUNE_SCAN_COOP_MIN, FVV_TUNE_SADW_RB_MIN_CTAS, FVV_TUNE_MASK_COLS2, FVV_TUNE_PDL = 0, 1, 2, 3
 FVV_DENSE_RECURSIVE, FVV_DENSE_DIRECT = 0, 1
 
 # every symbol include/fvv_b200.h declares (tests/test_abi.py checks both ways)

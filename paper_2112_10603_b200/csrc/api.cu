@@ -133,6 +133,7 @@ void make_geometry(const fvv_frame_desc* d, const fvv_interp_params* p, Geometry
     g->scan_coop_min = kScanCoopMinDefault;
     g->sadw_rb_min_ctas = kSadwRbMinCtasDefault;
     g->mask_cols2 = FVV_MASK_COLS2;
+    g->pdl = FVV_PDL;
 }
 
 // workspace = [header: candidate tables][pair slot 0][pair slot 1]...
@@ -320,6 +321,7 @@ int fvv_engine_set_tuning(fvv_engine* e, int key, int value) {
         case FVV_TUNE_SCAN_COOP_MIN: e->g.scan_coop_min = value < 0 ? kScanCoopMinDefault : value; break;
         case FVV_TUNE_SADW_RB_MIN_CTAS: e->g.sadw_rb_min_ctas = value < 0 ? kSadwRbMinCtasDefault : value; break;
         case FVV_TUNE_MASK_COLS2: e->g.mask_cols2 = value < 0 ? FVV_MASK_COLS2 : (value != 0); break;
+        case FVV_TUNE_PDL: e->g.pdl = value < 0 ? FVV_PDL : (value != 0); break;
         default: return fail(FVV_EINVAL, "unknown tuning key " + std::to_string(key));
     }
     return FVV_OK;

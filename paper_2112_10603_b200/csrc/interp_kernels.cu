@@ -43,6 +43,7 @@ namespace fvv {
 // s4/4 and s16/16 exactly.
 // ---------------------------------------------------------------------------
 __global__ void k_pyramid(Geometry g, PairTable pt, uint8_t* __restrict__ ws, Planes P) {
+    pdl_enter();
     const int w0 = g.lv[0].w, h0 = g.lv[0].h;
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
@@ -163,6 +164,7 @@ struct SadLaunch {
 template <int LEVEL, int KP, bool FULL8>
 __global__ void __launch_bounds__(256) k_sad(Geometry g, PairTable pt, uint8_t* __restrict__ ws,
                                              Planes P, SadLaunch sl) {
+    pdl_enter();
     extern __shared__ __align__(16) uint8_t smem[];
     const Level L = g.lv[LEVEL];
     const int B = L.block, r = L.r, side = 2 * r + 1;
@@ -389,6 +391,7 @@ struct Sad8Launch {
 template <int LEVEL, int KP>
 __global__ void __launch_bounds__(256, FVV_MINB_SAD8) k_sad8(Geometry g, PairTable pt, uint8_t* __restrict__ ws,
                                               Planes P, Sad8Launch sl) {
+    pdl_enter();
     extern __shared__ __align__(16) uint8_t smem[];
     const Level L = g.lv[LEVEL];
     const int r = L.r, side = 2 * r + 1;
@@ -534,6 +537,7 @@ struct SadPLaunch {
 template <int LEVEL, int SIDE>
 __global__ void __launch_bounds__(256, FVV_MINB_SADP) k_sadp(Geometry g, PairTable pt, uint8_t* __restrict__ ws,
                                               Planes P, SadPLaunch sl) {
+    pdl_enter();
     extern __shared__ __align__(16) uint8_t smem[];
     const Level L = g.lv[LEVEL];
     constexpr int r = SIDE / 2;
@@ -644,6 +648,7 @@ __global__ void __launch_bounds__(256, FVV_MINB_SADP) k_sadp(Geometry g, PairTab
 constexpr int kFH = 64, kFW = 64;
 template <int LEVEL>
 __global__ void __launch_bounds__(256) k_flow(Geometry g, uint8_t* __restrict__ ws, Planes P) {
+    pdl_enter();
     __shared__ int2 hu[kFH / 2 + 3][kFW];   // x-lerped rows of flow_{L-1}
     __shared__ int2 hb[kFH / 2 + 3][kFW];   // x-lerped block rows (B >= 2)
     __shared__ ITap cu[kFW], cb[kFW];
@@ -715,6 +720,7 @@ constexpr int kQH = 64, kQW = 64;  // 16 pixels per thread amortise the tile set
 template <int LEVEL>
 __global__ void __launch_bounds__(256) k_warpq(Geometry g, PairTable pt, uint8_t* __restrict__ ws,
                                                Planes P) {
+    pdl_enter();
     __shared__ int2 h[kQH / 2 + 3][kQW];
     __shared__ ITap cxt[kQW];
     __shared__ int4 rt[kQH];  // per tile row: base-flow y tap (i0 - s_lo, i1 - s_lo, f)
@@ -840,6 +846,7 @@ constexpr int kMW = 28, kMWarps = 4, kMH = FVV_KMH, kMaskUnroll = FVV_MASK_UNROL
 template <int FMT>
 __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geometry g, PairTable pt,
                                                                uint8_t* __restrict__ ws, Planes P) {
+    pdl_enter();
     const int W = g.W, H = g.H;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int pair = blockIdx.z;
@@ -1132,6 +1139,7 @@ constexpr int kM2Own = 60, kM2Warps = 4;
 template <int FMT>
 __global__ void __launch_bounds__(kM2Warps * 32, FVV_MINB_MASK2) k_mask_cols2(Geometry g, PairTable pt,
                                                                   uint8_t* __restrict__ ws, Planes P) {
+    pdl_enter();
     static_assert(FMT != FVV_RGB8, "RGB8 runs k_mask_cols");
     const int W = g.W, H = g.H;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1571,6 +1579,7 @@ __device__ __forceinline__ double d0_of(int s) { return div3(u2d_exact(s)); }  /
 template <bool COOP>
 __global__ void __launch_bounds__(kCR) k_scan_carry(Geometry g, const uint8_t* __restrict__ ws,
                                                     Planes P) {
+    pdl_enter();
     __shared__ __align__(16) uint16_t tile[2][kCR][kCTP];  // per lane: its own row segment
 #if FVV_SCAN_TSTORE
     __shared__ __align__(16) double ctile[kCR][kCC / 8 + 2];  // carry transpose (80 B pitch: no conflicts)
@@ -1755,6 +1764,7 @@ template <int FMT>
 __global__ void __launch_bounds__(128, FVV_MINB_BLEND) k_blend(Geometry g, PairTable pt, const uint8_t* __restrict__ ws,
                                                Planes P, int pair_base, bool write_frame,
                                                double* mask_out /* nullable: (launch pairs, H, W) */) {
+    pdl_enter();
     // thread = one 8-column group of ONE row; a warp holds 16 groups x the 2 rows
     // of a row pair (lanes 0-15: upper row, 16-31: lower row), so the chroma
     // 2x2-mean mask comes from a shuffle and each thread keeps one row's state
@@ -2050,6 +2060,7 @@ __device__ __forceinline__ uint32_t sadw_group(const uint32_t* Rb, const uint32_
 template <int LEVEL, int SIDE, int CG, int RB_>
 __global__ void __launch_bounds__(SadW<SIDE, CG, RB_>::THREADS, FVV_MINB_SADW(SIDE))
 k_sadw(Geometry g, PairTable pt, uint8_t* __restrict__ ws, Planes P, SadWLaunch sl) {
+    pdl_enter();
     using S = SadW<SIDE, CG, RB_>;
     extern __shared__ __align__(16) uint8_t smem[];
     uint32_t* Ts = reinterpret_cast<uint32_t*>(smem);              // WH x TWW raw words
@@ -2176,7 +2187,8 @@ static cudaError_t launch_sadw_rb(const Geometry& g, const PairTable& pt, uint8_
         if (e != cudaSuccess) return e;
     }
     dim3 grid((sl.bx_end + 7) / 8, (L.nby + S::NBYT - 1) / S::NBYT, 2 * npairs);
-    kern<<<grid, S::THREADS, S::SMEM, st>>>(g, pt, ws, P, sl);
+    cudaError_t le = launch_k(g.pdl, kern, grid, dim3(S::THREADS), S::SMEM, st, g, pt, ws, P, sl);
+    if (le != cudaSuccess) return le;
     return cudaGetLastError();
 }
 
@@ -2212,7 +2224,8 @@ static cudaError_t launch_sad_kp(const Geometry& g, const PairTable& pt, uint8_t
         if (e != cudaSuccess) return e;
     }
     dim3 grid((nbx + sl.nbx_cta - 1) / sl.nbx_cta, L.nby, 2 * npairs);
-    kern<<<grid, threads, smem, st>>>(g, pt, ws, P, sl);
+    cudaError_t le = launch_k(g.pdl, kern, grid, dim3(threads), smem, st, g, pt, ws, P, sl);
+    if (le != cudaSuccess) return le;
     return cudaGetLastError();
 }
 
@@ -2264,7 +2277,8 @@ static cudaError_t launch_sad8_kp(const Geometry& g, const PairTable& pt, uint8_
         if (e != cudaSuccess) return e;
     }
     dim3 grid((ncols + sl.nbx - 1) / sl.nbx, (L.nby + sl.nby - 1) / sl.nby, 2 * npairs);
-    kern<<<grid, threads, smem, st>>>(g, pt, ws, P, sl);
+    cudaError_t le = launch_k(g.pdl, kern, grid, dim3(threads), smem, st, g, pt, ws, P, sl);
+    if (le != cudaSuccess) return le;
     return cudaGetLastError();
 }
 
@@ -2326,8 +2340,8 @@ static cudaError_t run_sad(const Geometry& g, const PairTable& pt, uint8_t* ws, 
                 cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                 if (e2 != cudaSuccess) return e2;
             }
-            kern<<<grid, threads, smem, st>>>(g, pt, ws, P, sp);
-            return cudaGetLastError();
+            cudaError_t le = launch_k(g.pdl, kern, grid, dim3(threads), smem, st, g, pt, ws, P, sp);
+            return le != cudaSuccess ? le : cudaGetLastError();
         };
         switch (side) {
             case 3: e = go(k_sadp<LEVEL, 3>); break;
@@ -2417,37 +2431,37 @@ cudaError_t run_interp_stage(const Geometry& g, const PairTable& pt, uint8_t* ws
     };
 
     B(KC_PYRAMID);
-    k_pyramid<<<dim3((g.lv[0].w + 31) / 32, (g.lv[0].h + 7) / 8, 2 * npairs), dim3(32, 8), 0, st>>>(
-        g, pt, ws, P);
-    if ((e = E()) != cudaSuccess) return e;
+    e = launch_k(g.pdl, k_pyramid, dim3((g.lv[0].w + 31) / 32, (g.lv[0].h + 7) / 8, 2 * npairs), dim3(32, 8),
+                 0, st, g, pt, ws, P);
+    if (e != cudaSuccess || (e = E()) != cudaSuccess) return e;
 
     B(KC_SAD0);
     e = run_sad<0>(g, pt, ws, P, rank_of[0], cand_of_rank[0], npairs, st);
     if (e != cudaSuccess || (e = E()) != cudaSuccess) return e;
 
     B(KC_FLOW0);
-    k_flow<0><<<dim3((g.lv[0].w + kFW - 1) / kFW, (g.lv[0].h + kFH - 1) / kFH, 2 * npairs), 256, 0,
-                st>>>(g, ws, P);
-    if ((e = E()) != cudaSuccess) return e;
+    e = launch_k(g.pdl, k_flow<0>, dim3((g.lv[0].w + kFW - 1) / kFW, (g.lv[0].h + kFH - 1) / kFH, 2 * npairs),
+                 dim3(256), 0, st, g, ws, P);
+    if (e != cudaSuccess || (e = E()) != cudaSuccess) return e;
 
     B(KC_WARPQ1);
-    k_warpq<1><<<dim3((g.lv[1].w + kQW - 1) / kQW, (g.lv[1].h + kQH - 1) / kQH, 2 * npairs), 256, 0,
-                 st>>>(g, pt, ws, P);
-    if ((e = E()) != cudaSuccess) return e;
+    e = launch_k(g.pdl, k_warpq<1>, dim3((g.lv[1].w + kQW - 1) / kQW, (g.lv[1].h + kQH - 1) / kQH, 2 * npairs),
+                 dim3(256), 0, st, g, pt, ws, P);
+    if (e != cudaSuccess || (e = E()) != cudaSuccess) return e;
 
     B(KC_SAD1);
     e = run_sad<1>(g, pt, ws, P, rank_of[1], cand_of_rank[1], npairs, st);
     if (e != cudaSuccess || (e = E()) != cudaSuccess) return e;
 
     B(KC_FLOW1);
-    k_flow<1><<<dim3((g.lv[1].w + kFW - 1) / kFW, (g.lv[1].h + kFH - 1) / kFH, 2 * npairs), 256, 0,
-                st>>>(g, ws, P);
-    if ((e = E()) != cudaSuccess) return e;
+    e = launch_k(g.pdl, k_flow<1>, dim3((g.lv[1].w + kFW - 1) / kFW, (g.lv[1].h + kFH - 1) / kFH, 2 * npairs),
+                 dim3(256), 0, st, g, ws, P);
+    if (e != cudaSuccess || (e = E()) != cudaSuccess) return e;
 
     B(KC_WARPQ2);
-    k_warpq<2><<<dim3((g.lv[2].w + kQW - 1) / kQW, (g.lv[2].h + kQH - 1) / kQH, 2 * npairs), 256, 0,
-                 st>>>(g, pt, ws, P);
-    if ((e = E()) != cudaSuccess) return e;
+    e = launch_k(g.pdl, k_warpq<2>, dim3((g.lv[2].w + kQW - 1) / kQW, (g.lv[2].h + kQH - 1) / kQH, 2 * npairs),
+                 dim3(256), 0, st, g, pt, ws, P);
+    if (e != cudaSuccess || (e = E()) != cudaSuccess) return e;
 
     B(KC_SAD2);
     e = run_sad<2>(g, pt, ws, P, rank_of[2], cand_of_rank[2], npairs, st);
@@ -2456,34 +2470,33 @@ cudaError_t run_interp_stage(const Geometry& g, const PairTable& pt, uint8_t* ws
     B(KC_MASK_PROD);
     if (g.fmt != FVV_RGB8 && g.mask_cols2) {
         const dim3 grd((g.W + kM2Own * kM2Warps - 1) / (kM2Own * kM2Warps), (g.H + kMH - 1) / kMH, npairs);
-        if (g.fmt == FVV_YUV420) k_mask_cols2<FVV_YUV420><<<grd, kM2Warps * 32, 0, st>>>(g, pt, ws, P);
-        else k_mask_cols2<FVV_GRAY8><<<grd, kM2Warps * 32, 0, st>>>(g, pt, ws, P);
+        e = launch_k(g.pdl, g.fmt == FVV_YUV420 ? k_mask_cols2<FVV_YUV420> : k_mask_cols2<FVV_GRAY8>, grd,
+                     dim3(kM2Warps * 32), 0, st, g, pt, ws, P);
     } else {
         const dim3 grd((g.W + kMW * kMWarps - 1) / (kMW * kMWarps), (g.H + kMH - 1) / kMH, npairs);
-        if (g.fmt == FVV_YUV420) k_mask_cols<FVV_YUV420><<<grd, kMWarps * 32, 0, st>>>(g, pt, ws, P);
-        else if (g.fmt == FVV_RGB8) k_mask_cols<FVV_RGB8><<<grd, kMWarps * 32, 0, st>>>(g, pt, ws, P);
-        else k_mask_cols<FVV_GRAY8><<<grd, kMWarps * 32, 0, st>>>(g, pt, ws, P);
+        e = launch_k(g.pdl, g.fmt == FVV_YUV420 ? k_mask_cols<FVV_YUV420>
+                            : g.fmt == FVV_RGB8 ? k_mask_cols<FVV_RGB8> : k_mask_cols<FVV_GRAY8>,
+                     grd, dim3(kMWarps * 32), 0, st, g, pt, ws, P);
     }
-    if ((e = E()) != cudaSuccess) return e;
+    if (e != cudaSuccess || (e = E()) != cudaSuccess) return e;
 
     B(KC_SCAN);
     {
         // cooperative row staging pays once the launch has several warps per SM;
         // below that the per-warp critical path (its index math) dominates
         const dim3 grid((g.H + kCR - 1) / kCR, npairs);
-        if ((int)(grid.x * grid.y) >= g.scan_coop_min)
-            k_scan_carry<true><<<grid, kCR, 0, st>>>(g, ws, P);
-        else
-            k_scan_carry<false><<<grid, kCR, 0, st>>>(g, ws, P);
+        e = launch_k(g.pdl, (int)(grid.x * grid.y) >= g.scan_coop_min ? k_scan_carry<true> : k_scan_carry<false>,
+                     grid, dim3(kCR), 0, st, g, ws, P);
     }
-    if ((e = E()) != cudaSuccess) return e;
+    if (e != cudaSuccess || (e = E()) != cudaSuccess) return e;
     B(KC_BLEND);
     {
         const dim3 grd(((g.W + 7) / 8 + 63) / 64, g.H / 2, npairs);
-        if (g.fmt == FVV_YUV420) k_blend<FVV_YUV420><<<grd, 128, 0, st>>>(g, pt, ws, P, 0, true, mask_out);
-        else if (g.fmt == FVV_RGB8) k_blend<FVV_RGB8><<<grd, 128, 0, st>>>(g, pt, ws, P, 0, true, mask_out);
-        else k_blend<FVV_GRAY8><<<grd, 128, 0, st>>>(g, pt, ws, P, 0, true, mask_out);
+        e = launch_k(g.pdl, g.fmt == FVV_YUV420 ? k_blend<FVV_YUV420>
+                            : g.fmt == FVV_RGB8 ? k_blend<FVV_RGB8> : k_blend<FVV_GRAY8>,
+                     grd, dim3(128), 0, st, g, pt, ws, P, 0, true, mask_out);
     }
+    if (e != cudaSuccess) return e;
     return E();
 }
 

@@ -81,6 +81,7 @@ __global__ void k_downscale(FrameDims s, FrameDims q, int f, const uint8_t* __re
 // (the synthesized ones) were written by the synthesis kernel (fused tiling).
 __global__ void k_rig_clusters_1(FrameDims fd, ClusterJobs jobs, ViewSrc vs,
                                  uint8_t* __restrict__ clusters, int skip_period) {
+    pdl_enter();
     const uint8_t* __restrict__ views = vs.views;
     const ClusterJob jb = jobs.job[blockIdx.z];
     const int sw = jb.sw, sh = fd.H;
@@ -138,6 +139,7 @@ __global__ void k_rig_clusters_1(FrameDims fd, ClusterJobs jobs, ViewSrc vs,
 // straddles a cell.
 __global__ void k_rig_clusters(FrameDims fd, ClusterJobs jobs, ViewSrc vs,
                                uint8_t* __restrict__ clusters, int skip_period) {
+    pdl_enter();
     const uint8_t* __restrict__ views = vs.views;
     const ClusterJob jb = jobs.job[blockIdx.z];
     const int sw = jb.sw, sh = fd.H;
@@ -280,16 +282,17 @@ cudaError_t launch_rig_clusters_src(int W, int H, int fmt, const ClusterJob* job
     FrameDims fd = dims_of(W, H, fmt);
     for (int b = 0; b < njobs; b += kMaxClusters) {
         ClusterJobs cj;
+        cudaError_t e;
         int n = njobs - b < kMaxClusters ? njobs - b : kMaxClusters;
         for (int i = 0; i < n; i++) cj.job[i] = jobs[b + i];
         if (W % 32 == 0) {
             dim3 grd((unsigned)((max_cluster_bytes / 4 + 255) / 256), 1, n);
-            k_rig_clusters<<<grd, 256, 0, st>>>(fd, cj, vs, out, skip_period);
+            e = launch_k(true, k_rig_clusters, grd, dim3(256), 0, st, fd, cj, vs, out, skip_period);
         } else {
             dim3 grd((unsigned)((max_cluster_bytes + 255) / 256), 1, n);
-            k_rig_clusters_1<<<grd, 256, 0, st>>>(fd, cj, vs, out, skip_period);
+            e = launch_k(true, k_rig_clusters_1, grd, dim3(256), 0, st, fd, cj, vs, out, skip_period);
         }
-        cudaError_t e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;

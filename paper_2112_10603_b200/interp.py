@@ -136,7 +136,7 @@ class Interpolator:
             pass
 
     def set_tuning(self, scan_coop_min: int | None = None, sadw_rb_min_ctas: int | None = None,
-                   mask_cols2: int | None = None):
+                   mask_cols2: int | None = None, pdl: int | None = None):
         """Launch-variant thresholds (fvv_engine_set_tuning); results are
         identical for every setting -- the tests use it to force each variant.
         None leaves a knob unchanged, -1 restores its default."""
@@ -147,6 +147,8 @@ class Interpolator:
                                                      int(sadw_rb_min_ctas)))
         if mask_cols2 is not None:
             _lib.check(self._L.fvv_engine_set_tuning(self._h, _lib.FVV_TUNE_MASK_COLS2, int(mask_cols2)))
+        if pdl is not None:
+            _lib.check(self._L.fvv_engine_set_tuning(self._h, _lib.FVV_TUNE_PDL, int(pdl)))
         return self
 
     @property

@@ -9,7 +9,8 @@ stacked blocks from 2 CTAs per SM).  These tests run:
   against the oracle, byte for byte (views and clusters);
 * cfg2's `dense_views(..., 3)` at 1080p;
 * every golden vector and ragged sizes with each launch variant FORCED on
-  and off (fvv_engine_set_tuning), including partial scan chunks;
+  and off (fvv_engine_set_tuning), including partial scan chunks and plain launches
+  instead of programmatic dependent launch;
 * `assemble_cluster_frame` (k_assemble, the kernel plugin.install binds into
   the reference's `_stitch`) for gray and 4:2:0 with a part-empty last column;
 * the drop-in `dense_views` from a 2-worker ThreadPoolExecutor, as the
@@ -25,8 +26,8 @@ from oracle import oracle as O
 
 pytestmark = pytest.mark.gpu
 
-VARIANTS = {"all_on": dict(scan_coop_min=0, sadw_rb_min_ctas=0, mask_cols2=1),
-            "all_off": dict(scan_coop_min=1 << 30, sadw_rb_min_ctas=1 << 30, mask_cols2=0)}
+VARIANTS = {"all_on": dict(scan_coop_min=0, sadw_rb_min_ctas=0, mask_cols2=1, pdl=1),
+            "all_off": dict(scan_coop_min=1 << 30, sadw_rb_min_ctas=1 << 30, mask_cols2=0, pdl=0)}
 
 
 @pytest.fixture(scope="module")
