@@ -804,13 +804,6 @@ __global__ void __launch_bounds__(256) k_warpq(Geometry g, PairTable pt, uint8_t
     }
 }
 
-// f32(f64(S / 3)) for S = sn * 2^-k exact (the column pass of uniform_filter1d
-// on the occlusion cue): S is exact in f64, div3 is the correctly rounded
-// quotient, the cast rounds once more -- exactly the reference's arithmetic.
-__device__ __forceinline__ float third_f32(int sn, float scale) {
-    return (float)div3(__dmul_rn((double)sn, (double)scale));
-}
-
 // ---------------------------------------------------------------------------
 // k_mask_cols: everything of _mask_inputs (interp.py:78-94) that does not
 // depend on scipy's order of summation, plus the mid warps of every plane
@@ -897,10 +890,10 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
         if (a == 0.0f && o0v == 0.0f && c == 0.0f) return 0.0f;
         return (float)div3(__dadd_rn(__dadd_rn((double)a, (double)o0v), (double)c));
     };
-    const double oscale_d = (double)oscale;
+    const double c3k = 0x1.5555555555555p-2 * (double)oscale;  // RN(1/3) * 2^-(mb+1), exact
     auto colpass = [&](int a, int b, int c) {  // f32(f64(sum/3)) of occ in units 2^-(mb+1)
         const int sn = a + b + c;  // >= 0, < 2^31: (double)sn built exactly off the XU pipe
-        return sn ? (float)div3(__dmul_rn(u2d_exact((uint32_t)sn), oscale_d)) : 0.0f;
+        return sn ? third_scaled_f32((uint32_t)sn, c3k) : 0.0f;
     };
 
     // source-row caches: x-lerped rows ua, ua+1 of flow1 and ba, ba+1 of the block grid
@@ -1181,7 +1174,7 @@ __global__ void __launch_bounds__(kM2Warps * 32, FVV_MINB_MASK2) k_mask_cols2(Ge
     float* o_ol = plane<float>(ws, P, P.occ_l, pair);
     float* o_or = plane<float>(ws, P, P.occ_r, pair);
     uchar4* o_wc = FMT == FVV_YUV420 ? plane<uchar4>(ws, P, P.wc, pair) : nullptr;
-    const double oscale_d = (double)(1.0f / (float)(1 << (mb + 1)));
+    const double c3k = 0x1.5555555555555p-2 * (double)(1.0f / (float)(1 << (mb + 1)));  // exact
     const int ys = max(0, y0 - 2), ye = min(H - 1, y0 + kMH + 1);
     const int yo1 = min(H, y0 + kMH);
 
@@ -1196,7 +1189,7 @@ __global__ void __launch_bounds__(kM2Warps * 32, FVV_MINB_MASK2) k_mask_cols2(Ge
     };
     auto colpass = [&](int a, int b, int c) {  // f32(f64(sum/3)) of occ in units 2^-(mb+1)
         const int sn = a + b + c;
-        return sn ? (float)div3(__dmul_rn(u2d_exact((uint32_t)sn), oscale_d)) : 0.0f;
+        return sn ? third_scaled_f32((uint32_t)sn, c3k) : 0.0f;
     };
     auto row3 = [&](float a, float b, float c) {  // f32(f64(a + b + c) / 3)
         if (a == 0.0f && b == 0.0f && c == 0.0f) return 0.0f;
