@@ -341,6 +341,19 @@ int fvv_encode_blocks(const fvv_enc_job* jobs_dev, int njobs, long long total_bl
                       int* ntok, void* stream);
 int fvv_encode_tokens(const int16_t* zz, const long long* tok_off, long long nblocks, uint8_t* out, void* stream);
 
+/* DEFLATE of many independent byte streams on the device, byte-identical to
+ * zlib.compress(stream, 6)[2:-4] -- the raw DEFLATE data of each plane's token
+ * stream that codec.py:148 (_encode_plane) keeps.  zlib 1.3's level-6
+ * deflate_slow / trees.c decisions restated in csrc/zdeflate_core.h.
+ * offsets (host, nstreams + 1, ascending): stream s = data[offsets[s],
+ * offsets[s+1]) (data on the device).  out (device, 8-byte aligned, at least
+ * *out_capacity bytes) receives the compressed streams back to back;
+ * out_offsets (device, nstreams + 1) their offsets (out_offsets[0] = 0).
+ * Stream-ordered; the offsets are read on the host during the call. */
+int fvv_deflate_scratch_bytes(const long long* offsets, int nstreams, size_t* scratch_bytes, size_t* out_capacity);
+int fvv_deflate(const uint8_t* data, const long long* offsets, int nstreams, uint8_t* out, long long* out_offsets,
+                void* scratch, size_t scratch_bytes, void* stream);
+
 /* ---------------------------------------------------------------------------
  * TS packaging (host code; mpegts.py:188-212
  * mux_segment): one cluster's MPEG-TS segment from the tile records of its

@@ -14,7 +14,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libfvv_b200.so"
-SOURCES = ["interp_kernels.cu", "tile_kernels.cu", "conv_tc.cu", "vinet_kernels.cu", "refine_kernels.cu", "encode_kernels.cu", "ts_mux.cpp", "diag_kernels.cu", "literal_kernels.cu", "api.cu"]
+SOURCES = ["interp_kernels.cu", "tile_kernels.cu", "conv_tc.cu", "vinet_kernels.cu", "refine_kernels.cu", "encode_kernels.cu", "deflate_kernels.cu", "ts_mux.cpp", "diag_kernels.cu", "literal_kernels.cu", "api.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

@@ -29,7 +29,7 @@ EXPORTS = (
     "fvv_vinet_synth", "fvv_vinet_rig", "fvv_vinet_rig_clusters",
     "fvv_refine_image", "fvv_refine_inputs", "fvv_refine_flow_pool", "fvv_refine_warp_features",
     "fvv_nhwc_copy", "fvv_refine_output",
-    "fvv_encode_set_tables", "fvv_encode_blocks", "fvv_encode_tokens",
+    "fvv_encode_set_tables", "fvv_encode_blocks", "fvv_encode_tokens", "fvv_deflate_scratch_bytes", "fvv_deflate",
     "fvv_ts_segment_bytes", "fvv_ts_mux_segment",
 )
 

@@ -14,6 +14,7 @@
 #include "vinet.h"
 #include "refine.h"
 #include "encode.h"
+#include "deflate.h"
 #include "literal.h"
 
 namespace fvv {
@@ -1192,4 +1193,40 @@ extern "C" int fvv_encode_tokens(const int16_t* zz, const long long* tok_off, lo
     if (!zz || !tok_off || !out || nblocks < 0) return fail(FVV_EINVAL, "bad token batch");
     cudaError_t e = enc_tokens(zz, tok_off, nblocks, out, static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? FVV_OK : cuda_fail(e, "fvv_encode_tokens");
+}
+
+// ---------------------------------------------------------------------------
+// DEFLATE of many byte streams (deflate_kernels.cu): zlib.compress(x, 6)[2:-4]
+// ---------------------------------------------------------------------------
+static int deflate_lengths(const long long* offsets, int nstreams, std::vector<int64_t>& len) {
+    if (!offsets || nstreams < 1) return fail(FVV_EINVAL, "bad stream offsets");
+    len.resize(nstreams);
+    for (int s = 0; s < nstreams; s++) {
+        if (offsets[s + 1] < offsets[s] || offsets[s] < 0) return fail(FVV_EINVAL, "stream offsets must ascend");
+        len[s] = offsets[s + 1] - offsets[s];
+    }
+    return FVV_OK;
+}
+
+extern "C" int fvv_deflate_scratch_bytes(const long long* offsets, int nstreams, size_t* scratch_bytes,
+                                         size_t* out_capacity) {
+    std::vector<int64_t> len;
+    if (int r = deflate_lengths(offsets, nstreams, len)) return r;
+    if (scratch_bytes) *scratch_bytes = zd_scratch_bytes(len.data(), nstreams);
+    if (out_capacity) *out_capacity = zd_out_capacity(len.data(), nstreams);
+    return FVV_OK;
+}
+
+extern "C" int fvv_deflate(const uint8_t* data, const long long* offsets, int nstreams, uint8_t* out,
+                           long long* out_offsets, void* scratch, size_t scratch_bytes, void* stream) {
+    std::vector<int64_t> len;
+    if (int r = deflate_lengths(offsets, nstreams, len)) return r;
+    if (!data || !out || !out_offsets || !scratch) return fail(FVV_EINVAL, "null deflate buffer");
+    if (reinterpret_cast<uintptr_t>(out) % 8) return fail(FVV_EINVAL, "deflate output must be 8-byte aligned");
+    if (scratch_bytes < zd_scratch_bytes(len.data(), nstreams)) return fail(FVV_EINVAL, "deflate scratch too small");
+    static_assert(sizeof(long long) == sizeof(int64_t), "offsets are int64");
+    cudaError_t e = zd_deflate(data, reinterpret_cast<const int64_t*>(offsets), nstreams, out,
+                               reinterpret_cast<int64_t*>(out_offsets), scratch, scratch_bytes,
+                               static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? FVV_OK : cuda_fail(e, "fvv_deflate");
 }

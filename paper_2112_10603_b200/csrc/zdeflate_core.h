@@ -205,6 +205,50 @@ ZHD MatchRec match_search(int64_t p, int64_t n, const Win& win, const PDist& pdi
     return r;
 }
 
+// match_search with 32-bit window-relative indices over plain arrays (the
+// device form): sb / sp hold the bytes and links of positions [wb, ...), P is
+// the position relative to wb, la = n - p; the NIL edge is checked by the caller.
+ZHD uint32_t finish_rec32(int best, int dist) {
+    if (best <= 2 || (best == kMinMatch && dist > kTooFar)) return 0;
+    return ((uint32_t)best << 16) | (uint32_t)dist;
+}
+ZHD MatchRec match_search32(const uint8_t* sb, const uint16_t* sp, int P, int la, int pd0) {
+    MatchRec r{0, 0};
+    const int nice = la < kNiceLength ? la : kNiceLength;
+    const int maxlen = la < kMaxMatch ? la : kMaxMatch;
+    const int lim = P - kMaxDist;  // later candidates must lie above (distance < MAX_DIST)
+    const int s0 = sb[P], s1 = sb[P + 1];
+    int e1 = s1, e0 = sb[P + 2];   // scan[best - 1], scan[best]
+    int best = 2, bc = P, cnt = 0, c = P - pd0;
+    bool have32 = false;
+    for (;;) {
+        cnt++;
+        if (sb[c + best] == e0 && sb[c + best - 1] == e1 && sb[c] == s0 && sb[c + 1] == s1) {
+            int len = 3;
+            while (len < maxlen && sb[c + len] == sb[P + len]) len++;
+            if (len > best) {
+                best = len;
+                bc = c;
+                if (len >= nice) break;
+                e1 = sb[P + best - 1];
+                e0 = sb[P + best];
+            }
+        }
+        if (cnt == kMaxChain >> 2) {
+            r.r32 = finish_rec32(best, P - bc);
+            have32 = true;
+        }
+        if (cnt == kMaxChain) break;
+        const int d = sp[c];
+        if (d == 0) break;
+        c -= d;
+        if (c <= lim) break;
+    }
+    r.r128 = finish_rec32(best, P - bc);
+    if (!have32) r.r32 = r.r128;
+    return r;
+}
+
 // ---------------------------------------------------------------------------
 // Lazy parse (deflate_slow).  Symbols: (dist << 8) | lc as zlib's sym_buf
 // (dist 0: literal lc; else lc = match length - 3).
@@ -230,21 +274,83 @@ struct ParseState {
     int ml;             // match_length
     int64_t ms;         // match_start
     int avail;          // match_available
+    int final_lit;      // the input ended with a pending literal (emitted after the loop)
     int64_t slides;     // window slides so far
     int64_t nsym;       // symbols emitted
     int64_t blk_sym0, blk_byte0;
     int32_t nblocks;
 };
 
-ZHD void parse_init(ParseState& st) {
-    st.s = 0; st.ml = kMinMatch - 1; st.ms = 0; st.avail = 0; st.slides = 0; st.nsym = 0;
+ZHD void parse_init(ParseState& st, int64_t s0 = 0) {
+    st.s = s0; st.ml = kMinMatch - 1; st.ms = 0; st.avail = 0; st.final_lit = 0; st.slides = 0; st.nsym = 0;
     st.blk_sym0 = 0; st.blk_byte0 = 0; st.nblocks = 0;
 }
 
+// The parse's decisions depend on (s, match_length, match_start, match_available)
+// only, and with match_length 2 (no match pending: right after a match, in a run
+// of literals, or at a fresh start) match_start is never read again.  Two parses
+// of the same data that meet at a loop top with equal sync codes stay identical.
+// 0: not a sync state; 1: match_length 2, nothing pending; 2: match_length 2,
+// literal s - 1 pending.
+ZHD int sync_code(const ParseState& st) { return st.ml == kMinMatch - 1 ? 1 + st.avail : 0; }
+ZHD bool canonical(const ParseState& st) { return st.ml == kMinMatch - 1 && st.avail == 0; }
+
+// input bytes a symbol covers
+ZHD int sym_cover(uint32_t sym) { return (sym >> 8) ? (int)(sym & 0xff) + kMinMatch : 1; }
+
+// One deflate_slow iteration without the block bookkeeping (blocks are cut
+// from the finished symbol stream: every 16383 symbols).  At s >= n: the
+// pending literal, then false.
+template <typename Rec, typename Byte, typename Emit>
+ZHD bool parse_iter(ParseState& st, int64_t n, const Rec& rec, const Byte& byte, const Emit& emit) {
+    if (st.s >= n) {
+        if (st.avail) {
+            emit((uint32_t)byte(st.s - 1));
+            st.avail = 0;
+            st.final_lit = 1;
+        }
+        return false;
+    }
+    const int64_t la = n - st.s;
+    const int pl = st.ml;
+    const int64_t pm = st.ms;
+    st.ml = kMinMatch - 1;
+    if (la >= kMinMatch && pl < kMaxLazy) {
+        const MatchRec m = rec(st.s);
+        const uint32_t r = pl < kGoodLength ? m.r128 : m.r32;
+        const int len = (int)(r >> 16);
+        if (len > pl) {
+            st.ml = len;
+            st.ms = st.s - (int64_t)(r & 0xffffu);
+        }
+    }
+    if (pl >= kMinMatch && st.ml <= pl) {
+        emit(((uint32_t)(st.s - 1 - pm) << 8) | (uint32_t)(pl - kMinMatch));
+        st.s += pl - 1;
+        st.avail = 0;
+        st.ml = kMinMatch - 1;
+    } else if (st.avail) {
+        emit((uint32_t)byte(st.s - 1));
+        st.s++;
+    } else {
+        st.avail = 1;
+        st.s++;
+    }
+    return true;
+}
+
+// window slides done by loop top s (deflate_slow / fill_window)
+ZHD int64_t slides_at(int64_t s, int64_t n) {
+    int64_t k = 0;
+    while (slide_at(k, n) <= s) k++;
+    return k;
+}
+
+// One iteration of deflate_slow's loop at loop top st.s; after the input is
+// consumed, the final literal and the last block.  Returns false once done.
 template <typename Rec, typename Byte, typename Emit, typename Block>
-ZHD void parse_stream(int64_t n, const Rec& rec, const Byte& byte, const Emit& emit, const Block& block) {
-    ParseState st;
-    parse_init(st);
+ZHD bool parse_step(ParseState& st, int64_t n, const Rec& rec, const Byte& byte, const Emit& emit,
+                    const Block& block) {
     auto flush = [&](int64_t end, int last) {
         BlockDesc b;
         b.sym0 = st.blk_sym0;
@@ -256,39 +362,49 @@ ZHD void parse_stream(int64_t n, const Rec& rec, const Byte& byte, const Emit& e
         st.blk_sym0 = st.nsym;
         st.blk_byte0 = end;
     };
-    for (;;) {
-        while (st.s >= slide_at(st.slides, n)) st.slides++;
-        if (st.s >= n) break;
-        const int64_t la = n - st.s;
-        const int pl = st.ml;
-        const int64_t pm = st.ms;
-        st.ml = kMinMatch - 1;
-        if (la >= kMinMatch && pl < kMaxLazy) {
-            const MatchRec m = rec(st.s);
-            const uint32_t r = pl < kGoodLength ? m.r128 : m.r32;
-            const int len = (int)(r >> 16);
-            if (len > pl) {
-                st.ml = len;
-                st.ms = st.s - (int64_t)(r & 0xffffu);
-            }
-        }
-        if (pl >= kMinMatch && st.ml <= pl) {
-            emit(st.nsym++, ((uint32_t)(st.s - 1 - pm) << 8) | (uint32_t)(pl - kMinMatch));
-            st.s += pl - 1;
-            st.avail = 0;
-            st.ml = kMinMatch - 1;
-            if (st.nsym - st.blk_sym0 == kBlockSyms) flush(st.s, 0);
-        } else if (st.avail) {
-            emit(st.nsym++, (uint32_t)byte(st.s - 1));
-            if (st.nsym - st.blk_sym0 == kBlockSyms) flush(st.s, 0);
-            st.s++;
-        } else {
-            st.avail = 1;
-            st.s++;
+    while (st.s >= slide_at(st.slides, n)) st.slides++;
+    if (st.s >= n) {
+        if (st.avail) emit(st.nsym++, (uint32_t)byte(st.s - 1));
+        st.avail = 0;
+        flush(n, 1);
+        return false;
+    }
+    const int64_t la = n - st.s;
+    const int pl = st.ml;
+    const int64_t pm = st.ms;
+    st.ml = kMinMatch - 1;
+    if (la >= kMinMatch && pl < kMaxLazy) {
+        const MatchRec m = rec(st.s);
+        const uint32_t r = pl < kGoodLength ? m.r128 : m.r32;
+        const int len = (int)(r >> 16);
+        if (len > pl) {
+            st.ml = len;
+            st.ms = st.s - (int64_t)(r & 0xffffu);
         }
     }
-    if (st.avail) emit(st.nsym++, (uint32_t)byte(st.s - 1));
-    flush(n, 1);
+    if (pl >= kMinMatch && st.ml <= pl) {
+        emit(st.nsym++, ((uint32_t)(st.s - 1 - pm) << 8) | (uint32_t)(pl - kMinMatch));
+        st.s += pl - 1;
+        st.avail = 0;
+        st.ml = kMinMatch - 1;
+        if (st.nsym - st.blk_sym0 == kBlockSyms) flush(st.s, 0);
+    } else if (st.avail) {
+        emit(st.nsym++, (uint32_t)byte(st.s - 1));
+        if (st.nsym - st.blk_sym0 == kBlockSyms) flush(st.s, 0);
+        st.s++;
+    } else {
+        st.avail = 1;
+        st.s++;
+    }
+    return true;
+}
+
+template <typename Rec, typename Byte, typename Emit, typename Block>
+ZHD void parse_stream(int64_t n, const Rec& rec, const Byte& byte, const Emit& emit, const Block& block) {
+    ParseState st;
+    parse_init(st);
+    while (parse_step(st, n, rec, byte, emit, block)) {
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -461,8 +577,9 @@ ZHD void scan_tree(TreeWork& w, uint16_t* dl, int max_code) {
 }
 
 // Histogram already in w.lfc[0..285] / w.dfc[0..29] (END_BLOCK counted).
-// Builds the three trees, returns the block type _tr_flush_block picks.
-ZHD int block_trees(TreeWork& w, const ZTab& t, int64_t stored_len, bool buf_ok) {
+// Builds the three trees; returns static or dynamic and (opt_lenb) the byte
+// size _tr_flush_block compares a stored block against.
+ZHD int block_trees_ns(TreeWork& w, const ZTab& t, uint64_t& opt_lenb_out) {
     w.opt_len = w.static_len = 0;
     for (int n = 0; n < kLCodes; n++) w.lreal[n] = w.lfc[n];
     for (int n = 0; n < kDCodes; n++) w.dreal[n] = w.dfc[n];
@@ -484,9 +601,20 @@ ZHD int block_trees(TreeWork& w, const ZTab& t, int64_t stored_len, bool buf_ok)
     uint64_t opt_lenb = (w.opt_len + 3 + 7) >> 3;
     const uint64_t static_lenb = (w.static_len + 3 + 7) >> 3;
     if (static_lenb <= opt_lenb) opt_lenb = static_lenb;
-    if ((uint64_t)stored_len + 4 <= opt_lenb && buf_ok) return kStored;
-    if (static_lenb == opt_lenb) return kStatic;
-    return kDynamic;
+    opt_lenb_out = opt_lenb;
+    return static_lenb == opt_lenb ? kStatic : kDynamic;
+}
+
+// _tr_flush_block's choice: stored when it is no larger and the block's start
+// is still in the window (buf != NULL), else static or dynamic
+ZHD bool take_stored(int64_t stored_len, uint64_t opt_lenb, bool buf_ok) {
+    return (uint64_t)stored_len + 4 <= opt_lenb && buf_ok;
+}
+
+ZHD int block_trees(TreeWork& w, const ZTab& t, int64_t stored_len, bool buf_ok) {
+    uint64_t ob;
+    const int ty = block_trees_ns(w, t, ob);
+    return take_stored(stored_len, ob, buf_ok) ? kStored : ty;
 }
 
 // bits of one symbol under code lengths (llen, dlen)
@@ -523,24 +651,44 @@ ZHD void put_bits(uint64_t* words, uint64_t off, uint64_t val, int nbits) {
 #endif
 }
 
+// What the bit writer needs of a dynamic block's trees.
+struct TreeHdr {
+    uint16_t ldl[kLCodes + 2];   // literal/length code lengths (0..lmax)
+    uint16_t ddl[kDCodes + 2];   // distance code lengths (0..dmax)
+    uint16_t bcode[kBLCodes];    // bit-length tree codes (bit-reversed) and lengths
+    uint8_t blen[kBLCodes];
+    int16_t lmax, dmax, blmax;
+};
+
+ZHD void tree_hdr(TreeHdr& h, const TreeWork& w) {
+    for (int n = 0; n < kLCodes + 2; n++) h.ldl[n] = n <= w.lmax ? w.ldl[n] : 0;
+    for (int n = 0; n < kDCodes + 2; n++) h.ddl[n] = n <= w.dmax ? w.ddl[n] : 0;
+    for (int n = 0; n < kBLCodes; n++) {
+        h.bcode[n] = w.bfc[n];
+        h.blen[n] = (uint8_t)w.bdl[n];
+    }
+    h.lmax = (int16_t)w.lmax;
+    h.dmax = (int16_t)w.dmax;
+    h.blmax = (int16_t)w.blmax;
+}
+
 // send_all_trees: the dynamic block's tree description, returns the new offset
-ZHD uint64_t send_trees(uint64_t* out, uint64_t off, const TreeWork& w, const ZTab& t, const uint16_t* ldl,
-                        const uint16_t* ddl) {
-    const int lcodes = w.lmax + 1, dcodes = w.dmax + 1, blcodes = w.blmax + 1;
+ZHD uint64_t send_trees(uint64_t* out, uint64_t off, const TreeHdr& h, const ZTab& t) {
+    const int lcodes = h.lmax + 1, dcodes = h.dmax + 1, blcodes = h.blmax + 1;
     put_bits(out, off, (uint64_t)(lcodes - 257), 5); off += 5;
     put_bits(out, off, (uint64_t)(dcodes - 1), 5); off += 5;
     put_bits(out, off, (uint64_t)(blcodes - 4), 4); off += 4;
     for (int r = 0; r < blcodes; r++) {
-        put_bits(out, off, w.bdl[t.bl_order[r]], 3);
+        put_bits(out, off, h.blen[t.bl_order[r]], 3);
         off += 3;
     }
     auto code = [&](int c) {
-        put_bits(out, off, w.bfc[c], w.bdl[c]);
-        off += w.bdl[c];
+        put_bits(out, off, h.bcode[c], h.blen[c]);
+        off += h.blen[c];
     };
     for (int tree = 0; tree < 2; tree++) {
-        const uint16_t* dl = tree ? ddl : ldl;
-        const int max_code = tree ? w.dmax : w.lmax;
+        const uint16_t* dl = tree ? h.ddl : h.ldl;
+        const int max_code = tree ? h.dmax : h.lmax;
         int prevlen = -1, curlen, nextlen = dl[0], count = 0, max_count = 7, min_count = 4;
         if (nextlen == 0) max_count = 138, min_count = 3;
         for (int n = 0; n <= max_code; n++) {
@@ -572,6 +720,40 @@ ZHD uint64_t send_trees(uint64_t* out, uint64_t off, const TreeWork& w, const ZT
         }
     }
     return off;
+}
+
+// Everything the emitter needs of one block: type, codes, exact size in bits
+// (header included; a stored block's alignment depends on its offset and is
+// added by the layout pass).
+struct BlockCode {
+    TreeHdr h;
+    uint32_t lcl[kLCodes];  // (code << 8) | len
+    uint32_t dcl[kDCodes];
+    uint64_t bits;
+    int32_t type, pad;
+};
+
+// Finish a block after block_trees: codes and size.
+ZHD void block_code(BlockCode& bc, const TreeWork& w, const ZTab& t, int type, int64_t nbytes) {
+    bc.type = type;
+    if (type == kStored) {
+        bc.bits = 3 + 32 + 8 * (uint64_t)nbytes;  // + alignment
+        return;
+    }
+    uint64_t bits = 3;
+    if (type == kStatic) {
+        for (int n = 0; n < kLCodes; n++) bc.lcl[n] = ((uint32_t)t.s_lcode[n] << 8) | t.s_llen[n];
+        for (int n = 0; n < kDCodes; n++) bc.dcl[n] = ((uint32_t)t.s_dcode[n] << 8) | t.s_dlen[n];
+    } else {
+        tree_hdr(bc.h, w);
+        bits += dyn_header_bits(w, t);
+        for (int n = 0; n < kLCodes; n++) bc.lcl[n] = n <= w.lmax ? (((uint32_t)w.lfc[n] << 8) | w.ldl[n]) : 0;
+        for (int n = 0; n < kDCodes; n++) bc.dcl[n] = n <= w.dmax ? (((uint32_t)w.dfc[n] << 8) | w.ddl[n]) : 0;
+    }
+    for (int n = 0; n < kLCodes; n++)
+        bits += (uint64_t)w.lreal[n] * ((bc.lcl[n] & 0xff) + (n >= 257 ? t.xl[n - 257] : 0));
+    for (int n = 0; n < kDCodes; n++) bits += (uint64_t)w.dreal[n] * ((bc.dcl[n] & 0xff) + t.xd[n]);
+    bc.bits = bits;
 }
 
 // one symbol with codes (lcode/llen, dcode/dlen) at off

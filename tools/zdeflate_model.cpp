@@ -8,6 +8,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <random>
 #include <string>
@@ -38,6 +39,12 @@ static std::vector<uint8_t> model(const std::vector<uint8_t>& in, int* types = n
     auto pd = [&](int64_t i) { return (uint32_t)pdist[i]; };
     for (int64_t p = 0; p < n; p++) {
         rec[p] = match_search(p, n, win, pd);
+        if (n - p >= kMinMatch && pdist[p] && !nil_at_slide(p, n, pdist[p])) {  // the device form agrees
+            const int64_t wb = p > kWSize ? p - kWSize : 0;
+            const MatchRec r2 = match_search32(&in[wb], &pdist[wb], (int)(p - wb), (int)std::min<int64_t>(n - p, 1 << 20),
+                                               pdist[p]);
+            if (r2.r128 != rec[p].r128 || r2.r32 != rec[p].r32) { printf("match_search32 differs at %lld\n", (long long)p); abort(); }
+        }
         if (p + 2 < n && nil_at_slide(p, n, pdist[p])) g_nil_hits++;
     }
     // parse
@@ -68,7 +75,10 @@ static std::vector<uint8_t> model(const std::vector<uint8_t>& in, int* types = n
         w.lfc[kEndBlock] = 1;
         const int type = block_trees(w, t, b.nbytes, (b.flags & 2) != 0);
         if (types) types[type]++;
+        static BlockCode bc;
+        block_code(bc, w, t, type, b.nbytes);
         const int last = b.flags & 1;
+        const uint64_t start = off;
         if (type == kStored) {
             put_bits(out.data(), off, (uint64_t)((0 << 1) + last), 3);
             off += 3;
@@ -83,22 +93,146 @@ static std::vector<uint8_t> model(const std::vector<uint8_t>& in, int* types = n
         }
         put_bits(out.data(), off, (uint64_t)(((type == kStatic ? 1 : 2) << 1) + last), 3);
         off += 3;
-        if (type == kStatic) {
-            auto lco = [&](int c) { return ((uint32_t)t.s_lcode[c] << 8) | t.s_llen[c]; };
-            auto dco = [&](int c) { return ((uint32_t)t.s_dcode[c] << 8) | t.s_dlen[c]; };
-            for (int32_t i = 0; i < b.nsym; i++) off += put_sym(out.data(), off, t, syms[b.sym0 + i], lco, dco);
-            const uint32_t e = lco(kEndBlock);
-            put_bits(out.data(), off, e >> 8, e & 0xff);
-            off += e & 0xff;
+        if (type == kDynamic) off = send_trees(out.data(), off, bc.h, t);
+        auto lco = [&](int c) { return bc.lcl[c]; };
+        auto dco = [&](int c) { return bc.dcl[c]; };
+        for (int32_t i = 0; i < b.nsym; i++) off += put_sym(out.data(), off, t, syms[b.sym0 + i], lco, dco);
+        const uint32_t e = lco(kEndBlock);
+        put_bits(out.data(), off, e >> 8, e & 0xff);
+        off += e & 0xff;
+        if (off - start != bc.bits) { printf("block size mismatch %llu vs %llu\n", (unsigned long long)(off - start), (unsigned long long)bc.bits); abort(); }
+    }
+    const uint8_t* ob = reinterpret_cast<const uint8_t*>(out.data());
+    return std::vector<uint8_t>(ob, ob + (off + 7) / 8);
+}
+
+// The device pipeline's decomposition: speculative per-segment parses from a
+// canonical state, a per-stream fix-up pass that re-parses from each true entry
+// state until it meets a canonical loop top of the speculative parse, blocks cut
+// from the finished symbol stream, stored decisions in the layout pass.
+static int g_fix_iters = 0, g_nosync = 0;
+static std::vector<uint8_t> model_seg(const std::vector<uint8_t>& in, int64_t G) {
+    const int64_t n = (int64_t)in.size();
+    ZTab t;
+    ztab_fill(t);
+    std::vector<uint16_t> pdist(n + 1, 0);
+    std::vector<int64_t> head(1 << 15, -1);
+    for (int64_t p = 0; p + 2 < n; p++) {
+        const uint32_t h = hash3(&in[p]);
+        const int64_t q = head[h];
+        pdist[p] = (q > 0 && p - q <= kMaxDist) ? (uint16_t)(p - q) : 0;
+        head[h] = p;
+    }
+    std::vector<MatchRec> rec(n + 1);
+    for (int64_t p = 0; p < n; p++) {
+        rec[p] = MatchRec{0, 0};
+        if (n - p >= kMinMatch && pdist[p] && !nil_at_slide(p, n, pdist[p])) {
+            const int64_t wb = p > kWSize ? p - kWSize : 0;
+            rec[p] = match_search32(&in[wb], &pdist[wb], (int)(p - wb), (int)std::min<int64_t>(n - p, 1 << 20), pdist[p]);
+        }
+    }
+    auto rc = [&](int64_t p) { return rec[p]; };
+    auto by = [&](int64_t p) { return in[p]; };
+    const int64_t nseg = std::max<int64_t>(1, (n + G - 1) / G);
+    std::vector<std::vector<uint32_t>> spec(nseg), fix(nseg);
+    std::vector<ParseState> sexit(nseg);
+    std::vector<uint8_t> canon(n + 1, 0);
+    for (int64_t k = 0; k < nseg; k++) {  // speculative parses (independent)
+        const int64_t g0 = k * G, g1 = std::min(n, g0 + G);
+        const bool last = k == nseg - 1;
+        ParseState st;
+        parse_init(st, g0);
+        if (g0 < n) canon[g0] = 1;
+        auto em = [&](uint32_t v) { spec[k].push_back(v); };
+        while (st.s < g1) {
+            if (!parse_iter(st, n, rc, by, em)) break;
+            if (st.s < g1) canon[st.s] = (uint8_t)sync_code(st);
+        }
+        if (last) while (parse_iter(st, n, rc, by, em)) {}
+        sexit[k] = st;
+    }
+    std::vector<int64_t> skip(nseg, 0);
+    ParseState cur = sexit[0];
+    for (int64_t k = 1; k < nseg; k++) {  // fix-up, sequential per stream
+        const int64_t g0 = k * G, g1 = std::min(n, g0 + G);
+        const bool last = k == nseg - 1;
+        ParseState st = cur;
+        auto em = [&](uint32_t v) { fix[k].push_back(v); };
+        auto synced = [&]() { const int c = sync_code(st); return c != 0 && st.s < g1 && canon[st.s] == c; };
+        bool sync = synced();
+        while (!sync && st.s < g1) {
+            g_fix_iters++;
+            if (!parse_iter(st, n, rc, by, em)) break;
+            sync = synced();
+        }
+        if (sync) {
+            const int64_t target = st.s - st.avail;  // a pending literal is not emitted yet
+            int64_t cov = g0, i = 0;
+            while (cov < target) cov += sym_cover(spec[k][i++]);
+            if (cov != target) { printf("sync point off a symbol boundary\n"); abort(); }
+            skip[k] = i;
+            cur = sexit[k];
         } else {
-            off = send_trees(out.data(), off, w, t, w.ldl, w.ddl);
-            auto lco = [&](int c) { return ((uint32_t)w.lfc[c] << 8) | w.ldl[c]; };
-            auto dco = [&](int c) { return ((uint32_t)w.dfc[c] << 8) | w.ddl[c]; };
-            for (int32_t i = 0; i < b.nsym; i++) off += put_sym(out.data(), off, t, syms[b.sym0 + i], lco, dco);
+            g_nosync++;
+            skip[k] = (int64_t)spec[k].size();
+            if (last) while (parse_iter(st, n, rc, by, em)) {}
+            cur = st;
+        }
+    }
+    std::vector<uint32_t> syms;
+    for (int64_t k = 0; k < nseg; k++) {
+        syms.insert(syms.end(), fix[k].begin(), fix[k].end());
+        syms.insert(syms.end(), spec[k].begin() + skip[k], spec[k].end());
+    }
+    const int64_t nsym = (int64_t)syms.size();
+    const int64_t nblk = (nsym - cur.final_lit) / kBlockSyms + 1;
+    std::vector<uint64_t> out((compress_bound(n) + 7) / 8 + 2, 0);
+    uint64_t off = 0;
+    int64_t byte0 = 0;
+    static TreeWork w;
+    static BlockCode bc;
+    for (int64_t b = 0; b < nblk; b++) {
+        const int64_t j0 = b * kBlockSyms, j1 = b == nblk - 1 ? nsym : j0 + kBlockSyms;
+        for (int i = 0; i < kHeapSize; i++) w.lfc[i] = w.ldl[i] = 0;
+        for (int i = 0; i < 2 * kDCodes + 1; i++) w.dfc[i] = w.ddl[i] = 0;
+        for (int i = 0; i < 2 * kBLCodes + 1; i++) w.bfc[i] = w.bdl[i] = 0;
+        int64_t nbytes = 0;
+        for (int64_t i = j0; i < j1; i++) {
+            const uint32_t v = syms[i], dist = v >> 8, lc = v & 0xff;
+            nbytes += sym_cover(v);
+            if (dist == 0) w.lfc[lc]++;
+            else { w.lfc[t.lcode[lc] + 257]++; w.dfc[d_code(t, dist - 1)]++; }
+        }
+        w.lfc[kEndBlock] = 1;
+        uint64_t opt_lenb;
+        const int ty = block_trees_ns(w, t, opt_lenb);
+        block_code(bc, w, t, ty, nbytes);
+        const bool last = b == nblk - 1;
+        const int64_t end = byte0 + nbytes;
+        const int64_t top = last ? n : (syms[j1 - 1] >> 8 ? end - sym_cover(syms[j1 - 1]) + 1 : end);
+        const bool buf_ok = byte0 >= (int64_t)kWSize * slides_at(top, n);
+        const int type = take_stored(nbytes, opt_lenb, buf_ok) ? kStored : ty;
+        if (type == kStored) {
+            put_bits(out.data(), off, (uint64_t)last, 3);
+            off = (off + 3 + 7) & ~(uint64_t)7;
+            uint8_t* ob = reinterpret_cast<uint8_t*>(out.data());
+            const uint16_t len = (uint16_t)nbytes, nlen = (uint16_t)~len;
+            ob[off / 8] = len & 0xff; ob[off / 8 + 1] = len >> 8;
+            ob[off / 8 + 2] = nlen & 0xff; ob[off / 8 + 3] = nlen >> 8;
+            memcpy(ob + off / 8 + 4, &in[byte0], nbytes);
+            off += 32 + 8 * (uint64_t)nbytes;
+        } else {
+            put_bits(out.data(), off, (uint64_t)((type << 1) + last), 3);
+            off += 3;
+            if (type == kDynamic) off = send_trees(out.data(), off, bc.h, t);
+            auto lco = [&](int c) { return bc.lcl[c]; };
+            auto dco = [&](int c) { return bc.dcl[c]; };
+            for (int64_t i = j0; i < j1; i++) off += put_sym(out.data(), off, t, syms[i], lco, dco);
             const uint32_t e = lco(kEndBlock);
             put_bits(out.data(), off, e >> 8, e & 0xff);
             off += e & 0xff;
         }
+        byte0 = end;
     }
     const uint8_t* ob = reinterpret_cast<const uint8_t*>(out.data());
     return std::vector<uint8_t>(ob, ob + (off + 7) / 8);
@@ -114,6 +248,14 @@ static std::vector<uint8_t> zref(const std::vector<uint8_t>& in) {
 static int check(const char* name, const std::vector<uint8_t>& in) {
     int types[3] = {0, 0, 0};
     const auto a = model(in, types), b = zref(in);
+    std::vector<int64_t> gs = {16384, 4096, 997};
+    if (getenv("ZD_G")) gs = {atoll(getenv("ZD_G"))};
+    for (int64_t G : gs) {
+        if (model_seg(in, G) != b) {
+            printf("%s: segmented pipeline (G=%lld) differs\n", name, (long long)G);
+            return 1;
+        }
+    }
     size_t i = 0;
     while (i < a.size() && i < b.size() && a[i] == b[i]) i++;
     const bool ok = a == b;
@@ -136,6 +278,7 @@ int main(int argc, char** argv) {
             fclose(f);
             bad += check(argv[i], d);
         }
+        printf("segmented parse: %d fix-up iterations, %d segments without sync\n", g_fix_iters, g_nosync);
         return bad;
     }
     std::mt19937_64 rng(1234);
@@ -205,6 +348,7 @@ int main(int argc, char** argv) {
         v.resize(target);
         bad += check(("fuzz " + std::to_string(f)).c_str(), v);
     }
+    printf("segmented parse: %d fix-up iterations, %d segments without sync\n", g_fix_iters, g_nosync);
     printf("%s\n", bad ? "FAILURES" : "all identical");
     return bad;
 }
