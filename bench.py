@@ -772,8 +772,10 @@ def run_direct(cfg, eng, cams, views, clusters, stream, steps=10):
 def run_encoder(cfg, dev, cluster_bufs, stream, ticks=2):
     """The encoder hand-off: FVT1 records of every
     tile of every cluster frame of the rig frame (server/pipeline.py:294-318),
-    transform stage on the device (encoder.RigEncoder), DEFLATE on the host
-    threads.  gop 30 (PipelineConfig default): tick 0 is intra, the rest P."""
+    transform stage and DEFLATE (zlib-identical, deflate_kernels.cu) on the
+    device (encoder.RigEncoder), record framing on the host.  gop 30
+    (PipelineConfig default): tick 0 is intra, the rest P.  One tick is also
+    timed with DEFLATE on the host thread pool (the previous design)."""
     import time
 
     import torch
@@ -789,8 +791,10 @@ def run_encoder(cfg, dev, cluster_bufs, stream, ticks=2):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         nbytes = 0
+        recs0 = None
         for k in range(ticks):
             recs = enc.encode(cluster_bufs[(k + 1) % len(cluster_bufs)])
+            recs0 = recs if recs0 is None else recs0
             nbytes += sum(len(r) for c in recs for r in c)
         wall = (time.perf_counter() - t0) / ticks
         # device transform stage alone (blocks + tokens kernels), CUDA events
@@ -806,13 +810,35 @@ def run_encoder(cfg, dev, cluster_bufs, stream, ticks=2):
                                            ctypes.c_void_p(enc.ntok.data_ptr()), ctypes.c_void_p(stream.cuda_stream)))
         b.record(stream)
         torch.cuda.synchronize()
-    dev_ms = a.elapsed_time(b) / ticks
+        dev_ms_blocks = a.elapsed_time(b) / ticks
+        # device DEFLATE alone (all plane token streams of the last tick), CUDA events
+        from paper_2112_10603_b200.deflate import deflate_streams
+        po = enc._last_plane_offs
+        tok = enc.tokens[:po[-1]]
+        a.record(stream)
+        for _ in range(ticks):
+            deflate_streams(tok, po, stream=stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        zd_ms = a.elapsed_time(b) / ticks
+        # the previous design: DEFLATE with zlib on the host threads (one P tick)
+        enc_h = RigEncoder(build_layouts(ViewIndexModel(C, S), vps), W, H, fmt, quality=75, gop=30, device=dev,
+                           threads=threads, deflate="host")
+        enc_h.encode(cluster_bufs[0])
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        recs_h = enc_h.encode(cluster_bufs[1 % len(cluster_bufs)])
+        host_ms = (time.perf_counter() - t0) * 1e3
+    dev_ms = dev_ms_blocks
     tiles = sum(len(t) for t in enc.tiles)
     return {"path": "FVT1 tile records (codec.TileEncoder-identical bytes) of every tile of the rig frame's "
-                    "cluster frames: 8x8 DCT / quant / reconstruction / zigzag / tokens on the device, "
-                    "DEFLATE on %d host threads" % threads,
+                    "cluster frames: 8x8 DCT / quant / reconstruction / zigzag / tokens and DEFLATE "
+                    "(zlib level 6, byte-identical) on the device, record framing on the host",
             "tiles_per_rig_frame": tiles, "quality": 75, "gop": 30, "record": "P (closed loop, device-resident "
             "reconstruction)", "ms_per_rig_frame": wall * 1e3, "device_transform_ms": dev_ms,
+            "device_deflate_ms": zd_ms, "token_bytes_per_rig_frame": int(po[-1]),
+            "host_deflate_ms_per_rig_frame": host_ms, "host_deflate_threads": threads,
+            "records_identical_device_vs_host_zlib": recs_h == recs0,
             "bytes_per_rig_frame": nbytes / ticks,
             "parity": "byte-identical records vs reference-generated goldens, lossy I/P and lossless "
                       "(tests/test_gpu_encoder.py)"}

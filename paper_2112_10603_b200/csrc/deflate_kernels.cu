@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(256) k_zd_chain(const uint8_t* __restrict__ da
     }
 }
 
-__global__ void __launch_bounds__(256) k_zd_match(const uint8_t* __restrict__ data, const ZStream* __restrict__ zs,
+__global__ void __launch_bounds__(512) k_zd_match(const uint8_t* __restrict__ data, const ZStream* __restrict__ zs,
                                                   const ZChunk* __restrict__ ch, const uint16_t* __restrict__ pdist,
                                                   uint2* __restrict__ rec) {
     extern __shared__ __align__(16) uint8_t zsm[];
@@ -178,6 +178,7 @@ __global__ void __launch_bounds__(256) k_zd_match(const uint8_t* __restrict__ da
     for (int64_t i = threadIdx.x; i < pe - wb; i += blockDim.x) sp[i] = pg[wb + i];
     for (int64_t i = threadIdx.x; i < we - wb; i += blockDim.x) sb[i] = d[wb + i];
     __syncthreads();
+    uint2* out = rec + sd.in_off;
     for (int64_t p = c0 + threadIdx.x; p < c1; p += blockDim.x) {
         MatchRec r{0u, 0u};
         const int64_t la = n - p;
@@ -187,7 +188,7 @@ __global__ void __launch_bounds__(256) k_zd_match(const uint8_t* __restrict__ da
             if (pd0 && !nil_at_slide(p, n, (uint32_t)pd0))
                 r = match_search32(sb, sp, P, (int)min(la, (int64_t)(1 << 20)), pd0);
         }
-        rec[sd.in_off + p] = make_uint2(r.r128, r.r32);
+        out[p] = make_uint2(r.r128, r.r32);
     }
 }
 
@@ -576,7 +577,7 @@ cudaError_t zd_deflate(const uint8_t* data, const int64_t* in_off, int S, uint8_
     uint64_t* boff = reinterpret_cast<uint64_t*>(sc + p.boff);
     if (p.C1) k_zd_chain<<<p.C1, 256, kChainSmem, st>>>(data, dzs, reinterpret_cast<const ZChunk*>(sc + p.ch1), pdist);
     if (p.C2)
-        k_zd_match<<<p.C2, 256, kMatchSmem, st>>>(data, dzs, reinterpret_cast<const ZChunk*>(sc + p.ch2), pdist, rec);
+        k_zd_match<<<p.C2, 512, kMatchSmem, st>>>(data, dzs, reinterpret_cast<const ZChunk*>(sc + p.ch2), pdist, rec);
     k_zd_spec<<<p.G, 32, 0, st>>>(data, dzs, dsg, rec, canon, spec, sexit);
     k_zd_fix<<<(S + 127) / 128, 128, 0, st>>>(data, dzs, S, dsg, rec, canon, spec, fix, sexit, sfix, ssyms);
     k_zd_compact<<<p.G, 256, 0, st>>>(dzs, dsg, spec, fix, sexit, sfix, syms);

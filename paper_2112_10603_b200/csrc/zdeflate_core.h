@@ -212,40 +212,88 @@ ZHD uint32_t finish_rec32(int best, int dist) {
     if (best <= 2 || (best == kMinMatch && dist > kTooFar)) return 0;
     return ((uint32_t)best << 16) | (uint32_t)dist;
 }
+// 4 bytes at byte offset i (little endian) of a 4-byte aligned buffer with 8
+// bytes of readable padding past its end
+ZHD uint32_t ld32u(const uint8_t* b, int i) {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(b + (i & ~3));
+    const int sh = (i & 3) * 8;
+#ifdef __CUDA_ARCH__
+    return __funnelshift_r(w[0], w[1], sh);
+#else
+    return (uint32_t)((((uint64_t)w[1] << 32) | w[0]) >> sh);
+#endif
+}
+
+ZHD int ctz32(uint32_t x) {
+#ifdef __CUDA_ARCH__
+    return __ffs((int)x) - 1;
+#else
+    return __builtin_ctz(x);
+#endif
+}
+
+// Every candidate's match length from a branch-free 8-byte compare (scan words
+// cached), the continuation loop only for candidates matching 8+ bytes.  zlib's
+// quick rejection (bytes best-1, best, 0, 1) only skips candidates that cannot
+// beat best, so measuring them changes nothing: the running best, the first
+// (nearest) candidate reaching it, the nice cut and the 32 / 128 chain limits
+// are longest_match's and the result equals match_search's.  (A filter that
+// passes ~7 % of the candidates keeps most of a warp idle while a few lanes
+// measure; measuring all keeps the lanes together.)
 ZHD MatchRec match_search32(const uint8_t* sb, const uint16_t* sp, int P, int la, int pd0) {
     MatchRec r{0, 0};
     const int nice = la < kNiceLength ? la : kNiceLength;
     const int maxlen = la < kMaxMatch ? la : kMaxMatch;
     const int lim = P - kMaxDist;  // later candidates must lie above (distance < MAX_DIST)
-    const int s0 = sb[P], s1 = sb[P + 1];
-    int e1 = s1, e0 = sb[P + 2];   // scan[best - 1], scan[best]
+    const uint32_t p0 = ld32u(sb, P), p1 = ld32u(sb, P + 4);
     int best = 2, bc = P, cnt = 0, c = P - pd0;
-    bool have32 = false;
-    for (;;) {
-        cnt++;
-        if (sb[c + best] == e0 && sb[c + best - 1] == e1 && sb[c] == s0 && sb[c + 1] == s1) {
-            int len = 3;
-            while (len < maxlen && sb[c + len] == sb[P + len]) len++;
+    uint32_t pb = 0;  // scan bytes best-3 .. best once best >= 8
+    bool done = false;
+    for (int phase = 0; phase < 2 && !done; phase++) {
+        const int stop = phase ? kMaxChain : (kMaxChain >> 2);
+        while (cnt < stop) {
+            cnt++;
+            const int d = sp[c];
+            uint32_t x0, x1;
+            {  // 8 bytes at c from three aligned words
+                const uint32_t* w = reinterpret_cast<const uint32_t*>(sb + (c & ~3));
+                const int sh = (c & 3) * 8;
+                const uint32_t w0 = w[0], w1 = w[1], w2 = w[2];
+#ifdef __CUDA_ARCH__
+                x0 = __funnelshift_r(w0, w1, sh) ^ p0;
+                x1 = __funnelshift_r(w1, w2, sh) ^ p1;
+#else
+                x0 = (uint32_t)((((uint64_t)w1 << 32) | w0) >> sh) ^ p0;
+                x1 = (uint32_t)((((uint64_t)w2 << 32) | w1) >> sh) ^ p1;
+#endif
+            }
+            int len;
+            if (x0) {
+                len = ctz32(x0) >> 3;
+            } else if (x1) {
+                len = 4 + (ctz32(x1) >> 3);
+            } else if (best >= 8 && ld32u(sb, c + best - 3) != pb) {
+                len = 8;  // differs within bytes best-3 .. best: cannot beat best
+            } else {
+                len = 8;
+                uint32_t x = 0;
+                while (len < maxlen && (x = ld32u(sb, c + len) ^ ld32u(sb, P + len)) == 0) len += 4;
+                if (x) len += ctz32(x) >> 3;
+            }
+            if (len > maxlen) len = maxlen;
             if (len > best) {
                 best = len;
                 bc = c;
-                if (len >= nice) break;
-                e1 = sb[P + best - 1];
-                e0 = sb[P + best];
+                if (len >= nice) { done = true; break; }
+                if (best >= 8) pb = ld32u(sb, P + best - 3);
             }
+            if (d == 0) { done = true; break; }
+            c -= d;
+            if (c <= lim) { done = true; break; }
         }
-        if (cnt == kMaxChain >> 2) {
-            r.r32 = finish_rec32(best, P - bc);
-            have32 = true;
-        }
-        if (cnt == kMaxChain) break;
-        const int d = sp[c];
-        if (d == 0) break;
-        c -= d;
-        if (c <= lim) break;
+        if (phase == 0) r.r32 = finish_rec32(best, P - bc);
     }
     r.r128 = finish_rec32(best, P - bc);
-    if (!have32) r.r32 = r.r128;
     return r;
 }
 

@@ -7,10 +7,13 @@ codec.py:138-216, dct.py): per plane, 8x8 blocks -> DCT -> rint(c / step) ->
 zigzag -> (run, level) tokens -> DEFLATE, closed loop on the reconstruction.
 Here the blocks, transform, quantisation, reconstruction (kept on the device
 for the next P record), zigzag and token stream run in
-csrc/encode_kernels.cu over every (tile, plane) of a rig frame in one batch;
-the host runs only DEFLATE (zlib level 6, one thread per plane) and frames
-the records.  Records are byte-identical to codec.TileEncoder's
-(tests/test_gpu_encoder.py against reference-generated goldens).
+csrc/encode_kernels.cu over every (tile, plane) of a rig frame in one batch,
+and so does DEFLATE: csrc/deflate_kernels.cu compresses every plane's token
+stream at once, byte-identical to zlib.compress(tokens, 6) (deflate.py).  The
+host only frames the records.  Records are byte-identical to
+codec.TileEncoder's (tests/test_gpu_encoder.py against reference-generated
+goldens).  deflate="host" runs zlib on a host thread pool instead (the
+previous design, kept for timing comparisons).
 
     enc = RigEncoder(layouts, 1920, 1080, PixelFormat.YUV420, quality=75, gop=30)
     records = enc.encode(clusters, sizes)   # per cluster: [FrameRecord bytes per tile]
@@ -116,12 +119,15 @@ class RigEncoder:
     GOP as PipelineConfig.quality / .gop."""
 
     def __init__(self, layouts, width: int, height: int, fmt, quality: int = 75, gop: int = 30, device=None,
-                 threads: int = 8):
+                 threads: int = 8, deflate: str = "device"):
         import torch
         self._L = _lib.require_cuda()
         _sig(self._L)
         if gop < 1:
             raise ValueError("gop must be >= 1")
+        if deflate not in ("device", "host"):
+            raise ValueError("deflate must be 'device' or 'host'")
+        self.deflate = deflate
         self.step = quant_step(quality)
         self.quality, self.gop, self.lossless = int(quality), int(gop), quality == 100
         self.width, self.height, self.format = int(width), int(height), PixelFormat(int(fmt))
@@ -186,15 +192,24 @@ class RigEncoder:
                                        block0, ctypes.c_void_p(self.tokens.data_ptr()), st))
         offs = self.tok_off[:block0 + 1].cpu().numpy()
         ntot = int(offs[-1])
-        tok = self.tokens[:ntot * 3].cpu().numpy().tobytes()
         for tl in self.tiles:
             for _, t in tl:
                 t.index += 1
+        if self.deflate == "device":  # raw DEFLATE of every plane's tokens at once (codec.py:148)
+            from .deflate import deflate_streams
+            plane_offs = [int(offs[m[3]]) * 3 for m in meta] + [ntot * 3]
+            self._last_plane_offs = plane_offs
+            out, out_off = deflate_streams(self.tokens[:ntot * 3], plane_offs)
+            oo = out_off.cpu().numpy()
+            raw = out[:int(oo[-1])].cpu().numpy().tobytes()
+            datas = [raw[oo[i]:oo[i + 1]] for i in range(len(meta))]
+        else:
+            tok = self.tokens[:ntot * 3].cpu().numpy().tobytes()
 
-        def deflate(m):
-            _, _, _, b0, nb = m
-            return zlib.compress(tok[offs[b0] * 3:offs[b0 + nb] * 3], 6)[2:-4]  # raw DEFLATE (codec.py:148)
-        datas = list(self._pool.map(deflate, meta))
+            def deflate(m):
+                _, _, _, b0, nb = m
+                return zlib.compress(tok[offs[b0] * 3:offs[b0 + nb] * 3], 6)[2:-4]  # raw DEFLATE (codec.py:148)
+            datas = list(self._pool.map(deflate, meta))
         out = [[None] * len(tl) for tl in self.tiles]
         parts = {}
         for m, d in zip(meta, datas):

@@ -35,13 +35,16 @@ static std::vector<uint8_t> model(const std::vector<uint8_t>& in, int* types = n
     }
     // searches
     std::vector<MatchRec> rec(n + 1);
+    std::vector<uint32_t> pw((n + 16) / 4 + 4, 0);  // 4-byte aligned copy with padding (match_search32)
+    uint8_t* padded = reinterpret_cast<uint8_t*>(pw.data());
+    memcpy(padded, in.data(), n);
     auto win = [&](int64_t i) { return in[i]; };
     auto pd = [&](int64_t i) { return (uint32_t)pdist[i]; };
     for (int64_t p = 0; p < n; p++) {
         rec[p] = match_search(p, n, win, pd);
         if (n - p >= kMinMatch && pdist[p] && !nil_at_slide(p, n, pdist[p])) {  // the device form agrees
-            const int64_t wb = p > kWSize ? p - kWSize : 0;
-            const MatchRec r2 = match_search32(&in[wb], &pdist[wb], (int)(p - wb), (int)std::min<int64_t>(n - p, 1 << 20),
+            const int64_t wb = (p > kWSize ? p - kWSize : 0) & ~(int64_t)3;
+            const MatchRec r2 = match_search32(&padded[wb], &pdist[wb], (int)(p - wb), (int)std::min<int64_t>(n - p, 1 << 20),
                                                pdist[p]);
             if (r2.r128 != rec[p].r128 || r2.r32 != rec[p].r32) { printf("match_search32 differs at %lld\n", (long long)p); abort(); }
         }
@@ -124,11 +127,14 @@ static std::vector<uint8_t> model_seg(const std::vector<uint8_t>& in, int64_t G)
         head[h] = p;
     }
     std::vector<MatchRec> rec(n + 1);
+    std::vector<uint32_t> pw((n + 16) / 4 + 4, 0);
+    uint8_t* padded = reinterpret_cast<uint8_t*>(pw.data());
+    memcpy(padded, in.data(), n);
     for (int64_t p = 0; p < n; p++) {
         rec[p] = MatchRec{0, 0};
         if (n - p >= kMinMatch && pdist[p] && !nil_at_slide(p, n, pdist[p])) {
-            const int64_t wb = p > kWSize ? p - kWSize : 0;
-            rec[p] = match_search32(&in[wb], &pdist[wb], (int)(p - wb), (int)std::min<int64_t>(n - p, 1 << 20), pdist[p]);
+            const int64_t wb = (p > kWSize ? p - kWSize : 0) & ~(int64_t)3;
+            rec[p] = match_search32(&padded[wb], &pdist[wb], (int)(p - wb), (int)std::min<int64_t>(n - p, 1 << 20), pdist[p]);
         }
     }
     auto rc = [&](int64_t p) { return rec[p]; };
