@@ -190,20 +190,30 @@ class RigEncoder:
         torch.cumsum(self.ntok[:block0], 0, out=self.tok_off[1:block0 + 1])
         _lib.check(L.fvv_encode_tokens(ctypes.c_void_p(self.zz.data_ptr()), ctypes.c_void_p(self.tok_off.data_ptr()),
                                        block0, ctypes.c_void_p(self.tokens.data_ptr()), st))
-        offs = self.tok_off[:block0 + 1].cpu().numpy()
-        ntot = int(offs[-1])
         for tl in self.tiles:
             for _, t in tl:
                 t.index += 1
         if self.deflate == "device":  # raw DEFLATE of every plane's tokens at once (codec.py:148)
             from .deflate import deflate_streams
-            plane_offs = [int(offs[m[3]]) * 3 for m in meta] + [ntot * 3]
+            # token offsets at the plane boundaries only (not every block's)
+            if getattr(self, "_plane_idx", None) is None or self._plane_idx.numel() != len(meta) + 1:
+                self._plane_idx = torch.tensor([m[3] for m in meta] + [block0], dtype=torch.int64,
+                                               device=self.device)
+            po = (self.tok_off.index_select(0, self._plane_idx) * 3).cpu().numpy()
+            plane_offs = [int(v) for v in po]
             self._last_plane_offs = plane_offs
-            out, out_off = deflate_streams(self.tokens[:ntot * 3], plane_offs)
+            out, out_off = deflate_streams(self.tokens[:plane_offs[-1]], plane_offs)
             oo = out_off.cpu().numpy()
-            raw = out[:int(oo[-1])].cpu().numpy().tobytes()
+            nraw = int(oo[-1])
+            if getattr(self, "_pinned", None) is None or self._pinned.numel() < nraw:
+                self._pinned = torch.empty(max(nraw, 1 << 20), dtype=torch.uint8, pin_memory=True)
+            self._pinned[:nraw].copy_(out[:nraw], non_blocking=True)
+            torch.cuda.current_stream(self.device).synchronize()
+            raw = self._pinned[:nraw].numpy().tobytes()
             datas = [raw[oo[i]:oo[i + 1]] for i in range(len(meta))]
         else:
+            offs = self.tok_off[:block0 + 1].cpu().numpy()
+            ntot = int(offs[-1])
             tok = self.tokens[:ntot * 3].cpu().numpy().tobytes()
 
             def deflate(m):
