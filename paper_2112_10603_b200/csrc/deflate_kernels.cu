@@ -3,7 +3,7 @@
 // codec.py:148; algorithm and its zlib 1.3 provenance in zdeflate_core.h).
 //
 // Pipeline (one launch each, all streams of the batch together):
-//   k_zd_chain   per 8K-position chunk: hash-chain links (distance to the newest
+//   k_zd_chain   per 16K-position chunk: hash-chain links (distance to the newest
 //                earlier same-hash position), window heads by shared-memory
 //                atomicMax, then the chunk in position order by one warp with
 //                __match_any_sync resolving same-hash lanes
@@ -37,12 +37,12 @@ using namespace zd;
 
 namespace {
 
-constexpr int kCH1 = 8192;    // chain chunk (positions)
+constexpr int kCH1 = 16384;   // chain chunk (positions)
 constexpr int kCH2 = 4096;    // search chunk (positions)
 constexpr int kSeg = 16384;   // speculative parse segment (positions)
 constexpr int kSegPad = 260;  // symbols a segment's parse may run past its end
 constexpr int kPW = 2048;     // parse window (records staged per refill)
-constexpr size_t kChainSmem = 4 * 32768 + 2 * kCH1;
+constexpr size_t kChainSmem = 4 * 32768 + 2 * kCH1 + 2 * kCH1 + 64;
 constexpr size_t kMatchSmem = 2 * (size_t)(kWSize + kCH2) + (kWSize + kCH2 + kMaxMatch + 8);
 
 struct ZStream {
@@ -121,35 +121,108 @@ Plan make_plan(const int64_t* len, int S) {
     return p;
 }
 
+// Links are only ordered among positions of the same hash, so the chunk is
+// split by hash into 8 groups (h & 7), each a position-ordered list walked by
+// its own warp: 8 independent serial walks instead of one.
 __global__ void __launch_bounds__(256) k_zd_chain(const uint8_t* __restrict__ data, const ZStream* __restrict__ zs,
                                                   const ZChunk* __restrict__ ch, uint16_t* __restrict__ pdist) {
     extern __shared__ __align__(16) uint8_t zsm[];
-    uint32_t* head = reinterpret_cast<uint32_t*>(zsm);           // 32768 hash heads (0: none)
-    uint16_t* hs = reinterpret_cast<uint16_t*>(zsm + 4 * 32768);  // hashes of the chunk
+    uint32_t* head = reinterpret_cast<uint32_t*>(zsm);                    // 32768 hash heads (0: none)
+    uint16_t* hs = reinterpret_cast<uint16_t*>(zsm + 4 * 32768);           // hashes of the chunk
+    uint16_t* lst = reinterpret_cast<uint16_t*>(zsm + 4 * 32768 + 2 * kCH1);  // chunk offsets grouped by h & 7
+    int* gcount = reinterpret_cast<int*>(zsm + 4 * 32768 + 4 * kCH1);        // [8] group sizes, then starts
     const ZChunk ck = ch[blockIdx.x];
     const ZStream sd = zs[ck.s];
     const uint8_t* d = data + sd.in_off;
     const int64_t n = sd.n, c0 = ck.c0;
     const int64_t c1 = min(c0 + (int64_t)kCH1, n - 2);  // positions <= n - 3 carry a hash
+    const int cn = (int)(c1 - c0);
     const int64_t base = c0 - kMaxDist - 1;                // head values: position - base (>= 1)
-    for (int i = threadIdx.x; i < 32768; i += blockDim.x) head[i] = 0;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    for (int i = tid; i < 32768; i += blockDim.x) head[i] = 0;
+    if (tid < 16) gcount[tid] = 0;
     __syncthreads();
     // newest position of each hash within MAX_DIST before the chunk (position 0 is NIL)
-    for (int64_t q = max((int64_t)1, c0 - kMaxDist) + threadIdx.x; q < c0; q += blockDim.x)
+    for (int64_t q = max((int64_t)1, c0 - kMaxDist) + tid; q < c0; q += blockDim.x)
         atomicMax(&head[hash3(d + q)], (uint32_t)(q - base));
-    for (int64_t i = threadIdx.x; i < c1 - c0; i += blockDim.x) hs[i] = (uint16_t)hash3(d + c0 + i);
+    // thread t hashes chunk offsets [32 t, 32 t + 32) and counts them per group
+    int cnt[8];
+#pragma unroll
+    for (int g = 0; g < 8; g++) cnt[g] = 0;
+    const int i0 = tid * (kCH1 / 256);
+    for (int k = 0; k < kCH1 / 256; k++) {
+        const int i = i0 + k;
+        if (i < cn) {
+            const uint32_t h = hash3(d + c0 + i);
+            hs[i] = (uint16_t)h;
+#pragma unroll
+            for (int g = 0; g < 8; g++) cnt[g] += (int)((h & 7) == (uint32_t)g);
+        }
+    }
+    // exclusive scan of the per-thread counts, per group (thread order = position order)
+    int off[8];
+#pragma unroll
+    for (int g = 0; g < 8; g++) {
+        int v = cnt[g];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += u;
+        }
+        off[g] = v - cnt[g];  // within the warp
+    }
+    __shared__ int wtot[8][8];  // [warp][group]
+#pragma unroll
+    for (int g = 0; g < 8; g++)
+        if (lane == 31) wtot[wid][g] = off[g] + cnt[g];
     __syncthreads();
-    if (threadIdx.x >= 32) return;
-    const int lane = threadIdx.x;
-    for (int64_t b = c0; b < c1; b += 32) {
-        const int64_t p = b + lane;
-        const bool act = p < c1;
-        const uint32_t h = act ? hs[p - c0] : (0x8000u | lane);
+    if (tid < 8) {  // group sizes and starts
+        int tot = 0;
+        for (int w = 0; w < 8; w++) tot += wtot[w][tid];
+        gcount[tid] = tot;
+    }
+    __syncthreads();
+    int gstart[8];
+    {
+        int a = 0;
+#pragma unroll
+        for (int g = 0; g < 8; g++) {
+            gstart[g] = a;
+            a += gcount[g];
+        }
+    }
+#pragma unroll
+    for (int g = 0; g < 8; g++) {
+        int wo = 0;
+        for (int w = 0; w < wid; w++) wo += wtot[w][g];
+        off[g] += gstart[g] + wo;
+    }
+    for (int k = 0; k < kCH1 / 256; k++) {
+        const int i = i0 + k;
+        if (i < cn) {
+            const int g = hs[i] & 7;
+            int o = 0;
+#pragma unroll
+            for (int gg = 0; gg < 8; gg++)
+                if (gg == g) o = off[gg]++;
+            lst[o] = (uint16_t)i;
+        }
+    }
+    __syncthreads();
+    // warp w walks group w in position order
+    const int gs = gstart[wid], ge = gs + gcount[wid];
+    for (int b = gs; b < ge; b += 32) {
+        const bool act = b + lane < ge;
+        const int i = act ? lst[b + lane] : 0;
+        const int64_t p = c0 + i;
+        const uint32_t h = act ? hs[i] : (0x8000u | lane);
         const uint32_t m = __match_any_sync(0xffffffffu, h);
         const uint32_t lower = m & ((1u << lane) - 1u);
+        const int src = lower ? 31 - __clz(lower) : lane;
+        const int iq = __shfl_sync(0xffffffffu, i, src);
         int64_t q;
         if (lower) {
-            q = b + (31 - __clz(lower));
+            q = c0 + iq;
         } else {
             const uint32_t r = act ? head[h] : 0u;
             q = r ? base + r : 0;

@@ -131,3 +131,21 @@ def test_vinet_rig_clusters_validates_on_the_host():
     assert call(odd) == _lib.FVV_ELAYOUT
     assert call(d, ncams=600, stages=4) == _lib.FVV_EINVAL     # > 8192 global views for the tile table
     assert "8192" in L.fvv_last_error().decode()
+
+
+def test_deflate_sizes_and_offset_validation():
+    """fvv_deflate_scratch_bytes is host-only: output capacity is zlib's
+    compressBound summed over the streams; offsets must ascend."""
+    from paper_2112_10603_b200.deflate import _sig
+    L = _lib.load()
+    _sig(L)
+    offs = [0, 0, 1, 100, 70000]
+    arr = (ctypes.c_longlong * len(offs))(*offs)
+    sb, cap = ctypes.c_size_t(), ctypes.c_size_t()
+    assert L.fvv_deflate_scratch_bytes(arr, len(offs) - 1, ctypes.byref(sb), ctypes.byref(cap)) == 0
+    bound = lambda n: n + (n >> 12) + (n >> 14) + (n >> 25) + 13  # noqa: E731  zlib compressBound
+    assert cap.value >= sum(bound(b - a) for a, b in zip(offs, offs[1:]))
+    assert sb.value > 10 * 70000  # links, records, symbols per position
+    bad = (ctypes.c_longlong * 3)(0, 10, 5)
+    assert L.fvv_deflate_scratch_bytes(bad, 2, ctypes.byref(sb), ctypes.byref(cap)) != 0
+    assert b"ascend" in L.fvv_last_error()
