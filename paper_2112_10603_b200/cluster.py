@@ -178,15 +178,23 @@ def assemble_cluster_frame(anchor_frame, interp_frames: list, layout: ClusterLay
         if (small.width, small.height) != (cell_w, cell_h):
             raise LayoutError(f"tile {ref.index} is {small.width}x{small.height}, cell is {cell_w}x{cell_h}")
     L = _lib.require_cuda()
+    from .interp import _pinned, _to_host
     sw, sh, _ = cluster_geometry(w, h, len(small_refs))
-    anchor = torch.from_numpy(packed(anchor_frame)).cuda()
-    smalls = [torch.from_numpy(packed(f)).cuda() for f in interp_frames]
+    # anchor and every tile in one pinned staging buffer, one H2D copy
+    fa, fs = frame_nbytes(w, h, fmt), frame_nbytes(cell_w, cell_h, fmt)
+    host = _pinned("cluster_in", fa + fs * len(interp_frames))
+    hn = host.numpy()
+    hn[:fa] = packed(anchor_frame)
+    for i, f in enumerate(interp_frames):
+        hn[fa + i * fs:fa + (i + 1) * fs] = packed(f)
+    dev = host.to("cuda", non_blocking=True)
+    base = dev.data_ptr()
     out = torch.empty(frame_nbytes(sw, sh, fmt), dtype=torch.uint8, device="cuda")
     d = _lib.desc(w, h, fmt)
-    _lib.check(L.fvv_assemble_cluster(ctypes.byref(d), ctypes.c_void_p(anchor.data_ptr()),
-                                      _lib.ptr_array([s.data_ptr() for s in smalls]), len(smalls),
-                                      ctypes.c_void_p(out.data_ptr()), _stream()))
-    stitched = frame_from_packed(out.cpu().numpy(), sw, sh, fmt, anchor_frame.timestamp)
+    _lib.check(L.fvv_assemble_cluster(ctypes.byref(d), ctypes.c_void_p(base),
+                                      _lib.ptr_array([base + fa + i * fs for i in range(len(interp_frames))]),
+                                      len(interp_frames), ctypes.c_void_p(out.data_ptr()), _stream()))
+    stitched = frame_from_packed(_to_host(out, "cluster_out"), sw, sh, fmt, anchor_frame.timestamp)
     return ClusterFrame(layout.cluster_id, stitched, tile_rects(layout, w, h))
 
 
