@@ -268,10 +268,9 @@ ZHD MatchRec match_search32(const uint8_t* sb, const uint16_t* sp, int P, int la
 #endif
             }
             int len;
-            if (x0) {
-                len = ctz32(x0) >> 3;
-            } else if (x1) {
-                len = 4 + (ctz32(x1) >> 3);
+            if ((x0 | x1) != 0) {  // the common case: fewer than 8 equal bytes, no branch
+                const uint32_t y = x0 ? x0 : x1;
+                len = (ctz32(y) >> 3) + (x0 ? 0 : 4);
             } else if (best >= 8 && ld32u(sb, c + best - 3) != pb) {
                 len = 8;  // differs within bytes best-3 .. best: cannot beat best
             } else {
@@ -280,10 +279,11 @@ ZHD MatchRec match_search32(const uint8_t* sb, const uint16_t* sp, int P, int la
                 while (len < maxlen && (x = ld32u(sb, c + len) ^ ld32u(sb, P + len)) == 0) len += 4;
                 if (x) len += ctz32(x) >> 3;
             }
-            if (len > maxlen) len = maxlen;
-            if (len > best) {
-                best = len;
-                bc = c;
+            len = len < maxlen ? len : maxlen;
+            const bool imp = len > best;
+            best = imp ? len : best;
+            bc = imp ? c : bc;
+            if (imp) {
                 if (len >= nice) { done = true; break; }
                 if (best >= 8) pb = ld32u(sb, P + best - 3);
             }
