@@ -1121,13 +1121,16 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
 #ifndef FVV_MASK2_L2PF
 #define FVV_MASK2_L2PF 0  // > 0: prefetch.global.L2 of the luma rows this many rows ahead
 #endif
+#ifndef FVV_MASK2_UNROLL
+#define FVV_MASK2_UNROLL 1  // interior-row loop unroll: r2 sweep 1 / 2 / 3 = 3.59 / 4.00 / 4.55 ms, keep 1
+#endif
 #ifndef FVV_MASK2_PF
 #define FVV_MASK2_PF 0  // luma taps loaded one row ahead: r2 sweep 3.79 -> 3.94 ms (128 regs, spills), off
 #endif
 #if FVV_MASK2_PF && !FVV_MASK2_HB_CACHE
 #error "FVV_MASK2_PF needs the block-grid row cache"
 #endif
-constexpr int kM2Own = 60, kM2Warps = 4;
+constexpr int kM2Own = 60, kM2Warps = 4, kMask2Unroll = FVV_MASK2_UNROLL;
 
 template <int FMT>
 __global__ void __launch_bounds__(kM2Warps * 32, FVV_MINB_MASK2) k_mask_cols2(Geometry g, PairTable pt,
@@ -1493,6 +1496,7 @@ __global__ void __launch_bounds__(kM2Warps * 32, FVV_MINB_MASK2) k_mask_cols2(Ge
     const int b0 = min(max(y0 + 2, 3), yo1), b1 = max(b0, yo1);
     int yy = ys;
     for (; yy < b0; yy++) step(yy, std::true_type{});
+#pragma unroll kMask2Unroll
     for (; yy < b1; yy++) step(yy, std::false_type{});
     for (; yy <= ye; yy++) step(yy, std::true_type{});
     if (ye == H - 1) {
