@@ -1121,6 +1121,12 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
 #ifndef FVV_MASK2_L2PF
 #define FVV_MASK2_L2PF 0  // > 0: prefetch.global.L2 of the luma rows this many rows ahead
 #endif
+#ifndef FVV_MASK2_FPF
+#define FVV_MASK2_FPF 1  // > 0: L1 prefetch of the level-1 flow row this many rows past the next reload: r2 sweep 0 / 1 / 2 / 3 = 3.58 / 3.49 / 3.50 / 3.50 ms
+#endif
+#ifndef FVV_MASK2_HPF
+#define FVV_MASK2_HPF 0  // L1 prefetch of the next block-hit row: r2 sweep 3.49 -> 3.55 ms, off
+#endif
 #ifndef FVV_MASK2_UNROLL
 #define FVV_MASK2_UNROLL 1  // interior-row loop unroll: r2 sweep 1 / 2 / 3 = 3.59 / 4.00 / 4.55 ms, keep 1
 #endif
@@ -1349,6 +1355,15 @@ __global__ void __launch_bounds__(kM2Warps * 32, FVV_MINB_MASK2) k_mask_cols2(Ge
                     hu0[d][c] = ty.i0 == ua + 1 ? hu1[d][c] : xl_u(d, ty.i0, c);
                     hu1[d][c] = xl_u(d, ty.i0 + 1, c);
                 }
+#if FVV_MASK2_FPF
+            // the flow row the next reload reads (two walker rows on), into L1 now:
+            // F -> luma address -> gather is a dependent chain behind it
+            if (ty.i0 + 1 + FVV_MASK2_FPF < L1.h) {
+#pragma unroll
+                for (int d = 0; d < 2; d++)
+                    asm volatile("prefetch.global.L1 [%0];\n" ::"l"(f1[d] + (ty.i0 + 1 + FVV_MASK2_FPF) * L1.w + tu[0].i0));
+            }
+#endif
             ua = ty.i0;
         }
         const ITap tby = clamp_itap32(2 * yy - B2 + 1, lgD2, L2.nby);
@@ -1361,6 +1376,13 @@ __global__ void __launch_bounds__(kM2Warps * 32, FVV_MINB_MASK2) k_mask_cols2(Ge
                     hb0[d][c] = tby.i0 == ba + 1 ? hb1[d][c] : xl_b(d, tby.i0, c);
                     hb1[d][c] = xl_b(d, tby.i1, c);
                 }
+#if FVV_MASK2_HPF
+            if (tby.i1 + 1 < L2.nby) {
+#pragma unroll
+                for (int d = 0; d < 2; d++)
+                    asm volatile("prefetch.global.L1 [%0];\n" ::"l"(hh[d] + (tby.i1 + 1) * L2.nbx + tb[0].i0));
+            }
+#endif
             ba = tby.i0;
         }
 #else
