@@ -364,24 +364,25 @@ def run_b200(args, cfg, rank, world, local_rank):
     # H2D of every tick's cameras and D2H of its cluster frames inside the region,
     # overlapped with synthesis as a live stream would run them
     e2e_steps = max(3, args.steps // 2)
+    E2E_SLOTS = int(os.environ.get("FVV_E2E_SLOTS", "4"))  # r2: 2 / 3 / 4 slots = 10700 / 10726 / 10765 views/s e2e
     e2e_detail = {}
     if vps and world == 1:
         from paper_2112_10603_b200.pipeline import RigPipeline
         pipe = RigPipeline(W, H, fmt, C, S, vps, device=dev)
         hins = [hosts[t % F] for t in range(e2e_steps + 2)]
         houts = [torch.empty(pipe.clusters.numel(), dtype=torch.uint8).pin_memory() for _ in range(2)]
-        pipe.stream_ticks(hins[:2], houts)  # warm both slots (graph capture)
+        pipe.stream_ticks(hins[:E2E_SLOTS], houts, slots=E2E_SLOTS)  # warm every slot (graph capture)
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(pipe.stream)
-        pipe.stream_ticks(hins[:e2e_steps], [houts[t % 2] for t in range(e2e_steps)])
+        pipe.stream_ticks(hins[:e2e_steps], [houts[t % 2] for t in range(e2e_steps)], slots=E2E_SLOTS)
         e1.record(pipe.stream)
         torch.cuda.synchronize()
         e2e_ms = e0.elapsed_time(e1)
         e2e_value = step_views * e2e_steps / (e2e_ms / 1e3)
         h2d, d2h = hosts[0].numel(), pipe.clusters.numel()
-        e2e_detail = {"api": "RigPipeline.stream_ticks (2 slots, copies overlapped)"}
+        e2e_detail = {"api": "RigPipeline.stream_ticks (%d slots: copies and consecutive ticks overlapped)" % E2E_SLOTS}
         del pipe
     else:
         # double-buffered: H2D of step t+1 and D2H of step t-1 run on a copy stream

@@ -114,8 +114,11 @@ class RigPipeline:
 
         host_cams: list of pinned uint8 tensors (C, frame_bytes); host_out: list
         of pinned uint8 tensors (cluster bytes), same length.  Uses `slots`
-        device buffer sets (one CUDA graph each).  Returns when all copies are
-        enqueued; synchronise on `self.stream` (or the device) before reading.
+        device buffer sets, each with its own CUDA graph and compute stream, so
+        the synthesis of consecutive ticks overlaps as well (one tick's small
+        stage-1 launches run beside another's large ones).  Returns when all
+        copies are enqueued; synchronise on `self.stream` (or the device) before
+        reading.
         """
         import torch
         if not self._tiled:
@@ -129,18 +132,19 @@ class RigPipeline:
         done_out = [torch.cuda.Event() for _ in range(slots)]
         for t, (hin, hout) in enumerate(zip(host_cams, host_out)):
             k = t % slots
-            cams, clusters, graph = self._slots[k]
+            cams, clusters, graph = self._slots[k][:3]
             if t >= slots:
                 h2d.wait_event(done_cmp[k])          # the slot's previous tick has been consumed
             with torch.cuda.stream(h2d):
                 cams.copy_(hin, non_blocking=True)
                 done_in[k].record(h2d)
-            self.stream.wait_event(done_in[k])
+            cs = self._cstreams[k]
+            cs.wait_event(done_in[k])
             if t >= slots:
-                self.stream.wait_event(done_out[k])  # its clusters have left the device
-            with torch.cuda.stream(self.stream):
+                cs.wait_event(done_out[k])  # its clusters have left the device
+            with torch.cuda.stream(cs):
                 graph.replay()
-                done_cmp[k].record(self.stream)
+                done_cmp[k].record(cs)
             d2h.wait_event(done_cmp[k])
             with torch.cuda.stream(d2h):
                 hout.copy_(clusters, non_blocking=True)
@@ -150,6 +154,7 @@ class RigPipeline:
     def _make_slots(self, slots: int):
         import torch
         self._slots = []
+        self._cstreams = [self.stream] + [torch.cuda.Stream(device=self.engine.device) for _ in range(slots - 1)]
         for k in range(slots):
             if k == 0:
                 eng, cams, views, clusters = self.engine, self.cams, self.views, self.clusters
@@ -171,7 +176,9 @@ class RigPipeline:
             with torch.cuda.graph(graph, stream=self.stream):
                 run()
             self.stream.synchronize()
-            self._slots.append((cams, clusters, graph))
+            # the graph replays into this slot's engine workspace and views: keep
+            # them alive with it (a collected engine's memory would be reused)
+            self._slots.append((cams, clusters, graph, eng, views))
 
     def views_host(self) -> np.ndarray:
         self.stream.synchronize()

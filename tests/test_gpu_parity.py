@@ -233,16 +233,25 @@ def test_per_level_diagnostics_vs_golden(torch_cuda, name):
         assert np.array_equal(erl, g[f"lv{s}_err_rl"]), s
 
 
-def test_rig_pipeline_stream_ticks_overlapped(torch_cuda):
-    """Double-buffered live-stream form: every tick's clusters equal the golden ones."""
+@pytest.mark.parametrize("slots", [2, 3, 4])
+def test_rig_pipeline_stream_ticks_overlapped(torch_cuda, slots):
+    """Live-stream form (copies and consecutive ticks overlapped, one graph and
+    compute stream per slot): every tick's clusters equal the golden ones.  More
+    slots than two also checks that every slot's engine and views outlive
+    their graph (allocations made after the capture must not reuse them)."""
     from paper_2112_10603_b200.pipeline import RigPipeline
     g = load_golden("rig3_s2_vps2_yuv420_64x48")
     pipe = RigPipeline(64, 48, 1, 3, int(g["stages"]), int(g["vps"]))
     cams = torch_cuda.from_numpy(g["cams"]).pin_memory()
-    outs = [torch_cuda.empty(pipe.clusters.numel(), dtype=torch_cuda.uint8).pin_memory() for _ in range(5)]
-    pipe.stream_ticks([cams] * 5, outs)
+    outs = [torch_cuda.empty(pipe.clusters.numel(), dtype=torch_cuda.uint8).pin_memory() for _ in range(7)]
+    pipe.stream_ticks([cams] * 7, outs, slots=slots)
     torch_cuda.cuda.synchronize()
-    for o in outs:
+    junk = [torch_cuda.full((1 << 20,), 0x5A, dtype=torch_cuda.uint8, device="cuda") for _ in range(8)]
+    outs2 = [torch_cuda.zeros_like(o).pin_memory() for o in outs]
+    pipe.stream_ticks([cams] * 7, outs2, slots=slots)
+    torch_cuda.cuda.synchronize()
+    del junk
+    for o in outs + outs2:
         assert np.array_equal(o.numpy(), g["clusters"])
 
 
