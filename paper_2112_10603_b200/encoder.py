@@ -155,6 +155,36 @@ class RigEncoder:
         self.tokens = torch.empty(max(1, nblocks) * 65 * 3, dtype=torch.uint8, device=self.device)
         self._pool = ThreadPoolExecutor(max_workers=max(1, threads))
 
+    def _build_job_tables(self):
+        """The per-plane job fields that never change (geometry, block offsets,
+        reconstruction bank addresses) and the plane metadata, built once."""
+        import torch
+        rows, meta, block0 = [], [], 0
+        flat = 0
+        for c, tl in enumerate(self.tiles):
+            for ti, (rect, t) in enumerate(tl):
+                for pi, (off, pitch, pw, ph) in enumerate(t.planes):
+                    nbx, nby = (pw + 7) // 8, (ph + 7) // 8
+                    rows.append((c, flat, off, t.recon[0][pi].data_ptr(), t.recon[1][pi].data_ptr()))
+                    meta.append((c, ti, pi, block0, nbx * nby))
+                    block0 += nbx * nby
+                flat += 1
+        n = len(rows)
+        js = np.zeros(n, dtype=[("cluster", "<i8"), ("tile", "<i8"), ("off", "<u8"), ("bank0", "<u8"),
+                                ("bank1", "<u8")])
+        for i, r in enumerate(rows):
+            js[i] = r
+        jobs = np.zeros(n, dtype=_JOB)
+        for i, m in enumerate(meta):
+            _, ti, pi, b0, _nb = m
+            off, pitch, pw, ph = self.tiles[m[0]][ti][1].planes[pi]
+            jobs[i]["block0"], jobs[i]["pitch"], jobs[i]["w"], jobs[i]["h"] = b0, pitch, pw, ph
+            jobs[i]["nbx"], jobs[i]["nby"], jobs[i]["step"] = (pw + 7) // 8, (ph + 7) // 8, self.step
+        self._jobs_static, self._meta, self._nblocks_total = js, meta, block0
+        self._jobs_host = jobs
+        self._jobs_pinned = torch.empty(jobs.nbytes, dtype=torch.uint8, pin_memory=True)
+        self._jobs_dev = torch.empty(jobs.nbytes, dtype=torch.uint8, device=self.device)
+
     def _stream(self):
         import torch
         return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
@@ -168,20 +198,21 @@ class RigEncoder:
         if offsets is None:
             offsets = np.concatenate([[0], np.cumsum(self.frame_sizes)[:-1]]).tolist()
         base = clusters.data_ptr()
-        jobs = []
-        block0 = 0
-        meta = []  # (cluster, tile index, plane index, block0, nblocks)
-        for c, tl in enumerate(self.tiles):
-            for ti, (rect, t) in enumerate(tl):
-                is_p = t.index % self.gop != 0
-                cur, prv = t.recon[t.index & 1], t.recon[(t.index + 1) & 1]
-                for pi, (off, pitch, pw, ph) in enumerate(t.planes):
-                    nbx, nby = (pw + 7) // 8, (ph + 7) // 8
-                    jobs.append((base + offsets[c] + off, prv[pi].data_ptr() if is_p else 0, cur[pi].data_ptr(),
-                                 block0, pitch, pw, ph, nbx, nby, int(is_p), self.step, 0))
-                    meta.append((c, ti, pi, block0, nbx * nby))
-                    block0 += nbx * nby
-        jt = torch.from_numpy(np.array(jobs, dtype=_JOB).view(np.uint8)).to(self.device, non_blocking=False)
+        if getattr(self, "_jobs_static", None) is None:
+            self._build_job_tables()
+        js, meta, block0 = self._jobs_static, self._meta, self._nblocks_total
+        # per call: source addresses, reconstruction banks and frame type (vectorised)
+        idx = np.array([t.index for tl in self.tiles for _, t in tl], dtype=np.int64)[js["tile"]]
+        is_p = (idx % self.gop) != 0
+        par = (idx & 1).astype(bool)
+        jobs = self._jobs_host
+        jobs["src"] = np.uint64(base) + np.asarray(offsets, dtype=np.uint64)[js["cluster"]] + js["off"]
+        jobs["recon"] = np.where(par, js["bank1"], js["bank0"])
+        jobs["prev"] = np.where(is_p, np.where(par, js["bank0"], js["bank1"]), np.uint64(0))
+        jobs["is_p"] = is_p.astype(np.int32)
+        self._jobs_pinned.numpy()[:] = jobs.view(np.uint8)
+        jt = self._jobs_dev
+        jt.copy_(self._jobs_pinned, non_blocking=True)
         self._last_jobs, self._last_njobs = jt, len(jobs)
         L, st = self._L, self._stream()
         _lib.check(L.fvv_encode_blocks(ctypes.c_void_p(jt.data_ptr()), len(jobs), block0, int(self.lossless),
