@@ -251,6 +251,11 @@ __global__ void __launch_bounds__(512) k_zd_match(const uint8_t* __restrict__ da
     for (int64_t i = threadIdx.x; i < pe - wb; i += blockDim.x) sp[i] = pg[wb + i];
     for (int64_t i = threadIdx.x; i < we - wb; i += blockDim.x) sb[i] = d[wb + i];
     __syncthreads();
+    // shared-window addresses for the search's explicit ld.shared: taken through a
+    // volatile mov after the barrier, so no load can be scheduled above it
+    ShWin win;
+    asm volatile("mov.u32 %0, %1;" : "=r"(win.sb) : "r"((uint32_t)__cvta_generic_to_shared(sb)));
+    asm volatile("mov.u32 %0, %1;" : "=r"(win.sp) : "r"((uint32_t)__cvta_generic_to_shared(sp)));
     uint2* out = rec + sd.in_off;
     for (int64_t p = c0 + threadIdx.x; p < c1; p += blockDim.x) {
         MatchRec r{0u, 0u};
@@ -259,7 +264,7 @@ __global__ void __launch_bounds__(512) k_zd_match(const uint8_t* __restrict__ da
             const int P = (int)(p - wb);
             const int pd0 = sp[P];
             if (pd0 && !nil_at_slide(p, n, (uint32_t)pd0))
-                r = match_search32(sb, sp, P, (int)min(la, (int64_t)(1 << 20)), pd0);
+                r = match_search32w(win, P, (int)min(la, (int64_t)(1 << 20)), pd0);
         }
         out[p] = make_uint2(r.r128, r.r32);
     }

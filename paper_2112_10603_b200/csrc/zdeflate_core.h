@@ -240,12 +240,50 @@ ZHD int ctz32(uint32_t x) {
 // are longest_match's and the result equals match_search's.  (A filter that
 // passes ~7 % of the candidates keeps most of a warp idle while a few lanes
 // measure; measuring all keeps the lanes together.)
-ZHD MatchRec match_search32(const uint8_t* sb, const uint16_t* sp, int P, int la, int pd0) {
+// Window access for match_search32: the bytes as aligned 32-bit words and the
+// links.  Host: plain pointers.  Device (ShWin): 32-bit shared-window addresses
+// with explicit ld.shared, so the compiler does not rebuild a generic pointer
+// to the dynamic shared array inside the candidate loop.
+struct PtrWin {
+    const uint8_t* sb;
+    const uint16_t* sp;
+    ZHD uint32_t word(int wi) const { return reinterpret_cast<const uint32_t*>(sb)[wi]; }
+    ZHD int link(int i) const { return sp[i]; }
+};
+#ifdef __CUDACC__
+struct ShWin {
+    uint32_t sb, sp;  // shared-window addresses (sb 4-byte aligned)
+    __device__ __forceinline__ uint32_t word(int wi) const {
+        uint32_t v;
+        asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(sb + 4u * (uint32_t)wi));
+        return v;
+    }
+    __device__ __forceinline__ int link(int i) const {
+        unsigned short v;
+        asm("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(sp + 2u * (uint32_t)i));
+        return (int)v;
+    }
+};
+#endif
+
+template <typename Win>
+ZHD uint32_t win32u(const Win& W, int i) {  // 4 bytes at byte offset i
+    const int wi = i >> 2, sh = (i & 3) * 8;
+    const uint32_t w0 = W.word(wi), w1 = W.word(wi + 1);
+#ifdef __CUDA_ARCH__
+    return __funnelshift_r(w0, w1, sh);
+#else
+    return (uint32_t)((((uint64_t)w1 << 32) | w0) >> sh);
+#endif
+}
+
+template <typename Win>
+ZHD MatchRec match_search32w(const Win& W, int P, int la, int pd0) {
     MatchRec r{0, 0};
     const int nice = la < kNiceLength ? la : kNiceLength;
     const int maxlen = la < kMaxMatch ? la : kMaxMatch;
     const int lim = P - kMaxDist;  // later candidates must lie above (distance < MAX_DIST)
-    const uint32_t p0 = ld32u(sb, P), p1 = ld32u(sb, P + 4);
+    const uint32_t p0 = win32u(W, P), p1 = win32u(W, P + 4);
     int best = 2, bc = P, cnt = 0, c = P - pd0;
     uint32_t pb = 0;  // scan bytes best-3 .. best once best >= 8
     bool done = false;
@@ -253,12 +291,11 @@ ZHD MatchRec match_search32(const uint8_t* sb, const uint16_t* sp, int P, int la
         const int stop = phase ? kMaxChain : (kMaxChain >> 2);
         while (cnt < stop) {
             cnt++;
-            const int d = sp[c];
+            const int d = W.link(c);
             uint32_t x0, x1;
             {  // 8 bytes at c from three aligned words
-                const uint32_t* w = reinterpret_cast<const uint32_t*>(sb + (c & ~3));
-                const int sh = (c & 3) * 8;
-                const uint32_t w0 = w[0], w1 = w[1], w2 = w[2];
+                const int wi = c >> 2, sh = (c & 3) * 8;
+                const uint32_t w0 = W.word(wi), w1 = W.word(wi + 1), w2 = W.word(wi + 2);
 #ifdef __CUDA_ARCH__
                 x0 = __funnelshift_r(w0, w1, sh) ^ p0;
                 x1 = __funnelshift_r(w1, w2, sh) ^ p1;
@@ -271,12 +308,12 @@ ZHD MatchRec match_search32(const uint8_t* sb, const uint16_t* sp, int P, int la
             if ((x0 | x1) != 0) {  // the common case: fewer than 8 equal bytes, no branch
                 const uint32_t y = x0 ? x0 : x1;
                 len = (ctz32(y) >> 3) + (x0 ? 0 : 4);
-            } else if (best >= 8 && ld32u(sb, c + best - 3) != pb) {
+            } else if (best >= 8 && win32u(W, c + best - 3) != pb) {
                 len = 8;  // differs within bytes best-3 .. best: cannot beat best
             } else {
                 len = 8;
                 uint32_t x = 0;
-                while (len < maxlen && (x = ld32u(sb, c + len) ^ ld32u(sb, P + len)) == 0) len += 4;
+                while (len < maxlen && (x = win32u(W, c + len) ^ win32u(W, P + len)) == 0) len += 4;
                 if (x) len += ctz32(x) >> 3;
             }
             len = len < maxlen ? len : maxlen;
@@ -285,7 +322,7 @@ ZHD MatchRec match_search32(const uint8_t* sb, const uint16_t* sp, int P, int la
             bc = imp ? c : bc;
             if (imp) {
                 if (len >= nice) { done = true; break; }
-                if (best >= 8) pb = ld32u(sb, P + best - 3);
+                if (best >= 8) pb = win32u(W, P + best - 3);
             }
             if (d == 0) { done = true; break; }
             c -= d;
@@ -295,6 +332,11 @@ ZHD MatchRec match_search32(const uint8_t* sb, const uint16_t* sp, int P, int la
     }
     r.r128 = finish_rec32(best, P - bc);
     return r;
+}
+
+
+ZHD MatchRec match_search32(const uint8_t* sb, const uint16_t* sp, int P, int la, int pd0) {
+    return match_search32w(PtrWin{sb, sp}, P, la, pd0);
 }
 
 // ---------------------------------------------------------------------------
