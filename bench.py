@@ -368,6 +368,9 @@ def run_b200(args, cfg, rank, world, local_rank):
     e2e_detail = {}
     if vps and world == 1:
         from paper_2112_10603_b200.pipeline import RigPipeline
+        # slots bounded by free HBM (cfg5: ~48 GB of engine workspace per slot)
+        per_slot = engines[0].workspace_bytes + views_l[0].numel() + clusters_l[0].numel()
+        E2E_SLOTS = max(1, min(E2E_SLOTS, int(0.95 * torch.cuda.mem_get_info(dev)[0]) // max(1, per_slot)))
         pipe = RigPipeline(W, H, fmt, C, S, vps, device=dev)
         hins = [hosts[t % F] for t in range(e2e_steps + 2)]
         houts = [torch.empty(pipe.clusters.numel(), dtype=torch.uint8).pin_memory() for _ in range(2)]
