@@ -39,7 +39,10 @@ namespace {
 
 constexpr int kCH1 = 16384;   // chain chunk (positions)
 constexpr int kCH2 = 4096;    // search chunk (positions)
-constexpr int kSeg = 16384;   // speculative parse segment (positions)
+#ifndef FVV_ZD_SEG
+#define FVV_ZD_SEG 16384
+#endif
+constexpr int kSeg = FVV_ZD_SEG;  // speculative parse segment (positions)
 constexpr int kSegPad = 260;  // symbols a segment's parse may run past its end
 constexpr int kPW = 2048;     // parse window (records staged per refill)
 constexpr size_t kChainSmem = 4 * 32768 + 2 * kCH1 + 2 * kCH1 + 64;
