@@ -363,7 +363,7 @@ def run_b200(args, cfg, rank, world, local_rank):
     # ---- e2e: host buffers through the public API (RigPipeline.stream_ticks), ---
     # H2D of every tick's cameras and D2H of its cluster frames inside the region,
     # overlapped with synthesis as a live stream would run them
-    e2e_steps = max(3, args.steps // 2)
+    e2e_steps = max(3, args.steps)  # as many ticks as timed steps: the slots' fill and drain amortised alike
     E2E_SLOTS = int(os.environ.get("FVV_E2E_SLOTS", "4"))  # r2: 2 / 3 / 4 slots = 10700 / 10726 / 10765 views/s e2e
     e2e_detail = {}
     if vps and world == 1:
