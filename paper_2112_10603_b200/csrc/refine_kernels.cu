@@ -70,41 +70,48 @@ __global__ void k_ref_img(RefSrc src, int nsrc, int fmt, int W, int H, int Wp, i
 // U-Net input of every view (refine_inputs): x0 NHWC bf16 cstride 32 =
 // (A, B, warp(A, F_l,t), warp(B, F_r,t), w_t, F_l,t, F_r,t); merged (3, H, W) f32;
 // the canvas flows (F_l,t, F_r,t) f32 planar (4, Hp, Wp) for the context pyramid
-__global__ void k_ref_in(RefViews rv, int fmt, int W, int H, int Wp, int Hp, __nv_bfloat16* __restrict__ x0,
+__global__ void k_ref_in(RefViews rv, int nloop, int fmt, int W, int H, int Wp, int Hp, __nv_bfloat16* __restrict__ x0,
                          float* __restrict__ merged, float* __restrict__ flow0) {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y, b = blockIdx.z;
+    // nloop > 1: views b0 .. b0 + nloop - 1 share their source pair and state (a
+    // refine batch of one camera gap): the state, the mask and the unwarped frames
+    // are read once per pixel and only the t-dependent channels are redone
+    const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y, b0 = blockIdx.z * nloop;
     if (x >= Wp) return;
     const int xs = min(x, W - 1), ys = min(y, H - 1);
-    const uint8_t* L = rv.left[b];
-    const uint8_t* R = rv.right[b];
-    const float* S = rv.state[b];
-    const float t = rv.t[b];
+    const uint8_t* L = rv.left[b0];
+    const uint8_t* R = rv.right[b0];
+    const float* S = rv.state[b0];
     const size_t plane = (size_t)W * H, pix = (size_t)ys * W + xs;
-    const float tl = 2.0f * t, tr = 2.0f * (1.0f - t);
-    const float flx = S[pix] * tl, fly = S[plane + pix] * tl;
-    const float frx = S[2 * plane + pix] * tr, fry = S[3 * plane + pix] * tr;
+    const float sfx = S[pix], sfy = S[plane + pix], sgx = S[2 * plane + pix], sgy = S[3 * plane + pix];
     const float m = 1.0f / (1.0f + expf(-S[4 * plane + pix]));
-    const float wt = (1.0f - t) * m / ((1.0f - t) * m + t * (1.0f - m));
     const float3 A = net_px(L, fmt, W, H, xs, ys), B = net_px(R, fmt, W, H, xs, ys);
-    const float3 wl = warp_px(L, fmt, W, H, xs, ys, flx, fly), wr = warp_px(R, fmt, W, H, xs, ys, frx, fry);
-    __align__(16) __nv_bfloat16 buf[32];
-    const float v[17] = {A.x, A.y, A.z, B.x, B.y, B.z, wl.x, wl.y, wl.z, wr.x, wr.y, wr.z, wt, flx, fly, frx, fry};
-#pragma unroll
-    for (int i = 0; i < 32; i++) buf[i] = __float2bfloat16_rn(i < 17 ? v[i] : 0.0f);
-    uint4* o = reinterpret_cast<uint4*>(x0 + (((size_t)b * Hp + y) * Wp + x) * 32);
-#pragma unroll
-    for (int i = 0; i < 4; i++) o[i] = reinterpret_cast<const uint4*>(buf)[i];
     const size_t cp = (size_t)Wp * Hp, co = (size_t)y * Wp + x;
-    float* fo = flow0 + (size_t)b * 4 * cp;
-    fo[co] = flx;
-    fo[cp + co] = fly;
-    fo[2 * cp + co] = frx;
-    fo[3 * cp + co] = fry;
-    if (x < W && y < H) {
-        float* mo = merged + (size_t)b * 3 * plane;
-        mo[pix] = wt * wl.x + (1.0f - wt) * wr.x;
-        mo[plane + pix] = wt * wl.y + (1.0f - wt) * wr.y;
-        mo[2 * plane + pix] = wt * wl.z + (1.0f - wt) * wr.z;
+    for (int k = 0; k < nloop; k++) {
+        const int b = b0 + k;
+        const float t = rv.t[b];
+        const float tl = 2.0f * t, tr = 2.0f * (1.0f - t);
+        const float flx = sfx * tl, fly = sfy * tl;
+        const float frx = sgx * tr, fry = sgy * tr;
+        const float wt = (1.0f - t) * m / ((1.0f - t) * m + t * (1.0f - m));
+        const float3 wl = warp_px(L, fmt, W, H, xs, ys, flx, fly), wr = warp_px(R, fmt, W, H, xs, ys, frx, fry);
+        __align__(16) __nv_bfloat16 buf[32];
+        const float v[17] = {A.x, A.y, A.z, B.x, B.y, B.z, wl.x, wl.y, wl.z, wr.x, wr.y, wr.z, wt, flx, fly, frx, fry};
+#pragma unroll
+        for (int i = 0; i < 32; i++) buf[i] = __float2bfloat16_rn(i < 17 ? v[i] : 0.0f);
+        uint4* o = reinterpret_cast<uint4*>(x0 + (((size_t)b * Hp + y) * Wp + x) * 32);
+#pragma unroll
+        for (int i = 0; i < 4; i++) o[i] = reinterpret_cast<const uint4*>(buf)[i];
+        float* fo = flow0 + (size_t)b * 4 * cp;
+        fo[co] = flx;
+        fo[cp + co] = fly;
+        fo[2 * cp + co] = frx;
+        fo[3 * cp + co] = fry;
+        if (x < W && y < H) {
+            float* mo = merged + (size_t)b * 3 * plane;
+            mo[pix] = wt * wl.x + (1.0f - wt) * wr.x;
+            mo[plane + pix] = wt * wl.y + (1.0f - wt) * wr.y;
+            mo[2 * plane + pix] = wt * wl.z + (1.0f - wt) * wr.z;
+        }
     }
 }
 
@@ -227,8 +234,12 @@ cudaError_t ref_img(const RefSrc& src, int nsrc, int fmt, int W, int H, int Wp, 
 
 cudaError_t ref_inputs(const RefViews& rv, int nb, int fmt, int W, int H, int Wp, int Hp, void* x0, float* merged,
                        float* flow0, cudaStream_t st) {
-    k_ref_in<<<dim3((Wp + 127) / 128, Hp, nb), 128, 0, st>>>(rv, fmt, W, H, Wp, Hp,
-                                                            static_cast<__nv_bfloat16*>(x0), merged, flow0);
+    bool shared = true;
+    for (int b = 1; b < nb; b++)
+        shared = shared && rv.left[b] == rv.left[0] && rv.right[b] == rv.right[0] && rv.state[b] == rv.state[0];
+    const int nloop = shared ? nb : 1;
+    k_ref_in<<<dim3((Wp + 127) / 128, Hp, nb / nloop), 128, 0, st>>>(rv, nloop, fmt, W, H, Wp, Hp,
+                                                                    static_cast<__nv_bfloat16*>(x0), merged, flow0);
     return cudaGetLastError();
 }
 
