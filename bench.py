@@ -773,7 +773,7 @@ def run_direct(cfg, eng, cams, views, clusters, stream, steps=10):
                       "restatement (oracle/vinet_ref.synth) on the oracle's flows and mask (tests/test_gpu_timed_path.py)"}
 
 
-def run_encoder(cfg, dev, cluster_bufs, stream, ticks=2):
+def run_encoder(cfg, dev, cluster_bufs, stream, ticks=4):
     """The encoder hand-off: FVT1 records of every
     tile of every cluster frame of the rig frame (server/pipeline.py:294-318),
     transform stage and DEFLATE (zlib-identical, deflate_kernels.cu) on the
@@ -793,14 +793,16 @@ def run_encoder(cfg, dev, cluster_bufs, stream, ticks=2):
     with torch.cuda.stream(stream):
         enc.encode(cluster_bufs[0])  # intra tick (warm-up)
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
         nbytes = 0
         recs0 = None
+        walls = []
         for k in range(ticks):
+            t0 = time.perf_counter()
             recs = enc.encode(cluster_bufs[(k + 1) % len(cluster_bufs)])
+            walls.append(time.perf_counter() - t0)
             recs0 = recs if recs0 is None else recs0
             nbytes += sum(len(r) for c in recs for r in c)
-        wall = (time.perf_counter() - t0) / ticks
+        wall = statistics.median(walls)  # per tick; host-side hiccups do not skew it
         # device transform stage alone (blocks + tokens kernels), CUDA events
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         import ctypes
