@@ -240,7 +240,7 @@ class RigEncoder:
                 self._pinned = torch.empty(max(nraw, 1 << 20), dtype=torch.uint8, pin_memory=True)
             self._pinned[:nraw].copy_(out[:nraw], non_blocking=True)
             torch.cuda.current_stream(self.device).synchronize()
-            raw = self._pinned[:nraw].numpy().tobytes()
+            raw = memoryview(self._pinned.numpy())[:nraw]  # zero-copy views; each record copies once (join)
             datas = [raw[oo[i]:oo[i + 1]] for i in range(len(meta))]
         else:
             offs = self.tok_off[:block0 + 1].cpu().numpy()
