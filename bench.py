@@ -5,7 +5,7 @@ synthesized virtual views/s at 1080p; per-rig-frame latency).
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl b200|reference]
 
 One step = a batch of F independent rig frames of the live stream per rank
-(--frames-in-flight, default 1; F > 1 run concurrently on forked streams inside one
+(--frames-in-flight, default auto = 3 when they fit a quarter of HBM, else 1; F > 1 run concurrently on forked streams inside one
 CUDA graph): every dense view of every camera gap (recursive midpoints,
 server/pipeline.py:254-271) plus every cluster frame (server/pipeline.py:273-292).
 The per-rig-frame latency (one frame in flight) is measured separately and
@@ -238,11 +238,19 @@ def run_b200(args, cfg, rank, world, local_rank):
     total_views = (C - 1) * (1 << S) + 1
     max_pairs = (C - 1) * (1 << (S - 1))
     npairs_total = step_views  # interpolations per rig frame
-    F = max(1, args.frames_in_flight)
+    # frames in flight: --frames-in-flight N, or 0 = auto (3 when three rig frames' engines,
+    # views and clusters take under a quarter of HBM, else 1: cfg5's 48 GB engines stay single)
+    F_req = args.frames_in_flight
+    F = max(1, F_req) if F_req > 0 else 3
     engines, cams_l, views_l, clusters_l, hosts = [], [], [], [], []
     for i in range(F):
+        if F_req <= 0 and i == 1:
+            per = engines[0].workspace_bytes + views_l[0].numel() + (clusters_l[0].numel() if vps else 0)
+            if 3 * per > 0.25 * torch.cuda.get_device_properties(dev).total_memory:
+                F = 1
+                break
         e = Interpolator(W, H, fmt, max_pairs=max_pairs, device=dev)
-        h = torch.from_numpy(synth_rig(W, H, fmt, C, seed=42 + rank * F + i)).pin_memory()
+        h = torch.from_numpy(synth_rig(W, H, fmt, C, seed=42 + rank * 8 + i)).pin_memory()
         engines.append(e)
         hosts.append(h)
         cams_l.append(h.to(dev))
@@ -1086,8 +1094,9 @@ def main():
     ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-graph", action="store_true")
-    ap.add_argument("--frames-in-flight", type=int, default=1,
-                    help="independent rig frames of the live stream processed concurrently per step")
+    ap.add_argument("--frames-in-flight", type=int, default=0,
+                    help="independent rig frames of the live stream processed concurrently per step "
+                         "(0 = auto: 3 when they fit a quarter of HBM, else 1)")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-vinet", action="store_true", help="skip the VINet (CNN path) section")
     ap.add_argument("--no-encoder", action="store_true", help="skip the encoder hand-off section")
