@@ -581,10 +581,12 @@ def kernel_roofline(args, cfg, eng, run_once, npairs_total, clk, stream, tile_fn
     except (OSError, KeyError, ValueError):
         pass
     roofline = {"bound": bound, "kernel": dom, "achieved": achieved, "peak": peak, "unit": unit,
-                "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per step (ncu dram read+write)",
+                "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per rig frame (ncu dram read+write)",
                 "peak_source": peak_note, "issue": issue,
                 "kernel_ms_per_step": dom_ms, "kernel_share_of_step": dom_ms / step_kernel_ms,
-                "per_kernel_ms_per_step": {k: round(v[0], 4) for k, v in per_class.items()}}
+                "per_kernel_ms_per_step": {k: round(v[0], 4) for k, v in per_class.items()},
+                "kernel_timing_unit": "one rig frame (its stage kernels timed alone with CUDA events; "
+                                      "traffic from the ncu launch list is per rig frame too)"}
 
     launches_per_step = sum(v[1] for v in per_class.values())
     # SAD classes launch a second (ragged-column) kernel when the level width is not a multiple of 8
