@@ -19,7 +19,11 @@
 #include <type_traits>
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <mutex>
 
 #include "fvv_device.cuh"
 
@@ -1986,9 +1990,47 @@ struct SadW {
                             : (SIDE <= 5 ? FVV_SADW_RB5 : (SIDE <= 9 ? FVV_SADW_RB9 : (SIDE == 25 ? FVV_SADW_RB25 : 1)));
     static constexpr int NBYT = NBY * RB;                  // block rows per CTA
     static constexpr int WH = 8 * NBYT + 2 * R;            // window rows
+    // + 8: the window's TMA mbarrier (between the reference sums and the ranks, 8-aligned)
     static constexpr size_t SMEM = (size_t)WH * TWW * 4 + (size_t)8 * NBYT * 32 * 4 +
-                                   (size_t)NB * RB * 8 + (size_t)SIDE * SIDE * 2;
+                                   (size_t)NB * RB * 8 + 8 + (size_t)SIDE * SIDE * 2;
 };
+
+// The target window arrives by one TMA tile copy per CTA (FVV_SADW_TMA): box
+// WW x WH samples of the level's u16 target plane, viewed as a 3-D tensor
+// (x, y, pair slot) whose pair stride is the workspace slot stride, so one map
+// per (level, direction) serves every pair of the launch.  TMA zero-fills
+// outside the plane; CTAs on the frame edge then overwrite those samples with
+// the replicated edge (the window is clamp-indexed, flow.py:57-91 via
+// _kernels.py's edge padding).  FVV_SADW_TMA=0 keeps the per-thread cp.async
+// staging for A/B timing.
+#ifndef FVV_SADW_TMA
+#define FVV_SADW_TMA 1
+#endif
+__device__ __forceinline__ void sadw_mbar_init(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void sadw_tma_window(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
+                                                int z, uint32_t bytes) {
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(z), "r"(b)
+        : "memory");
+}
+__device__ __forceinline__ void sadw_mbar_wait0(uint64_t* bar) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "SADW_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+        "@!p bra SADW_WAIT_%=;\n"
+        "}\n" ::"r"(a)
+        : "memory");
+}
 
 struct SadWLaunch {
     int bx_end;                  // full 8-wide block columns (w / 8)
@@ -2078,15 +2120,17 @@ __device__ __forceinline__ uint32_t sadw_group(const uint32_t* Rb, const uint32_
 
 template <int LEVEL, int SIDE, int CG, int RB_>
 __global__ void __launch_bounds__(SadW<SIDE, CG, RB_>::THREADS, FVV_MINB_SADW(SIDE))
-k_sadw(Geometry g, PairTable pt, uint8_t* __restrict__ ws, Planes P, SadWLaunch sl) {
+k_sadw(Geometry g, PairTable pt, uint8_t* __restrict__ ws, Planes P, SadWLaunch sl,
+       const __grid_constant__ CUtensorMap tmw0, const __grid_constant__ CUtensorMap tmw1) {
     pdl_enter();
     using S = SadW<SIDE, CG, RB_>;
-    extern __shared__ __align__(16) uint8_t smem[];
-    uint32_t* Ts = reinterpret_cast<uint32_t*>(smem);              // WH x TWW raw words
+    extern __shared__ __align__(128) uint8_t sadw_smem[];          // TMA destination: 128-byte aligned
+    uint32_t* Ts = reinterpret_cast<uint32_t*>(sadw_smem);         // WH x TWW raw words
     uint32_t* Rs = Ts + S::WH * S::TWW;                            // 8*NBYT x 32 pair words
     uint32_t* best = Rs + 8 * S::NBYT * 32;                        // NB*RB keys
     int* suma = reinterpret_cast<int*>(best + S::NB * S::RB);      // NB*RB reference sums
-    int16_t* rk = reinterpret_cast<int16_t*>(suma + S::NB * S::RB);  // SIDE^2 ranks
+    uint64_t* wbar = reinterpret_cast<uint64_t*>(suma + S::NB * S::RB);  // window TMA barrier
+    int16_t* rk = reinterpret_cast<int16_t*>(wbar + 1);            // SIDE^2 ranks
 
     const Level& L = g.lv[LEVEL];
     const int w = L.w, h = L.h;
@@ -2099,6 +2143,15 @@ k_sadw(Geometry g, PairTable pt, uint8_t* __restrict__ ws, Planes P, SadWLaunch 
     const int xa = bx0 * 8 - S::XPAD, ya = by0 * 8 - S::R;
     constexpr int NCH = S::WW / 8;                                  // 16-byte chunks per row
     static_assert(NCH <= 16, "two window rows per warp pass");
+#if FVV_SADW_TMA
+    static_assert(S::WW <= 256 && S::WH <= 256, "TMA box dimensions");
+    (void)tg;
+    if (tid == 0) {
+        sadw_mbar_init(wbar);
+        sadw_tma_window(Ts, d ? &tmw1 : &tmw0, wbar, xa, ya, pair, (uint32_t)(S::WH * S::TWW * 4));
+    }
+#else
+    (void)tmw0; (void)tmw1;
     {
         const int lane = tid & 31, q = lane & 15;                   // chunk of this lane
         const int gx = xa + 8 * q;
@@ -2120,6 +2173,7 @@ k_sadw(Geometry g, PairTable pt, uint8_t* __restrict__ ws, Planes P, SadWLaunch 
         }
     }
     cp_async_commit();
+#endif
     // ---- stage: reference strip as pixel-pair words + per-block sums -------
     for (int i = tid; i < S::NB * S::RB; i += S::THREADS) { best[i] = 0xFFFFFFFFu; suma[i] = 0; }
     for (int i = tid; i < SIDE * SIDE; i += S::THREADS) rk[i] = sl.rank_of[i];
@@ -2157,7 +2211,34 @@ k_sadw(Geometry g, PairTable pt, uint8_t* __restrict__ ws, Planes P, SadWLaunch 
         FVV_DBG_ALIGN(Rs + yy * 32 + 4 * kx, 16);
         *reinterpret_cast<uint4*>(Rs + yy * 32 + 4 * kx) = v;
     }
+#if FVV_SADW_TMA
+    sadw_mbar_wait0(wbar);
+    if (xa < 0 || xa + S::WW > w || ya < 0 || ya + S::WH > h) {  // CTA-uniform: frame-edge windows
+        // columns: whole 16-byte chunks lie outside the plane (xa, w multiples of 8);
+        // they take the row's edge sample (row 0 / h-1 rows are fixed up next)
+        const uint16_t* Th = reinterpret_cast<const uint16_t*>(Ts);
+        for (int i = tid; i < S::WH * NCH; i += S::THREADS) {
+            const int t = i / NCH, q = i - t * NCH, gx = xa + 8 * q;
+            if (gx < 0 || gx + 8 > w) {
+                const uint32_t v = Th[t * S::WW + (gx < 0 ? -xa : w - 1 - xa)];
+                const uint32_t vv = v | (v << 16);
+                *reinterpret_cast<uint4*>(Ts + t * S::TWW + 4 * q) = make_uint4(vv, vv, vv, vv);
+            }
+        }
+        __syncthreads();
+        // rows outside the plane: copies of row 0 / h-1 (both inside the window)
+        for (int i = tid; i < S::WH * NCH; i += S::THREADS) {
+            const int t = i / NCH, q = i - t * NCH, gy = ya + t;
+            if (gy < 0 || gy > h - 1) {
+                const int ts = (gy < 0 ? 0 : h - 1) - ya;
+                *reinterpret_cast<uint4*>(Ts + t * S::TWW + 4 * q) =
+                    *reinterpret_cast<const uint4*>(Ts + ts * S::TWW + 4 * q);
+            }
+        }
+    }
+#else
     cp_async_wait_0();
+#endif
     __syncthreads();
 
     // ---- search ---------------------------------------------------------------
@@ -2195,6 +2276,32 @@ k_sadw(Geometry g, PairTable pt, uint8_t* __restrict__ ws, Planes P, SadWLaunch 
     }
 }
 
+// host: the (x, y, pair slot) u16 view of one target plane for the window copies
+static PFN_cuTensorMapEncodeTiled_v12000 sadw_encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    });
+    return fn;
+}
+static bool sadw_window_map(CUtensorMap* m, const void* base, int w, int h, int npairs, size_t pair_stride, int bw,
+                            int bh) {
+    auto fn = sadw_encode_fn();
+    if (!fn || (reinterpret_cast<uintptr_t>(base) & 15) || (pair_stride & 15) || ((size_t)w * 2) % 16) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)std::max(npairs, 1)};
+    const cuuint64_t strides[2] = {(cuuint64_t)w * 2, (cuuint64_t)pair_stride};
+    const cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int LEVEL, int SIDE, int CG, int RB_>
 static cudaError_t launch_sadw_rb(const Geometry& g, const PairTable& pt, uint8_t* ws, const Planes& P,
                                   SadWLaunch sl, int npairs, cudaStream_t st) {
@@ -2206,7 +2313,16 @@ static cudaError_t launch_sadw_rb(const Geometry& g, const PairTable& pt, uint8_
         if (e != cudaSuccess) return e;
     }
     dim3 grid((sl.bx_end + 7) / 8, (L.nby + S::NBYT - 1) / S::NBYT, 2 * npairs);
-    cudaError_t le = launch_k(g.pdl, kern, grid, dim3(S::THREADS), S::SMEM, st, g, pt, ws, P, sl);
+    CUtensorMap tm[2];
+    memset(tm, 0, sizeof(tm));
+#if FVV_SADW_TMA
+    for (int d = 0; d < 2; d++) {
+        const size_t off = LEVEL == 0 ? P.q0[1 - d] : LEVEL == 1 ? P.tq1[d] : P.tq2[d];
+        if (!sadw_window_map(&tm[d], ws + off, L.w, L.h, npairs, P.stride, S::WW, S::WH))
+            return cudaErrorInvalidValue;
+    }
+#endif
+    cudaError_t le = launch_k(g.pdl, kern, grid, dim3(S::THREADS), S::SMEM, st, g, pt, ws, P, sl, tm[0], tm[1]);
     if (le != cudaSuccess) return le;
     return cudaGetLastError();
 }
