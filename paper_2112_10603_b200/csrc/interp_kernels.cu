@@ -718,6 +718,10 @@ __global__ void __launch_bounds__(256) k_flow(Geometry g, uint8_t* __restrict__ 
 // units 1/4 (s4), level-2 samples integral (luma).
 // ---------------------------------------------------------------------------
 constexpr int kQH = 64, kQW = 64;  // 16 pixels per thread amortise the tile setup
+#ifndef FVV_WARPQ_UNROLL
+#define FVV_WARPQ_UNROLL 4  // interior loop unroll (16 rows per thread)
+#endif
+constexpr int kWarpqUnroll = FVV_WARPQ_UNROLL;
 #ifndef FVV_WARPQ_L1PF
 #define FVV_WARPQ_L1PF 0  // > 0: L1 prefetch of the luma row this many iterations ahead (r2 sweep 1/2/4: no change), off
 #endif
@@ -766,7 +770,7 @@ __global__ void __launch_bounds__(256) k_warpq(Geometry g, PairTable pt, uint8_t
         const int fmask = (1 << vb) - 1;
         const int xs = x << vb;
         uint16_t* op = outp + (size_t)(y0 + tg) * w + x;
-#pragma unroll 4
+#pragma unroll kWarpqUnroll
         for (int ty = tg; ty < kQH; ty += 4) {
             const int y = y0 + ty;
             const int4 r = rt[ty];
