@@ -1932,9 +1932,187 @@ __global__ void __launch_bounds__(128, FVV_MINB_BLEND) k_blend(Geometry g, PairT
     }
 }
 
+// k_blend_s: k_blend streamed per pixel -- the same operations in the same
+// order (bit-identical), but each pixel's mask is consumed (blend byte, mask
+// store, chroma pair sum) as soon as it is formed instead of staging 8 masks,
+// the warped luma and the sd window stay packed in their load registers, and
+// the chroma row is split across the row pair (upper lanes U, lower lanes V;
+// both hold the full 2x2 sum: RN((a+b)+(c+d)) either way round).  Its loads
+// (including the chroma sources) are all issued up front.
+#ifndef FVV_BLEND_STREAM
+#define FVV_BLEND_STREAM 1
+#endif
+#ifndef FVV_BLEND_WQ_EARLY
+#define FVV_BLEND_WQ_EARLY 0  // chroma sources loaded with the luma-row inputs (costs 4 live registers)
+#endif
+#ifndef FVV_MINB_BLEND_S
+#define FVV_MINB_BLEND_S 8  // r2 sweep (cfg4 ms per rig frame): 6 / 7 / 8 / 9 / 10 = 1.091 / 1.031 / 0.992 / 1.032 / 1.069 (k_blend 1.166)
+#endif
+template <int FMT>
+__global__ void __launch_bounds__(128, FVV_MINB_BLEND_S) k_blend_s(Geometry g, PairTable pt, const uint8_t* __restrict__ ws,
+                                                   Planes P, int pair_base, bool write_frame,
+                                                   double* mask_out /* nullable: (launch pairs, H, W) */) {
+    pdl_enter();
+    const int W = g.W, H = g.H;
+    const int pair = blockIdx.z + pair_base;
+    const int ng = (W + 7) / 8;
+    const int lane = threadIdx.x & 31;
+    const int rr = lane >> 4;                                               // row within the pair
+    const int gxr = blockIdx.x * (blockDim.x / 2) + (threadIdx.x >> 5) * 16 + (lane & 15);
+    const bool active = gxr < ng;
+    const int gx = active ? gxr : ng - 1;                                   // 8-column group
+    const int yp = blockIdx.y;                                              // row pair
+    const int x0 = gx * 8, n = min(8, W - x0);
+    const uint16_t* sd = cplane<uint16_t>(ws, P, P.sd, pair);
+    const double* carry = cplane<double>(ws, P, P.carry, pair);
+    const float* ol = cplane<float>(ws, P, P.occ_l, pair);
+    const float* orr = cplane<float>(ws, P, P.occ_r, pair);
+    const uint8_t* wl = cplane<uint8_t>(ws, P, P.wl, pair);
+    const uint8_t* wr = cplane<uint8_t>(ws, P, P.wr, pair);
+    uint8_t* out = pt.out[pair];
+    const int y = 2 * yp + rr;
+    const size_t ro = (size_t)y * W;
+    const uint16_t* srow = sd + ro;
+    // ---- loads ----
+    float vl[8], vr[8];
+    uint2 pl = make_uint2(0, 0), pr = make_uint2(0, 0);  // warped luma, 8 bytes per side
+    if (n == 8) {
+        const float4 a = *reinterpret_cast<const float4*>(ol + ro + x0);
+        const float4 b = *reinterpret_cast<const float4*>(ol + ro + x0 + 4);
+        const float4 c = *reinterpret_cast<const float4*>(orr + ro + x0);
+        const float4 d = *reinterpret_cast<const float4*>(orr + ro + x0 + 4);
+        vl[0] = a.x; vl[1] = a.y; vl[2] = a.z; vl[3] = a.w; vl[4] = b.x; vl[5] = b.y; vl[6] = b.z; vl[7] = b.w;
+        vr[0] = c.x; vr[1] = c.y; vr[2] = c.z; vr[3] = c.w; vr[4] = d.x; vr[5] = d.y; vr[6] = d.z; vr[7] = d.w;
+        if (FMT != FVV_RGB8) {  // u8 rows are only 4-byte aligned (W % 4 == 0)
+            pl = make_uint2(*reinterpret_cast<const uint32_t*>(wl + ro + x0), *reinterpret_cast<const uint32_t*>(wl + ro + x0 + 4));
+            pr = make_uint2(*reinterpret_cast<const uint32_t*>(wr + ro + x0), *reinterpret_cast<const uint32_t*>(wr + ro + x0 + 4));
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const int xx = min(x0 + j, W - 1);
+            vl[j] = ol[ro + xx]; vr[j] = orr[ro + xx];
+            if (FMT != FVV_RGB8) {
+                const int sh = 8 * (j & 3);
+                if (j < 4) { pl.x |= (uint32_t)wl[ro + xx] << sh; pr.x |= (uint32_t)wr[ro + xx] << sh; }
+                else { pl.y |= (uint32_t)wl[ro + xx] << sh; pr.y |= (uint32_t)wr[ro + xx] << sh; }
+            }
+        }
+    }
+    // sd[clamp(x0 - 2 + j)], j = 0..10: sa = (s0, s1), sb = (s2 .. s9), s10
+    uint32_t sa;
+    uint4 sb;
+    int s10;
+    if ((W & 7) == 0 && x0 >= 2 && x0 + 8 < W) {
+        sa = *reinterpret_cast<const uint32_t*>(srow + x0 - 2);
+        sb = *reinterpret_cast<const uint4*>(srow + x0);
+        s10 = srow[x0 + 8];
+    } else {
+        uint32_t t[10];
+#pragma unroll
+        for (int j = 0; j < 10; j++) t[j] = srow[clampi(x0 - 2 + j, 0, W - 1)];
+        sa = t[0] | (t[1] << 16);
+        sb = make_uint4(t[2] | (t[3] << 16), t[4] | (t[5] << 16), t[6] | (t[7] << 16), t[8] | (t[9] << 16));
+        s10 = srow[clampi(x0 + 8, 0, W - 1)];
+    }
+    auto sj = [&](int j) -> int {  // j compile time after unrolling
+        const uint32_t wv = j < 2 ? sa : (j < 4 ? sb.x : (j < 6 ? sb.y : (j < 8 ? sb.z : sb.w)));
+        return j == 10 ? s10 : (int)((j & 1) ? (wv >> 16) : (wv & 0xFFFFu));
+    };
+    double tmp = carry[(size_t)y * ng + gx];
+    // chroma sources of this group's 2x2 blocks (Ul, Ur, Vl, Vr), loaded with the rest
+    const int cw = g.cw, chh = g.ch;
+    const int cx0 = x0 / 2, nc = n / 2;
+    uchar4 wq[4];
+    auto load_wq = [&]() {
+        if (FMT == FVV_YUV420 && write_frame && active) {
+            const uchar4* wc = cplane<uchar4>(ws, P, P.wc, pair) + (size_t)yp * cw + cx0;
+            if (nc == 4 && (cw & 3) == 0) {
+                const uint4 v = *reinterpret_cast<const uint4*>(wc);
+                wq[0] = *reinterpret_cast<const uchar4*>(&v.x); wq[1] = *reinterpret_cast<const uchar4*>(&v.y);
+                wq[2] = *reinterpret_cast<const uchar4*>(&v.z); wq[3] = *reinterpret_cast<const uchar4*>(&v.w);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; j++) wq[j] = wc[min(j, nc - 1)];
+            }
+        }
+    };
+#if FVV_BLEND_WQ_EARLY
+    load_wq();
+#endif
+    // ---- per pixel: replay, mask, blend, stores ----
+    uint32_t lo = 0, hi = 0;
+    double csum[4];
+    double pe = 0.0;
+    double* mo = mask_out ? mask_out + (size_t)blockIdx.z * W * H + ro + x0 : nullptr;  // this launch's pair
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+        if (j > 0) tmp = __dadd_rn(tmp, __dsub_rn(d0_of(sj(j + 3)), d0_of(sj(j))));
+        const double m = j < n ? mask_of(tmp, vl[j], vr[j], g) : 0.0;
+        if (write_frame && active) {
+            if (FMT == FVV_RGB8) {
+                if (j < n) {
+                    const uint8_t* px = cplane<uint8_t>(ws, P, P.wrgb, pair) + (ro + x0 + j) * 6;
+                    uint8_t* o = out + (ro + x0 + j) * 3;
+#pragma unroll
+                    for (int ch = 0; ch < 3; ch++) o[ch] = blend_px(m, px[ch], px[3 + ch]);
+                }
+            } else {
+                const int sh = 8 * (j & 3);
+                const uint32_t a = ((j < 4 ? pl.x : pl.y) >> sh) & 0xFFu, b = ((j < 4 ? pr.x : pr.y) >> sh) & 0xFFu;
+                const uint32_t v = (uint32_t)blend_px(m, (int)a, (int)b) << sh;
+                if (j < 4) lo |= v; else hi |= v;
+            }
+        }
+        if (mo && active && j < n) mo[j] = m;
+        if (FMT == FVV_YUV420) {
+            if (j & 1) {
+                const double p = __dadd_rn(pe, m);                               // m(2k) + m(2k+1) of this row
+                const double o = __shfl_xor_sync(0xffffffffu, p, 16);            // the other row's pair sum
+                csum[j >> 1] = rr == 0 ? __dadd_rn(p, o) : __dadd_rn(o, p);      // (a + b) + (c + d)
+            } else {
+                pe = m;
+            }
+        }
+    }
+    if (FMT != FVV_RGB8 && write_frame && active) {
+        *reinterpret_cast<uint32_t*>(out + ro + x0) = lo;  // W % 4 == 0: n is 4 or 8
+        if (n == 8) *reinterpret_cast<uint32_t*>(out + ro + x0 + 4) = hi;
+    }
+    // chroma blend with the 2x2-mean mask (warp.py:83-88): upper lanes U, lower lanes V
+#if !FVV_BLEND_WQ_EARLY
+    load_wq();
+#endif
+    if (FMT == FVV_YUV420 && write_frame && active) {
+        uint8_t* co = out + (size_t)W * H + (size_t)rr * cw * chh + (size_t)yp * cw + cx0;
+        uint32_t pk = 0;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const double mc = __dmul_rn(csum[j], 0.25);  // /4 == *0.25 exactly
+            const uint8_t v = rr == 0 ? blend_px(mc, wq[j].x, wq[j].y) : blend_px(mc, wq[j].z, wq[j].w);
+            pk |= (uint32_t)v << (8 * j);
+        }
+        if (nc == 4 && (cw & 3) == 0) {
+            *reinterpret_cast<uint32_t*>(co) = pk;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; j++)
+                if (j < nc) co[j] = (uint8_t)(pk >> (8 * j));
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // host-side launch helpers (called from api.cu)
 // ---------------------------------------------------------------------------
+using BlendKernel = void (*)(Geometry, PairTable, const uint8_t*, Planes, int, bool, double*);
+static BlendKernel blend_kernel(int fmt) {
+#if FVV_BLEND_STREAM
+    return fmt == FVV_YUV420 ? k_blend_s<FVV_YUV420> : fmt == FVV_RGB8 ? k_blend_s<FVV_RGB8> : k_blend_s<FVV_GRAY8>;
+#else
+    return fmt == FVV_YUV420 ? k_blend<FVV_YUV420> : fmt == FVV_RGB8 ? k_blend<FVV_RGB8> : k_blend<FVV_GRAY8>;
+#endif
+}
 // ---------------------------------------------------------------------------
 // k_sadw: the 8x8-block search for 8-aligned levels (w % 8 == 0) -- pixel-pair
 // packing as k_sadp, restructured so that nearly every issued instruction is
@@ -2631,9 +2809,7 @@ cudaError_t run_interp_stage(const Geometry& g, const PairTable& pt, uint8_t* ws
     B(KC_BLEND);
     {
         const dim3 grd(((g.W + 7) / 8 + 63) / 64, g.H / 2, npairs);
-        e = launch_k(g.pdl, g.fmt == FVV_YUV420 ? k_blend<FVV_YUV420>
-                            : g.fmt == FVV_RGB8 ? k_blend<FVV_RGB8> : k_blend<FVV_GRAY8>,
-                     grd, dim3(128), 0, st, g, pt, ws, P, 0, true, mask_out);
+        e = launch_k(g.pdl, blend_kernel(g.fmt), grd, dim3(128), 0, st, g, pt, ws, P, 0, true, mask_out);
     }
     if (e != cudaSuccess) return e;
     return E();
@@ -2754,10 +2930,8 @@ cudaError_t run_diag(const Geometry& g, const PairTable& pt, uint8_t* ws, const 
     }
     if (mask) {
         const dim3 grd(((g.W + 7) / 8 + 63) / 64, g.H / 2, 1);
-        if (g.fmt == FVV_YUV420) k_blend<FVV_YUV420><<<grd, 128, 0, st>>>(g, pt, ws, P, pair, false, mask);
-        else if (g.fmt == FVV_RGB8) k_blend<FVV_RGB8><<<grd, 128, 0, st>>>(g, pt, ws, P, pair, false, mask);
-        else k_blend<FVV_GRAY8><<<grd, 128, 0, st>>>(g, pt, ws, P, pair, false, mask);
-        return cudaGetLastError();
+        const cudaError_t e = launch_k(false, blend_kernel(g.fmt), grd, dim3(128), 0, st, g, pt, ws, P, pair, false, mask);
+        return e != cudaSuccess ? e : cudaGetLastError();
     }
     return cudaSuccess;
 }
