@@ -5,7 +5,7 @@ synthesized virtual views/s at 1080p; per-rig-frame latency).
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl b200|reference]
 
 One step = a batch of F independent rig frames of the live stream per rank
-(--frames-in-flight, default auto = 3 when they fit a quarter of HBM, else 1; F > 1 run concurrently on forked streams inside one
+(--frames-in-flight, default auto = 6 / 3 / 1, the most that fit a quarter of HBM; F > 1 run concurrently on forked streams inside one
 CUDA graph): every dense view of every camera gap (recursive midpoints,
 server/pipeline.py:254-271) plus every cluster frame (server/pipeline.py:273-292).
 The per-rig-frame latency (one frame in flight) is measured separately and
@@ -238,16 +238,21 @@ def run_b200(args, cfg, rank, world, local_rank):
     total_views = (C - 1) * (1 << S) + 1
     max_pairs = (C - 1) * (1 << (S - 1))
     npairs_total = step_views  # interpolations per rig frame
-    # frames in flight: --frames-in-flight N, or 0 = auto (3 when three rig frames' engines,
-    # views and clusters take under a quarter of HBM, else 1: cfg5's 48 GB engines stay single)
+    # frames in flight: --frames-in-flight N, or 0 = auto (the largest of 6 / 3 / 1 whose rig
+    # frames' engines, views and clusters take under a quarter of HBM: cfg1-4 run 6, cfg5's 48 GB
+    # engines stay single; r2 v8 sweep F = 1 / 3 / 6 / 10: cfg1 7151 / 19314 / 35543 / 49381,
+    # cfg2 7485 / 9337 / 10489 / 10693, cfg3 10273 / 11034 / 11253 / 11273 views/s at the same
+    # per-frame latency)
     F_req = args.frames_in_flight
-    F = max(1, F_req) if F_req > 0 else 3
+    F = max(1, F_req) if F_req > 0 else 6
     engines, cams_l, views_l, clusters_l, hosts = [], [], [], [], []
-    for i in range(F):
+    i = 0
+    while i < F:
         if F_req <= 0 and i == 1:
             per = engines[0].workspace_bytes + views_l[0].numel() + (clusters_l[0].numel() if vps else 0)
-            if 3 * per > 0.25 * torch.cuda.get_device_properties(dev).total_memory:
-                F = 1
+            quarter = 0.25 * torch.cuda.get_device_properties(dev).total_memory
+            F = next(f for f in (6, 3, 1) if f == 1 or f * per <= quarter)
+            if F == 1:
                 break
         e = Interpolator(W, H, fmt, max_pairs=max_pairs, device=dev)
         h = torch.from_numpy(synth_rig(W, H, fmt, C, seed=42 + rank * 8 + i)).pin_memory()
@@ -258,6 +263,7 @@ def run_b200(args, cfg, rank, world, local_rank):
         if vps:
             sizes = rig_cluster_sizes(W, H, fmt, C, S, vps)
             clusters_l.append(torch.empty(sum(sizes), dtype=torch.uint8, device=dev))
+        i += 1
     eng, cams, views = engines[0], cams_l[0], views_l[0]
     clusters = clusters_l[0] if vps else None
     results = clusters_l if vps else views_l
