@@ -1141,6 +1141,12 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
 #ifndef FVV_MASK2_PF
 #define FVV_MASK2_PF 0  // luma taps loaded one row ahead: r2 sweep 3.79 -> 3.94 ms (128 regs, spills), off
 #endif
+#ifndef FVV_MASK2_DLERP
+#define FVV_MASK2_DLERP 0  // row lerps from (scaled base, difference) pairs, one IMAD per component: parity green, but more spills at 96 registers (r2 v8: 3.51 -> 3.66 ms), off
+#endif
+#if FVV_MASK2_DLERP && (FVV_MASK2_PF || !FVV_MASK2_HB_CACHE)
+#error "FVV_MASK2_DLERP needs the block-grid row cache and no tap prefetch"
+#endif
 #if FVV_MASK2_PF && !FVV_MASK2_HB_CACHE
 #error "FVV_MASK2_PF needs the block-grid row cache"
 #endif
@@ -1360,8 +1366,17 @@ __global__ void __launch_bounds__(kM2Warps * 32, FVV_MINB_MASK2) k_mask_cols2(Ge
             for (int d = 0; d < 2; d++)
 #pragma unroll
                 for (int c = 0; c < 2; c++) {
+#if FVV_MASK2_DLERP
+                    // (hu0, hu1) = (4 u0, u1 - u0): the row lerp is one multiply-add per component
+                    const int2 a = ty.i0 == ua + 1 ? make_int2((hu0[d][c].x >> 2) + hu1[d][c].x, (hu0[d][c].y >> 2) + hu1[d][c].y)
+                                                   : xl_u(d, ty.i0, c);
+                    const int2 b = xl_u(d, ty.i0 + 1, c);
+                    hu0[d][c] = make_int2(a.x << 2, a.y << 2);
+                    hu1[d][c] = make_int2(b.x - a.x, b.y - a.y);
+#else
                     hu0[d][c] = ty.i0 == ua + 1 ? hu1[d][c] : xl_u(d, ty.i0, c);
                     hu1[d][c] = xl_u(d, ty.i0 + 1, c);
+#endif
                 }
 #if FVV_MASK2_FPF
             // the flow row the next reload reads (two walker rows on), into L1 now:
@@ -1381,8 +1396,17 @@ __global__ void __launch_bounds__(kM2Warps * 32, FVV_MINB_MASK2) k_mask_cols2(Ge
             for (int d = 0; d < 2; d++)
 #pragma unroll
                 for (int c = 0; c < 2; c++) {
+#if FVV_MASK2_DLERP
+                    // (hb0, hb1) = (D2 p, q - p)
+                    const int2 a = tby.i0 == ba + 1 ? make_int2((hb0[d][c].x >> lgD2) + hb1[d][c].x, (hb0[d][c].y >> lgD2) + hb1[d][c].y)
+                                                    : xl_b(d, tby.i0, c);
+                    const int2 b = xl_b(d, tby.i1, c);
+                    hb0[d][c] = make_int2(a.x << lgD2, a.y << lgD2);
+                    hb1[d][c] = make_int2(b.x - a.x, b.y - a.y);
+#else
                     hb0[d][c] = tby.i0 == ba + 1 ? hb1[d][c] : xl_b(d, tby.i0, c);
                     hb1[d][c] = xl_b(d, tby.i1, c);
+#endif
                 }
 #if FVV_MASK2_HPF
             if (tby.i1 + 1 < L2.nby) {
@@ -1410,8 +1434,13 @@ __global__ void __launch_bounds__(kM2Warps * 32, FVV_MINB_MASK2) k_mask_cols2(Ge
             int fx[2];
 #pragma unroll
             for (int c = 0; c < 2; c++) {
+#if FVV_MASK2_DLERP
+                const int2 base = make_int2(hu0[d][c].x + ty.f * hu1[d][c].x, hu0[d][c].y + ty.f * hu1[d][c].y);
+                const int2 res = make_int2(hb0[d][c].x + tby.f * hb1[d][c].x, hb0[d][c].y + tby.f * hb1[d][c].y);
+#else
                 const int2 base = lerp_i2(hu0[d][c], hu1[d][c], 4, ty.f);
                 const int2 res = lerp_i2(hb0[d][c], hb1[d][c], D2, tby.f);
+#endif
                 Fpp_y[d][c] = Fp[d][c].y;
                 Fp[d][c] = Fc[d][c];
                 Fc[d][c] = make_int2(-((base.x << bs) + (res.x << rs)), -((base.y << bs) + (res.y << rs)));
