@@ -1142,7 +1142,7 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
 #define FVV_MASK2_PF 0  // luma taps loaded one row ahead: r2 sweep 3.79 -> 3.94 ms (128 regs, spills), off
 #endif
 #ifndef FVV_MASK2_DLERP
-#define FVV_MASK2_DLERP 0  // row lerps from (scaled base, difference) pairs, one IMAD per component: parity green, but more spills at 96 registers (r2 v8: 3.51 -> 3.66 ms), off
+#define FVV_MASK2_DLERP 0  // row lerps from (scaled base, difference) pairs, one IMAD per component: timed-path parity green, but more spills at 96 registers (r2 v8: 3.51 -> 3.66 ms), off
 #endif
 #if FVV_MASK2_DLERP && (FVV_MASK2_PF || !FVV_MASK2_HB_CACHE)
 #error "FVV_MASK2_DLERP needs the block-grid row cache and no tap prefetch"

@@ -75,7 +75,7 @@ def _smooth_pair(rng, w, h, fmt, shift):
                                      (36, 20, 0), (8, 8, 1), (4, 4, 0), (44, 12, 2),
                                      # 4:2:0 with W % 8 == 4 (a half last 8-column group, chroma width
                                      # % 4 == 2: the blend's unaligned chroma path)
-                                     (132, 40, 1), (60, 26, 1), (52, 100, 0)])
+                                     (132, 40, 1), (60, 28, 1), (52, 100, 0)])
 def test_random_pairs_batched_vs_oracle(torch_cuda, w, h, fmt):
     rng = np.random.default_rng(w * 1000 + h * 10 + fmt)
     lefts, rights = [], []
