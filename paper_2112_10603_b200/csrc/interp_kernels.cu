@@ -656,6 +656,7 @@ __global__ void __launch_bounds__(256) k_flow(Geometry g, uint8_t* __restrict__ 
     __shared__ int2 hu[kFH / 2 + 3][kFW];   // x-lerped rows of flow_{L-1}
     __shared__ int2 hb[kFH / 2 + 3][kFW];   // x-lerped block rows (B >= 2)
     __shared__ ITap cu[kFW], cb[kFW];
+    __shared__ int4 rtab[kFH];  // per tile row: block-grid y tap (i0 - b_lo, i1 - b_lo, f), base-flow y tap (i0 - s_lo, i1 - s_lo) packed
     const Level L = g.lv[LEVEL];
     const int pair = blockIdx.z >> 1, d = blockIdx.z & 1;
     const int x0 = blockIdx.x * kFW, y0 = blockIdx.y * kFH;
@@ -672,6 +673,16 @@ __global__ void __launch_bounds__(256) k_flow(Geometry g, uint8_t* __restrict__ 
     const int b_n = clamp_itap32(2 * ylast - B + 1, lgD, L.nby).i1 - b_lo + 1;
     const int s_lo = LEVEL > 0 ? clamp_itap32(2 * y0 - 1, 2, Lp.h).i0 : 0;
     const int s_n = LEVEL > 0 ? clamp_itap32(2 * ylast - 1, 2, Lp.h).i1 - s_lo + 1 : 0;
+    if (tid < kFH) {  // the row taps, once per tile instead of once per pixel
+        const int y = min(y0 + tid, L.h - 1);
+        const ITap t = clamp_itap32(2 * y - B + 1, lgD, L.nby);
+        int w = 0;
+        if (LEVEL > 0) {
+            const ITap u = clamp_itap32(2 * y - 1, 2, Lp.h);
+            w = (u.i0 - s_lo) | ((u.i1 - s_lo) << 8) | (u.f << 16);  // indices < kFH / 2 + 3, f <= 4
+        }
+        rtab[tid] = make_int4(t.i0 - b_lo, t.i1 - b_lo, t.f, w);
+    }
     __syncthreads();
     const BlockHit* hit = cplane<BlockHit>(ws, P, P.hit[LEVEL][d], pair);
     for (int row = tg; row < b_n; row += 4) {
@@ -697,12 +708,11 @@ __global__ void __launch_bounds__(256) k_flow(Geometry g, uint8_t* __restrict__ 
     for (int ty = tg; ty < kFH; ty += 4) {
         const int y = y0 + ty;
         if (y >= L.h) break;
-        const ITap t = clamp_itap32(2 * y - B + 1, lgD, L.nby);
-        const int2 res = lerp_i2(hb[t.i0 - b_lo][tx], hb[t.i1 - b_lo][tx], D, t.f);
+        const int4 rt = rtab[ty];
+        const int2 res = lerp_i2(hb[rt.x][tx], hb[rt.y][tx], D, rt.z);
         int2 f = make_int2(res.x << rs, res.y << rs);
         if (LEVEL > 0) {
-            const ITap u = clamp_itap32(2 * y - 1, 2, Lp.h);
-            const int2 base = lerp_i2(hu[u.i0 - s_lo][tx], hu[u.i1 - s_lo][tx], 4, u.f);
+            const int2 base = lerp_i2(hu[rt.w & 0xFF][tx], hu[(rt.w >> 8) & 0xFF][tx], 4, rt.w >> 16);
             f.x += base.x << bs;
             f.y += base.y << bs;
         }
