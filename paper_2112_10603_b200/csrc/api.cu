@@ -770,6 +770,7 @@ static int cluster_jobs_of(const fvv_frame_desc* d, int ncams, int stages, int v
         off += b;
         *maxb = std::max(*maxb, b);
     }
+    if (*maxb >= (1l << 31)) return fail(FVV_ELAYOUT, "a cluster frame of 2^31 bytes or more");  // 32-bit kernel indexing
     return FVV_OK;
 }
 

@@ -143,16 +143,18 @@ __global__ void k_rig_clusters(FrameDims fd, ClusterJobs jobs, ViewSrc vs,
     const uint8_t* __restrict__ views = vs.views;
     const ClusterJob jb = jobs.job[blockIdx.z];
     const int sw = jb.sw, sh = fd.H;
-    const long ysz = (long)sw * sh;
-    const long csz = (long)(sw / 2) * (sh / 2);
-    const long total = fd.fmt == FVV_YUV420 ? ysz + 2 * csz : ysz;
-    const long o = ((long)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    // 32-bit index math (a cluster frame is < 2^31 bytes: checked on the host): the
+    // 64-bit divisions this replaces are software sequences of ~70 instructions each
+    const unsigned ysz = (unsigned)sw * sh;
+    const unsigned csz = (unsigned)(sw / 2) * (sh / 2);
+    const unsigned total = fd.fmt == FVV_YUV420 ? ysz + 2 * csz : ysz;
+    const unsigned o = (blockIdx.x * blockDim.x + threadIdx.x) * 4u;
     if (o >= total) return;
     int p = 0;
-    long r = o;
-    if (o >= ysz) { p = 1 + (int)((o - ysz) / csz); r = (o - ysz) - (p - 1) * csz; }
-    const int pw = p ? sw / 2 : sw;
-    const int y = (int)(r / pw), x = (int)(r % pw);
+    unsigned r = o;
+    if (o >= ysz) { p = o - ysz >= csz ? 2 : 1; r = (o - ysz) - (p - 1) * csz; }
+    const unsigned pw = p ? sw / 2 : sw;
+    const int y = (int)(r / pw), x = (int)(r - (unsigned)y * pw);
     const int W = fd.W, H = fd.H;
     const int cellw = W / 4, cellh = H / 4;
     const int bx = p ? 2 * x : x, byy = p ? 2 * y : y;  // luma-grid position
