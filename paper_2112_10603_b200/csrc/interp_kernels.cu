@@ -2174,7 +2174,10 @@ static BlendKernel blend_kernel(int fmt) {
 // CG is even, so every group shares the pair parity of group 0.  Same exact integer SAD as k_sad.
 // ---------------------------------------------------------------------------
 #ifndef FVV_MINB_SADW
-#define FVV_MINB_SADW(side) ((side) > 13 ? 2 : ((side) > 9 ? 3 : 4))
+#define FVV_MINB_SADW(side) ((side) > 13 ? FVV_MINB_SADW25 : ((side) > 9 ? 3 : 4))
+#endif
+#ifndef FVV_MINB_SADW25
+#define FVV_MINB_SADW25 2
 #endif
 #ifdef FVV_DEBUG
 #include <cassert>
@@ -2186,7 +2189,11 @@ template <int SIDE, int CG, int RB_ = 0>
 struct SadW {
     static constexpr int R = SIDE / 2;
     static constexpr int NG = (SIDE + CG - 1) / CG;        // dx groups per dy row
-    static constexpr int NBY = (256 / (8 * SIDE * NG)) > 0 ? 256 / (8 * SIDE * NG) : 1;
+#ifndef FVV_SADW_NBY25
+#define FVV_SADW_NBY25 0  // > 0: block rows per CTA at 25x25 (default 1: 200 of 224 lanes per dx group busy); r2 sweep NBY 2 (min blocks 1): 1.04 -> 1.12 ms, off
+#endif
+    static constexpr int NBY = (SIDE == 25 && FVV_SADW_NBY25 > 0) ? FVV_SADW_NBY25
+                             : (256 / (8 * SIDE * NG)) > 0 ? 256 / (8 * SIDE * NG) : 1;
     static constexpr int NB = 8 * NBY;                     // blocks per CTA (8 x NBY)
     static constexpr int TPG = ((NB * SIDE + 31) / 32) * 32; // threads per dx group (whole warps)
     static constexpr int THREADS = TPG * NG;
