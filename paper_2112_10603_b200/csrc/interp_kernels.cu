@@ -1151,6 +1151,12 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
 #ifndef FVV_MASK2_PF
 #define FVV_MASK2_PF 0  // luma taps loaded one row ahead: r2 sweep 3.79 -> 3.94 ms (128 regs, spills), off
 #endif
+#ifndef FVV_MASK2_RTAB
+#define FVV_MASK2_RTAB 0  // walker rows' y taps from a per-CTA shared table: r2 sweep 3.49 -> 3.55 ms (more spills), off
+#endif
+#if FVV_MASK2_RTAB && FVV_MASK2_PF
+#error "FVV_MASK2_RTAB is for the default (no tap prefetch) walker"
+#endif
 #ifndef FVV_MASK2_DLERP
 #define FVV_MASK2_DLERP 0  // row lerps from (scaled base, difference) pairs, one IMAD per component: timed-path parity green, but more spills at 96 registers (r2 v8: 3.51 -> 3.66 ms), off
 #endif
@@ -1172,6 +1178,22 @@ __global__ void __launch_bounds__(kM2Warps * 32, FVV_MINB_MASK2) k_mask_cols2(Ge
     const int pair = blockIdx.z;
     const int y0 = blockIdx.y * kMH;
     const int xw0 = (blockIdx.x * kM2Warps + wid) * kM2Own;  // even
+#if FVV_MASK2_RTAB
+    // the walker rows' y taps (level-1 flow rows, level-2 block rows), once per CTA:
+    // rows ys .. ye as (ty.i0, ty.f, tby.i0, tby.i1 | tby.f << 16)
+    __shared__ int4 rtab[kMH + 4];
+    {
+        const int ys_ = max(0, y0 - 2), ye_ = min(H - 1, y0 + kMH + 1);
+        const int B2_ = g.lv[2].block, lg_ = 31 - __clz(2 * B2_);
+        for (int i = threadIdx.x; i <= ye_ - ys_; i += blockDim.x) {
+            const int yy = ys_ + i;
+            const Tap2 t = tap2(2 * yy - 1, 2, g.lv[1].h);
+            const ITap b = clamp_itap32(2 * yy - B2_ + 1, lg_, g.lv[2].nby);
+            rtab[i] = make_int4(t.i0, t.f, b.i0, b.i1 | (b.f << 16));
+        }
+        __syncthreads();  // the only block-level barrier: before any warp leaves
+    }
+#endif
     if (xw0 >= W) return;
     const int xa = xw0 - 2 + 2 * lane;  // this lane's columns xa, xa + 1 (xa even)
     int xcl[2], gmul[2];
@@ -1370,7 +1392,14 @@ __global__ void __launch_bounds__(kM2Warps * 32, FVV_MINB_MASK2) k_mask_cols2(Ge
             issue(yy + 1);
         }
 #else
+#if FVV_MASK2_RTAB
+        const int4 rtv = rtab[yy - ys];
+        Tap2 ty;
+        ty.i0 = rtv.x;
+        ty.f = rtv.y;
+#else
         const Tap2 ty = tap2(2 * yy - 1, 2, L1.h);
+#endif
         if (ty.i0 != ua) {
 #pragma unroll
             for (int d = 0; d < 2; d++)
@@ -1399,7 +1428,14 @@ __global__ void __launch_bounds__(kM2Warps * 32, FVV_MINB_MASK2) k_mask_cols2(Ge
 #endif
             ua = ty.i0;
         }
+#if FVV_MASK2_RTAB
+        ITap tby;
+        tby.i0 = rtv.z;
+        tby.i1 = rtv.w & 0xFFFF;
+        tby.f = rtv.w >> 16;
+#else
         const ITap tby = clamp_itap32(2 * yy - B2 + 1, lgD2, L2.nby);
+#endif
 #if FVV_MASK2_HB_CACHE
         if (tby.i0 != ba) {
 #pragma unroll
