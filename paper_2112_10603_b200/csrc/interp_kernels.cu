@@ -732,6 +732,9 @@ constexpr int kQH = 64, kQW = 64;  // 16 pixels per thread amortise the tile set
 #define FVV_WARPQ_UNROLL 4  // interior loop unroll (16 rows per thread)
 #endif
 constexpr int kWarpqUnroll = FVV_WARPQ_UNROLL;
+#ifndef FVV_WARPQ_PAIR
+#define FVV_WARPQ_PAIR 1  // interior tiles: two adjacent columns per thread
+#endif
 #ifndef FVV_WARPQ_L1PF
 #define FVV_WARPQ_L1PF 0  // > 0: L1 prefetch of the luma row this many iterations ahead (r2 sweep 1/2/4: no change), off
 #endif
@@ -739,7 +742,7 @@ template <int LEVEL>
 __global__ void __launch_bounds__(256) k_warpq(Geometry g, PairTable pt, uint8_t* __restrict__ ws,
                                                Planes P) {
     pdl_enter();
-    __shared__ int2 h[kQH / 2 + 3][kQW];
+    __shared__ __align__(16) int2 h[kQH / 2 + 3][kQW];
     __shared__ ITap cxt[kQW];
     __shared__ int4 rt[kQH];  // per tile row: base-flow y tap (i0 - s_lo, i1 - s_lo, f)
     const Level& L = g.lv[LEVEL];
@@ -763,8 +766,6 @@ __global__ void __launch_bounds__(256) k_warpq(Geometry g, PairTable pt, uint8_t
         h[row][tx] = lerp_i2(pr[t.i0], pr[t.i1], 4, t.f);
     }
     __syncthreads();
-    const int x = x0 + tx;
-    if (x >= L.w) return;
     const int vb = g.fb[LEVEL - 1] + 3;
     const int w = L.w;
     uint16_t* outp = plane<uint16_t>(ws, P, LEVEL == 1 ? P.tq1[d] : P.tq2[d], pair);
@@ -773,6 +774,48 @@ __global__ void __launch_bounds__(256) k_warpq(Geometry g, PairTable pt, uint8_t
                                           : (d ? pt.left[pair] : pt.right[pair]);
     const int M = g.qmargin[LEVEL];
     const bool interior = x0 >= M && x0 + kQW - 1 + M <= w - 2 && y0 >= M && y0 + kQH - 1 + M <= L.h - 2;
+#if FVV_WARPQ_PAIR
+    if (interior) {
+        // two adjacent columns per thread (x, x + 1; 8 rows apart per step): one 16-byte
+        // read of the x-lerped base rows and one 32-bit store serve both pixels
+        const int k = LEVEL == 1 ? 2 * vb - 1 : 2 * vb - 3;
+        const int fmask = (1 << vb) - 1;
+        const int px = tid & 31, rg = tid >> 5;
+        const int xp = x0 + 2 * px;
+        const int xs0 = xp << vb, xs1 = (xp + 1) << vb;
+        uint32_t* op = reinterpret_cast<uint32_t*>(outp + (size_t)(y0 + rg) * w + xp);  // xp, w even
+#pragma unroll kWarpqUnroll
+        for (int ty = rg; ty < kQH; ty += 8) {
+            const int y = y0 + ty;
+            const int4 r = rt[ty];
+            const int4 ha = *reinterpret_cast<const int4*>(&h[r.x][2 * px]);
+            const int4 hb = *reinterpret_cast<const int4*>(&h[r.y][2 * px]);
+            const int2 bc[2] = {lerp_i2(make_int2(ha.x, ha.y), make_int2(hb.x, hb.y), 4, r.z),
+                                lerp_i2(make_int2(ha.z, ha.w), make_int2(hb.z, hb.w), 4, r.z)};
+            uint32_t q[2];
+#pragma unroll
+            for (int c = 0; c < 2; c++) {
+                const int sx = (c ? xs1 : xs0) + bc[c].x, sy = (y << vb) + bc[c].y;
+                const int fx = sx & fmask, fy = sy & fmask;
+                const int off = (sy >> vb) * w + (sx >> vb);
+                int a, b, cc, e;
+                if (LEVEL == 1) {
+                    const uint16_t* p0 = s4 + (unsigned)off;
+                    a = p0[0]; b = p0[1]; cc = p0[w]; e = p0[w + 1];
+                } else {
+                    const uint8_t* p0 = yp + (unsigned)off;
+                    a = p0[0]; b = p0[1]; cc = p0[w]; e = p0[w + 1];
+                }
+                q[c] = (uint32_t)rne64((long long)bilerp_u(a, b, cc, e, fx, fy, vb), k);
+            }
+            *op = q[0] | (q[1] << 16);
+            op += 4 * (size_t)w;  // 8 rows of u16 pairs
+        }
+        return;
+    }
+#endif
+    const int x = x0 + tx;
+    if (x >= L.w) return;
     if (interior) {
         // every sample position (x, y) + base lies in [0, n-2] + [0, 1): no clamping,
         // taps are a shift and a mask (bit-identical to the clamped form here)
