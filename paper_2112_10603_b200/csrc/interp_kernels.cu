@@ -887,7 +887,10 @@ __global__ void __launch_bounds__(256) k_warpq(Geometry g, PairTable pt, uint8_t
 // padding for smooth3.  No shared memory, no index division.
 // ---------------------------------------------------------------------------
 #ifndef FVV_KMH
-#define FVV_KMH 64
+// walker band height: r2 v10 sweep (cfg4, 6 rig frames in flight; views/s and the one-frame
+// k_mask_cols2 ms) 32: 11392 / 3.62, 48: 11592 / 3.50, 64: 11697 / 3.49, 96: 11782 / 3.49,
+// 128: 11833 / 3.65 -- 96 is the largest band without a one-frame latency cost (fewer halo rows)
+#define FVV_KMH 96
 #endif
 #ifndef FVV_MASK_UNROLL
 #define FVV_MASK_UNROLL 1
@@ -1168,7 +1171,7 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
 // nearest / one-sided neighbours at the frame edges.
 // ---------------------------------------------------------------------------
 #ifndef FVV_MINB_MASK2
-#define FVV_MINB_MASK2 5  // r2 sweep: 4 (128 regs, no spills) 4.03 ms, 5 (96 regs) 3.85 ms per cfg4 step
+#define FVV_MINB_MASK2 5  // r2 sweep: 4 (128 regs, no spills) 4.03 ms, 5 (96 regs) 3.85 ms per cfg4 step; r2 v10 (6 frames in flight): 4 = +0.9 % views/s but +0.19 ms one-frame latency, 6 = -1.4 %
 #endif
 #ifndef FVV_MASK2_HB_CACHE
 #define FVV_MASK2_HB_CACHE 1
