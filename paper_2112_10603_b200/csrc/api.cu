@@ -135,6 +135,7 @@ void make_geometry(const fvv_frame_desc* d, const fvv_interp_params* p, Geometry
     g->sadw_rb_min_ctas = kSadwRbMinCtasDefault;
     g->mask_cols2 = FVV_MASK_COLS2;
     g->pdl = FVV_PDL;
+    g->mh = 64;  // the mask walker band height; run_interp picks it per launch
 }
 
 // workspace = [header: candidate tables][pair slot 0][pair slot 1]...

@@ -887,10 +887,19 @@ __global__ void __launch_bounds__(256) k_warpq(Geometry g, PairTable pt, uint8_t
 // padding for smooth3.  No shared memory, no index division.
 // ---------------------------------------------------------------------------
 #ifndef FVV_KMH
-// walker band height: r2 v10 sweep (cfg4, 6 rig frames in flight; views/s and the one-frame
-// k_mask_cols2 ms) 32: 11392 / 3.62, 48: 11592 / 3.50, 64: 11697 / 3.49, 96: 11782 / 3.49,
-// 128: 11833 / 3.65 -- 96 is the largest band without a one-frame latency cost (fewer halo rows)
-#define FVV_KMH 96
+// walker band height (Geometry::mh, chosen per launch): r2 v10 sweep (cfg4, 6 rig frames in
+// flight; views/s and the one-frame k_mask_cols2 ms) 32: 11392 / 3.62, 48: 11592 / 3.50,
+// 64: 11697 / 3.49, 96: 11782 / 3.49, 128: 11833 / 3.65.  96-row bands cut the halo rows but
+// also the CTAs: small launches (cfg1, cfg2's 1-4 pair stages) lose latency with them
+// (cfg1 0.15 -> 0.19 ms, cfg2 0.95 -> 1.08 ms), so launches of fewer than kMaskBigCtas
+// 96-row CTAs keep 64-row bands.
+#define FVV_KMH 64
+#endif
+#ifndef FVV_KMH_BIG
+#define FVV_KMH_BIG 96
+#endif
+#ifndef FVV_MASK_BIG_CTAS
+#define FVV_MASK_BIG_CTAS 1480  // two waves of 5 CTAs per SM on 148 SMs
 #endif
 #ifndef FVV_MASK_UNROLL
 #define FVV_MASK_UNROLL 1
@@ -907,7 +916,7 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
     const int W = g.W, H = g.H;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int pair = blockIdx.z;
-    const int y0 = blockIdx.y * kMH;
+    const int y0 = blockIdx.y * g.mh;
     const int xw0 = (blockIdx.x * kMWarps + wid) * kMW;
     if (xw0 >= W) return;  // whole warp outside the frame (no block-level sync in this kernel)
     const int x = xw0 - 2 + lane;
@@ -936,8 +945,8 @@ __global__ void __launch_bounds__(kMWarps * 32, FVV_MINB_MASK) k_mask_cols(Geome
     float* o_ol = plane<float>(ws, P, P.occ_l, pair);
     float* o_or = plane<float>(ws, P, P.occ_r, pair);
     const float oscale = 1.0f / (float)(1 << (mb + 1));
-    const int ys = max(0, y0 - 2), ye = min(H - 1, y0 + kMH + 1);
-    const int yo1 = min(H, y0 + kMH);  // output rows [y0, yo1)
+    const int ys = max(0, y0 - 2), ye = min(H - 1, y0 + g.mh + 1);
+    const int yo1 = min(H, y0 + g.mh);  // output rows [y0, yo1)
 
     auto xl_u = [&](int d, int row) {
         const int2* r = f1[d] + row * L1.w;
@@ -1222,14 +1231,14 @@ __global__ void __launch_bounds__(kM2Warps * 32, FVV_MINB_MASK2) k_mask_cols2(Ge
     const int W = g.W, H = g.H;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int pair = blockIdx.z;
-    const int y0 = blockIdx.y * kMH;
+    const int y0 = blockIdx.y * g.mh;
     const int xw0 = (blockIdx.x * kM2Warps + wid) * kM2Own;  // even
 #if FVV_MASK2_RTAB
     // the walker rows' y taps (level-1 flow rows, level-2 block rows), once per CTA:
     // rows ys .. ye as (ty.i0, ty.f, tby.i0, tby.i1 | tby.f << 16)
-    __shared__ int4 rtab[kMH + 4];
+    __shared__ int4 rtab[(kMH > FVV_KMH_BIG ? kMH : FVV_KMH_BIG) + 4];
     {
-        const int ys_ = max(0, y0 - 2), ye_ = min(H - 1, y0 + kMH + 1);
+        const int ys_ = max(0, y0 - 2), ye_ = min(H - 1, y0 + g.mh + 1);
         const int B2_ = g.lv[2].block, lg_ = 31 - __clz(2 * B2_);
         for (int i = threadIdx.x; i <= ye_ - ys_; i += blockDim.x) {
             const int yy = ys_ + i;
@@ -1276,8 +1285,8 @@ __global__ void __launch_bounds__(kM2Warps * 32, FVV_MINB_MASK2) k_mask_cols2(Ge
     float* o_or = plane<float>(ws, P, P.occ_r, pair);
     uchar4* o_wc = FMT == FVV_YUV420 ? plane<uchar4>(ws, P, P.wc, pair) : nullptr;
     const double c3k = 0x1.5555555555555p-2 * (double)(1.0f / (float)(1 << (mb + 1)));  // exact
-    const int ys = max(0, y0 - 2), ye = min(H - 1, y0 + kMH + 1);
-    const int yo1 = min(H, y0 + kMH);
+    const int ys = max(0, y0 - 2), ye = min(H - 1, y0 + g.mh + 1);
+    const int yo1 = min(H, y0 + g.mh);
 
     // neighbour values of a per-column quantity v[2] with the edge rules folded in
     auto nbrs = [&](const int (&v)[2], int (&l)[2], int (&r)[2]) {
@@ -2913,15 +2922,20 @@ cudaError_t run_interp_stage(const Geometry& g, const PairTable& pt, uint8_t* ws
     if (e != cudaSuccess || (e = E()) != cudaSuccess) return e;
 
     B(KC_MASK_PROD);
-    if (g.fmt != FVV_RGB8 && g.mask_cols2) {
-        const dim3 grd((g.W + kM2Own * kM2Warps - 1) / (kM2Own * kM2Warps), (g.H + kMH - 1) / kMH, npairs);
-        e = launch_k(g.pdl, g.fmt == FVV_YUV420 ? k_mask_cols2<FVV_YUV420> : k_mask_cols2<FVV_GRAY8>, grd,
-                     dim3(kM2Warps * 32), 0, st, g, pt, ws, P);
-    } else {
-        const dim3 grd((g.W + kMW * kMWarps - 1) / (kMW * kMWarps), (g.H + kMH - 1) / kMH, npairs);
-        e = launch_k(g.pdl, g.fmt == FVV_YUV420 ? k_mask_cols<FVV_YUV420>
-                            : g.fmt == FVV_RGB8 ? k_mask_cols<FVV_RGB8> : k_mask_cols<FVV_GRAY8>,
-                     grd, dim3(kMWarps * 32), 0, st, g, pt, ws, P);
+    {
+        const bool two = g.fmt != FVV_RGB8 && g.mask_cols2;
+        const int cols = two ? kM2Own * kM2Warps : kMW * kMWarps;
+        const long big = (long)((g.W + cols - 1) / cols) * ((g.H + FVV_KMH_BIG - 1) / FVV_KMH_BIG) * npairs;
+        Geometry gm = g;
+        gm.mh = big >= FVV_MASK_BIG_CTAS ? FVV_KMH_BIG : kMH;
+        const dim3 grd((g.W + cols - 1) / cols, (g.H + gm.mh - 1) / gm.mh, npairs);
+        if (two)
+            e = launch_k(g.pdl, g.fmt == FVV_YUV420 ? k_mask_cols2<FVV_YUV420> : k_mask_cols2<FVV_GRAY8>, grd,
+                         dim3(kM2Warps * 32), 0, st, gm, pt, ws, P);
+        else
+            e = launch_k(g.pdl, g.fmt == FVV_YUV420 ? k_mask_cols<FVV_YUV420>
+                                : g.fmt == FVV_RGB8 ? k_mask_cols<FVV_RGB8> : k_mask_cols<FVV_GRAY8>,
+                         grd, dim3(kMWarps * 32), 0, st, gm, pt, ws, P);
     }
     if (e != cudaSuccess || (e = E()) != cudaSuccess) return e;
 
