@@ -650,11 +650,14 @@ __global__ void __launch_bounds__(256, FVV_MINB_SADP) k_sadp(Geometry g, PairTab
 // terms are evaluated separably per 16x64 tile (x-lerp rows, then y-lerp).
 // ---------------------------------------------------------------------------
 constexpr int kFH = 64, kFW = 64;
+#ifndef FVV_FLOW_PAIR
+#define FVV_FLOW_PAIR 1
+#endif
 template <int LEVEL>
 __global__ void __launch_bounds__(256) k_flow(Geometry g, uint8_t* __restrict__ ws, Planes P) {
     pdl_enter();
-    __shared__ int2 hu[kFH / 2 + 3][kFW];   // x-lerped rows of flow_{L-1}
-    __shared__ int2 hb[kFH / 2 + 3][kFW];   // x-lerped block rows (B >= 2)
+    __shared__ __align__(16) int2 hu[kFH / 2 + 3][kFW];   // x-lerped rows of flow_{L-1}
+    __shared__ __align__(16) int2 hb[kFH / 2 + 3][kFW];   // x-lerped block rows (B >= 2)
     __shared__ ITap cu[kFW], cb[kFW];
     __shared__ int4 rtab[kFH];  // per tile row: block-grid y tap (i0 - b_lo, i1 - b_lo, f), base-flow y tap (i0 - s_lo, i1 - s_lo) packed
     const Level L = g.lv[LEVEL];
@@ -700,11 +703,49 @@ __global__ void __launch_bounds__(256) k_flow(Geometry g, uint8_t* __restrict__ 
         }
     }
     __syncthreads();
-    const int x = x0 + tx;
-    if (x >= L.w) return;
     const int rs = g.fb[LEVEL] - g.rb[LEVEL];
     const int bs = LEVEL > 0 ? g.fb[LEVEL] - (g.fb[LEVEL - 1] + 3) : 0;
     int2* out = plane<int2>(ws, P, LEVEL == 0 ? P.flow0[d] : P.flow1[d], pair);
+#if FVV_FLOW_PAIR
+    {
+        // two adjacent columns per thread (8 rows apart per step): 16-byte reads of the
+        // x-lerped rows, one 16-byte store when the row pitch keeps it aligned
+        const int px = tid & 31, rg = tid >> 5;
+        const int xq = x0 + 2 * px;
+        if (xq >= L.w) return;
+        const bool two = xq + 1 < L.w, vec = two && (L.w & 1) == 0;
+        for (int ty = rg; ty < kFH; ty += 8) {
+            const int y = y0 + ty;
+            if (y >= L.h) break;
+            const int4 rt = rtab[ty];
+            const int4 ba = *reinterpret_cast<const int4*>(&hb[rt.x][2 * px]);
+            const int4 bb = *reinterpret_cast<const int4*>(&hb[rt.y][2 * px]);
+            const int2 r0 = lerp_i2(make_int2(ba.x, ba.y), make_int2(bb.x, bb.y), D, rt.z);
+            const int2 r1 = lerp_i2(make_int2(ba.z, ba.w), make_int2(bb.z, bb.w), D, rt.z);
+            int4 f = make_int4(r0.x << rs, r0.y << rs, r1.x << rs, r1.y << rs);
+            if (LEVEL > 0) {
+                const int4 ua = *reinterpret_cast<const int4*>(&hu[rt.w & 0xFF][2 * px]);
+                const int4 ub = *reinterpret_cast<const int4*>(&hu[(rt.w >> 8) & 0xFF][2 * px]);
+                const int2 u0 = lerp_i2(make_int2(ua.x, ua.y), make_int2(ub.x, ub.y), 4, rt.w >> 16);
+                const int2 u1 = lerp_i2(make_int2(ua.z, ua.w), make_int2(ub.z, ub.w), 4, rt.w >> 16);
+                f.x += u0.x << bs;
+                f.y += u0.y << bs;
+                f.z += u1.x << bs;
+                f.w += u1.y << bs;
+            }
+            int2* o = out + (size_t)y * L.w + xq;
+            if (vec) {
+                *reinterpret_cast<int4*>(o) = f;
+            } else {
+                o[0] = make_int2(f.x, f.y);
+                if (two) o[1] = make_int2(f.z, f.w);
+            }
+        }
+        return;
+    }
+#endif
+    const int x = x0 + tx;
+    if (x >= L.w) return;
     for (int ty = tg; ty < kFH; ty += 4) {
         const int y = y0 + ty;
         if (y >= L.h) break;
