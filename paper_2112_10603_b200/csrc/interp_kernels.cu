@@ -1748,14 +1748,14 @@ __device__ __forceinline__ uint8_t blend_px(double m, int a, int b) {
 // parallel (thread = 2 rows x 8 columns, chroma from the row pair).
 // ---------------------------------------------------------------------------
 #ifndef FVV_KCC
-#define FVV_KCC 64
+#define FVV_KCC 96  // r2 v13 sweep (cfg4 scan ms per rig frame): 32 / 64 / 96 / 128 = 0.392 / 0.365 / 0.334 / 0.344
 #endif
 #ifndef FVV_SCAN_TSTORE
 #define FVV_SCAN_TSTORE 1
 #endif
 constexpr int kCR = 32, kCC = FVV_KCC;  // carry kernel: rows per CTA (one lane each), chunk columns
 constexpr int kCT = kCC + 16;       // staged u16 per row and chunk: sd[c0-8 .. c0+72)
-constexpr int kCTP = kCT + 4;       // row pitch: 2*kCTP B (168 B = 21 x 8 B at kCC 64): odd 8-byte count, 16 lanes hit 16 bank pairs
+constexpr int kCTP = kCT + 4;       // row pitch: 2*kCTP B (168 B = 21 x 8 B at kCC 64, 232 B = 29 x 8 B at 96): odd 8-byte count, 16 lanes hit 16 bank pairs
 // the double2 carry stores step by 2 up to kCC/8 and the transpose moves kCC/16 pieces per row
 static_assert(kCC % 16 == 0 && kCC >= 16, "FVV_KCC must be a positive multiple of 16");
 static_assert(((2 * kCTP) / 8) % 2 == 1 && (2 * kCTP) % 8 == 0, "carry row pitch must be an odd number of 8-byte words");
